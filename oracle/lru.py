@@ -1,0 +1,103 @@
+"""O5 — capacity-limited device plan with LRU eviction to host.
+
+TEST INFRASTRUCTURE (see oracle/__init__.py).
+
+MemHC's "pre-protected LRU" is named, not defined, in the paper; this
+follows DESIGN.md readings E-1..E-8:
+  E-1 before c_i: need = sum of non-resident operand sizes + output size; while
+      used + need > cap evict the least-recently-used resident tensor that is not
+      an operand of c_i.  Infeasible if operands + output > cap.
+  E-2 LRU clock: a global counter, one tick per touch; at c_i the operands are
+      touched in (left, right) order (a fetch is a touch), then the output.
+  E-3 evicting a leaf: 1 eviction, no D2H (the host copy is the caller's).
+  E-4 evicting an intermediate: 1 eviction + D2H on its FIRST eviction; the host
+      copy is kept until release, so later evictions of it are clean drops.
+  E-5 #transfers = h2d_count + d2h_count.
+  E-8 tensors nothing depends on are released at once (never "evicted").
+Leaves are fetched lazily at first use (G-6).  Release follows §II-C.
+"""
+
+
+class InfeasibleError(Exception):
+    pass
+
+
+def plan(dag, order, cap=None):
+    """Replay `order` on a device of `cap` bytes (None or <= 0: unbounded).
+
+    Returns dict: ops [(kind, node)], kinds in {"D2H","DROP","H2D","CONTRACT","FREE"}
+    ("D2H" = eviction with a copy to host, "DROP" = eviction without copy),
+    evictions, h2d_count, d2h_count, h2d_bytes, d2h_bytes, peak (device bytes after
+    each step's releases), transient_peak (device bytes right after the output is
+    produced), host_peak_bytes (host copies of evicted intermediates), used [per step].
+    """
+    if cap is not None and cap <= 0:
+        cap = None
+    nodes = dag.nodes
+    remaining = {u: len(n.parents) for u, n in nodes.items()}
+    resident = set()
+    host_copy = set()
+    lru = {}
+    clock = 0
+    used = 0
+    host_bytes = 0
+    st = dict(evictions=0, h2d_count=0, d2h_count=0, h2d_bytes=0, d2h_bytes=0,
+              peak=0, transient_peak=0, host_peak_bytes=0)
+    ops = []
+    used_trace = [0]
+    for u in order:
+        n = nodes[u]
+        operands = list(n.child)
+        work = sum(nodes[x].size for x in operands) + n.size
+        if cap is not None and work > cap:
+            raise InfeasibleError("contraction %d needs %d bytes > cap %d" % (u, work, cap))
+        need = sum(nodes[x].size for x in operands if x not in resident) + n.size
+        while cap is not None and used + need > cap:          # E-1
+            victim = min((x for x in resident if x not in operands), key=lambda x: lru[x])
+            st["evictions"] += 1
+            if nodes[victim].child and victim not in host_copy:   # E-4 first eviction
+                st["d2h_count"] += 1
+                st["d2h_bytes"] += nodes[victim].size
+                host_copy.add(victim)
+                host_bytes += nodes[victim].size
+                st["host_peak_bytes"] = max(st["host_peak_bytes"], host_bytes)
+                ops.append(("D2H", victim))
+            else:                                                  # E-3 / clean E-4
+                ops.append(("DROP", victim))
+            resident.discard(victim)
+            used -= nodes[victim].size
+        for x in operands:                                         # fetch + touch (E-2)
+            if x not in resident:
+                st["h2d_count"] += 1
+                st["h2d_bytes"] += nodes[x].size
+                resident.add(x)
+                used += nodes[x].size
+                ops.append(("H2D", x))
+            clock += 1
+            lru[x] = clock
+        resident.add(u)                                            # output
+        used += n.size
+        clock += 1
+        lru[u] = clock
+        ops.append(("CONTRACT", u))
+        st["transient_peak"] = max(st["transient_peak"], used)
+        for x in operands:                                         # release at last use
+            remaining[x] -= 1
+            if remaining[x] == 0:
+                resident.discard(x)
+                used -= nodes[x].size
+                if x in host_copy:
+                    host_copy.discard(x)
+                    host_bytes -= nodes[x].size
+                ops.append(("FREE", x))
+        if remaining[u] == 0:                                      # ROOT: released at once
+            resident.discard(u)
+            used -= n.size
+            ops.append(("FREE", u))
+        st["peak"] = max(st["peak"], used)
+        used_trace.append(used)
+    assert used == 0 and not resident and host_bytes == 0
+    st["ops"] = ops
+    st["used"] = used_trace
+    st["transfers"] = st["h2d_count"] + st["d2h_count"]
+    return st
