@@ -1,0 +1,202 @@
+/*
+ * cc.h — C ABI of the correlator-contraction engine (libcc.so).
+ *
+ * The engine executes the binary, batched, complex-double tensor contractions of a
+ * Redstar-style contraction DAG (§II-B) in a memory-minimising
+ * sequential schedule (§II-C problem statement, l.248; sibling scheduler §III-A,
+ * tree scheduler §III-B), releasing intermediates at last use (l.62, l.207-211) and
+ * evicting least-recently-used tensors to pinned host memory when the device pool is
+ * full (MemHC, l.136-139; eviction definition l.913).  "P:n" below = PAPER.md line n.
+ *
+ * Conventions
+ *  - Every function returns cc_status (0 = CC_OK, < 0 = error); no C++ exception crosses
+ *    the ABI.  cc_last_error(ctx) gives a message for the last failing call on ctx.
+ *  - complex128 tensors are interleaved (re, im) doubles, row-major, time slice t
+ *    outermost: meson node [Lt][N][N], baryon node [Lt][S][N][N][N] (S = spin
+ *    components, 64 in P:59), root value [Lt].  Byte sizes 16*Lt*N^2, 16*Lt*S*N^3, 16*Lt.
+ *  - Node ids and tree ids are caller-chosen int64, unique; ties in the schedulers are
+ *    broken by ascending id (readings S-1, S-3, T-1).
+ *  - A cc_ctx is one device (or host-only when device < 0); not thread-safe.
+ *  - Ordering: cc_create -> cc_load_dag -> [cc_partition] -> cc_schedule ->
+ *    cc_set_leaf* -> cc_execute -> cc_correlator / cc_root_value.  Calls out of order
+ *    return CC_E_STATE.  cc_schedule / cc_execute may be repeated (same plan re-run).
+ */
+#ifndef CC_H
+#define CC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CC_OK = 0,
+  CC_E_INVAL = -1,            /* bad argument                                         */
+  CC_E_PARSE = -2,            /* text format error (message carries the line number)  */
+  CC_E_CYCLE = -3,            /* the operand relation has a cycle                     */
+  CC_E_INCONSISTENT = -4,     /* duplicate id, operand kinds do not fit the op, ...   */
+  CC_E_MULTIROOT = -5,        /* a root shared by two trees / a parentless non-root   */
+  CC_E_UNKNOWN_NODE = -6,     /* operand / root / tree id not declared                */
+  CC_E_NOT_CLOSED = -7,       /* reserved (trees are closures of their roots)         */
+  CC_E_INFEASIBLE = -8,       /* operands + output of one contraction exceed cap      */
+  CC_E_STATE = -9,            /* call out of order, or op not allowed on this ctx     */
+  CC_E_BUFFER_TOO_SMALL = -10,
+  CC_E_CUDA = -11,            /* CUDA runtime error (message has the CUDA string)     */
+  CC_E_NOMEM = -12            /* arena / host allocation failed                       */
+} cc_status;
+
+/* Node kinds.  Index semantics (reading V-1):
+ *   CC_MM1   (meson A, meson B)   C[t,i,k]     = sum_j A[t,i,j] B[t,j,k]          O(N^3)
+ *   CC_BM1   (baryon A, meson M)  C[t,s,i,j,l] = sum_k A[t,s,i,j,k] M[t,k,l]      O(N^4)
+ *   CC_BB2   (baryon A, baryon B) C[t,i,l]     = sum_s sum_{j,k} A[t,s,i,j,k] B[t,s,j,k,l]
+ *   CC_TR_MM (meson A, meson B)   c[t]         = sum_{i,j} A[t,i,j] B[t,j,i]   (root only:
+ *                                  "contract all")
+ * CC_LEAF_X / CC_OP_X are abstract nodes of explicit size for scheduling-only DAGs
+ * (e.g. Table I); a DAG containing them can be scheduled/planned, not executed. */
+typedef enum {
+  CC_LEAF_M = 0, CC_LEAF_B = 1, CC_MM1 = 2, CC_BM1 = 3, CC_BB2 = 4, CC_TR_MM = 5,
+  CC_LEAF_X = 6, CC_OP_X = 7
+} cc_op;
+
+typedef struct { int32_t Lt, N, S; } cc_dims;
+
+/* a, b: ordered operand ids (left, right), -1 for leaves.  size: 0 = derive
+ * from the kind and dims; > 0 = explicit bytes (required for abstract nodes; must match
+ * the derived size for typed nodes). */
+typedef struct { int64_t id; int32_t op; int32_t pad_; int64_t a, b; int64_t size; } cc_node;
+/* A tree is its root plus the closure of the root under operands. */
+typedef struct { int64_t tree_id; int64_t root; } cc_tree;
+/* Correlator term: C_corr[t] += (re + i im) * root_tree[t]. */
+typedef struct { int64_t corr_id; int64_t tree_id; double re, im; } cc_term;
+
+typedef enum { CC_SIBLING = 0, CC_TREE = 1, CC_GIVEN = 2 } cc_algo;
+
+typedef struct {
+  int32_t algo;               /* cc_algo                                                   */
+  int32_t flags;              /* reserved, 0                                               */
+  uint64_t seed;              /* reserved (reading S-1 pins the "random leaf" to lowest id) */
+  int64_t cap_bytes;          /* device pool capacity for the LRU plan; <= 0: unbounded     */
+  const int64_t* given_order; /* CC_GIVEN: contraction order (node ids), n_given entries    */
+  int64_t n_given;
+} cc_sched_cfg;
+
+/* Logical plan statistics (integers are bit-exact with the oracle).
+ * peak / transient_peak: device bytes after releases / right after producing an output
+ * (§II-C M_i and reading G-5); evictions / h2d / d2h: readings E-1..E-5. */
+typedef struct {
+  int64_t n_contr, peak, transient_peak, evictions, h2d_count, d2h_count,
+          h2d_bytes, d2h_bytes, host_peak_bytes, model_peak, model_transient_peak;
+  double sched_seconds;       /* scheduler wall time only (Table IV analogue) */
+  double plan_seconds;        /* LRU plan + physical placement                              */
+  int64_t arena_high_water;   /* physical pool bytes used (>= peak; fragmentation headroom)  */
+} cc_plan_stats;
+
+typedef struct {
+  double seconds;             /* cc_execute wall time (device events, first op -> last op)  */
+  double kernel_seconds;      /* sum of contraction-kernel durations (0 unless profiled)    */
+  double flops;               /* algorithmic flops: MM1 8LtN^3, BM1/BB2 8LtSN^4, TR 8LtN^2   */
+  double hbm_bytes;           /* algorithmic HBM bytes of the kernels                       */
+  int64_t h2d_bytes, d2h_bytes; /* bytes actually copied (device-resident leaves: 0)         */
+  int64_t n_kernels;          /* kernel launches issued by this execute                     */
+} cc_exec_stats;
+
+/* One op of the physical plan (cc_plan_ops). kind: 0 H2D, 1 D2H (evict with copy),
+ * 2 DROP (evict, no copy), 3 CONTRACT, 4 FREE (release at last use). */
+typedef struct { int32_t kind; int32_t pad_; int64_t node; int64_t bytes; int64_t offset; } cc_plan_op;
+
+typedef struct cc_ctx cc_ctx;
+
+/* device < 0: host-only context (load/validate/schedule/plan only).
+ * dev_arena/arena_bytes: caller-owned device memory the pool sub-allocates (may be NULL/0
+ *   on a host-only ctx).  The top `CC_SCRATCH` bytes of it are kernel workspace (split-K
+ *   partials; outside the logical capacity, reading E-7).
+ * streams: caller-owned cudaStream_t (NULL: the library creates its own). */
+cc_status cc_create(cc_ctx** out, int device, void* dev_arena, size_t arena_bytes,
+                    void* compute_stream, void* h2d_stream, void* d2h_stream);
+void cc_destroy(cc_ctx* ctx);
+const char* cc_last_error(const cc_ctx* ctx);
+const char* cc_version(void);
+
+/* Copies the inputs; builds G=(V,E), validates, computes ranks (Eq. 1) and F_v/F_e. */
+cc_status cc_load_dag(cc_ctx* ctx, const cc_dims* dims, const cc_node* nodes, int64_t n_nodes,
+                      const cc_tree* trees, int64_t n_trees, const cc_term* terms, int64_t n_terms);
+/* Text format, one record per line, '#' comments:
+ *   dims <Lt> <N> <S>
+ *   node <id> leafM|leafB|leafX [size <bytes>]
+ *   node <id> MM1|BM1|BB2|TR_MM|OPX <a> <b> [size <bytes>]
+ *   tree <tree_id> <root>
+ *   term <corr_id> <tree_id> <re> <im>                                               */
+cc_status cc_load_dag_file(cc_ctx* ctx, const char* path);
+
+typedef struct { int64_t V, E, k, n_contr, n_leaves, max_rank, n_corr; double F_v, F_e; } cc_dag_stats;
+cc_status cc_dag_info(cc_ctx* ctx, cc_dag_stats* out);
+
+/* Restrict the context to one part of an n_parts split:
+ * mode 0 TIME: time slices [part*Lt/n, (part+1)*Lt/n) of every tensor (no replication);
+ * mode 1 TREES: a contiguous, flop-balanced chunk of the trees in tree-scheduler
+ *   selection order, with the sub-DAG they need (shared nodes replicated).
+ * Call after cc_load_dag, before cc_schedule.  n_parts == 1 restores the full DAG. */
+cc_status cc_partition(cc_ctx* ctx, int32_t n_parts, int32_t part, int32_t mode);
+/* Trees of the current part (ids, ascending); n_out receives the count. */
+cc_status cc_part_trees(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out);
+
+/* Runs the scheduler (Alg. 1-3 or Alg. 4-8), then the LRU plan at cfg->cap_bytes and the
+ * physical placement in the arena.  order_out (may be NULL: size query) receives the
+ * contraction order; n_order its length.  stats may be NULL. */
+cc_status cc_schedule(cc_ctx* ctx, const cc_sched_cfg* cfg, int64_t* order_out, int64_t order_cap,
+                      int64_t* n_order, cc_plan_stats* stats);
+/* §II-C trace of the current schedule: M_0..M_n (n+1 entries) and transient_1..n. */
+cc_status cc_memory_trace(cc_ctx* ctx, int64_t* m_out, int64_t* transient_out, int64_t cap, int64_t* n_out);
+/* The op queue of the current plan, in order. */
+cc_status cc_plan_ops(cc_ctx* ctx, cc_plan_op* out, int64_t cap, int64_t* n_out);
+/* Tree-scheduler selection order of the last CC_TREE schedule (tree ids). */
+cc_status cc_tree_order(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out);
+/* Per-step op queue as CSV (step, op, node, bytes, offset, device_used). */
+cc_status cc_plan_dump(cc_ctx* ctx, const char* csv_path);
+
+/* Leaf data.  host: caller-owned pinned (or registered) host buffer of the full leaf
+ * ([Lt_full,...], all time slices; a TIME part reads its own slices), valid until the
+ * last cc_execute returns.  dev: caller-owned device buffer of the leaf restricted to the
+ * current part (inputs already resident in HBM: no H2D is issued for it; evicting it is
+ * a no-op).  bytes must equal the (full / part) leaf size. */
+cc_status cc_set_leaf(cc_ctx* ctx, int64_t leaf_id, const void* host, size_t bytes);
+cc_status cc_set_leaf_device(cc_ctx* ctx, int64_t leaf_id, const void* dev, size_t bytes);
+
+/* Replays the plan on the device: H2D / D2H on the copy streams, contractions on the
+ * compute stream, event dependencies for RAW on data and WAR on reused memory; blocking.
+ * flags bit 0: capture/replay as a CUDA graph; bit 1: time every kernel (kernel_seconds). */
+cc_status cc_execute(cc_ctx* ctx, int32_t flags, cc_exec_stats* stats);
+/* Enqueue-only variant (no host sync): work is ordered on the compute stream. */
+cc_status cc_execute_async(cc_ctx* ctx, int32_t flags);
+
+/* Per-kind contraction-kernel time of the last cc_execute with flags bit 1 (kernels timed
+ * with CUDA events on the compute stream): seconds[op], counts[op] for op = cc_op (8 each). */
+cc_status cc_kernel_times(cc_ctx* ctx, double* seconds, int64_t* counts);
+
+/* Results.  out: 2*Lt_part doubles (interleaved complex) for the current part. */
+cc_status cc_correlator(cc_ctx* ctx, int64_t corr_id, double* out, int32_t Lt);
+cc_status cc_root_value(cc_ctx* ctx, int64_t tree_id, double* out, int32_t Lt);
+/* Device buffer [n_corr][Lt_part] complex128 of all correlators (corr ids ascending), for
+ * a torch / NCCL all-reduce; corr_ids (may be NULL) receives the ids in buffer order. */
+cc_status cc_correlator_device_ptr(cc_ctx* ctx, void** dev_ptr, int64_t* n_corr, int64_t* corr_ids);
+
+/* Kernel entry points (the contraction kernels alone; used by the element-wise parity
+ * tests and the roofline measurement).  All pointers are device pointers in the layouts
+ * above; they run on the ctx compute stream and do not synchronise. */
+cc_status cc_mm1(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt, int32_t N);
+cc_status cc_bm1(cc_ctx* ctx, const void* A, const void* M, void* C, int32_t Lt, int32_t N, int32_t S);
+cc_status cc_bb2(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt, int32_t N, int32_t S);
+cc_status cc_tr_mm(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t Lt, int32_t N);
+/* Synthetic leaf values (input generation, not the method; same recipe as synth/rng.py):
+ * n complex elements starting at flat element e0 of leaf `leaf_id`, written to dev. */
+cc_status cc_fill_synthetic(cc_ctx* ctx, void* dev, int64_t n, uint64_t seed, int64_t leaf_id,
+                            int64_t e0, int32_t mode, double sigma);
+/* Bytes of kernel workspace the ctx reserves at the top of the arena. */
+size_t cc_scratch_bytes(int32_t Lt, int32_t N, int32_t S);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CC_H */

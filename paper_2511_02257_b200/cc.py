@@ -1,0 +1,315 @@
+"""Thin ctypes binding of include/cc.h (libcc.so): argument marshalling only.
+
+Every computation (scheduling, planning, contractions, copies) runs inside libcc.so;
+this module only converts Python/numpy/torch arguments into the C ABI's plain pointers
+and sizes and raises CCError on a non-zero status.  There is no fallback: if the shared
+library is missing the import fails.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcc.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError("libcc.so not built (run python -c 'import __graft_entry__ as g; g.build()'): %s" % LIB_PATH)
+_lib = ctypes.CDLL(LIB_PATH)
+
+c_i32, c_i64, c_u64, c_dbl, c_void_p, c_size_t = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64,
+                                                  ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t)
+P = ctypes.POINTER
+
+CC_LEAF_M, CC_LEAF_B, CC_MM1, CC_BM1, CC_BB2, CC_TR_MM, CC_LEAF_X, CC_OP_X = range(8)
+CC_SIBLING, CC_TREE, CC_GIVEN = range(3)
+PART_TIME, PART_TREES = 0, 1
+EXEC_GRAPH, EXEC_TIME_KERNELS = 1, 2
+STATUS = {0: "OK", -1: "INVAL", -2: "PARSE", -3: "CYCLE", -4: "INCONSISTENT", -5: "MULTIROOT",
+          -6: "UNKNOWN_NODE", -7: "NOT_CLOSED", -8: "INFEASIBLE", -9: "STATE", -10: "BUFFER_TOO_SMALL",
+          -11: "CUDA", -12: "NOMEM"}
+OP_KINDS = ["H2D", "D2H", "DROP", "CONTRACT", "FREE"]
+
+
+class cc_dims(ctypes.Structure):
+    _fields_ = [("Lt", c_i32), ("N", c_i32), ("S", c_i32)]
+
+
+class cc_node(ctypes.Structure):
+    _fields_ = [("id", c_i64), ("op", c_i32), ("pad_", c_i32), ("a", c_i64), ("b", c_i64), ("size", c_i64)]
+
+
+class cc_tree(ctypes.Structure):
+    _fields_ = [("tree_id", c_i64), ("root", c_i64)]
+
+
+class cc_term(ctypes.Structure):
+    _fields_ = [("corr_id", c_i64), ("tree_id", c_i64), ("re", c_dbl), ("im", c_dbl)]
+
+
+class cc_sched_cfg(ctypes.Structure):
+    _fields_ = [("algo", c_i32), ("flags", c_i32), ("seed", c_u64), ("cap_bytes", c_i64),
+                ("given_order", P(c_i64)), ("n_given", c_i64)]
+
+
+class cc_plan_stats(ctypes.Structure):
+    _fields_ = [(n, c_i64) for n in ("n_contr", "peak", "transient_peak", "evictions", "h2d_count", "d2h_count",
+                                     "h2d_bytes", "d2h_bytes", "host_peak_bytes", "model_peak",
+                                     "model_transient_peak")] + \
+               [("sched_seconds", c_dbl), ("plan_seconds", c_dbl), ("arena_high_water", c_i64)]
+
+
+class cc_exec_stats(ctypes.Structure):
+    _fields_ = [("seconds", c_dbl), ("kernel_seconds", c_dbl), ("flops", c_dbl), ("hbm_bytes", c_dbl),
+                ("h2d_bytes", c_i64), ("d2h_bytes", c_i64), ("n_kernels", c_i64)]
+
+
+class cc_plan_op(ctypes.Structure):
+    _fields_ = [("kind", c_i32), ("pad_", c_i32), ("node", c_i64), ("bytes", c_i64), ("offset", c_i64)]
+
+
+class cc_dag_stats(ctypes.Structure):
+    _fields_ = [(n, c_i64) for n in ("V", "E", "k", "n_contr", "n_leaves", "max_rank", "n_corr")] + \
+               [("F_v", c_dbl), ("F_e", c_dbl)]
+
+
+def _sig(name, *args, res=c_i32):
+    f = getattr(_lib, name)
+    f.argtypes = list(args)
+    f.restype = res
+    return f
+
+
+_sig("cc_create", P(c_void_p), ctypes.c_int, c_void_p, c_size_t, c_void_p, c_void_p, c_void_p)
+_sig("cc_destroy", c_void_p, res=None)
+_sig("cc_last_error", c_void_p, res=ctypes.c_char_p)
+_sig("cc_version", res=ctypes.c_char_p)
+_sig("cc_load_dag", c_void_p, P(cc_dims), P(cc_node), c_i64, P(cc_tree), c_i64, P(cc_term), c_i64)
+_sig("cc_load_dag_file", c_void_p, ctypes.c_char_p)
+_sig("cc_dag_info", c_void_p, P(cc_dag_stats))
+_sig("cc_partition", c_void_p, c_i32, c_i32, c_i32)
+_sig("cc_part_trees", c_void_p, P(c_i64), c_i64, P(c_i64))
+_sig("cc_schedule", c_void_p, P(cc_sched_cfg), P(c_i64), c_i64, P(c_i64), P(cc_plan_stats))
+_sig("cc_memory_trace", c_void_p, P(c_i64), P(c_i64), c_i64, P(c_i64))
+_sig("cc_plan_ops", c_void_p, P(cc_plan_op), c_i64, P(c_i64))
+_sig("cc_tree_order", c_void_p, P(c_i64), c_i64, P(c_i64))
+_sig("cc_plan_dump", c_void_p, ctypes.c_char_p)
+_sig("cc_set_leaf", c_void_p, c_i64, c_void_p, c_size_t)
+_sig("cc_set_leaf_device", c_void_p, c_i64, c_void_p, c_size_t)
+_sig("cc_execute", c_void_p, c_i32, P(cc_exec_stats))
+_sig("cc_execute_async", c_void_p, c_i32)
+_sig("cc_kernel_times", c_void_p, P(c_dbl), P(c_i64))
+_sig("cc_correlator", c_void_p, c_i64, P(c_dbl), c_i32)
+_sig("cc_root_value", c_void_p, c_i64, P(c_dbl), c_i32)
+_sig("cc_correlator_device_ptr", c_void_p, P(c_void_p), P(c_i64), P(c_i64))
+_sig("cc_mm1", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32)
+_sig("cc_bm1", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32)
+_sig("cc_bb2", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32)
+_sig("cc_tr_mm", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32)
+_sig("cc_fill_synthetic", c_void_p, c_void_p, c_i64, c_u64, c_i64, c_i64, c_i32, c_dbl)
+_sig("cc_scratch_bytes", c_i32, c_i32, c_i32, res=c_size_t)
+
+EXPORTED = ["cc_create", "cc_destroy", "cc_last_error", "cc_version", "cc_load_dag", "cc_load_dag_file",
+            "cc_dag_info", "cc_partition", "cc_part_trees", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
+            "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_execute",
+            "cc_execute_async", "cc_kernel_times", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
+            "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_fill_synthetic", "cc_scratch_bytes"]
+
+
+class CCError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("%s (%d): %s" % (STATUS.get(status, "?"), status, msg))
+        self.status = status
+        self.code = STATUS.get(status, "?")
+
+
+def _ptr(x):
+    """Device/host address of a torch tensor, numpy array or int."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    raise TypeError("cannot take the address of %r" % type(x))
+
+
+def cc_version():
+    return _lib.cc_version().decode()
+
+
+def cc_scratch_bytes(Lt, N, S):
+    return int(_lib.cc_scratch_bytes(Lt, N, S))
+
+
+class Context:
+    """One cc_ctx.  Method names are the C functions without the cc_ prefix."""
+
+    def __init__(self, device=-1, arena=None, arena_bytes=None, streams=None):
+        h = c_void_p()
+        cs = hs = ds = None
+        if streams is not None:
+            cs, hs, ds = (s.cuda_stream if hasattr(s, "cuda_stream") else s for s in streams)
+        nbytes = arena_bytes if arena_bytes is not None else (
+            arena.numel() * arena.element_size() if arena is not None else 0)
+        st = _lib.cc_create(ctypes.byref(h), device, _ptr(arena), nbytes, cs, hs, ds)
+        self._h = h
+        self._keep = [arena, streams]
+        if st != 0:
+            msg = _lib.cc_last_error(h).decode() if h.value else "cc_create failed"
+            if h.value:
+                _lib.cc_destroy(h)
+                self._h = c_void_p()
+            raise CCError(st, msg)
+
+    def close(self):
+        if self._h and self._h.value:
+            _lib.cc_destroy(self._h)
+            self._h = c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, st):
+        if st != 0:
+            raise CCError(st, _lib.cc_last_error(self._h).decode())
+
+    # --- DAG -----------------------------------------------------------------------------
+    def load_dag(self, Lt, N, S, nodes, trees, terms):
+        """nodes: [(id, op, a, b, size)], trees: [(tree_id, root)], terms: [(corr, tree, re, im)]."""
+        nn = (cc_node * max(len(nodes), 1))()
+        for i, (nid, op, a, b, size) in enumerate(nodes):
+            nn[i] = cc_node(nid, op, 0, a, b, size)
+        tt = (cc_tree * max(len(trees), 1))()
+        for i, (t, r) in enumerate(trees):
+            tt[i] = cc_tree(t, r)
+        mm = (cc_term * max(len(terms), 1))()
+        for i, (c, t, re, im) in enumerate(terms):
+            mm[i] = cc_term(c, t, re, im)
+        d = cc_dims(Lt, N, S)
+        self._ck(_lib.cc_load_dag(self._h, ctypes.byref(d), nn, len(nodes), tt, len(trees), mm, len(terms)))
+
+    def load_workload(self, w):
+        self.load_dag(w.Lt, w.N, w.S, w.nodes, w.trees, w.terms)
+
+    def load_dag_file(self, path):
+        self._ck(_lib.cc_load_dag_file(self._h, path.encode()))
+
+    def dag_info(self):
+        s = cc_dag_stats()
+        self._ck(_lib.cc_dag_info(self._h, ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in cc_dag_stats._fields_}
+
+    def partition(self, n_parts, part, mode):
+        self._ck(_lib.cc_partition(self._h, n_parts, part, mode))
+
+    def part_trees(self):
+        n = c_i64()
+        self._ck(_lib.cc_part_trees(self._h, None, 0, ctypes.byref(n)))
+        out = (c_i64 * max(n.value, 1))()
+        self._ck(_lib.cc_part_trees(self._h, out, n.value, ctypes.byref(n)))
+        return list(out[:n.value])
+
+    # --- schedule / plan -----------------------------------------------------------------
+    def schedule(self, algo=CC_TREE, cap_bytes=0, given=None):
+        cfg = cc_sched_cfg()
+        cfg.algo = algo
+        cfg.cap_bytes = int(cap_bytes or 0)
+        if given is not None:
+            g = (c_i64 * max(len(given), 1))(*given)
+            cfg.given_order = ctypes.cast(g, P(c_i64))
+            cfg.n_given = len(given)
+        n = c_i64()
+        stats = cc_plan_stats()
+        self._ck(_lib.cc_schedule(self._h, ctypes.byref(cfg), None, 0, ctypes.byref(n), ctypes.byref(stats)))
+        out = (c_i64 * max(n.value, 1))()
+        self._ck(_lib.cc_schedule(self._h, ctypes.byref(cfg), out, n.value, ctypes.byref(n), ctypes.byref(stats)))
+        st = {f: getattr(stats, f) for f, _ in cc_plan_stats._fields_}
+        return list(out[:n.value]), st
+
+    def memory_trace(self):
+        n = c_i64()
+        self._ck(_lib.cc_memory_trace(self._h, None, None, 0, ctypes.byref(n)))
+        m = (c_i64 * (n.value + 1))()
+        t = (c_i64 * max(n.value, 1))()
+        self._ck(_lib.cc_memory_trace(self._h, m, t, n.value + 1, ctypes.byref(n)))
+        return list(m[:n.value + 1]), list(t[:n.value])
+
+    def plan_ops(self):
+        n = c_i64()
+        self._ck(_lib.cc_plan_ops(self._h, None, 0, ctypes.byref(n)))
+        out = (cc_plan_op * max(n.value, 1))()
+        self._ck(_lib.cc_plan_ops(self._h, out, n.value, ctypes.byref(n)))
+        return [(OP_KINDS[o.kind], o.node, o.bytes, o.offset) for o in out[:n.value]]
+
+    def tree_order(self):
+        n = c_i64()
+        self._ck(_lib.cc_tree_order(self._h, None, 0, ctypes.byref(n)))
+        out = (c_i64 * max(n.value, 1))()
+        self._ck(_lib.cc_tree_order(self._h, out, n.value, ctypes.byref(n)))
+        return list(out[:n.value])
+
+    def plan_dump(self, path):
+        self._ck(_lib.cc_plan_dump(self._h, path.encode()))
+
+    # --- data / execution ----------------------------------------------------------------
+    def set_leaf(self, leaf_id, host, nbytes=None):
+        nbytes = nbytes if nbytes is not None else host.numel() * host.element_size() if hasattr(host, "numel") \
+            else host.nbytes
+        self._ck(_lib.cc_set_leaf(self._h, leaf_id, _ptr(host), nbytes))
+
+    def set_leaf_device(self, leaf_id, dev, nbytes=None):
+        nbytes = nbytes if nbytes is not None else dev.numel() * dev.element_size()
+        self._ck(_lib.cc_set_leaf_device(self._h, leaf_id, _ptr(dev), nbytes))
+
+    def execute(self, flags=0):
+        s = cc_exec_stats()
+        self._ck(_lib.cc_execute(self._h, flags, ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in cc_exec_stats._fields_}
+
+    def execute_async(self, flags=0):
+        self._ck(_lib.cc_execute_async(self._h, flags))
+
+    def kernel_times(self):
+        s = (c_dbl * 8)()
+        c = (c_i64 * 8)()
+        self._ck(_lib.cc_kernel_times(self._h, s, c))
+        return list(s), list(c)
+
+    def correlator(self, corr_id, Lt):
+        out = np.empty(2 * Lt, dtype=np.float64)
+        self._ck(_lib.cc_correlator(self._h, corr_id, out.ctypes.data_as(P(c_dbl)), Lt))
+        return out[0::2] + 1j * out[1::2]
+
+    def root_value(self, tree_id, Lt):
+        out = np.empty(2 * Lt, dtype=np.float64)
+        self._ck(_lib.cc_root_value(self._h, tree_id, out.ctypes.data_as(P(c_dbl)), Lt))
+        return out[0::2] + 1j * out[1::2]
+
+    def correlator_device_ptr(self):
+        p = c_void_p()
+        n = c_i64()
+        self._ck(_lib.cc_correlator_device_ptr(self._h, ctypes.byref(p), ctypes.byref(n), None))
+        ids = (c_i64 * max(n.value, 1))()
+        self._ck(_lib.cc_correlator_device_ptr(self._h, ctypes.byref(p), ctypes.byref(n), ids))
+        return p.value, n.value, list(ids[:n.value])
+
+    # --- kernel entry points ---------------------------------------------------------------
+    def mm1(self, A, B, C, Lt, N):
+        self._ck(_lib.cc_mm1(self._h, _ptr(A), _ptr(B), _ptr(C), Lt, N))
+
+    def bm1(self, A, M, C, Lt, N, S):
+        self._ck(_lib.cc_bm1(self._h, _ptr(A), _ptr(M), _ptr(C), Lt, N, S))
+
+    def bb2(self, A, B, C, Lt, N, S):
+        self._ck(_lib.cc_bb2(self._h, _ptr(A), _ptr(B), _ptr(C), Lt, N, S))
+
+    def tr_mm(self, A, B, c, Lt, N):
+        self._ck(_lib.cc_tr_mm(self._h, _ptr(A), _ptr(B), _ptr(c), Lt, N))
+
+    def fill_synthetic(self, dev, n, seed, leaf_id, e0, mode, sigma):
+        self._ck(_lib.cc_fill_synthetic(self._h, _ptr(dev), n, seed, leaf_id, e0, mode, sigma))

@@ -1,0 +1,867 @@
+// C ABI (include/cc.h) and the device executor.
+//
+// The executor replays the offline physical plan (host/plan.cpp) on three streams:
+// H2D copies (leaf loads, re-fetches) and D2H copies (evictions) on two copy
+// streams, contractions on the compute stream; cross-stream event edges enforce RAW on
+// data and WAR/WAW on reused pool memory, so copies run ahead of compute as far as the
+// plan's logical residency allows (prefetch without changing the plan).  The whole
+// replay can be captured once as a CUDA graph and relaunched.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../host/dag.hpp"
+#include "../host/partition.hpp"
+#include "../host/plan.hpp"
+#include "../host/sched.hpp"
+#include "../kernels/kernels.hpp"
+#include "cc.h"
+
+using namespace cc;
+
+#define CC_VERSION "cc-b200 0.1 (sm_100a; FP64 DMMA + TMA; sibling/tree schedulers; LRU plan)"
+
+namespace {
+
+constexpr int64_t ALIGN = 1024;
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(CC_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct KindTimes {
+  double seconds[8] = {0};
+  int64_t count[8] = {0};
+};
+
+}  // namespace
+
+struct cc_ctx {
+  int device = -1;
+  bool host_only = true;
+  char* arena = nullptr;
+  int64_t arena_bytes = 0;
+  cudaStream_t cs = nullptr, hs = nullptr, ds = nullptr;
+  bool own_streams = false;
+  int num_sms = 148;
+  std::string err;
+
+  Input input;
+  bool loaded = false;
+  int32_t n_parts = 1, part = 0, mode = 0, t0 = 0, t1 = 0;
+  std::vector<int64_t> part_trees;
+  std::unique_ptr<Dag> dag;
+
+  bool scheduled = false;
+  std::vector<int32_t> order, tree_order;
+  ModelTrace mt;
+  LruPlan lp;
+  cc_plan_stats stats{};
+  int64_t cap = 0;
+
+  std::vector<const void*> leaf_host, leaf_dev;
+
+  // physical state
+  bool phys_valid = false;
+  PhysPlan pp;
+  int64_t pool_bytes = 0;
+  char* scratch = nullptr;
+  size_t gemm_ws_bytes = 0;
+  char* gemm_ws = nullptr;
+  char* trace_ws = nullptr;
+  double2* roots = nullptr;
+  double2* corr = nullptr;
+  int32_t* term_start = nullptr;
+  int32_t* term_tree = nullptr;
+  double* term_coef = nullptr;
+  std::vector<int32_t> corr_slot_of_term;
+  char* host_pool = nullptr;
+  int64_t host_pool_bytes = 0;
+  std::vector<cudaEvent_t> events;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_h_end = nullptr, ev_d_end = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  bool executed = false;
+  KindTimes ktimes;
+  int64_t last_n_kernels = 0;
+
+  // direct kernel entry points
+  char* direct_ws = nullptr;
+  size_t direct_ws_bytes = 0;
+
+  ~cc_ctx() { release_device(); }
+
+  void release_graph() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    gexec = nullptr;
+  }
+  void release_phys() {
+    release_graph();
+    for (auto e : events)
+      if (e) cudaEventDestroy(e);
+    events.clear();
+    if (host_pool) cudaFreeHost(host_pool);
+    host_pool = nullptr;
+    host_pool_bytes = 0;
+    phys_valid = false;
+  }
+  void release_device() {
+    if (host_only) return;
+    release_phys();
+    for (cudaEvent_t* e : {&ev_start, &ev_end, &ev_h_end, &ev_d_end})
+      if (*e) {
+        cudaEventDestroy(*e);
+        *e = nullptr;
+      }
+    if (direct_ws) cudaFree(direct_ws);
+    direct_ws = nullptr;
+    if (own_streams) {
+      for (cudaStream_t s : {cs, hs, ds})
+        if (s) cudaStreamDestroy(s);
+    }
+    cs = hs = ds = nullptr;
+  }
+  void need_device() const {
+    if (host_only) throw Error(CC_E_STATE, "host-only context (device < 0)");
+  }
+};
+
+static cc_status fail(cc_ctx* ctx, const Error& e) {
+  if (ctx) ctx->err = e.what();
+  return e.status;
+}
+
+#define API_BEGIN try {
+#define API_END                                                   \
+  }                                                               \
+  catch (const Error& e) { return fail(ctx, e); }                 \
+  catch (const std::bad_alloc&) {                                 \
+    if (ctx) ctx->err = "host allocation failed";                 \
+    return CC_E_NOMEM;                                            \
+  }                                                               \
+  catch (const std::exception& e) {                               \
+    if (ctx) ctx->err = e.what();                                 \
+    return CC_E_INVAL;                                            \
+  }                                                               \
+  return CC_OK;
+
+// ------------------------------------------------------------------------------------------
+namespace {
+
+void rebuild_dag(cc_ctx* ctx) {
+  const int32_t Lt = ctx->input.dims.Lt;
+  if (ctx->n_parts <= 1) {
+    ctx->t0 = 0;
+    ctx->t1 = Lt;
+    ctx->dag = std::make_unique<Dag>(ctx->input);
+    ctx->part_trees.clear();
+    for (const auto& t : ctx->dag->trees) ctx->part_trees.push_back(t.tree_id);
+  } else if (ctx->mode == 0) {
+    ctx->t0 = int32_t(int64_t(ctx->part) * Lt / ctx->n_parts);
+    ctx->t1 = int32_t(int64_t(ctx->part + 1) * Lt / ctx->n_parts);
+    if (ctx->t1 <= ctx->t0) throw Error(CC_E_INVAL, "TIME partition: part has no time slices");
+    ctx->dag = std::make_unique<Dag>(ctx->input, ctx->t1 - ctx->t0);
+    ctx->part_trees.clear();
+    for (const auto& t : ctx->dag->trees) ctx->part_trees.push_back(t.tree_id);
+  } else {
+    ctx->t0 = 0;
+    ctx->t1 = Lt;
+    Dag full(ctx->input);
+    std::vector<int32_t> parts = tree_parts(full, ctx->n_parts, nullptr);
+    std::vector<int64_t> keep;
+    for (size_t t = 0; t < full.trees.size(); ++t)
+      if (parts[t] == ctx->part) keep.push_back(full.trees[t].tree_id);
+    if (keep.empty()) throw Error(CC_E_INVAL, "TREES partition: part has no trees");
+    ctx->dag = std::make_unique<Dag>(ctx->input, 0, &keep);
+    ctx->part_trees = keep;
+  }
+  const size_t n = ctx->dag->nodes.size();
+  ctx->leaf_host.assign(n, nullptr);
+  ctx->leaf_dev.assign(n, nullptr);
+  ctx->scheduled = false;
+  ctx->executed = false;
+  ctx->phys_valid = false;
+  ctx->release_graph();
+}
+
+ZgemmProblem problem_for(int op, int64_t Lt, int64_t N, int64_t S, const void* a, const void* b, void* c) {
+  ZgemmProblem p{};
+  p.A = a;
+  p.B = b;
+  p.C = c;
+  p.batch = Lt;
+  if (op == CC_MM1) {
+    p.M = N; p.Nn = N; p.Kin = N; p.Ko = 1;
+    p.lda = N; p.sAo = 0; p.sAb = N * N;
+    p.ldb = N; p.sBo = 0; p.sBb = N * N;
+    p.ldc = N; p.sCb = N * N;
+  } else if (op == CC_BM1) {
+    p.M = S * N * N; p.Nn = N; p.Kin = N; p.Ko = 1;
+    p.lda = N; p.sAo = 0; p.sAb = S * N * N * N;
+    p.ldb = N; p.sBo = 0; p.sBb = N * N;
+    p.ldc = N; p.sCb = S * N * N * N;
+  } else {  // CC_BB2
+    p.M = N; p.Nn = N; p.Kin = N * N; p.Ko = S;
+    p.lda = N * N; p.sAo = N * N * N; p.sAb = S * N * N * N;
+    p.ldb = N; p.sBo = N * N * N; p.sBb = S * N * N * N;
+    p.ldc = N; p.sCb = N * N;
+  }
+  return p;
+}
+
+// Sets up scratch (kernel workspace, roots, correlators, term tables), the physical plan,
+// events and the host pool.  Called lazily by cc_execute.
+void prepare_phys(cc_ctx* ctx) {
+  if (ctx->phys_valid) return;
+  ctx->release_phys();
+  const Dag& g = *ctx->dag;
+  if (g.abstract) throw Error(CC_E_STATE, "abstract DAG (leafX/OPX) can be scheduled, not executed");
+  const int64_t Lt = g.Lt, N = g.N, S = g.S;
+  // scratch layout
+  size_t gemm_ws = 0;
+  bool has[8] = {false};
+  for (const auto& n : g.nodes) has[n.op] = true;
+  for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)})
+    if (has[op]) gemm_ws = std::max(gemm_ws, zgemm_workspace_bytes(problem_for(op, Lt, N, S, nullptr, nullptr, nullptr), ctx->num_sms));
+  const size_t trace_ws = trace_workspace_bytes(Lt, N);
+  const int64_t n_trees = int64_t(g.trees.size()), n_corr = int64_t(g.corr_ids.size()), n_terms = int64_t(g.terms.size());
+  const int64_t sz_gemm = round_up(int64_t(gemm_ws), ALIGN), sz_trace = round_up(int64_t(trace_ws), ALIGN);
+  const int64_t sz_roots = round_up(n_trees * Lt * 16, ALIGN), sz_corr = round_up(std::max<int64_t>(n_corr, 1) * Lt * 16, ALIGN);
+  const int64_t sz_ts = round_up((n_corr + 1) * 4, ALIGN), sz_tt = round_up(std::max<int64_t>(n_terms, 1) * 4, ALIGN);
+  const int64_t sz_tc = round_up(std::max<int64_t>(n_terms, 1) * 16, ALIGN);
+  const int64_t scratch = sz_gemm + sz_trace + sz_roots + sz_corr + sz_ts + sz_tt + sz_tc;
+  const int64_t pool = (ctx->arena_bytes - scratch) / ALIGN * ALIGN;
+  if (pool <= 0) throw Error(CC_E_NOMEM, "arena too small for the kernel workspace (" + std::to_string(scratch) + " B)");
+  ctx->pool_bytes = pool;
+  char* s = ctx->arena + pool;
+  ctx->gemm_ws = s; ctx->gemm_ws_bytes = size_t(sz_gemm); s += sz_gemm;
+  ctx->trace_ws = s; s += sz_trace;
+  ctx->roots = reinterpret_cast<double2*>(s); s += sz_roots;
+  ctx->corr = reinterpret_cast<double2*>(s); s += sz_corr;
+  ctx->term_start = reinterpret_cast<int32_t*>(s); s += sz_ts;
+  ctx->term_tree = reinterpret_cast<int32_t*>(s); s += sz_tt;
+  ctx->term_coef = reinterpret_cast<double*>(s); s += sz_tc;
+  // term tables grouped by correlator slot (corr ids ascending), input order within a slot
+  std::vector<int32_t> start(size_t(n_corr) + 1, 0), tree(size_t(std::max<int64_t>(n_terms, 1)), 0);
+  std::vector<double> coef(size_t(std::max<int64_t>(n_terms, 1)) * 2, 0.0);
+  {
+    std::vector<int32_t> slot(static_cast<size_t>(n_terms));
+    for (int64_t k = 0; k < n_terms; ++k) {
+      const auto it = std::lower_bound(g.corr_ids.begin(), g.corr_ids.end(), g.terms[size_t(k)].corr_id);
+      slot[size_t(k)] = int32_t(it - g.corr_ids.begin());
+      ++start[size_t(slot[size_t(k)]) + 1];
+    }
+    for (int64_t c = 0; c < n_corr; ++c) start[size_t(c) + 1] += start[size_t(c)];
+    std::vector<int32_t> fill(start.begin(), start.end() - 1);
+    for (int64_t k = 0; k < n_terms; ++k) {
+      const int32_t pos = fill[size_t(slot[size_t(k)])]++;
+      tree[size_t(pos)] = g.terms[size_t(k)].tree;
+      coef[2 * size_t(pos)] = g.terms[size_t(k)].coef.real();
+      coef[2 * size_t(pos) + 1] = g.terms[size_t(k)].coef.imag();
+    }
+  }
+  ck(cudaMemcpy(ctx->term_start, start.data(), start.size() * 4, cudaMemcpyHostToDevice), "term tables");
+  ck(cudaMemcpy(ctx->term_tree, tree.data(), tree.size() * 4, cudaMemcpyHostToDevice), "term tables");
+  ck(cudaMemcpy(ctx->term_coef, coef.data(), coef.size() * 8, cudaMemcpyHostToDevice), "term tables");
+  ck(cudaMemset(ctx->trace_ws, 0, trace_ws), "trace counters");
+  ck(cudaMemset(ctx->roots, 0, size_t(sz_roots)), "roots");
+  // physical plan over the pool
+  std::vector<uint8_t> on_dev(g.nodes.size(), 0);
+  for (size_t u = 0; u < g.nodes.size(); ++u) on_dev[u] = ctx->leaf_dev[u] != nullptr;
+  ctx->pp = build_phys(g, ctx->lp, on_dev, pool, ALIGN);
+  ctx->stats.arena_high_water = ctx->pp.pool_high_water;
+  if (ctx->pp.host_pool_bytes > 0) {
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_pool), size_t(ctx->pp.host_pool_bytes), cudaHostAllocDefault),
+       "pinned host pool");
+    ctx->host_pool_bytes = ctx->pp.host_pool_bytes;
+  }
+  ctx->events.assign(ctx->pp.ops.size(), nullptr);
+  for (size_t i = 0; i < ctx->pp.ops.size(); ++i)
+    if (ctx->pp.ops[i].source) ck(cudaEventCreateWithFlags(&ctx->events[i], cudaEventDisableTiming), "event");
+  ctx->phys_valid = true;
+}
+
+void launch_contract(cc_ctx* ctx, const Node& n, const void* a, const void* b, void* out, int64_t root_slot,
+                     int* nl) {
+  const Dag& g = *ctx->dag;
+  if (n.op == CC_TR_MM) {
+    ck(launch_trace(a, b, ctx->roots + root_slot * g.Lt, g.Lt, g.N, ctx->trace_ws, ctx->cs), "TR_MM kernel");
+    ++*nl;
+    return;
+  }
+  ZgemmProblem p = problem_for(n.op, g.Lt, g.N, g.S, a, b, out);
+  ck(launch_zgemm(p, ctx->gemm_ws, ctx->gemm_ws_bytes, ctx->num_sms, ctx->cs, nl), "contraction kernel");
+}
+
+// Issues the plan on the three streams.  Returns the number of kernel launches.
+int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* kev,
+          std::vector<int>* kev_kind) {
+  const Dag& g = *ctx->dag;
+  const int64_t per_t_m = 16LL * g.N * g.N;
+  cudaStream_t st[3] = {ctx->cs, ctx->hs, ctx->ds};
+  int nl = 0;
+  ck(cudaEventRecord(ctx->ev_start, ctx->cs), "event");
+  ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_start, 0), "wait");
+  ck(cudaStreamWaitEvent(ctx->ds, ctx->ev_start, 0), "wait");
+  for (size_t i = 0; i < ctx->pp.ops.size(); ++i) {
+    const PhysOp& op = ctx->pp.ops[i];
+    if (op.stream == S_NONE) continue;
+    cudaStream_t s = st[op.stream];
+    for (int32_t d : op.deps) ck(cudaStreamWaitEvent(s, ctx->events[size_t(d)], 0), "wait");
+    const Node& n = g.nodes[size_t(op.node)];
+    switch (op.kind) {
+      case OP_H2D: {
+        const void* src;
+        if (n.leaf()) {
+          const char* h = static_cast<const char*>(ctx->leaf_host[size_t(op.node)]);
+          if (!h) throw Error(CC_E_STATE, "leaf " + std::to_string(n.id) + " has no data (cc_set_leaf)");
+          const int64_t per_t = n.op == CC_LEAF_M ? per_t_m : per_t_m * g.S * g.N;
+          src = h + int64_t(ctx->t0) * per_t;
+        } else {
+          src = ctx->host_pool + op.host_off;
+        }
+        ck(cudaMemcpyAsync(ctx->arena + op.dev_off, src, size_t(op.bytes), cudaMemcpyHostToDevice, s), "H2D");
+        break;
+      }
+      case OP_D2H:
+        ck(cudaMemcpyAsync(ctx->host_pool + op.host_off, ctx->arena + op.dev_off, size_t(op.bytes),
+                           cudaMemcpyDeviceToHost, s),
+           "D2H");
+        break;
+      case OP_CONTRACT: {
+        const void* a = op.loc_a == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.l)] : ctx->arena + op.off_a;
+        const void* b = op.loc_b == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.r)] : ctx->arena + op.off_b;
+        void* out = op.dev_off >= 0 ? ctx->arena + op.dev_off : nullptr;
+        const int64_t slot = n.type == ROOT ? g.tree_of_root[size_t(op.node)] : -1;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (time_kernels) {
+          ck(cudaEventCreate(&e0), "event");
+          ck(cudaEventCreate(&e1), "event");
+          ck(cudaEventRecord(e0, s), "event");
+        }
+        launch_contract(ctx, n, a, b, out, slot, &nl);
+        if (time_kernels) {
+          ck(cudaEventRecord(e1, s), "event");
+          kev->push_back({e0, e1});
+          kev_kind->push_back(n.op);
+        }
+        break;
+      }
+      default:
+        break;
+    }
+    if (op.source) ck(cudaEventRecord(ctx->events[i], s), "event");
+  }
+  ck(launch_correlate(ctx->roots, ctx->corr, int64_t(g.corr_ids.size()), g.Lt, ctx->term_start, ctx->term_tree,
+                      ctx->term_coef, ctx->cs),
+     "correlate kernel");
+  ++nl;
+  ck(cudaEventRecord(ctx->ev_h_end, ctx->hs), "event");
+  ck(cudaEventRecord(ctx->ev_d_end, ctx->ds), "event");
+  ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_h_end, 0), "wait");
+  ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_d_end, 0), "wait");
+  return nl;
+}
+
+void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
+  ctx->need_device();
+  if (!ctx->scheduled) throw Error(CC_E_STATE, "cc_execute before cc_schedule");
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  prepare_phys(ctx);
+  const bool use_graph = (flags & 1) != 0;
+  const bool time_kernels = (flags & 2) != 0 && !use_graph;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;
+  std::vector<int> kev_kind;
+  cudaEvent_t t_begin, t_end;
+  ck(cudaEventCreate(&t_begin), "event");
+  ck(cudaEventCreate(&t_end), "event");
+  ck(cudaEventRecord(t_begin, ctx->cs), "event");
+  if (use_graph) {
+    if (!ctx->gexec) {
+      cudaGraph_t graph;
+      ck(cudaStreamBeginCapture(ctx->cs, cudaStreamCaptureModeThreadLocal), "graph capture");
+      try {
+        ctx->last_n_kernels = issue(ctx, false, nullptr, nullptr);
+      } catch (...) {
+        cudaStreamEndCapture(ctx->cs, &graph);
+        throw;
+      }
+      ck(cudaStreamEndCapture(ctx->cs, &graph), "graph capture");
+      ck(cudaGraphInstantiate(&ctx->gexec, graph, 0), "graph instantiate");
+      cudaGraphDestroy(graph);
+    }
+    ck(cudaGraphLaunch(ctx->gexec, ctx->cs), "graph launch");
+  } else {
+    ctx->last_n_kernels = issue(ctx, time_kernels, &kev, &kev_kind);
+  }
+  ck(cudaEventRecord(t_end, ctx->cs), "event");
+  ctx->executed = true;
+  if (blocking) {
+    ck(cudaEventSynchronize(t_end), "execute");
+    ck(cudaGetLastError(), "execute");
+  }
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    if (blocking) {
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, t_begin, t_end), "elapsed");
+      stats->seconds = ms * 1e-3;
+    }
+    const Dag& g = *ctx->dag;
+    for (const auto& op : ctx->pp.ops)
+      if (op.kind == OP_CONTRACT) {
+        stats->flops += node_flops(g.nodes[size_t(op.node)], g.Lt, g.N, g.S);
+        stats->hbm_bytes += node_hbm_bytes(g.nodes[size_t(op.node)], g.Lt, g.N, g.S);
+      }
+    stats->h2d_bytes = ctx->pp.h2d_bytes;
+    stats->d2h_bytes = ctx->pp.d2h_bytes;
+    stats->n_kernels = ctx->last_n_kernels;
+  }
+  ctx->ktimes = KindTimes{};
+  for (size_t i = 0; i < kev.size(); ++i) {
+    float ms = 0;
+    if (blocking) cudaEventElapsedTime(&ms, kev[i].first, kev[i].second);
+    ctx->ktimes.seconds[kev_kind[i]] += ms * 1e-3;
+    ctx->ktimes.count[kev_kind[i]] += 1;
+    cudaEventDestroy(kev[i].first);
+    cudaEventDestroy(kev[i].second);
+  }
+  if (stats) {
+    double ks = 0;
+    for (int k = 0; k < 8; ++k) ks += ctx->ktimes.seconds[k];
+    stats->kernel_seconds = ks;
+  }
+  cudaEventDestroy(t_begin);
+  cudaEventDestroy(t_end);
+}
+
+void ensure_direct_ws(cc_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->direct_ws_bytes) return;
+  if (ctx->direct_ws) ck(cudaFree(ctx->direct_ws), "cudaFree");
+  ctx->direct_ws = nullptr;
+  ctx->direct_ws_bytes = 0;
+  ck(cudaMalloc(reinterpret_cast<void**>(&ctx->direct_ws), bytes), "workspace");
+  ck(cudaMemset(ctx->direct_ws, 0, bytes), "workspace");
+  ctx->direct_ws_bytes = bytes;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+extern "C" {
+
+const char* cc_version(void) { return CC_VERSION; }
+
+const char* cc_last_error(const cc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+cc_status cc_create(cc_ctx** out, int device, void* dev_arena, size_t arena_bytes, void* compute_stream,
+                    void* h2d_stream, void* d2h_stream) {
+  cc_ctx* ctx = nullptr;
+  if (!out) return CC_E_INVAL;
+  *out = nullptr;
+  try {
+    ctx = new cc_ctx();
+  } catch (...) {
+    return CC_E_NOMEM;
+  }
+  API_BEGIN
+  ctx->device = device;
+  ctx->host_only = device < 0;
+  *out = ctx;
+  if (!ctx->host_only) {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10) throw Error(CC_E_CUDA, std::string("needs an sm_100 GPU (B200), found ") + prop.name);
+    ctx->num_sms = prop.multiProcessorCount;
+    ctx->arena = static_cast<char*>(dev_arena);
+    ctx->arena_bytes = int64_t(arena_bytes);
+    if (compute_stream) {
+      ctx->cs = static_cast<cudaStream_t>(compute_stream);
+      ctx->hs = static_cast<cudaStream_t>(h2d_stream);
+      ctx->ds = static_cast<cudaStream_t>(d2h_stream);
+      if (!ctx->hs || !ctx->ds) throw Error(CC_E_INVAL, "give all three streams or none");
+    } else {
+      ctx->own_streams = true;
+      ck(cudaStreamCreateWithFlags(&ctx->cs, cudaStreamNonBlocking), "stream");
+      ck(cudaStreamCreateWithFlags(&ctx->hs, cudaStreamNonBlocking), "stream");
+      ck(cudaStreamCreateWithFlags(&ctx->ds, cudaStreamNonBlocking), "stream");
+    }
+    for (cudaEvent_t* e : {&ctx->ev_start, &ctx->ev_end, &ctx->ev_h_end, &ctx->ev_d_end})
+      ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+  }
+  API_END
+}
+
+void cc_destroy(cc_ctx* ctx) { delete ctx; }
+
+cc_status cc_load_dag(cc_ctx* ctx, const cc_dims* dims, const cc_node* nodes, int64_t n_nodes, const cc_tree* trees,
+                      int64_t n_trees, const cc_term* terms, int64_t n_terms) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!dims || (n_nodes > 0 && !nodes) || (n_trees > 0 && !trees) || (n_terms > 0 && !terms) || n_nodes < 0 ||
+      n_trees < 0 || n_terms < 0)
+    throw Error(CC_E_INVAL, "null or negative DAG arrays");
+  Input in;
+  in.dims = *dims;
+  in.nodes.assign(nodes, nodes + n_nodes);
+  in.trees.assign(trees, trees + n_trees);
+  in.terms.assign(terms, terms + n_terms);
+  ctx->loaded = false;
+  ctx->input = std::move(in);
+  ctx->n_parts = 1;
+  ctx->part = 0;
+  rebuild_dag(ctx);
+  ctx->loaded = true;
+  API_END
+}
+
+cc_status cc_load_dag_file(cc_ctx* ctx, const char* path) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!path) throw Error(CC_E_INVAL, "null path");
+  Input in = parse_text_file(path);
+  ctx->loaded = false;
+  ctx->input = std::move(in);
+  ctx->n_parts = 1;
+  ctx->part = 0;
+  rebuild_dag(ctx);
+  ctx->loaded = true;
+  API_END
+}
+
+cc_status cc_dag_info(cc_ctx* ctx, cc_dag_stats* out) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->loaded) throw Error(CC_E_STATE, "no DAG loaded");
+  if (!out) throw Error(CC_E_INVAL, "null output");
+  *out = ctx->dag->stats();
+  API_END
+}
+
+cc_status cc_partition(cc_ctx* ctx, int32_t n_parts, int32_t part, int32_t mode) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->loaded) throw Error(CC_E_STATE, "no DAG loaded");
+  if (n_parts < 1 || part < 0 || part >= n_parts || mode < 0 || mode > 1) throw Error(CC_E_INVAL, "bad partition");
+  ctx->n_parts = n_parts;
+  ctx->part = part;
+  ctx->mode = mode;
+  rebuild_dag(ctx);
+  API_END
+}
+
+cc_status cc_part_trees(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->loaded) throw Error(CC_E_STATE, "no DAG loaded");
+  if (n_out) *n_out = int64_t(ctx->part_trees.size());
+  if (out) {
+    if (cap < int64_t(ctx->part_trees.size())) throw Error(CC_E_BUFFER_TOO_SMALL, "buffer too small");
+    std::copy(ctx->part_trees.begin(), ctx->part_trees.end(), out);
+  }
+  API_END
+}
+
+cc_status cc_schedule(cc_ctx* ctx, const cc_sched_cfg* cfg, int64_t* order_out, int64_t order_cap, int64_t* n_order,
+                      cc_plan_stats* stats) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->loaded) throw Error(CC_E_STATE, "cc_schedule before cc_load_dag");
+  if (!cfg) throw Error(CC_E_INVAL, "null config");
+  const Dag& g = *ctx->dag;
+  ctx->scheduled = false;
+  ctx->executed = false;
+  ctx->release_phys();
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<int32_t> order;
+  std::vector<int32_t> tree_order;
+  if (cfg->algo == CC_SIBLING) {
+    order = sibling_schedule(g);
+  } else if (cfg->algo == CC_TREE) {
+    TreeSchedule ts = tree_schedule(g);
+    order = std::move(ts.order);
+    tree_order = std::move(ts.tree_order);
+  } else if (cfg->algo == CC_GIVEN) {
+    if (cfg->n_given < 0 || (cfg->n_given > 0 && !cfg->given_order)) throw Error(CC_E_INVAL, "bad given order");
+    order.reserve(size_t(cfg->n_given));
+    for (int64_t i = 0; i < cfg->n_given; ++i) order.push_back(g.idx(cfg->given_order[i]));
+  } else {
+    throw Error(CC_E_INVAL, "unknown scheduler");
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  check_order(g, order);
+  ctx->mt = simulate_model(g, order);
+  ctx->lp = lru_plan(g, order, cfg->cap_bytes);
+  auto t2 = std::chrono::steady_clock::now();
+  ctx->order = std::move(order);
+  ctx->tree_order = std::move(tree_order);
+  ctx->cap = cfg->cap_bytes;
+  cc_plan_stats& s = ctx->stats;
+  s = cc_plan_stats{};
+  s.n_contr = g.n_contr;
+  s.peak = ctx->lp.peak;
+  s.transient_peak = ctx->lp.transient_peak;
+  s.evictions = ctx->lp.evictions;
+  s.h2d_count = ctx->lp.h2d_count;
+  s.d2h_count = ctx->lp.d2h_count;
+  s.h2d_bytes = ctx->lp.h2d_bytes;
+  s.d2h_bytes = ctx->lp.d2h_bytes;
+  s.host_peak_bytes = ctx->lp.host_peak;
+  s.model_peak = ctx->mt.peak;
+  s.model_transient_peak = ctx->mt.transient_peak;
+  s.sched_seconds = std::chrono::duration<double>(t1 - t0).count();
+  s.plan_seconds = std::chrono::duration<double>(t2 - t1).count();
+  ctx->scheduled = true;
+  if (n_order) *n_order = int64_t(ctx->order.size());
+  if (order_out) {
+    if (order_cap < int64_t(ctx->order.size())) throw Error(CC_E_BUFFER_TOO_SMALL, "order buffer too small");
+    for (size_t i = 0; i < ctx->order.size(); ++i) order_out[i] = g.nodes[size_t(ctx->order[i])].id;
+  }
+  if (stats) *stats = s;
+  API_END
+}
+
+cc_status cc_memory_trace(cc_ctx* ctx, int64_t* m_out, int64_t* transient_out, int64_t cap, int64_t* n_out) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->scheduled) throw Error(CC_E_STATE, "no schedule");
+  const int64_t n = int64_t(ctx->mt.transient.size());
+  if (n_out) *n_out = n;
+  if (m_out) {
+    if (cap < n + 1) throw Error(CC_E_BUFFER_TOO_SMALL, "buffer too small");
+    std::copy(ctx->mt.M.begin(), ctx->mt.M.end(), m_out);
+  }
+  if (transient_out) {
+    if (cap < n) throw Error(CC_E_BUFFER_TOO_SMALL, "buffer too small");
+    std::copy(ctx->mt.transient.begin(), ctx->mt.transient.end(), transient_out);
+  }
+  API_END
+}
+
+cc_status cc_plan_ops(cc_ctx* ctx, cc_plan_op* out, int64_t cap, int64_t* n_out) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->scheduled) throw Error(CC_E_STATE, "no schedule");
+  const auto& ops = ctx->lp.ops;
+  if (n_out) *n_out = int64_t(ops.size());
+  if (out) {
+    if (cap < int64_t(ops.size())) throw Error(CC_E_BUFFER_TOO_SMALL, "buffer too small");
+    const bool phys = ctx->phys_valid;
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const Node& n = ctx->dag->nodes[size_t(ops[i].node)];
+      out[i] = cc_plan_op{ops[i].kind, 0, n.id, n.size, phys ? ctx->pp.ops[i].dev_off : -1};
+    }
+  }
+  API_END
+}
+
+cc_status cc_tree_order(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->scheduled) throw Error(CC_E_STATE, "no schedule");
+  if (n_out) *n_out = int64_t(ctx->tree_order.size());
+  if (out) {
+    if (cap < int64_t(ctx->tree_order.size())) throw Error(CC_E_BUFFER_TOO_SMALL, "buffer too small");
+    for (size_t i = 0; i < ctx->tree_order.size(); ++i) out[i] = ctx->dag->trees[size_t(ctx->tree_order[i])].tree_id;
+  }
+  API_END
+}
+
+cc_status cc_plan_dump(cc_ctx* ctx, const char* csv_path) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->scheduled) throw Error(CC_E_STATE, "no schedule");
+  std::ofstream f(csv_path);
+  if (!f) throw Error(CC_E_INVAL, "cannot write " + std::string(csv_path ? csv_path : "(null)"));
+  static const char* kinds[5] = {"H2D", "D2H", "DROP", "CONTRACT", "FREE"};
+  f << "step,op,node,bytes,offset,device_used\n";
+  int64_t step = 0;
+  for (size_t i = 0; i < ctx->lp.ops.size(); ++i) {
+    const auto& op = ctx->lp.ops[i];
+    const Node& n = ctx->dag->nodes[size_t(op.node)];
+    if (op.kind == OP_CONTRACT) ++step;
+    f << step << ',' << kinds[op.kind] << ',' << n.id << ',' << n.size << ','
+      << (ctx->phys_valid ? ctx->pp.ops[i].dev_off : -1) << ',' << ctx->lp.used[size_t(step)] << '\n';
+  }
+  API_END
+}
+
+cc_status cc_set_leaf(cc_ctx* ctx, int64_t leaf_id, const void* host, size_t bytes) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->loaded) throw Error(CC_E_STATE, "no DAG loaded");
+  const Dag& g = *ctx->dag;
+  auto it = g.index.find(leaf_id);
+  if (it == g.index.end()) {
+    // a leaf of another TREES part: accepted and ignored
+    for (const auto& n : ctx->input.nodes)
+      if (n.id == leaf_id) return CC_OK;
+    throw Error(CC_E_UNKNOWN_NODE, "unknown leaf " + std::to_string(leaf_id));
+  }
+  const Node& n = g.nodes[size_t(it->second)];
+  if (!n.leaf()) throw Error(CC_E_INVAL, "node " + std::to_string(leaf_id) + " is not a leaf");
+  const int64_t full = tensor_bytes(n.op, ctx->input.dims.Lt, g.N, g.S);
+  if (int64_t(bytes) != full) throw Error(CC_E_INVAL, "leaf " + std::to_string(leaf_id) + ": expected " + std::to_string(full) + " bytes");
+  if (!host) throw Error(CC_E_INVAL, "null host pointer");
+  const bool was_dev = ctx->leaf_dev[size_t(it->second)] != nullptr;
+  ctx->leaf_host[size_t(it->second)] = host;
+  ctx->leaf_dev[size_t(it->second)] = nullptr;
+  if (was_dev) {
+    ctx->phys_valid = false;
+    ctx->release_graph();
+  }
+  ctx->release_graph();  // host pointers are baked into a captured graph
+  API_END
+}
+
+cc_status cc_set_leaf_device(cc_ctx* ctx, int64_t leaf_id, const void* dev, size_t bytes) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->loaded) throw Error(CC_E_STATE, "no DAG loaded");
+  const Dag& g = *ctx->dag;
+  auto it = g.index.find(leaf_id);
+  if (it == g.index.end()) {
+    for (const auto& n : ctx->input.nodes)
+      if (n.id == leaf_id) return CC_OK;
+    throw Error(CC_E_UNKNOWN_NODE, "unknown leaf " + std::to_string(leaf_id));
+  }
+  const Node& n = g.nodes[size_t(it->second)];
+  if (!n.leaf()) throw Error(CC_E_INVAL, "node " + std::to_string(leaf_id) + " is not a leaf");
+  if (int64_t(bytes) != n.size) throw Error(CC_E_INVAL, "leaf " + std::to_string(leaf_id) + ": expected " + std::to_string(n.size) + " bytes");
+  if (!dev) throw Error(CC_E_INVAL, "null device pointer");
+  const bool was_dev = ctx->leaf_dev[size_t(it->second)] != nullptr;
+  ctx->leaf_dev[size_t(it->second)] = dev;
+  ctx->leaf_host[size_t(it->second)] = nullptr;
+  if (!was_dev) ctx->phys_valid = false;
+  ctx->release_graph();
+  API_END
+}
+
+cc_status cc_execute(cc_ctx* ctx, int32_t flags, cc_exec_stats* stats) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  execute(ctx, flags, true, stats);
+  API_END
+}
+
+cc_status cc_execute_async(cc_ctx* ctx, int32_t flags) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  execute(ctx, flags & 1, false, nullptr);
+  API_END
+}
+
+cc_status cc_correlator(cc_ctx* ctx, int64_t corr_id, double* out, int32_t Lt) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  ctx->need_device();
+  if (!ctx->executed) throw Error(CC_E_STATE, "cc_correlator before cc_execute");
+  const Dag& g = *ctx->dag;
+  if (Lt != g.Lt) throw Error(CC_E_INVAL, "Lt must be the part's Lt (" + std::to_string(g.Lt) + ")");
+  auto it = std::lower_bound(g.corr_ids.begin(), g.corr_ids.end(), corr_id);
+  if (it == g.corr_ids.end() || *it != corr_id) throw Error(CC_E_UNKNOWN_NODE, "unknown correlator " + std::to_string(corr_id));
+  const int64_t slot = it - g.corr_ids.begin();
+  ck(cudaStreamSynchronize(ctx->cs), "sync");
+  ck(cudaMemcpy(out, ctx->corr + slot * g.Lt, size_t(g.Lt) * 16, cudaMemcpyDeviceToHost), "correlator D2H");
+  API_END
+}
+
+cc_status cc_root_value(cc_ctx* ctx, int64_t tree_id, double* out, int32_t Lt) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  ctx->need_device();
+  if (!ctx->executed) throw Error(CC_E_STATE, "cc_root_value before cc_execute");
+  const Dag& g = *ctx->dag;
+  if (Lt != g.Lt) throw Error(CC_E_INVAL, "Lt must be the part's Lt");
+  int64_t slot = -1;
+  for (size_t t = 0; t < g.trees.size(); ++t)
+    if (g.trees[t].tree_id == tree_id) slot = int64_t(t);
+  if (slot < 0) throw Error(CC_E_UNKNOWN_NODE, "unknown tree " + std::to_string(tree_id));
+  ck(cudaStreamSynchronize(ctx->cs), "sync");
+  ck(cudaMemcpy(out, ctx->roots + slot * g.Lt, size_t(g.Lt) * 16, cudaMemcpyDeviceToHost), "root D2H");
+  API_END
+}
+
+cc_status cc_correlator_device_ptr(cc_ctx* ctx, void** dev_ptr, int64_t* n_corr, int64_t* corr_ids) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  ctx->need_device();
+  if (!ctx->executed) throw Error(CC_E_STATE, "before cc_execute");
+  const Dag& g = *ctx->dag;
+  if (dev_ptr) *dev_ptr = ctx->corr;
+  if (n_corr) *n_corr = int64_t(g.corr_ids.size());
+  if (corr_ids) std::copy(g.corr_ids.begin(), g.corr_ids.end(), corr_ids);
+  API_END
+}
+
+cc_status cc_kernel_times(cc_ctx* ctx, double* seconds, int64_t* counts) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  for (int k = 0; k < 8; ++k) {
+    if (seconds) seconds[k] = ctx->ktimes.seconds[k];
+    if (counts) counts[k] = ctx->ktimes.count[k];
+  }
+  API_END
+}
+
+static cc_status direct_gemm(cc_ctx* ctx, int op, const void* A, const void* B, void* C, int32_t Lt, int32_t N,
+                             int32_t S) {
+  API_BEGIN
+  ctx->need_device();
+  if (!A || !B || !C || Lt <= 0 || N <= 0 || S <= 0) throw Error(CC_E_INVAL, "bad kernel arguments");
+  ZgemmProblem p = problem_for(op, Lt, N, S, A, B, C);
+  ensure_direct_ws(ctx, std::max<size_t>(zgemm_workspace_bytes(p, ctx->num_sms), 256));
+  int nl = 0;
+  ck(launch_zgemm(p, ctx->direct_ws, ctx->direct_ws_bytes, ctx->num_sms, ctx->cs, &nl), "contraction kernel");
+  API_END
+}
+
+cc_status cc_mm1(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt, int32_t N) {
+  if (!ctx) return CC_E_INVAL;
+  return direct_gemm(ctx, CC_MM1, A, B, C, Lt, N, 1);
+}
+cc_status cc_bm1(cc_ctx* ctx, const void* A, const void* M, void* C, int32_t Lt, int32_t N, int32_t S) {
+  if (!ctx) return CC_E_INVAL;
+  return direct_gemm(ctx, CC_BM1, A, M, C, Lt, N, S);
+}
+cc_status cc_bb2(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt, int32_t N, int32_t S) {
+  if (!ctx) return CC_E_INVAL;
+  return direct_gemm(ctx, CC_BB2, A, B, C, Lt, N, S);
+}
+cc_status cc_tr_mm(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t Lt, int32_t N) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  ctx->need_device();
+  if (!A || !B || !c || Lt <= 0 || N <= 0) throw Error(CC_E_INVAL, "bad kernel arguments");
+  ensure_direct_ws(ctx, trace_workspace_bytes(Lt, N));
+  ck(launch_trace(A, B, c, Lt, N, ctx->direct_ws, ctx->cs), "TR_MM kernel");
+  API_END
+}
+
+cc_status cc_fill_synthetic(cc_ctx* ctx, void* dev, int64_t n, uint64_t seed, int64_t leaf_id, int64_t e0, int32_t mode,
+                            double sigma) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  ctx->need_device();
+  if (!dev || n < 0 || e0 < 0 || mode < 0 || mode > 1) throw Error(CC_E_INVAL, "bad arguments");
+  ck(launch_fill_synthetic(dev, n, seed, leaf_id, e0, mode, sigma, ctx->cs), "fill kernel");
+  API_END
+}
+
+size_t cc_scratch_bytes(int32_t Lt, int32_t N, int32_t S) {
+  // upper bound of prepare_phys's scratch for DAGs with up to 2^16 trees/terms/correlators
+  size_t ws = 0;
+  for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)})
+    ws = std::max(ws, zgemm_workspace_bytes(problem_for(op, Lt, N, S, nullptr, nullptr, nullptr), 148));
+  return ws + trace_workspace_bytes(Lt, N) + size_t(Lt) * 16 * 3 * 65536 + (size_t(16) << 20);
+}
+
+}  // extern "C"

@@ -1,0 +1,352 @@
+// Memory model, LRU device plan and physical placement.
+//
+// simulate_model: §II-C: for c_i (i) load the leaf operands not in
+//   memory, (ii) produce the output, (iii) release tensors no remaining contraction needs,
+//   including a ROOT output; M_i after (iii), transient after (ii) (reading G-5).
+// lru_plan: MemHC-style "pre-protected LRU" eviction to host, readings E-1..E-8:
+//   before c_i evict least-recently-used non-operand tensors until operands + output fit;
+//   leaves are dropped (no D2H), an intermediate is copied to host on its first eviction
+//   and the host copy is kept until release; fetches are touches; LRU ties cannot occur
+//   (one clock tick per touch: operands left then right, then the output).
+// build_phys: offline placement of every residency in the device pool (best fit) and the
+//   host pool, plus cross-stream event dependencies: RAW on data (ready op of each operand,
+//   D2H before a re-fetch) and WAR/WAW on reused byte ranges.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <limits>
+
+namespace cc {
+
+void check_order(const Dag& g, const std::vector<int32_t>& order) {
+  std::vector<int32_t> pos(g.nodes.size(), -1);
+  for (size_t i = 0; i < order.size(); ++i) {
+    const int32_t u = order[i];
+    if (u < 0 || u >= int32_t(g.nodes.size())) throw Error(CC_E_INVAL, "schedule: bad node");
+    if (g.nodes[u].leaf()) throw Error(CC_E_INVAL, "schedule: leaf " + std::to_string(g.nodes[u].id) + " scheduled");
+    if (pos[u] >= 0) throw Error(CC_E_INVAL, "schedule: node " + std::to_string(g.nodes[u].id) + " twice");
+    pos[u] = int32_t(i);
+  }
+  if (int64_t(order.size()) != g.n_contr) throw Error(CC_E_INVAL, "schedule: missing contractions");
+  for (size_t i = 0; i < order.size(); ++i) {
+    const Node& n = g.nodes[order[i]];
+    for (int32_t c : {n.l, n.r})
+      if (!g.nodes[c].leaf() && pos[c] > int32_t(i))
+        throw Error(CC_E_INVAL, "schedule: node " + std::to_string(n.id) + " before its child " +
+                                    std::to_string(g.nodes[c].id));
+  }
+}
+
+ModelTrace simulate_model(const Dag& g, const std::vector<int32_t>& order) {
+  ModelTrace tr;
+  std::vector<int32_t> remaining(g.nodes.size());
+  std::vector<uint8_t> resident(g.nodes.size(), 0);
+  for (size_t u = 0; u < g.nodes.size(); ++u) remaining[u] = int32_t(g.nodes[u].parents.size());
+  int64_t used = 0;
+  tr.M.reserve(order.size() + 1);
+  tr.transient.reserve(order.size());
+  tr.M.push_back(0);
+  for (int32_t u : order) {
+    const Node& n = g.nodes[u];
+    for (int32_t c : {n.l, n.r})                  // (i) lazy leaf loads
+      if (g.nodes[c].leaf() && !resident[c]) {
+        resident[c] = 1;
+        used += g.nodes[c].size;
+      }
+    resident[u] = 1;                               // (ii)
+    used += n.size;
+    tr.transient.push_back(used);
+    tr.transient_peak = std::max(tr.transient_peak, used);
+    for (int32_t c : {n.l, n.r})                  // (iii)
+      if (--remaining[c] == 0) {
+        resident[c] = 0;
+        used -= g.nodes[c].size;
+      }
+    if (remaining[u] == 0) {
+      resident[u] = 0;
+      used -= n.size;
+    }
+    tr.M.push_back(used);
+    tr.peak = std::max(tr.peak, used);
+  }
+  return tr;
+}
+
+LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap) {
+  const bool bounded = cap > 0;
+  const size_t n = g.nodes.size();
+  LruPlan p;
+  std::vector<int32_t> remaining(n);
+  std::vector<uint8_t> resident(n, 0), host_copy(n, 0);
+  std::vector<int64_t> stamp(n, 0);
+  for (size_t u = 0; u < n; ++u) remaining[u] = int32_t(g.nodes[u].parents.size());
+  // resident tensors ordered by last touch: (stamp, node)
+  std::set<std::pair<int64_t, int32_t>> lru;
+  int64_t clock = 0, used = 0, host = 0;
+  p.used.reserve(order.size() + 1);
+  p.used.push_back(0);
+  auto touch = [&](int32_t x) {
+    if (resident[x]) lru.erase({stamp[x], x});
+    stamp[x] = ++clock;
+    lru.insert({stamp[x], x});
+  };
+  for (int32_t u : order) {
+    const Node& nd = g.nodes[u];
+    const int32_t ops[2] = {nd.l, nd.r};
+    const int64_t work = g.nodes[nd.l].size + g.nodes[nd.r].size + nd.size;
+    if (bounded && work > cap)
+      throw Error(CC_E_INFEASIBLE, "contraction " + std::to_string(nd.id) + " needs " + std::to_string(work) +
+                                       " bytes > cap " + std::to_string(cap));
+    int64_t need = nd.size;
+    for (int32_t x : ops)
+      if (!resident[x]) need += g.nodes[x].size;
+    while (bounded && used + need > cap) {          // E-1
+      auto it = lru.begin();
+      while (it != lru.end() && (it->second == ops[0] || it->second == ops[1])) ++it;
+      if (it == lru.end()) throw Error(CC_E_INFEASIBLE, "no evictable tensor");
+      const int32_t v = it->second;
+      lru.erase(it);
+      ++p.evictions;
+      if (!g.nodes[v].leaf() && !host_copy[v]) {    // E-4: first eviction copies to host
+        ++p.d2h_count;
+        p.d2h_bytes += g.nodes[v].size;
+        host_copy[v] = 1;
+        host += g.nodes[v].size;
+        p.host_peak = std::max(p.host_peak, host);
+        p.ops.push_back({OP_D2H, v});
+      } else {                                       // E-3 / clean re-eviction
+        p.ops.push_back({OP_DROP, v});
+      }
+      resident[v] = 0;
+      used -= g.nodes[v].size;
+    }
+    for (int32_t x : ops) {                          // fetch + touch, left then right (E-2)
+      if (!resident[x]) {
+        ++p.h2d_count;
+        p.h2d_bytes += g.nodes[x].size;
+        used += g.nodes[x].size;
+        p.ops.push_back({OP_H2D, x});
+        stamp[x] = ++clock;
+        resident[x] = 1;
+        lru.insert({stamp[x], x});
+      } else {
+        touch(x);
+      }
+    }
+    used += nd.size;                                  // output
+    stamp[u] = ++clock;
+    resident[u] = 1;
+    lru.insert({stamp[u], u});
+    p.ops.push_back({OP_CONTRACT, u});
+    p.transient_peak = std::max(p.transient_peak, used);
+    for (int32_t x : ops)                             // release at last use (E-8)
+      if (--remaining[x] == 0) {
+        lru.erase({stamp[x], x});
+        resident[x] = 0;
+        used -= g.nodes[x].size;
+        if (host_copy[x]) {
+          host_copy[x] = 0;
+          host -= g.nodes[x].size;
+        }
+        p.ops.push_back({OP_FREE, x});
+      }
+    if (remaining[u] == 0) {                          // ROOT output released at once
+      lru.erase({stamp[u], u});
+      resident[u] = 0;
+      used -= nd.size;
+      p.ops.push_back({OP_FREE, u});
+    }
+    p.peak = std::max(p.peak, used);
+    p.used.push_back(used);
+  }
+  if (used != 0 || host != 0) throw Error(CC_E_STATE, "plan: accounting did not return to zero");
+  return p;
+}
+
+// ---------------------------------------------------------------------------------------
+RangeAlloc::RangeAlloc(int64_t capacity) {
+  if (capacity > 0) {
+    by_off_[0] = capacity;
+    by_size_.insert({capacity, 0});
+  }
+}
+
+int64_t RangeAlloc::alloc(int64_t bytes) {
+  auto it = by_size_.lower_bound({bytes, std::numeric_limits<int64_t>::min()});
+  if (it == by_size_.end()) return -1;
+  const int64_t size = it->first, off = it->second;
+  by_size_.erase(it);
+  by_off_.erase(off);
+  if (size > bytes) {
+    by_off_[off + bytes] = size - bytes;
+    by_size_.insert({size - bytes, off + bytes});
+  }
+  high_ = std::max(high_, off + bytes);
+  return off;
+}
+
+void RangeAlloc::free(int64_t off, int64_t bytes) {
+  auto next = by_off_.lower_bound(off);
+  if (next != by_off_.end() && next->first == off + bytes) {
+    bytes += next->second;
+    by_size_.erase({next->second, next->first});
+    next = by_off_.erase(next);
+  }
+  if (next != by_off_.begin()) {
+    auto prev = std::prev(next);
+    if (prev->first + prev->second == off) {
+      off = prev->first;
+      bytes += prev->second;
+      by_size_.erase({prev->second, prev->first});
+      by_off_.erase(prev);
+    }
+  }
+  by_off_[off] = bytes;
+  by_size_.insert({bytes, off});
+}
+
+RangeTracker::RangeTracker(int64_t capacity) {
+  pieces_[0] = Piece{capacity, {-1, -1, -1}};
+}
+
+void RangeTracker::split(int64_t at) {
+  auto it = pieces_.upper_bound(at);
+  if (it == pieces_.begin()) return;
+  --it;
+  if (it->first == at || it->second.end <= at) return;
+  Piece hi = it->second;
+  it->second.end = at;
+  pieces_[at] = hi;
+}
+
+void RangeTracker::access(int64_t off, int64_t bytes, int stream, int32_t op, std::vector<int32_t>& deps) {
+  split(off);
+  split(off + bytes);
+  for (auto it = pieces_.find(off); it != pieces_.end() && it->first < off + bytes; ++it) {
+    for (int s = 0; s < 3; ++s)
+      if (s != stream && it->second.last[s] >= 0) deps.push_back(it->second.last[s]);
+    it->second.last[stream] = op;
+  }
+}
+
+static int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>& leaf_on_device,
+                    int64_t pool_bytes, int64_t align) {
+  PhysPlan pp;
+  const size_t n = g.nodes.size();
+  // host pool: sized for the worst case (sum of all D2H'd sizes), placed best-fit
+  int64_t host_cap = 0;
+  for (const auto& op : lp.ops)
+    if (op.kind == OP_D2H) host_cap += round_up(g.nodes[op.node].size, align);
+  RangeAlloc dev(pool_bytes), hostp(host_cap);
+  RangeTracker dtr(pool_bytes), htr(std::max<int64_t>(host_cap, 1));
+  std::vector<int64_t> dev_off(n, -1), host_off(n, -1);
+  std::vector<int32_t> ready(n, -1), ready_stream(n, -1), d2h_op(n, -1);
+  auto need_ready = [&](int32_t x, int stream, std::vector<int32_t>& deps) {
+    if (ready[x] >= 0 && ready_stream[x] != stream) deps.push_back(ready[x]);
+  };
+  for (const auto& lop : lp.ops) {
+    const int32_t x = lop.node;
+    const Node& nd = g.nodes[x];
+    const int32_t me = int32_t(pp.ops.size());
+    PhysOp op{lop.kind, x, S_NONE};
+    op.bytes = nd.size;
+    const int64_t rb = round_up(nd.size, align);
+    switch (lop.kind) {
+      case OP_H2D: {
+        if (nd.leaf() && leaf_on_device[x]) break;            // already in HBM: no copy
+        const int64_t off = dev.alloc(rb);
+        if (off < 0) throw Error(CC_E_NOMEM, "device pool fragmented/too small for node " + std::to_string(nd.id));
+        dev_off[x] = off;
+        op.stream = S_H2D;
+        op.dev_off = off;
+        dtr.access(off, rb, S_H2D, me, op.deps);
+        if (!nd.leaf()) {                                       // re-fetch of an evicted intermediate
+          op.host_off = host_off[x];
+          if (d2h_op[x] >= 0) op.deps.push_back(d2h_op[x]);
+          htr.access(host_off[x], rb, S_H2D, me, op.deps);
+        }
+        ready[x] = me;
+        ready_stream[x] = S_H2D;
+        pp.h2d_bytes += nd.size;
+        break;
+      }
+      case OP_D2H: {
+        const int64_t hoff = hostp.alloc(rb);
+        if (hoff < 0) throw Error(CC_E_NOMEM, "host pool allocation failed");
+        host_off[x] = hoff;
+        op.stream = S_D2H;
+        op.dev_off = dev_off[x];
+        op.host_off = hoff;
+        need_ready(x, S_D2H, op.deps);
+        dtr.access(dev_off[x], rb, S_D2H, me, op.deps);
+        htr.access(hoff, rb, S_D2H, me, op.deps);
+        d2h_op[x] = me;
+        dev.free(dev_off[x], rb);
+        dev_off[x] = -1;
+        pp.d2h_bytes += nd.size;
+        break;
+      }
+      case OP_DROP: {
+        if (dev_off[x] >= 0) {
+          dev.free(dev_off[x], rb);
+          dev_off[x] = -1;
+        }
+        break;
+      }
+      case OP_CONTRACT: {
+        op.stream = S_COMPUTE;
+        const int32_t ab[2] = {nd.l, nd.r};
+        for (int k = 0; k < 2; ++k) {
+          const int32_t c = ab[k];
+          int32_t& loc = k ? op.loc_b : op.loc_a;
+          int64_t& off = k ? op.off_b : op.off_a;
+          if (g.nodes[c].leaf() && leaf_on_device[c]) {
+            loc = LOC_DEVLEAF;
+            off = -1;
+          } else {
+            if (dev_off[c] < 0) throw Error(CC_E_STATE, "plan: operand not resident");
+            loc = LOC_POOL;
+            off = dev_off[c];
+            need_ready(c, S_COMPUTE, op.deps);
+            dtr.access(off, round_up(g.nodes[c].size, align), S_COMPUTE, me, op.deps);
+          }
+        }
+        if (nd.type == ROOT) {
+          op.dev_off = -1;                                      // root values buffer
+        } else {
+          const int64_t off = dev.alloc(rb);
+          if (off < 0) throw Error(CC_E_NOMEM, "device pool fragmented/too small for node " + std::to_string(nd.id));
+          dev_off[x] = off;
+          op.dev_off = off;
+          dtr.access(off, rb, S_COMPUTE, me, op.deps);
+        }
+        ready[x] = me;
+        ready_stream[x] = S_COMPUTE;
+        break;
+      }
+      case OP_FREE: {
+        if (dev_off[x] >= 0) {
+          dev.free(dev_off[x], rb);
+          dev_off[x] = -1;
+        }
+        if (host_off[x] >= 0) {
+          hostp.free(host_off[x], rb);
+          host_off[x] = -1;
+        }
+        break;
+      }
+    }
+    std::sort(op.deps.begin(), op.deps.end());
+    op.deps.erase(std::unique(op.deps.begin(), op.deps.end()), op.deps.end());
+    pp.ops.push_back(std::move(op));
+  }
+  for (auto& op : pp.ops)
+    for (int32_t d : op.deps) pp.ops[size_t(d)].source = true;
+  pp.pool_high_water = dev.high_water();
+  pp.host_pool_bytes = host_cap;
+  return pp;
+}
+
+}  // namespace cc

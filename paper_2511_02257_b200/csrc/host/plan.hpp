@@ -1,0 +1,86 @@
+// Memory model (§II-C), LRU device plan (MemHC-style eviction) and physical placement.
+#pragma once
+#include <map>
+#include <set>
+#include <vector>
+
+#include "dag.hpp"
+
+namespace cc {
+
+// §II-C: M_0..M_n after releases; transient_i after producing c_i's output
+// (reading G-5); leaves loaded lazily (G-6).
+struct ModelTrace {
+  std::vector<int64_t> M, transient;
+  int64_t peak = 0, transient_peak = 0;
+};
+ModelTrace simulate_model(const Dag& g, const std::vector<int32_t>& order);
+// Throws CC_E_INVAL when `order` is not a valid schedule of g.
+void check_order(const Dag& g, const std::vector<int32_t>& order);
+
+enum OpKind : int32_t { OP_H2D = 0, OP_D2H = 1, OP_DROP = 2, OP_CONTRACT = 3, OP_FREE = 4 };
+struct LogicalOp { int32_t kind; int32_t node; };
+
+// Capacity-limited LRU plan, readings E-1..E-8.
+struct LruPlan {
+  std::vector<LogicalOp> ops;
+  std::vector<int64_t> used;         // device bytes after each contraction's releases
+  int64_t evictions = 0, h2d_count = 0, d2h_count = 0, h2d_bytes = 0, d2h_bytes = 0;
+  int64_t peak = 0, transient_peak = 0, host_peak = 0;
+};
+LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap);
+
+// Best-fit allocator with coalescing over [0, capacity).
+class RangeAlloc {
+ public:
+  explicit RangeAlloc(int64_t capacity = 0);
+  int64_t alloc(int64_t bytes);      // -1 if no block fits
+  void free(int64_t off, int64_t bytes);
+  int64_t high_water() const { return high_; }
+ private:
+  std::map<int64_t, int64_t> by_off_;
+  std::set<std::pair<int64_t, int64_t>> by_size_;
+  int64_t high_ = 0;
+};
+
+// Per-byte-range record of the last op that touched it on each stream, used to derive
+// WAR / WAW dependencies when a range is reused (offline, at plan time).
+class RangeTracker {
+ public:
+  explicit RangeTracker(int64_t capacity = 0);
+  // ops that a new access by `op` on `stream` must wait for (other streams only)
+  void access(int64_t off, int64_t bytes, int stream, int32_t op, std::vector<int32_t>& deps);
+ private:
+  struct Piece { int64_t end; int32_t last[3]; };
+  std::map<int64_t, Piece> pieces_;
+  void split(int64_t at);
+};
+
+enum Stream : int32_t { S_COMPUTE = 0, S_H2D = 1, S_D2H = 2, S_NONE = -1 };
+
+// Where an operand lives at a given op.
+enum Loc : int32_t { LOC_POOL = 0, LOC_DEVLEAF = 1, LOC_ROOTS = 2 };
+
+struct PhysOp {
+  int32_t kind;                      // OpKind
+  int32_t node;
+  int32_t stream;                    // Stream (S_NONE: bookkeeping only)
+  int64_t bytes = 0;
+  int64_t dev_off = -1;              // pool offset of the tensor this op moves / produces
+  int64_t host_off = -1;             // host-pool offset (evicted intermediates), -1: caller leaf
+  int32_t loc_a = LOC_POOL, loc_b = LOC_POOL;
+  int64_t off_a = -1, off_b = -1;    // operand pool offsets (CONTRACT)
+  std::vector<int32_t> deps;         // ops on other streams that must complete first
+  bool source = false;               // some later op waits on this one (record an event)
+};
+
+struct PhysPlan {
+  std::vector<PhysOp> ops;
+  int64_t pool_high_water = 0, host_pool_bytes = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0;   // bytes physically copied
+};
+// leaf_on_device[u]: the leaf is a caller device buffer (no H2D / no pool space).
+PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>& leaf_on_device,
+                    int64_t pool_bytes, int64_t align);
+
+}  // namespace cc

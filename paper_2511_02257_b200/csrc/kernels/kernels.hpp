@@ -1,0 +1,45 @@
+// Device kernels of the contraction engine (sm_100a).  Host-callable launchers.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cc {
+
+// Batched complex (interleaved complex128) GEMM with a two-level K index:
+//   C[b][m][n] = sum_{ko < Ko} sum_{ki < Kin} A[b][m][ko,ki] * B[b][ko,ki][n]
+//   A(b,m,ko,ki) at A + b*sAb + ko*sAo + m*lda + ki      (complex-element strides)
+//   B(b,ko,ki,n) at B + b*sBb + ko*sBo + ki*ldb + n
+//   C(b,m,n)     at C + b*sCb + m*ldc + n
+// MM1, BM1 and BB2 are all instances.  Runs on FP64 DMMA fed by TMA.
+struct ZgemmProblem {
+  const void* A;
+  const void* B;
+  void* C;
+  int64_t M, Nn, Kin, Ko, batch;
+  int64_t lda, sAo, sAb;
+  int64_t ldb, sBo, sBb;
+  int64_t ldc, sCb;
+};
+
+// Workspace bytes a problem needs for its deterministic split-K partials.
+size_t zgemm_workspace_bytes(const ZgemmProblem& p, int num_sms);
+cudaError_t launch_zgemm(const ZgemmProblem& p, void* workspace, size_t ws_bytes, int num_sms,
+                         cudaStream_t stream, int* n_launches);
+
+// c[t] = sum_{i,j} A[t,i,j] B[t,j,i]; out[t] (complex128) written with a fixed-order
+// reduction.  counters: Lt ints, zero on entry, zero again on exit.  partials: Lt*ceil(N/32)
+// complex128.
+size_t trace_workspace_bytes(int64_t Lt, int64_t N);
+cudaError_t launch_trace(const void* A, const void* B, void* out, int64_t Lt, int64_t N, void* workspace,
+                         cudaStream_t stream);
+
+// corr[c][t] = sum over the terms of correlator c (in input order) of coef * roots[tree][t].
+// term_start: n_corr+1 offsets into (term_tree, term_coef).
+cudaError_t launch_correlate(const void* roots, void* corr, int64_t n_corr, int64_t Lt, const int32_t* term_start,
+                             const int32_t* term_tree, const double* term_coef, cudaStream_t stream);
+
+// Synthetic leaf values (input generation; same recipe as synth/rng.py).
+cudaError_t launch_fill_synthetic(void* dev, int64_t n, uint64_t seed, int64_t leaf_id, int64_t e0, int mode,
+                                  double sigma, cudaStream_t stream);
+
+}  // namespace cc

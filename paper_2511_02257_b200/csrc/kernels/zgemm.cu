@@ -1,0 +1,366 @@
+// Batched complex-double GEMM on FP64 DMMA tensor cores, fed by TMA (sm_100a).
+//
+// Serves the three "exterior contract" kinds (index semantics DESIGN.md
+// reading V-1): MM1 (meson x meson, O(N^3)), BM1 (baryon x meson, single
+// index, O(N^4)) and BB2 (baryon x baryon, double index + spin, O(N^4)) are
+// one batched GEMM with a two-level K index after index fusion (kernels.hpp).
+//
+// Design:
+//  - complex arithmetic as the real embedding: A is read as real [M][2K] (interleaved
+//    complex already is), B is expanded on the fly into 2x2 blocks [[br, bi], [-bi, br]],
+//    C comes out interleaved; one real GEMM, 8 real flops per complex MAC (4M, V-3).
+//  - FP64 tensor cores: mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4 (tcgen05 has no f64 kind).
+//    A warp tile of WM rows x WN complex columns keeps (WM/8)*(WN/4) accumulator pairs.
+//  - K-slot permutation: lane t of an 8x4 fragment holds complex k = 2t+h (h = 0,1) of an
+//    8-complex chunk, re part for the first DMMA and im part for the second, so each lane
+//    does one 16-byte shared load per operand per (chunk, h) and both loads are free of
+//    bank conflicts under the TMA 128-byte swizzle.
+//  - TMA (cp.async.bulk.tensor, SWIZZLE_128B, zero fill out of bounds for ragged tails),
+//    STAGES-deep mbarrier ring, one producer warp, NCW consumer warps.
+//  - deterministic split-K: each split writes a partial tile; a separate kernel sums the
+//    partials in split order (no atomics), so results are bit-identical run to run.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "kernels.hpp"
+
+namespace cc {
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double neg(double x) {
+  return __longlong_as_double(__double_as_longlong(x) ^ static_cast<long long>(0x8000000000000000ULL));
+}
+
+struct KArgs {
+  double2* C;
+  double2* ws;
+  int64_t M, Nn, ldc, sCb;
+  int32_t tiles_m, kt_per_o, kt_total, splits, batch;
+};
+
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int NCW = WARPS_M * WARPS_N;  // consumer (DMMA) warps
+  static constexpr int THREADS = (NCW + 1) * 32;
+  static constexpr int MI = WM / 8, NI = WN / 4;
+  static constexpr int A_BYTES = BM * BK * 16, B_BYTES = BK * BN * 16;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+  static_assert(BK % 8 == 0 && BN % 8 == 0 && BM % 8 == 0, "tile dims");
+  static_assert(WM % 8 == 0 && WN % 4 == 0, "warp tile dims");
+  static_assert((BM * 128) % 1024 == 0 && (BK * 128) % 1024 == 0, "128B swizzle needs 1024B-aligned sub-tiles");
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1)
+    zgemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, KArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x;
+  const int tm = tile % args.tiles_m, tn = tile / args.tiles_m;
+  const int split = blockIdx.y, b = blockIdx.z;
+  const int j0 = int((int64_t(split) * args.kt_total) / args.splits);
+  const int j1 = int((int64_t(split + 1) * args.kt_total) / args.splits);
+  const int m0 = tm * C::BM, n0 = tn * C::BN;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == C::NCW) {
+    // ----------------------------- TMA producer ---------------------------------------
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int j = j0; j < j1; ++j) {
+        const int ko = j / args.kt_per_o;
+        const int ki0 = (j - ko * args.kt_per_o) * C::BK;
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+        uint8_t* sA = smem + stage * C::STAGE_BYTES;
+        uint8_t* sB = sA + C::A_BYTES;
+#pragma unroll
+        for (int kc = 0; kc < C::BK / 8; ++kc)
+          tma_load_4d(sA + kc * C::BM * 128, &tmA, &full[stage], 2 * (ki0 + kc * 8), m0, ko, b);
+#pragma unroll
+        for (int nc = 0; nc < C::BN / 8; ++nc)
+          tma_load_4d(sB + nc * C::BK * 128, &tmB, &full[stage], 2 * (n0 + nc * 8), ki0, ko, b);
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------- DMMA consumers -------------------------------------
+  const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
+  const int g = lane >> 2, t = lane & 3;
+  const bool q = (g & 1) != 0;  // real column parity of this lane's B fragment column
+  double acc[C::MI][C::NI][2];
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int k = 0; k < C::NI; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
+
+  // per-lane shared-memory byte offsets (within a stage) of the fragments
+  int a_row_off[C::MI];
+  int a_key[C::MI];
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i) {
+    const int r = wm * C::WM + i * 8 + g;
+    a_row_off[i] = r * 128;
+    a_key[i] = r & 7;
+  }
+  int b_col_off[C::NI];
+  int b_slot[C::NI];
+#pragma unroll
+  for (int k = 0; k < C::NI; ++k) {
+    const int n = wn * C::WN + k * 4 + (g >> 1);
+    b_col_off[k] = (n >> 3) * C::BK * 128;
+    b_slot[k] = n & 7;
+  }
+
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int j = j0; j < j1; ++j) {
+    mbar_wait(&full[stage], phase);
+    const uint8_t* sA = smem + stage * C::STAGE_BYTES;
+    const uint8_t* sB = sA + C::A_BYTES;
+#pragma unroll
+    for (int kc = 0; kc < C::BK / 8; ++kc) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int s = 2 * t + h;       // complex k slot within the 8-complex chunk
+        const int krow = kc * 8 + s;   // B row within the stage
+        double2 a[C::MI];
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+          a[i] = *reinterpret_cast<const double2*>(sA + kc * C::BM * 128 + a_row_off[i] + ((s ^ a_key[i]) << 4));
+#pragma unroll
+        for (int k = 0; k < C::NI; ++k) {
+          const double2 bv =
+              *reinterpret_cast<const double2*>(sB + b_col_off[k] + krow * 128 + ((b_slot[k] ^ (krow & 7)) << 4));
+          // B' = [[br, bi], [-bi, br]]: row (k, re) -> (br | bi), row (k, im) -> (-bi | br)
+          const double b_re_row = q ? bv.y : bv.x;
+          const double b_im_row = q ? bv.x : neg(bv.y);
+#pragma unroll
+          for (int i = 0; i < C::MI; ++i) {
+            dmma(acc[i][k][0], acc[i][k][1], a[i].x, b_re_row);
+            dmma(acc[i][k][0], acc[i][k][1], a[i].y, b_im_row);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == C::STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+
+  // epilogue: lane (g, t) owns complex C[row g][col t] of each 8x(4 complex) tile
+  double2* out;
+  int64_t ld;
+  if (args.splits > 1) {
+    out = args.ws + (int64_t(split) * args.batch + b) * args.M * args.Nn;
+    ld = args.Nn;
+  } else {
+    out = args.C + int64_t(b) * args.sCb;
+    ld = args.ldc;
+  }
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i) {
+    const int64_t row = m0 + wm * C::WM + i * 8 + g;
+    if (row >= args.M) continue;
+#pragma unroll
+    for (int k = 0; k < C::NI; ++k) {
+      const int64_t col = n0 + wn * C::WN + k * 4 + t;
+      if (col < args.Nn) out[row * ld + col] = make_double2(acc[i][k][0], acc[i][k][1]);
+    }
+  }
+}
+
+// C[b][m][n] = sum_{s < splits} ws[s][b][m][n], in split order (deterministic).
+__global__ void splitk_reduce_kernel(const double2* __restrict__ ws, double2* __restrict__ C, int64_t M, int64_t Nn,
+                                     int64_t ldc, int64_t sCb, int batch, int splits) {
+  const int64_t per_b = M * Nn, total = per_b * batch;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    double re = 0.0, im = 0.0;
+    for (int s = 0; s < splits; ++s) {
+      const double2 v = __ldg(ws + int64_t(s) * total + e);
+      re += v.x;
+      im += v.y;
+    }
+    const int64_t b = e / per_b, r = e - b * per_b;
+    const int64_t m = r / Nn, n = r - m * Nn;
+    C[b * sCb + m * ldc + n] = make_double2(re, im);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint64_t strides_bytes[3],
+              uint32_t box1) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t gd[4] = {dims[0], dims[1], dims[2], dims[3]};
+  cuuint64_t gs[3] = {strides_bytes[0], strides_bytes[1], strides_bytes[2]};
+  cuuint32_t box[4] = {16, box1, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), gd, gs, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+using Big = Cfg<64, 64, 16, 32, 16, 4>;
+
+template <class C>
+int choose_splits(const ZgemmProblem& p, int num_sms, int64_t ctas, int64_t kt_total) {
+  // enough CTAs for a few full waves when the output is too small to fill the GPU; each
+  // split keeps >= 8 k-tiles so the pipeline stays deep
+  if (ctas >= num_sms) return 1;
+  int64_t want = (int64_t(4) * num_sms + ctas - 1) / ctas;
+  int64_t cap = kt_total / 8;
+  int64_t s = want < cap ? want : cap;
+  return s < 1 ? 1 : int(s);
+}
+
+template <class C>
+size_t ws_bytes(const ZgemmProblem& p, int num_sms) {
+  const int64_t tiles = ((p.M + C::BM - 1) / C::BM) * ((p.Nn + C::BN - 1) / C::BN);
+  const int64_t kt_total = p.Ko * ((p.Kin + C::BK - 1) / C::BK);
+  const int splits = choose_splits<C>(p, num_sms, tiles * p.batch, kt_total);
+  return splits > 1 ? size_t(splits) * size_t(p.batch) * size_t(p.M) * size_t(p.Nn) * 16 : 0;
+}
+
+template <class C>
+cudaError_t launch_cfg(const ZgemmProblem& p, void* ws, size_t ws_size, int num_sms, cudaStream_t st, int* nl) {
+  CUtensorMap ta, tb;
+  const uint64_t sAo = p.Ko > 1 ? p.sAo : p.lda * p.M;
+  const uint64_t sBo = p.Ko > 1 ? p.sBo : p.ldb * p.Kin;
+  const uint64_t da[4] = {uint64_t(2 * p.Kin), uint64_t(p.M), uint64_t(p.Ko), uint64_t(p.batch)};
+  const uint64_t sa[3] = {uint64_t(p.lda) * 16, sAo * 16, uint64_t(p.batch > 1 ? p.sAb : sAo * p.Ko) * 16};
+  const uint64_t db[4] = {uint64_t(2 * p.Nn), uint64_t(p.Kin), uint64_t(p.Ko), uint64_t(p.batch)};
+  const uint64_t sb[3] = {uint64_t(p.ldb) * 16, sBo * 16, uint64_t(p.batch > 1 ? p.sBb : sBo * p.Ko) * 16};
+  if (!make_map(&ta, p.A, da, sa, C::BM) || !make_map(&tb, p.B, db, sb, C::BK)) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(zgemm_dmma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles_m = int((p.M + C::BM - 1) / C::BM), tiles_n = int((p.Nn + C::BN - 1) / C::BN);
+  const int kt_per_o = int((p.Kin + C::BK - 1) / C::BK);
+  const int64_t kt_total = p.Ko * kt_per_o;
+  const int64_t ctas = int64_t(tiles_m) * tiles_n * p.batch;
+  int splits = choose_splits<C>(p, num_sms, ctas, kt_total);
+  if (splits > 1 && (ws == nullptr || ws_size < ws_bytes<C>(p, num_sms))) splits = 1;
+  KArgs a;
+  a.C = static_cast<double2*>(p.C);
+  a.ws = static_cast<double2*>(ws);
+  a.M = p.M;
+  a.Nn = p.Nn;
+  a.ldc = p.ldc;
+  a.sCb = p.sCb;
+  a.tiles_m = tiles_m;
+  a.kt_per_o = kt_per_o;
+  a.kt_total = int(kt_total);
+  a.splits = splits;
+  a.batch = int(p.batch);
+  dim3 grid(unsigned(tiles_m * tiles_n), unsigned(splits), unsigned(p.batch));
+  zgemm_dmma_kernel<C><<<grid, C::THREADS, C::SMEM, st>>>(ta, tb, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (nl) ++*nl;
+  if (splits > 1) {
+    const int64_t total = p.batch * p.M * p.Nn;
+    int blocks = int((total + 255) / 256);
+    if (blocks > 8 * num_sms) blocks = 8 * num_sms;
+    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(a.ws, a.C, p.M, p.Nn, p.ldc, p.sCb, int(p.batch), splits);
+    e = cudaGetLastError();
+    if (nl) ++*nl;
+  }
+  return e;
+}
+
+}  // namespace
+
+size_t zgemm_workspace_bytes(const ZgemmProblem& p, int num_sms) { return ws_bytes<Big>(p, num_sms); }
+
+cudaError_t launch_zgemm(const ZgemmProblem& p, void* workspace, size_t ws_size, int num_sms, cudaStream_t stream,
+                         int* n_launches) {
+  if (p.M <= 0 || p.Nn <= 0 || p.Kin <= 0 || p.Ko <= 0 || p.batch <= 0) return cudaErrorInvalidValue;
+  if (p.batch > 65535) return cudaErrorInvalidValue;
+  return launch_cfg<Big>(p, workspace, ws_size, num_sms, stream, n_launches);
+}
+
+}  // namespace cc

@@ -1,0 +1,81 @@
+"""Helpers for the -m gpu parity tests: run a synth Workload through the C ABI."""
+import numpy as np
+
+from oracle import values
+from oracle.dag import Dag
+
+
+def pinned_from(v):
+    import torch
+    h = torch.empty(v.size * 2, dtype=torch.float64, pin_memory=True)
+    h.numpy()[:] = np.ascontiguousarray(v).view(np.float64).ravel()
+    return h
+
+
+def device_from(v):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(v).view(np.float64).ravel().copy()).cuda()
+
+
+def to_numpy_c(t, shape):
+    a = t.detach().cpu().numpy().view(np.complex128)
+    return a.reshape(shape)
+
+
+def run_gpu(w, algo=None, cap=0, flags=0, device_leaves=False, arena_mb=256, leaf_fn=None, ctx=None,
+            part=None):
+    """Returns (ctx, roots{tree: [Lt]}, corr{c: [Lt]}, plan stats, exec stats)."""
+    import torch
+    from paper_2511_02257_b200 import cc
+    dag = Dag(w)
+    if ctx is None:
+        arena = torch.empty(arena_mb << 20, dtype=torch.uint8, device="cuda")
+        ctx = cc.Context(0, arena)
+    ctx.load_workload(w)
+    if part is not None:
+        ctx.partition(*part)
+    order, st = ctx.schedule(cc.CC_TREE if algo is None else algo, cap_bytes=cap)
+    keep = []
+    Lt_part = w.Lt
+    t0 = 0
+    if part is not None and part[2] == cc.PART_TIME:
+        from oracle.partition import time_range
+        t0, t1 = time_range(w.Lt, part[0], part[1])
+        Lt_part = t1 - t0
+    for u, n in dag.nodes.items():
+        if n.child:
+            continue
+        v = leaf_fn(u, n.op) if leaf_fn else values.synthetic_leaf(w, u, n.op)
+        if device_leaves:
+            d = device_from(v[t0:t0 + Lt_part])
+            keep.append(d)
+            ctx.set_leaf_device(u, d)
+        else:
+            h = pinned_from(v)
+            keep.append(h)
+            ctx.set_leaf(u, h)
+    ex = ctx.execute(flags)
+    ctx._leaf_buffers = keep
+    trees = ctx.part_trees()
+    roots = {t: ctx.root_value(t, Lt_part) for t in trees}
+    corr = {}
+    _, n_corr, ids = ctx.correlator_device_ptr()
+    for c in ids:
+        corr[c] = ctx.correlator(c, Lt_part)
+    return ctx, roots, corr, st, ex
+
+
+def assert_roots_close(got, want, rel=1e-10):
+    worst = 0.0
+    for t, w in want.items():
+        g = got[t]
+        err = np.max(np.abs(g - w) / np.maximum(np.abs(w), 1e-300))
+        worst = max(worst, float(err))
+    assert worst <= rel, "worst relative root error %g > %g" % (worst, rel)
+    return worst
+
+
+def assert_corr_close(dag, roots_oracle, got, want, rel=1e-10):
+    scale = values.term_scale(dag, roots_oracle)
+    for c, w in want.items():
+        assert np.all(np.abs(got[c] - w) <= rel * scale[c] + 1e-300), c

@@ -1,0 +1,199 @@
+"""Bit-exact parity of the C++ host library (libcc.so, host-only context) with the oracle.
+
+Integers only (CPU): schedule order (sibling Alg. 1-3, tree Alg. 4-8), tree selection
+order, §II-C memory trace (M_i and transients), LRU plan op queue and counters
+(evictions, transfers, bytes, peaks), partitions, validation error classes.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+from synth import dags
+from oracle.dag import Dag, OracleError
+from oracle import sibling, tree, lru, partition
+from oracle.memory import simulate
+
+cc = pytest.importorskip("paper_2511_02257_b200.cc")
+
+
+def _ctx(w):
+    c = cc.Context(-1)
+    c.load_workload(w)
+    return c
+
+
+def _check(w, caps=(None,)):
+    dag = Dag(w)
+    c = _ctx(w)
+    s_or = sibling.schedule(dag)
+    s_cc, st = c.schedule(cc.CC_SIBLING)
+    assert s_cc == s_or
+    sim = simulate(dag, s_or)
+    m, tr = c.memory_trace()
+    assert m == sim["residency"] and tr == sim["transient"]
+    assert st["model_peak"] == sim["peak"] and st["model_transient_peak"] == sim["transient_peak"]
+    ts = tree.TreeScheduler(dag)
+    t_or = ts.run()
+    t_cc, _ = c.schedule(cc.CC_TREE)
+    assert t_cc == t_or
+    assert c.tree_order() == ts.tree_order
+    for order, algo in ((s_or, cc.CC_SIBLING), (t_or, cc.CC_TREE)):
+        for cap in caps:
+            try:
+                p = lru.plan(dag, order, cap)
+            except lru.InfeasibleError:
+                with pytest.raises(cc.CCError) as ei:
+                    c.schedule(algo, cap_bytes=cap or 0)
+                assert ei.value.code == "INFEASIBLE"
+                continue
+            _, st = c.schedule(algo, cap_bytes=cap or 0)
+            for k in ("evictions", "h2d_count", "d2h_count", "h2d_bytes", "d2h_bytes", "peak",
+                      "transient_peak"):
+                assert st[k] == p[k], (k, cap)
+            assert st["host_peak_bytes"] == p["host_peak_bytes"]
+            ops = [(k, n) for (k, n, _, _) in c.plan_ops()]
+            assert ops == p["ops"]
+        # the GIVEN path replays an arbitrary valid order
+        _, st = c.schedule(cc.CC_GIVEN, given=order)
+        assert st["model_peak"] == simulate(dag, order)["peak"]
+    return dag
+
+
+def test_fixtures_exact():
+    _check(dags.fixture_dstar(), caps=(None, 2, 3, 4, 5))
+    _check(dags.fixture_f1(), caps=(None, 2, 3, 4, 5))
+
+
+def test_random_abstract_dags():
+    for seed in range(250):
+        w = dags.random_dag(seed, n_leaves=3 + seed % 7, n_trees=1 + seed % 9,
+                            max_ops_per_tree=1 + seed % 5, share_p=(seed % 10) / 10, max_size=1 + seed % 6)
+        dag = Dag(w)
+        tp = simulate(dag, sibling.schedule(dag))["transient_peak"]
+        _check(w, caps=(None, tp, max(1, tp - 2), max(1, tp // 2)))
+
+
+def test_random_typed_dags():
+    for seed in range(30):
+        w = dags.random_dag(seed, n_leaves=8, n_trees=15, typed=True, Lt=3, N=5)
+        _check(w, caps=(None, 16 * 3 * 25 * 4, 16 * 3 * 25 * 6))
+
+
+def test_configs_small_scale():
+    mes = 16 * 2 * 8 * 8
+    _check(dags.config_c1(), caps=(None,))
+    _check(dags.config_c2(N=8, Lt=2), caps=(None, 6 * mes, 10 * mes))
+    _check(dags.config_c3(N=4, Lt=2, S=4), caps=(None,))
+    _check(dags.config_c4(N=4, Lt=1, S=4, n_trees=300), caps=(None, 16 * 4 * 64 * 6, 16 * 4 * 64 * 9))
+
+
+@pytest.mark.slow
+def test_configs_full_scale_integers():
+    _check(dags.config_c2(), caps=(None, 1 << 30))
+    _check(dags.config_c4(), caps=(None, 32 * 10 ** 9))
+
+
+def test_dag_stats_match():
+    for w in (dags.fixture_dstar(), dags.config_c2(N=8, Lt=2), dags.config_c4(N=4, Lt=1, S=4, n_trees=100)):
+        s_or = Dag(w).stats()
+        s_cc = _ctx(w).dag_info()
+        for k in ("V", "E", "k", "n_contr", "max_rank"):
+            assert s_cc[k] == s_or[k]
+        assert s_cc["F_v"] == pytest.approx(s_or["F_v"], rel=1e-15)
+        assert s_cc["F_e"] == pytest.approx(s_or["F_e"], rel=1e-15)
+
+
+def _err(w):
+    try:
+        Dag(w)
+        o = None
+    except OracleError as e:
+        o = e.code
+    try:
+        _ctx(w)
+        c = None
+    except cc.CCError as e:
+        c = e.code
+    return o, c
+
+
+def test_validation_error_classes():
+    L, O = dags.LEAF_X, dags.OP_X
+    base = [(0, L, -1, -1, 1), (1, L, -1, -1, 1)]
+    cases = [
+        dags.Workload("cyc", 1, 1, 1, nodes=base + [(2, O, 0, 3, 1), (3, O, 2, 1, 1), (4, O, 3, 0, 1)], trees=[(0, 4)]),
+        dags.Workload("same", 1, 1, 1, nodes=base + [(2, O, 0, 0, 1)], trees=[(0, 2)]),
+        dags.Workload("multi", 1, 1, 1, nodes=base + [(2, O, 0, 1, 1)], trees=[(0, 2), (1, 2)]),
+        dags.Workload("unk", 1, 1, 1, nodes=base + [(2, O, 0, 9, 1)], trees=[(0, 2)]),
+        dags.Workload("dup", 1, 1, 1, nodes=base + [(1, L, -1, -1, 1)], trees=[]),
+        dags.Workload("kind", 2, 2, 2, nodes=[(0, dags.LEAF_M, -1, -1, 0), (1, dags.LEAF_B, -1, -1, 0),
+                                              (2, dags.MM1, 0, 1, 0), (3, dags.TR_MM, 2, 0, 0)], trees=[(0, 3)]),
+        dags.Workload("noroot", 1, 1, 1, nodes=base + [(2, O, 0, 1, 1)], trees=[]),
+        dags.Workload("badterm", 1, 1, 1, nodes=base + [(2, O, 0, 1, 1)], trees=[(0, 2)], terms=[(0, 5, 1.0, 0.0)]),
+    ]
+    for w in cases:
+        o, c = _err(w)
+        assert o is not None and o == c, (w.name, o, c)
+
+
+def test_text_file_load(tmp_path):
+    for w in (dags.fixture_dstar(), dags.config_c2(N=8, Lt=2, n_loop4=40)):
+        p = tmp_path / (w.name + ".txt")
+        p.write_text(w.to_text())
+        c = cc.Context(-1)
+        c.load_dag_file(str(p))
+        assert c.schedule(cc.CC_TREE)[0] == tree.schedule(Dag(w))
+    bad = tmp_path / "bad.txt"
+    bad.write_text("dims 1 1 1\nnode 0 leafX size 1\nnode 1 bogus 0 0\n")
+    with pytest.raises(cc.CCError, match="line 3"):
+        cc.Context(-1).load_dag_file(str(bad))
+
+
+def test_tree_partitions_match_oracle():
+    for w, n in ((dags.config_c2(N=8, Lt=2), 3), (dags.config_c4(N=4, Lt=1, S=4, n_trees=300), 4),
+                 (dags.config_c5(N=8, Lt=2, n_pairs=60, n_trees=400), 8)):
+        dag = Dag(w)
+        parts = partition.tree_parts(dag, n)
+        c = _ctx(w)
+        seen = set()
+        for p in range(n):
+            c.partition(n, p, cc.PART_TREES)
+            mine = c.part_trees()
+            assert mine == sorted(t for t, q in parts.items() if q == p)
+            seen |= set(mine)
+            sub = partition.sub_workload(w, mine)
+            sd = Dag(sub)
+            assert c.schedule(cc.CC_TREE)[0] == tree.schedule(sd)
+        assert seen == set(dag.tree_ids)
+
+
+def test_time_partitions_sizes():
+    w = dags.config_c2(N=8, Lt=6, n_loop4=30)
+    c = _ctx(w)
+    for p in range(4):
+        c.partition(4, p, cc.PART_TIME)
+        t0, t1 = partition.time_range(6, 4, p)
+        wp = dags.Workload(w.name, t1 - t0, w.N, w.S, nodes=w.nodes, trees=w.trees, terms=w.terms)
+        dag = Dag(wp)
+        order, st = c.schedule(cc.CC_TREE)
+        assert order == tree.schedule(dag)
+        assert st["peak"] == simulate(dag, order)["peak"]
+
+
+def test_abi_exports_every_declared_symbol(repo_root):
+    hdr = open(os.path.join(repo_root, "include", "cc.h")).read()
+    declared = set(re.findall(r"^\s*(?:cc_status|void|const char\*|size_t)\s+(cc_\w+)\s*\(", hdr, re.M))
+    out = subprocess.run(["nm", "-D", "--defined-only", cc.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (cc_\w+)$", out, re.M))
+    assert declared and declared <= exported, declared - exported
+    assert set(cc.EXPORTED) == declared
+
+
+def test_device_calls_fail_on_host_only_ctx():
+    c = _ctx(dags.config_c1())
+    c.schedule(cc.CC_TREE)
+    with pytest.raises(cc.CCError) as e:
+        c.execute()
+    assert e.value.code == "STATE"
