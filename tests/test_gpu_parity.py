@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 from synth import dags, rng as srng  # noqa: E402
 from oracle import values, lru, tree, partition  # noqa: E402
 from oracle.dag import Dag  # noqa: E402
-from tests.gpu_helpers import run_gpu, assert_roots_close, assert_corr_close, device_from, to_numpy_c  # noqa: E402
+from gpu_helpers import run_gpu, assert_roots_close, assert_corr_close, device_from, to_numpy_c  # noqa: E402
 
 
 @pytest.fixture(scope="module")
