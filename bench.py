@@ -1,0 +1,382 @@
+"""Benchmark: correlator time-to-solution of the BASELINE.json configs[1] workload.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {cc,reference}] [--config c2]
+Under torchrun (N > 1) every rank runs one TIME part (Lt/N time slices, no replication)
+and the per-slice correlator sums are all-reduced over NCCL (§8(e)); rank 0 prints ONE
+JSON line.  See DESIGN.md §Measurement for every field.
+
+One step = one pass of the hot path over the workload:
+  value: cc_execute (plan replay: every contraction + TR + correlator sums; graph mode) with
+         the leaves already resident in HBM, + the NCCL all-reduce when N > 1;
+  e2e:   the public API from pinned host buffers: cc_load_dag + cc_schedule (tree scheduler
+         + LRU plan) + cc_set_leaf + cc_execute (H2D of every leaf inside) + correlator D2H.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import dags, rng as srng  # noqa: E402
+
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak.json")
+
+
+def workload(name):
+    if name == "c2":
+        return dags.config_c2()
+    if name == "c1":
+        return dags.config_c1()
+    if name == "c3":
+        return dags.config_c3()
+    if name == "c2s":
+        return dags.config_c2(N=64, Lt=16, n_loop4=100, n_loop2=8)
+    raise SystemExit("unknown config " + name)
+
+
+def leaf_sigma(w, op):
+    return srng.meson_sigma(w.N) if op == dags.LEAF_M else srng.baryon_sigma(w.N, w.S)
+
+
+def leaf_shape(w, op):
+    return (w.Lt, w.N, w.N) if op == dags.LEAF_M else (w.Lt, w.S, w.N, w.N, w.N)
+
+
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 6:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------
+def oracle_baseline(w, max_seconds=20.0):
+    """The oracle as it stands (oracle/values.py, numpy complex128) on this host's cores,
+    over a bounded sample of time slices; returns (seconds for the whole workload, sample)."""
+    from oracle import values
+    from oracle.dag import Dag
+    from threadpoolctl import threadpool_info
+    dag = Dag(w)
+    ops = {u: n.op for u, n in dag.nodes.items()}
+    cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    done, t_spent, t = 0, 0.0, 0
+    chunk = max(1, w.Lt // 16)
+    while t < w.Lt and t_spent < max_seconds:
+        t1 = min(w.Lt, t + chunk)
+        leaves = {u: values.synthetic_leaf(w, u, ops[u], (t, t1)) for u in dag.nodes if not dag.nodes[u].child}
+        t0 = time.perf_counter()
+        roots = values.evaluate(dag, lambda u: leaves[u])
+        values.correlators(dag, roots)
+        t_spent += time.perf_counter() - t0
+        done += t1 - t
+        t = t1
+    full = t_spent * w.Lt / done
+    return full, cores, "%d of %d time slices, all %d trees (per-slice independence: x%.2f)" % (
+        done, w.Lt, len(w.trees), w.Lt / done)
+
+
+def run_reference(args, rank):
+    w = workload(args.config)
+    if rank != 0:
+        return
+    steps = []
+    for i in range(args.warmup + args.steps):
+        full, cores, sample = oracle_baseline(w, max_seconds=max(2.0, 60.0 / (args.warmup + args.steps)))
+        if i >= args.warmup:
+            steps.append(full)
+    v = float(np.mean(steps))
+    line = {"impl": "reference", "metric": "correlator time-to-solution", "value": v, "unit": "s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_dict(w, args),
+            "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(w, args):
+    return {"workload": "%s (BASELINE.json configs[1]: pi-pi I=2 correlator set, %d graphs sharing meson "
+                        "nodes, N=%d, Lt=%d)" % (w.name, len(w.trees), w.N, w.Lt),
+            "N": w.N, "Lt": w.Lt, "S": w.S, "trees": len(w.trees), "scheduler": "tree (Alg. 4-8)",
+            "parallelism": "time-slice split x%d + NCCL all-reduce of correlators" % args.gpus if args.gpus > 1
+            else "single GPU",
+            "l2": "flushed (256 MiB write) before every timed step; inputs (512 MiB of leaves) exceed L2",
+            "leaves": "value: device-resident (HBM); e2e: pinned host, H2D inside the step"}
+
+
+# ---------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cc", choices=["cc", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2511_02257_b200 import cc
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = workload(args.config)
+    from oracle.partition import time_range  # pure arithmetic of the split; no oracle compute
+    t0, t1 = time_range(w.Lt, world, rank) if world > 1 else (0, w.Lt)
+    Lt_p = t1 - t0
+
+    streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
+    cs = streams[0]
+    arena = torch.empty(6 << 30, dtype=torch.uint8, device=dev)
+    ctx = cc.Context(local, arena, streams=streams)
+
+    # leaves: device-resident copy of this rank's slices (value) + pinned host full leaves (e2e)
+    leaf_ops = [(n[0], n[1]) for n in w.nodes if n[1] in (dags.LEAF_M, dags.LEAF_B)]
+    dev_leaves, host_leaves = {}, {}
+    for (u, op) in leaf_ops:
+        shape = leaf_shape(w, op)
+        per_t = int(np.prod(shape[1:]))
+        d = torch.empty(2 * Lt_p * per_t, dtype=torch.float64, device=dev)
+        ctx.fill_synthetic(d, Lt_p * per_t, w.data_seed, u, t0 * per_t, w.leaf_mode, leaf_sigma(w, op))
+        dev_leaves[u] = d
+        h = torch.empty(2 * w.Lt * per_t, dtype=torch.float64, pin_memory=True)
+        full = torch.empty(2 * w.Lt * per_t, dtype=torch.float64, device=dev)
+        ctx.fill_synthetic(full, w.Lt * per_t, w.data_seed, u, 0, w.leaf_mode, leaf_sigma(w, op))
+        torch.cuda.synchronize()
+        h.copy_(full)
+        del full
+        host_leaves[u] = h
+    torch.cuda.synchronize()
+
+    # ---- value: plan replay with resident leaves --------------------------------------------------
+    ctx.load_workload(w)
+    if world > 1:
+        ctx.partition(world, rank, cc.PART_TIME)
+    order, pst = ctx.schedule(cc.CC_TREE)
+    for u, d in dev_leaves.items():
+        ctx.set_leaf_device(u, d)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ptr, n_corr, corr_ids = None, None, None
+    corr_full = None
+
+    def step_value():
+        ctx.execute_async(cc.EXEC_GRAPH)
+        if world > 1:
+            with torch.cuda.stream(cs):
+                corr_full.zero_()
+                corr_full[:, t0:t1].copy_(corr_view)
+                dist.all_reduce(corr_full)
+
+    # first execute builds the graph; bind the correlator buffer view for the all-reduce
+    ctx.execute(cc.EXEC_GRAPH)
+    ptr, n_corr, corr_ids = ctx.correlator_device_ptr()
+    corr_view = _device_view(ptr, (n_corr, Lt_p), dev)
+    corr_full = torch.zeros((n_corr, w.Lt), dtype=torch.complex128, device=dev)
+
+    for _ in range(args.warmup):
+        step_value()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(cs):
+                flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+            step_value()
+            e1.record(cs)
+            times.append((e0, e1))
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_s = [a.elapsed_time(b) * 1e-3 for a, b in times]
+    t_value = float(np.sum(step_s))
+    n_kernels_step = None
+
+    # ---- per-kernel times (instrumented replay, flags bit 1: CUDA events around every kernel on
+    # the compute stream) for the roofline of the dominant kernel ---------------------------------
+    ksec, kcnt, inst_s = [0.0] * 8, [0] * 8, 0.0
+    for _ in range(3):
+        ex = ctx.execute(cc.EXEC_TIME_KERNELS)
+        s_, c_ = ctx.kernel_times()
+        ksec = [a + b for a, b in zip(ksec, s_)]
+        kcnt = [a + b for a, b in zip(kcnt, c_)]
+        inst_s += ex["seconds"]
+    n_kernels_step = ex["n_kernels"]
+    mm1_avg = ksec[cc.CC_MM1] / max(kcnt[cc.CC_MM1], 1)
+    tr_avg = ksec[cc.CC_TR_MM] / max(kcnt[cc.CC_TR_MM], 1)
+    Lt_k, N = Lt_p, w.N
+    mm1_flops = 8.0 * Lt_k * N ** 3
+    step_flops = ex["flops"]
+
+    # ---- e2e: the public API from pinned host buffers ------------------------------------------------
+    arena2 = torch.empty(6 << 30, dtype=torch.uint8, device=dev)
+    ctx2 = cc.Context(local, arena2, streams=streams)
+    e2e = []
+    h2d_step = d2h_step = 0
+
+    def step_e2e():
+        ctx2.load_workload(w)
+        if world > 1:
+            ctx2.partition(world, rank, cc.PART_TIME)
+        ctx2.schedule(cc.CC_TREE)
+        for u, h in host_leaves.items():
+            ctx2.set_leaf(u, h)
+        st = ctx2.execute(0)
+        out = [ctx2.correlator(c, Lt_p) for c in corr_ids]
+        return st, out
+
+    for _ in range(max(1, args.warmup)):
+        step_e2e()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(cs)
+        st, out = step_e2e()
+        e1.record(cs)
+        e1.synchronize()
+        e2e.append(e0.elapsed_time(e1) * 1e-3)
+        h2d_step = st["h2d_bytes"]
+        d2h_step = st["d2h_bytes"] + n_corr * Lt_p * 16
+    t_e2e = float(np.sum(e2e))
+
+    # max over ranks
+    if world > 1:
+        tt = torch.tensor([t_value, t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_value, t_e2e = float(tt[0]), float(tt[1])
+
+    if rank == 0:
+        peak, peak_src = fp64_peak()
+        achieved = mm1_flops / mm1_avg / 1e12 if mm1_avg > 0 else None
+        line = {
+            "metric": "correlator time-to-solution", "value": t_value / args.steps, "unit": "s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_value / args.steps * 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(w, args),
+            "e2e": {"value": t_e2e / args.steps, "unit": "s", "h2d_bytes_per_step": int(h2d_step),
+                    "d2h_bytes_per_step": int(d2h_step)},
+            "gpu_launches": int(n_kernels_step * args.steps),
+            "contraction_tflops": step_flops / (t_value / args.steps) / 1e12,
+            "roofline": {"bound": "tensor", "kernel": "zgemm_dmma (MM1, N=%d, Lt=%d)" % (N, Lt_k),
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(),
+                         "peak_source": peak_src, "mm1_avg_us": mm1_avg * 1e6, "tr_avg_us": tr_avg * 1e6,
+                         "mm1_share_of_step": ksec[cc.CC_MM1] / inst_s if inst_s else None,
+                         "how": "CUDA events around every kernel on the compute stream (cc_execute flags bit 1), "
+                                "3 instrumented replays after the timed region"},
+            "plan": {"peak_bytes": pst["peak"], "transient_peak_bytes": pst["transient_peak"],
+                     "evictions": pst["evictions"], "h2d_bytes": pst["h2d_bytes"], "d2h_bytes": pst["d2h_bytes"],
+                     "sched_ms": pst["sched_seconds"] * 1e3, "plan_ms": pst["plan_seconds"] * 1e3},
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu_baseline:
+            full, cores, sample = oracle_baseline(w)
+            line["cpu_baseline"] = {"value": full, "unit": "s", "cores": cores, "kind": "oracle", "sample": sample}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _device_view(ptr, shape, dev):
+    """A torch complex128 view of a device buffer owned by libcc (no copy)."""
+    import torch
+    n = int(np.prod(shape))
+
+    class _Holder:
+        __cuda_array_interface__ = {"shape": (n * 2,), "typestr": "<f8", "data": (ptr, False), "version": 2}
+    t = torch.as_tensor(_Holder(), device=dev)
+    return t.view(torch.complex128).view(*shape)
+
+
+def fp64_peak():
+    try:
+        with open(FP64_PEAK_FILE) as f:
+            d = json.load(f)
+        return d["tflops"], d["source"]
+    except (OSError, KeyError, ValueError):
+        return 37.0, "fallback: DMMA microbenchmark of round 1 (profiles/r01_microbench_fp64_pcie.txt)"
+
+
+def ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("zgemm_traffic_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+if __name__ == "__main__":
+    main()

@@ -92,9 +92,11 @@ struct cc_ctx {
   KindTimes ktimes;
   int64_t last_n_kernels = 0;
 
-  // direct kernel entry points
+  // direct kernel entry points (GEMM split-K partials; trace partials + zeroed counters)
   char* direct_ws = nullptr;
   size_t direct_ws_bytes = 0;
+  char* direct_tr_ws = nullptr;
+  size_t direct_tr_ws_bytes = 0;
 
   ~cc_ctx() { release_device(); }
 
@@ -122,6 +124,8 @@ struct cc_ctx {
       }
     if (direct_ws) cudaFree(direct_ws);
     direct_ws = nullptr;
+    if (direct_tr_ws) cudaFree(direct_tr_ws);
+    direct_tr_ws = nullptr;
     if (own_streams) {
       for (cudaStream_t s : {cs, hs, ds})
         if (s) cudaStreamDestroy(s);
@@ -442,14 +446,14 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   cudaEventDestroy(t_end);
 }
 
-void ensure_direct_ws(cc_ctx* ctx, size_t bytes) {
-  if (bytes <= ctx->direct_ws_bytes) return;
-  if (ctx->direct_ws) ck(cudaFree(ctx->direct_ws), "cudaFree");
-  ctx->direct_ws = nullptr;
-  ctx->direct_ws_bytes = 0;
-  ck(cudaMalloc(reinterpret_cast<void**>(&ctx->direct_ws), bytes), "workspace");
-  ck(cudaMemset(ctx->direct_ws, 0, bytes), "workspace");
-  ctx->direct_ws_bytes = bytes;
+void ensure_ws(char*& ws, size_t& have, size_t bytes) {
+  if (bytes <= have) return;
+  if (ws) ck(cudaFree(ws), "cudaFree");
+  ws = nullptr;
+  have = 0;
+  ck(cudaMalloc(reinterpret_cast<void**>(&ws), bytes), "workspace");
+  ck(cudaMemset(ws, 0, bytes), "workspace");  // trace counters must start at zero
+  have = bytes;
 }
 
 }  // namespace
@@ -818,7 +822,7 @@ static cc_status direct_gemm(cc_ctx* ctx, int op, const void* A, const void* B, 
   ctx->need_device();
   if (!A || !B || !C || Lt <= 0 || N <= 0 || S <= 0) throw Error(CC_E_INVAL, "bad kernel arguments");
   ZgemmProblem p = problem_for(op, Lt, N, S, A, B, C);
-  ensure_direct_ws(ctx, std::max<size_t>(zgemm_workspace_bytes(p, ctx->num_sms), 256));
+  ensure_ws(ctx->direct_ws, ctx->direct_ws_bytes, std::max<size_t>(zgemm_workspace_bytes(p, ctx->num_sms), 256));
   int nl = 0;
   ck(launch_zgemm(p, ctx->direct_ws, ctx->direct_ws_bytes, ctx->num_sms, ctx->cs, &nl), "contraction kernel");
   API_END
@@ -841,8 +845,10 @@ cc_status cc_tr_mm(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t L
   API_BEGIN
   ctx->need_device();
   if (!A || !B || !c || Lt <= 0 || N <= 0) throw Error(CC_E_INVAL, "bad kernel arguments");
-  ensure_direct_ws(ctx, trace_workspace_bytes(Lt, N));
-  ck(launch_trace(A, B, c, Lt, N, ctx->direct_ws, ctx->cs), "TR_MM kernel");
+  ensure_ws(ctx->direct_tr_ws, ctx->direct_tr_ws_bytes, trace_workspace_bytes(Lt, N));
+  // counters must be zero; a previous direct call with another Lt may have left partials there
+  ck(cudaMemsetAsync(ctx->direct_tr_ws, 0, size_t(Lt) * 4, ctx->cs), "memset");
+  ck(launch_trace(A, B, c, Lt, N, ctx->direct_tr_ws, ctx->cs), "TR_MM kernel");
   API_END
 }
 

@@ -1,19 +1,21 @@
 // "Contract all" for tree roots and the correlator sums.
 //
-// TR_MM: c[t] = sum_{i,j} A[t,i,j] * B[t,j,i]  (reading V-1).  HBM/L2-bound (0.25 flop/B):
-// CTA (t, i-block of 32 rows) streams A[t, i-block, :] and B[t, :, i-block] in 32x32
-// complex sub-tiles with coalesced 512-byte row segments, transposes the B sub-tile
-// through padded shared memory (conflict-free), and accumulates per thread.  The CTA
-// partial is reduced in a fixed order (warp shuffle tree, then warps in order); the last
-// CTA of a time slice (ticket counter) sums the partials in block order.  No floating-point
-// atomics: the result is bit-identical from run to run.
+// TR_MM: c[t] = sum_{i,j} A[t,i,j] * B[t,j,i]  (reading V-1).  HBM/L2-bound (0.25 flop/B).
+// Work unit = (t, I, J): the 32x32 complex block A[t, I, J] and its transpose partner
+// B[t, J, I] (16 KB each, coalesced 512-byte row segments).  One CTA per unit, so every
+// thread issues its 8 independent 16-byte loads up front and the whole GPU keeps
+// megabytes in flight; B's block is transposed through padded shared memory
+// (conflict-free).  The unit partial is reduced in a fixed order (warp shuffle tree, then
+// warps in order) into partials[t][unit]; the last CTA of a time slice (ticket counter)
+// sums the partials in unit order.  No floating-point atomics: the result is bit-identical
+// from run to run.
 #include "kernels.hpp"
 
 namespace cc {
 namespace {
 
-constexpr int TB = 32;          // sub-tile edge (complex elements)
-constexpr int TR_THREADS = 256; // 8 warps; warp w owns rows w, w+8, w+16, w+24 of a sub-tile
+constexpr int TB = 32;          // block edge (complex elements)
+constexpr int TR_THREADS = 256; // 8 warps; warp w owns rows w, w+8, w+16, w+24 of a block
 
 __device__ __forceinline__ double2 cmul_acc(double2 acc, double2 a, double2 b) {
   acc.x = fma(a.x, b.x, acc.x);
@@ -25,34 +27,32 @@ __device__ __forceinline__ double2 cmul_acc(double2 acc, double2 a, double2 b) {
 
 __global__ void __launch_bounds__(TR_THREADS)
     trace_kernel(const double2* __restrict__ A, const double2* __restrict__ B, double2* __restrict__ out, int64_t N,
-                 int nblk, double2* __restrict__ partials, int* __restrict__ counters) {
+                 int nb, double2* __restrict__ partials, int* __restrict__ counters) {
   __shared__ double2 sB[TB][TB + 1];
   __shared__ double2 red[TR_THREADS / 32];
   __shared__ int is_last;
-  const int t = blockIdx.y, blk = blockIdx.x;
+  const int t = blockIdx.y;
+  const int unit = blockIdx.x;            // unit = I * nb + J
+  const int I = unit / nb, J = unit - I * nb;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t i0 = int64_t(blk) * TB;
+  const int64_t i0 = int64_t(I) * TB, j0 = int64_t(J) * TB;
   const double2* At = A + int64_t(t) * N * N;
   const double2* Bt = B + int64_t(t) * N * N;
-  double2 acc = make_double2(0.0, 0.0);
-  for (int64_t j0 = 0; j0 < N; j0 += TB) {
-    // B sub-tile rows j0..j0+31, columns i0..i0+31 (coalesced along i)
+  double2 a[TB / 8], b[TB / 8];
 #pragma unroll
-    for (int rr = 0; rr < TB / 8; ++rr) {
-      const int r = warp + rr * 8;
-      const int64_t j = j0 + r, i = i0 + lane;
-      sB[r][lane] = (j < N && i < N) ? __ldg(Bt + j * N + i) : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-    // A sub-tile rows i0..i0+31 (this warp: rows warp + 8 rr), columns j0 + lane
-#pragma unroll
-    for (int rr = 0; rr < TB / 8; ++rr) {
-      const int r = warp + rr * 8;
-      const int64_t i = i0 + r, j = j0 + lane;
-      if (i < N && j < N) acc = cmul_acc(acc, __ldg(At + i * N + j), sB[lane][r]);  // B[j][i]
-    }
-    __syncthreads();
+  for (int rr = 0; rr < TB / 8; ++rr) {
+    const int r = warp + rr * 8;
+    const int64_t ia = i0 + r, ja = j0 + lane;   // A[t, I0 + r, J0 + lane]
+    const int64_t jb = j0 + r, ib = i0 + lane;   // B[t, J0 + r, I0 + lane]
+    a[rr] = (ia < N && ja < N) ? __ldg(At + ia * N + ja) : make_double2(0.0, 0.0);
+    b[rr] = (jb < N && ib < N) ? __ldg(Bt + jb * N + ib) : make_double2(0.0, 0.0);
   }
+#pragma unroll
+  for (int rr = 0; rr < TB / 8; ++rr) sB[warp + rr * 8][lane] = b[rr];
+  __syncthreads();
+  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int rr = 0; rr < TB / 8; ++rr) acc = cmul_acc(acc, a[rr], sB[lane][warp + rr * 8]);  // B[J0+lane][I0+r]
   // fixed-order CTA reduction
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
@@ -61,33 +61,45 @@ __global__ void __launch_bounds__(TR_THREADS)
   }
   if (lane == 0) red[warp] = acc;
   __syncthreads();
+  const int nunits = nb * nb;
   if (threadIdx.x == 0) {
     double2 s = red[0];
     for (int w = 1; w < TR_THREADS / 32; ++w) {
       s.x += red[w].x;
       s.y += red[w].y;
     }
-    if (nblk == 1) {
+    if (nunits == 1) {
       out[t] = s;
       is_last = 0;
     } else {
-      partials[int64_t(t) * nblk + blk] = s;
+      partials[int64_t(t) * nunits + unit] = s;
       __threadfence();
       const int ticket = atomicAdd(&counters[t], 1);
-      is_last = (ticket == nblk - 1);
+      is_last = (ticket == nunits - 1);
     }
   }
   __syncthreads();
-  if (is_last && threadIdx.x == 0) {
+  if (is_last) {
+    // last CTA of slice t: fixed-order sum of the unit partials (warp 0: lane-strided
+    // partial sums, then a shuffle tree; the order depends only on nunits)
     __threadfence();
-    double2 s = make_double2(0.0, 0.0);
-    const volatile double* pp = reinterpret_cast<const volatile double*>(partials + int64_t(t) * nblk);
-    for (int k = 0; k < nblk; ++k) {
-      s.x += pp[2 * k];
-      s.y += pp[2 * k + 1];
+    if (warp == 0) {
+      const volatile double* pp = reinterpret_cast<const volatile double*>(partials + int64_t(t) * nunits);
+      double sx = 0.0, sy = 0.0;
+      for (int k = lane; k < nunits; k += 32) {
+        sx += pp[2 * k];
+        sy += pp[2 * k + 1];
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      }
+      if (lane == 0) {
+        out[t] = make_double2(sx, sy);
+        counters[t] = 0;  // ready for the next launch
+      }
     }
-    out[t] = s;
-    counters[t] = 0;  // ready for the next launch
   }
 }
 
@@ -139,19 +151,20 @@ __global__ void fill_synthetic_kernel(double2* out, int64_t n, uint64_t key, int
 }  // namespace
 
 size_t trace_workspace_bytes(int64_t Lt, int64_t N) {
-  const int64_t nblk = (N + TB - 1) / TB;
-  return size_t(Lt * nblk) * 16 + size_t(Lt) * sizeof(int) + 256;
+  const int64_t nb = (N + TB - 1) / TB;
+  return size_t(Lt * nb * nb) * 16 + size_t(Lt) * sizeof(int) + 256;
 }
 
 cudaError_t launch_trace(const void* A, const void* B, void* out, int64_t Lt, int64_t N, void* workspace,
                          cudaStream_t stream) {
   if (Lt <= 0 || N <= 0 || Lt > 65535) return cudaErrorInvalidValue;
-  const int nblk = int((N + TB - 1) / TB);
-  double2* partials = static_cast<double2*>(workspace);
-  int* counters = reinterpret_cast<int*>(static_cast<char*>(workspace) + size_t(Lt * nblk) * 16);
-  dim3 grid{unsigned(nblk), unsigned(Lt), 1u};
+  const int nb = int((N + TB - 1) / TB);
+  // layout: counters (Lt ints, left at zero by every launch) then the unit partials
+  int* counters = static_cast<int*>(workspace);
+  double2* partials = reinterpret_cast<double2*>(static_cast<char*>(workspace) + ((size_t(Lt) * 4 + 255) / 256) * 256);
+  dim3 grid{unsigned(nb * nb), unsigned(Lt), 1u};
   trace_kernel<<<grid, TR_THREADS, 0, stream>>>(static_cast<const double2*>(A), static_cast<const double2*>(B),
-                                               static_cast<double2*>(out), N, nblk, partials, counters);
+                                               static_cast<double2*>(out), N, nb, partials, counters);
   return cudaGetLastError();
 }
 
