@@ -275,6 +275,7 @@ void prepare_phys(cc_ctx* ctx) {
   ck(cudaMemcpy(ctx->term_tree, tree.data(), tree.size() * 4, cudaMemcpyHostToDevice), "term tables");
   ck(cudaMemcpy(ctx->term_coef, coef.data(), coef.size() * 8, cudaMemcpyHostToDevice), "term tables");
   ck(cudaMemset(ctx->trace_ws, 0, trace_ws), "trace counters");
+  if (sz_gemm > 0) ck(cudaMemset(ctx->gemm_ws, 0, size_t(sz_gemm)), "gemm flags");
   ck(cudaMemset(ctx->roots, 0, size_t(sz_roots)), "roots");
   // physical plan over the pool
   std::vector<uint8_t> on_dev(g.nodes.size(), 0);

@@ -2,13 +2,14 @@
 //
 // TR_MM: c[t] = sum_{i,j} A[t,i,j] * B[t,j,i]  (reading V-1).  HBM/L2-bound (0.25 flop/B).
 // Work unit = (t, I, J): the 32x32 complex block A[t, I, J] and its transpose partner
-// B[t, J, I] (16 KB each, coalesced 512-byte row segments).  One CTA per unit, so every
-// thread issues its 8 independent 16-byte loads up front and the whole GPU keeps
-// megabytes in flight; B's block is transposed through padded shared memory
-// (conflict-free).  The unit partial is reduced in a fixed order (warp shuffle tree, then
-// warps in order) into partials[t][unit]; the last CTA of a time slice (ticket counter)
-// sums the partials in unit order.  No floating-point atomics: the result is bit-identical
-// from run to run.
+// B[t, J, I] (16 KB each, coalesced 512-byte row segments).  Slice t is split into P
+// pieces of consecutive units (P chosen so Lt*P ~ 2 CTAs per SM); CTA (t, p) walks its
+// units with the next unit's eight 16-byte loads per thread issued before the current
+// unit is consumed (software prefetch keeps ~8 KB per warp in flight), transposes B's block
+// through padded shared memory (conflict-free) and accumulates per thread.  The CTA partial
+// is reduced in a fixed order (shuffle tree, then warps in order) into partials[t][p]; the
+// last CTA of slice t (ticket counter) sums the P partials in order.  No floating-point
+// atomics: the result is bit-identical from run to run.
 #include "kernels.hpp"
 
 namespace cc {
@@ -16,6 +17,7 @@ namespace {
 
 constexpr int TB = 32;          // block edge (complex elements)
 constexpr int TR_THREADS = 256; // 8 warps; warp w owns rows w, w+8, w+16, w+24 of a block
+constexpr int RPW = TB / 8;     // rows per warp
 
 __device__ __forceinline__ double2 cmul_acc(double2 acc, double2 a, double2 b) {
   acc.x = fma(a.x, b.x, acc.x);
@@ -25,34 +27,50 @@ __device__ __forceinline__ double2 cmul_acc(double2 acc, double2 a, double2 b) {
   return acc;
 }
 
-__global__ void __launch_bounds__(TR_THREADS)
-    trace_kernel(const double2* __restrict__ A, const double2* __restrict__ B, double2* __restrict__ out, int64_t N,
-                 int nb, double2* __restrict__ partials, int* __restrict__ counters) {
-  __shared__ double2 sB[TB][TB + 1];
-  __shared__ double2 red[TR_THREADS / 32];
-  __shared__ int is_last;
-  const int t = blockIdx.y;
-  const int unit = blockIdx.x;            // unit = I * nb + J
+__device__ __forceinline__ void load_unit(const double2* __restrict__ At, const double2* __restrict__ Bt, int64_t N,
+                                          int nb, int unit, int warp, int lane, double2 (&a)[RPW],
+                                          double2 (&b)[RPW]) {
   const int I = unit / nb, J = unit - I * nb;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i0 = int64_t(I) * TB, j0 = int64_t(J) * TB;
-  const double2* At = A + int64_t(t) * N * N;
-  const double2* Bt = B + int64_t(t) * N * N;
-  double2 a[TB / 8], b[TB / 8];
 #pragma unroll
-  for (int rr = 0; rr < TB / 8; ++rr) {
+  for (int rr = 0; rr < RPW; ++rr) {
     const int r = warp + rr * 8;
     const int64_t ia = i0 + r, ja = j0 + lane;   // A[t, I0 + r, J0 + lane]
     const int64_t jb = j0 + r, ib = i0 + lane;   // B[t, J0 + r, I0 + lane]
     a[rr] = (ia < N && ja < N) ? __ldg(At + ia * N + ja) : make_double2(0.0, 0.0);
     b[rr] = (jb < N && ib < N) ? __ldg(Bt + jb * N + ib) : make_double2(0.0, 0.0);
   }
-#pragma unroll
-  for (int rr = 0; rr < TB / 8; ++rr) sB[warp + rr * 8][lane] = b[rr];
-  __syncthreads();
+}
+
+__global__ void __launch_bounds__(TR_THREADS, 2)
+    trace_kernel(const double2* __restrict__ A, const double2* __restrict__ B, double2* __restrict__ out, int64_t N,
+                 int nb, int P, double2* __restrict__ partials, int* __restrict__ counters) {
+  __shared__ double2 sB[TB][TB + 1];
+  __shared__ double2 red[TR_THREADS / 32];
+  __shared__ int is_last;
+  const int t = blockIdx.y, p = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int U = nb * nb;
+  const int u0 = int((int64_t(p) * U) / P), u1 = int((int64_t(p + 1) * U) / P);
+  const double2* At = A + int64_t(t) * N * N;
+  const double2* Bt = B + int64_t(t) * N * N;
   double2 acc = make_double2(0.0, 0.0);
+  double2 a[RPW], b[RPW], an[RPW], bn[RPW];
+  if (u0 < u1) load_unit(At, Bt, N, nb, u0, warp, lane, a, b);
+  for (int u = u0; u < u1; ++u) {
+    if (u + 1 < u1) load_unit(At, Bt, N, nb, u + 1, warp, lane, an, bn);
 #pragma unroll
-  for (int rr = 0; rr < TB / 8; ++rr) acc = cmul_acc(acc, a[rr], sB[lane][warp + rr * 8]);  // B[J0+lane][I0+r]
+    for (int rr = 0; rr < RPW; ++rr) sB[warp + rr * 8][lane] = b[rr];
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) acc = cmul_acc(acc, a[rr], sB[lane][warp + rr * 8]);  // B[J0+lane][I0+r]
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+      a[rr] = an[rr];
+      b[rr] = bn[rr];
+    }
+  }
   // fixed-order CTA reduction
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
@@ -61,32 +79,31 @@ __global__ void __launch_bounds__(TR_THREADS)
   }
   if (lane == 0) red[warp] = acc;
   __syncthreads();
-  const int nunits = nb * nb;
   if (threadIdx.x == 0) {
     double2 s = red[0];
     for (int w = 1; w < TR_THREADS / 32; ++w) {
       s.x += red[w].x;
       s.y += red[w].y;
     }
-    if (nunits == 1) {
+    if (P == 1) {
       out[t] = s;
       is_last = 0;
     } else {
-      partials[int64_t(t) * nunits + unit] = s;
+      partials[int64_t(t) * P + p] = s;
       __threadfence();
       const int ticket = atomicAdd(&counters[t], 1);
-      is_last = (ticket == nunits - 1);
+      is_last = (ticket == P - 1);
     }
   }
   __syncthreads();
   if (is_last) {
-    // last CTA of slice t: fixed-order sum of the unit partials (warp 0: lane-strided
-    // partial sums, then a shuffle tree; the order depends only on nunits)
+    // last CTA of slice t: fixed-order sum of the P partials (lane-strided partial sums,
+    // then a shuffle tree; the order depends only on P)
     __threadfence();
     if (warp == 0) {
-      const volatile double* pp = reinterpret_cast<const volatile double*>(partials + int64_t(t) * nunits);
+      const volatile double* pp = reinterpret_cast<const volatile double*>(partials + int64_t(t) * P);
       double sx = 0.0, sy = 0.0;
-      for (int k = lane; k < nunits; k += 32) {
+      for (int k = lane; k < P; k += 32) {
         sx += pp[2 * k];
         sy += pp[2 * k + 1];
       }
@@ -103,24 +120,48 @@ __global__ void __launch_bounds__(TR_THREADS)
   }
 }
 
-// corr[c][t] = sum over terms of c (input order) of coef * roots[tree][t]
+int trace_pieces(int64_t Lt, int64_t N) {
+  const int64_t nb = (N + TB - 1) / TB, U = nb * nb;
+  int64_t P = (2 * 148) / Lt;   // all CTAs resident at 2 per SM
+  if (P > U) P = U;
+  if (P < 1) P = 1;
+  return int(P);
+}
+
+// corr[c][t] = sum over terms of c (input order) of coef * roots[tree][t].  One CTA per
+// correlator; its term list is staged through shared memory in chunks and the threads run
+// over t, so root loads are coalesced across t.
+constexpr int CORR_CHUNK = 256;
+
 __global__ void correlate_kernel(const double2* __restrict__ roots, double2* __restrict__ corr, int64_t n_corr,
                                  int64_t Lt, const int32_t* __restrict__ term_start,
                                  const int32_t* __restrict__ term_tree, const double* __restrict__ term_coef) {
-  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (e >= n_corr * Lt) return;
-  const int64_t c = e / Lt, t = e - c * Lt;
-  double re = 0.0, im = 0.0;
-  for (int k = term_start[c]; k < term_start[c + 1]; ++k) {
-    const double2 r = roots[int64_t(term_tree[k]) * Lt + t];
-    const double cr = term_coef[2 * k], ci = term_coef[2 * k + 1];
-    // (cr + i ci)(r.x + i r.y), each term rounded as the oracle does: coef * root, then add
-    const double pr = cr * r.x - ci * r.y;
-    const double pi = cr * r.y + ci * r.x;
-    re += pr;
-    im += pi;
+  __shared__ int32_t s_tree[CORR_CHUNK];
+  __shared__ double2 s_coef[CORR_CHUNK];
+  const int64_t c = blockIdx.x;
+  const int k0 = term_start[c], k1 = term_start[c + 1];
+  for (int64_t tb = 0; tb < Lt; tb += blockDim.x) {
+    const int64_t t = tb + threadIdx.x;
+    double re = 0.0, im = 0.0;
+    for (int kc = k0; kc < k1; kc += CORR_CHUNK) {
+      const int n = (k1 - kc) < CORR_CHUNK ? (k1 - kc) : CORR_CHUNK;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        s_tree[i] = term_tree[kc + i];
+        s_coef[i] = make_double2(term_coef[2 * (kc + i)], term_coef[2 * (kc + i) + 1]);
+      }
+      __syncthreads();
+      if (t < Lt) {
+        for (int i = 0; i < n; ++i) {
+          const double2 r = roots[int64_t(s_tree[i]) * Lt + t];
+          const double2 cf = s_coef[i];
+          re += cf.x * r.x - cf.y * r.y;
+          im += cf.x * r.y + cf.y * r.x;
+        }
+      }
+    }
+    if (t < Lt) corr[c * Lt + t] = make_double2(re, im);
   }
-  corr[e] = make_double2(re, im);
 }
 
 // ---- synthetic inputs (input generation only; recipe of synth/rng.py) ------------------
@@ -151,29 +192,28 @@ __global__ void fill_synthetic_kernel(double2* out, int64_t n, uint64_t key, int
 }  // namespace
 
 size_t trace_workspace_bytes(int64_t Lt, int64_t N) {
-  const int64_t nb = (N + TB - 1) / TB;
-  return size_t(Lt * nb * nb) * 16 + size_t(Lt) * sizeof(int) + 256;
+  return size_t(Lt * trace_pieces(Lt, N)) * 16 + ((size_t(Lt) * 4 + 255) / 256) * 256;
 }
 
 cudaError_t launch_trace(const void* A, const void* B, void* out, int64_t Lt, int64_t N, void* workspace,
                          cudaStream_t stream) {
   if (Lt <= 0 || N <= 0 || Lt > 65535) return cudaErrorInvalidValue;
   const int nb = int((N + TB - 1) / TB);
+  const int P = trace_pieces(Lt, N);
   // layout: counters (Lt ints, left at zero by every launch) then the unit partials
   int* counters = static_cast<int*>(workspace);
   double2* partials = reinterpret_cast<double2*>(static_cast<char*>(workspace) + ((size_t(Lt) * 4 + 255) / 256) * 256);
-  dim3 grid{unsigned(nb * nb), unsigned(Lt), 1u};
+  dim3 grid{unsigned(P), unsigned(Lt), 1u};
   trace_kernel<<<grid, TR_THREADS, 0, stream>>>(static_cast<const double2*>(A), static_cast<const double2*>(B),
-                                               static_cast<double2*>(out), N, nb, partials, counters);
+                                               static_cast<double2*>(out), N, nb, P, partials, counters);
   return cudaGetLastError();
 }
 
 cudaError_t launch_correlate(const void* roots, void* corr, int64_t n_corr, int64_t Lt, const int32_t* term_start,
                              const int32_t* term_tree, const double* term_coef, cudaStream_t stream) {
-  const int64_t total = n_corr * Lt;
-  if (total <= 0) return cudaSuccess;
-  const int blocks = int((total + 255) / 256);
-  correlate_kernel<<<blocks, 256, 0, stream>>>(static_cast<const double2*>(roots), static_cast<double2*>(corr), n_corr,
+  if (n_corr <= 0 || Lt <= 0) return cudaSuccess;
+  const int threads = Lt >= 256 ? 256 : int((Lt + 31) / 32 * 32);
+  correlate_kernel<<<unsigned(n_corr), threads, 0, stream>>>(static_cast<const double2*>(roots), static_cast<double2*>(corr), n_corr,
                                                Lt, term_start, term_tree, term_coef);
   return cudaGetLastError();
 }

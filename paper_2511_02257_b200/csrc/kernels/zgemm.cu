@@ -17,8 +17,14 @@
 //    bank conflicts under the TMA 128-byte swizzle.
 //  - TMA (cp.async.bulk.tensor, SWIZZLE_128B, zero fill out of bounds for ragged tails),
 //    STAGES-deep mbarrier ring, one producer warp, NCW consumer warps.
-//  - deterministic split-K: each split writes a partial tile; a separate kernel sums the
-//    partials in split order (no atomics), so results are bit-identical run to run.
+//  - persistent stream-K: grid = #SMs, CTA c owns the contiguous k-iteration range
+//    [c*T/G, (c+1)*T/G) of the flattened (tile, k-tile) space, so every SM gets the same
+//    number of DMMA k-iterations (no wave quantisation) and the TMA ring streams across tile
+//    boundaries.  A tile split between CTAs is finished by the CTA holding its last
+//    k-iteration ("owner"), which adds the partials of the earlier CTAs in a fixed order
+//    (c-1, c-2, ...), read from an L2 workspace after a per-warp release/acquire flag; every
+//    CTA first computes the head of its last, shared tile so owners never wait long.
+//    No floating-point atomics: results are bit-identical run to run.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -72,9 +78,11 @@ __device__ __forceinline__ double neg(double x) {
 
 struct KArgs {
   double2* C;
-  double2* ws;
+  double* ws;           // G slots x NCW warps x (MI*NI*2) x 32 lanes doubles
+  int* flags;           // G x NCW; zero on entry and on exit
   int64_t M, Nn, ldc, sCb;
-  int32_t tiles_m, kt_per_o, kt_total, splits, batch;
+  int64_t total;        // n_tiles * KT
+  int32_t tiles_m, tiles_n, kt_per_o, KT, G;
 };
 
 template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
@@ -84,13 +92,46 @@ struct Cfg {
   static constexpr int NCW = WARPS_M * WARPS_N;  // consumer (DMMA) warps
   static constexpr int THREADS = (NCW + 1) * 32;
   static constexpr int MI = WM / 8, NI = WN / 4;
+  static constexpr int FRAG = MI * NI * 2;       // accumulator doubles per lane
   static constexpr int A_BYTES = BM * BK * 16, B_BYTES = BK * BN * 16;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+  static constexpr int SLOT_DOUBLES = NCW * FRAG * 32;
   static_assert(BK % 8 == 0 && BN % 8 == 0 && BM % 8 == 0, "tile dims");
   static_assert(WM % 8 == 0 && WN % 4 == 0, "warp tile dims");
   static_assert((BM * 128) % 1024 == 0 && (BK * 128) % 1024 == 0, "128B swizzle needs 1024B-aligned sub-tiles");
 };
+
+// The k-iteration range of CTA c and its segments (one per tile touched), in processing
+// order: the head of a shared last tile first, then the tiles in ascending order.
+struct Range {
+  int64_t s, e;
+  int64_t first_tile, last_tile;
+  bool reorder;
+  __device__ Range(const KArgs& a, int c) {
+    s = (int64_t(c) * a.total) / a.G;
+    e = (int64_t(c + 1) * a.total) / a.G;
+    first_tile = s / a.KT;
+    last_tile = (e - 1) / a.KT;
+    reorder = (last_tile > first_tile) && (e - last_tile * a.KT < a.KT);
+  }
+  __device__ int64_t count() const { return e > s ? last_tile - first_tile + 1 : 0; }
+  __device__ int64_t tile(int64_t j) const {
+    if (!reorder) return first_tile + j;
+    return j == 0 ? last_tile : first_tile + j - 1;
+  }
+};
+
+__device__ __forceinline__ int64_t range_start(int64_t c, const KArgs& a) { return (c * a.total) / a.G; }
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, 1)
@@ -101,12 +142,10 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   uint64_t* empty = full + C::STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x;
-  const int tm = tile % args.tiles_m, tn = tile / args.tiles_m;
-  const int split = blockIdx.y, b = blockIdx.z;
-  const int j0 = int((int64_t(split) * args.kt_total) / args.splits);
-  const int j1 = int((int64_t(split + 1) * args.kt_total) / args.splits);
-  const int m0 = tm * C::BM, n0 = tn * C::BN;
+  const int cta = blockIdx.x;
+  const Range rg(args, cta);
+  const int64_t n_seg = rg.count();
+  const int64_t tiles_mn = int64_t(args.tiles_m) * args.tiles_n;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -124,22 +163,31 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
       int stage = 0;
       uint32_t phase = 0;
-      for (int j = j0; j < j1; ++j) {
-        const int ko = j / args.kt_per_o;
-        const int ki0 = (j - ko * args.kt_per_o) * C::BK;
-        mbar_wait(&empty[stage], phase ^ 1);
-        mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-        uint8_t* sA = smem + stage * C::STAGE_BYTES;
-        uint8_t* sB = sA + C::A_BYTES;
+      for (int64_t j = 0; j < n_seg; ++j) {
+        const int64_t tile = rg.tile(j);
+        const int64_t b = tile / tiles_mn;
+        const int64_t r = tile - b * tiles_mn;
+        const int tn = int(r / args.tiles_m), tm = int(r - int64_t(tn) * args.tiles_m);
+        const int64_t base = tile * args.KT;
+        const int k0 = int((rg.s > base ? rg.s : base) - base);
+        const int k1 = int((rg.e < base + args.KT ? rg.e : base + args.KT) - base);
+        for (int k = k0; k < k1; ++k) {
+          const int ko = k / args.kt_per_o;
+          const int ki0 = (k - ko * args.kt_per_o) * C::BK;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          uint8_t* sA = smem + stage * C::STAGE_BYTES;
+          uint8_t* sB = sA + C::A_BYTES;
 #pragma unroll
-        for (int kc = 0; kc < C::BK / 8; ++kc)
-          tma_load_4d(sA + kc * C::BM * 128, &tmA, &full[stage], 2 * (ki0 + kc * 8), m0, ko, b);
+          for (int kc = 0; kc < C::BK / 8; ++kc)
+            tma_load_4d(sA + kc * C::BM * 128, &tmA, &full[stage], 2 * (ki0 + kc * 8), tm * C::BM, ko, int(b));
 #pragma unroll
-        for (int nc = 0; nc < C::BN / 8; ++nc)
-          tma_load_4d(sB + nc * C::BK * 128, &tmB, &full[stage], 2 * (n0 + nc * 8), ki0, ko, b);
-        if (++stage == C::STAGES) {
-          stage = 0;
-          phase ^= 1;
+          for (int nc = 0; nc < C::BN / 8; ++nc)
+            tma_load_4d(sB + nc * C::BK * 128, &tmB, &full[stage], 2 * (tn * C::BN + nc * 8), ki0, ko, int(b));
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -150,23 +198,14 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
   const int g = lane >> 2, t = lane & 3;
   const bool q = (g & 1) != 0;  // real column parity of this lane's B fragment column
-  double acc[C::MI][C::NI][2];
-#pragma unroll
-  for (int i = 0; i < C::MI; ++i)
-#pragma unroll
-    for (int k = 0; k < C::NI; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
-
-  // per-lane shared-memory byte offsets (within a stage) of the fragments
-  int a_row_off[C::MI];
-  int a_key[C::MI];
+  int a_row_off[C::MI], a_key[C::MI];
 #pragma unroll
   for (int i = 0; i < C::MI; ++i) {
     const int r = wm * C::WM + i * 8 + g;
     a_row_off[i] = r * 128;
     a_key[i] = r & 7;
   }
-  int b_col_off[C::NI];
-  int b_slot[C::NI];
+  int b_col_off[C::NI], b_slot[C::NI];
 #pragma unroll
   for (int k = 0; k < C::NI; ++k) {
     const int n = wn * C::WN + k * 4 + (g >> 1);
@@ -176,79 +215,106 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 
   int stage = 0;
   uint32_t phase = 0;
-  for (int j = j0; j < j1; ++j) {
-    mbar_wait(&full[stage], phase);
-    const uint8_t* sA = smem + stage * C::STAGE_BYTES;
-    const uint8_t* sB = sA + C::A_BYTES;
+  for (int64_t j = 0; j < n_seg; ++j) {
+    const int64_t tile = rg.tile(j);
+    const int64_t base = tile * args.KT;
+    const int k0 = int((rg.s > base ? rg.s : base) - base);
+    const int k1 = int((rg.e < base + args.KT ? rg.e : base + args.KT) - base);
+    double acc[C::MI][C::NI][2];
 #pragma unroll
-    for (int kc = 0; kc < C::BK / 8; ++kc) {
+    for (int i = 0; i < C::MI; ++i)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int s = 2 * t + h;       // complex k slot within the 8-complex chunk
-        const int krow = kc * 8 + s;   // B row within the stage
-        double2 a[C::MI];
+      for (int k = 0; k < C::NI; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
+
+    for (int kk = k0; kk < k1; ++kk) {
+      mbar_wait(&full[stage], phase);
+      const uint8_t* sA = smem + stage * C::STAGE_BYTES;
+      const uint8_t* sB = sA + C::A_BYTES;
 #pragma unroll
-        for (int i = 0; i < C::MI; ++i)
-          a[i] = *reinterpret_cast<const double2*>(sA + kc * C::BM * 128 + a_row_off[i] + ((s ^ a_key[i]) << 4));
+      for (int kc = 0; kc < C::BK / 8; ++kc) {
 #pragma unroll
-        for (int k = 0; k < C::NI; ++k) {
-          const double2 bv =
-              *reinterpret_cast<const double2*>(sB + b_col_off[k] + krow * 128 + ((b_slot[k] ^ (krow & 7)) << 4));
-          // B' = [[br, bi], [-bi, br]]: row (k, re) -> (br | bi), row (k, im) -> (-bi | br)
-          const double b_re_row = q ? bv.y : bv.x;
-          const double b_im_row = q ? bv.x : neg(bv.y);
+        for (int h = 0; h < 2; ++h) {
+          const int s = 2 * t + h;       // complex k slot within the 8-complex chunk
+          const int krow = kc * 8 + s;   // B row within the stage
+          double2 a[C::MI];
 #pragma unroll
-          for (int i = 0; i < C::MI; ++i) {
-            dmma(acc[i][k][0], acc[i][k][1], a[i].x, b_re_row);
-            dmma(acc[i][k][0], acc[i][k][1], a[i].y, b_im_row);
+          for (int i = 0; i < C::MI; ++i)
+            a[i] = *reinterpret_cast<const double2*>(sA + kc * C::BM * 128 + a_row_off[i] + ((s ^ a_key[i]) << 4));
+#pragma unroll
+          for (int k = 0; k < C::NI; ++k) {
+            const double2 bv =
+                *reinterpret_cast<const double2*>(sB + b_col_off[k] + krow * 128 + ((b_slot[k] ^ (krow & 7)) << 4));
+            // B' = [[br, bi], [-bi, br]]: row (k, re) -> (br | bi), row (k, im) -> (-bi | br)
+            const double b_re_row = q ? bv.y : bv.x;
+            const double b_im_row = q ? bv.x : neg(bv.y);
+#pragma unroll
+            for (int i = 0; i < C::MI; ++i) {
+              dmma(acc[i][k][0], acc[i][k][1], a[i].x, b_re_row);
+              dmma(acc[i][k][0], acc[i][k][1], a[i].y, b_im_row);
+            }
           }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == C::STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
-    if (++stage == C::STAGES) {
-      stage = 0;
-      phase ^= 1;
-    }
-  }
 
-  // epilogue: lane (g, t) owns complex C[row g][col t] of each 8x(4 complex) tile
-  double2* out;
-  int64_t ld;
-  if (args.splits > 1) {
-    out = args.ws + (int64_t(split) * args.batch + b) * args.M * args.Nn;
-    ld = args.Nn;
-  } else {
-    out = args.C + int64_t(b) * args.sCb;
-    ld = args.ldc;
-  }
+    if (k1 < args.KT) {
+      // contributor: publish this warp's partial fragment for the tile's owner
+      double* slot = args.ws + (int64_t(cta) * C::NCW + warp) * (C::FRAG * 32);
 #pragma unroll
-  for (int i = 0; i < C::MI; ++i) {
-    const int64_t row = m0 + wm * C::WM + i * 8 + g;
-    if (row >= args.M) continue;
+      for (int i = 0; i < C::MI; ++i)
 #pragma unroll
-    for (int k = 0; k < C::NI; ++k) {
-      const int64_t col = n0 + wn * C::WN + k * 4 + t;
-      if (col < args.Nn) out[row * ld + col] = make_double2(acc[i][k][0], acc[i][k][1]);
+        for (int k = 0; k < C::NI; ++k) {
+          __stcg(slot + ((i * C::NI + k) * 2 + 0) * 32 + lane, acc[i][k][0]);
+          __stcg(slot + ((i * C::NI + k) * 2 + 1) * 32 + lane, acc[i][k][1]);
+        }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release(&args.flags[cta * C::NCW + warp], 1);
+      continue;
     }
-  }
-}
-
-// C[b][m][n] = sum_{s < splits} ws[s][b][m][n], in split order (deterministic).
-__global__ void splitk_reduce_kernel(const double2* __restrict__ ws, double2* __restrict__ C, int64_t M, int64_t Nn,
-                                     int64_t ldc, int64_t sCb, int batch, int splits) {
-  const int64_t per_b = M * Nn, total = per_b * batch;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    double re = 0.0, im = 0.0;
-    for (int s = 0; s < splits; ++s) {
-      const double2 v = __ldg(ws + int64_t(s) * total + e);
-      re += v.x;
-      im += v.y;
+    if (k0 > 0) {
+      // owner: add the partials of the earlier CTAs in fixed order c-1, c-2, ...
+      const int64_t it0 = base;
+      int64_t cf = (it0 * args.G) / args.total;
+      while (cf + 1 < args.G && range_start(cf + 1, args) <= it0) ++cf;
+      while (cf > 0 && range_start(cf, args) > it0) --cf;
+      for (int64_t c2 = int64_t(cta) - 1; c2 >= cf; --c2) {
+        int* flag = &args.flags[c2 * C::NCW + warp];
+        while (ld_acquire(flag) == 0) {
+        }
+        const double* slot = args.ws + (c2 * C::NCW + warp) * (C::FRAG * 32);
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int k = 0; k < C::NI; ++k) {
+            acc[i][k][0] += __ldcg(slot + ((i * C::NI + k) * 2 + 0) * 32 + lane);
+            acc[i][k][1] += __ldcg(slot + ((i * C::NI + k) * 2 + 1) * 32 + lane);
+          }
+        __syncwarp();
+        if (lane == 0) *flag = 0;  // consumed; zero again for the next launch
+      }
     }
-    const int64_t b = e / per_b, r = e - b * per_b;
-    const int64_t m = r / Nn, n = r - m * Nn;
-    C[b * sCb + m * ldc + n] = make_double2(re, im);
+    // store: lane (g, t) owns complex C[row g][col t] of each 8 x (4 complex) tile
+    const int64_t b = tile / tiles_mn;
+    const int64_t r = tile - b * tiles_mn;
+    const int tn = int(r / args.tiles_m), tm = int(r - int64_t(tn) * args.tiles_m);
+    double2* out = args.C + b * args.sCb;
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i) {
+      const int64_t row = int64_t(tm) * C::BM + wm * C::WM + i * 8 + g;
+      if (row >= args.M) continue;
+#pragma unroll
+      for (int k = 0; k < C::NI; ++k) {
+        const int64_t col = int64_t(tn) * C::BN + wn * C::WN + k * 4 + t;
+        if (col < args.Nn) out[row * args.ldc + col] = make_double2(acc[i][k][0], acc[i][k][1]);
+      }
+    }
   }
 }
 
@@ -284,22 +350,30 @@ bool make_map(CUtensorMap* map, const void* base, const uint64_t dims[4], const 
 using Big = Cfg<64, 64, 16, 32, 16, 4>;
 
 template <class C>
-int choose_splits(const ZgemmProblem& p, int num_sms, int64_t ctas, int64_t kt_total) {
-  // enough CTAs for a few full waves when the output is too small to fill the GPU; each
-  // split keeps >= 8 k-tiles so the pipeline stays deep
-  if (ctas >= num_sms) return 1;
-  int64_t want = (int64_t(4) * num_sms + ctas - 1) / ctas;
-  int64_t cap = kt_total / 8;
-  int64_t s = want < cap ? want : cap;
-  return s < 1 ? 1 : int(s);
+void geometry(const ZgemmProblem& p, int num_sms, int& tiles_m, int& tiles_n, int& kt_per_o, int64_t& total,
+              int& G) {
+  tiles_m = int((p.M + C::BM - 1) / C::BM);
+  tiles_n = int((p.Nn + C::BN - 1) / C::BN);
+  kt_per_o = int((p.Kin + C::BK - 1) / C::BK);
+  const int64_t KT = p.Ko * kt_per_o;
+  total = int64_t(tiles_m) * tiles_n * p.batch * KT;
+  G = int(total < num_sms ? total : num_sms);
+}
+
+// The flag region has a fixed size (max grid) so that it stays zero across problems that
+// share a workspace: every launch leaves all its flags at zero.
+template <class C>
+size_t flag_bytes(int num_sms) {
+  return ((size_t(num_sms) * C::NCW * 4 + 255) / 256) * 256;
 }
 
 template <class C>
 size_t ws_bytes(const ZgemmProblem& p, int num_sms) {
-  const int64_t tiles = ((p.M + C::BM - 1) / C::BM) * ((p.Nn + C::BN - 1) / C::BN);
-  const int64_t kt_total = p.Ko * ((p.Kin + C::BK - 1) / C::BK);
-  const int splits = choose_splits<C>(p, num_sms, tiles * p.batch, kt_total);
-  return splits > 1 ? size_t(splits) * size_t(p.batch) * size_t(p.M) * size_t(p.Nn) * 16 : 0;
+  int tm, tn, kpo, G;
+  int64_t total;
+  geometry<C>(p, num_sms, tm, tn, kpo, total, G);
+  const size_t slots = size_t(G) * C::SLOT_DOUBLES * 8;
+  return flag_bytes<C>(num_sms) + slots;
 }
 
 template <class C>
@@ -318,37 +392,23 @@ cudaError_t launch_cfg(const ZgemmProblem& p, void* ws, size_t ws_size, int num_
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles_m = int((p.M + C::BM - 1) / C::BM), tiles_n = int((p.Nn + C::BN - 1) / C::BN);
-  const int kt_per_o = int((p.Kin + C::BK - 1) / C::BK);
-  const int64_t kt_total = p.Ko * kt_per_o;
-  const int64_t ctas = int64_t(tiles_m) * tiles_n * p.batch;
-  int splits = choose_splits<C>(p, num_sms, ctas, kt_total);
-  if (splits > 1 && (ws == nullptr || ws_size < ws_bytes<C>(p, num_sms))) splits = 1;
+  if (ws == nullptr || ws_size < ws_bytes<C>(p, num_sms)) return cudaErrorInvalidValue;
   KArgs a;
+  int G;
+  geometry<C>(p, num_sms, a.tiles_m, a.tiles_n, a.kt_per_o, a.total, G);
+  a.G = G;
+  a.KT = int(p.Ko * a.kt_per_o);
   a.C = static_cast<double2*>(p.C);
-  a.ws = static_cast<double2*>(ws);
+  const size_t flags = flag_bytes<C>(num_sms);
+  a.flags = static_cast<int*>(ws);
+  a.ws = reinterpret_cast<double*>(static_cast<char*>(ws) + flags);
   a.M = p.M;
   a.Nn = p.Nn;
   a.ldc = p.ldc;
   a.sCb = p.sCb;
-  a.tiles_m = tiles_m;
-  a.kt_per_o = kt_per_o;
-  a.kt_total = int(kt_total);
-  a.splits = splits;
-  a.batch = int(p.batch);
-  dim3 grid(unsigned(tiles_m * tiles_n), unsigned(splits), unsigned(p.batch));
-  zgemm_dmma_kernel<C><<<grid, C::THREADS, C::SMEM, st>>>(ta, tb, a);
+  zgemm_dmma_kernel<C><<<G, C::THREADS, C::SMEM, st>>>(ta, tb, a);
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  if (nl) ++*nl;
-  if (splits > 1) {
-    const int64_t total = p.batch * p.M * p.Nn;
-    int blocks = int((total + 255) / 256);
-    if (blocks > 8 * num_sms) blocks = 8 * num_sms;
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(a.ws, a.C, p.M, p.Nn, p.ldc, p.sCb, int(p.batch), splits);
-    e = cudaGetLastError();
-    if (nl) ++*nl;
-  }
+  if (e == cudaSuccess && nl) ++*nl;
   return e;
 }
 
@@ -359,7 +419,8 @@ size_t zgemm_workspace_bytes(const ZgemmProblem& p, int num_sms) { return ws_byt
 cudaError_t launch_zgemm(const ZgemmProblem& p, void* workspace, size_t ws_size, int num_sms, cudaStream_t stream,
                          int* n_launches) {
   if (p.M <= 0 || p.Nn <= 0 || p.Kin <= 0 || p.Ko <= 0 || p.batch <= 0) return cudaErrorInvalidValue;
-  if (p.batch > 65535) return cudaErrorInvalidValue;
+  if (2 * p.Kin > (int64_t(1) << 31) || p.M > (int64_t(1) << 31) || p.batch > (int64_t(1) << 31))
+    return cudaErrorInvalidValue;
   return launch_cfg<Big>(p, workspace, ws_size, num_sms, stream, n_launches);
 }
 

@@ -215,3 +215,36 @@ def test_c2_full_size_sampled_slices():
         r_or, c_or = values.run_workload(w, dag, t_range=(t, t + 1))
         assert_roots_close({k: v[t:t + 1] for k, v in roots.items()}, r_or)
         assert_corr_close(dag, r_or, {k: v[t:t + 1] for k, v in corr.items()}, c_or)
+
+
+def test_stream_k_repeatable_bitwise(ctx):
+    """Persistent stream-K: a tile split across CTAs is fixed up in a static order, so two
+    launches give identical bits (also across problem sizes sharing the workspace)."""
+    for (Lt, N, S, kind) in ((3, 100, 1, "mm1"), (1, 40, 64, "bb2"), (2, 8, 1, "mm1"), (1, 64, 16, "bb2")):
+        if kind == "mm1":
+            A = _random_phase((Lt, N, N), 11)
+            B = _random_phase((Lt, N, N), 12)
+            C1 = torch.empty(Lt * N * N * 2, dtype=torch.float64, device="cuda")
+            C2 = torch.empty_like(C1)
+            dA, dB = device_from(A), device_from(B)
+            ctx.mm1(dA, dB, C1, Lt, N)
+            ctx.mm1(dA, dB, C2, Lt, N)
+            want = values.mm1(A, B)
+            scale = np.matmul(np.abs(A), np.abs(B))
+            shape = (Lt, N, N)
+        else:
+            A = _random_phase((Lt, S, N, N, N), 13)
+            B = _random_phase((Lt, S, N, N, N), 14)
+            C1 = torch.empty(Lt * N * N * 2, dtype=torch.float64, device="cuda")
+            C2 = torch.empty_like(C1)
+            dA, dB = device_from(A), device_from(B)
+            ctx.bb2(dA, dB, C1, Lt, N, S)
+            ctx.bb2(dA, dB, C2, Lt, N, S)
+            want = values.bb2(A, B)
+            scale = sum(np.matmul(np.abs(A[:, s]).reshape(Lt, N, N * N), np.abs(B[:, s]).reshape(Lt, N * N, N))
+                        for s in range(S))
+            shape = (Lt, N, N)
+        torch.cuda.synchronize()
+        g1, g2 = to_numpy_c(C1, shape), to_numpy_c(C2, shape)
+        assert np.array_equal(g1, g2)
+        assert np.all(np.abs(g1 - want) <= 1e-13 * scale)

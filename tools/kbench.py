@@ -21,7 +21,8 @@ def timeit(fn, stream, reps=10, warm=3, flush=None):
     ts = []
     for _ in range(reps):
         if flush is not None:
-            flush.zero_()
+            with torch.cuda.stream(stream):
+                flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
