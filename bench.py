@@ -264,7 +264,7 @@ def main():
     # the compute stream) for the roofline of the dominant kernel ---------------------------------
     ksec, kcnt, inst_s = [0.0] * 8, [0] * 8, 0.0
     for _ in range(3):
-        ex = ctx.execute(cc.EXEC_TIME_KERNELS)
+        ex = ctx.execute(cc.EXEC_GRAPH | cc.EXEC_TIME_KERNELS)
         s_, c_ = ctx.kernel_times()
         ksec = [a + b for a, b in zip(ksec, s_)]
         kcnt = [a + b for a, b in zip(kcnt, c_)]
@@ -333,8 +333,8 @@ def main():
                          "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(),
                          "peak_source": peak_src, "mm1_avg_us": mm1_avg * 1e6, "tr_avg_us": tr_avg * 1e6,
                          "mm1_share_of_step": ksec[cc.CC_MM1] / inst_s if inst_s else None,
-                         "how": "CUDA events around every kernel on the compute stream (cc_execute flags bit 1), "
-                                "3 instrumented replays after the timed region"},
+                         "how": "CUDA events captured around every kernel of the plan's CUDA graph, on the compute "
+                                "stream (cc_execute flags 1|2); 3 replays right after the timed region"},
             "plan": {"peak_bytes": pst["peak"], "transient_peak_bytes": pst["transient_peak"],
                      "evictions": pst["evictions"], "h2d_bytes": pst["h2d_bytes"], "d2h_bytes": pst["d2h_bytes"],
                      "sched_ms": pst["sched_seconds"] * 1e3, "plan_ms": pst["plan_seconds"] * 1e3},

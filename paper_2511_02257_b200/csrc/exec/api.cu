@@ -88,6 +88,11 @@ struct cc_ctx {
   std::vector<cudaEvent_t> events;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_h_end = nullptr, ev_d_end = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  // graph with CUDA events around every kernel (flags 1|2): per-kind kernel times of a
+  // graph replay, free of host launch overhead
+  cudaGraphExec_t gexec_timed = nullptr;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed_ev;
+  std::vector<int> timed_kind;
   bool executed = false;
   KindTimes ktimes;
   int64_t last_n_kernels = 0;
@@ -103,6 +108,14 @@ struct cc_ctx {
   void release_graph() {
     if (gexec) cudaGraphExecDestroy(gexec);
     gexec = nullptr;
+    if (gexec_timed) cudaGraphExecDestroy(gexec_timed);
+    gexec_timed = nullptr;
+    for (auto& pr : timed_ev) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    timed_ev.clear();
+    timed_kind.clear();
   }
   void release_phys() {
     release_graph();
@@ -381,28 +394,35 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
   prepare_phys(ctx);
   const bool use_graph = (flags & 1) != 0;
-  const bool time_kernels = (flags & 2) != 0 && !use_graph;
+  const bool time_kernels = (flags & 2) != 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;
   std::vector<int> kev_kind;
+  bool own_kev = true;
   cudaEvent_t t_begin, t_end;
   ck(cudaEventCreate(&t_begin), "event");
   ck(cudaEventCreate(&t_end), "event");
   ck(cudaEventRecord(t_begin, ctx->cs), "event");
   if (use_graph) {
-    if (!ctx->gexec) {
+    cudaGraphExec_t& gx = time_kernels ? ctx->gexec_timed : ctx->gexec;
+    if (!gx) {
       cudaGraph_t graph;
       ck(cudaStreamBeginCapture(ctx->cs, cudaStreamCaptureModeThreadLocal), "graph capture");
       try {
-        ctx->last_n_kernels = issue(ctx, false, nullptr, nullptr);
+        ctx->last_n_kernels = issue(ctx, time_kernels, &ctx->timed_ev, &ctx->timed_kind);
       } catch (...) {
         cudaStreamEndCapture(ctx->cs, &graph);
         throw;
       }
       ck(cudaStreamEndCapture(ctx->cs, &graph), "graph capture");
-      ck(cudaGraphInstantiate(&ctx->gexec, graph, 0), "graph instantiate");
+      ck(cudaGraphInstantiate(&gx, graph, 0), "graph instantiate");
       cudaGraphDestroy(graph);
     }
-    ck(cudaGraphLaunch(ctx->gexec, ctx->cs), "graph launch");
+    ck(cudaGraphLaunch(gx, ctx->cs), "graph launch");
+    if (time_kernels) {
+      kev = ctx->timed_ev;
+      kev_kind = ctx->timed_kind;
+      own_kev = false;
+    }
   } else {
     ctx->last_n_kernels = issue(ctx, time_kernels, &kev, &kev_kind);
   }
@@ -435,8 +455,10 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
     if (blocking) cudaEventElapsedTime(&ms, kev[i].first, kev[i].second);
     ctx->ktimes.seconds[kev_kind[i]] += ms * 1e-3;
     ctx->ktimes.count[kev_kind[i]] += 1;
-    cudaEventDestroy(kev[i].first);
-    cudaEventDestroy(kev[i].second);
+    if (own_kev) {
+      cudaEventDestroy(kev[i].first);
+      cudaEventDestroy(kev[i].second);
+    }
   }
   if (stats) {
     double ks = 0;

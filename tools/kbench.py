@@ -15,21 +15,23 @@ sys.path.insert(0, ROOT)
 from paper_2511_02257_b200 import cc  # noqa: E402
 
 
-def timeit(fn, stream, reps=10, warm=3, flush=None):
+def timeit(fn, stream, reps=10, warm=3, flush=None, inner=20):
+    """Median over `reps` of (time of `inner` back-to-back launches)/inner; the stream is kept
+    backlogged (a flush kernel queued first) so host launch overhead is not measured."""
     for _ in range(warm):
         fn()
     ts = []
     for _ in range(reps):
-        if flush is not None:
-            with torch.cuda.stream(stream):
-                flush.zero_()
+        with torch.cuda.stream(stream):
+            flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        fn()
+        for _ in range(inner):
+            fn()
         e1.record(stream)
         e1.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1e-3)
+        ts.append(e0.elapsed_time(e1) * 1e-3 / inner)
     ts.sort()
     return ts[len(ts) // 2]
 
@@ -74,7 +76,7 @@ def main():
             fn = lambda: ctx.tr_mm(A, B, C, Lt, N)  # noqa: E731
             flops = 8.0 * Lt * N * N
             byts = 32.0 * Lt * N * N
-        t = timeit(fn, s, flush=flush)
+        t = timeit(fn, s, flush=flush, inner=3 if flops > 1e11 else 20)
         r = dict(kind=kind, Lt=Lt, N=N, S=S, us=t * 1e6, tflops=flops / t / 1e12, gbs=byts / t / 1e9)
         rows.append(r)
         print("%-4s Lt=%4d N=%5d S=%3d  %10.1f us  %7.2f TFLOP/s  %8.1f GB/s" %
