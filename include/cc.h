@@ -166,7 +166,11 @@ cc_status cc_set_leaf_device(cc_ctx* ctx, int64_t leaf_id, const void* dev, size
 
 /* Replays the plan on the device: H2D / D2H on the copy streams, contractions on the
  * compute stream, event dependencies for RAW on data and WAR on reused memory; blocking.
- * flags bit 0: capture/replay as a CUDA graph; bit 1: time every kernel (kernel_seconds). */
+ * flags bit 0: capture/replay as a CUDA graph; bit 1: time every kernel (kernel_seconds; not
+ * with bit 0).  bit 2 / bit 3: kernel-only replay of the plan's GEMM-kind (MM1/BM1/BB2) /
+ * TR_MM launches alone, in plan order, as a cached graph, after a full execute: stats->seconds
+ * = device time of the replay, n_kernels = launches, flops/hbm_bytes = their algorithmic work
+ * (average launch duration for the roofline, without host launch overhead). */
 cc_status cc_execute(cc_ctx* ctx, int32_t flags, cc_exec_stats* stats);
 /* Enqueue-only variant (no host sync): work is ordered on the compute stream. */
 cc_status cc_execute_async(cc_ctx* ctx, int32_t flags);

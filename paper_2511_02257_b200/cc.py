@@ -23,7 +23,7 @@ P = ctypes.POINTER
 CC_LEAF_M, CC_LEAF_B, CC_MM1, CC_BM1, CC_BB2, CC_TR_MM, CC_LEAF_X, CC_OP_X = range(8)
 CC_SIBLING, CC_TREE, CC_GIVEN = range(3)
 PART_TIME, PART_TREES = 0, 1
-EXEC_GRAPH, EXEC_TIME_KERNELS = 1, 2
+EXEC_GRAPH, EXEC_TIME_KERNELS, EXEC_ONLY_GEMM, EXEC_ONLY_TRACE = 1, 2, 4, 8
 STATUS = {0: "OK", -1: "INVAL", -2: "PARSE", -3: "CYCLE", -4: "INCONSISTENT", -5: "MULTIROOT",
           -6: "UNKNOWN_NODE", -7: "NOT_CLOSED", -8: "INFEASIBLE", -9: "STATE", -10: "BUFFER_TOO_SMALL",
           -11: "CUDA", -12: "NOMEM"}

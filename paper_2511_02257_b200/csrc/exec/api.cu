@@ -6,6 +6,7 @@
 // data and WAR/WAW on reused pool memory, so copies run ahead of compute as far as the
 // plan's logical residency allows (prefetch without changing the plan).  The whole
 // replay can be captured once as a CUDA graph and relaunched.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -13,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -21,6 +23,7 @@
 #include "../host/partition.hpp"
 #include "../host/plan.hpp"
 #include "../host/sched.hpp"
+#include "../kernels/dataflow.hpp"
 #include "../kernels/kernels.hpp"
 #include "cc.h"
 
@@ -88,14 +91,42 @@ struct cc_ctx {
   std::vector<cudaEvent_t> events;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_h_end = nullptr, ev_d_end = nullptr;
   cudaGraphExec_t gexec = nullptr;
-  // graph with CUDA events around every kernel (flags 1|2): per-kind kernel times of a
-  // graph replay, free of host launch overhead
-  cudaGraphExec_t gexec_timed = nullptr;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed_ev;
-  std::vector<int> timed_kind;
+  // kernel-only replays (flags 4: GEMM kinds, 8: TR_MM): the plan's contraction launches of
+  // those kinds alone, in plan order, as a CUDA graph -> average launch duration of a kind
+  // with no host launch overhead (the roofline measurement)
+  cudaGraphExec_t gexec_kind[2] = {nullptr, nullptr};
   bool executed = false;
   KindTimes ktimes;
   int64_t last_n_kernels = 0;
+
+  // dataflow execution (persistent workers): device metadata + per-launch sync area
+  bool df_valid = false;
+  char* df_meta = nullptr;          // cudaMalloc: ops, deps, tensor maps, sync area
+  size_t df_meta_bytes = 0;
+  DfArgs df_gemm{}, df_trace{};
+  int* df_sync = nullptr;           // zeroed per launch (with the two queue heads before it)
+  size_t df_sync_bytes = 0;
+  char* df_chunk_ws = nullptr;      // arena scratch: chunk partial rings, trace partial rings
+  int64_t df_chunk_slot = 0, df_chunk_cnt_slot = 0;
+  char* df_trace_ws = nullptr;
+  int64_t df_trace_slot = 0;
+  struct DfCopy {
+    int32_t op;                     // plan op index
+    int32_t stream;                 // S_H2D / S_D2H
+    void* dst;
+    const void* src;
+    size_t bytes;
+    int32_t flag_slot;
+    std::vector<std::pair<int32_t, int32_t>> wait_values;  // (sync slot, target)
+    std::vector<int32_t> wait_events;                        // copy ops on the other copy stream
+    bool source = false;
+  };
+  std::vector<DfCopy> df_copies;
+  std::vector<cudaEvent_t> df_events;  // per copy (index into df_copies), when some copy waits on it
+  cudaStream_t cs2 = nullptr;       // second compute stream (trace worker)
+  cudaEvent_t ev_cs2 = nullptr;
+  cudaGraphExec_t gexec_df = nullptr;
+  int64_t df_gemm_items = 0, df_trace_items = 0;
 
   // direct kernel entry points (GEMM split-K partials; trace partials + zeroed counters)
   char* direct_ws = nullptr;
@@ -105,20 +136,29 @@ struct cc_ctx {
 
   ~cc_ctx() { release_device(); }
 
+  void release_df() {
+    if (gexec_df) cudaGraphExecDestroy(gexec_df);
+    gexec_df = nullptr;
+    if (df_meta) cudaFree(df_meta);
+    df_meta = nullptr;
+    for (auto e : df_events)
+      if (e) cudaEventDestroy(e);
+    df_events.clear();
+    df_copies.clear();
+    df_valid = false;
+  }
   void release_graph() {
+    release_df();
     if (gexec) cudaGraphExecDestroy(gexec);
     gexec = nullptr;
-    if (gexec_timed) cudaGraphExecDestroy(gexec_timed);
-    gexec_timed = nullptr;
-    for (auto& pr : timed_ev) {
-      cudaEventDestroy(pr.first);
-      cudaEventDestroy(pr.second);
+    for (auto& gk : gexec_kind) {
+      if (gk) cudaGraphExecDestroy(gk);
+      gk = nullptr;
     }
-    timed_ev.clear();
-    timed_kind.clear();
   }
   void release_phys() {
     release_graph();
+    release_df();
     for (auto e : events)
       if (e) cudaEventDestroy(e);
     events.clear();
@@ -137,6 +177,10 @@ struct cc_ctx {
       }
     if (direct_ws) cudaFree(direct_ws);
     direct_ws = nullptr;
+    if (cs2) cudaStreamDestroy(cs2);
+    cs2 = nullptr;
+    if (ev_cs2) cudaEventDestroy(ev_cs2);
+    ev_cs2 = nullptr;
     if (direct_tr_ws) cudaFree(direct_tr_ws);
     direct_tr_ws = nullptr;
     if (own_streams) {
@@ -233,6 +277,31 @@ ZgemmProblem problem_for(int op, int64_t Lt, int64_t N, int64_t S, const void* a
   return p;
 }
 
+constexpr int64_t DF_CHUNK_RING = 4;   // GEMM ops split in k that may be in flight at once
+constexpr int64_t DF_TRACE_RING = 16;  // TR ops that may be in flight at once
+
+// Work split of one GEMM op for the dataflow worker: tiles of BM x BN, KT k-tiles; an op
+// with fewer tiles than SMs is split into k-chunks so it still spreads over the GPU.
+void df_gemm_geometry(const ZgemmProblem& p, int64_t& tiles, int64_t& KT, int64_t& chunks, int num_sms) {
+  int BM, BN, BK, slot;
+  df_gemm_tile_dims(&BM, &BN, &BK, &slot);
+  tiles = ((p.M + BM - 1) / BM) * ((p.Nn + BN - 1) / BN) * p.batch;
+  KT = p.Ko * ((p.Kin + BK - 1) / BK);
+  chunks = 1;
+  if (tiles < num_sms) {
+    const int64_t want = (2 * num_sms + tiles - 1) / tiles;
+    const int64_t cap = std::max<int64_t>(1, KT / 4);
+    chunks = std::min(want, cap);
+  }
+}
+
+// Pieces per time slice of a TR op: ~8 blocks of 32x32 (256 KB of operands) per item.
+int64_t df_trace_pieces(int64_t Lt, int64_t N) {
+  const int64_t nb = (N + 31) / 32, U = nb * nb;
+  (void)Lt;
+  return std::max<int64_t>(1, (U + 7) / 8);
+}
+
 // Sets up scratch (kernel workspace, roots, correlators, term tables), the physical plan,
 // events and the host pool.  Called lazily by cc_execute.
 void prepare_phys(cc_ctx* ctx) {
@@ -253,7 +322,24 @@ void prepare_phys(cc_ctx* ctx) {
   const int64_t sz_roots = round_up(n_trees * Lt * 16, ALIGN), sz_corr = round_up(std::max<int64_t>(n_corr, 1) * Lt * 16, ALIGN);
   const int64_t sz_ts = round_up((n_corr + 1) * 4, ALIGN), sz_tt = round_up(std::max<int64_t>(n_terms, 1) * 4, ALIGN);
   const int64_t sz_tc = round_up(std::max<int64_t>(n_terms, 1) * 16, ALIGN);
-  const int64_t scratch = sz_gemm + sz_trace + sz_roots + sz_corr + sz_ts + sz_tt + sz_tc;
+  // dataflow workspaces: rings of chunk-partial slots (GEMM ops split in k) and of trace
+  // partial slots (per-op tickets and [Lt][P] partials)
+  ctx->df_chunk_slot = ctx->df_chunk_cnt_slot = 0;
+  for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)}) {
+    if (!has[op]) continue;
+    int64_t tiles, KT, chunks;
+    df_gemm_geometry(problem_for(op, Lt, N, S, nullptr, nullptr, nullptr), tiles, KT, chunks, ctx->num_sms);
+    if (chunks > 1) {
+      int BM, BN, BK, slot;
+      df_gemm_tile_dims(&BM, &BN, &BK, &slot);
+      ctx->df_chunk_slot = std::max(ctx->df_chunk_slot, round_up(tiles * chunks * slot * 8, ALIGN));
+      ctx->df_chunk_cnt_slot = std::max(ctx->df_chunk_cnt_slot, round_up(tiles * 4, ALIGN));
+    }
+  }
+  ctx->df_trace_slot = round_up(Lt * df_trace_pieces(Lt, N) * 16, ALIGN) + round_up(Lt * 4, ALIGN);
+  const int64_t sz_df_chunk = DF_CHUNK_RING * (ctx->df_chunk_slot + ctx->df_chunk_cnt_slot);
+  const int64_t sz_df_trace = DF_TRACE_RING * ctx->df_trace_slot;
+  const int64_t scratch = sz_gemm + sz_trace + sz_roots + sz_corr + sz_ts + sz_tt + sz_tc + sz_df_chunk + sz_df_trace;
   const int64_t pool = (ctx->arena_bytes - scratch) / ALIGN * ALIGN;
   if (pool <= 0) throw Error(CC_E_NOMEM, "arena too small for the kernel workspace (" + std::to_string(scratch) + " B)");
   ctx->pool_bytes = pool;
@@ -265,6 +351,10 @@ void prepare_phys(cc_ctx* ctx) {
   ctx->term_start = reinterpret_cast<int32_t*>(s); s += sz_ts;
   ctx->term_tree = reinterpret_cast<int32_t*>(s); s += sz_tt;
   ctx->term_coef = reinterpret_cast<double*>(s); s += sz_tc;
+  ctx->df_chunk_ws = s; s += sz_df_chunk;
+  ctx->df_trace_ws = s; s += sz_df_trace;
+  if (sz_df_chunk > 0) ck(cudaMemset(ctx->df_chunk_ws, 0, size_t(sz_df_chunk)), "dataflow workspace");
+  if (sz_df_trace > 0) ck(cudaMemset(ctx->df_trace_ws, 0, size_t(sz_df_trace)), "dataflow workspace");
   // term tables grouped by correlator slot (corr ids ascending), input order within a slot
   std::vector<int32_t> start(size_t(n_corr) + 1, 0), tree(size_t(std::max<int64_t>(n_terms, 1)), 0);
   std::vector<double> coef(size_t(std::max<int64_t>(n_terms, 1)) * 2, 0.0);
@@ -304,6 +394,351 @@ void prepare_phys(cc_ctx* ctx) {
   for (size_t i = 0; i < ctx->pp.ops.size(); ++i)
     if (ctx->pp.ops[i].source) ck(cudaEventCreateWithFlags(&ctx->events[i], cudaEventDisableTiming), "event");
   ctx->phys_valid = true;
+}
+
+
+// ------------------------------------------------------------------------------------------
+// Dataflow execution: the plan's contractions as work items of two persistent workers,
+// copies on the copy streams, synchronised through integer slots (kernels/dataflow.hpp).
+
+// Reads/writes of byte ranges in plan order -> data dependencies between plan ops (RAW on the
+// last writer; WAR/WAW on the last writer and every reader since).
+class RWTracker {
+ public:
+  explicit RWTracker(int64_t capacity) { pieces_[0] = Piece{std::max<int64_t>(capacity, 1), -1, {}}; }
+  void read(int64_t off, int64_t n, int32_t op, std::vector<int32_t>& deps) {
+    visit(off, n, [&](Piece& p) {
+      if (p.writer >= 0) deps.push_back(p.writer);
+      p.readers.push_back(op);
+    });
+  }
+  void write(int64_t off, int64_t n, int32_t op, std::vector<int32_t>& deps) {
+    visit(off, n, [&](Piece& p) {
+      if (p.writer >= 0) deps.push_back(p.writer);
+      deps.insert(deps.end(), p.readers.begin(), p.readers.end());
+      p.readers.clear();
+      p.writer = op;
+    });
+  }
+
+ private:
+  struct Piece {
+    int64_t end;
+    int32_t writer;
+    std::vector<int32_t> readers;
+  };
+  std::map<int64_t, Piece> pieces_;
+  void split(int64_t at) {
+    auto it = pieces_.upper_bound(at);
+    if (it == pieces_.begin()) return;
+    --it;
+    if (it->first == at || it->second.end <= at) return;
+    Piece hi = it->second;
+    it->second.end = at;
+    pieces_[at] = hi;
+  }
+  template <class F>
+  void visit(int64_t off, int64_t n, F f) {
+    split(off);
+    split(off + n);
+    for (auto it = pieces_.find(off); it != pieces_.end() && it->first < off + n; ++it) f(it->second);
+  }
+};
+
+using PFN_waitval = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_waitval df_wait_fn() {
+  static PFN_waitval fn = nullptr;
+  static bool done = false;
+  if (!done) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_waitval>(p);
+    done = true;
+  }
+  return fn;
+}
+PFN_waitval df_write_fn() {
+  static PFN_waitval fn = nullptr;
+  static bool done = false;
+  if (!done) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_waitval>(p);
+    done = true;
+  }
+  return fn;
+}
+
+void prepare_dataflow(cc_ctx* ctx) {
+  if (ctx->df_valid) return;
+  prepare_phys(ctx);
+  const Dag& g = *ctx->dag;
+  const auto& ops = ctx->pp.ops;
+  const int64_t Lt = g.Lt, N = g.N;
+  const int32_t n_ops = int32_t(ops.size());
+  const int64_t per_t_m = 16LL * g.N * g.N;
+  // 1. data dependencies over the device pool and the host pool
+  RWTracker dev(ctx->pool_bytes), host(std::max<int64_t>(ctx->pp.host_pool_bytes, 1));
+  std::vector<std::vector<int32_t>> deps(static_cast<size_t>(n_ops));
+  for (int32_t i = 0; i < n_ops; ++i) {
+    const PhysOp& op = ops[size_t(i)];
+    const Node& n = g.nodes[size_t(op.node)];
+    const int64_t rb = round_up(n.size, ALIGN);
+    auto& d = deps[size_t(i)];
+    if (op.kind == OP_H2D && op.stream != S_NONE) {
+      dev.write(op.dev_off, rb, i, d);
+      if (op.host_off >= 0) host.read(op.host_off, rb, i, d);
+    } else if (op.kind == OP_D2H) {
+      dev.read(op.dev_off, rb, i, d);
+      host.write(op.host_off, rb, i, d);
+    } else if (op.kind == OP_CONTRACT) {
+      if (op.loc_a == LOC_POOL) dev.read(op.off_a, round_up(g.nodes[size_t(n.l)].size, ALIGN), i, d);
+      if (op.loc_b == LOC_POOL) dev.read(op.off_b, round_up(g.nodes[size_t(n.r)].size, ALIGN), i, d);
+      if (op.dev_off >= 0) dev.write(op.dev_off, rb, i, d);
+    }
+    std::sort(d.begin(), d.end());
+    d.erase(std::unique(d.begin(), d.end()), d.end());
+    d.erase(std::remove(d.begin(), d.end(), i), d.end());
+  }
+  // 2. sync slots and work items
+  std::vector<int32_t> slot(size_t(n_ops), -1), target(size_t(n_ops), 0), df_index(size_t(n_ops), -1);
+  int32_t n_sync = 0;
+  std::vector<DfOp> gops, tops;
+  std::vector<int32_t> gplan, tplan;   // plan op index of each DfOp
+  std::vector<uint8_t> tmaps;
+  int64_t g_items = 0, t_items = 0;
+  int64_t n_chunked = 0, n_traced = 0;
+  std::vector<int32_t> chunk_ring_user(size_t(DF_CHUNK_RING), -1), trace_ring_user(size_t(DF_TRACE_RING), -1);
+  std::vector<std::vector<int32_t>> ring_deps(static_cast<size_t>(n_ops));
+  int BM, BN, BK, slot_doubles;
+  df_gemm_tile_dims(&BM, &BN, &BK, &slot_doubles);
+  for (int32_t i = 0; i < n_ops; ++i) {
+    const PhysOp& op = ops[size_t(i)];
+    if (op.stream == S_NONE) continue;
+    slot[size_t(i)] = n_sync++;
+    if (op.kind != OP_CONTRACT) {
+      target[size_t(i)] = 1;
+      continue;
+    }
+    const Node& n = g.nodes[size_t(op.node)];
+    const void* a = op.loc_a == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.l)] : ctx->arena + op.off_a;
+    const void* b = op.loc_b == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.r)] : ctx->arena + op.off_b;
+    DfOp d{};
+    d.sync_id = slot[size_t(i)];
+    if (n.op == CC_TR_MM) {
+      const int64_t P = df_trace_pieces(Lt, N);
+      d.kind = 1;
+      d.n_items = int32_t(Lt * P);
+      d.first_item = t_items;
+      d.A = a;
+      d.B = b;
+      d.out = ctx->roots + int64_t(g.tree_of_root[size_t(op.node)]) * Lt;
+      d.N = N;
+      d.Lt = Lt;
+      d.nb = int32_t((N + 31) / 32);
+      d.P = int32_t(P);
+      const int64_t r = n_traced % DF_TRACE_RING;
+      char* base = ctx->df_trace_ws + r * ctx->df_trace_slot;
+      d.tr_cnt = reinterpret_cast<int*>(base);
+      d.tr_part = base + round_up(Lt * 4, ALIGN);
+      if (trace_ring_user[size_t(r)] >= 0) ring_deps[size_t(i)].push_back(trace_ring_user[size_t(r)]);
+      trace_ring_user[size_t(r)] = i;
+      ++n_traced;
+      t_items += d.n_items;
+      df_index[size_t(i)] = int32_t(tops.size());
+      tops.push_back(d);
+      tplan.push_back(i);
+    } else {
+      void* out = ctx->arena + op.dev_off;
+      ZgemmProblem p = problem_for(n.op, Lt, N, g.S, a, b, out);
+      int64_t tiles, KT, chunks;
+      df_gemm_geometry(p, tiles, KT, chunks, ctx->num_sms);
+      d.kind = 0;
+      d.n_items = int32_t(tiles * chunks);
+      d.first_item = g_items;
+      d.tiles_m = int32_t((p.M + BM - 1) / BM);
+      d.tiles_n = int32_t((p.Nn + BN - 1) / BN);
+      d.kt_per_o = int32_t((p.Kin + BK - 1) / BK);
+      d.KT = int32_t(KT);
+      d.n_chunks = int32_t(chunks);
+      d.M = p.M;
+      d.Nn = p.Nn;
+      d.ldc = p.ldc;
+      d.sCb = p.sCb;
+      d.C = out;
+      if (chunks > 1) {
+        const int64_t r = n_chunked % DF_CHUNK_RING;
+        char* base = ctx->df_chunk_ws + r * (ctx->df_chunk_slot + ctx->df_chunk_cnt_slot);
+        d.part = base;
+        d.tile_cnt = reinterpret_cast<int*>(base + ctx->df_chunk_slot);
+        if (chunk_ring_user[size_t(r)] >= 0) ring_deps[size_t(i)].push_back(chunk_ring_user[size_t(r)]);
+        chunk_ring_user[size_t(r)] = i;
+        ++n_chunked;
+      }
+      d.tmap = int32_t(tmaps.size() / 256);
+      tmaps.resize(tmaps.size() + 256);
+      if (!df_encode_maps(tmaps.data() + size_t(d.tmap) * 256, p.A, p.B, p.M, p.Nn, p.Kin, p.Ko, p.batch, p.lda,
+                          p.sAo, p.sAb, p.ldb, p.sBo, p.sBb))
+        throw Error(CC_E_CUDA, "TMA descriptor encoding failed");
+      g_items += d.n_items;
+      df_index[size_t(i)] = int32_t(gops.size());
+      gops.push_back(d);
+      gplan.push_back(i);
+    }
+    target[size_t(i)] = d.n_items;
+  }
+  // 3. dependency lists of compute ops, wait lists of copies
+  std::vector<int32_t> dep_slot, dep_target;
+  auto fill_deps = [&](std::vector<DfOp>& v, const std::vector<int32_t>& plan) {
+    for (size_t k = 0; k < v.size(); ++k) {
+      const int32_t i = plan[k];
+      v[k].dep_begin = int32_t(dep_slot.size());
+      std::vector<int32_t> all = deps[size_t(i)];
+      all.insert(all.end(), ring_deps[size_t(i)].begin(), ring_deps[size_t(i)].end());
+      std::sort(all.begin(), all.end());
+      all.erase(std::unique(all.begin(), all.end()), all.end());
+      for (int32_t j : all) {
+        if (slot[size_t(j)] < 0) continue;
+        dep_slot.push_back(slot[size_t(j)]);
+        dep_target.push_back(target[size_t(j)]);
+      }
+      v[k].dep_count = int32_t(dep_slot.size()) - v[k].dep_begin;
+    }
+  };
+  fill_deps(gops, gplan);
+  fill_deps(tops, tplan);
+  ctx->df_copies.clear();
+  std::vector<int32_t> copy_index(static_cast<size_t>(n_ops), -1);
+  for (int32_t i = 0; i < n_ops; ++i) {
+    const PhysOp& op = ops[size_t(i)];
+    if (op.stream != S_H2D && op.stream != S_D2H) continue;
+    const Node& n = g.nodes[size_t(op.node)];
+    cc_ctx::DfCopy c;
+    c.op = i;
+    c.stream = op.stream;
+    c.bytes = size_t(op.bytes);
+    c.flag_slot = slot[size_t(i)];
+    if (op.kind == OP_H2D) {
+      c.dst = ctx->arena + op.dev_off;
+      if (n.leaf()) {
+        const char* h = static_cast<const char*>(ctx->leaf_host[size_t(op.node)]);
+        if (!h) throw Error(CC_E_STATE, "leaf " + std::to_string(n.id) + " has no data (cc_set_leaf)");
+        const int64_t per_t = n.op == CC_LEAF_M ? per_t_m : per_t_m * g.S * g.N;
+        c.src = h + int64_t(ctx->t0) * per_t;
+      } else {
+        c.src = ctx->host_pool + op.host_off;
+      }
+    } else {
+      c.dst = ctx->host_pool + op.host_off;
+      c.src = ctx->arena + op.dev_off;
+    }
+    for (int32_t j : deps[size_t(i)]) {
+      const PhysOp& oj = ops[size_t(j)];
+      if (oj.kind == OP_CONTRACT) {
+        c.wait_values.push_back({slot[size_t(j)], target[size_t(j)]});
+      } else if (oj.stream != op.stream && copy_index[size_t(j)] >= 0) {
+        c.wait_events.push_back(copy_index[size_t(j)]);
+        ctx->df_copies[size_t(copy_index[size_t(j)])].source = true;
+      }
+    }
+    copy_index[size_t(i)] = int32_t(ctx->df_copies.size());
+    ctx->df_copies.push_back(std::move(c));
+  }
+  if (!ctx->df_copies.empty() && (!df_wait_fn() || !df_write_fn()))
+    throw Error(CC_E_CUDA, "stream memory operations (cuStreamWaitValue32) unavailable");
+  ctx->df_events.assign(ctx->df_copies.size(), nullptr);
+  for (size_t k = 0; k < ctx->df_copies.size(); ++k)
+    if (ctx->df_copies[k].source) ck(cudaEventCreateWithFlags(&ctx->df_events[k], cudaEventDisableTiming), "event");
+  // 4. upload metadata: [heads | sync][gops][tops][dep_slot][dep_target][tmaps]
+  const size_t sz_sync = round_up(16 + int64_t(n_sync) * 4, 256);
+  const size_t sz_g = round_up(int64_t(std::max<size_t>(gops.size(), 1) * sizeof(DfOp)), 256);
+  const size_t sz_t = round_up(int64_t(std::max<size_t>(tops.size(), 1) * sizeof(DfOp)), 256);
+  const size_t sz_d = round_up(int64_t(std::max<size_t>(dep_slot.size(), 1) * 4), 256);
+  const size_t sz_m = round_up(int64_t(std::max<size_t>(tmaps.size(), 256)), 256);
+  const size_t total = sz_sync + sz_g + sz_t + 2 * sz_d + sz_m;
+  ck(cudaMalloc(reinterpret_cast<void**>(&ctx->df_meta), total), "dataflow metadata");
+  ctx->df_meta_bytes = total;
+  char* m = ctx->df_meta;
+  unsigned long long* heads = reinterpret_cast<unsigned long long*>(m);
+  ctx->df_sync = reinterpret_cast<int*>(m + 16);
+  ctx->df_sync_bytes = sz_sync;
+  char* pg = m + sz_sync;
+  char* pt = pg + sz_g;
+  char* pds = pt + sz_t;
+  char* pdt = pds + sz_d;
+  char* pm = pdt + sz_d;
+  ck(cudaMemset(m, 0, total), "dataflow metadata");
+  if (!gops.empty()) ck(cudaMemcpy(pg, gops.data(), gops.size() * sizeof(DfOp), cudaMemcpyHostToDevice), "upload");
+  if (!tops.empty()) ck(cudaMemcpy(pt, tops.data(), tops.size() * sizeof(DfOp), cudaMemcpyHostToDevice), "upload");
+  if (!dep_slot.empty()) {
+    ck(cudaMemcpy(pds, dep_slot.data(), dep_slot.size() * 4, cudaMemcpyHostToDevice), "upload");
+    ck(cudaMemcpy(pdt, dep_target.data(), dep_target.size() * 4, cudaMemcpyHostToDevice), "upload");
+  }
+  if (!tmaps.empty()) ck(cudaMemcpy(pm, tmaps.data(), tmaps.size(), cudaMemcpyHostToDevice), "upload");
+  for (DfArgs* a : {&ctx->df_gemm, &ctx->df_trace}) {
+    a->dep_slot = reinterpret_cast<const int32_t*>(pds);
+    a->dep_target = reinterpret_cast<const int32_t*>(pdt);
+    a->tmaps = pm;
+    a->sync = ctx->df_sync;
+  }
+  ctx->df_gemm.q = DfQueue{reinterpret_cast<const DfOp*>(pg), int32_t(gops.size()), g_items, heads};
+  ctx->df_trace.q = DfQueue{reinterpret_cast<const DfOp*>(pt), int32_t(tops.size()), t_items, heads + 1};
+  ctx->df_gemm_items = g_items;
+  ctx->df_trace_items = t_items;
+  if (!ctx->cs2) {
+    ck(cudaStreamCreateWithFlags(&ctx->cs2, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&ctx->ev_cs2, cudaEventDisableTiming), "event");
+  }
+  ctx->df_valid = true;
+}
+
+// Enqueues one dataflow replay; returns the number of kernel launches.
+int issue_dataflow(cc_ctx* ctx) {
+  const Dag& g = *ctx->dag;
+  int nl = 0;
+  ck(cudaMemsetAsync(ctx->df_meta, 0, ctx->df_sync_bytes, ctx->cs), "memset");
+  ck(cudaEventRecord(ctx->ev_start, ctx->cs), "event");
+  ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_start, 0), "wait");
+  ck(cudaStreamWaitEvent(ctx->ds, ctx->ev_start, 0), "wait");
+  ck(cudaStreamWaitEvent(ctx->cs2, ctx->ev_start, 0), "wait");
+  cudaStream_t st[3] = {ctx->cs, ctx->hs, ctx->ds};
+  for (size_t k = 0; k < ctx->df_copies.size(); ++k) {
+    const auto& c = ctx->df_copies[k];
+    cudaStream_t s = st[c.stream];
+    for (int32_t e : c.wait_events) ck(cudaStreamWaitEvent(s, ctx->df_events[size_t(e)], 0), "wait");
+    for (const auto& wv : c.wait_values)
+      if (df_wait_fn()(s, reinterpret_cast<CUdeviceptr>(ctx->df_sync + wv.first), cuuint32_t(wv.second),
+                       CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        throw Error(CC_E_CUDA, "cuStreamWaitValue32 failed");
+    ck(cudaMemcpyAsync(c.dst, c.src, c.bytes, c.stream == S_H2D ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s),
+       "copy");
+    if (df_write_fn()(s, reinterpret_cast<CUdeviceptr>(ctx->df_sync + c.flag_slot), 1, 0) != CUDA_SUCCESS)
+      throw Error(CC_E_CUDA, "cuStreamWriteValue32 failed");
+    if (c.source) ck(cudaEventRecord(ctx->df_events[k], s), "event");
+  }
+  if (ctx->df_gemm_items > 0) {
+    ck(df_launch_gemm(ctx->df_gemm, ctx->num_sms, ctx->cs), "gemm worker");
+    ++nl;
+  }
+  if (ctx->df_trace_items > 0) {
+    ck(df_launch_trace(ctx->df_trace, ctx->num_sms, ctx->cs2), "trace worker");
+    ++nl;
+  }
+  ck(cudaEventRecord(ctx->ev_cs2, ctx->cs2), "event");
+  ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_cs2, 0), "wait");
+  ck(launch_correlate(ctx->roots, ctx->corr, int64_t(g.corr_ids.size()), g.Lt, ctx->term_start, ctx->term_tree,
+                      ctx->term_coef, ctx->cs),
+     "correlate kernel");
+  ++nl;
+  ck(cudaEventRecord(ctx->ev_h_end, ctx->hs), "event");
+  ck(cudaEventRecord(ctx->ev_d_end, ctx->ds), "event");
+  ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_h_end, 0), "wait");
+  ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_d_end, 0), "wait");
+  return nl;
 }
 
 void launch_contract(cc_ctx* ctx, const Node& n, const void* a, const void* b, void* out, int64_t root_slot,
@@ -388,41 +823,121 @@ int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cud
   return nl;
 }
 
+// Replays only the contraction launches of one class (0: MM1/BM1/BB2, 1: TR_MM) of the
+// current plan, in plan order, as a cached CUDA graph; requires a previous full execute
+// (operands are wherever the plan put them; outputs are overwritten).  stats->seconds is
+// the device time of the whole replay, stats->n_kernels the launches of that class.
+void kernel_only(cc_ctx* ctx, int cls, cc_exec_stats* stats) {
+  if (!ctx->executed) throw Error(CC_E_STATE, "kernel-only replay needs a previous full cc_execute");
+  const Dag& g = *ctx->dag;
+  cudaGraphExec_t& gx = ctx->gexec_kind[cls];
+  int nl = 0;
+  double flops = 0, bytes = 0;
+  for (const auto& op : ctx->pp.ops) {
+    if (op.kind != OP_CONTRACT) continue;
+    const Node& n = g.nodes[size_t(op.node)];
+    if ((n.op == CC_TR_MM) != (cls == 1)) continue;
+    ++nl;
+    flops += node_flops(n, g.Lt, g.N, g.S);
+    bytes += node_hbm_bytes(n, g.Lt, g.N, g.S);
+  }
+  if (!gx) {
+    cudaGraph_t graph;
+    ck(cudaStreamBeginCapture(ctx->cs, cudaStreamCaptureModeThreadLocal), "graph capture");
+    int launched = 0;
+    try {
+      for (const auto& op : ctx->pp.ops) {
+        if (op.kind != OP_CONTRACT) continue;
+        const Node& n = g.nodes[size_t(op.node)];
+        if ((n.op == CC_TR_MM) != (cls == 1)) continue;
+        const void* a = op.loc_a == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.l)] : ctx->arena + op.off_a;
+        const void* b = op.loc_b == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.r)] : ctx->arena + op.off_b;
+        if (!a || !b) throw Error(CC_E_STATE, "kernel-only replay: operand without a device address");
+        void* out = op.dev_off >= 0 ? ctx->arena + op.dev_off : nullptr;
+        const int64_t slot = n.type == ROOT ? g.tree_of_root[size_t(op.node)] : -1;
+        launch_contract(ctx, n, a, b, out, slot, &launched);
+      }
+    } catch (...) {
+      cudaStreamEndCapture(ctx->cs, &graph);
+      throw;
+    }
+    ck(cudaStreamEndCapture(ctx->cs, &graph), "graph capture");
+    ck(cudaGraphInstantiate(&gx, graph, 0), "graph instantiate");
+    cudaGraphDestroy(graph);
+  }
+  cudaEvent_t e0, e1;
+  ck(cudaEventCreate(&e0), "event");
+  ck(cudaEventCreate(&e1), "event");
+  ck(cudaEventRecord(e0, ctx->cs), "event");
+  ck(cudaGraphLaunch(gx, ctx->cs), "graph launch");
+  ck(cudaEventRecord(e1, ctx->cs), "event");
+  ck(cudaEventSynchronize(e1), "kernel-only replay");
+  float ms = 0;
+  ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->seconds = ms * 1e-3;
+    stats->flops = flops;
+    stats->hbm_bytes = bytes;
+    stats->n_kernels = nl;
+  }
+}
+
 void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   ctx->need_device();
   if (!ctx->scheduled) throw Error(CC_E_STATE, "cc_execute before cc_schedule");
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
   prepare_phys(ctx);
+  if (flags & 12) {
+    kernel_only(ctx, (flags & 4) ? 0 : 1, stats);
+    return;
+  }
   const bool use_graph = (flags & 1) != 0;
-  const bool time_kernels = (flags & 2) != 0;
+  const bool legacy = (flags & 16) != 0 || (flags & 2) != 0;
+  const bool time_kernels = (flags & 2) != 0 && !use_graph;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;
   std::vector<int> kev_kind;
-  bool own_kev = true;
+  if (!legacy) prepare_dataflow(ctx);
   cudaEvent_t t_begin, t_end;
   ck(cudaEventCreate(&t_begin), "event");
   ck(cudaEventCreate(&t_end), "event");
   ck(cudaEventRecord(t_begin, ctx->cs), "event");
-  if (use_graph) {
-    cudaGraphExec_t& gx = time_kernels ? ctx->gexec_timed : ctx->gexec;
-    if (!gx) {
+  if (!legacy) {
+    if (use_graph && ctx->df_copies.empty()) {
+      if (!ctx->gexec_df) {
+        cudaGraph_t graph;
+        ck(cudaStreamBeginCapture(ctx->cs, cudaStreamCaptureModeThreadLocal), "graph capture");
+        try {
+          ctx->last_n_kernels = issue_dataflow(ctx);
+        } catch (...) {
+          cudaStreamEndCapture(ctx->cs, &graph);
+          throw;
+        }
+        ck(cudaStreamEndCapture(ctx->cs, &graph), "graph capture");
+        ck(cudaGraphInstantiate(&ctx->gexec_df, graph, 0), "graph instantiate");
+        cudaGraphDestroy(graph);
+      }
+      ck(cudaGraphLaunch(ctx->gexec_df, ctx->cs), "graph launch");
+    } else {
+      ctx->last_n_kernels = issue_dataflow(ctx);
+    }
+  } else if (use_graph) {
+    if (!ctx->gexec) {
       cudaGraph_t graph;
       ck(cudaStreamBeginCapture(ctx->cs, cudaStreamCaptureModeThreadLocal), "graph capture");
       try {
-        ctx->last_n_kernels = issue(ctx, time_kernels, &ctx->timed_ev, &ctx->timed_kind);
+        ctx->last_n_kernels = issue(ctx, false, nullptr, nullptr);
       } catch (...) {
         cudaStreamEndCapture(ctx->cs, &graph);
         throw;
       }
       ck(cudaStreamEndCapture(ctx->cs, &graph), "graph capture");
-      ck(cudaGraphInstantiate(&gx, graph, 0), "graph instantiate");
+      ck(cudaGraphInstantiate(&ctx->gexec, graph, 0), "graph instantiate");
       cudaGraphDestroy(graph);
     }
-    ck(cudaGraphLaunch(gx, ctx->cs), "graph launch");
-    if (time_kernels) {
-      kev = ctx->timed_ev;
-      kev_kind = ctx->timed_kind;
-      own_kev = false;
-    }
+    ck(cudaGraphLaunch(ctx->gexec, ctx->cs), "graph launch");
   } else {
     ctx->last_n_kernels = issue(ctx, time_kernels, &kev, &kev_kind);
   }
@@ -455,10 +970,8 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
     if (blocking) cudaEventElapsedTime(&ms, kev[i].first, kev[i].second);
     ctx->ktimes.seconds[kev_kind[i]] += ms * 1e-3;
     ctx->ktimes.count[kev_kind[i]] += 1;
-    if (own_kev) {
-      cudaEventDestroy(kev[i].first);
-      cudaEventDestroy(kev[i].second);
-    }
+    cudaEventDestroy(kev[i].first);
+    cudaEventDestroy(kev[i].second);
   }
   if (stats) {
     double ks = 0;

@@ -1,0 +1,139 @@
+// Device helpers shared by the contraction kernels (sm_100a): mbarrier, TMA, FP64 DMMA,
+// acquire/release, the DMMA tile configuration and the complex DMMA k-tile step.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace cc {
+namespace dev {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double neg(double x) {
+  return __longlong_as_double(__double_as_longlong(x) ^ static_cast<long long>(0x8000000000000000ULL));
+}
+
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int NCW = WARPS_M * WARPS_N;  // consumer (DMMA) warps
+  static constexpr int THREADS = (NCW + 1) * 32;
+  static constexpr int MI = WM / 8, NI = WN / 4;
+  static constexpr int FRAG = MI * NI * 2;       // accumulator doubles per lane
+  static constexpr int A_BYTES = BM * BK * 16, B_BYTES = BK * BN * 16;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+  static constexpr int SLOT_DOUBLES = NCW * FRAG * 32;
+  static_assert(BK % 8 == 0 && BN % 8 == 0 && BM % 8 == 0, "tile dims");
+  static_assert(WM % 8 == 0 && WN % 4 == 0, "warp tile dims");
+  static_assert((BM * 128) % 1024 == 0 && (BK * 128) % 1024 == 0, "128B swizzle needs 1024B-aligned sub-tiles");
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+
+// One k-tile (BK complex) of a warp's WM x WN complex accumulator block from the stage's
+// swizzled shared-memory tiles (see zgemm.cu header for the fragment mapping).
+template <class C>
+__device__ __forceinline__ void dmma_ktile(const uint8_t* sA, const uint8_t* sB, const int (&a_row_off)[C::MI],
+                                           const int (&a_key)[C::MI], const int (&b_col_off)[C::NI],
+                                           const int (&b_slot)[C::NI], int t, bool q,
+                                           double (&acc)[C::MI][C::NI][2]) {
+#pragma unroll
+  for (int kc = 0; kc < C::BK / 8; ++kc) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int s = 2 * t + h;       // complex k slot within the 8-complex chunk
+      const int krow = kc * 8 + s;   // B row within the stage
+      double2 a[C::MI];
+      double b_re_row[C::NI], b_im_row[C::NI];
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+        a[i] = *reinterpret_cast<const double2*>(sA + kc * C::BM * 128 + a_row_off[i] + ((s ^ a_key[i]) << 4));
+#pragma unroll
+      for (int k = 0; k < C::NI; ++k) {
+        const double2 bv =
+            *reinterpret_cast<const double2*>(sB + b_col_off[k] + krow * 128 + ((b_slot[k] ^ (krow & 7)) << 4));
+        // B' = [[br, bi], [-bi, br]]: row (k, re) -> (br | bi), row (k, im) -> (-bi | br)
+        b_re_row[k] = q ? bv.y : bv.x;
+        b_im_row[k] = q ? bv.x : neg(bv.y);
+      }
+      // two sweeps: dependent DMMAs on one accumulator are MI*NI instructions apart
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int k = 0; k < C::NI; ++k) dmma(acc[i][k][0], acc[i][k][1], a[i].x, b_re_row[k]);
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int k = 0; k < C::NI; ++k) dmma(acc[i][k][0], acc[i][k][1], a[i].y, b_im_row[k]);
+    }
+  }
+}
+
+// Per-lane fragment offsets of a consumer warp (wm, wn) within a stage.
+template <class C>
+__device__ __forceinline__ void frag_offsets(int wm, int wn, int g, int (&a_row_off)[C::MI], int (&a_key)[C::MI],
+                                             int (&b_col_off)[C::NI], int (&b_slot)[C::NI]) {
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i) {
+    const int r = wm * C::WM + i * 8 + g;
+    a_row_off[i] = r * 128;
+    a_key[i] = r & 7;
+  }
+#pragma unroll
+  for (int k = 0; k < C::NI; ++k) {
+    const int n = wn * C::WN + k * 4 + (g >> 1);
+    b_col_off[k] = (n >> 3) * C::BK * 128;
+    b_slot[k] = n & 7;
+  }
+}
+
+using Big = Cfg<64, 64, 16, 32, 16, 4>;
+
+}  // namespace dev
+}  // namespace cc

@@ -1,0 +1,349 @@
+// Persistent dataflow workers for a whole plan (see dataflow.hpp for the protocol).
+//
+// gemm_worker: one CTA per SM, 8 DMMA warps (warp tile 32 rows x 16 complex, CTA tile
+//   64 x 64 complex); thread 0 also drives the TMA ring (prefetch distance STAGES-1 k-tiles,
+//   refilled as soon as every warp released the previous stage).  An item is one output
+//   tile, or one k-chunk of a tile for ops with few tiles (BB2); the CTA that completes the
+//   last chunk of a tile (ticket) sums the chunk partials in chunk order — deterministic.
+//   Register cap 192 so a trace-worker CTA fits on the same SM.
+// trace_worker: 256 threads, <= 64 registers, streams its (t, piece) unit range with L2-only
+//   loads (.cg: operands were written by other SMs during this launch), fixed-order
+//   reductions, last-piece finisher per time slice.
+// Both publish completion with per-thread fences, a CTA barrier and one atomic increment
+// of the op's done counter; waiters spin with ld.acquire.gpu and issue a proxy fence
+// before TMA reads data other SMs wrote with ordinary stores.
+#include "common.cuh"
+#include "dataflow.hpp"
+#include "kernels.hpp"
+
+namespace cc {
+namespace {
+using namespace dev;
+
+using GC = Cfg<64, 64, 16, 32, 16, 4>;   // same tile math as zgemm; consumers = all 8 warps
+constexpr int GW_THREADS = GC::NCW * 32;  // 256: no dedicated producer warp
+constexpr int TR_TB = 32;
+constexpr int TR_THREADS = 256;
+
+__device__ __forceinline__ void tma_load_4d_g(void* dst, const void* map, uint64_t* bar, int c0, int c1, int c2,
+                                              int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__device__ __forceinline__ int find_op(const DfQueue& q, int64_t item) {
+  int lo = 0, hi = q.n_ops - 1;
+  while (lo < hi) {  // last op with first_item <= item
+    const int mid = (lo + hi + 1) >> 1;
+    if (q.ops[mid].first_item <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void wait_deps(const DfArgs& a, const DfOp& op) {
+  for (int d = 0; d < op.dep_count; ++d) {
+    const int* slot = a.sync + a.dep_slot[op.dep_begin + d];
+    const int target = a.dep_target[op.dep_begin + d];
+    while (ld_acquire(slot) < target) __nanosleep(64);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+__global__ void __maxnreg__(192) gemm_worker(DfArgs a) {
+  using C = GC;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  __shared__ int64_t s_item;
+  __shared__ int s_fin;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
+  const int g = lane >> 2, t = lane & 3;
+  const bool q = (g & 1) != 0;
+  int a_row_off[C::MI], a_key[C::MI], b_col_off[C::NI], b_slot[C::NI];
+  frag_offsets<C>(wm, wn, g, a_row_off, a_key, b_col_off, b_slot);
+
+  uint32_t ring = 0;  // k-tiles consumed so far by this CTA (identical in every thread)
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(a.q.head, 1ull);
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= a.q.n_items) break;
+    const DfOp& op = a.q.ops[find_op(a.q, item)];
+    if (tid == 0) {
+      wait_deps(a, op);
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int64_t local = item - op.first_item;
+    const int64_t tile = local / op.n_chunks;
+    const int chunk = int(local - tile * op.n_chunks);
+    const int k0 = int((int64_t(chunk) * op.KT) / op.n_chunks);
+    const int k1 = int((int64_t(chunk + 1) * op.KT) / op.n_chunks);
+    const int64_t tiles_mn = int64_t(op.tiles_m) * op.tiles_n;
+    const int64_t b = tile / tiles_mn;
+    const int64_t rr = tile - b * tiles_mn;
+    const int tn = int(rr / op.tiles_m), tm = int(rr - int64_t(tn) * op.tiles_m);
+    const void* tA = static_cast<const uint8_t*>(a.tmaps) + size_t(2 * op.tmap) * 128;
+    const void* tB = static_cast<const uint8_t*>(a.tmaps) + size_t(2 * op.tmap + 1) * 128;
+    const int nk = k1 - k0;
+
+    auto issue = [&](uint32_t r, int k) {
+      const int st = int(r % C::STAGES);
+      const uint32_t ph = (r / C::STAGES) & 1u;
+      mbar_wait(&empty[st], ph ^ 1u);
+      mbar_expect_tx(&full[st], C::STAGE_BYTES);
+      uint8_t* sA = smem + st * C::STAGE_BYTES;
+      uint8_t* sB = sA + C::A_BYTES;
+      const int ko = k / op.kt_per_o;
+      const int ki0 = (k - ko * op.kt_per_o) * C::BK;
+#pragma unroll
+      for (int kc = 0; kc < C::BK / 8; ++kc)
+        tma_load_4d_g(sA + kc * C::BM * 128, tA, &full[st], 2 * (ki0 + kc * 8), tm * C::BM, ko, int(b));
+#pragma unroll
+      for (int nc = 0; nc < C::BN / 8; ++nc)
+        tma_load_4d_g(sB + nc * C::BK * 128, tB, &full[st], 2 * (tn * C::BN + nc * 8), ki0, ko, int(b));
+    };
+    if (tid == 0) {
+      const int pre = nk < C::STAGES - 1 ? nk : C::STAGES - 1;
+      for (int j = 0; j < pre; ++j) issue(ring + j, k0 + j);
+    }
+
+    double acc[C::MI][C::NI][2];
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int k = 0; k < C::NI; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
+    for (int i = 0; i < nk; ++i) {
+      if (tid == 0 && i + C::STAGES - 1 < nk) issue(ring + i + C::STAGES - 1, k0 + i + C::STAGES - 1);
+      const uint32_t r = ring + i;
+      const int st = int(r % C::STAGES);
+      mbar_wait(&full[st], (r / C::STAGES) & 1u);
+      const uint8_t* sA = smem + st * C::STAGE_BYTES;
+      dmma_ktile<C>(sA, sA + C::A_BYTES, a_row_off, a_key, b_col_off, b_slot, t, q, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    ring += nk;
+
+    double2* out = static_cast<double2*>(op.C) + b * op.sCb;
+    bool store = true;
+    if (op.n_chunks > 1) {
+      // publish this chunk's partial, then the last chunk of the tile sums all of them
+      double* base = static_cast<double*>(op.part) + (tile * op.n_chunks) * int64_t(C::SLOT_DOUBLES);
+      double* mine = base + int64_t(chunk) * C::SLOT_DOUBLES + warp * (C::FRAG * 32);
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int k = 0; k < C::NI; ++k) {
+          __stcg(mine + ((i * C::NI + k) * 2 + 0) * 32 + lane, acc[i][k][0]);
+          __stcg(mine + ((i * C::NI + k) * 2 + 1) * 32 + lane, acc[i][k][1]);
+        }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        const int old = atomicAdd(&op.tile_cnt[tile], 1);
+        s_fin = (old == op.n_chunks - 1);
+        if (s_fin) op.tile_cnt[tile] = 0;
+      }
+      __syncthreads();
+      store = s_fin != 0;
+      if (store) {
+        __threadfence();
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int k = 0; k < C::NI; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
+        for (int c = 0; c < op.n_chunks; ++c) {
+          const double* src = base + int64_t(c) * C::SLOT_DOUBLES + warp * (C::FRAG * 32);
+#pragma unroll
+          for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+            for (int k = 0; k < C::NI; ++k) {
+              acc[i][k][0] += __ldcg(src + ((i * C::NI + k) * 2 + 0) * 32 + lane);
+              acc[i][k][1] += __ldcg(src + ((i * C::NI + k) * 2 + 1) * 32 + lane);
+            }
+        }
+      }
+    }
+    if (store) {
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i) {
+        const int64_t row = int64_t(tm) * C::BM + wm * C::WM + i * 8 + g;
+        if (row >= op.M) continue;
+#pragma unroll
+        for (int k = 0; k < C::NI; ++k) {
+          const int64_t col = int64_t(tn) * C::BN + wn * C::WN + k * 4 + t;
+          if (col < op.Nn) out[row * op.ldc + col] = make_double2(acc[i][k][0], acc[i][k][1]);
+        }
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(a.sync + op.sync_id, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ double2 cmul_acc(double2 acc, double2 x, double2 y) {
+  acc.x = fma(x.x, y.x, acc.x);
+  acc.x = fma(-x.y, y.y, acc.x);
+  acc.y = fma(x.x, y.y, acc.y);
+  acc.y = fma(x.y, y.x, acc.y);
+  return acc;
+}
+
+__global__ void __launch_bounds__(TR_THREADS, 4) trace_worker(DfArgs a) {
+  __shared__ double2 sB[TR_TB][TR_TB + 1];
+  __shared__ double2 red[TR_THREADS / 32];
+  __shared__ int64_t s_item;
+  __shared__ int s_last;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(a.q.head, 1ull);
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= a.q.n_items) break;
+    const DfOp& op = a.q.ops[find_op(a.q, item)];
+    if (tid == 0) wait_deps(a, op);
+    __syncthreads();
+    const int64_t local = item - op.first_item;
+    const int t = int(local / op.P), p = int(local - int64_t(t) * op.P);
+    const int U = op.nb * op.nb;
+    const int u0 = int((int64_t(p) * U) / op.P), u1 = int((int64_t(p + 1) * U) / op.P);
+    const int64_t N = op.N;
+    const double2* At = static_cast<const double2*>(op.A) + int64_t(t) * N * N;
+    const double2* Bt = static_cast<const double2*>(op.B) + int64_t(t) * N * N;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int u = u0; u < u1; ++u) {
+      const int I = u / op.nb, J = u - I * op.nb;
+      const int64_t i0 = int64_t(I) * TR_TB, j0 = int64_t(J) * TR_TB;
+      double2 av[TR_TB / 8], bv[TR_TB / 8];
+#pragma unroll
+      for (int q = 0; q < TR_TB / 8; ++q) {
+        const int r = warp + q * 8;
+        const int64_t ia = i0 + r, ja = j0 + lane, jb = j0 + r, ib = i0 + lane;
+        av[q] = (ia < N && ja < N) ? __ldcg(At + ia * N + ja) : make_double2(0.0, 0.0);
+        bv[q] = (jb < N && ib < N) ? __ldcg(Bt + jb * N + ib) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < TR_TB / 8; ++q) sB[warp + q * 8][lane] = bv[q];
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < TR_TB / 8; ++q) acc = cmul_acc(acc, av[q], sB[lane][warp + q * 8]);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    double2* outp = static_cast<double2*>(op.out);
+    if (tid == 0) {
+      double2 s = red[0];
+      for (int w = 1; w < TR_THREADS / 32; ++w) {
+        s.x += red[w].x;
+        s.y += red[w].y;
+      }
+      if (op.P == 1) {
+        outp[t] = s;
+        s_last = 0;
+      } else {
+        static_cast<double2*>(op.tr_part)[int64_t(t) * op.P + p] = s;
+        __threadfence();
+        const int ticket = atomicAdd(&op.tr_cnt[t], 1);
+        s_last = (ticket == op.P - 1);
+      }
+    }
+    __syncthreads();
+    if (s_last && warp == 0) {
+      __threadfence();
+      const double* pp = static_cast<const double*>(op.tr_part) + 2 * int64_t(t) * op.P;
+      double sx = 0.0, sy = 0.0;
+      for (int k = lane; k < op.P; k += 32) {
+        sx += __ldcg(pp + 2 * k);
+        sy += __ldcg(pp + 2 * k + 1);
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      }
+      if (lane == 0) {
+        outp[t] = make_double2(sx, sy);
+        op.tr_cnt[t] = 0;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(a.sync + op.sync_id, 1);
+  }
+}
+
+}  // namespace
+
+size_t df_gemm_smem_bytes() { return size_t(GC::SMEM); }
+
+void df_gemm_tile_dims(int* BM, int* BN, int* BK, int* slot_doubles) {
+  *BM = GC::BM;
+  *BN = GC::BN;
+  *BK = GC::BK;
+  *slot_doubles = GC::SLOT_DOUBLES;
+}
+
+int df_trace_block() { return TR_TB; }
+
+cudaError_t df_launch_gemm(const DfArgs& a, int grid, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_worker, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  gemm_worker<<<grid, GW_THREADS, GC::SMEM, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t df_launch_trace(const DfArgs& a, int grid, cudaStream_t s) {
+  trace_worker<<<grid, TR_THREADS, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+bool df_encode_maps(void* dst, const void* A, const void* B, int64_t M, int64_t Nn, int64_t Kin, int64_t Ko,
+                    int64_t batch, int64_t lda, int64_t sAo, int64_t sAb, int64_t ldb, int64_t sBo, int64_t sBb) {
+  ZgemmProblem p{};
+  p.A = A;
+  p.B = B;
+  p.M = M;
+  p.Nn = Nn;
+  p.Kin = Kin;
+  p.Ko = Ko;
+  p.batch = batch;
+  p.lda = lda;
+  p.sAo = sAo;
+  p.sAb = sAb;
+  p.ldb = ldb;
+  p.sBo = sBo;
+  p.sBb = sBb;
+  return encode_zgemm_maps(dst, static_cast<uint8_t*>(dst) + 128, p, GC::BM, GC::BK);
+}
+
+}  // namespace cc

@@ -1,0 +1,68 @@
+// Dataflow execution of a whole plan by persistent worker kernels (host/device shared PODs).
+//
+// The plan's contractions become work items in two queues, in plan order: GEMM tiles
+// (MM1/BM1/BB2; a tile may be split into k-chunks) for the DMMA worker, and TR_MM unit
+// ranges for the trace worker.  Both workers are persistent (one CTA per SM each, sized to
+// be co-resident on an SM), grab items with an atomic queue head, and before an item spin
+// on the integer sync slots of the items' op dependencies: done counters of earlier ops
+// (RAW on operands, WAR/WAW on reused pool memory) and completion flags written by the copy
+// streams after an H2D (cuStreamWriteValue32).  Items only ever wait on earlier plan
+// positions and every queue is dispatched in order, so the earliest unfinished item always
+// has its dependencies satisfied: the execution cannot deadlock.
+#pragma once
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace cc {
+
+struct DfOp {
+  int32_t kind;           // 0 GEMM, 1 TRACE
+  int32_t n_items;
+  int64_t first_item;     // index of the op's first item in its queue
+  int32_t sync_id;        // done counter (sync[sync_id] reaches n_items)
+  int32_t dep_begin, dep_count;
+  // GEMM: C[b][m][n] = sum_k A[b][m][k] B[b][k][n] (zgemm semantics, kernels.hpp)
+  int32_t tmap;           // tensor maps 2*tmap (A) and 2*tmap+1 (B)
+  int32_t tiles_m, tiles_n, kt_per_o, KT, n_chunks;
+  int64_t M, Nn, ldc, sCb;
+  void* C;
+  void* part;             // chunked: partial tiles [tile][chunk][slot]
+  int* tile_cnt;          // chunked: per-tile finished-chunk counters (reset by the finisher)
+  // TRACE: out[t] = sum_{i,j} A[t,i,j] B[t,j,i]
+  const void* A;
+  const void* B;
+  void* out;
+  int64_t N, Lt;
+  int32_t nb, P;          // 32x32 blocks per row; items (pieces) per time slice
+  void* tr_part;          // [Lt][P] complex partials
+  int* tr_cnt;            // [Lt] tickets (reset by the finisher)
+};
+
+struct DfQueue {
+  const DfOp* ops;
+  int32_t n_ops;
+  int64_t n_items;
+  unsigned long long* head;  // atomic queue head (zeroed per launch)
+};
+
+struct DfArgs {
+  DfQueue q;
+  const int32_t* dep_slot;    // sync slot an op waits on
+  const int32_t* dep_target;  // value the slot must reach
+  const void* tmaps;          // CUtensorMap array (64-byte aligned, global memory)
+  int* sync;                  // done counters + copy flags (zeroed per launch)
+};
+
+// Launch the persistent workers (stream-ordered; the sync area must be zero).
+size_t df_gemm_smem_bytes();
+cudaError_t df_launch_gemm(const DfArgs& a, int grid, cudaStream_t s);
+cudaError_t df_launch_trace(const DfArgs& a, int grid, cudaStream_t s);
+// Tile / chunk geometry the builder needs (matches the worker's Cfg).
+void df_gemm_tile_dims(int* BM, int* BN, int* BK, int* slot_doubles);
+int df_trace_block();
+// Encode the TMA maps of one GEMM problem into dst[0] (A) and dst[1] (B).
+bool df_encode_maps(void* dst, const void* A, const void* B, int64_t M, int64_t Nn, int64_t Kin, int64_t Ko,
+                    int64_t batch, int64_t lda, int64_t sAo, int64_t sAb, int64_t ldb, int64_t sBo, int64_t sBb);
+
+}  // namespace cc

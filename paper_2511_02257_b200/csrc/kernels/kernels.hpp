@@ -21,6 +21,10 @@ struct ZgemmProblem {
   int64_t ldc, sCb;
 };
 
+// TMA maps (CUtensorMap, 128 B each) of a problem's A and B for a BM x BK / BK x 8 box
+// with 128-byte swizzle, as the DMMA kernels read them.
+bool encode_zgemm_maps(void* mapA, void* mapB, const ZgemmProblem& p, int BM, int BK);
+
 // Workspace bytes a problem needs for its deterministic split-K partials.
 size_t zgemm_workspace_bytes(const ZgemmProblem& p, int num_sms);
 cudaError_t launch_zgemm(const ZgemmProblem& p, void* workspace, size_t ws_bytes, int num_sms,

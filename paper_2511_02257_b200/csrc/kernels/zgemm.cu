@@ -31,50 +31,12 @@
 #include <cstdio>
 #include <mutex>
 
+#include "common.cuh"
 #include "kernels.hpp"
 
 namespace cc {
 namespace {
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
-                                            int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-      : "+d"(c0), "+d"(c1)
-      : "d"(a), "d"(b));
-}
-__device__ __forceinline__ double neg(double x) {
-  return __longlong_as_double(__double_as_longlong(x) ^ static_cast<long long>(0x8000000000000000ULL));
-}
+using namespace dev;
 
 struct KArgs {
   double2* C;
@@ -83,23 +45,6 @@ struct KArgs {
   int64_t M, Nn, ldc, sCb;
   int64_t total;        // n_tiles * KT
   int32_t tiles_m, tiles_n, kt_per_o, KT, G;
-};
-
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
-struct Cfg {
-  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
-  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
-  static constexpr int NCW = WARPS_M * WARPS_N;  // consumer (DMMA) warps
-  static constexpr int THREADS = (NCW + 1) * 32;
-  static constexpr int MI = WM / 8, NI = WN / 4;
-  static constexpr int FRAG = MI * NI * 2;       // accumulator doubles per lane
-  static constexpr int A_BYTES = BM * BK * 16, B_BYTES = BK * BN * 16;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
-  static constexpr int SLOT_DOUBLES = NCW * FRAG * 32;
-  static_assert(BK % 8 == 0 && BN % 8 == 0 && BM % 8 == 0, "tile dims");
-  static_assert(WM % 8 == 0 && WN % 4 == 0, "warp tile dims");
-  static_assert((BM * 128) % 1024 == 0 && (BK * 128) % 1024 == 0, "128B swizzle needs 1024B-aligned sub-tiles");
 };
 
 // The k-iteration range of CTA c and its segments (one per tile touched), in processing
@@ -123,15 +68,6 @@ struct Range {
 };
 
 __device__ __forceinline__ int64_t range_start(int64_t c, const KArgs& a) { return (c * a.total) / a.G; }
-
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, 1)
@@ -347,7 +283,6 @@ bool make_map(CUtensorMap* map, const void* base, const uint64_t dims[4], const 
   return r == CUDA_SUCCESS;
 }
 
-using Big = Cfg<64, 64, 16, 32, 16, 4>;
 
 template <class C>
 void geometry(const ZgemmProblem& p, int num_sms, int& tiles_m, int& tiles_n, int& kt_per_o, int64_t& total,
@@ -413,6 +348,17 @@ cudaError_t launch_cfg(const ZgemmProblem& p, void* ws, size_t ws_size, int num_
 }
 
 }  // namespace
+
+bool encode_zgemm_maps(void* mapA, void* mapB, const ZgemmProblem& p, int BM, int BK) {
+  const uint64_t sAo = p.Ko > 1 ? p.sAo : p.lda * p.M;
+  const uint64_t sBo = p.Ko > 1 ? p.sBo : p.ldb * p.Kin;
+  const uint64_t da[4] = {uint64_t(2 * p.Kin), uint64_t(p.M), uint64_t(p.Ko), uint64_t(p.batch)};
+  const uint64_t sa[3] = {uint64_t(p.lda) * 16, sAo * 16, uint64_t(p.batch > 1 ? p.sAb : sAo * p.Ko) * 16};
+  const uint64_t db[4] = {uint64_t(2 * p.Nn), uint64_t(p.Kin), uint64_t(p.Ko), uint64_t(p.batch)};
+  const uint64_t sb[3] = {uint64_t(p.ldb) * 16, sBo * 16, uint64_t(p.batch > 1 ? p.sBb : sBo * p.Ko) * 16};
+  return make_map(static_cast<CUtensorMap*>(mapA), p.A, da, sa, uint32_t(BM)) &&
+         make_map(static_cast<CUtensorMap*>(mapB), p.B, db, sb, uint32_t(BK));
+}
 
 size_t zgemm_workspace_bytes(const ZgemmProblem& p, int num_sms) { return ws_bytes<Big>(p, num_sms); }
 

@@ -55,6 +55,8 @@ def run_gpu(w, algo=None, cap=0, flags=0, device_leaves=False, arena_mb=256, lea
             keep.append(h)
             ctx.set_leaf(u, h)
     ex = ctx.execute(flags)
+    if flags & 1:
+        ex = ctx.execute(flags)     # a graph replay after the capturing run
     ctx._leaf_buffers = keep
     trees = ctx.part_trees()
     roots = {t: ctx.root_value(t, Lt_part) for t in trees}

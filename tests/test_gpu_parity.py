@@ -134,8 +134,10 @@ def test_c1_synthetic():
     assert ex["h2d_bytes"] == 4 * 16 * w.Lt * w.N ** 2
 
 
-@pytest.mark.parametrize("flags", [0, 1, 2])
+@pytest.mark.parametrize("flags", [0, 1, 2, 16, 17])
 def test_c2_small_all_modes(flags):
+    """flags 0/1: dataflow workers (stream / CUDA graph); 2: op-by-op with per-kernel
+    timing; 16/17: op-by-op launches (stream / graph)."""
     w = dags.config_c2(N=40, Lt=3, n_loop4=80, n_loop2=6, n_corr=4)
     dag = Dag(w)
     r_or, c_or = values.run_workload(w, dag)
@@ -154,16 +156,20 @@ def test_schedule_and_mode_invariance_bitwise():
         other = run_gpu(w, **kw)[1]
         for t in base:
             assert np.array_equal(base[t], other[t]), kw
+    # the op-by-op path (stream-K kernels) sums in another order: equal within tolerance
+    legacy = run_gpu(w, flags=16)[1]
+    assert_roots_close(legacy, base, rel=1e-13)
 
 
 def test_c3_nucleon_small():
-    for (N, Lt, S) in ((8, 2, 4), (12, 2, 64)):
+    for (N, Lt, S) in ((8, 2, 4), (12, 2, 64), (20, 1, 64)):
         w = dags.config_c3(N=N, Lt=Lt, S=S)
         dag = Dag(w)
         r_or, c_or = values.run_workload(w, dag)
-        _, roots, corr, st, ex = run_gpu(w)
-        assert_roots_close(roots, r_or)
-        assert_corr_close(dag, r_or, corr, c_or)
+        for flags in (0, 16):
+            _, roots, corr, st, ex = run_gpu(w, flags=flags)
+            assert_roots_close(roots, r_or)
+            assert_corr_close(dag, r_or, corr, c_or)
 
 
 def test_c4_evictions_under_cap():
@@ -177,7 +183,7 @@ def test_c4_evictions_under_cap():
     p = lru.plan(dag, order, cap)
     assert p["evictions"] > 0 and p["d2h_count"] > 0
     r_or, c_or = values.run_workload(w, dag)
-    for flags in (0, 1):
+    for flags in (0, 1, 16):
         _, roots, corr, st, ex = run_gpu(w, cap=cap, flags=flags)
         assert st["evictions"] == p["evictions"] and st["h2d_bytes"] == p["h2d_bytes"]
         assert ex["d2h_bytes"] == p["d2h_bytes"] and ex["h2d_bytes"] == p["h2d_bytes"]
