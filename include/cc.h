@@ -170,7 +170,10 @@ cc_status cc_set_leaf_device(cc_ctx* ctx, int64_t leaf_id, const void* dev, size
  * with bit 0).  bit 2 / bit 3: kernel-only replay of the plan's GEMM-kind (MM1/BM1/BB2) /
  * TR_MM launches alone, in plan order, as a cached graph, after a full execute: stats->seconds
  * = device time of the replay, n_kernels = launches, flops/hbm_bytes = their algorithmic work
- * (average launch duration for the roofline, without host launch overhead). */
+ * (average launch duration for the roofline, without host launch overhead).  The default
+ * executor is the dataflow one (persistent DMMA-tile and trace workers, kernels/dataflow.hpp);
+ * bit 4 selects op-by-op launches instead; bit 5 records the per-item timeline
+ * (cc_dataflow_profile). */
 cc_status cc_execute(cc_ctx* ctx, int32_t flags, cc_exec_stats* stats);
 /* Enqueue-only variant (no host sync): work is ordered on the compute stream. */
 cc_status cc_execute_async(cc_ctx* ctx, int32_t flags);
@@ -178,6 +181,17 @@ cc_status cc_execute_async(cc_ctx* ctx, int32_t flags);
 /* Per-kind contraction-kernel time of the last cc_execute with flags bit 1 (kernels timed
  * with CUDA events on the compute stream): seconds[op], counts[op] for op = cc_op (8 each). */
 cc_status cc_kernel_times(cc_ctx* ctx, double* seconds, int64_t* counts);
+
+/* Progress of the dataflow executor (diagnostics; readable while a replay runs): out[0], out[1]
+ * = items taken from the GEMM / TR queues, out[2..] = the sync slots (done counters of the
+ * plan's contractions and copy-completion flags, in plan order). */
+cc_status cc_dataflow_state(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out);
+
+/* Per-item timeline of the last cc_execute with flags bit 5 (dataflow profiling): for every
+ * work item (GEMM queue first, then TR queue) 8 uint64: dispatch, dependencies-ready and end
+ * times (%globaltimer, ns), the SM id, and for GEMM items the first-operand-arrival and
+ * end-of-k-loop times.  out may be NULL (size query: 8*(n_gemm+n_trace)). */
+cc_status cc_dataflow_profile(cc_ctx* ctx, uint64_t* out, int64_t cap, int64_t* n_gemm, int64_t* n_trace);
 
 /* Results.  out: 2*Lt_part doubles (interleaved complex) for the current part. */
 cc_status cc_correlator(cc_ctx* ctx, int64_t corr_id, double* out, int32_t Lt);

@@ -23,7 +23,7 @@ P = ctypes.POINTER
 CC_LEAF_M, CC_LEAF_B, CC_MM1, CC_BM1, CC_BB2, CC_TR_MM, CC_LEAF_X, CC_OP_X = range(8)
 CC_SIBLING, CC_TREE, CC_GIVEN = range(3)
 PART_TIME, PART_TREES = 0, 1
-EXEC_GRAPH, EXEC_TIME_KERNELS, EXEC_ONLY_GEMM, EXEC_ONLY_TRACE = 1, 2, 4, 8
+EXEC_GRAPH, EXEC_TIME_KERNELS, EXEC_ONLY_GEMM, EXEC_ONLY_TRACE, EXEC_OP_BY_OP, EXEC_PROFILE = 1, 2, 4, 8, 16, 32
 STATUS = {0: "OK", -1: "INVAL", -2: "PARSE", -3: "CYCLE", -4: "INCONSISTENT", -5: "MULTIROOT",
           -6: "UNKNOWN_NODE", -7: "NOT_CLOSED", -8: "INFEASIBLE", -9: "STATE", -10: "BUFFER_TOO_SMALL",
           -11: "CUDA", -12: "NOMEM"}
@@ -98,6 +98,8 @@ _sig("cc_set_leaf_device", c_void_p, c_i64, c_void_p, c_size_t)
 _sig("cc_execute", c_void_p, c_i32, P(cc_exec_stats))
 _sig("cc_execute_async", c_void_p, c_i32)
 _sig("cc_kernel_times", c_void_p, P(c_dbl), P(c_i64))
+_sig("cc_dataflow_state", c_void_p, P(c_i64), c_i64, P(c_i64))
+_sig("cc_dataflow_profile", c_void_p, P(c_u64), c_i64, P(c_i64), P(c_i64))
 _sig("cc_correlator", c_void_p, c_i64, P(c_dbl), c_i32)
 _sig("cc_root_value", c_void_p, c_i64, P(c_dbl), c_i32)
 _sig("cc_correlator_device_ptr", c_void_p, P(c_void_p), P(c_i64), P(c_i64))
@@ -111,7 +113,7 @@ _sig("cc_scratch_bytes", c_i32, c_i32, c_i32, res=c_size_t)
 EXPORTED = ["cc_create", "cc_destroy", "cc_last_error", "cc_version", "cc_load_dag", "cc_load_dag_file",
             "cc_dag_info", "cc_partition", "cc_part_trees", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
             "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_execute",
-            "cc_execute_async", "cc_kernel_times", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
+            "cc_execute_async", "cc_kernel_times", "cc_dataflow_state", "cc_dataflow_profile", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
             "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_fill_synthetic", "cc_scratch_bytes"]
 
 
@@ -279,6 +281,24 @@ class Context:
         c = (c_i64 * 8)()
         self._ck(_lib.cc_kernel_times(self._h, s, c))
         return list(s), list(c)
+
+    def dataflow_state(self):
+        n = c_i64()
+        self._ck(_lib.cc_dataflow_state(self._h, None, 0, ctypes.byref(n)))
+        out = (c_i64 * max(n.value, 1))()
+        self._ck(_lib.cc_dataflow_state(self._h, out, n.value, ctypes.byref(n)))
+        return list(out[:n.value])
+
+    def dataflow_profile(self):
+        """(gemm_items, trace_items) arrays [n, 8]: dispatch, ready, end (ns), smid, first data, k-loop end."""
+        ng, nt = c_i64(), c_i64()
+        self._ck(_lib.cc_dataflow_profile(self._h, None, 0, ctypes.byref(ng), ctypes.byref(nt)))
+        n = ng.value + nt.value
+        out = np.zeros(8 * max(n, 1), dtype=np.uint64)
+        self._ck(_lib.cc_dataflow_profile(self._h, out.ctypes.data_as(P(c_u64)), 8 * n, ctypes.byref(ng),
+                                          ctypes.byref(nt)))
+        a = out[:8 * n].reshape(n, 8)
+        return a[:ng.value], a[ng.value:]
 
     def correlator(self, corr_id, Lt):
         out = np.empty(2 * Lt, dtype=np.float64)

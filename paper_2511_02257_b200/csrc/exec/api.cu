@@ -127,6 +127,7 @@ struct cc_ctx {
   cudaEvent_t ev_cs2 = nullptr;
   cudaGraphExec_t gexec_df = nullptr;
   int64_t df_gemm_items = 0, df_trace_items = 0;
+  unsigned long long* df_prof = nullptr;   // per-item timeline (flags bit 5)
 
   // direct kernel entry points (GEMM split-K partials; trace partials + zeroed counters)
   char* direct_ws = nullptr;
@@ -137,6 +138,8 @@ struct cc_ctx {
   ~cc_ctx() { release_device(); }
 
   void release_df() {
+    if (df_prof) cudaFree(df_prof);
+    df_prof = nullptr;
     if (gexec_df) cudaGraphExecDestroy(gexec_df);
     gexec_df = nullptr;
     if (df_meta) cudaFree(df_meta);
@@ -295,11 +298,11 @@ void df_gemm_geometry(const ZgemmProblem& p, int64_t& tiles, int64_t& KT, int64_
   }
 }
 
-// Pieces per time slice of a TR op: ~8 blocks of 32x32 (256 KB of operands) per item.
+// Pieces per time slice of a TR op: ~16 blocks of 32x32 (512 KB of operands) per item.
 int64_t df_trace_pieces(int64_t Lt, int64_t N) {
   const int64_t nb = (N + 31) / 32, U = nb * nb;
   (void)Lt;
-  return std::max<int64_t>(1, (U + 7) / 8);
+  return std::max<int64_t>(1, (U + 15) / 16);
 }
 
 // Sets up scratch (kernel workspace, roots, correlators, term tables), the physical plan,
@@ -383,7 +386,18 @@ void prepare_phys(cc_ctx* ctx) {
   // physical plan over the pool
   std::vector<uint8_t> on_dev(g.nodes.size(), 0);
   for (size_t u = 0; u < g.nodes.size(); ++u) on_dev[u] = ctx->leaf_dev[u] != nullptr;
-  ctx->pp = build_phys(g, ctx->lp, on_dev, pool, ALIGN);
+  // Placement: next-fit over the pool (freed memory is reused in FIFO order, so the next
+  // writer of a byte range rarely has to wait for its last reader — the dataflow executor
+  // overlaps more).  With a capacity cap the physical pool is held to 1.25 x cap so the
+  // physical footprint follows the logical one; the logical plan is unchanged either way.
+  int64_t phys_limit = pool;
+  if (ctx->cap > 0) phys_limit = std::min(pool, round_up(ctx->cap + ctx->cap / 4, ALIGN));
+  try {
+    ctx->pp = build_phys(g, ctx->lp, on_dev, phys_limit, ALIGN, RangeAlloc::NEXT_FIT);
+  } catch (const Error& e) {
+    if (e.status != CC_E_NOMEM) throw;
+    ctx->pp = build_phys(g, ctx->lp, on_dev, pool, ALIGN, RangeAlloc::BEST_FIT);
+  }
   ctx->stats.arena_high_water = ctx->pp.pool_high_water;
   if (ctx->pp.host_pool_bytes > 0) {
     ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_pool), size_t(ctx->pp.host_pool_bytes), cudaHostAllocDefault),
@@ -475,6 +489,7 @@ PFN_waitval df_write_fn() {
 
 void prepare_dataflow(cc_ctx* ctx) {
   if (ctx->df_valid) return;
+  if (getenv("CC_DEBUG")) fprintf(stderr, "[cc] prepare_dataflow\n");
   prepare_phys(ctx);
   const Dag& g = *ctx->dag;
   const auto& ops = ctx->pp.ops;
@@ -689,6 +704,8 @@ void prepare_dataflow(cc_ctx* ctx) {
   ctx->df_trace.q = DfQueue{reinterpret_cast<const DfOp*>(pt), int32_t(tops.size()), t_items, heads + 1};
   ctx->df_gemm_items = g_items;
   ctx->df_trace_items = t_items;
+  ctx->df_gemm.prof = nullptr;
+  ctx->df_trace.prof = nullptr;
   if (!ctx->cs2) {
     ck(cudaStreamCreateWithFlags(&ctx->cs2, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&ctx->ev_cs2, cudaEventDisableTiming), "event");
@@ -700,6 +717,10 @@ void prepare_dataflow(cc_ctx* ctx) {
 int issue_dataflow(cc_ctx* ctx) {
   const Dag& g = *ctx->dag;
   int nl = 0;
+  static const bool dbg = getenv("CC_DEBUG") != nullptr;
+#define DBG(...) do { if (dbg) { fprintf(stderr, "[cc] " __VA_ARGS__); fputc('\n', stderr); fflush(stderr); } } while (0)
+  DBG("issue_dataflow: %zu copies, %lld gemm items, %lld trace items", ctx->df_copies.size(),
+      (long long)ctx->df_gemm_items, (long long)ctx->df_trace_items);
   ck(cudaMemsetAsync(ctx->df_meta, 0, ctx->df_sync_bytes, ctx->cs), "memset");
   ck(cudaEventRecord(ctx->ev_start, ctx->cs), "event");
   ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_start, 0), "wait");
@@ -714,20 +735,30 @@ int issue_dataflow(cc_ctx* ctx) {
       if (df_wait_fn()(s, reinterpret_cast<CUdeviceptr>(ctx->df_sync + wv.first), cuuint32_t(wv.second),
                        CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
         throw Error(CC_E_CUDA, "cuStreamWaitValue32 failed");
+    DBG("copy %zu: stream %d bytes %zu waits %zu/%zu", k, c.stream, c.bytes, c.wait_values.size(), c.wait_events.size());
     ck(cudaMemcpyAsync(c.dst, c.src, c.bytes, c.stream == S_H2D ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s),
        "copy");
+    DBG("copy %zu enqueued", k);
     if (df_write_fn()(s, reinterpret_cast<CUdeviceptr>(ctx->df_sync + c.flag_slot), 1, 0) != CUDA_SUCCESS)
       throw Error(CC_E_CUDA, "cuStreamWriteValue32 failed");
     if (c.source) ck(cudaEventRecord(ctx->df_events[k], s), "event");
   }
+  DBG("copies enqueued");
+  // Each worker is sized to one CTA per SM and the two are meant to share every SM (DMMA
+  // tiles + streaming traces).  Grids of num_sms - 2 keep two SMs free of each kind, so
+  // both workers always have a resident CTA even if co-residency were impossible: items
+  // only wait on earlier items, so progress is then guaranteed (dataflow.hpp).
+  const int grid = std::max(1, ctx->num_sms - 2);
   if (ctx->df_gemm_items > 0) {
-    ck(df_launch_gemm(ctx->df_gemm, ctx->num_sms, ctx->cs), "gemm worker");
+    ck(df_launch_gemm(ctx->df_gemm, grid, ctx->cs), "gemm worker");
+    DBG("gemm worker launched");
     ++nl;
   }
   if (ctx->df_trace_items > 0) {
-    ck(df_launch_trace(ctx->df_trace, ctx->num_sms, ctx->cs2), "trace worker");
+    ck(df_launch_trace(ctx->df_trace, grid, ctx->cs2), "trace worker");
     ++nl;
   }
+  DBG("workers launched");
   ck(cudaEventRecord(ctx->ev_cs2, ctx->cs2), "event");
   ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_cs2, 0), "wait");
   ck(launch_correlate(ctx->roots, ctx->corr, int64_t(g.corr_ids.size()), g.Lt, ctx->term_start, ctx->term_tree,
@@ -899,7 +930,21 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   const bool time_kernels = (flags & 2) != 0 && !use_graph;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;
   std::vector<int> kev_kind;
-  if (!legacy) prepare_dataflow(ctx);
+  if (!legacy) {
+    prepare_dataflow(ctx);
+    const bool prof = (flags & 32) != 0;
+    if (prof && !ctx->df_prof) {
+      const int64_t n = ctx->df_gemm_items + ctx->df_trace_items;
+      ck(cudaMalloc(reinterpret_cast<void**>(&ctx->df_prof), size_t(std::max<int64_t>(n, 1)) * 64), "profile buffer");
+      ck(cudaMemset(ctx->df_prof, 0, size_t(std::max<int64_t>(n, 1)) * 64), "profile buffer");
+    }
+    ctx->df_gemm.prof = prof ? ctx->df_prof : nullptr;
+    ctx->df_trace.prof = prof ? ctx->df_prof + 8 * ctx->df_gemm_items : nullptr;
+    if (prof && ctx->gexec_df) {
+      cudaGraphExecDestroy(ctx->gexec_df);
+      ctx->gexec_df = nullptr;
+    }
+  }
   cudaEvent_t t_begin, t_end;
   ck(cudaEventCreate(&t_begin), "event");
   ck(cudaEventCreate(&t_end), "event");
@@ -1036,6 +1081,9 @@ cc_status cc_create(cc_ctx** out, int device, void* dev_arena, size_t arena_byte
     }
     for (cudaEvent_t* e : {&ctx->ev_start, &ctx->ev_end, &ctx->ev_h_end, &ctx->ev_d_end})
       ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    ck(zgemm_preload(), "kernel load");
+    ck(trace_preload(), "kernel load");
+    ck(df_preload(), "kernel load");
   }
   API_END
 }
@@ -1339,6 +1387,46 @@ cc_status cc_correlator_device_ptr(cc_ctx* ctx, void** dev_ptr, int64_t* n_corr,
   if (dev_ptr) *dev_ptr = ctx->corr;
   if (n_corr) *n_corr = int64_t(g.corr_ids.size());
   if (corr_ids) std::copy(g.corr_ids.begin(), g.corr_ids.end(), corr_ids);
+  API_END
+}
+
+cc_status cc_dataflow_state(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  ctx->need_device();
+  if (!ctx->df_valid) throw Error(CC_E_STATE, "no dataflow plan");
+  const size_t n_int = (ctx->df_sync_bytes - 16) / 4;
+  std::vector<char> buf(ctx->df_sync_bytes);
+  cudaStream_t s;
+  ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  ck(cudaMemcpyAsync(buf.data(), ctx->df_meta, buf.size(), cudaMemcpyDeviceToHost, s), "state copy");
+  ck(cudaStreamSynchronize(s), "state copy");
+  cudaStreamDestroy(s);
+  const int64_t n = 2 + int64_t(n_int);
+  if (n_out) *n_out = n;
+  if (out) {
+    if (cap < n) throw Error(CC_E_BUFFER_TOO_SMALL, "buffer too small");
+    const unsigned long long* h = reinterpret_cast<const unsigned long long*>(buf.data());
+    out[0] = int64_t(h[0]);
+    out[1] = int64_t(h[1]);
+    const int* sy = reinterpret_cast<const int*>(buf.data() + 16);
+    for (size_t i = 0; i < n_int; ++i) out[2 + i] = sy[i];
+  }
+  API_END
+}
+
+cc_status cc_dataflow_profile(cc_ctx* ctx, uint64_t* out, int64_t cap, int64_t* n_gemm, int64_t* n_trace) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  ctx->need_device();
+  if (!ctx->df_prof) throw Error(CC_E_STATE, "no profiled dataflow execute (flags bit 5)");
+  const int64_t n = ctx->df_gemm_items + ctx->df_trace_items;
+  if (n_gemm) *n_gemm = ctx->df_gemm_items;
+  if (n_trace) *n_trace = ctx->df_trace_items;
+  if (out) {
+    if (cap < 8 * n) throw Error(CC_E_BUFFER_TOO_SMALL, "buffer too small");
+    ck(cudaMemcpy(out, ctx->df_prof, size_t(n) * 64, cudaMemcpyDeviceToHost), "profile copy");
+  }
   API_END
 }
 

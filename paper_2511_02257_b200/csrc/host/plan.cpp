@@ -164,18 +164,15 @@ LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap) {
 }
 
 // ---------------------------------------------------------------------------------------
-RangeAlloc::RangeAlloc(int64_t capacity) {
+RangeAlloc::RangeAlloc(int64_t capacity, Policy policy) : policy_(policy) {
   if (capacity > 0) {
     by_off_[0] = capacity;
     by_size_.insert({capacity, 0});
   }
 }
 
-int64_t RangeAlloc::alloc(int64_t bytes) {
-  auto it = by_size_.lower_bound({bytes, std::numeric_limits<int64_t>::min()});
-  if (it == by_size_.end()) return -1;
-  const int64_t size = it->first, off = it->second;
-  by_size_.erase(it);
+int64_t RangeAlloc::take(int64_t off, int64_t size, int64_t bytes) {
+  by_size_.erase({size, off});
   by_off_.erase(off);
   if (size > bytes) {
     by_off_[off + bytes] = size - bytes;
@@ -183,6 +180,44 @@ int64_t RangeAlloc::alloc(int64_t bytes) {
   }
   high_ = std::max(high_, off + bytes);
   return off;
+}
+
+int64_t RangeAlloc::alloc(int64_t bytes) {
+  if (policy_ == NEXT_FIT) {
+    // first fit at or after the cursor (a block straddling the cursor is used from the
+    // cursor on), then wrap around once
+    for (int pass = 0; pass < 2; ++pass) {
+      auto it = by_off_.upper_bound(pass == 0 ? cursor_ : -1);
+      if (it != by_off_.begin()) {
+        auto prev = std::prev(it);
+        if (pass == 0 && prev->first + prev->second > cursor_) it = prev;
+      }
+      for (; it != by_off_.end(); ++it) {
+        int64_t off = it->first, size = it->second;
+        if (pass == 0 && off < cursor_) {
+          // split the block at the cursor so allocation proceeds forward
+          const int64_t lo = cursor_ - off;
+          if (size - lo < bytes) continue;
+          by_size_.erase({size, off});
+          by_off_.erase(off);
+          by_off_[off] = lo;
+          by_size_.insert({lo, off});
+          off = cursor_;
+          size -= lo;
+          by_off_[off] = size;
+          by_size_.insert({size, off});
+        }
+        if (size >= bytes) {
+          cursor_ = off + bytes;
+          return take(off, size, bytes);
+        }
+      }
+    }
+    return -1;
+  }
+  auto it = by_size_.lower_bound({bytes, std::numeric_limits<int64_t>::min()});
+  if (it == by_size_.end()) return -1;
+  return take(it->second, it->first, bytes);
 }
 
 void RangeAlloc::free(int64_t off, int64_t bytes) {
@@ -232,14 +267,14 @@ void RangeTracker::access(int64_t off, int64_t bytes, int stream, int32_t op, st
 static int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>& leaf_on_device,
-                    int64_t pool_bytes, int64_t align) {
+                    int64_t pool_bytes, int64_t align, RangeAlloc::Policy policy) {
   PhysPlan pp;
   const size_t n = g.nodes.size();
   // host pool: sized for the worst case (sum of all D2H'd sizes), placed best-fit
   int64_t host_cap = 0;
   for (const auto& op : lp.ops)
     if (op.kind == OP_D2H) host_cap += round_up(g.nodes[op.node].size, align);
-  RangeAlloc dev(pool_bytes), hostp(host_cap);
+  RangeAlloc dev(pool_bytes, policy), hostp(host_cap);
   RangeTracker dtr(pool_bytes), htr(std::max<int64_t>(host_cap, 1));
   std::vector<int64_t> dev_off(n, -1), host_off(n, -1);
   std::vector<int32_t> ready(n, -1), ready_stream(n, -1), d2h_op(n, -1);

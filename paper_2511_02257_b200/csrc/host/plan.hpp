@@ -30,10 +30,15 @@ struct LruPlan {
 };
 LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap);
 
-// Best-fit allocator with coalescing over [0, capacity).
+// Allocator with coalescing over [0, capacity).  BEST_FIT packs tightly; NEXT_FIT takes
+// the first block that fits at or after a rotating cursor (wrapping once), so freed memory
+// is reused in FIFO order — the write-after-read distance between a tensor's last reader
+// and the next writer of its bytes is as long as the pool allows (more overlap for the
+// dataflow executor), at the cost of a higher physical high-water mark.
 class RangeAlloc {
  public:
-  explicit RangeAlloc(int64_t capacity = 0);
+  enum Policy { BEST_FIT = 0, NEXT_FIT = 1 };
+  explicit RangeAlloc(int64_t capacity = 0, Policy policy = BEST_FIT);
   int64_t alloc(int64_t bytes);      // -1 if no block fits
   void free(int64_t off, int64_t bytes);
   int64_t high_water() const { return high_; }
@@ -41,6 +46,9 @@ class RangeAlloc {
   std::map<int64_t, int64_t> by_off_;
   std::set<std::pair<int64_t, int64_t>> by_size_;
   int64_t high_ = 0;
+  Policy policy_ = BEST_FIT;
+  int64_t cursor_ = 0;
+  int64_t take(int64_t off, int64_t size, int64_t bytes);
 };
 
 // Per-byte-range record of the last op that touched it on each stream, used to derive
@@ -81,6 +89,6 @@ struct PhysPlan {
 };
 // leaf_on_device[u]: the leaf is a caller device buffer (no H2D / no pool space).
 PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>& leaf_on_device,
-                    int64_t pool_bytes, int64_t align);
+                    int64_t pool_bytes, int64_t align, RangeAlloc::Policy policy = RangeAlloc::BEST_FIT);
 
 }  // namespace cc

@@ -77,27 +77,33 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 
 
 // One k-tile (BK complex) of a warp's WM x WN complex accumulator block from the stage's
-// swizzled shared-memory tiles (see zgemm.cu header for the fragment mapping).
+// swizzled shared-memory tiles (see zgemm.cu header for the fragment mapping).  Lane
+// (g = lane/4, t = lane%4); rows of the warp start at row0 = wm*WM, its complex columns at
+// col0 = wn*WN.  With WM, WN multiples of 8 every swizzle key is a lane constant:
+// A row r = row0 + 8i + g has key g; B column n = col0 + 4k + g/2 sits in 128-byte chunk
+// n/8 = col0/8 + k/2 at slot 4(k%2) + g/2.
 template <class C>
-__device__ __forceinline__ void dmma_ktile(const uint8_t* sA, const uint8_t* sB, const int (&a_row_off)[C::MI],
-                                           const int (&a_key)[C::MI], const int (&b_col_off)[C::NI],
-                                           const int (&b_slot)[C::NI], int t, bool q,
-                                           double (&acc)[C::MI][C::NI][2]) {
+__device__ __forceinline__ void dmma_ktile(const uint8_t* sA, const uint8_t* sB, int wm, int wn, int g, int t,
+                                           bool q, double (&acc)[C::MI][C::NI][2]) {
+  static_assert(C::WM % 8 == 0 && C::WN % 8 == 0, "lane-constant swizzle keys need WM, WN % 8 == 0");
+  const uint8_t* a_base = sA + (wm * C::WM + g) * 128;
+  const uint8_t* b_base = sB + (wn * C::WN / 8) * (C::BK * 128);
 #pragma unroll
   for (int kc = 0; kc < C::BK / 8; ++kc) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int s = 2 * t + h;       // complex k slot within the 8-complex chunk
-      const int krow = kc * 8 + s;   // B row within the stage
+      const int krow = kc * 8 + s;   // B row within the stage (krow & 7 == s)
       double2 a[C::MI];
       double b_re_row[C::NI], b_im_row[C::NI];
 #pragma unroll
       for (int i = 0; i < C::MI; ++i)
-        a[i] = *reinterpret_cast<const double2*>(sA + kc * C::BM * 128 + a_row_off[i] + ((s ^ a_key[i]) << 4));
+        a[i] = *reinterpret_cast<const double2*>(a_base + kc * C::BM * 128 + i * 1024 + ((s ^ g) << 4));
 #pragma unroll
       for (int k = 0; k < C::NI; ++k) {
-        const double2 bv =
-            *reinterpret_cast<const double2*>(sB + b_col_off[k] + krow * 128 + ((b_slot[k] ^ (krow & 7)) << 4));
+        const int slot = 4 * (k & 1) + (g >> 1);
+        const double2 bv = *reinterpret_cast<const double2*>(b_base + (k >> 1) * (C::BK * 128) + krow * 128 +
+                                                             ((slot ^ s) << 4));
         // B' = [[br, bi], [-bi, br]]: row (k, re) -> (br | bi), row (k, im) -> (-bi | br)
         b_re_row[k] = q ? bv.y : bv.x;
         b_im_row[k] = q ? bv.x : neg(bv.y);
@@ -112,24 +118,6 @@ __device__ __forceinline__ void dmma_ktile(const uint8_t* sA, const uint8_t* sB,
 #pragma unroll
         for (int k = 0; k < C::NI; ++k) dmma(acc[i][k][0], acc[i][k][1], a[i].y, b_im_row[k]);
     }
-  }
-}
-
-// Per-lane fragment offsets of a consumer warp (wm, wn) within a stage.
-template <class C>
-__device__ __forceinline__ void frag_offsets(int wm, int wn, int g, int (&a_row_off)[C::MI], int (&a_key)[C::MI],
-                                             int (&b_col_off)[C::NI], int (&b_slot)[C::NI]) {
-#pragma unroll
-  for (int i = 0; i < C::MI; ++i) {
-    const int r = wm * C::WM + i * 8 + g;
-    a_row_off[i] = r * 128;
-    a_key[i] = r & 7;
-  }
-#pragma unroll
-  for (int k = 0; k < C::NI; ++k) {
-    const int n = wn * C::WN + k * 4 + (g >> 1);
-    b_col_off[k] = (n >> 3) * C::BK * 128;
-    b_slot[k] = n & 7;
   }
 }
 

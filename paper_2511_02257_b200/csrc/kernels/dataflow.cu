@@ -6,9 +6,9 @@
 //   tile, or one k-chunk of a tile for ops with few tiles (BB2); the CTA that completes the
 //   last chunk of a tile (ticket) sums the chunk partials in chunk order — deterministic.
 //   Register cap 192 so a trace-worker CTA fits on the same SM.
-// trace_worker: 256 threads, <= 64 registers, streams its (t, piece) unit range with L2-only
-//   loads (.cg: operands were written by other SMs during this launch), fixed-order
-//   reductions, last-piece finisher per time slice.
+// trace_worker: 256 threads, <= 64 registers, 66 KB of shared memory: streams its (t, piece)
+//   unit range through a 2-stage cp.async ring (L2-only copies: operands were written by other
+//   SMs during this launch), fixed-order reductions, last-piece finisher per time slice.
 // Both publish completion with per-thread fences, a CTA barrier and one atomic increment
 // of the op's done counter; waiters spin with ld.acquire.gpu and issue a proxy fence
 // before TMA reads data other SMs wrote with ordinary stores.
@@ -20,7 +20,8 @@ namespace cc {
 namespace {
 using namespace dev;
 
-using GC = Cfg<64, 64, 16, 32, 16, 4>;   // same tile math as zgemm; consumers = all 8 warps
+using GC = Cfg<64, 64, 16, 32, 16, 3>;   // same tile math as zgemm; consumers = all 8 warps; 3 stages
+                                         // leave shared memory for a 4-stage trace worker on the SM
 constexpr int GW_THREADS = GC::NCW * 32;  // 256: no dedicated producer warp
 constexpr int TR_TB = 32;
 constexpr int TR_THREADS = 256;
@@ -44,6 +45,17 @@ __device__ __forceinline__ int find_op(const DfQueue& q, int64_t item) {
   return lo;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ void wait_deps(const DfArgs& a, const DfOp& op) {
   for (int d = 0; d < op.dep_count; ++d) {
     const int* slot = a.sync + a.dep_slot[op.dep_begin + d];
@@ -53,13 +65,58 @@ __device__ __forceinline__ void wait_deps(const DfArgs& a, const DfOp& op) {
 }
 
 // ---------------------------------------------------------------------------------------------
-__global__ void __maxnreg__(192) gemm_worker(DfArgs a) {
+// The producer's view of a GEMM item (kept in shared memory, written and read by thread 0).
+struct ItemInfo {
+  int64_t item;
+  int64_t tile;
+  const void* tA;
+  const void* tB;
+  int32_t op, tm, tn, b, k0, nk, kt_per_o, chunk;
+};
+
+__device__ __forceinline__ void decode_item(const DfArgs& a, int64_t item, ItemInfo& inf) {
+  inf.item = item;
+  if (item >= a.q.n_items) return;
+  const int oi = find_op(a.q, item);
+  const DfOp& op = a.q.ops[oi];
+  const int64_t local = item - op.first_item;
+  const int64_t tile = local / op.n_chunks;
+  const int chunk = int(local - tile * op.n_chunks);
+  const int64_t tiles_mn = int64_t(op.tiles_m) * op.tiles_n;
+  const int64_t b = tile / tiles_mn;
+  const int64_t rr = tile - b * tiles_mn;
+  inf.op = oi;
+  inf.tile = tile;
+  inf.chunk = chunk;
+  inf.tn = int(rr / op.tiles_m);
+  inf.tm = int(rr - int64_t(inf.tn) * op.tiles_m);
+  inf.b = int(b);
+  inf.k0 = int((int64_t(chunk) * op.KT) / op.n_chunks);
+  inf.nk = int((int64_t(chunk + 1) * op.KT) / op.n_chunks) - inf.k0;
+  inf.kt_per_o = op.kt_per_o;
+  inf.tA = static_cast<const uint8_t*>(a.tmaps) + size_t(2 * op.tmap) * 128;
+  inf.tB = static_cast<const uint8_t*>(a.tmaps) + size_t(2 * op.tmap + 1) * 128;
+}
+
+__device__ __forceinline__ bool deps_ready(const DfArgs& a, const DfOp& op) {
+  for (int d = 0; d < op.dep_count; ++d)
+    if (ld_acquire(a.sync + a.dep_slot[op.dep_begin + d]) < a.dep_target[op.dep_begin + d]) return false;
+  return true;
+}
+
+// Persistent DMMA worker.  Thread 0 streams TMA k-tiles through the STAGES ring as one
+// continuous sequence of positions: while the CTA finishes an item it already fetched the
+// next item from the queue and, if that item's dependencies are complete (checked without
+// blocking), loads its first k-tiles — pipeline fill and queue latency overlap the current
+// item's last k-tiles and epilogue.  Thread 0 never blocks inside an item on anything but
+// the ring, so the no-deadlock argument of dataflow.hpp holds.
+__global__ void __maxnreg__(168) gemm_worker(DfArgs a) {
   using C = GC;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
-  __shared__ int64_t s_item;
+  __shared__ ItemInfo s_info[2];
   __shared__ int s_fin;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -69,60 +126,58 @@ __global__ void __maxnreg__(192) gemm_worker(DfArgs a) {
       mbar_init(&empty[s], C::NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    decode_item(a, int64_t(atomicAdd(a.q.head, 1ull)), s_info[0]);
   }
   __syncthreads();
 
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
   const int g = lane >> 2, t = lane & 3;
   const bool q = (g & 1) != 0;
-  int a_row_off[C::MI], a_key[C::MI], b_col_off[C::NI], b_slot[C::NI];
-  frag_offsets<C>(wm, wn, g, a_row_off, a_key, b_col_off, b_slot);
 
-  uint32_t ring = 0;  // k-tiles consumed so far by this CTA (identical in every thread)
+  // position r of the ring <-> k-tile k of item `inf` (thread 0 only)
+  auto issue = [&](uint32_t r, const ItemInfo& inf, int k) {
+    const int st = int(r % C::STAGES);
+    const uint32_t ph = (r / C::STAGES) & 1u;
+    mbar_wait(&empty[st], ph ^ 1u);
+    mbar_expect_tx(&full[st], C::STAGE_BYTES);
+    uint8_t* sA = smem + st * C::STAGE_BYTES;
+    uint8_t* sB = sA + C::A_BYTES;
+    const int kk = inf.k0 + k;
+    const int ko = kk / inf.kt_per_o;
+    const int ki0 = (kk - ko * inf.kt_per_o) * C::BK;
+#pragma unroll
+    for (int kc = 0; kc < C::BK / 8; ++kc)
+      tma_load_4d_g(sA + kc * C::BM * 128, inf.tA, &full[st], 2 * (ki0 + kc * 8), inf.tm * C::BM, ko, inf.b);
+#pragma unroll
+    for (int nc = 0; nc < C::BN / 8; ++nc)
+      tma_load_4d_g(sB + nc * C::BK * 128, inf.tB, &full[st], 2 * (inf.tn * C::BN + nc * 8), ki0, ko, inf.b);
+  };
+  auto acquire_maps = [&](const ItemInfo& inf) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tA) : "memory");
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tB) : "memory");
+  };
+
+  uint32_t ring = 0;    // positions consumed (all threads)
+  uint32_t issued = 0;  // positions issued (thread 0)
+  int par = 0;
   for (;;) {
-    if (tid == 0) s_item = atomicAdd(a.q.head, 1ull);
-    __syncthreads();
-    const int64_t item = s_item;
+    ItemInfo& cur = s_info[par];
+    ItemInfo& nxt = s_info[par ^ 1];
+    const int64_t item = cur.item;
     if (item >= a.q.n_items) break;
-    const DfOp& op = a.q.ops[find_op(a.q, item)];
+    const DfOp& op = a.q.ops[cur.op];
+    const int nk = cur.nk;
+    unsigned long long t_disp = 0, t_ready = 0, t_first = 0, t_comp = 0;
+    bool next_ok = false;
     if (tid == 0) {
-      wait_deps(a, op);
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-    __syncthreads();
-
-    const int64_t local = item - op.first_item;
-    const int64_t tile = local / op.n_chunks;
-    const int chunk = int(local - tile * op.n_chunks);
-    const int k0 = int((int64_t(chunk) * op.KT) / op.n_chunks);
-    const int k1 = int((int64_t(chunk + 1) * op.KT) / op.n_chunks);
-    const int64_t tiles_mn = int64_t(op.tiles_m) * op.tiles_n;
-    const int64_t b = tile / tiles_mn;
-    const int64_t rr = tile - b * tiles_mn;
-    const int tn = int(rr / op.tiles_m), tm = int(rr - int64_t(tn) * op.tiles_m);
-    const void* tA = static_cast<const uint8_t*>(a.tmaps) + size_t(2 * op.tmap) * 128;
-    const void* tB = static_cast<const uint8_t*>(a.tmaps) + size_t(2 * op.tmap + 1) * 128;
-    const int nk = k1 - k0;
-
-    auto issue = [&](uint32_t r, int k) {
-      const int st = int(r % C::STAGES);
-      const uint32_t ph = (r / C::STAGES) & 1u;
-      mbar_wait(&empty[st], ph ^ 1u);
-      mbar_expect_tx(&full[st], C::STAGE_BYTES);
-      uint8_t* sA = smem + st * C::STAGE_BYTES;
-      uint8_t* sB = sA + C::A_BYTES;
-      const int ko = k / op.kt_per_o;
-      const int ki0 = (k - ko * op.kt_per_o) * C::BK;
-#pragma unroll
-      for (int kc = 0; kc < C::BK / 8; ++kc)
-        tma_load_4d_g(sA + kc * C::BM * 128, tA, &full[st], 2 * (ki0 + kc * 8), tm * C::BM, ko, int(b));
-#pragma unroll
-      for (int nc = 0; nc < C::BN / 8; ++nc)
-        tma_load_4d_g(sB + nc * C::BK * 128, tB, &full[st], 2 * (tn * C::BN + nc * 8), ki0, ko, int(b));
-    };
-    if (tid == 0) {
-      const int pre = nk < C::STAGES - 1 ? nk : C::STAGES - 1;
-      for (int j = 0; j < pre; ++j) issue(ring + j, k0 + j);
+      if (a.prof) t_disp = gtimer();
+      if (issued == ring) {           // nothing of this item was prefetched: wait for it
+        wait_deps(a, op);
+        acquire_maps(cur);
+      }
+      if (a.prof) t_ready = gtimer();
+      decode_item(a, int64_t(atomicAdd(a.q.head, 1ull)), nxt);
     }
 
     double acc[C::MI][C::NI][2];
@@ -131,18 +186,42 @@ __global__ void __maxnreg__(192) gemm_worker(DfArgs a) {
 #pragma unroll
       for (int k = 0; k < C::NI; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
     for (int i = 0; i < nk; ++i) {
-      if (tid == 0 && i + C::STAGES - 1 < nk) issue(ring + i + C::STAGES - 1, k0 + i + C::STAGES - 1);
+      if (tid == 0) {
+        const uint32_t target = ring + uint32_t(i) + C::STAGES - 1;
+        while (issued <= target) {
+          if (issued < ring + uint32_t(nk)) {
+            issue(issued, cur, int(issued - ring));
+          } else {
+            if (nxt.item >= a.q.n_items) break;
+            if (!next_ok) {
+              next_ok = deps_ready(a, a.q.ops[nxt.op]);
+              if (!next_ok) break;
+              acquire_maps(nxt);
+            }
+            const int j = int(issued - ring - uint32_t(nk));
+            if (j >= nxt.nk) break;
+            issue(issued, nxt, j);
+          }
+          ++issued;
+        }
+      }
+      __syncwarp();  // warp 0 reconverges before the .aligned DMMA instructions
       const uint32_t r = ring + i;
       const int st = int(r % C::STAGES);
       mbar_wait(&full[st], (r / C::STAGES) & 1u);
+      if (i == 0 && tid == 0 && a.prof) t_first = gtimer();
       const uint8_t* sA = smem + st * C::STAGE_BYTES;
-      dmma_ktile<C>(sA, sA + C::A_BYTES, a_row_off, a_key, b_col_off, b_slot, t, q, acc);
+      dmma_ktile<C>(sA, sA + C::A_BYTES, wm, wn, g, t, q, acc);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
     ring += nk;
+    if (tid == 0 && a.prof) t_comp = gtimer();
 
-    double2* out = static_cast<double2*>(op.C) + b * op.sCb;
+    const int64_t tile = cur.tile;
+    const int chunk = cur.chunk;
+    const int tm = cur.tm, tn = cur.tn;
+    double2* out = static_cast<double2*>(op.C) + int64_t(cur.b) * op.sCb;
     bool store = true;
     if (op.n_chunks > 1) {
       // publish this chunk's partial, then the last chunk of the tile sums all of them
@@ -194,9 +273,22 @@ __global__ void __maxnreg__(192) gemm_worker(DfArgs a) {
         }
       }
     }
-    __threadfence();
     __syncthreads();
-    if (tid == 0) atomicAdd(a.sync + op.sync_id, 1);
+    if (tid == 0) {
+      __threadfence();   // cumulative: the CTA's stores (ordered by the barrier) before the count
+      atomicAdd(a.sync + op.sync_id, 1);
+      if (a.prof) {
+        unsigned long long* pr = a.prof + 8 * item;
+        pr[0] = t_disp;
+        pr[1] = t_ready;
+        pr[2] = gtimer();
+        pr[3] = smid();
+        pr[4] = t_first;
+        pr[5] = t_comp;
+      }
+    }
+    par ^= 1;
+    __syncthreads();   // the next item's info (written by thread 0) is visible to all
   }
 }
 
@@ -209,8 +301,46 @@ __device__ __forceinline__ double2 cmul_acc(double2 acc, double2 x, double2 y) {
   return acc;
 }
 
+// trace unit = 32x32 complex block A[t, I, J] and its partner B[t, J, I], staged in shared
+// memory by cp.async (16-byte L2-only copies, zero-filled outside N), TR_STAGES deep, so the
+// next units stream in without holding registers.  B is read transposed (lane = row), so its
+// 16-byte element (r, c) is stored at column c ^ (r & 7): the 8 lanes of a shared-memory
+// phase then hit 8 different 16-byte bank groups (conflict-free, no padding).
+constexpr int TR_STAGES = 4;
+constexpr int TR_A_BYTES = TR_TB * TR_TB * 16;
+constexpr int TR_B_BYTES = TR_TB * TR_TB * 16;   // XOR-swizzled (see below)
+constexpr int TR_SMEM = TR_STAGES * (TR_A_BYTES + TR_B_BYTES);
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const unsigned d = smem_u32(dst);
+  const int n = valid ? 16 : 0;   // src-size 0: the 16 bytes are zero-filled
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Issue the copies of unit u of slice (At, Bt) into stage st (every thread: 4 + 4 chunks).
+__device__ __forceinline__ void tr_issue(uint8_t* smem, int st, const double2* At, const double2* Bt, int64_t N,
+                                         int nb, int u, int tid) {
+  const int I = u / nb, J = u - I * nb;
+  const int64_t i0 = int64_t(I) * TR_TB, j0 = int64_t(J) * TR_TB;
+  double2* sA = reinterpret_cast<double2*>(smem + st * (TR_A_BYTES + TR_B_BYTES));
+  double2* sB = reinterpret_cast<double2*>(smem + st * (TR_A_BYTES + TR_B_BYTES) + TR_A_BYTES);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = tid + q * TR_THREADS;   // 0..1023: row e/32, column e%32
+    const int r = e >> 5, c = e & 31;
+    const int64_t ia = i0 + r, ja = j0 + c;   // A[t, I0 + r, J0 + c]
+    const int64_t jb = j0 + r, ib = i0 + c;   // B[t, J0 + r, I0 + c]
+    const bool va = ia < N && ja < N, vb = jb < N && ib < N;
+    cp_async16(sA + r * TR_TB + c, va ? At + ia * N + ja : At, va);
+    cp_async16(sB + r * TR_TB + (c ^ (r & 7)), vb ? Bt + jb * N + ib : Bt, vb);
+  }
+}
+
 __global__ void __launch_bounds__(TR_THREADS, 4) trace_worker(DfArgs a) {
-  __shared__ double2 sB[TR_TB][TR_TB + 1];
+  extern __shared__ __align__(16) uint8_t tr_smem[];
   __shared__ double2 red[TR_THREADS / 32];
   __shared__ int64_t s_item;
   __shared__ int s_last;
@@ -221,7 +351,12 @@ __global__ void __launch_bounds__(TR_THREADS, 4) trace_worker(DfArgs a) {
     const int64_t item = s_item;
     if (item >= a.q.n_items) break;
     const DfOp& op = a.q.ops[find_op(a.q, item)];
-    if (tid == 0) wait_deps(a, op);
+    unsigned long long t_disp = 0, t_ready = 0;
+    if (tid == 0) {
+      if (a.prof) t_disp = gtimer();
+      wait_deps(a, op);
+      if (a.prof) t_ready = gtimer();
+    }
     __syncthreads();
     const int64_t local = item - op.first_item;
     const int t = int(local / op.P), p = int(local - int64_t(t) * op.P);
@@ -231,24 +366,27 @@ __global__ void __launch_bounds__(TR_THREADS, 4) trace_worker(DfArgs a) {
     const double2* At = static_cast<const double2*>(op.A) + int64_t(t) * N * N;
     const double2* Bt = static_cast<const double2*>(op.B) + int64_t(t) * N * N;
     double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int s = 0; s < TR_STAGES; ++s) {
+      if (u0 + s < u1) tr_issue(tr_smem, s, At, Bt, N, op.nb, u0 + s, tid);
+      cp_async_commit();
+    }
     for (int u = u0; u < u1; ++u) {
-      const int I = u / op.nb, J = u - I * op.nb;
-      const int64_t i0 = int64_t(I) * TR_TB, j0 = int64_t(J) * TR_TB;
-      double2 av[TR_TB / 8], bv[TR_TB / 8];
+      const int st = (u - u0) % TR_STAGES;
+      cp_async_wait<TR_STAGES - 1>();
+      __syncthreads();
+      const double2* sA = reinterpret_cast<const double2*>(tr_smem + st * (TR_A_BYTES + TR_B_BYTES));
+      const double2* sB = reinterpret_cast<const double2*>(tr_smem + st * (TR_A_BYTES + TR_B_BYTES) + TR_A_BYTES);
 #pragma unroll
       for (int q = 0; q < TR_TB / 8; ++q) {
         const int r = warp + q * 8;
-        const int64_t ia = i0 + r, ja = j0 + lane, jb = j0 + r, ib = i0 + lane;
-        av[q] = (ia < N && ja < N) ? __ldcg(At + ia * N + ja) : make_double2(0.0, 0.0);
-        bv[q] = (jb < N && ib < N) ? __ldcg(Bt + jb * N + ib) : make_double2(0.0, 0.0);
+        acc = cmul_acc(acc, sA[r * TR_TB + lane], sB[lane * TR_TB + (r ^ (lane & 7))]);  // A[I0+r][J0+lane] B[J0+lane][I0+r]
       }
-#pragma unroll
-      for (int q = 0; q < TR_TB / 8; ++q) sB[warp + q * 8][lane] = bv[q];
       __syncthreads();
-#pragma unroll
-      for (int q = 0; q < TR_TB / 8; ++q) acc = cmul_acc(acc, av[q], sB[lane][warp + q * 8]);
-      __syncthreads();
+      if (u + TR_STAGES < u1) tr_issue(tr_smem, st, At, Bt, N, op.nb, u + TR_STAGES, tid);
+      cp_async_commit();
     }
+    cp_async_wait<0>();
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
@@ -294,13 +432,37 @@ __global__ void __launch_bounds__(TR_THREADS, 4) trace_worker(DfArgs a) {
     }
     __threadfence();
     __syncthreads();
-    if (tid == 0) atomicAdd(a.sync + op.sync_id, 1);
+    if (tid == 0) {
+      atomicAdd(a.sync + op.sync_id, 1);
+      if (a.prof) {
+        unsigned long long* pr = a.prof + 8 * item;
+        pr[0] = t_disp;
+        pr[1] = t_ready;
+        pr[2] = gtimer();
+        pr[3] = smid();
+      }
+    }
   }
 }
 
 }  // namespace
 
 size_t df_gemm_smem_bytes() { return size_t(GC::SMEM); }
+
+cudaError_t df_preload() {
+  cudaFuncAttributes attr;
+  cudaError_t e = cudaFuncGetAttributes(&attr, gemm_worker);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&attr, trace_worker);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_worker, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::SMEM);
+  // both workers ask for the largest shared-memory carveout, so an SM configured for a GEMM
+  // worker (132 KB) still has room for a trace worker (17 KB): the two co-reside
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm_worker, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(trace_worker, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(trace_worker, cudaFuncAttributeMaxDynamicSharedMemorySize, TR_SMEM);
+  return e;
+}
 
 void df_gemm_tile_dims(int* BM, int* BN, int* BK, int* slot_doubles) {
   *BM = GC::BM;
@@ -323,7 +485,7 @@ cudaError_t df_launch_gemm(const DfArgs& a, int grid, cudaStream_t s) {
 }
 
 cudaError_t df_launch_trace(const DfArgs& a, int grid, cudaStream_t s) {
-  trace_worker<<<grid, TR_THREADS, 0, s>>>(a);
+  trace_worker<<<grid, TR_THREADS, TR_SMEM, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -52,8 +52,10 @@ struct DfArgs {
   const int32_t* dep_target;  // value the slot must reach
   const void* tmaps;          // CUtensorMap array (64-byte aligned, global memory)
   int* sync;                  // done counters + copy flags (zeroed per launch)
+  unsigned long long* prof;   // optional: per item {dispatch, ready, end, smid} %globaltimer ns
 };
 
+cudaError_t df_preload();
 // Launch the persistent workers (stream-ordered; the sync area must be zero).
 size_t df_gemm_smem_bytes();
 cudaError_t df_launch_gemm(const DfArgs& a, int grid, cudaStream_t s);

@@ -42,6 +42,12 @@ cudaError_t launch_trace(const void* A, const void* B, void* out, int64_t Lt, in
 cudaError_t launch_correlate(const void* roots, void* corr, int64_t n_corr, int64_t Lt, const int32_t* term_start,
                              const int32_t* term_tree, const double* term_coef, cudaStream_t stream);
 
+// Force-load the kernels of each translation unit (CUDA lazy loading would otherwise load a
+// kernel at its first launch, which can wait for an idle device — a deadlock while copy
+// streams wait on a persistent worker).  Also sets their shared-memory attributes.
+cudaError_t zgemm_preload();
+cudaError_t trace_preload();
+
 // Synthetic leaf values (input generation; same recipe as synth/rng.py).
 cudaError_t launch_fill_synthetic(void* dev, int64_t n, uint64_t seed, int64_t leaf_id, int64_t e0, int mode,
                                   double sigma, cudaStream_t stream);

@@ -191,6 +191,14 @@ __global__ void fill_synthetic_kernel(double2* out, int64_t n, uint64_t key, int
 
 }  // namespace
 
+cudaError_t trace_preload() {
+  cudaFuncAttributes attr;
+  cudaError_t e = cudaFuncGetAttributes(&attr, trace_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&attr, correlate_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&attr, fill_synthetic_kernel);
+  return e;
+}
+
 size_t trace_workspace_bytes(int64_t Lt, int64_t N) {
   return size_t(Lt * trace_pieces(Lt, N)) * 16 + ((size_t(Lt) * 4 + 255) / 256) * 256;
 }

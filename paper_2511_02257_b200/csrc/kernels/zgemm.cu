@@ -360,6 +360,13 @@ bool encode_zgemm_maps(void* mapA, void* mapB, const ZgemmProblem& p, int BM, in
          make_map(static_cast<CUtensorMap*>(mapB), p.B, db, sb, uint32_t(BK));
 }
 
+cudaError_t zgemm_preload() {
+  cudaFuncAttributes attr;
+  cudaError_t e = cudaFuncGetAttributes(&attr, zgemm_dmma_kernel<Big>);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(zgemm_dmma_kernel<Big>, cudaFuncAttributeMaxDynamicSharedMemorySize, Big::SMEM);
+}
+
 size_t zgemm_workspace_bytes(const ZgemmProblem& p, int num_sms) { return ws_bytes<Big>(p, num_sms); }
 
 cudaError_t launch_zgemm(const ZgemmProblem& p, void* workspace, size_t ws_size, int num_sms, cudaStream_t stream,

@@ -1,0 +1,56 @@
+"""Timeline summary of one dataflow replay of the bench workload (flags bit 5)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2511_02257_b200 import cc  # noqa: E402
+from synth import dags, rng as srng  # noqa: E402
+
+w = dags.config_c2() if len(sys.argv) < 2 else getattr(dags, "config_" + sys.argv[1])()
+dev = torch.device("cuda:0")
+ctx = cc.Context(0, torch.empty(6 << 30, dtype=torch.uint8, device=dev))
+ctx.load_workload(w)
+ctx.schedule(cc.CC_TREE)
+keep = []
+for (u, op, a, b, s) in w.nodes:
+    if op not in (dags.LEAF_M, dags.LEAF_B):
+        continue
+    n = w.Lt * w.N * w.N * (1 if op == dags.LEAF_M else w.S * w.N)
+    d = torch.empty(2 * n, dtype=torch.float64, device=dev)
+    sig = srng.meson_sigma(w.N) if op == dags.LEAF_M else srng.baryon_sigma(w.N, w.S)
+    ctx.fill_synthetic(d, n, w.data_seed, u, 0, 0, sig)
+    keep.append(d)
+    ctx.set_leaf_device(u, d)
+for _ in range(3):
+    ctx.execute(0)
+ex = ctx.execute(cc.EXEC_PROFILE)
+g, t = ctx.dataflow_profile()
+t0 = min(g[:, 0].min() if len(g) else 2**63, t[:, 0].min() if len(t) else 2**63)
+t1 = max(g[:, 2].max() if len(g) else 0, t[:, 2].max() if len(t) else 0)
+span = (t1 - t0) / 1e3
+print("execute %.3f ms, worker span %.3f ms" % (ex["seconds"] * 1e3, span / 1e3))
+for name, a in (("gemm", g), ("trace", t)):
+    if not len(a):
+        continue
+    a = a.astype(np.float64)
+    wait = (a[:, 1] - a[:, 0]) / 1e3
+    work = (a[:, 2] - a[:, 1]) / 1e3
+    sms = len(np.unique(a[:, 3]))
+    print("%-5s items %6d on %3d SMs: work %.1f us avg (sum %.2f ms), dep-wait %.2f us avg (sum %.2f ms), "
+          "busy %.1f%% of %d SMs x span" % (name, len(a), sms, work.mean(), work.sum() / 1e3, wait.mean(),
+                                              wait.sum() / 1e3, 100 * work.sum() / (sms * span), sms))
+    # per-SM timeline occupancy gaps
+    q = np.percentile(work, [10, 50, 90, 99])
+    print("      work percentiles 10/50/90/99: %s us" % np.round(q, 1))
+    if name == "gemm":
+        fill = (a[:, 4] - a[:, 1]) / 1e3
+        loop = (a[:, 5] - a[:, 4]) / 1e3
+        epi = (a[:, 2] - a[:, 5]) / 1e3
+        print("      fill %.2f us, k-loop %.2f us, epilogue+publish %.2f us (avg)" % (fill.mean(), loop.mean(), epi.mean()))
+    first = (a[:, 0].min() - t0) / 1e3
+    last = (a[:, 2].max() - t0) / 1e3
+    print("      first dispatch at %.1f us, last end at %.1f us" % (first, last))
+os._exit(0)
