@@ -45,8 +45,11 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
 }
+// sign flip as an integer XOR on the high word (ALU pipe, not the FP64 pipe)
 __device__ __forceinline__ double neg(double x) {
-  return __longlong_as_double(__double_as_longlong(x) ^ static_cast<long long>(0x8000000000000000ULL));
+  double r;
+  asm("{\n.reg .b32 lo, hi;\nmov.b64 {lo, hi}, %1;\nxor.b32 hi, hi, 0x80000000;\nmov.b64 %0, {lo, hi};\n}" : "=d"(r) : "d"(x));
+  return r;
 }
 
 template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>

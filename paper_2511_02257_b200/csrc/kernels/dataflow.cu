@@ -20,11 +20,12 @@ namespace cc {
 namespace {
 using namespace dev;
 
-using GC = Cfg<64, 64, 16, 32, 16, 3>;   // same tile math as zgemm; consumers = all 8 warps; 3 stages
-                                         // leave shared memory for a 4-stage trace worker on the SM
-constexpr int GW_THREADS = GC::NCW * 32;  // 256: no dedicated producer warp
+using GC = Cfg<64, 64, 16, 32, 16, 3>;   // same tile math as zgemm; 3 stages leave shared memory
+                                         // for a 4-stage trace worker on the SM
+constexpr int GW_THREADS = GC::NCW * 32;  // 256 consumer threads (+1 producer warp)
 constexpr int TR_TB = 32;
-constexpr int TR_THREADS = 256;
+constexpr int TR_THREADS = 128;   // 4 warps: one per SM sub-partition (see gemm_worker)
+constexpr int TR_WARPS = TR_THREADS / 32;
 
 __device__ __forceinline__ void tma_load_4d_g(void* dst, const void* map, uint64_t* bar, int c0, int c1, int c2,
                                               int c3) {
@@ -65,19 +66,24 @@ __device__ __forceinline__ void wait_deps(const DfArgs& a, const DfOp& op) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// The producer's view of a GEMM item (kept in shared memory, written and read by thread 0).
+// One GEMM item as the producer decoded it (shared memory, handed to the consumer warps).
 struct ItemInfo {
-  int64_t item;
+  int64_t item;          // >= n_items: stop
   int64_t tile;
   const void* tA;
   const void* tB;
   int32_t op, tm, tn, b, k0, nk, kt_per_o, chunk;
+  unsigned long long t_disp, t_ready;   // profiling
 };
 
-__device__ __forceinline__ void decode_item(const DfArgs& a, int64_t item, ItemInfo& inf) {
+// Decode `item` (hint: the op of the previous item — consecutive items usually share it,
+// which skips the binary search over the op table).
+__device__ __forceinline__ int decode_item(const DfArgs& a, int64_t item, ItemInfo& inf, int hint) {
   inf.item = item;
-  if (item >= a.q.n_items) return;
-  const int oi = find_op(a.q, item);
+  if (item >= a.q.n_items) return hint;
+  int oi = hint;
+  if (oi < 0 || item < a.q.ops[oi].first_item || item >= a.q.ops[oi].first_item + a.q.ops[oi].n_items)
+    oi = find_op(a.q, item);
   const DfOp& op = a.q.ops[oi];
   const int64_t local = item - op.first_item;
   const int64_t tile = local / op.n_chunks;
@@ -96,27 +102,34 @@ __device__ __forceinline__ void decode_item(const DfArgs& a, int64_t item, ItemI
   inf.kt_per_o = op.kt_per_o;
   inf.tA = static_cast<const uint8_t*>(a.tmaps) + size_t(2 * op.tmap) * 128;
   inf.tB = static_cast<const uint8_t*>(a.tmaps) + size_t(2 * op.tmap + 1) * 128;
+  return oi;
 }
 
-__device__ __forceinline__ bool deps_ready(const DfArgs& a, const DfOp& op) {
-  for (int d = 0; d < op.dep_count; ++d)
-    if (ld_acquire(a.sync + a.dep_slot[op.dep_begin + d]) < a.dep_target[op.dep_begin + d]) return false;
-  return true;
-}
+constexpr int GW_INFO = 4;   // decoded items in flight between producer and consumers
 
-// Persistent DMMA worker.  Thread 0 streams TMA k-tiles through the STAGES ring as one
-// continuous sequence of positions: while the CTA finishes an item it already fetched the
-// next item from the queue and, if that item's dependencies are complete (checked without
-// blocking), loads its first k-tiles — pipeline fill and queue latency overlap the current
-// item's last k-tiles and epilogue.  Thread 0 never blocks inside an item on anything but
-// the ring, so the no-deadlock argument of dataflow.hpp holds.
-__global__ void __maxnreg__(168) gemm_worker(DfArgs a) {
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Persistent DMMA worker: 8 consumer warps (DMMA) + 1 producer warp.  The producer takes
+// items from the queue, decodes them, waits for their dependencies and streams their TMA
+// k-tiles through the STAGES ring; decoded items reach the consumers through a small ring of
+// ItemInfo slots guarded by mbarriers.  Queue latency, dependency checks and pipeline fill of
+// item n+1 thus overlap the DMMA work and epilogue of item n.  Only the producer ever waits
+// on dependencies, and only for items no consumer has started, so the no-deadlock argument of
+// dataflow.hpp holds.
+// Register budget: the SM's register file is split over 4 sub-partitions (warp w on w % 4),
+// 16K registers each; with 9 warps here sub-partition 0 holds 3 of them, so 152 registers per
+// thread leave exactly one 56-register warp of the 4-warp trace worker room on every
+// sub-partition (3*32*152 + 32*56 = 16384): the two workers co-reside on each SM.
+__global__ void __maxnreg__(152) gemm_worker(DfArgs a) {
   using C = GC;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned stage base, derived from the __shared__ array by pointer arithmetic so
+  // the compiler keeps the shared address space (LDS, not generic LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
-  __shared__ ItemInfo s_info[2];
+  __shared__ ItemInfo s_info[GW_INFO];
+  __shared__ uint64_t info_full[GW_INFO], info_empty[GW_INFO];
   __shared__ int s_fin;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -125,60 +138,70 @@ __global__ void __maxnreg__(168) gemm_worker(DfArgs a) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NCW);
     }
+    for (int s = 0; s < GW_INFO; ++s) {
+      mbar_init(&info_full[s], 1);
+      mbar_init(&info_empty[s], C::NCW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    decode_item(a, int64_t(atomicAdd(a.q.head, 1ull)), s_info[0]);
   }
   __syncthreads();
 
+  if (warp == C::NCW) {
+    // ------------------------------- producer -------------------------------------------
+    if (lane != 0) return;
+    uint32_t pos = 0;   // ring positions issued
+    int hint = -1;
+    for (uint32_t n = 0;; ++n) {
+      const int slot = int(n % GW_INFO);
+      mbar_wait(&info_empty[slot], ((n / GW_INFO) & 1u) ^ 1u);
+      ItemInfo& inf = s_info[slot];
+      const unsigned long long t0 = a.prof ? gtimer() : 0ull;
+      hint = decode_item(a, int64_t(atomicAdd(a.q.head, 1ull)), inf, hint);
+      const bool stop = inf.item >= a.q.n_items;
+      if (!stop) {
+        wait_deps(a, a.q.ops[inf.op]);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tA) : "memory");
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tB) : "memory");
+      }
+      inf.t_disp = t0;
+      inf.t_ready = a.prof ? gtimer() : 0ull;
+      mbar_arrive(&info_full[slot]);   // release: the info is visible to the consumers
+      if (stop) break;
+      for (int k = 0; k < inf.nk; ++k, ++pos) {
+        const int st = int(pos % C::STAGES);
+        mbar_wait(&empty[st], ((pos / C::STAGES) & 1u) ^ 1u);
+        mbar_expect_tx(&full[st], C::STAGE_BYTES);
+        uint8_t* sA = smem + st * C::STAGE_BYTES;
+        uint8_t* sB = sA + C::A_BYTES;
+        const int kk = inf.k0 + k;
+        const int ko = kk / inf.kt_per_o;
+        const int ki0 = (kk - ko * inf.kt_per_o) * C::BK;
+#pragma unroll
+        for (int kc = 0; kc < C::BK / 8; ++kc)
+          tma_load_4d_g(sA + kc * C::BM * 128, inf.tA, &full[st], 2 * (ki0 + kc * 8), inf.tm * C::BM, ko, inf.b);
+#pragma unroll
+        for (int nc = 0; nc < C::BN / 8; ++nc)
+          tma_load_4d_g(sB + nc * C::BK * 128, inf.tB, &full[st], 2 * (inf.tn * C::BN + nc * 8), ki0, ko, inf.b);
+      }
+    }
+    return;
+  }
+
+  // --------------------------------- consumers ---------------------------------------------
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
   const int g = lane >> 2, t = lane & 3;
   const bool q = (g & 1) != 0;
-
-  // position r of the ring <-> k-tile k of item `inf` (thread 0 only)
-  auto issue = [&](uint32_t r, const ItemInfo& inf, int k) {
-    const int st = int(r % C::STAGES);
-    const uint32_t ph = (r / C::STAGES) & 1u;
-    mbar_wait(&empty[st], ph ^ 1u);
-    mbar_expect_tx(&full[st], C::STAGE_BYTES);
-    uint8_t* sA = smem + st * C::STAGE_BYTES;
-    uint8_t* sB = sA + C::A_BYTES;
-    const int kk = inf.k0 + k;
-    const int ko = kk / inf.kt_per_o;
-    const int ki0 = (kk - ko * inf.kt_per_o) * C::BK;
-#pragma unroll
-    for (int kc = 0; kc < C::BK / 8; ++kc)
-      tma_load_4d_g(sA + kc * C::BM * 128, inf.tA, &full[st], 2 * (ki0 + kc * 8), inf.tm * C::BM, ko, inf.b);
-#pragma unroll
-    for (int nc = 0; nc < C::BN / 8; ++nc)
-      tma_load_4d_g(sB + nc * C::BK * 128, inf.tB, &full[st], 2 * (inf.tn * C::BN + nc * 8), ki0, ko, inf.b);
-  };
-  auto acquire_maps = [&](const ItemInfo& inf) {
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tA) : "memory");
-    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tB) : "memory");
-  };
-
-  uint32_t ring = 0;    // positions consumed (all threads)
-  uint32_t issued = 0;  // positions issued (thread 0)
-  int par = 0;
-  for (;;) {
-    ItemInfo& cur = s_info[par];
-    ItemInfo& nxt = s_info[par ^ 1];
+  uint32_t ring = 0;
+  for (uint32_t n = 0;; ++n) {
+    const int slot = int(n % GW_INFO);
+    mbar_wait(&info_full[slot], (n / GW_INFO) & 1u);
+    const ItemInfo& cur = s_info[slot];
     const int64_t item = cur.item;
     if (item >= a.q.n_items) break;
     const DfOp& op = a.q.ops[cur.op];
     const int nk = cur.nk;
-    unsigned long long t_disp = 0, t_ready = 0, t_first = 0, t_comp = 0;
-    bool next_ok = false;
-    if (tid == 0) {
-      if (a.prof) t_disp = gtimer();
-      if (issued == ring) {           // nothing of this item was prefetched: wait for it
-        wait_deps(a, op);
-        acquire_maps(cur);
-      }
-      if (a.prof) t_ready = gtimer();
-      decode_item(a, int64_t(atomicAdd(a.q.head, 1ull)), nxt);
-    }
+    unsigned long long t_first = 0, t_comp = 0;
 
     double acc[C::MI][C::NI][2];
 #pragma unroll
@@ -186,26 +209,6 @@ __global__ void __maxnreg__(168) gemm_worker(DfArgs a) {
 #pragma unroll
       for (int k = 0; k < C::NI; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
     for (int i = 0; i < nk; ++i) {
-      if (tid == 0) {
-        const uint32_t target = ring + uint32_t(i) + C::STAGES - 1;
-        while (issued <= target) {
-          if (issued < ring + uint32_t(nk)) {
-            issue(issued, cur, int(issued - ring));
-          } else {
-            if (nxt.item >= a.q.n_items) break;
-            if (!next_ok) {
-              next_ok = deps_ready(a, a.q.ops[nxt.op]);
-              if (!next_ok) break;
-              acquire_maps(nxt);
-            }
-            const int j = int(issued - ring - uint32_t(nk));
-            if (j >= nxt.nk) break;
-            issue(issued, nxt, j);
-          }
-          ++issued;
-        }
-      }
-      __syncwarp();  // warp 0 reconverges before the .aligned DMMA instructions
       const uint32_t r = ring + i;
       const int st = int(r % C::STAGES);
       mbar_wait(&full[st], (r / C::STAGES) & 1u);
@@ -235,13 +238,13 @@ __global__ void __maxnreg__(168) gemm_worker(DfArgs a) {
           __stcg(mine + ((i * C::NI + k) * 2 + 1) * 32 + lane, acc[i][k][1]);
         }
       __threadfence();
-      __syncthreads();
+      named_sync(1, GW_THREADS);
       if (tid == 0) {
         const int old = atomicAdd(&op.tile_cnt[tile], 1);
         s_fin = (old == op.n_chunks - 1);
         if (s_fin) op.tile_cnt[tile] = 0;
       }
-      __syncthreads();
+      named_sync(1, GW_THREADS);
       store = s_fin != 0;
       if (store) {
         __threadfence();
@@ -273,22 +276,22 @@ __global__ void __maxnreg__(168) gemm_worker(DfArgs a) {
         }
       }
     }
-    __syncthreads();
+    named_sync(1, GW_THREADS);
     if (tid == 0) {
-      __threadfence();   // cumulative: the CTA's stores (ordered by the barrier) before the count
+      __threadfence();   // cumulative: the consumers' stores (ordered by the barrier) before the count
       atomicAdd(a.sync + op.sync_id, 1);
       if (a.prof) {
         unsigned long long* pr = a.prof + 8 * item;
-        pr[0] = t_disp;
-        pr[1] = t_ready;
+        pr[0] = cur.t_disp;
+        pr[1] = cur.t_ready;
         pr[2] = gtimer();
         pr[3] = smid();
         pr[4] = t_first;
         pr[5] = t_comp;
       }
     }
-    par ^= 1;
-    __syncthreads();   // the next item's info (written by thread 0) is visible to all
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&info_empty[slot]);
   }
 }
 
@@ -306,7 +309,7 @@ __device__ __forceinline__ double2 cmul_acc(double2 acc, double2 x, double2 y) {
 // next units stream in without holding registers.  B is read transposed (lane = row), so its
 // 16-byte element (r, c) is stored at column c ^ (r & 7): the 8 lanes of a shared-memory
 // phase then hit 8 different 16-byte bank groups (conflict-free, no padding).
-constexpr int TR_STAGES = 4;
+constexpr int TR_STAGES = 3;
 constexpr int TR_A_BYTES = TR_TB * TR_TB * 16;
 constexpr int TR_B_BYTES = TR_TB * TR_TB * 16;   // XOR-swizzled (see below)
 constexpr int TR_SMEM = TR_STAGES * (TR_A_BYTES + TR_B_BYTES);
@@ -328,7 +331,7 @@ __device__ __forceinline__ void tr_issue(uint8_t* smem, int st, const double2* A
   double2* sA = reinterpret_cast<double2*>(smem + st * (TR_A_BYTES + TR_B_BYTES));
   double2* sB = reinterpret_cast<double2*>(smem + st * (TR_A_BYTES + TR_B_BYTES) + TR_A_BYTES);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < 1024 / TR_THREADS; ++q) {
     const int e = tid + q * TR_THREADS;   // 0..1023: row e/32, column e%32
     const int r = e >> 5, c = e & 31;
     const int64_t ia = i0 + r, ja = j0 + c;   // A[t, I0 + r, J0 + c]
@@ -339,7 +342,7 @@ __device__ __forceinline__ void tr_issue(uint8_t* smem, int st, const double2* A
   }
 }
 
-__global__ void __launch_bounds__(TR_THREADS, 4) trace_worker(DfArgs a) {
+__global__ void __maxnreg__(56) trace_worker(DfArgs a) {
   extern __shared__ __align__(16) uint8_t tr_smem[];
   __shared__ double2 red[TR_THREADS / 32];
   __shared__ int64_t s_item;
@@ -378,8 +381,8 @@ __global__ void __launch_bounds__(TR_THREADS, 4) trace_worker(DfArgs a) {
       const double2* sA = reinterpret_cast<const double2*>(tr_smem + st * (TR_A_BYTES + TR_B_BYTES));
       const double2* sB = reinterpret_cast<const double2*>(tr_smem + st * (TR_A_BYTES + TR_B_BYTES) + TR_A_BYTES);
 #pragma unroll
-      for (int q = 0; q < TR_TB / 8; ++q) {
-        const int r = warp + q * 8;
+      for (int q = 0; q < TR_TB / TR_WARPS; ++q) {
+        const int r = warp + q * TR_WARPS;
         acc = cmul_acc(acc, sA[r * TR_TB + lane], sB[lane * TR_TB + (r ^ (lane & 7))]);  // A[I0+r][J0+lane] B[J0+lane][I0+r]
       }
       __syncthreads();
@@ -480,7 +483,7 @@ cudaError_t df_launch_gemm(const DfArgs& a, int grid, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  gemm_worker<<<grid, GW_THREADS, GC::SMEM, s>>>(a);
+  gemm_worker<<<grid, GW_THREADS + 32, GC::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -53,4 +53,16 @@ for name, a in (("gemm", g), ("trace", t)):
     first = (a[:, 0].min() - t0) / 1e3
     last = (a[:, 2].max() - t0) / 1e3
     print("      first dispatch at %.1f us, last end at %.1f us" % (first, last))
+# time bins: items running and mean duration per 0.5 ms
+span_ns = t1 - t0
+nb = int(span_ns // 500000) + 1
+print("bin(ms)  gemm_items  gemm_us  trace_items  trace_us  trace_SMs")
+for k in range(nb):
+    lo, hi = t0 + k * 500000, t0 + (k + 1) * 500000
+    row = []
+    for a in (g, t):
+        m = (a[:, 1] >= lo) & (a[:, 1] < hi)
+        d = (a[m, 2].astype(np.float64) - a[m, 1]) / 1e3
+        row.append((int(m.sum()), d.mean() if m.any() else 0.0, len(np.unique(a[m, 3]))))
+    print("%5.1f  %8d  %7.1f  %8d  %7.1f  %4d" % (k * 0.5, row[0][0], row[0][1], row[1][0], row[1][1], row[1][2]))
 os._exit(0)
