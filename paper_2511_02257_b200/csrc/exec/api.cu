@@ -15,6 +15,7 @@
 #include <cstring>
 #include <fstream>
 #include <map>
+#include <queue>
 #include <memory>
 #include <string>
 #include <vector>
@@ -522,8 +523,8 @@ void prepare_dataflow(cc_ctx* ctx) {
   // 2. sync slots and work items
   std::vector<int32_t> slot(size_t(n_ops), -1), target(size_t(n_ops), 0), df_index(size_t(n_ops), -1);
   int32_t n_sync = 0;
-  std::vector<DfOp> gops, tops;
-  std::vector<int32_t> gplan, tplan;   // plan op index of each DfOp
+  std::vector<DfOp> gops;
+  std::vector<int32_t> gplan;          // plan op index of each DfOp (one queue, plan order)
   std::vector<uint8_t> tmaps;
   int64_t g_items = 0, t_items = 0;
   int64_t n_chunked = 0, n_traced = 0;
@@ -548,7 +549,7 @@ void prepare_dataflow(cc_ctx* ctx) {
       const int64_t P = df_trace_pieces(Lt, N);
       d.kind = 1;
       d.n_items = int32_t(Lt * P);
-      d.first_item = t_items;
+      d.first_item = g_items;
       d.A = a;
       d.B = b;
       d.out = ctx->roots + int64_t(g.tree_of_root[size_t(op.node)]) * Lt;
@@ -563,10 +564,14 @@ void prepare_dataflow(cc_ctx* ctx) {
       if (trace_ring_user[size_t(r)] >= 0) ring_deps[size_t(i)].push_back(trace_ring_user[size_t(r)]);
       trace_ring_user[size_t(r)] = i;
       ++n_traced;
-      t_items += d.n_items;
-      df_index[size_t(i)] = int32_t(tops.size());
-      tops.push_back(d);
-      tplan.push_back(i);
+      d.tmap = int32_t(tmaps.size() / 256);
+      tmaps.resize(tmaps.size() + 256);
+      if (!df_encode_trace_maps(tmaps.data() + size_t(d.tmap) * 256, a, b, Lt, N))
+        throw Error(CC_E_CUDA, "TMA descriptor encoding failed");
+      g_items += d.n_items;
+      df_index[size_t(i)] = int32_t(gops.size());
+      gops.push_back(d);
+      gplan.push_back(i);
     } else {
       void* out = ctx->arena + op.dev_off;
       ZgemmProblem p = problem_for(n.op, Lt, N, g.S, a, b, out);
@@ -606,7 +611,67 @@ void prepare_dataflow(cc_ctx* ctx) {
     }
     target[size_t(i)] = d.n_items;
   }
-  // 3. dependency lists of compute ops, wait lists of copies
+  // 3. queue order: a topological order of the plan's ops (compute and copy; consecutive
+  // copies on one stream are chained, since a copy stream runs in plan order) that delays each
+  // TR_MM op by DF_TR_DELAY compute positions, so a trace item is usually claimed after its
+  // operand GEMMs completed (no worker blocks on it) while the GEMMs behind it keep the DMMA
+  // pipes busy.  Any topological order keeps the dataflow deadlock-free (dataflow.hpp).
+  {
+    static const int64_t delay = getenv("CC_DF_TR_DELAY") ? atoll(getenv("CC_DF_TR_DELAY")) : 8;
+    std::vector<std::vector<int32_t>> succ(static_cast<size_t>(n_ops));
+    std::vector<int32_t> indeg(static_cast<size_t>(n_ops), 0), rank(static_cast<size_t>(n_ops), 0);
+    int32_t last_copy[3] = {-1, -1, -1};
+    int32_t r = 0;
+    for (int32_t i = 0; i < n_ops; ++i) {
+      if (slot[size_t(i)] < 0) continue;
+      rank[size_t(i)] = r;
+      if (ops[size_t(i)].kind == OP_CONTRACT) ++r;
+      std::vector<int32_t> pre = deps[size_t(i)];
+      pre.insert(pre.end(), ring_deps[size_t(i)].begin(), ring_deps[size_t(i)].end());
+      if (ops[size_t(i)].kind != OP_CONTRACT) {
+        int32_t& lc = last_copy[ops[size_t(i)].stream];
+        if (lc >= 0) pre.push_back(lc);
+        lc = i;
+      }
+      std::sort(pre.begin(), pre.end());
+      pre.erase(std::unique(pre.begin(), pre.end()), pre.end());
+      for (int32_t j : pre)
+        if (slot[size_t(j)] >= 0) {
+          succ[size_t(j)].push_back(i);
+          ++indeg[size_t(i)];
+        }
+    }
+    auto key = [&](int32_t i) {
+      const PhysOp& op = ops[size_t(i)];
+      const bool tr = op.kind == OP_CONTRACT && g.nodes[size_t(op.node)].op == CC_TR_MM;
+      return int64_t(rank[size_t(i)]) + (tr ? delay : 0);
+    };
+    std::priority_queue<std::pair<int64_t, int32_t>, std::vector<std::pair<int64_t, int32_t>>, std::greater<>> ready;
+    for (int32_t i = 0; i < n_ops; ++i)
+      if (slot[size_t(i)] >= 0 && indeg[size_t(i)] == 0) ready.push({key(i), i});
+    std::vector<int32_t> order;
+    while (!ready.empty()) {
+      const int32_t i = ready.top().second;
+      ready.pop();
+      if (ops[size_t(i)].kind == OP_CONTRACT) order.push_back(i);
+      for (int32_t k : succ[size_t(i)])
+        if (--indeg[size_t(k)] == 0) ready.push({key(k), k});
+    }
+    if (order.size() != gops.size()) throw Error(CC_E_STATE, "dataflow: dependency cycle");
+    std::vector<DfOp> nops;
+    std::vector<int32_t> nplan;
+    int64_t first = 0;
+    for (int32_t i : order) {
+      DfOp d = gops[size_t(df_index[size_t(i)])];
+      d.first_item = first;
+      first += d.n_items;
+      nops.push_back(d);
+      nplan.push_back(i);
+    }
+    gops.swap(nops);
+    gplan.swap(nplan);
+  }
+  // 4. dependency lists of compute ops, wait lists of copies
   std::vector<int32_t> dep_slot, dep_target;
   auto fill_deps = [&](std::vector<DfOp>& v, const std::vector<int32_t>& plan) {
     for (size_t k = 0; k < v.size(); ++k) {
@@ -625,7 +690,6 @@ void prepare_dataflow(cc_ctx* ctx) {
     }
   };
   fill_deps(gops, gplan);
-  fill_deps(tops, tplan);
   ctx->df_copies.clear();
   std::vector<int32_t> copy_index(static_cast<size_t>(n_ops), -1);
   for (int32_t i = 0; i < n_ops; ++i) {
@@ -668,10 +732,10 @@ void prepare_dataflow(cc_ctx* ctx) {
   ctx->df_events.assign(ctx->df_copies.size(), nullptr);
   for (size_t k = 0; k < ctx->df_copies.size(); ++k)
     if (ctx->df_copies[k].source) ck(cudaEventCreateWithFlags(&ctx->df_events[k], cudaEventDisableTiming), "event");
-  // 4. upload metadata: [heads | sync][gops][tops][dep_slot][dep_target][tmaps]
+  // 5. upload metadata: [heads | sync][gops][tops][dep_slot][dep_target][tmaps]
   const size_t sz_sync = round_up(16 + int64_t(n_sync) * 4, 256);
   const size_t sz_g = round_up(int64_t(std::max<size_t>(gops.size(), 1) * sizeof(DfOp)), 256);
-  const size_t sz_t = round_up(int64_t(std::max<size_t>(tops.size(), 1) * sizeof(DfOp)), 256);
+  const size_t sz_t = 256;
   const size_t sz_d = round_up(int64_t(std::max<size_t>(dep_slot.size(), 1) * 4), 256);
   const size_t sz_m = round_up(int64_t(std::max<size_t>(tmaps.size(), 256)), 256);
   const size_t total = sz_sync + sz_g + sz_t + 2 * sz_d + sz_m;
@@ -688,7 +752,7 @@ void prepare_dataflow(cc_ctx* ctx) {
   char* pm = pdt + sz_d;
   ck(cudaMemset(m, 0, total), "dataflow metadata");
   if (!gops.empty()) ck(cudaMemcpy(pg, gops.data(), gops.size() * sizeof(DfOp), cudaMemcpyHostToDevice), "upload");
-  if (!tops.empty()) ck(cudaMemcpy(pt, tops.data(), tops.size() * sizeof(DfOp), cudaMemcpyHostToDevice), "upload");
+
   if (!dep_slot.empty()) {
     ck(cudaMemcpy(pds, dep_slot.data(), dep_slot.size() * 4, cudaMemcpyHostToDevice), "upload");
     ck(cudaMemcpy(pdt, dep_target.data(), dep_target.size() * 4, cudaMemcpyHostToDevice), "upload");
@@ -700,8 +764,9 @@ void prepare_dataflow(cc_ctx* ctx) {
     a->tmaps = pm;
     a->sync = ctx->df_sync;
   }
+  (void)pt;
   ctx->df_gemm.q = DfQueue{reinterpret_cast<const DfOp*>(pg), int32_t(gops.size()), g_items, heads};
-  ctx->df_trace.q = DfQueue{reinterpret_cast<const DfOp*>(pt), int32_t(tops.size()), t_items, heads + 1};
+  ctx->df_trace.q = DfQueue{reinterpret_cast<const DfOp*>(pt), 0, 0, heads + 1};
   ctx->df_gemm_items = g_items;
   ctx->df_trace_items = t_items;
   ctx->df_gemm.prof = nullptr;
@@ -744,18 +809,9 @@ int issue_dataflow(cc_ctx* ctx) {
     if (c.source) ck(cudaEventRecord(ctx->df_events[k], s), "event");
   }
   DBG("copies enqueued");
-  // Each worker is sized to one CTA per SM and the two are meant to share every SM (DMMA
-  // tiles + streaming traces).  Grids of num_sms - 2 keep two SMs free of each kind, so
-  // both workers always have a resident CTA even if co-residency were impossible: items
-  // only wait on earlier items, so progress is then guaranteed (dataflow.hpp).
-  const int grid = std::max(1, ctx->num_sms - 2);
   if (ctx->df_gemm_items > 0) {
-    ck(df_launch_gemm(ctx->df_gemm, grid, ctx->cs), "gemm worker");
-    DBG("gemm worker launched");
-    ++nl;
-  }
-  if (ctx->df_trace_items > 0) {
-    ck(df_launch_trace(ctx->df_trace, grid, ctx->cs2), "trace worker");
+    ck(df_launch(ctx->df_gemm, ctx->num_sms, ctx->cs), "dataflow worker");
+    DBG("worker launched");
     ++nl;
   }
   DBG("workers launched");

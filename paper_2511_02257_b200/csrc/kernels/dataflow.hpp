@@ -1,14 +1,13 @@
-// Dataflow execution of a whole plan by persistent worker kernels (host/device shared PODs).
+// Dataflow execution of a whole plan by a persistent worker kernel (host/device shared PODs).
 //
-// The plan's contractions become work items in two queues, in plan order: GEMM tiles
-// (MM1/BM1/BB2; a tile may be split into k-chunks) for the DMMA worker, and TR_MM unit
-// ranges for the trace worker.  Both workers are persistent (one CTA per SM each, sized to
-// be co-resident on an SM), grab items with an atomic queue head, and before an item spin
-// on the integer sync slots of the items' op dependencies: done counters of earlier ops
-// (RAW on operands, WAR/WAW on reused pool memory) and completion flags written by the copy
-// streams after an H2D (cuStreamWriteValue32).  Items only ever wait on earlier plan
-// positions and every queue is dispatched in order, so the earliest unfinished item always
-// has its dependencies satisfied: the execution cannot deadlock.
+// The plan's contractions become work items of one queue, in plan order: GEMM tiles
+// (MM1/BM1/BB2; a tile may be split into k-chunks) and TR_MM block-pair ranges.  The worker
+// is persistent (one CTA per SM), grabs items with an atomic queue head, and before an item
+// its producer warp spins on the integer sync slots of the item's op dependencies: done
+// counters of earlier ops (RAW on operands, WAR/WAW on reused pool memory) and completion
+// flags written by the copy streams after a copy (cuStreamWriteValue32).  Items only ever
+// wait on earlier plan positions and the queue is dispatched in order, so the earliest
+// unfinished item always has its dependencies satisfied: the execution cannot deadlock.
 #pragma once
 #include <cstdint>
 
@@ -47,7 +46,7 @@ struct DfQueue {
 };
 
 struct DfArgs {
-  DfQueue q;
+  DfQueue q;                  // items of every op, in plan order
   const int32_t* dep_slot;    // sync slot an op waits on
   const int32_t* dep_target;  // value the slot must reach
   const void* tmaps;          // CUtensorMap array (64-byte aligned, global memory)
@@ -56,15 +55,15 @@ struct DfArgs {
 };
 
 cudaError_t df_preload();
-// Launch the persistent workers (stream-ordered; the sync area must be zero).
-size_t df_gemm_smem_bytes();
-cudaError_t df_launch_gemm(const DfArgs& a, int grid, cudaStream_t s);
-cudaError_t df_launch_trace(const DfArgs& a, int grid, cudaStream_t s);
+// Launch the persistent worker (stream-ordered; the sync area must be zero).
+cudaError_t df_launch(const DfArgs& a, int grid, cudaStream_t s);
 // Tile / chunk geometry the builder needs (matches the worker's Cfg).
 void df_gemm_tile_dims(int* BM, int* BN, int* BK, int* slot_doubles);
 int df_trace_block();
 // Encode the TMA maps of one GEMM problem into dst[0] (A) and dst[1] (B).
 bool df_encode_maps(void* dst, const void* A, const void* B, int64_t M, int64_t Nn, int64_t Kin, int64_t Ko,
                     int64_t batch, int64_t lda, int64_t sAo, int64_t sAb, int64_t ldb, int64_t sBo, int64_t sBb);
+// TMA maps of a TR_MM op's operands ([Lt][N][N] complex, 32-row boxes).
+bool df_encode_trace_maps(void* dst, const void* A, const void* B, int64_t Lt, int64_t N);
 
 }  // namespace cc

@@ -121,7 +121,7 @@ def test_c1_all_ones_exact():
     w = dags.config_c1()
     _, roots, corr, st, ex = run_gpu(w, leaf_fn=lambda u, op: np.ones((w.Lt, w.N, w.N), complex))
     assert np.array_equal(roots[0], np.full(w.Lt, float(w.N) ** 4, complex))     # N^4 = 2^20
-    assert ex["n_kernels"] >= 3
+    assert ex["n_kernels"] >= 2
 
 
 def test_c1_synthetic():

@@ -27,7 +27,8 @@ for (u, op, a, b, s) in w.nodes:
 for _ in range(3):
     ctx.execute(0)
 ex = ctx.execute(cc.EXEC_PROFILE)
-g, t = ctx.dataflow_profile()
+g0, _ = ctx.dataflow_profile()
+g, t = g0[g0[:, 6] == 0], g0[g0[:, 6] == 1]
 t0 = min(g[:, 0].min() if len(g) else 2**63, t[:, 0].min() if len(t) else 2**63)
 t1 = max(g[:, 2].max() if len(g) else 0, t[:, 2].max() if len(t) else 0)
 span = (t1 - t0) / 1e3
@@ -37,7 +38,7 @@ for name, a in (("gemm", g), ("trace", t)):
         continue
     a = a.astype(np.float64)
     wait = (a[:, 1] - a[:, 0]) / 1e3
-    work = (a[:, 2] - a[:, 1]) / 1e3
+    work = (a[:, 2] - a[:, 4]) / 1e3
     sms = len(np.unique(a[:, 3]))
     print("%-5s items %6d on %3d SMs: work %.1f us avg (sum %.2f ms), dep-wait %.2f us avg (sum %.2f ms), "
           "busy %.1f%% of %d SMs x span" % (name, len(a), sms, work.mean(), work.sum() / 1e3, wait.mean(),
@@ -45,11 +46,14 @@ for name, a in (("gemm", g), ("trace", t)):
     # per-SM timeline occupancy gaps
     q = np.percentile(work, [10, 50, 90, 99])
     print("      work percentiles 10/50/90/99: %s us" % np.round(q, 1))
-    if name == "gemm":
-        fill = (a[:, 4] - a[:, 1]) / 1e3
-        loop = (a[:, 5] - a[:, 4]) / 1e3
-        epi = (a[:, 2] - a[:, 5]) / 1e3
-        print("      fill %.2f us, k-loop %.2f us, epilogue+publish %.2f us (avg)" % (fill.mean(), loop.mean(), epi.mean()))
+    # consumer side: start (info received) -> first data -> end of stage loop -> end
+    wait_data = (a[:, 7] - a[:, 4]) / 1e3
+    loop = (a[:, 5] - a[:, 7]) / 1e3
+    epi = (a[:, 2] - a[:, 5]) / 1e3
+    busy = (a[:, 2] - a[:, 4]) / 1e3
+    print("      consumer: wait first data %.2f us, stage loop %.2f us, epilogue+publish %.2f us, total %.2f us"
+          % (wait_data.mean(), loop.mean(), epi.mean(), busy.mean()))
+    print("      consumer busy %.1f%% of SM x span" % (100 * busy.sum() / (sms * span)))
     first = (a[:, 0].min() - t0) / 1e3
     last = (a[:, 2].max() - t0) / 1e3
     print("      first dispatch at %.1f us, last end at %.1f us" % (first, last))
