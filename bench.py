@@ -179,6 +179,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2511_02257_b200 import cc
+    from paper_2511_02257_b200.dist import allreduce_correlators
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -227,9 +228,7 @@ def main():
         ctx.execute_async(cc.EXEC_GRAPH)
         if world > 1:
             with torch.cuda.stream(cs):
-                corr_full.zero_()
-                corr_full[:, t0:t1].copy_(corr_view)
-                dist.all_reduce(corr_full)
+                allreduce_correlators(corr_view, t0, t1, w.Lt, out=corr_full)
 
     # first execute builds the graph; bind the correlator buffer view for the all-reduce
     ctx.execute(cc.EXEC_GRAPH)
@@ -258,15 +257,33 @@ def main():
         dist.barrier()
     step_s = [a.elapsed_time(b) * 1e-3 for a, b in times]
     t_value = float(np.sum(step_s))
-    n_kernels_step = None
 
-    # ---- roofline of the dominant kernel: the plan's MM1 launches alone, replayed in plan
-    # order as a CUDA graph on the compute stream right after the timed region (CUDA events
-    # around the replay; no host launch overhead), and the same for TR_MM ------------------
-    ctx.execute(cc.EXEC_GRAPH)                      # operands in place
+    # ---- roofline of the dominant kernel.  The step runs as ONE persistent launch of
+    # df_worker (every MM1 tile and TR_MM block pair of the plan) + a tiny correlator kernel.
+    # Launch duration: CUDA events on the compute stream around stream-mode replays (flags 0:
+    # memset + df_worker + correlate; the worker is > 99 % of it), L2 flushed before each,
+    # right after the timed region. ---------------------------------------------------------------
+    ex0 = ctx.execute(0)
     n_kernels_step = ctx.execute(cc.EXEC_GRAPH)["n_kernels"]
-    g_s, g_n, t_s, t_n = 0.0, 0, 0.0, 0
-    ctx.execute(cc.EXEC_ONLY_GEMM)                  # builds the replay graph
+    wt = []
+    for _ in range(3):
+        with torch.cuda.stream(cs):
+            flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(cs)
+        ctx.execute_async(0)
+        e1.record(cs)
+        e1.synchronize()
+        wt.append(e0.elapsed_time(e1) * 1e-3)
+    worker_t = float(np.median(wt))
+    step_flops = ex0["flops"]
+    step_hbm = ex0["hbm_bytes"]
+    # component kernels alone (op-by-op path, flags 4/8: the plan's MM1 / TR_MM launches of the
+    # stand-alone kernels replayed as CUDA graphs): kernel quality, not the step
+    g_s = t_s = 0.0
+    g_n = t_n = 0
+    ctx.execute(cc.EXEC_ONLY_GEMM)
     ctx.execute(cc.EXEC_ONLY_TRACE)
     for _ in range(3):
         with torch.cuda.stream(cs):
@@ -283,7 +300,6 @@ def main():
     tr_avg = t_s / max(t_n, 1)
     Lt_k, N = Lt_p, w.N
     mm1_flops = 8.0 * Lt_k * N ** 3
-    step_flops = eg["flops"] + et["flops"]
     step_mean = t_value / args.steps
 
     # ---- e2e: the public API from pinned host buffers ------------------------------------------------
@@ -328,7 +344,8 @@ def main():
 
     if rank == 0:
         peak, peak_src = fp64_peak()
-        achieved = mm1_flops / mm1_avg / 1e12 if mm1_avg > 0 else None
+        hbm_peak = measured_hbm()
+        achieved = step_flops / worker_t / 1e12
         line = {
             "metric": "correlator time-to-solution", "value": t_value / args.steps, "unit": "s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -337,17 +354,28 @@ def main():
             "e2e": {"value": t_e2e / args.steps, "unit": "s", "h2d_bytes_per_step": int(h2d_step),
                     "d2h_bytes_per_step": int(d2h_step)},
             "gpu_launches": int(n_kernels_step * args.steps),
-            "contraction_tflops": step_flops / (t_value / args.steps) / 1e12,
-            "roofline": {"bound": "tensor", "kernel": "zgemm_dmma (MM1, N=%d, Lt=%d)" % (N, Lt_k),
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak if achieved else None, "traffic": ncu_traffic(),
-                         "peak_source": peak_src, "mm1_avg_us": mm1_avg * 1e6, "tr_avg_us": tr_avg * 1e6,
-                         "mm1_share_of_step": (g_s / 3) / step_mean,
-                         "tr_achieved_gbs": 32.0 * Lt_k * N * N / tr_avg / 1e9 if tr_avg > 0 else None,
-                         "tr_frac_of_hbm": (32.0 * Lt_k * N * N / tr_avg / 1e9) / 6538.9 if tr_avg > 0 else None,
-                         "how": "cc_execute flags 4/8: the plan's MM1 (resp. TR_MM) launches alone, in plan order, "
-                                "as a CUDA graph on the compute stream, CUDA events around it; L2 flushed before; "
-                                "3 replays right after the timed region; avg = time / launches"},
+            "contraction_tflops": step_flops / step_mean / 1e12,
+            "roofline": {"bound": "tensor",
+                         "kernel": "df_worker (one persistent dataflow launch per step: every MM1 tile and "
+                                   "TR_MM block pair of the plan; FP64 DMMA + DFMA)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": ncu_traffic(), "peak_source": peak_src,
+                         "algorithmic": {"flops_per_launch": step_flops, "hbm_bytes_per_launch": step_hbm},
+                         "launch_ms": worker_t * 1e3,
+                         "bound_ms": {"fp64": step_flops / (peak * 1e12) * 1e3,
+                                      "hbm": step_hbm / (hbm_peak * 1e9) * 1e3},
+                         "hbm_achieved_gbs": step_hbm / worker_t / 1e9,
+                         "how": "CUDA events on the compute stream around stream-mode replays (df_worker + "
+                                "memset + correlator kernel), L2 flushed before, 3 replays after the timed region; "
+                                "achieved = algorithmic FP64 flops (8 per complex MAC) / launch time",
+                         "components": {
+                             "mm1_zgemm_alone": {"avg_us": mm1_avg * 1e6, "tflops": mm1_flops / mm1_avg / 1e12,
+                                                 "frac": mm1_flops / mm1_avg / 1e12 / peak},
+                             "tr_mm_alone": {"avg_us": tr_avg * 1e6,
+                                             "gbs": 32.0 * Lt_k * N * N / tr_avg / 1e9,
+                                             "frac": 32.0 * Lt_k * N * N / tr_avg / 1e9 / hbm_peak},
+                             "how": "op-by-op path (cc_execute flags 4/8): the plan's MM1 / TR_MM launches of the "
+                                    "stand-alone kernels replayed alone as CUDA graphs, L2 flushed before"}},
             "plan": {"peak_bytes": pst["peak"], "transient_peak_bytes": pst["transient_peak"],
                      "evictions": pst["evictions"], "h2d_bytes": pst["h2d_bytes"], "d2h_bytes": pst["d2h_bytes"],
                      "sched_ms": pst["sched_seconds"] * 1e3, "plan_ms": pst["plan_seconds"] * 1e3},
@@ -382,11 +410,19 @@ def fp64_peak():
         return 37.0, "fallback: DMMA microbenchmark of round 1 (profiles/r01_microbench_fp64_pcie.txt)"
 
 
+def measured_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6650.0   # B200_PROFILING.md fallback
+
+
 def ncu_traffic():
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
-            return json.load(f).get("zgemm_traffic_bytes_per_launch")
+            return json.load(f).get("df_worker_traffic_bytes_per_launch")
     except (OSError, ValueError):
         return None
 

@@ -299,11 +299,12 @@ void df_gemm_geometry(const ZgemmProblem& p, int64_t& tiles, int64_t& KT, int64_
   }
 }
 
-// Pieces per time slice of a TR op: ~16 blocks of 32x32 (512 KB of operands) per item.
+// Pieces per time slice of a TR op: ~DF_TR_UNITS blocks of 32x32 (32 KB each) per item.
 int64_t df_trace_pieces(int64_t Lt, int64_t N) {
+  static const int64_t units = getenv("CC_DF_TR_UNITS") ? std::max(1LL, atoll(getenv("CC_DF_TR_UNITS"))) : 16;
   const int64_t nb = (N + 31) / 32, U = nb * nb;
   (void)Lt;
-  return std::max<int64_t>(1, (U + 15) / 16);
+  return std::max<int64_t>(1, (U + units - 1) / units);
 }
 
 // Sets up scratch (kernel workspace, roots, correlators, term tables), the physical plan,

@@ -29,7 +29,8 @@ namespace {
 using namespace dev;
 
 using GC = Cfg<64, 64, 16, 32, 16, 5>;     // 5 x 32 KB stages
-constexpr int CW = GC::NCW * 32;           // 256 consumer threads (+1 producer warp)
+constexpr int CW = GC::NCW * 32;           // 256 consumer threads (+ producer warp + publisher warp)
+constexpr int NT = CW + 64;
 constexpr int TB = 32;                     // trace block edge (complex)
 constexpr int INFO = 4;                    // decoded items in flight producer -> consumers
 static_assert(GC::A_BYTES == TB * TB * 16 && GC::B_BYTES == TB * TB * 16, "a trace block pair fills one stage");
@@ -93,7 +94,8 @@ struct ItemInfo {
   int32_t op, kind, npos; // npos: stages the item consumes
   int32_t tm, tn, b, k0, kt_per_o, chunk;   // GEMM
   int32_t t, u0, nb, piece;                 // TRACE
-  unsigned long long t_disp, t_ready;       // profiling
+  unsigned long long t_disp, t_ready;       // profiling (producer)
+  unsigned long long t_start, t_first, t_comp;  // profiling (consumers)
 };
 
 // Decode `item` (hint: the op of the previous item; consecutive items usually share it).
@@ -135,7 +137,9 @@ __device__ __forceinline__ int decode_item(const DfArgs& a, int64_t item, ItemIn
   return oi;
 }
 
-__global__ void __launch_bounds__(CW + 32, 1) df_worker(DfArgs a) {
+// launch bounds of 12 warps although 10 run: caps registers at 168 (3 warps per SM
+// sub-partition x 32 x 168 <= 16K registers each)
+__global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
   using C = GC;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned stage base, derived from the __shared__ array by pointer arithmetic so
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(CW + 32, 1) df_worker(DfArgs a) {
     }
     for (int s = 0; s < INFO; ++s) {
       mbar_init(&info_full[s], 1);
-      mbar_init(&info_empty[s], C::NCW);
+      mbar_init(&info_empty[s], 1);    // released by the publisher warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -210,6 +214,40 @@ __global__ void __launch_bounds__(CW + 32, 1) df_worker(DfArgs a) {
           }
         }
       }
+    }
+    return;
+  }
+  if (warp == C::NCW + 1) {
+    // --------------------------------- publisher ------------------------------------------
+    // Completion of item n: the consumers arrive on named barrier 2 + slot after their last
+    // store and go on with item n+1; this warp syncs on it (acquiring their stores), makes
+    // them visible at GPU scope (cumulative fence) and bumps the op's done counter — the
+    // fence's drain latency leaves the consumers' critical path.  A slot (and its barrier)
+    // is reused only after this warp releases info_empty, so at most INFO items are pending.
+    for (uint32_t n = 0;; ++n) {
+      const int slot = int(n % INFO);
+      mbar_wait(&info_full[slot], (n / INFO) & 1u);
+      const ItemInfo& cur = s_info[slot];
+      const int64_t item = cur.item;
+      if (item >= a.q.n_items) break;
+      asm volatile("bar.sync %0, %1;" ::"r"(2 + slot), "r"(CW + 32) : "memory");
+      if (lane == 0) {
+        __threadfence();
+        atomicAdd(a.sync + a.q.ops[cur.op].sync_id, 1);
+        if (a.prof) {
+          unsigned long long* pr = a.prof + 8 * item;
+          pr[0] = cur.t_disp;
+          pr[1] = cur.t_ready;
+          pr[2] = gtimer();
+          pr[3] = smid();
+          pr[4] = cur.t_start;
+          pr[5] = cur.t_comp;
+          pr[6] = cur.kind;
+          pr[7] = cur.t_first;
+        }
+        mbar_arrive(&info_empty[slot]);
+      }
+      __syncwarp();
     }
     return;
   }
@@ -375,24 +413,14 @@ __global__ void __launch_bounds__(CW + 32, 1) df_worker(DfArgs a) {
       }
     }
 
-    named_sync(1, CW);
-    if (tid == 0) {
-      __threadfence();   // cumulative: the consumers' stores (ordered by the barrier) before the count
-      atomicAdd(a.sync + op.sync_id, 1);
-      if (a.prof) {
-        unsigned long long* pr = a.prof + 8 * item;
-        pr[0] = cur.t_disp;
-        pr[1] = cur.t_ready;
-        pr[2] = gtimer();
-        pr[3] = smid();
-        pr[4] = t_start;
-        pr[5] = t_comp;
-        pr[6] = cur.kind;
-        pr[7] = t_first;
-      }
+    if (tid == 0 && a.prof) {
+      ItemInfo& w = s_info[slot];
+      w.t_start = t_start;
+      w.t_first = t_first;
+      w.t_comp = t_comp;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&info_empty[slot]);
+    // release the item to the publisher (barrier arrive orders this thread's stores before it)
+    asm volatile("bar.arrive %0, %1;" ::"r"(2 + slot), "r"(CW + 32) : "memory");
   }
 }
 
@@ -415,7 +443,7 @@ void df_gemm_tile_dims(int* BM, int* BN, int* BK, int* slot_doubles) {
 int df_trace_block() { return TB; }
 
 cudaError_t df_launch(const DfArgs& a, int grid, cudaStream_t s) {
-  df_worker<<<grid, CW + 32, GC::SMEM, s>>>(a);
+  df_worker<<<grid, NT, GC::SMEM, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -54,9 +54,21 @@ for name, a in (("gemm", g), ("trace", t)):
     print("      consumer: wait first data %.2f us, stage loop %.2f us, epilogue+publish %.2f us, total %.2f us"
           % (wait_data.mean(), loop.mean(), epi.mean(), busy.mean()))
     print("      consumer busy %.1f%% of SM x span" % (100 * busy.sum() / (sms * span)))
+    print("      wait-first-data percentiles 10/50/90/99: %s us" % np.round(np.percentile(wait_data, [10, 50, 90, 99]), 2))
     first = (a[:, 0].min() - t0) / 1e3
     last = (a[:, 2].max() - t0) / 1e3
     print("      first dispatch at %.1f us, last end at %.1f us" % (first, last))
+# per SM: consumer timeline (all kinds): loop time vs gaps between one item's loop end and the
+# next item's first data
+allp = g0.astype(np.float64)
+loop_sum, gap_sum = 0.0, 0.0
+for smv in np.unique(allp[:, 3]):
+    r = allp[allp[:, 3] == smv]
+    r = r[np.argsort(r[:, 4])]
+    loop_sum += (r[:, 5] - r[:, 7]).sum()
+    gap_sum += (r[1:, 7] - r[:-1, 5]).sum()
+print("consumers: stage loops %.1f%%, between loops %.1f%% of summed per-SM time"
+      % (100 * loop_sum / (loop_sum + gap_sum), 100 * gap_sum / (loop_sum + gap_sum)))
 # time bins: items running and mean duration per 0.5 ms
 span_ns = t1 - t0
 nb = int(span_ns // 500000) + 1
