@@ -188,9 +188,12 @@ cc_status cc_kernel_times(cc_ctx* ctx, double* seconds, int64_t* counts);
 cc_status cc_dataflow_state(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out);
 
 /* Per-item timeline of the last cc_execute with flags bit 5 (dataflow profiling): for every
- * work item (GEMM queue first, then TR queue) 8 uint64: dispatch, dependencies-ready and end
- * times (%globaltimer, ns), the SM id, and for GEMM items the first-operand-arrival and
- * end-of-k-loop times.  out may be NULL (size query: 8*(n_gemm+n_trace)). */
+ * work item (GEMM queue first, then TR queue) 8 uint64: claim, dependencies-ready and
+ * published times (%globaltimer, ns), the SM id, first-operand-arrival and end-of-stage-loop
+ * times, the kind (0 GEMM, 1 TR_MM) and the first-arrival time again; then one record per
+ * worker CTA: consumer cycles (clock64) waiting for GEMM / TR_MM stage data, cycles in GEMM /
+ * TR_MM stage math and epilogues, GEMM / TR_MM stages consumed, SM id.  out may be NULL
+ * (size query: 8*(n_gemm+n_trace+num_sms)). */
 cc_status cc_dataflow_profile(cc_ctx* ctx, uint64_t* out, int64_t cap, int64_t* n_gemm, int64_t* n_trace);
 
 /* Results.  out: 2*Lt_part doubles (interleaved complex) for the current part. */

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcc.so")
+LIB_PATH = os.environ.get("CC_LIB") or os.path.join(_HERE, "libcc.so")   # CC_LIB: experiment builds
 if not os.path.exists(LIB_PATH):
     raise ImportError("libcc.so not built (run python -c 'import __graft_entry__ as g; g.build()'): %s" % LIB_PATH)
 _lib = ctypes.CDLL(LIB_PATH)
@@ -289,15 +289,21 @@ class Context:
         self._ck(_lib.cc_dataflow_state(self._h, out, n.value, ctypes.byref(n)))
         return list(out[:n.value])
 
-    def dataflow_profile(self):
-        """(gemm_items, trace_items) arrays [n, 8]: dispatch, ready, end (ns), smid, first data, k-loop end."""
+    def dataflow_profile(self, per_sm=False):
+        """(gemm_items, trace_items) arrays [n, 8]: claim, ready, published (ns), smid, first data,
+        stage-loop end, kind; with per_sm also the per-CTA cycle counters [num_sms, 8] (cc.h)."""
         ng, nt = c_i64(), c_i64()
         self._ck(_lib.cc_dataflow_profile(self._h, None, 0, ctypes.byref(ng), ctypes.byref(nt)))
         n = ng.value + nt.value
-        out = np.zeros(8 * max(n, 1), dtype=np.uint64)
-        self._ck(_lib.cc_dataflow_profile(self._h, out.ctypes.data_as(P(c_u64)), 8 * n, ctypes.byref(ng),
+        n_all = n + 1024  # + one record per worker CTA (at most 1024 SMs)
+        out = np.zeros(8 * n_all, dtype=np.uint64)
+        self._ck(_lib.cc_dataflow_profile(self._h, out.ctypes.data_as(P(c_u64)), 8 * n_all, ctypes.byref(ng),
                                           ctypes.byref(nt)))
         a = out[:8 * n].reshape(n, 8)
+        if per_sm:
+            sm = out[8 * n:].reshape(-1, 8).view(np.int64)
+            sm = sm[(sm[:, 4] + sm[:, 5]) > 0]
+            return a[:ng.value], a[ng.value:], sm
         return a[:ng.value], a[ng.value:]
 
     def correlator(self, corr_id, Lt):

@@ -104,7 +104,7 @@ struct cc_ctx {
   bool df_valid = false;
   char* df_meta = nullptr;          // cudaMalloc: ops, deps, tensor maps, sync area
   size_t df_meta_bytes = 0;
-  DfArgs df_gemm{}, df_trace{};
+  DfArgs df_gemm{};                 // the dataflow worker's arguments (both queues)
   int* df_sync = nullptr;           // zeroed per launch (with the two queue heads before it)
   size_t df_sync_bytes = 0;
   char* df_chunk_ws = nullptr;      // arena scratch: chunk partial rings, trace partial rings
@@ -524,8 +524,8 @@ void prepare_dataflow(cc_ctx* ctx) {
   // 2. sync slots and work items
   std::vector<int32_t> slot(size_t(n_ops), -1), target(size_t(n_ops), 0), df_index(size_t(n_ops), -1);
   int32_t n_sync = 0;
-  std::vector<DfOp> gops;
-  std::vector<int32_t> gplan;          // plan op index of each DfOp (one queue, plan order)
+  std::vector<DfOp> gops, tops;
+  std::vector<int32_t> gplan, tplan;   // plan op index of each DfOp (queue order)
   std::vector<uint8_t> tmaps;
   int64_t g_items = 0, t_items = 0;
   int64_t n_chunked = 0, n_traced = 0;
@@ -659,18 +659,29 @@ void prepare_dataflow(cc_ctx* ctx) {
         if (--indeg[size_t(k)] == 0) ready.push({key(k), k});
     }
     if (order.size() != gops.size()) throw Error(CC_E_STATE, "dataflow: dependency cycle");
-    std::vector<DfOp> nops;
-    std::vector<int32_t> nplan;
-    int64_t first = 0;
+    std::vector<DfOp> nops, tops_v;
+    std::vector<int32_t> nplan, tplan_v;
+    int64_t first = 0, tfirst = 0;
     for (int32_t i : order) {
       DfOp d = gops[size_t(df_index[size_t(i)])];
-      d.first_item = first;
-      first += d.n_items;
-      nops.push_back(d);
-      nplan.push_back(i);
+      if (d.kind == 0) {
+        d.first_item = first;
+        first += d.n_items;
+        nops.push_back(d);
+        nplan.push_back(i);
+      } else {
+        d.first_item = tfirst;
+        tfirst += d.n_items;
+        tops_v.push_back(d);
+        tplan_v.push_back(i);
+      }
     }
     gops.swap(nops);
     gplan.swap(nplan);
+    tops.swap(tops_v);
+    tplan.swap(tplan_v);
+    g_items = first;
+    t_items = tfirst;
   }
   // 4. dependency lists of compute ops, wait lists of copies
   std::vector<int32_t> dep_slot, dep_target;
@@ -691,6 +702,7 @@ void prepare_dataflow(cc_ctx* ctx) {
     }
   };
   fill_deps(gops, gplan);
+  fill_deps(tops, tplan);
   ctx->df_copies.clear();
   std::vector<int32_t> copy_index(static_cast<size_t>(n_ops), -1);
   for (int32_t i = 0; i < n_ops; ++i) {
@@ -736,10 +748,16 @@ void prepare_dataflow(cc_ctx* ctx) {
   // 5. upload metadata: [heads | sync][gops][tops][dep_slot][dep_target][tmaps]
   const size_t sz_sync = round_up(16 + int64_t(n_sync) * 4, 256);
   const size_t sz_g = round_up(int64_t(std::max<size_t>(gops.size(), 1) * sizeof(DfOp)), 256);
-  const size_t sz_t = 256;
+  const size_t sz_t = round_up(int64_t(std::max<size_t>(tops.size(), 1) * sizeof(DfOp)), 256);
   const size_t sz_d = round_up(int64_t(std::max<size_t>(dep_slot.size(), 1) * 4), 256);
   const size_t sz_m = round_up(int64_t(std::max<size_t>(tmaps.size(), 256)), 256);
-  const size_t total = sz_sync + sz_g + sz_t + 2 * sz_d + sz_m;
+  std::vector<int32_t> gitem_op(size_t(std::max<int64_t>(g_items, 1)), 0), titem_op(size_t(std::max<int64_t>(t_items, 1)), 0);
+  for (size_t k = 0; k < gops.size(); ++k)
+    std::fill(gitem_op.begin() + gops[k].first_item, gitem_op.begin() + gops[k].first_item + gops[k].n_items, int32_t(k));
+  for (size_t k = 0; k < tops.size(); ++k)
+    std::fill(titem_op.begin() + tops[k].first_item, titem_op.begin() + tops[k].first_item + tops[k].n_items, int32_t(k));
+  const size_t sz_gi = round_up(int64_t(gitem_op.size() * 4), 256), sz_ti = round_up(int64_t(titem_op.size() * 4), 256);
+  const size_t total = sz_sync + sz_g + sz_t + 2 * sz_d + sz_m + sz_gi + sz_ti;
   ck(cudaMalloc(reinterpret_cast<void**>(&ctx->df_meta), total), "dataflow metadata");
   ctx->df_meta_bytes = total;
   char* m = ctx->df_meta;
@@ -751,27 +769,41 @@ void prepare_dataflow(cc_ctx* ctx) {
   char* pds = pt + sz_t;
   char* pdt = pds + sz_d;
   char* pm = pdt + sz_d;
+  char* pgi = pm + sz_m;
+  char* pti = pgi + sz_gi;
   ck(cudaMemset(m, 0, total), "dataflow metadata");
+  ck(cudaMemcpy(pgi, gitem_op.data(), gitem_op.size() * 4, cudaMemcpyHostToDevice), "upload");
+  ck(cudaMemcpy(pti, titem_op.data(), titem_op.size() * 4, cudaMemcpyHostToDevice), "upload");
   if (!gops.empty()) ck(cudaMemcpy(pg, gops.data(), gops.size() * sizeof(DfOp), cudaMemcpyHostToDevice), "upload");
+  if (!tops.empty()) ck(cudaMemcpy(pt, tops.data(), tops.size() * sizeof(DfOp), cudaMemcpyHostToDevice), "upload");
 
   if (!dep_slot.empty()) {
     ck(cudaMemcpy(pds, dep_slot.data(), dep_slot.size() * 4, cudaMemcpyHostToDevice), "upload");
     ck(cudaMemcpy(pdt, dep_target.data(), dep_target.size() * 4, cudaMemcpyHostToDevice), "upload");
   }
   if (!tmaps.empty()) ck(cudaMemcpy(pm, tmaps.data(), tmaps.size(), cudaMemcpyHostToDevice), "upload");
-  for (DfArgs* a : {&ctx->df_gemm, &ctx->df_trace}) {
-    a->dep_slot = reinterpret_cast<const int32_t*>(pds);
-    a->dep_target = reinterpret_cast<const int32_t*>(pdt);
-    a->tmaps = pm;
-    a->sync = ctx->df_sync;
+  DfArgs& da = ctx->df_gemm;
+  da.dep_slot = reinterpret_cast<const int32_t*>(pds);
+  da.dep_target = reinterpret_cast<const int32_t*>(pdt);
+  da.tmaps = pm;
+  da.sync = ctx->df_sync;
+  da.q = DfQueue{reinterpret_cast<const DfOp*>(pg), reinterpret_cast<const int32_t*>(pgi), int32_t(gops.size()),
+                 g_items, heads};
+  da.qt = DfQueue{reinterpret_cast<const DfOp*>(pt), reinterpret_cast<const int32_t*>(pti), int32_t(tops.size()),
+                  t_items, heads + 1};
+  {
+    auto env_int = [](const char* k, int dflt, int lo, int hi) {
+      const char* v = getenv(k);
+      return std::min(std::max(v ? atoi(v) : dflt, lo), hi);
+    };
+    da.tr_ratio = env_int("CC_DF_TR_RATIO", 2, 0, 64);
+    da.ahead_g = env_int("CC_DF_AHEAD_G", 2, 1, 4);
+    da.ahead_t = env_int("CC_DF_AHEAD_T", 2, 1, 4);
   }
-  (void)pt;
-  ctx->df_gemm.q = DfQueue{reinterpret_cast<const DfOp*>(pg), int32_t(gops.size()), g_items, heads};
-  ctx->df_trace.q = DfQueue{reinterpret_cast<const DfOp*>(pt), 0, 0, heads + 1};
   ctx->df_gemm_items = g_items;
   ctx->df_trace_items = t_items;
-  ctx->df_gemm.prof = nullptr;
-  ctx->df_trace.prof = nullptr;
+  da.prof = nullptr;
+  da.prof_t = nullptr;
   if (!ctx->cs2) {
     ck(cudaStreamCreateWithFlags(&ctx->cs2, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&ctx->ev_cs2, cudaEventDisableTiming), "event");
@@ -810,7 +842,7 @@ int issue_dataflow(cc_ctx* ctx) {
     if (c.source) ck(cudaEventRecord(ctx->df_events[k], s), "event");
   }
   DBG("copies enqueued");
-  if (ctx->df_gemm_items > 0) {
+  if (ctx->df_gemm_items + ctx->df_trace_items > 0) {
     ck(df_launch(ctx->df_gemm, ctx->num_sms, ctx->cs), "dataflow worker");
     DBG("worker launched");
     ++nl;
@@ -991,12 +1023,13 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
     prepare_dataflow(ctx);
     const bool prof = (flags & 32) != 0;
     if (prof && !ctx->df_prof) {
-      const int64_t n = ctx->df_gemm_items + ctx->df_trace_items;
-      ck(cudaMalloc(reinterpret_cast<void**>(&ctx->df_prof), size_t(std::max<int64_t>(n, 1)) * 64), "profile buffer");
-      ck(cudaMemset(ctx->df_prof, 0, size_t(std::max<int64_t>(n, 1)) * 64), "profile buffer");
+      const int64_t n = ctx->df_gemm_items + ctx->df_trace_items + ctx->num_sms;
+      ck(cudaMalloc(reinterpret_cast<void**>(&ctx->df_prof), size_t(n) * 64), "profile buffer");
+      ck(cudaMemset(ctx->df_prof, 0, size_t(n) * 64), "profile buffer");
     }
     ctx->df_gemm.prof = prof ? ctx->df_prof : nullptr;
-    ctx->df_trace.prof = prof ? ctx->df_prof + 8 * ctx->df_gemm_items : nullptr;
+    ctx->df_gemm.prof_t = prof ? ctx->df_prof + 8 * ctx->df_gemm_items : nullptr;
+    ctx->df_gemm.prof_sm = prof ? reinterpret_cast<long long*>(ctx->df_prof + 8 * (ctx->df_gemm_items + ctx->df_trace_items)) : nullptr;
     if (prof && ctx->gexec_df) {
       cudaGraphExecDestroy(ctx->gexec_df);
       ctx->gexec_df = nullptr;
@@ -1477,7 +1510,7 @@ cc_status cc_dataflow_profile(cc_ctx* ctx, uint64_t* out, int64_t cap, int64_t* 
   API_BEGIN
   ctx->need_device();
   if (!ctx->df_prof) throw Error(CC_E_STATE, "no profiled dataflow execute (flags bit 5)");
-  const int64_t n = ctx->df_gemm_items + ctx->df_trace_items;
+  const int64_t n = ctx->df_gemm_items + ctx->df_trace_items + ctx->num_sms;
   if (n_gemm) *n_gemm = ctx->df_gemm_items;
   if (n_trace) *n_trace = ctx->df_trace_items;
   if (out) {

@@ -1,25 +1,30 @@
 // Persistent dataflow worker for a whole plan (see dataflow.hpp for the protocol).
 //
-// One CTA per SM: 8 consumer warps + 1 producer warp.  The producer takes the plan's work
-// items from one queue in plan order, decodes them, waits for their dependencies and streams
-// their operands through a STAGES-deep TMA ring of 32 KB stages:
-//   GEMM item (MM1/BM1/BB2 output tile, or one k-chunk of it): one stage per 16-complex
-//     k-tile (A 64x16 + B 16x64 complex), consumed by the FP64 DMMA k-tile step
-//     (common.cuh, 64 x 64 complex CTA tile, warp tile 32 x 16);
-//   TR_MM item (a range of 32x32 block pairs of one time slice): one stage per block pair
-//     (A[t,I,J] and B[t,J,I], 16 KB each, 128-byte swizzled), consumed with FP64 FMAs.
-// Decoded items reach the consumers through a small ring of ItemInfo slots guarded by
-// mbarriers, so queue latency, dependency checks and pipeline fill of item n+1 overlap the
-// math of item n.  The same warps issue the DMMAs and the trace FMAs: both run on the SM's
-// FP64 datapath, where a co-resident DFMA kernel is starved by DMMA issue (measured:
-// tools/microbench/dmma_dfma_share.cu); the trace operands stream in by TMA behind the GEMM
-// work instead.
+// One CTA per SM, 11 warps:
+//   8 consumer warps  — DMMA k-tiles and trace block pairs, in ring order;
+//   1 issuer warp     — streams operands of ready items through a STAGES-deep TMA ring of
+//                       32 KB stages (shared memory only, never blocks on global memory):
+//     GEMM item (MM1/BM1/BB2 output tile, or one k-chunk of it): one stage per 16-complex
+//       k-tile (A 64x16 + B 16x64 complex), consumed by the FP64 DMMA k-tile step
+//       (common.cuh, 64 x 64 complex CTA tile, warp tile 32 x 16);
+//     TR_MM item (a range of 32x32 block pairs of one time slice): one stage per block pair
+//       (A[t,I,J] and B[t,J,I], 16 KB each, 128-byte swizzled), consumed with FP64 FMAs;
+//     TR_MM stages are interleaved between GEMM k-tiles (tr_ratio per k-tile), so the trace
+//     operands stream from HBM while the DMMAs run;
+//   2 scheduler warps — one per queue (GEMM, TR_MM): claim items, decode them, poll their
+//                       dependencies without blocking, hand ready items to the issuer, and
+//                       publish finished items (fence + done counter).
+// The trace math runs on the consumer warps between k-tiles because DMMA and DFMA share the
+// SM's FP64 datapath: a co-resident DFMA kernel is starved by DMMA issue (measured:
+// tools/microbench/dmma_dfma_share.cu).
 // Reductions are deterministic: a chunked tile is summed chunk by chunk by the CTA that
-// completes its last chunk (ticket); a trace slice's pieces are summed in piece order by the
-// CTA that completes its last piece; CTA partials use fixed shuffle trees.  Completion is
-// published with a consumer barrier, one release fence and one atomic increment of the op's
-// done counter; the producer acquires it (ld.acquire.gpu) and issues a proxy fence before TMA
-// reads data other SMs wrote with ordinary stores.
+// completes its last chunk (ticket); a TR_MM item's warp partials are summed in warp order by
+// the TR scheduler, and a slice's pieces in piece order by the CTA completing its last piece.
+// Completion: consumer warps arrive on the item's done mbarrier after their stores
+// (__syncwarp orders the lanes' stores first); the scheduler acquires it, fences at GPU scope
+// (cumulative) and increments the op's done counter; a dependent CTA's scheduler acquires the
+// counter (ld.acquire.gpu) and issues a proxy fence before TMA reads data other SMs wrote
+// with ordinary stores.
 #include "common.cuh"
 #include "dataflow.hpp"
 #include "kernels.hpp"
@@ -28,11 +33,14 @@ namespace cc {
 namespace {
 using namespace dev;
 
-using GC = Cfg<64, 64, 16, 32, 16, 5>;     // 5 x 32 KB stages
-constexpr int CW = GC::NCW * 32;           // 256 consumer threads (+ producer warp + publisher warp)
-constexpr int NT = CW + 64;
+#ifndef DF_STAGES
+#define DF_STAGES 6
+#endif
+using GC = Cfg<64, 64, 16, 32, 16, DF_STAGES>;   // 32 KB stages
+constexpr int CW = GC::NCW * 32;           // 256 consumer threads (+ issuer + 2 scheduler warps)
+constexpr int NT = CW + 96;
 constexpr int TB = 32;                     // trace block edge (complex)
-constexpr int INFO = 4;                    // decoded items in flight producer -> consumers
+constexpr int INFO = 4;                    // item slots per queue (claimed-ready-running-unpublished)
 static_assert(GC::A_BYTES == TB * TB * 16 && GC::B_BYTES == TB * TB * 16, "a trace block pair fills one stage");
 
 __device__ __forceinline__ void tma_load_4d_g(void* dst, const void* map, uint64_t* bar, int c0, int c1, int c2,
@@ -44,14 +52,14 @@ __device__ __forceinline__ void tma_load_4d_g(void* dst, const void* map, uint64
       : "memory");
 }
 
-__device__ __forceinline__ int find_op(const DfQueue& q, int64_t item) {
-  int lo = 0, hi = q.n_ops - 1;
-  while (lo < hi) {  // last op with first_item <= item
-    const int mid = (lo + hi + 1) >> 1;
-    if (q.ops[mid].first_item <= item) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -63,14 +71,6 @@ __device__ __forceinline__ unsigned smid() {
   unsigned r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
   return r;
-}
-
-__device__ __forceinline__ void wait_deps(const DfArgs& a, const DfOp& op) {
-  for (int d = 0; d < op.dep_count; ++d) {
-    const int* slot = a.sync + a.dep_slot[op.dep_begin + d];
-    const int target = a.dep_target[op.dep_begin + d];
-    while (ld_acquire(slot) < target) __nanosleep(64);
-  }
 }
 
 __device__ __forceinline__ void named_sync(int id, int n) {
@@ -85,9 +85,9 @@ __device__ __forceinline__ double2 cmul_acc(double2 acc, double2 x, double2 y) {
   return acc;
 }
 
-// One work item as the producer decoded it (shared memory, handed to the consumers).
+// One work item as the producer decoded it (shared memory, read by consumers and publisher).
 struct ItemInfo {
-  int64_t item;           // >= n_items: stop
+  int64_t item;           // < 0: stop
   int64_t tile;           // GEMM
   const void* tA;
   const void* tB;
@@ -95,22 +95,19 @@ struct ItemInfo {
   int32_t tm, tn, b, k0, kt_per_o, chunk;   // GEMM
   int32_t t, u0, nb, piece;                 // TRACE
   unsigned long long t_disp, t_ready;       // profiling (producer)
-  unsigned long long t_start, t_first, t_comp;  // profiling (consumers)
+  unsigned long long t_first, t_comp;       // profiling (consumers)
 };
 
-// Decode `item` (hint: the op of the previous item; consecutive items usually share it).
-__device__ __forceinline__ int decode_item(const DfArgs& a, int64_t item, ItemInfo& inf, int hint) {
+// Decode `item` of queue q.
+__device__ __forceinline__ void decode_item(const DfQueue& q, int64_t item, ItemInfo& inf, const void* tmaps) {
   inf.item = item;
-  if (item >= a.q.n_items) return hint;
-  int oi = hint;
-  if (oi < 0 || item < a.q.ops[oi].first_item || item >= a.q.ops[oi].first_item + a.q.ops[oi].n_items)
-    oi = find_op(a.q, item);
-  const DfOp& op = a.q.ops[oi];
+  const int oi = q.item_op[item];
+  const DfOp& op = q.ops[oi];
   const int64_t local = item - op.first_item;
   inf.op = oi;
   inf.kind = op.kind;
-  inf.tA = static_cast<const uint8_t*>(a.tmaps) + size_t(2 * op.tmap) * 128;
-  inf.tB = static_cast<const uint8_t*>(a.tmaps) + size_t(2 * op.tmap + 1) * 128;
+  inf.tA = static_cast<const uint8_t*>(tmaps) + size_t(2 * op.tmap) * 128;
+  inf.tB = static_cast<const uint8_t*>(tmaps) + size_t(2 * op.tmap + 1) * 128;
   if (op.kind == 0) {
     const int64_t tile = local / op.n_chunks;
     const int chunk = int(local - tile * op.n_chunks);
@@ -134,10 +131,49 @@ __device__ __forceinline__ int decode_item(const DfArgs& a, int64_t item, ItemIn
     inf.u0 = int((int64_t(p) * U) / op.P);
     inf.npos = int((int64_t(p + 1) * U) / op.P) - inf.u0;
   }
-  return oi;
 }
 
-// launch bounds of 12 warps although 10 run: caps registers at 168 (3 warps per SM
+// Non-blocking dependency poll: advances *dep past satisfied dependencies.
+__device__ __forceinline__ bool deps_ready(const DfArgs& a, const DfOp& op, int* dep) {
+  while (*dep < op.dep_count) {
+    const int k = op.dep_begin + *dep;
+    if (ld_acquire(a.sync + a.dep_slot[k]) < a.dep_target[k]) return false;
+    ++*dep;
+  }
+  return true;
+}
+
+// Stage descriptor (producer -> consumers, one per ring stage)
+constexpr uint32_t SK_TRACE = 1, SK_STOP = 2;   // 0: GEMM k-tile
+constexpr uint32_t SD_FIRST = 1u << 5, SD_LAST = 1u << 6;
+static_assert(INFO <= 8, "slot field is 3 bits");
+
+__device__ __forceinline__ void gemm_stage_loads(const ItemInfo& inf, int k, uint8_t* sA, uint64_t* bar) {
+  using C = GC;
+  uint8_t* sB = sA + C::A_BYTES;
+  const int kk = inf.k0 + k;
+  const int ko = kk / inf.kt_per_o;
+  const int ki0 = (kk - ko * inf.kt_per_o) * C::BK;
+#pragma unroll
+  for (int kc = 0; kc < C::BK / 8; ++kc)
+    tma_load_4d_g(sA + kc * C::BM * 128, inf.tA, bar, 2 * (ki0 + kc * 8), inf.tm * C::BM, ko, inf.b);
+#pragma unroll
+  for (int nc = 0; nc < C::BN / 8; ++nc)
+    tma_load_4d_g(sB + nc * C::BK * 128, inf.tB, bar, 2 * (inf.tn * C::BN + nc * 8), ki0, ko, inf.b);
+}
+
+__device__ __forceinline__ void trace_stage_loads(const ItemInfo& inf, int k, uint8_t* sA, uint64_t* bar) {
+  uint8_t* sB = sA + GC::A_BYTES;
+  const int u = inf.u0 + k;
+  const int I = u / inf.nb, J = u - I * inf.nb;
+#pragma unroll
+  for (int ch = 0; ch < TB / 8; ++ch) {  // A[t, I*32 + r, J*32 + 8ch + s] and B[t, J*32 + r, I*32 + 8ch + s]
+    tma_load_4d_g(sA + ch * TB * 128, inf.tA, bar, 2 * (J * TB + 8 * ch), I * TB, 0, inf.t);
+    tma_load_4d_g(sB + ch * TB * 128, inf.tB, bar, 2 * (I * TB + 8 * ch), J * TB, 0, inf.t);
+  }
+}
+
+// launch bounds of 12 warps although 11 run: caps registers at 168 (3 warps per SM
 // sub-partition x 32 x 168 <= 16K registers each)
 __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
   using C = GC;
@@ -147,9 +183,10 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
-  __shared__ ItemInfo s_info[INFO];
-  __shared__ uint64_t info_full[INFO], info_empty[INFO];
-  __shared__ double2 red[GC::NCW];
+  __shared__ ItemInfo s_info[2][INFO];
+  __shared__ uint64_t info_full[2][INFO], done[2][INFO];
+  __shared__ uint32_t s_desc[C::STAGES];
+  __shared__ double2 red[INFO][GC::NCW];    // TR_MM item partials per consumer warp, per slot
   __shared__ int s_flag;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -158,96 +195,178 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NCW);
     }
-    for (int s = 0; s < INFO; ++s) {
-      mbar_init(&info_full[s], 1);
-      mbar_init(&info_empty[s], 1);    // released by the publisher warp
-    }
+    for (int x = 0; x < 2; ++x)
+      for (int s = 0; s < INFO; ++s) {
+        mbar_init(&info_full[x][s], 1);     // scheduler -> issuer: item ready
+        mbar_init(&done[x][s], C::NCW);     // consumers -> scheduler: item finished
+      }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
   if (warp == C::NCW) {
-    // --------------------------------- producer -------------------------------------------
+    // ----------------------------------- issuer -------------------------------------------
+    // Takes ready items of both kinds from the schedulers (shared memory only) and streams
+    // their operands through the one TMA ring: TR_MM stages go between GEMM k-tiles (up to
+    // tr_ratio per k-tile), so the trace operands arrive while the DMMAs run.  It never
+    // touches global memory itself and blocks only on a free ring stage.
     if (lane != 0) return;
-    uint32_t pos = 0;   // ring positions issued
-    int hint = -1;
-    for (uint32_t n = 0;; ++n) {
-      const int slot = int(n % INFO);
-      mbar_wait(&info_empty[slot], ((n / INFO) & 1u) ^ 1u);
-      ItemInfo& inf = s_info[slot];
-      const unsigned long long t0 = a.prof ? gtimer() : 0ull;
-      hint = decode_item(a, int64_t(atomicAdd(a.q.head, 1ull)), inf, hint);
-      const bool stop = inf.item >= a.q.n_items;
-      if (!stop) {
-        wait_deps(a, a.q.ops[inf.op]);
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tA) : "memory");
-        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tB) : "memory");
-      }
-      inf.t_disp = t0;
-      inf.t_ready = a.prof ? gtimer() : 0ull;
-      mbar_arrive(&info_full[slot]);   // release: the decoded item is visible to the consumers
-      if (stop) break;
-      for (int k = 0; k < inf.npos; ++k, ++pos) {
-        const int st = int(pos % C::STAGES);
-        mbar_wait(&empty[st], ((pos / C::STAGES) & 1u) ^ 1u);
-        mbar_expect_tx(&full[st], C::STAGE_BYTES);
-        uint8_t* sA = smem + st * C::STAGE_BYTES;
-        uint8_t* sB = sA + C::A_BYTES;
-        if (inf.kind == 0) {
-          const int kk = inf.k0 + k;
-          const int ko = kk / inf.kt_per_o;
-          const int ki0 = (kk - ko * inf.kt_per_o) * C::BK;
+    uint32_t nx[2] = {0u, 0u};
+    bool have[2] = {false, false}, ex[2] = {false, false};
+    int slot_of[2] = {0, 0}, k_of[2] = {0, 0}, np_of[2] = {0, 0};
+    uint32_t pos = 0;
+    int credit = 0;
+    for (;;) {
 #pragma unroll
-          for (int kc = 0; kc < C::BK / 8; ++kc)
-            tma_load_4d_g(sA + kc * C::BM * 128, inf.tA, &full[st], 2 * (ki0 + kc * 8), inf.tm * C::BM, ko, inf.b);
-#pragma unroll
-          for (int nc = 0; nc < C::BN / 8; ++nc)
-            tma_load_4d_g(sB + nc * C::BK * 128, inf.tB, &full[st], 2 * (inf.tn * C::BN + nc * 8), ki0, ko, inf.b);
-        } else {
-          const int u = inf.u0 + k;
-          const int I = u / inf.nb, J = u - I * inf.nb;
-#pragma unroll
-          for (int ch = 0; ch < TB / 8; ++ch) {  // A[t, I*32 + r, J*32 + 8ch + s] and B[t, J*32 + r, I*32 + 8ch + s]
-            tma_load_4d_g(sA + ch * TB * 128, inf.tA, &full[st], 2 * (J * TB + 8 * ch), I * TB, 0, inf.t);
-            tma_load_4d_g(sB + ch * TB * 128, inf.tB, &full[st], 2 * (I * TB + 8 * ch), J * TB, 0, inf.t);
+      for (int x = 0; x < 2; ++x) {
+        if (!have[x] && !ex[x]) {
+          const int s = int(nx[x] % INFO);
+          if (mbar_test(&info_full[x][s], (nx[x] / INFO) & 1u)) {
+            ++nx[x];
+            if (s_info[x][s].item < 0) {
+              ex[x] = true;
+            } else {
+              have[x] = true;
+              slot_of[x] = s;
+              k_of[x] = 0;
+              np_of[x] = s_info[x][s].npos;
+            }
           }
         }
       }
+      if (ex[0] && ex[1]) break;
+      if (!have[0] && !have[1]) {
+        __nanosleep(20);
+        continue;
+      }
+      const int x = (have[1] && (!have[0] || credit > 0)) ? 1 : 0;
+      if (have[0]) credit = x ? credit - 1 : min(credit + a.tr_ratio, 2 * a.tr_ratio);
+      const ItemInfo& inf = s_info[x][slot_of[x]];
+      const int k = k_of[x];
+      const int st = int(pos % C::STAGES);
+      mbar_wait(&empty[st], ((pos / C::STAGES) & 1u) ^ 1u);
+      s_desc[st] = uint32_t(x) | (uint32_t(slot_of[x]) << 2) | (k == 0 ? SD_FIRST : 0u) |
+                   (k == np_of[x] - 1 ? SD_LAST : 0u);
+      mbar_expect_tx(&full[st], C::STAGE_BYTES);
+      uint8_t* sA = smem + st * C::STAGE_BYTES;
+      if (x == 0) gemm_stage_loads(inf, k, sA, &full[st]);
+      else trace_stage_loads(inf, k, sA, &full[st]);
+      ++pos;
+      if (++k_of[x] == np_of[x]) have[x] = false;
     }
+    const int st = int(pos % C::STAGES);
+    mbar_wait(&empty[st], ((pos / C::STAGES) & 1u) ^ 1u);
+    s_desc[st] = SK_STOP;
+    mbar_arrive(&full[st]);
     return;
   }
-  if (warp == C::NCW + 1) {
-    // --------------------------------- publisher ------------------------------------------
-    // Completion of item n: the consumers arrive on named barrier 2 + slot after their last
-    // store and go on with item n+1; this warp syncs on it (acquiring their stores), makes
-    // them visible at GPU scope (cumulative fence) and bumps the op's done counter — the
-    // fence's drain latency leaves the consumers' critical path.  A slot (and its barrier)
-    // is reused only after this warp releases info_empty, so at most INFO items are pending.
-    for (uint32_t n = 0;; ++n) {
-      const int slot = int(n % INFO);
-      mbar_wait(&info_full[slot], (n / INFO) & 1u);
-      const ItemInfo& cur = s_info[slot];
-      const int64_t item = cur.item;
-      if (item >= a.q.n_items) break;
-      asm volatile("bar.sync %0, %1;" ::"r"(2 + slot), "r"(CW + 32) : "memory");
-      if (lane == 0) {
+  if (warp > C::NCW) {
+    // ------------------------------ schedulers / publishers -------------------------------
+    // Warp NCW+1 serves the GEMM queue, warp NCW+2 the TR_MM queue.  Each claims items (at
+    // most `ahead` unpublished), decodes them, polls their dependencies without blocking and
+    // hands ready items to the issuer in claim order; and it publishes finished items in the
+    // same order (the consumers finish the items of one kind in ring order): after the
+    // consumer warps' arrivals on done[slot] (acquiring their stores) it makes the stores
+    // visible at GPU scope (cumulative fence) and bumps the op's done counter, so neither the
+    // global-memory latency of claiming and polling nor the fence's drain sits on the
+    // issuer's or the consumers' path.
+    if (lane != 0) return;
+    const int x = warp - C::NCW - 1;
+    const DfQueue& Q = x == 0 ? a.q : a.qt;
+    unsigned long long* prof = x == 0 ? a.prof : a.prof_t;
+    const uint32_t ahead = uint32_t(x == 0 ? a.ahead_g : a.ahead_t);
+    uint32_t n_alloc = 0, n_pub = 0;
+    bool exhausted = Q.n_items == 0, pending = false, stopped = false;
+    ItemInfo inf;
+    int dep = 0;
+    for (;;) {
+      bool idle = true;
+      while (n_pub < n_alloc && !(stopped && n_pub == n_alloc - 1)) {
+        const int s = int(n_pub % INFO);
+        if (!mbar_test(&done[x][s], (n_pub / INFO) & 1u)) break;
+        const ItemInfo& cur = s_info[x][s];
+        const DfOp& op = Q.ops[cur.op];
+        if (x == 1) {
+          // TR_MM piece: fixed-order sum of the consumer warps' partials; a slice's pieces are
+          // summed in piece order by the CTA that completes its last piece (ticket)
+          double2 v = red[s][0];
+#pragma unroll
+          for (int w = 1; w < C::NCW; ++w) {
+            v.x += red[s][w].x;
+            v.y += red[s][w].y;
+          }
+          double2* outp = static_cast<double2*>(op.out);
+          if (op.P == 1) {
+            outp[cur.t] = v;
+          } else {
+            double2* pp = static_cast<double2*>(op.tr_part) + int64_t(cur.t) * op.P;
+            pp[cur.piece] = v;
+            __threadfence();
+            if (atomicAdd(&op.tr_cnt[cur.t], 1) == op.P - 1) {
+              op.tr_cnt[cur.t] = 0;
+              __threadfence();
+              double2 sum = __ldcg(pp);
+              for (int k = 1; k < op.P; ++k) {
+                const double2 pk = __ldcg(pp + k);
+                sum.x += pk.x;
+                sum.y += pk.y;
+              }
+              outp[cur.t] = sum;
+            }
+          }
+        }
         __threadfence();
-        atomicAdd(a.sync + a.q.ops[cur.op].sync_id, 1);
-        if (a.prof) {
-          unsigned long long* pr = a.prof + 8 * item;
+        atomicAdd(a.sync + op.sync_id, 1);
+        if (prof) {
+          unsigned long long* pr = prof + 8 * cur.item;
           pr[0] = cur.t_disp;
           pr[1] = cur.t_ready;
           pr[2] = gtimer();
           pr[3] = smid();
-          pr[4] = cur.t_start;
+          pr[4] = cur.t_first;
           pr[5] = cur.t_comp;
-          pr[6] = cur.kind;
+          pr[6] = uint64_t(x);
           pr[7] = cur.t_first;
         }
-        mbar_arrive(&info_empty[slot]);
+        ++n_pub;
+        idle = false;
       }
-      __syncwarp();
+      if (stopped) {
+        if (n_pub == n_alloc - 1) break;
+      } else if (!pending && !exhausted && n_alloc - n_pub < ahead) {
+        const unsigned long long t0 = prof ? gtimer() : 0ull;
+        const int64_t it = int64_t(atomicAdd(Q.head, 1ull));
+        if (it >= Q.n_items) {
+          exhausted = true;
+        } else {
+          decode_item(Q, it, inf, a.tmaps);
+          inf.t_disp = t0;
+          pending = true;
+          dep = 0;
+        }
+        idle = false;
+      }
+      if (pending && deps_ready(a, Q.ops[inf.op], &dep)) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tA) : "memory");
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tB) : "memory");
+        inf.t_ready = prof ? gtimer() : 0ull;
+        const int s = int(n_alloc % INFO);
+        s_info[x][s] = inf;
+        mbar_arrive(&info_full[x][s]);     // release: the item is visible to issuer and consumers
+        ++n_alloc;
+        pending = false;
+        idle = false;
+      }
+      if (!stopped && exhausted && !pending && n_alloc - n_pub < INFO) {
+        const int s = int(n_alloc % INFO);
+        s_info[x][s].item = -1;
+        mbar_arrive(&info_full[x][s]);
+        ++n_alloc;
+        stopped = true;
+        idle = false;
+      }
+      if (idle) __nanosleep(32);
     }
     return;
   }
@@ -256,37 +375,58 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
   const int g = lane >> 2, t = lane & 3;
   const bool q = (g & 1) != 0;
-  uint32_t ring = 0;
-  for (uint32_t n = 0;; ++n) {
-    const int slot = int(n % INFO);
-    mbar_wait(&info_full[slot], (n / INFO) & 1u);
-    const ItemInfo& cur = s_info[slot];
-    const int64_t item = cur.item;
-    if (item >= a.q.n_items) break;
-    const DfOp& op = a.q.ops[cur.op];
-    const int npos = cur.npos;
-    unsigned long long t_first = 0, t_comp = 0;
-    const unsigned long long t_start = (tid == 0 && a.prof) ? gtimer() : 0ull;
-
-    if (cur.kind == 0) {
-      // ---------------- GEMM tile (or k-chunk of a tile) ----------------
-      double acc[C::MI][C::NI][2];
-#pragma unroll
-      for (int i = 0; i < C::MI; ++i)
-#pragma unroll
-        for (int k = 0; k < C::NI; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
-      for (int i = 0; i < npos; ++i) {
-        const uint32_t r = ring + i;
-        const int st = int(r % C::STAGES);
-        mbar_wait(&full[st], (r / C::STAGES) & 1u);
-        if (i == 0 && tid == 0 && a.prof) t_first = gtimer();
-        const uint8_t* sA = smem + st * C::STAGE_BYTES;
-        dmma_ktile<C>(sA, sA + C::A_BYTES, wm, wn, g, t, q, acc);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
+  const bool prof = a.prof != nullptr;
+  double acc[C::MI][C::NI][2];
+  double2 tacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  // profile (thread 0): clock64 cycles waiting for stage data / in stage math+epilogue, per kind
+  long long c_wait[2] = {0, 0}, c_work[2] = {0, 0}, n_st[2] = {0, 0}, ta = 0, tb = 0;
+  int lastk = 0;
+  for (uint32_t r = 0;; ++r) {
+    const int st = int(r % C::STAGES);
+    if (prof && tid == 0) {
+      ta = clock64();
+      if (r > 0) c_work[lastk] += ta - tb;
+    }
+    mbar_wait(&full[st], (r / C::STAGES) & 1u);
+    const uint32_t d = s_desc[st];
+    const uint32_t kind = d & 3u;
+    if (kind == SK_STOP) {
+      if (prof && tid == 0 && a.prof_sm) {
+        long long* ps = a.prof_sm + 8 * blockIdx.x;
+        ps[0] = c_wait[0];
+        ps[1] = c_wait[1];
+        ps[2] = c_work[0];
+        ps[3] = c_work[1];
+        ps[4] = n_st[0];
+        ps[5] = n_st[1];
+        ps[6] = smid();
       }
-      ring += npos;
-      if (tid == 0 && a.prof) t_comp = gtimer();
+      break;
+    }
+    if (prof && tid == 0) {
+      tb = clock64();
+      c_wait[kind] += tb - ta;
+      ++n_st[kind];
+      lastk = int(kind);
+    }
+    const int slot = int((d >> 2) & 7u);
+    const uint8_t* sA = smem + st * C::STAGE_BYTES;
+    if (kind != SK_TRACE) {
+      // ---------------- GEMM k-tile of a tile (or k-chunk of a tile) ----------------
+      if (d & SD_FIRST) {
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int k = 0; k < C::NI; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
+        if (tid == 0 && prof) s_info[0][slot].t_first = gtimer();
+      }
+      dmma_ktile<C>(sA, sA + C::A_BYTES, wm, wn, g, t, q, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (!(d & SD_LAST)) continue;
+      const ItemInfo& cur = s_info[0][slot];
+      const DfOp& op = a.q.ops[cur.op];
+      if (tid == 0 && prof) s_info[0][slot].t_comp = gtimer();
       const int64_t tile = cur.tile;
       const int chunk = cur.chunk;
       double2* out = static_cast<double2*>(op.C) + int64_t(cur.b) * op.sCb;
@@ -341,86 +481,44 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
           }
         }
       }
+      // item finished: this warp's stores (ordered by __syncwarp) before the arrival
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[0][slot]);
     } else {
-      // ---------------- TR_MM piece: sum over block pairs of A[r][c] * B[c][r] ----------------
-      double2 acc = make_double2(0.0, 0.0);
-      for (int i = 0; i < npos; ++i) {
-        const uint32_t r = ring + i;
-        const int st = int(r % C::STAGES);
-        mbar_wait(&full[st], (r / C::STAGES) & 1u);
-        if (i == 0 && tid == 0 && a.prof) t_first = gtimer();
-        const uint8_t* sA = smem + st * C::STAGE_BYTES;
-        const uint8_t* sB = sA + C::A_BYTES;
-        // element (row, col) of a 32x32 block: chunk col/8, 128-byte row `row`, 16-byte slot
-        // (col%8) ^ (row%8) (TMA 128-byte swizzle); warp w takes rows w, w+8, w+16, w+24 of A,
-        // lane = column c: A[r][c] row-contiguous, B[c][r] one 128-byte row per lane — both
-        // conflict-free.
-#pragma unroll
-        for (int qq = 0; qq < TB / 8; ++qq) {
-          const int rr = warp + qq * 8, c = lane;
-          const double2 av = *reinterpret_cast<const double2*>(sA + (c >> 3) * (TB * 128) + rr * 128 +
-                                                               (((c & 7) ^ (rr & 7)) << 4));
-          const double2 bv = *reinterpret_cast<const double2*>(sB + (rr >> 3) * (TB * 128) + c * 128 +
-                                                               (((rr & 7) ^ (c & 7)) << 4));
-          acc = cmul_acc(acc, av, bv);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
+      // ---------------- TR_MM block pair: sum of A[r][c] * B[c][r] ----------------
+      if (d & SD_FIRST) {
+        tacc[0] = tacc[1] = make_double2(0.0, 0.0);
+        if (tid == 0 && prof) s_info[1][slot].t_first = gtimer();
       }
-      ring += npos;
-      if (tid == 0 && a.prof) t_comp = gtimer();
+      const uint8_t* sB = sA + C::A_BYTES;
+      // element (row, col) of a 32x32 block: chunk col/8, 128-byte row `row`, 16-byte slot
+      // (col%8) ^ (row%8) (TMA 128-byte swizzle); warp w takes rows w, w+8, w+16, w+24 of A,
+      // lane = column c: A[r][c] row-contiguous, B[c][r] one 128-byte row per lane — both
+      // conflict-free.
+#pragma unroll
+      for (int qq = 0; qq < TB / 8; ++qq) {
+        const int rr = warp + qq * 8, c = lane;
+        const double2 av = *reinterpret_cast<const double2*>(sA + (c >> 3) * (TB * 128) + rr * 128 +
+                                                             (((c & 7) ^ (rr & 7)) << 4));
+        const double2 bv = *reinterpret_cast<const double2*>(sB + (rr >> 3) * (TB * 128) + c * 128 +
+                                                             (((rr & 7) ^ (c & 7)) << 4));
+        tacc[qq & 1] = cmul_acc(tacc[qq & 1], av, bv);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (!(d & SD_LAST)) continue;
+      if (tid == 0 && prof) s_info[1][slot].t_comp = gtimer();
+      double2 acc2 = make_double2(tacc[0].x + tacc[1].x, tacc[0].y + tacc[1].y);
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc2.x += __shfl_xor_sync(0xffffffffu, acc2.x, o);
+        acc2.y += __shfl_xor_sync(0xffffffffu, acc2.y, o);
       }
-      if (lane == 0) red[warp] = acc;
-      named_sync(1, CW);
-      double2* outp = static_cast<double2*>(op.out);
-      if (tid == 0) {
-        double2 s = red[0];
-        for (int w = 1; w < C::NCW; ++w) {
-          s.x += red[w].x;
-          s.y += red[w].y;
-        }
-        if (op.P == 1) {
-          outp[cur.t] = s;
-          s_flag = 0;
-        } else {
-          static_cast<double2*>(op.tr_part)[int64_t(cur.t) * op.P + cur.piece] = s;
-          __threadfence();
-          const int ticket = atomicAdd(&op.tr_cnt[cur.t], 1);
-          s_flag = (ticket == op.P - 1);
-          if (s_flag) op.tr_cnt[cur.t] = 0;
-        }
-      }
-      named_sync(1, CW);
-      if (s_flag && warp == 0) {
-        // the last piece of slice t: fixed-order sum of the P pieces
-        __threadfence();
-        const double* pp = static_cast<const double*>(op.tr_part) + 2 * int64_t(cur.t) * op.P;
-        double sx = 0.0, sy = 0.0;
-        for (int k = lane; k < op.P; k += 32) {
-          sx += __ldcg(pp + 2 * k);
-          sy += __ldcg(pp + 2 * k + 1);
-        }
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) {
-          sx += __shfl_xor_sync(0xffffffffu, sx, o);
-          sy += __shfl_xor_sync(0xffffffffu, sy, o);
-        }
-        if (lane == 0) outp[cur.t] = make_double2(sx, sy);
-      }
+      // the TR scheduler sums the warps' partials (fixed order) when it publishes the item
+      if (lane == 0) red[slot][warp] = acc2;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[1][slot]);
     }
-
-    if (tid == 0 && a.prof) {
-      ItemInfo& w = s_info[slot];
-      w.t_start = t_start;
-      w.t_first = t_first;
-      w.t_comp = t_comp;
-    }
-    // release the item to the publisher (barrier arrive orders this thread's stores before it)
-    asm volatile("bar.arrive %0, %1;" ::"r"(2 + slot), "r"(CW + 32) : "memory");
   }
 }
 

@@ -1,13 +1,18 @@
 // Dataflow execution of a whole plan by a persistent worker kernel (host/device shared PODs).
 //
-// The plan's contractions become work items of one queue, in plan order: GEMM tiles
-// (MM1/BM1/BB2; a tile may be split into k-chunks) and TR_MM block-pair ranges.  The worker
-// is persistent (one CTA per SM), grabs items with an atomic queue head, and before an item
-// its producer warp spins on the integer sync slots of the item's op dependencies: done
-// counters of earlier ops (RAW on operands, WAR/WAW on reused pool memory) and completion
-// flags written by the copy streams after a copy (cuStreamWriteValue32).  Items only ever
-// wait on earlier plan positions and the queue is dispatched in order, so the earliest
-// unfinished item always has its dependencies satisfied: the execution cannot deadlock.
+// The plan's contractions become work items of two queues, each in one topological order of
+// the plan: GEMM tiles (MM1/BM1/BB2; a tile may be split into k-chunks) and TR_MM block-pair
+// ranges.  The worker is persistent (one CTA per SM); its producer holds at most one claimed
+// item of each queue (atomic queue heads) and polls, without blocking, the integer sync slots
+// of the items' op dependencies: done counters of earlier ops (RAW on operands, WAR/WAW on
+// reused pool memory) and completion flags written by the copy streams after a copy
+// (cuStreamWriteValue32).  Only stages of ready items enter the TMA ring.
+// Deadlock freedom: let X be the earliest unfinished item in the merged topological order.
+// Its dependencies are finished.  If X is claimed, its holder's producer sees it ready and
+// issues it; every stage already in a ring belongs to a ready item, so the consumers drain
+// the ring.  If X is unclaimed, every claimed item of X's queue precedes X and is therefore
+// finished, so the next claim from that queue (which a producer makes as soon as it holds
+// no item of that kind) is X.  Either way X finishes.
 #pragma once
 #include <cstdint>
 
@@ -40,18 +45,24 @@ struct DfOp {
 
 struct DfQueue {
   const DfOp* ops;
+  const int32_t* item_op;    // op index of each item
   int32_t n_ops;
   int64_t n_items;
   unsigned long long* head;  // atomic queue head (zeroed per launch)
 };
 
 struct DfArgs {
-  DfQueue q;                  // items of every op, in plan order
+  DfQueue q;                  // GEMM items
+  DfQueue qt;                 // TR_MM items
   const int32_t* dep_slot;    // sync slot an op waits on
   const int32_t* dep_target;  // value the slot must reach
   const void* tmaps;          // CUtensorMap array (64-byte aligned, global memory)
   int* sync;                  // done counters + copy flags (zeroed per launch)
-  unsigned long long* prof;   // optional: per item {dispatch, ready, end, smid} %globaltimer ns
+  unsigned long long* prof;   // optional: per GEMM item {claim, ready, end, smid, first data, loop end, kind, -}
+  unsigned long long* prof_t; // optional: the same per TR_MM item
+  long long* prof_sm;         // optional: per CTA {wait cycles G/T, work cycles G/T, stages G/T, smid, -}
+  int32_t tr_ratio;           // TR_MM stages the issuer may interleave per GEMM k-tile
+  int32_t ahead_g, ahead_t;   // items a CTA may hold claimed-but-unpublished per queue (<= 4)
 };
 
 cudaError_t df_preload();

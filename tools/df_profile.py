@@ -24,10 +24,19 @@ for (u, op, a, b, s) in w.nodes:
     ctx.fill_synthetic(d, n, w.data_seed, u, 0, 0, sig)
     keep.append(d)
     ctx.set_leaf_device(u, d)
-for _ in range(3):
-    ctx.execute(0)
+ts = []
+for _ in range(5):
+    ts.append(ctx.execute(0)["seconds"] * 1e3)
+print("plain executes (ms):", np.round(ts, 3))
 ex = ctx.execute(cc.EXEC_PROFILE)
-g0, _ = ctx.dataflow_profile()
+gp, tp, psm = ctx.dataflow_profile(per_sm=True)
+tot = psm[:, :4].sum(axis=1).astype(np.float64)
+print("per CTA (clock64): wait G %.1f%%  wait T %.1f%%  work G %.1f%%  work T %.1f%%;  stages G %d  T %d;"
+      "  per stage: G wait %.0f + work %.0f cyc, T wait %.0f + work %.0f cyc"
+      % tuple([100 * psm[:, k].sum() / tot.sum() for k in range(4)] + [psm[:, 4].sum(), psm[:, 5].sum()] +
+              [psm[:, 0].sum() / max(psm[:, 4].sum(), 1), psm[:, 2].sum() / max(psm[:, 4].sum(), 1),
+               psm[:, 1].sum() / max(psm[:, 5].sum(), 1), psm[:, 3].sum() / max(psm[:, 5].sum(), 1)]))
+g0 = np.vstack([gp, tp])
 g, t = g0[g0[:, 6] == 0], g0[g0[:, 6] == 1]
 t0 = min(g[:, 0].min() if len(g) else 2**63, t[:, 0].min() if len(t) else 2**63)
 t1 = max(g[:, 2].max() if len(g) else 0, t[:, 2].max() if len(t) else 0)
