@@ -100,6 +100,8 @@ typedef struct {
   double hbm_bytes;           /* algorithmic HBM bytes of the kernels                       */
   int64_t h2d_bytes, d2h_bytes; /* bytes actually copied (device-resident leaves: 0)         */
   int64_t n_kernels;          /* kernel launches issued by this execute                     */
+  double copy_seconds;        /* start -> last H2D/D2H copy done (blocking stream-mode
+                                 dataflow execute with copies; else 0)                     */
 } cc_exec_stats;
 
 /* One op of the physical plan (cc_plan_ops). kind: 0 H2D, 1 D2H (evict with copy),

@@ -60,7 +60,7 @@ class cc_plan_stats(ctypes.Structure):
 
 class cc_exec_stats(ctypes.Structure):
     _fields_ = [("seconds", c_dbl), ("kernel_seconds", c_dbl), ("flops", c_dbl), ("hbm_bytes", c_dbl),
-                ("h2d_bytes", c_i64), ("d2h_bytes", c_i64), ("n_kernels", c_i64)]
+                ("h2d_bytes", c_i64), ("d2h_bytes", c_i64), ("n_kernels", c_i64), ("copy_seconds", c_dbl)]
 
 
 class cc_plan_op(ctypes.Structure):

@@ -30,6 +30,21 @@
 
 using namespace cc;
 
+namespace {
+// CC_TIMING=1: host-side phase times of plan preparation / issue on stderr
+struct PhaseTimer {
+  const char* what;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit PhaseTimer(const char* w) : what(w) {}
+  void lap(const char* step) {
+    static const bool on = getenv("CC_TIMING") != nullptr;
+    const auto t1 = std::chrono::steady_clock::now();
+    if (on) fprintf(stderr, "[cc timing] %s/%s %.3f ms\n", what, step, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+}  // namespace
+
 #define CC_VERSION "cc-b200 0.1 (sm_100a; FP64 DMMA + TMA; sibling/tree schedulers; LRU plan)"
 
 namespace {
@@ -91,6 +106,8 @@ struct cc_ctx {
   int64_t host_pool_bytes = 0;
   std::vector<cudaEvent_t> events;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_h_end = nullptr, ev_d_end = nullptr;
+  cudaEvent_t ev_copy_h = nullptr, ev_copy_d = nullptr;   // timing: last copy done (stream mode)
+  bool copy_timed = false;
   cudaGraphExec_t gexec = nullptr;
   // kernel-only replays (flags 4: GEMM kinds, 8: TR_MM): the plan's contraction launches of
   // those kinds alone, in plan order, as a CUDA graph -> average launch duration of a kind
@@ -102,7 +119,8 @@ struct cc_ctx {
 
   // dataflow execution (persistent workers): device metadata + per-launch sync area
   bool df_valid = false;
-  char* df_meta = nullptr;          // cudaMalloc: ops, deps, tensor maps, sync area
+  char* df_meta = nullptr;          // ops, deps, tensor maps, sync area: top of the pool, else cudaMalloc
+  bool df_meta_owned = false;       // cudaMalloc'ed (the arena had no room above the plan's high water)
   size_t df_meta_bytes = 0;
   DfArgs df_gemm{};                 // the dataflow worker's arguments (both queues)
   int* df_sync = nullptr;           // zeroed per launch (with the two queue heads before it)
@@ -121,8 +139,10 @@ struct cc_ctx {
     std::vector<std::pair<int32_t, int32_t>> wait_values;  // (sync slot, target)
     std::vector<int32_t> wait_events;                        // copy ops on the other copy stream
     bool source = false;
+    int32_t chunks = 1;             // H2D in time-slice chunks: the flag counts finished chunks
   };
   std::vector<DfCopy> df_copies;
+  std::vector<int32_t> df_issue;    // enqueue order of df_copies (sources before waiters)
   std::vector<cudaEvent_t> df_events;  // per copy (index into df_copies), when some copy waits on it
   cudaStream_t cs2 = nullptr;       // second compute stream (trace worker)
   cudaEvent_t ev_cs2 = nullptr;
@@ -143,12 +163,14 @@ struct cc_ctx {
     df_prof = nullptr;
     if (gexec_df) cudaGraphExecDestroy(gexec_df);
     gexec_df = nullptr;
-    if (df_meta) cudaFree(df_meta);
+    if (df_meta && df_meta_owned) cudaFree(df_meta);
     df_meta = nullptr;
+    df_meta_owned = false;
     for (auto e : df_events)
       if (e) cudaEventDestroy(e);
     df_events.clear();
     df_copies.clear();
+    df_issue.clear();
     df_valid = false;
   }
   void release_graph() {
@@ -174,7 +196,7 @@ struct cc_ctx {
   void release_device() {
     if (host_only) return;
     release_phys();
-    for (cudaEvent_t* e : {&ev_start, &ev_end, &ev_h_end, &ev_d_end})
+    for (cudaEvent_t* e : {&ev_start, &ev_end, &ev_h_end, &ev_d_end, &ev_copy_h, &ev_copy_d})
       if (*e) {
         cudaEventDestroy(*e);
         *e = nullptr;
@@ -311,7 +333,9 @@ int64_t df_trace_pieces(int64_t Lt, int64_t N) {
 // events and the host pool.  Called lazily by cc_execute.
 void prepare_phys(cc_ctx* ctx) {
   if (ctx->phys_valid) return;
+  PhaseTimer pt("prepare_phys");
   ctx->release_phys();
+  pt.lap("release");
   const Dag& g = *ctx->dag;
   if (g.abstract) throw Error(CC_E_STATE, "abstract DAG (leafX/OPX) can be scheduled, not executed");
   const int64_t Lt = g.Lt, N = g.N, S = g.S;
@@ -385,6 +409,7 @@ void prepare_phys(cc_ctx* ctx) {
   ck(cudaMemset(ctx->trace_ws, 0, trace_ws), "trace counters");
   if (sz_gemm > 0) ck(cudaMemset(ctx->gemm_ws, 0, size_t(sz_gemm)), "gemm flags");
   ck(cudaMemset(ctx->roots, 0, size_t(sz_roots)), "roots");
+  pt.lap("scratch+tables");
   // physical plan over the pool
   std::vector<uint8_t> on_dev(g.nodes.size(), 0);
   for (size_t u = 0; u < g.nodes.size(); ++u) on_dev[u] = ctx->leaf_dev[u] != nullptr;
@@ -401,6 +426,7 @@ void prepare_phys(cc_ctx* ctx) {
     ctx->pp = build_phys(g, ctx->lp, on_dev, pool, ALIGN, RangeAlloc::BEST_FIT);
   }
   ctx->stats.arena_high_water = ctx->pp.pool_high_water;
+  pt.lap("build_phys");
   if (ctx->pp.host_pool_bytes > 0) {
     ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_pool), size_t(ctx->pp.host_pool_bytes), cudaHostAllocDefault),
        "pinned host pool");
@@ -409,6 +435,7 @@ void prepare_phys(cc_ctx* ctx) {
   ctx->events.assign(ctx->pp.ops.size(), nullptr);
   for (size_t i = 0; i < ctx->pp.ops.size(); ++i)
     if (ctx->pp.ops[i].source) ck(cudaEventCreateWithFlags(&ctx->events[i], cudaEventDisableTiming), "event");
+  pt.lap("host pool+events");
   ctx->phys_valid = true;
 }
 
@@ -493,6 +520,7 @@ void prepare_dataflow(cc_ctx* ctx) {
   if (ctx->df_valid) return;
   if (getenv("CC_DEBUG")) fprintf(stderr, "[cc] prepare_dataflow\n");
   prepare_phys(ctx);
+  PhaseTimer tmr("prepare_dataflow");
   const Dag& g = *ctx->dag;
   const auto& ops = ctx->pp.ops;
   const int64_t Lt = g.Lt, N = g.N;
@@ -521,6 +549,7 @@ void prepare_dataflow(cc_ctx* ctx) {
     d.erase(std::unique(d.begin(), d.end()), d.end());
     d.erase(std::remove(d.begin(), d.end(), i), d.end());
   }
+  tmr.lap("rw deps");
   // 2. sync slots and work items
   std::vector<int32_t> slot(size_t(n_ops), -1), target(size_t(n_ops), 0), df_index(size_t(n_ops), -1);
   int32_t n_sync = 0;
@@ -533,12 +562,22 @@ void prepare_dataflow(cc_ctx* ctx) {
   std::vector<std::vector<int32_t>> ring_deps(static_cast<size_t>(n_ops));
   int BM, BN, BK, slot_doubles;
   df_gemm_tile_dims(&BM, &BN, &BK, &slot_doubles);
+  // CC_H2D_CHUNK_MB: H2D copies in time-slice chunks of about that size (default off: every
+  // chunk costs a stream memory operation, measured ~8 us of copy-engine idle each on B200)
+  const double chunk_mb = getenv("CC_H2D_CHUNK_MB") ? atof(getenv("CC_H2D_CHUNK_MB")) : 0.0;
+  const int64_t h2d_chunk = chunk_mb > 0 ? std::max<int64_t>(4096, int64_t(chunk_mb * 1048576.0)) : INT64_MAX;
   for (int32_t i = 0; i < n_ops; ++i) {
     const PhysOp& op = ops[size_t(i)];
     if (op.stream == S_NONE) continue;
     slot[size_t(i)] = n_sync++;
     if (op.kind != OP_CONTRACT) {
+      // H2D copies go in time-slice chunks of ~h2d_chunk bytes; consumers of a chunked copy
+      // wait only for the chunk holding their slice (target -C: C chunks over Lt slices)
       target[size_t(i)] = 1;
+      if (op.kind == OP_H2D && op.stream == S_H2D && Lt > 1 && op.bytes % Lt == 0) {
+        const int64_t C = std::min<int64_t>(Lt, std::max<int64_t>(1, op.bytes / h2d_chunk + (op.bytes % h2d_chunk != 0)));
+        if (C > 1) target[size_t(i)] = -int32_t(C);
+      }
       continue;
     }
     const Node& n = g.nodes[size_t(op.node)];
@@ -612,6 +651,8 @@ void prepare_dataflow(cc_ctx* ctx) {
     }
     target[size_t(i)] = d.n_items;
   }
+  tmr.lap("items+tmaps");
+  std::vector<int64_t> qpos(size_t(n_ops), INT64_MAX);   // merged queue position of compute ops
   // 3. queue order: a topological order of the plan's ops (compute and copy; consecutive
   // copies on one stream are chained, since a copy stream runs in plan order) that delays each
   // TR_MM op by DF_TR_DELAY compute positions, so a trace item is usually claimed after its
@@ -654,7 +695,10 @@ void prepare_dataflow(cc_ctx* ctx) {
     while (!ready.empty()) {
       const int32_t i = ready.top().second;
       ready.pop();
-      if (ops[size_t(i)].kind == OP_CONTRACT) order.push_back(i);
+      if (ops[size_t(i)].kind == OP_CONTRACT) {
+        qpos[size_t(i)] = int64_t(order.size());
+        order.push_back(i);
+      }
       for (int32_t k : succ[size_t(i)])
         if (--indeg[size_t(k)] == 0) ready.push({key(k), k});
     }
@@ -683,6 +727,7 @@ void prepare_dataflow(cc_ctx* ctx) {
     g_items = first;
     t_items = tfirst;
   }
+  tmr.lap("queue order");
   // 4. dependency lists of compute ops, wait lists of copies
   std::vector<int32_t> dep_slot, dep_target;
   auto fill_deps = [&](std::vector<DfOp>& v, const std::vector<int32_t>& plan) {
@@ -737,14 +782,74 @@ void prepare_dataflow(cc_ctx* ctx) {
         ctx->df_copies[size_t(copy_index[size_t(j)])].source = true;
       }
     }
+    if (target[size_t(i)] < 0) c.chunks = -target[size_t(i)];
     copy_index[size_t(i)] = int32_t(ctx->df_copies.size());
     ctx->df_copies.push_back(std::move(c));
+  }
+  {
+    // Copy enqueue order.  A copy stream runs its copies in order; an H2D copy that waits on
+    // nothing (fresh pool memory) may move earlier among the wait-free copies of its run
+    // (runs are delimited by copies that wait) without risking a deadlock: it blocks on
+    // nothing and only completes sooner for whoever needs it.  Wait-free H2D copies are
+    // ordered by the merged-queue position of their first GEMM consumer (TR-only consumers
+    // after every GEMM one), so the GEMM work — most of the step — can start early and the
+    // copies feed it in the order the queue wants them.
+    const size_t nc = ctx->df_copies.size();
+    std::vector<int64_t> key(nc, INT64_MAX);
+    std::vector<std::vector<int32_t>> consumers(static_cast<size_t>(n_ops));
+    for (int32_t i = 0; i < n_ops; ++i)
+      if (ops[size_t(i)].kind == OP_CONTRACT)
+        for (int32_t j : deps[size_t(i)]) consumers[size_t(j)].push_back(i);
+    for (size_t k = 0; k < nc; ++k) {
+      const auto& c = ctx->df_copies[k];
+      for (int32_t i : consumers[size_t(c.op)]) {
+        const bool tr = g.nodes[size_t(ops[size_t(i)].node)].op == CC_TR_MM;
+        key[k] = std::min(key[k], qpos[size_t(i)] + (tr ? int64_t(n_ops) : 0));
+      }
+    }
+    std::vector<int32_t> seq[3];
+    for (size_t k = 0; k < nc; ++k) seq[ctx->df_copies[k].stream].push_back(int32_t(k));
+    const bool reorder = getenv("CC_COPY_REORDER") ? atoi(getenv("CC_COPY_REORDER")) != 0 : true;
+    if (reorder) {
+      auto& h = seq[S_H2D];
+      size_t a = 0;
+      while (a < h.size()) {
+        size_t b = a;
+        auto free_of_waits = [&](int32_t k) {
+          const auto& c = ctx->df_copies[size_t(k)];
+          return c.wait_values.empty() && c.wait_events.empty();
+        };
+        while (b < h.size() && free_of_waits(h[b])) ++b;
+        std::stable_sort(h.begin() + int64_t(a), h.begin() + int64_t(b),
+                         [&](int32_t x, int32_t y) { return key[size_t(x)] < key[size_t(y)]; });
+        a = b + 1;
+      }
+    }
+    // merge the two streams' sequences so every event source is enqueued before its waiters
+    std::vector<uint8_t> done(nc, 0);
+    size_t p[3] = {0, 0, 0};
+    ctx->df_issue.clear();
+    while (ctx->df_issue.size() < nc) {
+      int pick = -1;
+      for (int st : {int(S_H2D), int(S_D2H)}) {
+        if (p[st] >= seq[st].size()) continue;
+        const auto& c = ctx->df_copies[size_t(seq[st][p[st]])];
+        bool ok = true;
+        for (int32_t e : c.wait_events) ok = ok && done[size_t(e)];
+        if (ok && (pick < 0 || seq[st][p[st]] < seq[pick][p[pick]])) pick = st;
+      }
+      if (pick < 0) throw Error(CC_E_STATE, "dataflow: copy order cycle");
+      const int32_t k = seq[pick][p[pick]++];
+      done[size_t(k)] = 1;
+      ctx->df_issue.push_back(k);
+    }
   }
   if (!ctx->df_copies.empty() && (!df_wait_fn() || !df_write_fn()))
     throw Error(CC_E_CUDA, "stream memory operations (cuStreamWaitValue32) unavailable");
   ctx->df_events.assign(ctx->df_copies.size(), nullptr);
   for (size_t k = 0; k < ctx->df_copies.size(); ++k)
     if (ctx->df_copies[k].source) ck(cudaEventCreateWithFlags(&ctx->df_events[k], cudaEventDisableTiming), "event");
+  tmr.lap("deps+copies+events");
   // 5. upload metadata: [heads | sync][gops][tops][dep_slot][dep_target][tmaps]
   const size_t sz_sync = round_up(16 + int64_t(n_sync) * 4, 256);
   const size_t sz_g = round_up(int64_t(std::max<size_t>(gops.size(), 1) * sizeof(DfOp)), 256);
@@ -758,7 +863,16 @@ void prepare_dataflow(cc_ctx* ctx) {
     std::fill(titem_op.begin() + tops[k].first_item, titem_op.begin() + tops[k].first_item + tops[k].n_items, int32_t(k));
   const size_t sz_gi = round_up(int64_t(gitem_op.size() * 4), 256), sz_ti = round_up(int64_t(titem_op.size() * 4), 256);
   const size_t total = sz_sync + sz_g + sz_t + 2 * sz_d + sz_m + sz_gi + sz_ti;
-  ck(cudaMalloc(reinterpret_cast<void**>(&ctx->df_meta), total), "dataflow metadata");
+  // device region: the top of the pool when the plan's high water leaves room (no allocation
+  // on the execute path), else a cudaMalloc
+  const int64_t meta_off = (ctx->pool_bytes - int64_t(total)) / 256 * 256;
+  if (meta_off >= ctx->pp.pool_high_water) {
+    ctx->df_meta = ctx->arena + meta_off;
+    ctx->df_meta_owned = false;
+  } else {
+    ck(cudaMalloc(reinterpret_cast<void**>(&ctx->df_meta), total), "dataflow metadata");
+    ctx->df_meta_owned = true;
+  }
   ctx->df_meta_bytes = total;
   char* m = ctx->df_meta;
   unsigned long long* heads = reinterpret_cast<unsigned long long*>(m);
@@ -771,17 +885,21 @@ void prepare_dataflow(cc_ctx* ctx) {
   char* pm = pdt + sz_d;
   char* pgi = pm + sz_m;
   char* pti = pgi + sz_gi;
-  ck(cudaMemset(m, 0, total), "dataflow metadata");
-  ck(cudaMemcpy(pgi, gitem_op.data(), gitem_op.size() * 4, cudaMemcpyHostToDevice), "upload");
-  ck(cudaMemcpy(pti, titem_op.data(), titem_op.size() * 4, cudaMemcpyHostToDevice), "upload");
-  if (!gops.empty()) ck(cudaMemcpy(pg, gops.data(), gops.size() * sizeof(DfOp), cudaMemcpyHostToDevice), "upload");
-  if (!tops.empty()) ck(cudaMemcpy(pt, tops.data(), tops.size() * sizeof(DfOp), cudaMemcpyHostToDevice), "upload");
-
-  if (!dep_slot.empty()) {
-    ck(cudaMemcpy(pds, dep_slot.data(), dep_slot.size() * 4, cudaMemcpyHostToDevice), "upload");
-    ck(cudaMemcpy(pdt, dep_target.data(), dep_target.size() * 4, cudaMemcpyHostToDevice), "upload");
+  {
+    // one host image, one copy
+    std::vector<char> img(total, 0);
+    auto put = [&](char* dst, const void* src, size_t n) {
+      if (n) std::memcpy(img.data() + (dst - m), src, n);
+    };
+    put(pgi, gitem_op.data(), gitem_op.size() * 4);
+    put(pti, titem_op.data(), titem_op.size() * 4);
+    put(pg, gops.data(), gops.size() * sizeof(DfOp));
+    put(pt, tops.data(), tops.size() * sizeof(DfOp));
+    put(pds, dep_slot.data(), dep_slot.size() * 4);
+    put(pdt, dep_target.data(), dep_target.size() * 4);
+    put(pm, tmaps.data(), tmaps.size());
+    ck(cudaMemcpy(m, img.data(), total, cudaMemcpyHostToDevice), "dataflow metadata upload");
   }
-  if (!tmaps.empty()) ck(cudaMemcpy(pm, tmaps.data(), tmaps.size(), cudaMemcpyHostToDevice), "upload");
   DfArgs& da = ctx->df_gemm;
   da.dep_slot = reinterpret_cast<const int32_t*>(pds);
   da.dep_target = reinterpret_cast<const int32_t*>(pdt);
@@ -797,6 +915,7 @@ void prepare_dataflow(cc_ctx* ctx) {
       return std::min(std::max(v ? atoi(v) : dflt, lo), hi);
     };
     da.tr_ratio = env_int("CC_DF_TR_RATIO", 2, 0, 64);
+    da.Lt = int32_t(Lt);
     da.ahead_g = env_int("CC_DF_AHEAD_G", 2, 1, 4);
     da.ahead_t = env_int("CC_DF_AHEAD_T", 2, 1, 4);
   }
@@ -808,15 +927,17 @@ void prepare_dataflow(cc_ctx* ctx) {
     ck(cudaStreamCreateWithFlags(&ctx->cs2, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&ctx->ev_cs2, cudaEventDisableTiming), "event");
   }
+  tmr.lap("upload");
   ctx->df_valid = true;
 }
 
 // Enqueues one dataflow replay; returns the number of kernel launches.
-int issue_dataflow(cc_ctx* ctx) {
+int issue_dataflow(cc_ctx* ctx, bool time_copies = false) {
   const Dag& g = *ctx->dag;
   int nl = 0;
   static const bool dbg = getenv("CC_DEBUG") != nullptr;
 #define DBG(...) do { if (dbg) { fprintf(stderr, "[cc] " __VA_ARGS__); fputc('\n', stderr); fflush(stderr); } } while (0)
+  PhaseTimer tmr("issue_dataflow");
   DBG("issue_dataflow: %zu copies, %lld gemm items, %lld trace items", ctx->df_copies.size(),
       (long long)ctx->df_gemm_items, (long long)ctx->df_trace_items);
   ck(cudaMemsetAsync(ctx->df_meta, 0, ctx->df_sync_bytes, ctx->cs), "memset");
@@ -825,7 +946,8 @@ int issue_dataflow(cc_ctx* ctx) {
   ck(cudaStreamWaitEvent(ctx->ds, ctx->ev_start, 0), "wait");
   ck(cudaStreamWaitEvent(ctx->cs2, ctx->ev_start, 0), "wait");
   cudaStream_t st[3] = {ctx->cs, ctx->hs, ctx->ds};
-  for (size_t k = 0; k < ctx->df_copies.size(); ++k) {
+  for (const int32_t kk : ctx->df_issue) {
+    const size_t k = size_t(kk);
     const auto& c = ctx->df_copies[k];
     cudaStream_t s = st[c.stream];
     for (int32_t e : c.wait_events) ck(cudaStreamWaitEvent(s, ctx->df_events[size_t(e)], 0), "wait");
@@ -834,20 +956,35 @@ int issue_dataflow(cc_ctx* ctx) {
                        CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
         throw Error(CC_E_CUDA, "cuStreamWaitValue32 failed");
     DBG("copy %zu: stream %d bytes %zu waits %zu/%zu", k, c.stream, c.bytes, c.wait_values.size(), c.wait_events.size());
-    ck(cudaMemcpyAsync(c.dst, c.src, c.bytes, c.stream == S_H2D ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, s),
-       "copy");
+    const cudaMemcpyKind kind = c.stream == S_H2D ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    const size_t per_t = c.bytes / size_t(std::max<int64_t>(g.Lt, 1));
+    for (int32_t ch = 0; ch < c.chunks; ++ch) {
+      // chunk ch: slices [ch*Lt/C, (ch+1)*Lt/C); flag = chunks finished
+      const size_t t0 = c.chunks == 1 ? 0 : size_t(int64_t(ch) * g.Lt / c.chunks);
+      const size_t t1 = c.chunks == 1 ? 0 : size_t(int64_t(ch + 1) * g.Lt / c.chunks);
+      const size_t off = t0 * per_t, len = c.chunks == 1 ? c.bytes : (t1 - t0) * per_t;
+      ck(cudaMemcpyAsync(static_cast<char*>(c.dst) + off, static_cast<const char*>(c.src) + off, len, kind, s), "copy");
+      if (df_write_fn()(s, reinterpret_cast<CUdeviceptr>(ctx->df_sync + c.flag_slot), cuuint32_t(ch + 1), 0) !=
+          CUDA_SUCCESS)
+        throw Error(CC_E_CUDA, "cuStreamWriteValue32 failed");
+    }
     DBG("copy %zu enqueued", k);
-    if (df_write_fn()(s, reinterpret_cast<CUdeviceptr>(ctx->df_sync + c.flag_slot), 1, 0) != CUDA_SUCCESS)
-      throw Error(CC_E_CUDA, "cuStreamWriteValue32 failed");
     if (c.source) ck(cudaEventRecord(ctx->df_events[k], s), "event");
   }
   DBG("copies enqueued");
+  if (time_copies) {
+    ck(cudaEventRecord(ctx->ev_copy_h, ctx->hs), "event");
+    ck(cudaEventRecord(ctx->ev_copy_d, ctx->ds), "event");
+  }
+  ctx->copy_timed = time_copies;
+  tmr.lap("copies");
   if (ctx->df_gemm_items + ctx->df_trace_items > 0) {
     ck(df_launch(ctx->df_gemm, ctx->num_sms, ctx->cs), "dataflow worker");
     DBG("worker launched");
     ++nl;
   }
   DBG("workers launched");
+  tmr.lap("worker");
   ck(cudaEventRecord(ctx->ev_cs2, ctx->cs2), "event");
   ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_cs2, 0), "wait");
   ck(launch_correlate(ctx->roots, ctx->corr, int64_t(g.corr_ids.size()), g.Lt, ctx->term_start, ctx->term_tree,
@@ -1056,7 +1193,7 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
       }
       ck(cudaGraphLaunch(ctx->gexec_df, ctx->cs), "graph launch");
     } else {
-      ctx->last_n_kernels = issue_dataflow(ctx);
+      ctx->last_n_kernels = issue_dataflow(ctx, blocking);
     }
   } else if (use_graph) {
     if (!ctx->gexec) {
@@ -1088,6 +1225,12 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
       float ms = 0;
       ck(cudaEventElapsedTime(&ms, t_begin, t_end), "elapsed");
       stats->seconds = ms * 1e-3;
+      if (ctx->copy_timed && !ctx->df_copies.empty()) {
+        float mh = 0, md = 0;
+        ck(cudaEventElapsedTime(&mh, t_begin, ctx->ev_copy_h), "elapsed");
+        ck(cudaEventElapsedTime(&md, t_begin, ctx->ev_copy_d), "elapsed");
+        stats->copy_seconds = std::max(mh, md) * 1e-3;
+      }
     }
     const Dag& g = *ctx->dag;
     for (const auto& op : ctx->pp.ops)
@@ -1171,6 +1314,7 @@ cc_status cc_create(cc_ctx** out, int device, void* dev_arena, size_t arena_byte
     }
     for (cudaEvent_t* e : {&ctx->ev_start, &ctx->ev_end, &ctx->ev_h_end, &ctx->ev_d_end})
       ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    for (cudaEvent_t* e : {&ctx->ev_copy_h, &ctx->ev_copy_d}) ck(cudaEventCreate(e), "event");
     ck(zgemm_preload(), "kernel load");
     ck(trace_preload(), "kernel load");
     ck(df_preload(), "kernel load");

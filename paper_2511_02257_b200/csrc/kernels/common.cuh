@@ -59,6 +59,7 @@ struct Cfg {
   static constexpr int NCW = WARPS_M * WARPS_N;  // consumer (DMMA) warps
   static constexpr int THREADS = (NCW + 1) * 32;
   static constexpr int MI = WM / 8, NI = WN / 4;
+  static constexpr int NJ = WN / 8;              // 3M: 8-complex column blocks per warp tile
   static constexpr int FRAG = MI * NI * 2;       // accumulator doubles per lane
   static constexpr int A_BYTES = BM * BK * 16, B_BYTES = BK * BN * 16;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -122,6 +123,72 @@ __device__ __forceinline__ void dmma_ktile(const uint8_t* sA, const uint8_t* sB,
         for (int k = 0; k < C::NI; ++k) dmma(acc[i][k][0], acc[i][k][1], a[i].y, b_im_row[k]);
     }
   }
+}
+
+// 3M (Gauss) form of the same k-tile: three real products per complex one,
+//   P0 += Ar Br,  P1 += Ai Bi,  P2 += (Ar + Ai)(Br + Bi),
+// so that C = (P0 - P1) + i (P2 - P0 - P1) (see gauss3m_combine): 6 instead of 8 real flops
+// per complex MAC (reading V-3).  The DMMA k index t of lane (g, t) is complex
+// k = 8 kc + 2t + h for both operands (same conflict-free permutation as dmma_ktile); the
+// real accumulator D[g][2t + e] of block (i, j) is complex C[row0 + 8i + g][col0 + 8j + 2t + e].
+// The operand sums of one k-quad as ONE asm block: the FP64 adds share the datapath with the
+// DMMAs, and grouping them keeps the compiler from scattering them between DMMAs.
+template <int MI, int NJ>
+__device__ __forceinline__ void gauss3m_sums(const double (&ar)[MI], const double (&ai)[MI], double (&as)[MI],
+                                             const double (&br)[NJ], const double (&bi)[NJ], double (&bs)[NJ]) {
+  static_assert(MI == 4 && NJ == 2, "grouped sums are written for the 32 x 16 warp tile");
+  asm("add.f64 %0, %6, %7;\n\tadd.f64 %1, %8, %9;\n\tadd.f64 %2, %10, %11;\n\tadd.f64 %3, %12, %13;\n\t"
+      "add.f64 %4, %14, %15;\n\tadd.f64 %5, %16, %17;"
+      : "=d"(as[0]), "=d"(as[1]), "=d"(as[2]), "=d"(as[3]), "=d"(bs[0]), "=d"(bs[1])
+      : "d"(ar[0]), "d"(ai[0]), "d"(ar[1]), "d"(ai[1]), "d"(ar[2]), "d"(ai[2]), "d"(ar[3]), "d"(ai[3]), "d"(br[0]),
+        "d"(bi[0]), "d"(br[1]), "d"(bi[1]));
+}
+
+template <class C>
+__device__ __forceinline__ void dmma3m_ktile(const uint8_t* sA, const uint8_t* sB, int wm, int wn, int g, int t,
+                                             double (&p)[3][C::MI][C::NJ][2]) {
+  static_assert(C::WM % 8 == 0 && C::WN % 8 == 0, "lane-constant swizzle keys need WM, WN % 8 == 0");
+  const uint8_t* a_base = sA + (wm * C::WM + g) * 128;
+  const uint8_t* b_base = sB + (wn * C::WN / 8) * (C::BK * 128);
+#pragma unroll
+  for (int kc = 0; kc < C::BK / 8; ++kc) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int s = 2 * t + h;       // complex k slot within the 8-complex chunk
+      const int krow = kc * 8 + s;   // B row within the stage (krow & 7 == s)
+      double ar[C::MI], ai[C::MI], as[C::MI], br[C::NJ], bi[C::NJ], bs[C::NJ];
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i) {
+        const double2 a = *reinterpret_cast<const double2*>(a_base + kc * C::BM * 128 + i * 1024 + ((s ^ g) << 4));
+        ar[i] = a.x;
+        ai[i] = a.y;
+      }
+#pragma unroll
+      for (int j = 0; j < C::NJ; ++j) {
+        const double2 b = *reinterpret_cast<const double2*>(b_base + j * (C::BK * 128) + krow * 128 + ((g ^ s) << 4));
+        br[j] = b.x;
+        bi[j] = b.y;
+      }
+      gauss3m_sums<C::MI, C::NJ>(ar, ai, as, br, bi, bs);
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NJ; ++j) dmma(p[0][i][j][0], p[0][i][j][1], ar[i], br[j]);
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NJ; ++j) dmma(p[1][i][j][0], p[1][i][j][1], ai[i], bi[j]);
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NJ; ++j) dmma(p[2][i][j][0], p[2][i][j][1], as[i], bs[j]);
+    }
+  }
+}
+// complex result of the 3M products of accumulator (i, j, e)
+template <class C>
+__device__ __forceinline__ double2 gauss3m_combine(const double (&p)[3][C::MI][C::NJ][2], int i, int j, int e) {
+  return make_double2(p[0][i][j][e] - p[1][i][j][e], (p[2][i][j][e] - p[0][i][j][e]) - p[1][i][j][e]);
 }
 
 using Big = Cfg<64, 64, 16, 32, 16, 4>;

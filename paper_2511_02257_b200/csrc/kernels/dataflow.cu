@@ -133,11 +133,16 @@ __device__ __forceinline__ void decode_item(const DfQueue& q, int64_t item, Item
   }
 }
 
-// Non-blocking dependency poll: advances *dep past satisfied dependencies.
-__device__ __forceinline__ bool deps_ready(const DfArgs& a, const DfOp& op, int* dep) {
+// Non-blocking dependency poll of an item working on time slice `slice`: advances *dep past
+// satisfied dependencies.  A chunked copy (target -C) is needed only up to the chunk holding
+// the slice: chunk k covers slices [k*Lt/C, (k+1)*Lt/C), so slice s is in chunk
+// floor(((s+1)*C - 1) / Lt).
+__device__ __forceinline__ bool deps_ready(const DfArgs& a, const DfOp& op, int slice, int* dep) {
   while (*dep < op.dep_count) {
     const int k = op.dep_begin + *dep;
-    if (ld_acquire(a.sync + a.dep_slot[k]) < a.dep_target[k]) return false;
+    int target = a.dep_target[k];
+    if (target < 0) target = int((int64_t(slice + 1) * (-target) - 1) / a.Lt) + 1;
+    if (ld_acquire(a.sync + a.dep_slot[k]) < target) return false;
     ++*dep;
   }
   return true;
@@ -346,7 +351,7 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
         }
         idle = false;
       }
-      if (pending && deps_ready(a, Q.ops[inf.op], &dep)) {
+      if (pending && deps_ready(a, Q.ops[inf.op], x == 0 ? inf.b : inf.t, &dep)) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
         asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tA) : "memory");
         asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tB) : "memory");
@@ -374,12 +379,11 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
   // ----------------------------------- consumers ---------------------------------------------
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
   const int g = lane >> 2, t = lane & 3;
-  const bool q = (g & 1) != 0;
   const bool prof = a.prof != nullptr;
-  double acc[C::MI][C::NI][2];
+  double acc[3][C::MI][C::NJ][2];   // 3M products (common.cuh dmma3m_ktile)
   double2 tacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
   // profile (thread 0): clock64 cycles waiting for stage data / in stage math+epilogue, per kind
-  long long c_wait[2] = {0, 0}, c_work[2] = {0, 0}, n_st[2] = {0, 0}, ta = 0, tb = 0;
+  long long c_wait[2] = {0, 0}, c_work[2] = {0, 0}, n_st[2] = {0, 0}, ta = 0, tb = 0, c_epi = 0, te = 0;
   int lastk = 0;
   for (uint32_t r = 0;; ++r) {
     const int st = int(r % C::STAGES);
@@ -400,6 +404,7 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
         ps[4] = n_st[0];
         ps[5] = n_st[1];
         ps[6] = smid();
+        ps[7] = c_epi;
       }
       break;
     }
@@ -415,33 +420,49 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
       // ---------------- GEMM k-tile of a tile (or k-chunk of a tile) ----------------
       if (d & SD_FIRST) {
 #pragma unroll
-        for (int i = 0; i < C::MI; ++i)
+        for (int x = 0; x < 3; ++x)
 #pragma unroll
-          for (int k = 0; k < C::NI; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
+          for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+            for (int j = 0; j < C::NJ; ++j) acc[x][i][j][0] = acc[x][i][j][1] = 0.0;
         if (tid == 0 && prof) s_info[0][slot].t_first = gtimer();
       }
-      dmma_ktile<C>(sA, sA + C::A_BYTES, wm, wn, g, t, q, acc);
+      dmma3m_ktile<C>(sA, sA + C::A_BYTES, wm, wn, g, t, acc);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
       if (!(d & SD_LAST)) continue;
+      if (prof && tid == 0) te = clock64();
       const ItemInfo& cur = s_info[0][slot];
       const DfOp& op = a.q.ops[cur.op];
       if (tid == 0 && prof) s_info[0][slot].t_comp = gtimer();
       const int64_t tile = cur.tile;
       const int chunk = cur.chunk;
       double2* out = static_cast<double2*>(op.C) + int64_t(cur.b) * op.sCb;
-      bool store = true;
-      if (op.n_chunks > 1) {
+      // complex results C[row0 + 8i + g][col0 + 8j + 2t + e] = gauss3m_combine(acc, i, j, e)
+      if (op.n_chunks == 1) {
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i) {
+          const int64_t row = int64_t(cur.tm) * C::BM + wm * C::WM + i * 8 + g;
+          if (row >= op.M) continue;
+#pragma unroll
+          for (int j = 0; j < C::NJ; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int64_t col = int64_t(cur.tn) * C::BN + wn * C::WN + j * 8 + 2 * t + e;
+              if (col < op.Nn) out[row * op.ldc + col] = gauss3m_combine<C>(acc, i, j, e);
+            }
+        }
+      } else {
         // publish this chunk's partial; the CTA completing the tile's last chunk sums them
-        double* base = static_cast<double*>(op.part) + (tile * op.n_chunks) * int64_t(C::SLOT_DOUBLES);
-        double* mine = base + int64_t(chunk) * C::SLOT_DOUBLES + warp * (C::FRAG * 32);
+        double2* base = static_cast<double2*>(op.part) + (tile * op.n_chunks) * int64_t(C::SLOT_DOUBLES / 2);
+        double2* mine = base + int64_t(chunk) * (C::SLOT_DOUBLES / 2) + warp * (C::FRAG / 2 * 32);
 #pragma unroll
         for (int i = 0; i < C::MI; ++i)
 #pragma unroll
-          for (int k = 0; k < C::NI; ++k) {
-            __stcg(mine + ((i * C::NI + k) * 2 + 0) * 32 + lane, acc[i][k][0]);
-            __stcg(mine + ((i * C::NI + k) * 2 + 1) * 32 + lane, acc[i][k][1]);
-          }
+          for (int j = 0; j < C::NJ; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              __stcg(mine + ((i * C::NJ + j) * 2 + e) * 32 + lane, gauss3m_combine<C>(acc, i, j, e));
         __threadfence();
         named_sync(1, CW);
         if (tid == 0) {
@@ -450,40 +471,33 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
           if (s_flag) op.tile_cnt[tile] = 0;
         }
         named_sync(1, CW);
-        store = s_flag != 0;
-        if (store) {
+        if (s_flag) {
           __threadfence();
+          const double2* w0 = base + warp * (C::FRAG / 2 * 32);
 #pragma unroll
-          for (int i = 0; i < C::MI; ++i)
+          for (int i = 0; i < C::MI; ++i) {
+            const int64_t row = int64_t(cur.tm) * C::BM + wm * C::WM + i * 8 + g;
 #pragma unroll
-            for (int k = 0; k < C::NI; ++k) acc[i][k][0] = acc[i][k][1] = 0.0;
-          for (int c = 0; c < op.n_chunks; ++c) {
-            const double* src = base + int64_t(c) * C::SLOT_DOUBLES + warp * (C::FRAG * 32);
+            for (int j = 0; j < C::NJ; ++j)
 #pragma unroll
-            for (int i = 0; i < C::MI; ++i)
-#pragma unroll
-              for (int k = 0; k < C::NI; ++k) {
-                acc[i][k][0] += __ldcg(src + ((i * C::NI + k) * 2 + 0) * 32 + lane);
-                acc[i][k][1] += __ldcg(src + ((i * C::NI + k) * 2 + 1) * 32 + lane);
+              for (int e = 0; e < 2; ++e) {
+                const int f = ((i * C::NJ + j) * 2 + e) * 32 + lane;
+                double2 v = __ldcg(w0 + f);
+                for (int c = 1; c < op.n_chunks; ++c) {
+                  const double2 u = __ldcg(w0 + int64_t(c) * (C::SLOT_DOUBLES / 2) + f);
+                  v.x += u.x;
+                  v.y += u.y;
+                }
+                const int64_t col = int64_t(cur.tn) * C::BN + wn * C::WN + j * 8 + 2 * t + e;
+                if (row < op.M && col < op.Nn) out[row * op.ldc + col] = v;
               }
-          }
-        }
-      }
-      if (store) {
-#pragma unroll
-        for (int i = 0; i < C::MI; ++i) {
-          const int64_t row = int64_t(cur.tm) * C::BM + wm * C::WM + i * 8 + g;
-          if (row >= op.M) continue;
-#pragma unroll
-          for (int k = 0; k < C::NI; ++k) {
-            const int64_t col = int64_t(cur.tn) * C::BN + wn * C::WN + k * 4 + t;
-            if (col < op.Nn) out[row * op.ldc + col] = make_double2(acc[i][k][0], acc[i][k][1]);
           }
         }
       }
       // item finished: this warp's stores (ordered by __syncwarp) before the arrival
       __syncwarp();
       if (lane == 0) mbar_arrive(&done[0][slot]);
+      if (prof && tid == 0) c_epi += clock64() - te;
     } else {
       // ---------------- TR_MM block pair: sum of A[r][c] * B[c][r] ----------------
       if (d & SD_FIRST) {

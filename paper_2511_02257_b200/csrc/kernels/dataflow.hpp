@@ -55,7 +55,8 @@ struct DfArgs {
   DfQueue q;                  // GEMM items
   DfQueue qt;                 // TR_MM items
   const int32_t* dep_slot;    // sync slot an op waits on
-  const int32_t* dep_target;  // value the slot must reach
+  const int32_t* dep_target;  // value the slot must reach; -C: a copy in C time-slice chunks,
+                              // the item needs the chunk holding its slice (value chunk+1)
   const void* tmaps;          // CUtensorMap array (64-byte aligned, global memory)
   int* sync;                  // done counters + copy flags (zeroed per launch)
   unsigned long long* prof;   // optional: per GEMM item {claim, ready, end, smid, first data, loop end, kind, -}
@@ -63,6 +64,7 @@ struct DfArgs {
   long long* prof_sm;         // optional: per CTA {wait cycles G/T, work cycles G/T, stages G/T, smid, -}
   int32_t tr_ratio;           // TR_MM stages the issuer may interleave per GEMM k-tile
   int32_t ahead_g, ahead_t;   // items a CTA may hold claimed-but-unpublished per queue (<= 4)
+  int32_t Lt;                 // time slices (chunked-copy targets)
 };
 
 cudaError_t df_preload();

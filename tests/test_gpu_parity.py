@@ -161,6 +161,36 @@ def test_schedule_and_mode_invariance_bitwise():
     assert_roots_close(legacy, base, rel=1e-13)
 
 
+def test_chunked_and_reordered_h2d_copies(monkeypatch):
+    """Host leaves copied in time-slice chunks (items wait only for the chunk holding their
+    slice) and wait-free copies moved ahead in queue order: same values as the oracle and
+    bit-identical to whole-tensor copies in plan order (the copy schedule never changes
+    the arithmetic)."""
+    w = dags.config_c2(N=40, Lt=8, n_loop4=60, n_loop2=6, n_corr=4)
+    dag = Dag(w)
+    r_or, c_or = values.run_workload(w, dag)
+    monkeypatch.setenv("CC_H2D_CHUNK_MB", "100")
+    monkeypatch.setenv("CC_COPY_REORDER", "0")
+    base = run_gpu(w)[1]
+    for chunk_mb, reorder in (("0.0625", "0"), ("0.0625", "1"), ("0.01", "1"), ("100", "1")):
+        monkeypatch.setenv("CC_H2D_CHUNK_MB", chunk_mb)
+        monkeypatch.setenv("CC_COPY_REORDER", reorder)
+        for flags in (0, 1):
+            _, roots, corr, st, ex = run_gpu(w, flags=flags)
+            assert_roots_close(roots, r_or)
+            assert_corr_close(dag, r_or, corr, c_or)
+            for t in base:
+                assert np.array_equal(base[t], roots[t]), (chunk_mb, reorder, flags)
+    # baryon leaves (Lt=2 -> at most 2 chunks)
+    monkeypatch.setenv("CC_H2D_CHUNK_MB", "0.0625")
+    w = dags.config_c3(N=12, Lt=2, S=64)
+    dag = Dag(w)
+    r_or, c_or = values.run_workload(w, dag)
+    _, roots, corr, st, ex = run_gpu(w)
+    assert_roots_close(roots, r_or)
+    assert_corr_close(dag, r_or, corr, c_or)
+
+
 def test_c3_nucleon_small():
     for (N, Lt, S) in ((8, 2, 4), (12, 2, 64), (20, 1, 64)):
         w = dags.config_c3(N=N, Lt=Lt, S=S)

@@ -31,6 +31,8 @@ print("plain executes (ms):", np.round(ts, 3))
 ex = ctx.execute(cc.EXEC_PROFILE)
 gp, tp, psm = ctx.dataflow_profile(per_sm=True)
 tot = psm[:, :4].sum(axis=1).astype(np.float64)
+print("GEMM epilogue (thread 0, included in work G): %.0f cycles per item, %.1f%% of consumer time"
+      % (psm[:, 7].sum() / max(psm[:, 4].sum() / 8, 1), 100 * psm[:, 7].sum() / tot.sum()))
 print("per CTA (clock64): wait G %.1f%%  wait T %.1f%%  work G %.1f%%  work T %.1f%%;  stages G %d  T %d;"
       "  per stage: G wait %.0f + work %.0f cyc, T wait %.0f + work %.0f cyc"
       % tuple([100 * psm[:, k].sum() / tot.sum() for k in range(4)] + [psm[:, 4].sum(), psm[:, 5].sum()] +
