@@ -71,7 +71,9 @@ typedef struct { int64_t tree_id; int64_t root; } cc_tree;
 /* Correlator term: C_corr[t] += (re + i im) * root_tree[t]. */
 typedef struct { int64_t corr_id; int64_t tree_id; double re, im; } cc_term;
 
-typedef enum { CC_SIBLING = 0, CC_TREE = 1, CC_GIVEN = 2 } cc_algo;
+/* CC_RSGS: RS-GS-like baseline — Redstar's similarity sort of trees (the paper's
+ * RS-GS comparison of §IV) under DESIGN.md readings R-1..R-4. */
+typedef enum { CC_SIBLING = 0, CC_TREE = 1, CC_GIVEN = 2, CC_RSGS = 3 } cc_algo;
 
 typedef struct {
   int32_t algo;               /* cc_algo                                                   */
@@ -153,7 +155,7 @@ cc_status cc_schedule(cc_ctx* ctx, const cc_sched_cfg* cfg, int64_t* order_out, 
 cc_status cc_memory_trace(cc_ctx* ctx, int64_t* m_out, int64_t* transient_out, int64_t cap, int64_t* n_out);
 /* The op queue of the current plan, in order. */
 cc_status cc_plan_ops(cc_ctx* ctx, cc_plan_op* out, int64_t cap, int64_t* n_out);
-/* Tree-scheduler selection order of the last CC_TREE schedule (tree ids). */
+/* Tree order of the last CC_TREE (selection order) or CC_RSGS (similarity chain) schedule (tree ids). */
 cc_status cc_tree_order(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out);
 /* Per-step op queue as CSV (step, op, node, bytes, offset, device_used). */
 cc_status cc_plan_dump(cc_ctx* ctx, const char* csv_path);

@@ -21,7 +21,7 @@ c_i32, c_i64, c_u64, c_dbl, c_void_p, c_size_t = (ctypes.c_int32, ctypes.c_int64
 P = ctypes.POINTER
 
 CC_LEAF_M, CC_LEAF_B, CC_MM1, CC_BM1, CC_BB2, CC_TR_MM, CC_LEAF_X, CC_OP_X = range(8)
-CC_SIBLING, CC_TREE, CC_GIVEN = range(3)
+CC_SIBLING, CC_TREE, CC_GIVEN, CC_RSGS = range(4)
 PART_TIME, PART_TREES = 0, 1
 EXEC_GRAPH, EXEC_TIME_KERNELS, EXEC_ONLY_GEMM, EXEC_ONLY_TRACE, EXEC_OP_BY_OP, EXEC_PROFILE = 1, 2, 4, 8, 16, 32
 STATUS = {0: "OK", -1: "INVAL", -2: "PARSE", -3: "CYCLE", -4: "INCONSISTENT", -5: "MULTIROOT",

@@ -1411,6 +1411,9 @@ cc_status cc_schedule(cc_ctx* ctx, const cc_sched_cfg* cfg, int64_t* order_out, 
     TreeSchedule ts = tree_schedule(g);
     order = std::move(ts.order);
     tree_order = std::move(ts.tree_order);
+  } else if (cfg->algo == CC_RSGS) {
+    order = rsgs_schedule(g);
+    tree_order = rsgs_tree_chain(g);
   } else if (cfg->algo == CC_GIVEN) {
     if (cfg->n_given < 0 || (cfg->n_given > 0 && !cfg->given_order)) throw Error(CC_E_INVAL, "bad given order");
     order.reserve(size_t(cfg->n_given));

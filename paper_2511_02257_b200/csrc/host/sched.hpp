@@ -17,4 +17,9 @@ struct TreeSchedule {
 // Alg. 4-8, tree scheduler (§III-B); O(kE).
 TreeSchedule tree_schedule(const Dag& g);
 
+// RS-GS-like baseline (Redstar's similarity sort, §II-A; readings R-1..R-4):
+// the similarity chain of tree indices and the resulting contraction order.
+std::vector<int32_t> rsgs_tree_chain(const Dag& g);
+std::vector<int32_t> rsgs_schedule(const Dag& g);
+
 }  // namespace cc

@@ -152,7 +152,8 @@ def test_schedule_and_mode_invariance_bitwise():
     from paper_2511_02257_b200 import cc
     w = dags.config_c2(N=24, Lt=2, n_loop4=40, n_loop2=4, n_corr=3)
     base = run_gpu(w, algo=cc.CC_TREE)[1]
-    for kw in (dict(algo=cc.CC_SIBLING), dict(flags=1), dict(device_leaves=True), dict(flags=1, device_leaves=True)):
+    for kw in (dict(algo=cc.CC_SIBLING), dict(algo=cc.CC_RSGS), dict(flags=1), dict(device_leaves=True),
+               dict(flags=1, device_leaves=True)):
         other = run_gpu(w, **kw)[1]
         for t in base:
             assert np.array_equal(base[t], other[t]), kw

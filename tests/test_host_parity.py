@@ -197,3 +197,30 @@ def test_device_calls_fail_on_host_only_ctx():
     with pytest.raises(cc.CCError) as e:
         c.execute()
     assert e.value.code == "STATE"
+
+
+def test_rsgs_matches_oracle():
+    """CC_RSGS (RS-GS-like baseline, readings R-1..R-4) == oracle/rsgs.py, order and chain,
+    on random DAGs and the configs at full scale; plans under caps too."""
+    from oracle import rsgs
+    cases = [dags.fixture_dstar(), dags.fixture_f1()]
+    cases += [dags.random_dag(s, n_leaves=3 + s % 7, n_trees=1 + s % 9, max_ops_per_tree=1 + s % 5,
+                              share_p=(s % 10) / 10, max_size=1 + s % 6) for s in range(120)]
+    cases += [dags.config_c2(), dags.config_c4(), dags.config_c5(N=256, n_pairs=400, n_trees=3000)]
+    for w in cases:
+        dag = Dag(w)
+        c = _ctx(w)
+        o_cc, st = c.schedule(cc.CC_RSGS)
+        assert o_cc == rsgs.schedule(dag)
+        assert c.tree_order() == rsgs.tree_chain(dag)
+        sim = simulate(dag, o_cc)
+        assert st["model_peak"] == sim["peak"]
+    w = dags.config_c4(N=8, Lt=1, S=4, n_trees=200)
+    dag = Dag(w)
+    order = rsgs.schedule(dag)
+    c = _ctx(w)
+    for cap in (None, 12 * 16 * 4 * 8 ** 3, 7 * 16 * 4 * 8 ** 3):
+        p = lru.plan(dag, order, cap)
+        _, st = c.schedule(cc.CC_RSGS, cap_bytes=cap or 0)
+        for k in ("evictions", "h2d_count", "d2h_count", "h2d_bytes", "d2h_bytes", "peak", "transient_peak"):
+            assert st[k] == p[k], (k, cap)
