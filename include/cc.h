@@ -96,7 +96,8 @@ typedef struct {
 } cc_plan_stats;
 
 typedef struct {
-  double seconds;             /* cc_execute wall time (device events, first op -> last op)  */
+  double seconds;             /* cc_execute time: device events from entry (before any plan
+                                 preparation) to the last op; time to solution            */
   double kernel_seconds;      /* sum of contraction-kernel durations (0 unless profiled)    */
   double flops;               /* algorithmic flops: MM1 8LtN^3, BM1/BB2 8LtSN^4, TR 8LtN^2   */
   double hbm_bytes;           /* algorithmic HBM bytes of the kernels                       */

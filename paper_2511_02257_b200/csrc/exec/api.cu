@@ -143,6 +143,14 @@ struct cc_ctx {
   };
   std::vector<DfCopy> df_copies;
   std::vector<int32_t> df_issue;    // enqueue order of df_copies (sources before waiters)
+  std::vector<uint8_t> df_early;    // per plan op: H2D already enqueued during preparation
+  bool df_early_active = false;     // the next issue skips those copies and the sync zeroing
+  char* df_sync_base = nullptr;     // queue heads (16 B) + sync ints: top of the pool
+  char* df_meta_img = nullptr;      // pinned host image of the dataflow metadata (SM-driven upload)
+  size_t df_meta_img_bytes = 0;
+  cudaEvent_t ev_meta = nullptr;    // after the last metadata upload (the image is reused)
+  std::vector<std::vector<char>> upload_keep;   // host images of prepare_phys uploads
+  cudaEvent_t ev_pre = nullptr;
   std::vector<cudaEvent_t> df_events;  // per copy (index into df_copies), when some copy waits on it
   cudaStream_t cs2 = nullptr;       // second compute stream (trace worker)
   cudaEvent_t ev_cs2 = nullptr;
@@ -196,13 +204,16 @@ struct cc_ctx {
   void release_device() {
     if (host_only) return;
     release_phys();
-    for (cudaEvent_t* e : {&ev_start, &ev_end, &ev_h_end, &ev_d_end, &ev_copy_h, &ev_copy_d})
+    for (cudaEvent_t* e : {&ev_start, &ev_end, &ev_h_end, &ev_d_end, &ev_copy_h, &ev_copy_d, &ev_pre, &ev_meta})
       if (*e) {
         cudaEventDestroy(*e);
         *e = nullptr;
       }
     if (direct_ws) cudaFree(direct_ws);
     direct_ws = nullptr;
+    if (df_meta_img) cudaFreeHost(df_meta_img);
+    df_meta_img = nullptr;
+    df_meta_img_bytes = 0;
     if (cs2) cudaStreamDestroy(cs2);
     cs2 = nullptr;
     if (ev_cs2) cudaEventDestroy(ev_cs2);
@@ -382,8 +393,10 @@ void prepare_phys(cc_ctx* ctx) {
   ctx->term_coef = reinterpret_cast<double*>(s); s += sz_tc;
   ctx->df_chunk_ws = s; s += sz_df_chunk;
   ctx->df_trace_ws = s; s += sz_df_trace;
-  if (sz_df_chunk > 0) ck(cudaMemset(ctx->df_chunk_ws, 0, size_t(sz_df_chunk)), "dataflow workspace");
-  if (sz_df_trace > 0) ck(cudaMemset(ctx->df_trace_ws, 0, size_t(sz_df_trace)), "dataflow workspace");
+  // every upload / clear is ordered on the compute stream (the copy streams may already be
+  // busy; a legacy-stream cudaMemcpy from pageable memory can return before its DMA lands)
+  if (sz_df_chunk > 0) ck(cudaMemsetAsync(ctx->df_chunk_ws, 0, size_t(sz_df_chunk), ctx->cs), "dataflow workspace");
+  if (sz_df_trace > 0) ck(cudaMemsetAsync(ctx->df_trace_ws, 0, size_t(sz_df_trace), ctx->cs), "dataflow workspace");
   // term tables grouped by correlator slot (corr ids ascending), input order within a slot
   std::vector<int32_t> start(size_t(n_corr) + 1, 0), tree(size_t(std::max<int64_t>(n_terms, 1)), 0);
   std::vector<double> coef(size_t(std::max<int64_t>(n_terms, 1)) * 2, 0.0);
@@ -403,12 +416,22 @@ void prepare_phys(cc_ctx* ctx) {
       coef[2 * size_t(pos) + 1] = g.terms[size_t(k)].coef.imag();
     }
   }
-  ck(cudaMemcpy(ctx->term_start, start.data(), start.size() * 4, cudaMemcpyHostToDevice), "term tables");
-  ck(cudaMemcpy(ctx->term_tree, tree.data(), tree.size() * 4, cudaMemcpyHostToDevice), "term tables");
-  ck(cudaMemcpy(ctx->term_coef, coef.data(), coef.size() * 8, cudaMemcpyHostToDevice), "term tables");
-  ck(cudaMemset(ctx->trace_ws, 0, trace_ws), "trace counters");
-  if (sz_gemm > 0) ck(cudaMemset(ctx->gemm_ws, 0, size_t(sz_gemm)), "gemm flags");
-  ck(cudaMemset(ctx->roots, 0, size_t(sz_roots)), "roots");
+  ctx->upload_keep.clear();
+  auto upload = [&](void* dst, std::vector<char>&& img) {
+    ctx->upload_keep.push_back(std::move(img));   // host image alive until the next prepare
+    const auto& v = ctx->upload_keep.back();
+    ck(cudaMemcpyAsync(dst, v.data(), v.size(), cudaMemcpyHostToDevice, ctx->cs), "upload");
+  };
+  auto bytes_of = [](const auto& vec) {
+    const char* p = reinterpret_cast<const char*>(vec.data());
+    return std::vector<char>(p, p + vec.size() * sizeof(vec[0]));
+  };
+  upload(ctx->term_start, bytes_of(start));
+  upload(ctx->term_tree, bytes_of(tree));
+  upload(ctx->term_coef, bytes_of(coef));
+  ck(cudaMemsetAsync(ctx->trace_ws, 0, trace_ws, ctx->cs), "trace counters");
+  if (sz_gemm > 0) ck(cudaMemsetAsync(ctx->gemm_ws, 0, size_t(sz_gemm), ctx->cs), "gemm flags");
+  ck(cudaMemsetAsync(ctx->roots, 0, size_t(sz_roots), ctx->cs), "roots");
   pt.lap("scratch+tables");
   // physical plan over the pool
   std::vector<uint8_t> on_dev(g.nodes.size(), 0);
@@ -516,7 +539,44 @@ PFN_waitval df_write_fn() {
   return fn;
 }
 
-void prepare_dataflow(cc_ctx* ctx) {
+// Source / destination of a plan copy op.
+std::pair<const void*, void*> copy_endpoints(cc_ctx* ctx, const PhysOp& op) {
+  const Dag& g = *ctx->dag;
+  const Node& n = g.nodes[size_t(op.node)];
+  if (op.kind == OP_H2D) {
+    if (n.leaf()) {
+      const char* h = static_cast<const char*>(ctx->leaf_host[size_t(op.node)]);
+      if (!h) throw Error(CC_E_STATE, "leaf " + std::to_string(n.id) + " has no data (cc_set_leaf)");
+      const int64_t per_t_m = 16LL * g.N * g.N;
+      const int64_t per_t = n.op == CC_LEAF_M ? per_t_m : per_t_m * g.S * g.N;
+      return {h + int64_t(ctx->t0) * per_t, ctx->arena + op.dev_off};
+    }
+    return {ctx->host_pool + op.host_off, ctx->arena + op.dev_off};
+  }
+  return {ctx->arena + op.dev_off, ctx->host_pool + op.host_off};
+}
+
+// One plan copy on `s`: C time-slice chunks, each followed by a flag write (value = chunks
+// done) — the dataflow worker's items wait on the flag (chunk of their slice, kernels/dataflow.hpp).
+void enqueue_copy(cc_ctx* ctx, cudaStream_t s, const void* src, void* dst, size_t bytes, cudaMemcpyKind kind,
+                  int32_t chunks, int32_t flag_slot) {
+  const Dag& g = *ctx->dag;
+  const size_t per_t = bytes / size_t(std::max<int64_t>(g.Lt, 1));
+  for (int32_t ch = 0; ch < chunks; ++ch) {
+    // chunk ch: slices [ch*Lt/C, (ch+1)*Lt/C)
+    const size_t t0 = chunks == 1 ? 0 : size_t(int64_t(ch) * g.Lt / chunks);
+    const size_t t1 = chunks == 1 ? 0 : size_t(int64_t(ch + 1) * g.Lt / chunks);
+    const size_t off = t0 * per_t, len = chunks == 1 ? bytes : (t1 - t0) * per_t;
+    ck(cudaMemcpyAsync(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len, kind, s), "copy");
+    if (df_write_fn()(s, reinterpret_cast<CUdeviceptr>(ctx->df_sync + flag_slot), cuuint32_t(ch + 1), 0) != CUDA_SUCCESS)
+      throw Error(CC_E_CUDA, "cuStreamWriteValue32 failed");
+  }
+}
+
+// early: start the wait-free H2D copies at the head of the copy order on the H2D stream as
+// soon as that order is known, so they overlap the rest of the host-side preparation (queues,
+// tensor maps, upload); the next issue_dataflow only adds their flag writes.
+void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   if (ctx->df_valid) return;
   if (getenv("CC_DEBUG")) fprintf(stderr, "[cc] prepare_dataflow\n");
   prepare_phys(ctx);
@@ -550,18 +610,98 @@ void prepare_dataflow(cc_ctx* ctx) {
     d.erase(std::remove(d.begin(), d.end(), i), d.end());
   }
   tmr.lap("rw deps");
-  // 2. sync slots and work items
+  // 1b. copy issue order per stream (plan op indices).  A copy stream runs its copies in
+  // order.  Within a run of H2D copies that wait on nothing (fresh pool memory), the copies
+  // may be reordered without risking a deadlock (a wait-free copy blocks on nothing, so
+  // moving it earlier only completes it sooner for whoever needs it; the run's end — a copy
+  // that waits — keeps its place).  The run is ordered greedily by the work it enables: next
+  // = the copy that completes the input set (transitively, through compute ops) of the most
+  // estimated compute time, so the GEMMs — most of the step — can start early and the work
+  // left after the last copy lands is small.  CC_COPY_REORDER=0 keeps plan order.
+  std::vector<int32_t> copy_seq[3];
+  std::vector<int64_t> copy_pos(size_t(n_ops), 0);   // H2D issue position (0 for non-copies)
+  {
+    for (int32_t i = 0; i < n_ops; ++i)
+      if (ops[size_t(i)].stream == S_H2D || ops[size_t(i)].stream == S_D2H)
+        copy_seq[ops[size_t(i)].stream].push_back(i);
+    const int reorder = getenv("CC_COPY_REORDER") ? atoi(getenv("CC_COPY_REORDER")) : 1;
+    auto& h = copy_seq[S_H2D];
+    if (reorder && h.size() > 1) {
+      // weight of op i towards a missing input while m inputs are missing: mode 1 counts
+      // only ops completed by the copy (m == 1); mode 2 spreads cost / m^2 over the missing
+      // inputs, so a copy also earns credit for bringing trees (root traces need four
+      // leaves) closer to completion
+      auto w = [&](int32_t m) { return m <= 0 ? 0.0 : (reorder == 1 ? (m == 1 ? 1.0 : 0.0) : 1.0 / (double(m) * m)); };
+      // leaf-copy inputs of every compute op (transitively), and its estimated time
+      std::vector<std::vector<int32_t>> need(static_cast<size_t>(n_ops));
+      std::vector<double> cost(size_t(n_ops), 0.0);
+      const double tr_weight = getenv("CC_COPY_TR_WEIGHT") ? atof(getenv("CC_COPY_TR_WEIGHT")) : 1.0;
+      for (int32_t i = 0; i < n_ops; ++i) {
+        const PhysOp& op = ops[size_t(i)];
+        if (op.kind != OP_CONTRACT) continue;
+        const Node& n = g.nodes[size_t(op.node)];
+        cost[size_t(i)] = node_flops(n, g.Lt, g.N, g.S) / 37e12 + node_hbm_bytes(n, g.Lt, g.N, g.S) / 6.5e12;
+        if (n.op == CC_TR_MM) cost[size_t(i)] *= tr_weight;
+        auto& v = need[size_t(i)];
+        for (int32_t j : deps[size_t(i)]) {
+          const PhysOp& oj = ops[size_t(j)];
+          if (oj.stream == S_H2D) v.push_back(j);
+          else if (oj.kind == OP_CONTRACT) v.insert(v.end(), need[size_t(j)].begin(), need[size_t(j)].end());
+        }
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+      }
+      std::vector<std::vector<int32_t>> users(static_cast<size_t>(n_ops));
+      for (int32_t i = 0; i < n_ops; ++i)
+        for (int32_t j : need[size_t(i)]) users[size_t(j)].push_back(i);
+      std::vector<int32_t> missing(size_t(n_ops), 0);
+      for (int32_t i = 0; i < n_ops; ++i) missing[size_t(i)] = int32_t(need[size_t(i)].size());
+      std::vector<uint8_t> loaded(size_t(n_ops), 0);
+      auto wait_free = [&](int32_t i) { return deps[size_t(i)].empty(); };
+      // copies issued before a run count as loaded when the run is ordered
+      size_t a = 0;
+      while (a < h.size()) {
+        size_t b = a;
+        while (b < h.size() && wait_free(h[b])) ++b;
+        // greedy over h[a, b): score(c) = time of ops whose only missing input is c
+        std::vector<int32_t> run(h.begin() + int64_t(a), h.begin() + int64_t(b)), out;
+        std::vector<double> score(size_t(n_ops), 0.0);
+        std::vector<uint8_t> in_run(size_t(n_ops), 0);
+        for (int32_t c : run) in_run[size_t(c)] = 1;
+        for (int32_t c : run)
+          for (int32_t i : users[size_t(c)]) score[size_t(c)] += cost[size_t(i)] * w(missing[size_t(i)]);
+        std::vector<uint8_t> taken(run.size(), 0);
+        for (size_t step = 0; step < run.size(); ++step) {
+          size_t best = run.size();
+          for (size_t q = 0; q < run.size(); ++q)
+            if (!taken[q] && (best == run.size() || score[size_t(run[q])] > score[size_t(run[best])])) best = q;
+          taken[best] = 1;
+          const int32_t c = run[best];
+          out.push_back(c);
+          loaded[size_t(c)] = 1;
+          for (int32_t i : users[size_t(c)]) {
+            const int32_t m = missing[size_t(i)]--;
+            const double d = cost[size_t(i)] * (w(m - 1) - w(m));
+            if (d != 0.0)
+              for (int32_t j : need[size_t(i)])
+                if (!loaded[size_t(j)] && in_run[size_t(j)]) score[size_t(j)] += d;
+          }
+        }
+        std::copy(out.begin(), out.end(), h.begin() + int64_t(a));
+        // the run's closing copy (waits on something) keeps its place
+        if (b < h.size()) {
+          const int32_t c = h[b];
+          loaded[size_t(c)] = 1;
+          for (int32_t i : users[size_t(c)]) --missing[size_t(i)];
+        }
+        a = b + 1;
+      }
+    }
+    for (size_t k = 0; k < h.size(); ++k) copy_pos[size_t(h[k])] = int64_t(k) + 1;
+  }
+  // sync slots (done counters of compute ops, flags of copies) and H2D chunk counts
   std::vector<int32_t> slot(size_t(n_ops), -1), target(size_t(n_ops), 0), df_index(size_t(n_ops), -1);
   int32_t n_sync = 0;
-  std::vector<DfOp> gops, tops;
-  std::vector<int32_t> gplan, tplan;   // plan op index of each DfOp (queue order)
-  std::vector<uint8_t> tmaps;
-  int64_t g_items = 0, t_items = 0;
-  int64_t n_chunked = 0, n_traced = 0;
-  std::vector<int32_t> chunk_ring_user(size_t(DF_CHUNK_RING), -1), trace_ring_user(size_t(DF_TRACE_RING), -1);
-  std::vector<std::vector<int32_t>> ring_deps(static_cast<size_t>(n_ops));
-  int BM, BN, BK, slot_doubles;
-  df_gemm_tile_dims(&BM, &BN, &BK, &slot_doubles);
   // CC_H2D_CHUNK_MB: H2D copies in time-slice chunks of about that size (default off: every
   // chunk costs a stream memory operation, measured ~8 us of copy-engine idle each on B200)
   const double chunk_mb = getenv("CC_H2D_CHUNK_MB") ? atof(getenv("CC_H2D_CHUNK_MB")) : 0.0;
@@ -571,15 +711,59 @@ void prepare_dataflow(cc_ctx* ctx) {
     if (op.stream == S_NONE) continue;
     slot[size_t(i)] = n_sync++;
     if (op.kind != OP_CONTRACT) {
-      // H2D copies go in time-slice chunks of ~h2d_chunk bytes; consumers of a chunked copy
-      // wait only for the chunk holding their slice (target -C: C chunks over Lt slices)
+      // consumers of a copy in C > 1 time-slice chunks wait only for the chunk holding their
+      // slice (target -C); else the flag reaches 1
       target[size_t(i)] = 1;
       if (op.kind == OP_H2D && op.stream == S_H2D && Lt > 1 && op.bytes % Lt == 0) {
         const int64_t C = std::min<int64_t>(Lt, std::max<int64_t>(1, op.bytes / h2d_chunk + (op.bytes % h2d_chunk != 0)));
         if (C > 1) target[size_t(i)] = -int32_t(C);
       }
-      continue;
     }
+  }
+  // The sync area (2 queue heads + n_sync ints), zeroed before every launch, sits at the top
+  // of the pool (above the plan's high-water mark); the rest of the metadata goes below it.
+  const size_t sz_sync = round_up(16 + int64_t(n_sync) * 4, 256);
+  {
+    const int64_t sync_off = (ctx->pool_bytes - int64_t(sz_sync)) / 256 * 256;
+    if (sync_off < ctx->pp.pool_high_water) throw Error(CC_E_NOMEM, "arena too small for the dataflow sync area");
+    ctx->df_sync_base = ctx->arena + sync_off;
+    ctx->df_sync = reinterpret_cast<int*>(ctx->df_sync_base + 16);
+    ctx->df_sync_bytes = sz_sync;
+  }
+  // early copies: zero the sync area on the H2D stream, then start the wait-free H2D copies at
+  // the head of the copy order, each followed by its flag write, so they overlap the rest of
+  // the host-side preparation; the compute stream waits for the zeroing only.
+  ctx->df_early.assign(size_t(n_ops), 0);
+  ctx->df_early_active = false;
+  if (early && !copy_seq[S_H2D].empty() && deps[size_t(copy_seq[S_H2D][0])].empty()) {
+    ck(cudaEventRecord(ctx->ev_pre, ctx->cs), "event");        // after all earlier work on cs
+    ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_pre, 0), "wait");
+    ck(cudaMemsetAsync(ctx->df_sync_base, 0, sz_sync, ctx->hs), "memset");
+    ck(cudaEventRecord(ctx->ev_pre, ctx->hs), "event");
+    ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_pre, 0), "wait");
+    for (int32_t i : copy_seq[S_H2D]) {
+      if (!deps[size_t(i)].empty()) break;
+      const PhysOp& op = ops[size_t(i)];
+      const auto ep = copy_endpoints(ctx, op);
+      enqueue_copy(ctx, ctx->hs, ep.first, ep.second, size_t(op.bytes), cudaMemcpyHostToDevice,
+                   target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
+      ctx->df_early[size_t(i)] = 1;
+    }
+    ctx->df_early_active = true;
+  }
+  // 2. work items
+  std::vector<DfOp> gops, tops;
+  std::vector<int32_t> gplan, tplan;   // plan op index of each DfOp (queue order)
+  std::vector<uint8_t> tmaps;
+  int64_t g_items = 0, t_items = 0;
+  int64_t n_chunked = 0, n_traced = 0;
+  std::vector<int32_t> chunk_ring_user(size_t(DF_CHUNK_RING), -1), trace_ring_user(size_t(DF_TRACE_RING), -1);
+  std::vector<std::vector<int32_t>> ring_deps(static_cast<size_t>(n_ops));
+  int BM, BN, BK, slot_doubles;
+  df_gemm_tile_dims(&BM, &BN, &BK, &slot_doubles);
+  for (int32_t i = 0; i < n_ops; ++i) {
+    const PhysOp& op = ops[size_t(i)];
+    if (op.stream == S_NONE || op.kind != OP_CONTRACT) continue;
     const Node& n = g.nodes[size_t(op.node)];
     const void* a = op.loc_a == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.l)] : ctx->arena + op.off_a;
     const void* b = op.loc_b == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.r)] : ctx->arena + op.off_b;
@@ -597,13 +781,7 @@ void prepare_dataflow(cc_ctx* ctx) {
       d.Lt = Lt;
       d.nb = int32_t((N + 31) / 32);
       d.P = int32_t(P);
-      const int64_t r = n_traced % DF_TRACE_RING;
-      char* base = ctx->df_trace_ws + r * ctx->df_trace_slot;
-      d.tr_cnt = reinterpret_cast<int*>(base);
-      d.tr_part = base + round_up(Lt * 4, ALIGN);
-      if (trace_ring_user[size_t(r)] >= 0) ring_deps[size_t(i)].push_back(trace_ring_user[size_t(r)]);
-      trace_ring_user[size_t(r)] = i;
-      ++n_traced;
+      // partial slots (P > 1) come from a ring assigned in queue order below
       d.tmap = int32_t(tmaps.size() / 256);
       tmaps.resize(tmaps.size() + 256);
       if (!df_encode_trace_maps(tmaps.data() + size_t(d.tmap) * 256, a, b, Lt, N))
@@ -630,15 +808,7 @@ void prepare_dataflow(cc_ctx* ctx) {
       d.ldc = p.ldc;
       d.sCb = p.sCb;
       d.C = out;
-      if (chunks > 1) {
-        const int64_t r = n_chunked % DF_CHUNK_RING;
-        char* base = ctx->df_chunk_ws + r * (ctx->df_chunk_slot + ctx->df_chunk_cnt_slot);
-        d.part = base;
-        d.tile_cnt = reinterpret_cast<int*>(base + ctx->df_chunk_slot);
-        if (chunk_ring_user[size_t(r)] >= 0) ring_deps[size_t(i)].push_back(chunk_ring_user[size_t(r)]);
-        chunk_ring_user[size_t(r)] = i;
-        ++n_chunked;
-      }
+      // chunk-partial slots (chunks > 1) come from a ring assigned in queue order below
       d.tmap = int32_t(tmaps.size() / 256);
       tmaps.resize(tmaps.size() + 256);
       if (!df_encode_maps(tmaps.data() + size_t(d.tmap) * 256, p.A, p.B, p.M, p.Nn, p.Kin, p.Ko, p.batch, p.lda,
@@ -662,7 +832,11 @@ void prepare_dataflow(cc_ctx* ctx) {
     static const int64_t delay = getenv("CC_DF_TR_DELAY") ? atoll(getenv("CC_DF_TR_DELAY")) : 8;
     std::vector<std::vector<int32_t>> succ(static_cast<size_t>(n_ops));
     std::vector<int32_t> indeg(static_cast<size_t>(n_ops), 0), rank(static_cast<size_t>(n_ops), 0);
-    int32_t last_copy[3] = {-1, -1, -1};
+    std::vector<int32_t> chain_prev(size_t(n_ops), -1);   // previous copy on the same stream (issue order)
+    for (int st : {int(S_H2D), int(S_D2H)})
+      for (size_t k = 1; k < copy_seq[st].size(); ++k) chain_prev[size_t(copy_seq[st][k])] = copy_seq[st][k - 1];
+    // avail: the H2D issue position after which an op's inputs can all be there
+    std::vector<int64_t> avail(size_t(n_ops), 0);
     int32_t r = 0;
     for (int32_t i = 0; i < n_ops; ++i) {
       if (slot[size_t(i)] < 0) continue;
@@ -670,11 +844,8 @@ void prepare_dataflow(cc_ctx* ctx) {
       if (ops[size_t(i)].kind == OP_CONTRACT) ++r;
       std::vector<int32_t> pre = deps[size_t(i)];
       pre.insert(pre.end(), ring_deps[size_t(i)].begin(), ring_deps[size_t(i)].end());
-      if (ops[size_t(i)].kind != OP_CONTRACT) {
-        int32_t& lc = last_copy[ops[size_t(i)].stream];
-        if (lc >= 0) pre.push_back(lc);
-        lc = i;
-      }
+      if (ops[size_t(i)].kind != OP_CONTRACT && chain_prev[size_t(i)] >= 0) pre.push_back(chain_prev[size_t(i)]);
+      for (int32_t j : pre) avail[size_t(i)] = std::max(avail[size_t(i)], std::max(avail[size_t(j)], copy_pos[size_t(j)]));
       std::sort(pre.begin(), pre.end());
       pre.erase(std::unique(pre.begin(), pre.end()), pre.end());
       for (int32_t j : pre)
@@ -683,10 +854,11 @@ void prepare_dataflow(cc_ctx* ctx) {
           ++indeg[size_t(i)];
         }
     }
+    // priority: inputs' availability first (copy issue order), then plan rank (+ the TR delay)
     auto key = [&](int32_t i) {
       const PhysOp& op = ops[size_t(i)];
       const bool tr = op.kind == OP_CONTRACT && g.nodes[size_t(op.node)].op == CC_TR_MM;
-      return int64_t(rank[size_t(i)]) + (tr ? delay : 0);
+      return avail[size_t(i)] * (int64_t(n_ops) + delay + 1) + int64_t(rank[size_t(i)]) + (tr ? delay : 0);
     };
     std::priority_queue<std::pair<int64_t, int32_t>, std::vector<std::pair<int64_t, int32_t>>, std::greater<>> ready;
     for (int32_t i = 0; i < n_ops; ++i)
@@ -726,6 +898,27 @@ void prepare_dataflow(cc_ctx* ctx) {
     tplan.swap(tplan_v);
     g_items = first;
     t_items = tfirst;
+    // Workspace rings (chunk partials of k-split GEMM ops, slice partials of TR ops split in
+    // P > 1 pieces), assigned in queue order: the op taking a slot depends on the slot's
+    // previous user, which is earlier in the same queue — the queue order stays topological.
+    for (size_t k = 0; k < gops.size(); ++k) {
+      if (gops[k].n_chunks <= 1) continue;
+      const int64_t r = n_chunked++ % DF_CHUNK_RING;
+      char* base = ctx->df_chunk_ws + r * (ctx->df_chunk_slot + ctx->df_chunk_cnt_slot);
+      gops[k].part = base;
+      gops[k].tile_cnt = reinterpret_cast<int*>(base + ctx->df_chunk_slot);
+      if (chunk_ring_user[size_t(r)] >= 0) ring_deps[size_t(gplan[k])].push_back(chunk_ring_user[size_t(r)]);
+      chunk_ring_user[size_t(r)] = gplan[k];
+    }
+    for (size_t k = 0; k < tops.size(); ++k) {
+      if (tops[k].P <= 1) continue;
+      const int64_t r = n_traced++ % DF_TRACE_RING;
+      char* base = ctx->df_trace_ws + r * ctx->df_trace_slot;
+      tops[k].tr_cnt = reinterpret_cast<int*>(base);
+      tops[k].tr_part = base + round_up(Lt * 4, ALIGN);
+      if (trace_ring_user[size_t(r)] >= 0) ring_deps[size_t(tplan[k])].push_back(trace_ring_user[size_t(r)]);
+      trace_ring_user[size_t(r)] = tplan[k];
+    }
   }
   tmr.lap("queue order");
   // 4. dependency lists of compute ops, wait lists of copies
@@ -759,19 +952,10 @@ void prepare_dataflow(cc_ctx* ctx) {
     c.stream = op.stream;
     c.bytes = size_t(op.bytes);
     c.flag_slot = slot[size_t(i)];
-    if (op.kind == OP_H2D) {
-      c.dst = ctx->arena + op.dev_off;
-      if (n.leaf()) {
-        const char* h = static_cast<const char*>(ctx->leaf_host[size_t(op.node)]);
-        if (!h) throw Error(CC_E_STATE, "leaf " + std::to_string(n.id) + " has no data (cc_set_leaf)");
-        const int64_t per_t = n.op == CC_LEAF_M ? per_t_m : per_t_m * g.S * g.N;
-        c.src = h + int64_t(ctx->t0) * per_t;
-      } else {
-        c.src = ctx->host_pool + op.host_off;
-      }
-    } else {
-      c.dst = ctx->host_pool + op.host_off;
-      c.src = ctx->arena + op.dev_off;
+    {
+      const auto ep = copy_endpoints(ctx, op);
+      c.src = ep.first;
+      c.dst = ep.second;
     }
     for (int32_t j : deps[size_t(i)]) {
       const PhysOp& oj = ops[size_t(j)];
@@ -787,44 +971,10 @@ void prepare_dataflow(cc_ctx* ctx) {
     ctx->df_copies.push_back(std::move(c));
   }
   {
-    // Copy enqueue order.  A copy stream runs its copies in order; an H2D copy that waits on
-    // nothing (fresh pool memory) may move earlier among the wait-free copies of its run
-    // (runs are delimited by copies that wait) without risking a deadlock: it blocks on
-    // nothing and only completes sooner for whoever needs it.  Wait-free H2D copies are
-    // ordered by the merged-queue position of their first GEMM consumer (TR-only consumers
-    // after every GEMM one), so the GEMM work — most of the step — can start early and the
-    // copies feed it in the order the queue wants them.
     const size_t nc = ctx->df_copies.size();
-    std::vector<int64_t> key(nc, INT64_MAX);
-    std::vector<std::vector<int32_t>> consumers(static_cast<size_t>(n_ops));
-    for (int32_t i = 0; i < n_ops; ++i)
-      if (ops[size_t(i)].kind == OP_CONTRACT)
-        for (int32_t j : deps[size_t(i)]) consumers[size_t(j)].push_back(i);
-    for (size_t k = 0; k < nc; ++k) {
-      const auto& c = ctx->df_copies[k];
-      for (int32_t i : consumers[size_t(c.op)]) {
-        const bool tr = g.nodes[size_t(ops[size_t(i)].node)].op == CC_TR_MM;
-        key[k] = std::min(key[k], qpos[size_t(i)] + (tr ? int64_t(n_ops) : 0));
-      }
-    }
     std::vector<int32_t> seq[3];
-    for (size_t k = 0; k < nc; ++k) seq[ctx->df_copies[k].stream].push_back(int32_t(k));
-    const bool reorder = getenv("CC_COPY_REORDER") ? atoi(getenv("CC_COPY_REORDER")) != 0 : true;
-    if (reorder) {
-      auto& h = seq[S_H2D];
-      size_t a = 0;
-      while (a < h.size()) {
-        size_t b = a;
-        auto free_of_waits = [&](int32_t k) {
-          const auto& c = ctx->df_copies[size_t(k)];
-          return c.wait_values.empty() && c.wait_events.empty();
-        };
-        while (b < h.size() && free_of_waits(h[b])) ++b;
-        std::stable_sort(h.begin() + int64_t(a), h.begin() + int64_t(b),
-                         [&](int32_t x, int32_t y) { return key[size_t(x)] < key[size_t(y)]; });
-        a = b + 1;
-      }
-    }
+    for (int st : {int(S_H2D), int(S_D2H)})
+      for (int32_t i : copy_seq[st]) seq[st].push_back(copy_index[size_t(i)]);
     // merge the two streams' sequences so every event source is enqueued before its waiters
     std::vector<uint8_t> done(nc, 0);
     size_t p[3] = {0, 0, 0};
@@ -851,7 +1001,6 @@ void prepare_dataflow(cc_ctx* ctx) {
     if (ctx->df_copies[k].source) ck(cudaEventCreateWithFlags(&ctx->df_events[k], cudaEventDisableTiming), "event");
   tmr.lap("deps+copies+events");
   // 5. upload metadata: [heads | sync][gops][tops][dep_slot][dep_target][tmaps]
-  const size_t sz_sync = round_up(16 + int64_t(n_sync) * 4, 256);
   const size_t sz_g = round_up(int64_t(std::max<size_t>(gops.size(), 1) * sizeof(DfOp)), 256);
   const size_t sz_t = round_up(int64_t(std::max<size_t>(tops.size(), 1) * sizeof(DfOp)), 256);
   const size_t sz_d = round_up(int64_t(std::max<size_t>(dep_slot.size(), 1) * 4), 256);
@@ -862,10 +1011,10 @@ void prepare_dataflow(cc_ctx* ctx) {
   for (size_t k = 0; k < tops.size(); ++k)
     std::fill(titem_op.begin() + tops[k].first_item, titem_op.begin() + tops[k].first_item + tops[k].n_items, int32_t(k));
   const size_t sz_gi = round_up(int64_t(gitem_op.size() * 4), 256), sz_ti = round_up(int64_t(titem_op.size() * 4), 256);
-  const size_t total = sz_sync + sz_g + sz_t + 2 * sz_d + sz_m + sz_gi + sz_ti;
+  const size_t total = sz_g + sz_t + 2 * sz_d + sz_m + sz_gi + sz_ti;
   // device region: the top of the pool when the plan's high water leaves room (no allocation
   // on the execute path), else a cudaMalloc
-  const int64_t meta_off = (ctx->pool_bytes - int64_t(total)) / 256 * 256;
+  const int64_t meta_off = (int64_t(ctx->df_sync_base - ctx->arena) - int64_t(total)) / 256 * 256;
   if (meta_off >= ctx->pp.pool_high_water) {
     ctx->df_meta = ctx->arena + meta_off;
     ctx->df_meta_owned = false;
@@ -875,10 +1024,8 @@ void prepare_dataflow(cc_ctx* ctx) {
   }
   ctx->df_meta_bytes = total;
   char* m = ctx->df_meta;
-  unsigned long long* heads = reinterpret_cast<unsigned long long*>(m);
-  ctx->df_sync = reinterpret_cast<int*>(m + 16);
-  ctx->df_sync_bytes = sz_sync;
-  char* pg = m + sz_sync;
+  unsigned long long* heads = reinterpret_cast<unsigned long long*>(ctx->df_sync_base);
+  char* pg = m;
   char* pt = pg + sz_g;
   char* pds = pt + sz_t;
   char* pdt = pds + sz_d;
@@ -886,8 +1033,21 @@ void prepare_dataflow(cc_ctx* ctx) {
   char* pgi = pm + sz_m;
   char* pti = pgi + sz_gi;
   {
-    // one host image, one copy
-    std::vector<char> img(total, 0);
+    // one host image, one copy, ordered on the compute stream before the worker launch
+    if (ctx->df_meta_img_bytes < total) {
+      if (ctx->df_meta_img) cudaFreeHost(ctx->df_meta_img);
+      ctx->df_meta_img = nullptr;
+      ctx->df_meta_img_bytes = 0;
+      ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->df_meta_img), total, cudaHostAllocDefault), "metadata staging");
+      ctx->df_meta_img_bytes = total;
+    } else {
+      ck(cudaEventSynchronize(ctx->ev_meta), "metadata staging");   // the previous upload has read it
+    }
+    struct Img {
+      char* p;
+      char* data() { return p; }
+    } img{ctx->df_meta_img};
+    std::memset(img.data(), 0, total);
     auto put = [&](char* dst, const void* src, size_t n) {
       if (n) std::memcpy(img.data() + (dst - m), src, n);
     };
@@ -898,7 +1058,9 @@ void prepare_dataflow(cc_ctx* ctx) {
     put(pds, dep_slot.data(), dep_slot.size() * 4);
     put(pdt, dep_target.data(), dep_target.size() * 4);
     put(pm, tmaps.data(), tmaps.size());
-    ck(cudaMemcpy(m, img.data(), total, cudaMemcpyHostToDevice), "dataflow metadata upload");
+    // SM-driven upload on the compute stream: the copy engines may be busy with early leaf copies
+    ck(launch_upload(m, img.data(), total, ctx->num_sms, ctx->cs), "dataflow metadata upload");
+    ck(cudaEventRecord(ctx->ev_meta, ctx->cs), "event");
   }
   DfArgs& da = ctx->df_gemm;
   da.dep_slot = reinterpret_cast<const int32_t*>(pds);
@@ -940,7 +1102,7 @@ int issue_dataflow(cc_ctx* ctx, bool time_copies = false) {
   PhaseTimer tmr("issue_dataflow");
   DBG("issue_dataflow: %zu copies, %lld gemm items, %lld trace items", ctx->df_copies.size(),
       (long long)ctx->df_gemm_items, (long long)ctx->df_trace_items);
-  ck(cudaMemsetAsync(ctx->df_meta, 0, ctx->df_sync_bytes, ctx->cs), "memset");
+  if (!ctx->df_early_active) ck(cudaMemsetAsync(ctx->df_sync_base, 0, ctx->df_sync_bytes, ctx->cs), "memset");
   ck(cudaEventRecord(ctx->ev_start, ctx->cs), "event");
   ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_start, 0), "wait");
   ck(cudaStreamWaitEvent(ctx->ds, ctx->ev_start, 0), "wait");
@@ -956,22 +1118,15 @@ int issue_dataflow(cc_ctx* ctx, bool time_copies = false) {
                        CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
         throw Error(CC_E_CUDA, "cuStreamWaitValue32 failed");
     DBG("copy %zu: stream %d bytes %zu waits %zu/%zu", k, c.stream, c.bytes, c.wait_values.size(), c.wait_events.size());
-    const cudaMemcpyKind kind = c.stream == S_H2D ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
-    const size_t per_t = c.bytes / size_t(std::max<int64_t>(g.Lt, 1));
-    for (int32_t ch = 0; ch < c.chunks; ++ch) {
-      // chunk ch: slices [ch*Lt/C, (ch+1)*Lt/C); flag = chunks finished
-      const size_t t0 = c.chunks == 1 ? 0 : size_t(int64_t(ch) * g.Lt / c.chunks);
-      const size_t t1 = c.chunks == 1 ? 0 : size_t(int64_t(ch + 1) * g.Lt / c.chunks);
-      const size_t off = t0 * per_t, len = c.chunks == 1 ? c.bytes : (t1 - t0) * per_t;
-      ck(cudaMemcpyAsync(static_cast<char*>(c.dst) + off, static_cast<const char*>(c.src) + off, len, kind, s), "copy");
-      if (df_write_fn()(s, reinterpret_cast<CUdeviceptr>(ctx->df_sync + c.flag_slot), cuuint32_t(ch + 1), 0) !=
-          CUDA_SUCCESS)
-        throw Error(CC_E_CUDA, "cuStreamWriteValue32 failed");
-    }
+    // copies started during preparation (flags included) are skipped
+    if (!(ctx->df_early_active && ctx->df_early[size_t(c.op)]))
+      enqueue_copy(ctx, s, c.src, c.dst, c.bytes, c.stream == S_H2D ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                   c.chunks, c.flag_slot);
     DBG("copy %zu enqueued", k);
     if (c.source) ck(cudaEventRecord(ctx->df_events[k], s), "event");
   }
   DBG("copies enqueued");
+  ctx->df_early_active = false;   // later replays copy everything and zero the sync area on cs
   if (time_copies) {
     ck(cudaEventRecord(ctx->ev_copy_h, ctx->hs), "event");
     ck(cudaEventRecord(ctx->ev_copy_d, ctx->ds), "event");
@@ -1156,13 +1311,17 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   const bool time_kernels = (flags & 2) != 0 && !use_graph;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;
   std::vector<int> kev_kind;
+  cudaEvent_t t_begin, t_end;
+  ck(cudaEventCreate(&t_begin), "event");
+  ck(cudaEventCreate(&t_end), "event");
+  ck(cudaEventRecord(t_begin, ctx->cs), "event");   // before any preparation: seconds = time to solution
   if (!legacy) {
-    prepare_dataflow(ctx);
+    prepare_dataflow(ctx, getenv("CC_EARLY_COPIES") ? atoi(getenv("CC_EARLY_COPIES")) != 0 : true);
     const bool prof = (flags & 32) != 0;
     if (prof && !ctx->df_prof) {
       const int64_t n = ctx->df_gemm_items + ctx->df_trace_items + ctx->num_sms;
       ck(cudaMalloc(reinterpret_cast<void**>(&ctx->df_prof), size_t(n) * 64), "profile buffer");
-      ck(cudaMemset(ctx->df_prof, 0, size_t(n) * 64), "profile buffer");
+      ck(cudaMemsetAsync(ctx->df_prof, 0, size_t(n) * 64, ctx->cs), "profile buffer");
     }
     ctx->df_gemm.prof = prof ? ctx->df_prof : nullptr;
     ctx->df_gemm.prof_t = prof ? ctx->df_prof + 8 * ctx->df_gemm_items : nullptr;
@@ -1172,10 +1331,6 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
       ctx->gexec_df = nullptr;
     }
   }
-  cudaEvent_t t_begin, t_end;
-  ck(cudaEventCreate(&t_begin), "event");
-  ck(cudaEventCreate(&t_end), "event");
-  ck(cudaEventRecord(t_begin, ctx->cs), "event");
   if (!legacy) {
     if (use_graph && ctx->df_copies.empty()) {
       if (!ctx->gexec_df) {
@@ -1267,6 +1422,7 @@ void ensure_ws(char*& ws, size_t& have, size_t bytes) {
   have = 0;
   ck(cudaMalloc(reinterpret_cast<void**>(&ws), bytes), "workspace");
   ck(cudaMemset(ws, 0, bytes), "workspace");  // trace counters must start at zero
+  ck(cudaDeviceSynchronize(), "workspace");   // (legacy-stream memset; kernels run on other streams)
   have = bytes;
 }
 
@@ -1312,7 +1468,7 @@ cc_status cc_create(cc_ctx** out, int device, void* dev_arena, size_t arena_byte
       ck(cudaStreamCreateWithFlags(&ctx->hs, cudaStreamNonBlocking), "stream");
       ck(cudaStreamCreateWithFlags(&ctx->ds, cudaStreamNonBlocking), "stream");
     }
-    for (cudaEvent_t* e : {&ctx->ev_start, &ctx->ev_end, &ctx->ev_h_end, &ctx->ev_d_end})
+    for (cudaEvent_t* e : {&ctx->ev_start, &ctx->ev_end, &ctx->ev_h_end, &ctx->ev_d_end, &ctx->ev_pre, &ctx->ev_meta})
       ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
     for (cudaEvent_t* e : {&ctx->ev_copy_h, &ctx->ev_copy_d}) ck(cudaEventCreate(e), "event");
     ck(zgemm_preload(), "kernel load");
@@ -1595,7 +1751,8 @@ cc_status cc_correlator(cc_ctx* ctx, int64_t corr_id, double* out, int32_t Lt) {
   if (it == g.corr_ids.end() || *it != corr_id) throw Error(CC_E_UNKNOWN_NODE, "unknown correlator " + std::to_string(corr_id));
   const int64_t slot = it - g.corr_ids.begin();
   ck(cudaStreamSynchronize(ctx->cs), "sync");
-  ck(cudaMemcpy(out, ctx->corr + slot * g.Lt, size_t(g.Lt) * 16, cudaMemcpyDeviceToHost), "correlator D2H");
+  ck(cudaMemcpyAsync(out, ctx->corr + slot * g.Lt, size_t(g.Lt) * 16, cudaMemcpyDeviceToHost, ctx->cs), "correlator D2H");
+  ck(cudaStreamSynchronize(ctx->cs), "correlator D2H");
   API_END
 }
 
@@ -1611,7 +1768,8 @@ cc_status cc_root_value(cc_ctx* ctx, int64_t tree_id, double* out, int32_t Lt) {
     if (g.trees[t].tree_id == tree_id) slot = int64_t(t);
   if (slot < 0) throw Error(CC_E_UNKNOWN_NODE, "unknown tree " + std::to_string(tree_id));
   ck(cudaStreamSynchronize(ctx->cs), "sync");
-  ck(cudaMemcpy(out, ctx->roots + slot * g.Lt, size_t(g.Lt) * 16, cudaMemcpyDeviceToHost), "root D2H");
+  ck(cudaMemcpyAsync(out, ctx->roots + slot * g.Lt, size_t(g.Lt) * 16, cudaMemcpyDeviceToHost, ctx->cs), "root D2H");
+  ck(cudaStreamSynchronize(ctx->cs), "root D2H");
   API_END
 }
 
@@ -1636,7 +1794,7 @@ cc_status cc_dataflow_state(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_o
   std::vector<char> buf(ctx->df_sync_bytes);
   cudaStream_t s;
   ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-  ck(cudaMemcpyAsync(buf.data(), ctx->df_meta, buf.size(), cudaMemcpyDeviceToHost, s), "state copy");
+  ck(cudaMemcpyAsync(buf.data(), ctx->df_sync_base, buf.size(), cudaMemcpyDeviceToHost, s), "state copy");
   ck(cudaStreamSynchronize(s), "state copy");
   cudaStreamDestroy(s);
   const int64_t n = 2 + int64_t(n_int);

@@ -45,6 +45,9 @@ cudaError_t launch_correlate(const void* roots, void* corr, int64_t n_corr, int6
 // Force-load the kernels of each translation unit (CUDA lazy loading would otherwise load a
 // kernel at its first launch, which can wait for an idle device — a deadlock while copy
 // streams wait on a persistent worker).  Also sets their shared-memory attributes.
+// Copy bytes (multiple of 16, 16-byte aligned) from pinned host memory to device memory
+// with SM loads over PCIe, ordered on `stream` (not behind pending copy-engine transfers).
+cudaError_t launch_upload(void* dst, const void* src_pinned, size_t bytes, int num_sms, cudaStream_t stream);
 cudaError_t zgemm_preload();
 cudaError_t trace_preload();
 

@@ -191,11 +191,14 @@ __global__ void fill_synthetic_kernel(double2* out, int64_t n, uint64_t key, int
 
 }  // namespace
 
+__global__ void upload_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16);
+
 cudaError_t trace_preload() {
   cudaFuncAttributes attr;
   cudaError_t e = cudaFuncGetAttributes(&attr, trace_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&attr, correlate_kernel);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&attr, fill_synthetic_kernel);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&attr, upload_kernel);
   return e;
 }
 
@@ -223,6 +226,23 @@ cudaError_t launch_correlate(const void* roots, void* corr, int64_t n_corr, int6
   const int threads = Lt >= 256 ? 256 : int((Lt + 31) / 32 * 32);
   correlate_kernel<<<unsigned(n_corr), threads, 0, stream>>>(static_cast<const double2*>(roots), static_cast<double2*>(corr), n_corr,
                                                Lt, term_start, term_tree, term_coef);
+  return cudaGetLastError();
+}
+
+// SM-driven upload from pinned host memory (UVA) to device memory: a stream-ordered copy
+// that does not queue behind the copy engines' pending transfers (the leaf H2D copies).
+__global__ void upload_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+cudaError_t launch_upload(void* dst, const void* src_pinned, size_t bytes, int num_sms, cudaStream_t stream) {
+  if (bytes == 0) return cudaSuccess;
+  if ((bytes & 15) || (reinterpret_cast<uintptr_t>(dst) & 15) || (reinterpret_cast<uintptr_t>(src_pinned) & 15))
+    return cudaErrorInvalidValue;
+  const int64_t n16 = int64_t(bytes / 16);
+  const int64_t blocks = std::min<int64_t>(int64_t(num_sms) * 4, (n16 + 255) / 256);
+  upload_kernel<<<unsigned(blocks), 256, 0, stream>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src_pinned), n16);
   return cudaGetLastError();
 }
 

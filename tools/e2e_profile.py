@@ -45,6 +45,13 @@ t2 = time.perf_counter()
 print("load+schedule %.2f ms; first execute %.2f ms wall (%.2f ms device); h2d %.1f MB"
       % ((t1 - t0) * 1e3, (t2 - t1) * 1e3, st["seconds"] * 1e3, st["h2d_bytes"] / 1e6))
 for _ in range(3):
+    ctx.schedule(cc.CC_TREE)          # invalidates the plan: the next execute prepares again
+    t3 = time.perf_counter()
+    st = ctx.execute(0)
+    t4 = time.perf_counter()
+    print("re-prepared execute: %.2f ms wall, %.2f ms device (time to solution), copies done at %.2f ms"
+          % ((t4 - t3) * 1e3, st["seconds"] * 1e3, st["copy_seconds"] * 1e3))
+for _ in range(3):
     t3 = time.perf_counter()
     st = ctx.execute(0)
     t4 = time.perf_counter()
@@ -74,4 +81,12 @@ print("profiled execute %.2f ms; item ready-time percentiles (us) 1/10/50/90/99/
 g = gp.astype(np.float64)
 print("gemm first ready %.0f us, gemm ready 50%% at %.0f us, last gemm end %.0f us"
       % ((g[:, 1].min() - tb) / 1e3, (np.median(g[:, 1]) - tb) / 1e3, (g[:, 2].max() - tb) / 1e3))
+tpf = tp.astype(np.float64)
+print("bin(ms)  gemm_done  trace_done  trace_ready")
+span = en.max()
+for k in range(int(span // 500) + 1):
+    lo, hi = tb + k * 500e3, tb + (k + 1) * 500e3
+    print("%5.1f  %8d  %8d  %8d" % (k * 0.5, ((g[:, 2] >= lo) & (g[:, 2] < hi)).sum(),
+                                   ((tpf[:, 2] >= lo) & (tpf[:, 2] < hi)).sum(),
+                                   ((tpf[:, 1] >= lo) & (tpf[:, 1] < hi)).sum()))
 os._exit(0)

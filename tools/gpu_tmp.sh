@@ -1,1 +1,4 @@
-for cfg in "100 0" "100 1" "8 1" "16 1" "4 1"; do set -- $cfg; echo "== chunk $1 MB reorder $2"; CC_H2D_CHUNK_MB=$1 CC_COPY_REORDER=$2 timeout -s KILL 200 python tools/e2e_profile.py 2>&1 | grep "prepared execute\|gemm first" | tail -2; done
+timeout -s KILL 60 python tools/t_e2e_debug.py 128 8
+timeout -s KILL 300 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -3
+timeout -s KILL 200 python tools/e2e_profile.py 2>&1 | head -9
+CC_EARLY_COPIES=0 timeout -s KILL 200 python tools/e2e_profile.py 2>&1 | head -9 | grep re-prep
