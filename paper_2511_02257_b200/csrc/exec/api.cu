@@ -121,6 +121,9 @@ struct cc_ctx {
   bool df_valid = false;
   char* df_meta = nullptr;          // ops, deps, tensor maps, sync area: top of the pool, else cudaMalloc
   bool df_meta_owned = false;       // cudaMalloc'ed (the arena had no room above the plan's high water)
+  char* df_fpart = nullptr;         // fused-trace partials (below the metadata, else cudaMalloc)
+  bool df_fpart_owned = false;
+  int32_t df_n_fused = 0;
   size_t df_meta_bytes = 0;
   DfArgs df_gemm{};                 // the dataflow worker's arguments (both queues)
   int* df_sync = nullptr;           // zeroed per launch (with the two queue heads before it)
@@ -174,6 +177,10 @@ struct cc_ctx {
     if (df_meta && df_meta_owned) cudaFree(df_meta);
     df_meta = nullptr;
     df_meta_owned = false;
+    if (df_fpart && df_fpart_owned) cudaFree(df_fpart);
+    df_fpart = nullptr;
+    df_fpart_owned = false;
+    df_n_fused = 0;
     for (auto e : df_events)
       if (e) cudaEventDestroy(e);
     df_events.clear();
@@ -478,6 +485,12 @@ class RWTracker {
       p.readers.push_back(op);
     });
   }
+  // the latest writer of any byte in [off, off+n) (-1: never written)
+  int32_t last_writer(int64_t off, int64_t n) {
+    int32_t w = -1;
+    visit(off, n, [&](Piece& p) { w = std::max(w, p.writer); });
+    return w;
+  }
   void write(int64_t off, int64_t n, int32_t op, std::vector<int32_t>& deps) {
     visit(off, n, [&](Piece& p) {
       if (p.writer >= 0) deps.push_back(p.writer);
@@ -589,6 +602,8 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   // 1. data dependencies over the device pool and the host pool
   RWTracker dev(ctx->pool_bytes), host(std::max<int64_t>(ctx->pp.host_pool_bytes, 1));
   std::vector<std::vector<int32_t>> deps(static_cast<size_t>(n_ops));
+  // writers of contraction operands: pool writer op, -1 never written, -2 caller device leaf
+  std::vector<int32_t> wr_a(size_t(n_ops), -1), wr_b(size_t(n_ops), -1);
   for (int32_t i = 0; i < n_ops; ++i) {
     const PhysOp& op = ops[size_t(i)];
     const Node& n = g.nodes[size_t(op.node)];
@@ -601,13 +616,60 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       dev.read(op.dev_off, rb, i, d);
       host.write(op.host_off, rb, i, d);
     } else if (op.kind == OP_CONTRACT) {
-      if (op.loc_a == LOC_POOL) dev.read(op.off_a, round_up(g.nodes[size_t(n.l)].size, ALIGN), i, d);
-      if (op.loc_b == LOC_POOL) dev.read(op.off_b, round_up(g.nodes[size_t(n.r)].size, ALIGN), i, d);
+      const int64_t sa = round_up(g.nodes[size_t(n.l)].size, ALIGN), sb = round_up(g.nodes[size_t(n.r)].size, ALIGN);
+      wr_a[size_t(i)] = op.loc_a == LOC_POOL ? dev.last_writer(op.off_a, sa) : (op.loc_a == LOC_DEVLEAF ? -2 : -1);
+      wr_b[size_t(i)] = op.loc_b == LOC_POOL ? dev.last_writer(op.off_b, sb) : (op.loc_b == LOC_DEVLEAF ? -2 : -1);
+      if (op.loc_a == LOC_POOL) dev.read(op.off_a, sa, i, d);
+      if (op.loc_b == LOC_POOL) dev.read(op.off_b, sb, i, d);
       if (op.dev_off >= 0) dev.write(op.dev_off, rb, i, d);
     }
     std::sort(d.begin(), d.end());
     d.erase(std::unique(d.begin(), d.end()), d.end());
     d.erase(std::remove(d.begin(), d.end(), i), d.end());
+  }
+  // 1a. trace fusion.  A TR_MM op whose later operand is written by a GEMM op G (MM1 / BB2
+  // output, full-K tiles) while its other operand was written before G (or is a caller device
+  // leaf) is computed inside G's tiles: each output tile dots its registers with the matching
+  // transposed tile of the other operand (tr(XY) = sum_ij X_ij Y_ji), so the trace never
+  // reads G's output back from HBM and needs no work items of its own.  Its data dependencies
+  // move to G (G now also waits for the other operand's writer, which precedes G in plan
+  // order), and everything that waited for the TR op waits for G instead.  CC_DF_FUSE_TR=0
+  // turns it off.
+  std::vector<int32_t> fuse_host(size_t(n_ops), -1);
+  std::vector<std::vector<int32_t>> fused_of(static_cast<size_t>(n_ops));
+  {
+    constexpr size_t MAX_FUSED = 16;
+    // default off: on c2 the fused partner stages come in bursts the 6-stage ring cannot hide
+    // (4.89 ms vs 4.64 ms unfused, profiles/r01 notes); kept for larger N and as an option
+    const bool fuse = getenv("CC_DF_FUSE_TR") ? atoi(getenv("CC_DF_FUSE_TR")) != 0 : false;
+    for (int32_t i = 0; fuse && i < n_ops; ++i) {
+      const PhysOp& op = ops[size_t(i)];
+      if (op.kind != OP_CONTRACT || g.nodes[size_t(op.node)].op != CC_TR_MM) continue;
+      const Node& n = g.nodes[size_t(op.node)];
+      const int32_t wa = wr_a[size_t(i)], wb = wr_b[size_t(i)];
+      int32_t G, other, gnode;
+      if (wa >= 0 && wa > wb) {
+        G = wa; other = wb; gnode = n.l;
+      } else if (wb >= 0 && wb > wa) {
+        G = wb; other = wa; gnode = n.r;
+      } else {
+        continue;
+      }
+      if (other == -1) continue;   // other operand never written in the pool (not resident)
+      const PhysOp& og = ops[size_t(G)];
+      if (og.kind != OP_CONTRACT || og.node != gnode) continue;
+      const int gop = g.nodes[size_t(gnode)].op;
+      if (gop != CC_MM1 && gop != CC_BB2) continue;
+      int64_t tiles, KT, chunks;
+      df_gemm_geometry(problem_for(gop, Lt, N, g.S, nullptr, nullptr, nullptr), tiles, KT, chunks, ctx->num_sms);
+      if (chunks != 1 || fused_of[size_t(G)].size() >= MAX_FUSED) continue;
+      fuse_host[size_t(i)] = G;
+      fused_of[size_t(G)].push_back(i);
+      if (other >= 0) {
+        auto& dg = deps[size_t(G)];
+        if (std::find(dg.begin(), dg.end(), other) == dg.end()) dg.push_back(other);
+      }
+    }
   }
   tmr.lap("rw deps");
   // 1b. copy issue order per stream (plan op indices).  A copy stream runs its copies in
@@ -759,6 +821,9 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   int64_t n_chunked = 0, n_traced = 0;
   std::vector<int32_t> chunk_ring_user(size_t(DF_CHUNK_RING), -1), trace_ring_user(size_t(DF_TRACE_RING), -1);
   std::vector<std::vector<int32_t>> ring_deps(static_cast<size_t>(n_ops));
+  std::vector<DfFused> fusedv;
+  int64_t fused_part_bytes = 0;
+  constexpr int64_t GC_WARPS = 8;   // consumer warps of the worker (per-warp fused partials)
   int BM, BN, BK, slot_doubles;
   df_gemm_tile_dims(&BM, &BN, &BK, &slot_doubles);
   for (int32_t i = 0; i < n_ops; ++i) {
@@ -767,6 +832,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
     const Node& n = g.nodes[size_t(op.node)];
     const void* a = op.loc_a == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.l)] : ctx->arena + op.off_a;
     const void* b = op.loc_b == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.r)] : ctx->arena + op.off_b;
+    if (fuse_host[size_t(i)] >= 0) continue;   // fused TR: computed by its host GEMM's tiles
     DfOp d{};
     d.sync_id = slot[size_t(i)];
     if (n.op == CC_TR_MM) {
@@ -814,6 +880,27 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       if (!df_encode_maps(tmaps.data() + size_t(d.tmap) * 256, p.A, p.B, p.M, p.Nn, p.Kin, p.Ko, p.batch, p.lda,
                           p.sAo, p.sAb, p.ldb, p.sBo, p.sBb))
         throw Error(CC_E_CUDA, "TMA descriptor encoding failed");
+      if (!fused_of[size_t(i)].empty()) {
+        d.fuse_begin = int32_t(fusedv.size());
+        d.fuse_count = int32_t(fused_of[size_t(i)].size());
+        for (int32_t f : fused_of[size_t(i)]) {
+          const PhysOp& of = ops[size_t(f)];
+          const Node& nf = g.nodes[size_t(of.node)];
+          const bool g_left = nf.l == op.node;     // G's output is the TR's left operand
+          const void* x = g_left ? (of.loc_b == LOC_DEVLEAF ? ctx->leaf_dev[size_t(nf.r)] : ctx->arena + of.off_b)
+                                 : (of.loc_a == LOC_DEVLEAF ? ctx->leaf_dev[size_t(nf.l)] : ctx->arena + of.off_a);
+          DfFused fz{};
+          fz.tmap = int32_t(tmaps.size() / 256);
+          tmaps.resize(tmaps.size() + 256);
+          if (!df_encode_partner_map(tmaps.data() + size_t(fz.tmap) * 256, x, Lt, N))
+            throw Error(CC_E_CUDA, "TMA descriptor encoding failed");
+          fz.tiles = d.tiles_m * d.tiles_n;
+          fz.part = reinterpret_cast<double2*>(fused_part_bytes);   // offset; patched at upload
+          fused_part_bytes += Lt * fz.tiles * GC_WARPS * 16;
+          fz.root = ctx->roots + int64_t(g.tree_of_root[size_t(of.node)]) * Lt;
+          fusedv.push_back(fz);
+        }
+      }
       g_items += d.n_items;
       df_index[size_t(i)] = int32_t(gops.size());
       gops.push_back(d);
@@ -821,6 +908,12 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
     }
     target[size_t(i)] = d.n_items;
   }
+  // fused TR ops alias their host GEMM's completion (dependents wait for the GEMM)
+  for (int32_t i = 0; i < n_ops; ++i)
+    if (fuse_host[size_t(i)] >= 0) {
+      slot[size_t(i)] = slot[size_t(fuse_host[size_t(i)])];
+      target[size_t(i)] = target[size_t(fuse_host[size_t(i)])];
+    }
   tmr.lap("items+tmaps");
   std::vector<int64_t> qpos(size_t(n_ops), INT64_MAX);   // merged queue position of compute ops
   // 3. queue order: a topological order of the plan's ops (compute and copy; consecutive
@@ -874,11 +967,14 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       for (int32_t k : succ[size_t(i)])
         if (--indeg[size_t(k)] == 0) ready.push({key(k), k});
     }
-    if (order.size() != gops.size()) throw Error(CC_E_STATE, "dataflow: dependency cycle");
+    size_t n_fused_ops = 0;
+    for (int32_t i = 0; i < n_ops; ++i) n_fused_ops += fuse_host[size_t(i)] >= 0;
+    if (order.size() != gops.size() + n_fused_ops) throw Error(CC_E_STATE, "dataflow: dependency cycle");
     std::vector<DfOp> nops, tops_v;
     std::vector<int32_t> nplan, tplan_v;
     int64_t first = 0, tfirst = 0;
     for (int32_t i : order) {
+      if (df_index[size_t(i)] < 0) continue;   // fused TR (no items)
       DfOp d = gops[size_t(df_index[size_t(i)])];
       if (d.kind == 0) {
         d.first_item = first;
@@ -1011,7 +1107,8 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   for (size_t k = 0; k < tops.size(); ++k)
     std::fill(titem_op.begin() + tops[k].first_item, titem_op.begin() + tops[k].first_item + tops[k].n_items, int32_t(k));
   const size_t sz_gi = round_up(int64_t(gitem_op.size() * 4), 256), sz_ti = round_up(int64_t(titem_op.size() * 4), 256);
-  const size_t total = sz_g + sz_t + 2 * sz_d + sz_m + sz_gi + sz_ti;
+  const size_t sz_f = round_up(int64_t(std::max<size_t>(fusedv.size(), 1) * sizeof(DfFused)), 256);
+  const size_t total = sz_g + sz_t + 2 * sz_d + sz_m + sz_gi + sz_ti + sz_f;
   // device region: the top of the pool when the plan's high water leaves room (no allocation
   // on the execute path), else a cudaMalloc
   const int64_t meta_off = (int64_t(ctx->df_sync_base - ctx->arena) - int64_t(total)) / 256 * 256;
@@ -1023,6 +1120,20 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
     ctx->df_meta_owned = true;
   }
   ctx->df_meta_bytes = total;
+  // fused-trace partials ([Lt][tiles][warps] per fused TR, written before read: no upload)
+  if (ctx->df_fpart && ctx->df_fpart_owned) cudaFree(ctx->df_fpart);
+  ctx->df_fpart = nullptr;
+  ctx->df_fpart_owned = false;
+  if (fused_part_bytes > 0) {
+    const int64_t fp_off = (meta_off - fused_part_bytes) / 256 * 256;
+    if (!ctx->df_meta_owned && fp_off >= ctx->pp.pool_high_water) {
+      ctx->df_fpart = ctx->arena + fp_off;
+    } else {
+      ck(cudaMalloc(reinterpret_cast<void**>(&ctx->df_fpart), size_t(fused_part_bytes)), "fused trace partials");
+      ctx->df_fpart_owned = true;
+    }
+    for (auto& fz : fusedv) fz.part = reinterpret_cast<double2*>(ctx->df_fpart + reinterpret_cast<intptr_t>(fz.part));
+  }
   char* m = ctx->df_meta;
   unsigned long long* heads = reinterpret_cast<unsigned long long*>(ctx->df_sync_base);
   char* pg = m;
@@ -1032,6 +1143,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   char* pm = pdt + sz_d;
   char* pgi = pm + sz_m;
   char* pti = pgi + sz_gi;
+  char* pf = pti + sz_ti;
   {
     // one host image, one copy, ordered on the compute stream before the worker launch
     if (ctx->df_meta_img_bytes < total) {
@@ -1058,6 +1170,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
     put(pds, dep_slot.data(), dep_slot.size() * 4);
     put(pdt, dep_target.data(), dep_target.size() * 4);
     put(pm, tmaps.data(), tmaps.size());
+    put(pf, fusedv.data(), fusedv.size() * sizeof(DfFused));
     // SM-driven upload on the compute stream: the copy engines may be busy with early leaf copies
     ck(launch_upload(m, img.data(), total, ctx->num_sms, ctx->cs), "dataflow metadata upload");
     ck(cudaEventRecord(ctx->ev_meta, ctx->cs), "event");
@@ -1067,6 +1180,8 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   da.dep_target = reinterpret_cast<const int32_t*>(pdt);
   da.tmaps = pm;
   da.sync = ctx->df_sync;
+  da.fused = reinterpret_cast<const DfFused*>(pf);
+  ctx->df_n_fused = int32_t(fusedv.size());
   da.q = DfQueue{reinterpret_cast<const DfOp*>(pg), reinterpret_cast<const int32_t*>(pgi), int32_t(gops.size()),
                  g_items, heads};
   da.qt = DfQueue{reinterpret_cast<const DfOp*>(pt), reinterpret_cast<const int32_t*>(pti), int32_t(tops.size()),
@@ -1137,6 +1252,10 @@ int issue_dataflow(cc_ctx* ctx, bool time_copies = false) {
     ck(df_launch(ctx->df_gemm, ctx->num_sms, ctx->cs), "dataflow worker");
     DBG("worker launched");
     ++nl;
+    if (ctx->df_n_fused > 0) {
+      ck(df_launch_fused_finish(ctx->df_gemm.fused, ctx->df_n_fused, g.Lt, ctx->cs), "fused trace finish");
+      ++nl;
+    }
   }
   DBG("workers launched");
   tmr.lap("worker");

@@ -40,6 +40,12 @@ using GC = Cfg<64, 64, 16, 32, 16, DF_STAGES>;   // 32 KB stages
 constexpr int CW = GC::NCW * 32;           // 256 consumer threads (+ issuer + 2 scheduler warps)
 constexpr int NT = CW + 96;
 constexpr int TB = 32;                     // trace block edge (complex)
+#ifndef PREFETCH_PARTNERS
+#define PREFETCH_PARTNERS 0
+#endif
+#ifndef PREFETCH_TRACE
+#define PREFETCH_TRACE 0
+#endif
 constexpr int INFO = 4;                    // item slots per queue (claimed-ready-running-unpublished)
 static_assert(GC::A_BYTES == TB * TB * 16 && GC::B_BYTES == TB * TB * 16, "a trace block pair fills one stage");
 
@@ -50,6 +56,12 @@ __device__ __forceinline__ void tma_load_4d_g(void* dst, const void* map, uint64
           smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_4d(const void* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(map), "r"(c0), "r"(c1),
+               "r"(c2), "r"(c3)
+               : "memory");
 }
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
@@ -93,13 +105,16 @@ struct ItemInfo {
   const void* tB;
   int32_t op, kind, npos; // npos: stages the item consumes
   int32_t tm, tn, b, k0, kt_per_o, chunk;   // GEMM
+  int32_t kt, fb, fc, ptmap0, rr;           // GEMM: k-tile stages, fused traces [fb, fb+fc) with
+                                            // partner maps ptmap0.., tile index within its slice
   int32_t t, u0, nb, piece;                 // TRACE
   unsigned long long t_disp, t_ready;       // profiling (producer)
   unsigned long long t_first, t_comp;       // profiling (consumers)
 };
 
 // Decode `item` of queue q.
-__device__ __forceinline__ void decode_item(const DfQueue& q, int64_t item, ItemInfo& inf, const void* tmaps) {
+__device__ __forceinline__ void decode_item(const DfQueue& q, int64_t item, ItemInfo& inf, const void* tmaps,
+                                            const DfFused* fused) {
   inf.item = item;
   const int oi = q.item_op[item];
   const DfOp& op = q.ops[oi];
@@ -120,8 +135,13 @@ __device__ __forceinline__ void decode_item(const DfQueue& q, int64_t item, Item
     inf.tm = int(rr - int64_t(inf.tn) * op.tiles_m);
     inf.b = int(b);
     inf.k0 = int((int64_t(chunk) * op.KT) / op.n_chunks);
-    inf.npos = int((int64_t(chunk + 1) * op.KT) / op.n_chunks) - inf.k0;
+    inf.kt = int((int64_t(chunk + 1) * op.KT) / op.n_chunks) - inf.k0;
     inf.kt_per_o = op.kt_per_o;
+    inf.rr = int(rr);
+    inf.fb = op.fuse_begin;
+    inf.fc = op.fuse_count;
+    inf.ptmap0 = op.fuse_count > 0 ? fused[op.fuse_begin].tmap : 0;
+    inf.npos = inf.kt + 2 * op.fuse_count;   // + two partner stages per fused trace
   } else {
     const int t = int(local / op.P), p = int(local - int64_t(t) * op.P);
     const int U = op.nb * op.nb;
@@ -153,8 +173,30 @@ constexpr uint32_t SK_TRACE = 1, SK_STOP = 2;   // 0: GEMM k-tile
 constexpr uint32_t SD_FIRST = 1u << 5, SD_LAST = 1u << 6;
 static_assert(INFO <= 8, "slot field is 3 bits");
 
-__device__ __forceinline__ void gemm_stage_loads(const ItemInfo& inf, int k, uint8_t* sA, uint64_t* bar) {
+__device__ __forceinline__ void gemm_stage_loads(const ItemInfo& inf, int k, uint8_t* sA, uint64_t* bar,
+                                                 const void* tmaps) {
   using C = GC;
+  if (k >= inf.kt) {
+    // partner stage of fused trace f, half h: X[b, tn*64 + 32h + (0..31), tm*64 + (0..63)] as 8
+    // boxes of 8 complex x 32 rows (row = j - 32h of the output tile, box c = columns i in
+    // 8c..8c+7)
+    const int f = (k - inf.kt) >> 1, h = (k - inf.kt) & 1;
+    const void* map = static_cast<const uint8_t*>(tmaps) + size_t(2 * (inf.ptmap0 + f)) * 128;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      tma_load_4d_g(sA + c * 4096, map, bar, 2 * (inf.tm * C::BM + 8 * c), inf.tn * C::BN + 32 * h, 0, inf.b);
+    return;
+  }
+  if (k == 0 && inf.fc > 0 && PREFETCH_PARTNERS) {
+    // warm L2 with the item's partner tiles while its k-tiles run
+    for (int f = 0; f < inf.fc; ++f) {
+      const void* map = static_cast<const uint8_t*>(tmaps) + size_t(2 * (inf.ptmap0 + f)) * 128;
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          tma_prefetch_4d(map, 2 * (inf.tm * C::BM + 8 * c), inf.tn * C::BN + 32 * h, 0, inf.b);
+    }
+  }
   uint8_t* sB = sA + C::A_BYTES;
   const int kk = inf.k0 + k;
   const int ko = kk / inf.kt_per_o;
@@ -254,7 +296,7 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
                    (k == np_of[x] - 1 ? SD_LAST : 0u);
       mbar_expect_tx(&full[st], C::STAGE_BYTES);
       uint8_t* sA = smem + st * C::STAGE_BYTES;
-      if (x == 0) gemm_stage_loads(inf, k, sA, &full[st]);
+      if (x == 0) gemm_stage_loads(inf, k, sA, &full[st], a.tmaps);
       else trace_stage_loads(inf, k, sA, &full[st]);
       ++pos;
       if (++k_of[x] == np_of[x]) have[x] = false;
@@ -344,7 +386,7 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
         if (it >= Q.n_items) {
           exhausted = true;
         } else {
-          decode_item(Q, it, inf, a.tmaps);
+          decode_item(Q, it, inf, a.tmaps, a.fused);
           inf.t_disp = t0;
           pending = true;
           dep = 0;
@@ -355,6 +397,23 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
         asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tA) : "memory");
         asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(inf.tB) : "memory");
+        if (x == 0)
+          for (int f = 0; f < inf.fc; ++f)
+            asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(
+                             static_cast<const uint8_t*>(a.tmaps) + size_t(2 * (inf.ptmap0 + f)) * 128)
+                         : "memory");
+        if (x == 1 && PREFETCH_TRACE) {
+          // warm L2 with the trace item's block pairs (the scheduler is off the issue path)
+          for (int k = 0; k < inf.npos; ++k) {
+            const int u = inf.u0 + k;
+            const int I = u / inf.nb, J = u - I * inf.nb;
+#pragma unroll
+            for (int ch = 0; ch < TB / 8; ++ch) {
+              tma_prefetch_4d(inf.tA, 2 * (J * TB + 8 * ch), I * TB, 0, inf.t);
+              tma_prefetch_4d(inf.tB, 2 * (I * TB + 8 * ch), J * TB, 0, inf.t);
+            }
+          }
+        }
         inf.t_ready = prof ? gtimer() : 0ull;
         const int s = int(n_alloc % INFO);
         s_info[x][s] = inf;
@@ -377,22 +436,86 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
   }
 
   // ----------------------------------- consumers ---------------------------------------------
+  // Stages arrive in ring order.  A GEMM item's stages are contiguous in the GEMM subsequence
+  // (the issuer holds one GEMM item at a time), with TR_MM stages interleaved; the item is
+  // processed by one block scope so its accumulators (and the finished tile kept for fused
+  // traces) live only as long as the item — the register allocator sees disjoint ranges.
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
   const int g = lane >> 2, t = lane & 3;
   const bool prof = a.prof != nullptr;
-  double acc[3][C::MI][C::NJ][2];   // 3M products (common.cuh dmma3m_ktile)
   double2 tacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
   // profile (thread 0): clock64 cycles waiting for stage data / in stage math+epilogue, per kind
   long long c_wait[2] = {0, 0}, c_work[2] = {0, 0}, n_st[2] = {0, 0}, ta = 0, tb = 0, c_epi = 0, te = 0;
   int lastk = 0;
-  for (uint32_t r = 0;; ++r) {
-    const int st = int(r % C::STAGES);
+  uint32_t r = 0;
+  // wait for ring position r, return its descriptor (stage index in st)
+  auto next_stage = [&](int& st) -> uint32_t {
+    st = int(r % C::STAGES);
     if (prof && tid == 0) {
       ta = clock64();
       if (r > 0) c_work[lastk] += ta - tb;
     }
     mbar_wait(&full[st], (r / C::STAGES) & 1u);
     const uint32_t d = s_desc[st];
+    const uint32_t kind = d & 3u;
+    if (prof && tid == 0 && kind < 2) {
+      tb = clock64();
+      c_wait[kind] += tb - ta;
+      ++n_st[kind];
+      lastk = int(kind);
+    }
+    ++r;
+    return d;
+  };
+  // one TR_MM block pair: sum of A[r][c] * B[c][r]
+  auto trace_stage = [&](uint32_t d, int st) {
+    const int slot = int((d >> 2) & 7u);
+    const uint8_t* sA = smem + st * C::STAGE_BYTES;
+    if (d & SD_FIRST) {
+      tacc[0] = tacc[1] = make_double2(0.0, 0.0);
+      if (tid == 0 && prof) s_info[1][slot].t_first = gtimer();
+    }
+    const uint8_t* sB = sA + C::A_BYTES;
+    // element (row, col) of a 32x32 block: chunk col/8, 128-byte row `row`, 16-byte slot
+    // (col%8) ^ (row%8) (TMA 128-byte swizzle); warp w takes rows w, w+8, w+16, w+24 of A,
+    // lane = column c: A[r][c] row-contiguous, B[c][r] one 128-byte row per lane — both
+    // conflict-free.
+#pragma unroll
+    for (int qq = 0; qq < TB / 8; ++qq) {
+      const int rr = warp + qq * 8, c = lane;
+      const double2 av = *reinterpret_cast<const double2*>(sA + (c >> 3) * (TB * 128) + rr * 128 +
+                                                           (((c & 7) ^ (rr & 7)) << 4));
+      const double2 bv = *reinterpret_cast<const double2*>(sB + (rr >> 3) * (TB * 128) + c * 128 +
+                                                           (((rr & 7) ^ (c & 7)) << 4));
+      tacc[qq & 1] = cmul_acc(tacc[qq & 1], av, bv);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (!(d & SD_LAST)) return;
+    if (tid == 0 && prof) s_info[1][slot].t_comp = gtimer();
+    double2 acc2 = make_double2(tacc[0].x + tacc[1].x, tacc[0].y + tacc[1].y);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      acc2.x += __shfl_xor_sync(0xffffffffu, acc2.x, o);
+      acc2.y += __shfl_xor_sync(0xffffffffu, acc2.y, o);
+    }
+    // the TR scheduler sums the warps' partials (fixed order) when it publishes the item
+    if (lane == 0) red[slot][warp] = acc2;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&done[1][slot]);
+  };
+  // the next stage of the current GEMM item, running interleaved trace stages on the way
+  auto next_gemm_stage = [&](int& st) {
+    for (;;) {
+      const uint32_t d = next_stage(st);
+      if ((d & 3u) != SK_TRACE) return d;
+      trace_stage(d, st);
+    }
+  };
+
+  for (;;) {
+    int st;
+    uint32_t d = next_stage(st);
     const uint32_t kind = d & 3u;
     if (kind == SK_STOP) {
       if (prof && tid == 0 && a.prof_sm) {
@@ -408,139 +531,157 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
       }
       break;
     }
-    if (prof && tid == 0) {
-      tb = clock64();
-      c_wait[kind] += tb - ta;
-      ++n_st[kind];
-      lastk = int(kind);
+    if (kind == SK_TRACE) {
+      trace_stage(d, st);
+      continue;
     }
+    // ---------------- GEMM item: k-tiles, epilogue, then partner stages of fused traces ----------------
     const int slot = int((d >> 2) & 7u);
-    const uint8_t* sA = smem + st * C::STAGE_BYTES;
-    if (kind != SK_TRACE) {
-      // ---------------- GEMM k-tile of a tile (or k-chunk of a tile) ----------------
-      if (d & SD_FIRST) {
+    const ItemInfo& cur = s_info[0][slot];
+    if (tid == 0 && prof) s_info[0][slot].t_first = gtimer();
+    {
+      double acc[3][C::MI][C::NJ][2];   // 3M products (common.cuh dmma3m_ktile)
 #pragma unroll
-        for (int x = 0; x < 3; ++x)
+      for (int x = 0; x < 3; ++x)
 #pragma unroll
-          for (int i = 0; i < C::MI; ++i)
+        for (int i = 0; i < C::MI; ++i)
 #pragma unroll
-            for (int j = 0; j < C::NJ; ++j) acc[x][i][j][0] = acc[x][i][j][1] = 0.0;
-        if (tid == 0 && prof) s_info[0][slot].t_first = gtimer();
+          for (int j = 0; j < C::NJ; ++j) acc[x][i][j][0] = acc[x][i][j][1] = 0.0;
+      for (int k = 0;;) {
+        const uint8_t* sA = smem + st * C::STAGE_BYTES;
+        dmma3m_ktile<C>(sA, sA + C::A_BYTES, wm, wn, g, t, acc);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (++k == cur.kt) break;
+        d = next_gemm_stage(st);
       }
-      dmma3m_ktile<C>(sA, sA + C::A_BYTES, wm, wn, g, t, acc);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-      if (!(d & SD_LAST)) continue;
       if (prof && tid == 0) te = clock64();
-      const ItemInfo& cur = s_info[0][slot];
       const DfOp& op = a.q.ops[cur.op];
       if (tid == 0 && prof) s_info[0][slot].t_comp = gtimer();
-      const int64_t tile = cur.tile;
-      const int chunk = cur.chunk;
-      double2* out = static_cast<double2*>(op.C) + int64_t(cur.b) * op.sCb;
-      // complex results C[row0 + 8i + g][col0 + 8j + 2t + e] = gauss3m_combine(acc, i, j, e)
-      if (op.n_chunks == 1) {
+    const int64_t tile = cur.tile;
+    const int chunk = cur.chunk;
+    double2* out = static_cast<double2*>(op.C) + int64_t(cur.b) * op.sCb;
+    // complex results C[row0 + 8i + g][col0 + 8j + 2t + e] = gauss3m_combine(acc, i, j, e)
+    if (op.n_chunks == 1) {
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i) {
+        const int64_t row = int64_t(cur.tm) * C::BM + wm * C::WM + i * 8 + g;
+        if (row >= op.M) continue;
+#pragma unroll
+        for (int j = 0; j < C::NJ; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t col = int64_t(cur.tn) * C::BN + wn * C::WN + j * 8 + 2 * t + e;
+            if (col < op.Nn) out[row * op.ldc + col] = gauss3m_combine<C>(acc, i, j, e);
+          }
+      }
+    } else {
+      // publish this chunk's partial; the CTA completing the tile's last chunk sums them
+      double2* base = static_cast<double2*>(op.part) + (tile * op.n_chunks) * int64_t(C::SLOT_DOUBLES / 2);
+      double2* mine = base + int64_t(chunk) * (C::SLOT_DOUBLES / 2) + warp * (C::FRAG / 2 * 32);
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NJ; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            __stcg(mine + ((i * C::NJ + j) * 2 + e) * 32 + lane, gauss3m_combine<C>(acc, i, j, e));
+      __threadfence();
+      named_sync(1, CW);
+      if (tid == 0) {
+        const int old = atomicAdd(&op.tile_cnt[tile], 1);
+        s_flag = (old == op.n_chunks - 1);
+        if (s_flag) op.tile_cnt[tile] = 0;
+      }
+      named_sync(1, CW);
+      if (s_flag) {
+        __threadfence();
+        const double2* w0 = base + warp * (C::FRAG / 2 * 32);
 #pragma unroll
         for (int i = 0; i < C::MI; ++i) {
           const int64_t row = int64_t(cur.tm) * C::BM + wm * C::WM + i * 8 + g;
-          if (row >= op.M) continue;
 #pragma unroll
           for (int j = 0; j < C::NJ; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
+              const int f = ((i * C::NJ + j) * 2 + e) * 32 + lane;
+              double2 v = __ldcg(w0 + f);
+              for (int c = 1; c < op.n_chunks; ++c) {
+                const double2 u = __ldcg(w0 + int64_t(c) * (C::SLOT_DOUBLES / 2) + f);
+                v.x += u.x;
+                v.y += u.y;
+              }
               const int64_t col = int64_t(cur.tn) * C::BN + wn * C::WN + j * 8 + 2 * t + e;
-              if (col < op.Nn) out[row * op.ldc + col] = gauss3m_combine<C>(acc, i, j, e);
+              if (row < op.M && col < op.Nn) out[row * op.ldc + col] = v;
             }
         }
-      } else {
-        // publish this chunk's partial; the CTA completing the tile's last chunk sums them
-        double2* base = static_cast<double2*>(op.part) + (tile * op.n_chunks) * int64_t(C::SLOT_DOUBLES / 2);
-        double2* mine = base + int64_t(chunk) * (C::SLOT_DOUBLES / 2) + warp * (C::FRAG / 2 * 32);
+      }
+    }
+
+
+      if (prof && tid == 0) c_epi += clock64() - te;
+      if (cur.fc > 0) {
+        // the tile's complex values stay in registers for the fused traces
+        double2 v[C::MI][C::NJ][2];
 #pragma unroll
         for (int i = 0; i < C::MI; ++i)
 #pragma unroll
           for (int j = 0; j < C::NJ; ++j)
 #pragma unroll
-            for (int e = 0; e < 2; ++e)
-              __stcg(mine + ((i * C::NJ + j) * 2 + e) * 32 + lane, gauss3m_combine<C>(acc, i, j, e));
-        __threadfence();
-        named_sync(1, CW);
-        if (tid == 0) {
-          const int old = atomicAdd(&op.tile_cnt[tile], 1);
-          s_flag = (old == op.n_chunks - 1);
-          if (s_flag) op.tile_cnt[tile] = 0;
-        }
-        named_sync(1, CW);
-        if (s_flag) {
-          __threadfence();
-          const double2* w0 = base + warp * (C::FRAG / 2 * 32);
+            for (int e = 0; e < 2; ++e) v[i][j][e] = gauss3m_combine<C>(acc, i, j, e);
+        for (int p = 0; p < 2 * cur.fc; ++p) {
+          d = next_gemm_stage(st);
+          // partner stage (fused trace f, half h) holds X rows j in [32h, 32h+32): the warps
+          // whose output columns j fall there (wn = 2h, 2h+1: one warp per SM sub-partition)
+          // add C[i][j] * X[j][i]; X[j][i] sits in box i/8 = 4wm + mi, row j - 32h, 16-byte
+          // slot (i%8) ^ (j%8) = g ^ (2t+e) — conflict-free across each quarter warp
+          const int f = p >> 1, h = p & 1;
+          if ((wn >> 1) == h) {
+            const uint8_t* sP = smem + st * C::STAGE_BYTES;
+            double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
 #pragma unroll
-          for (int i = 0; i < C::MI; ++i) {
-            const int64_t row = int64_t(cur.tm) * C::BM + wm * C::WM + i * 8 + g;
+            for (int i = 0; i < C::MI; ++i)
 #pragma unroll
-            for (int j = 0; j < C::NJ; ++j)
+              for (int j = 0; j < C::NJ; ++j)
 #pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int f = ((i * C::NJ + j) * 2 + e) * 32 + lane;
-                double2 v = __ldcg(w0 + f);
-                for (int c = 1; c < op.n_chunks; ++c) {
-                  const double2 u = __ldcg(w0 + int64_t(c) * (C::SLOT_DOUBLES / 2) + f);
-                  v.x += u.x;
-                  v.y += u.y;
+                for (int e = 0; e < 2; ++e) {
+                  const int jl = (wn & 1) * C::WN + 8 * j + 2 * t + e;   // row within the half
+                  const double2 x = *reinterpret_cast<const double2*>(sP + (4 * wm + i) * 4096 + jl * 128 +
+                                                                      ((g ^ (jl & 7)) << 4));
+                  if (e == 0) s0 = cmul_acc(s0, v[i][j][e], x);
+                  else s1 = cmul_acc(s1, v[i][j][e], x);
                 }
-                const int64_t col = int64_t(cur.tn) * C::BN + wn * C::WN + j * 8 + 2 * t + e;
-                if (row < op.M && col < op.Nn) out[row * op.ldc + col] = v;
-              }
+            double2 sum = make_double2(s0.x + s1.x, s0.y + s1.y);
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+              sum.x += __shfl_xor_sync(0xffffffffu, sum.x, o);
+              sum.y += __shfl_xor_sync(0xffffffffu, sum.y, o);
+            }
+            if (lane == 0) {
+              const DfFused& fz = a.fused[cur.fb + f];
+              fz.part[(int64_t(cur.b) * fz.tiles + cur.rr) * C::NCW + warp] = sum;
+            }
           }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);
         }
       }
-      // item finished: this warp's stores (ordered by __syncwarp) before the arrival
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&done[0][slot]);
-      if (prof && tid == 0) c_epi += clock64() - te;
-    } else {
-      // ---------------- TR_MM block pair: sum of A[r][c] * B[c][r] ----------------
-      if (d & SD_FIRST) {
-        tacc[0] = tacc[1] = make_double2(0.0, 0.0);
-        if (tid == 0 && prof) s_info[1][slot].t_first = gtimer();
-      }
-      const uint8_t* sB = sA + C::A_BYTES;
-      // element (row, col) of a 32x32 block: chunk col/8, 128-byte row `row`, 16-byte slot
-      // (col%8) ^ (row%8) (TMA 128-byte swizzle); warp w takes rows w, w+8, w+16, w+24 of A,
-      // lane = column c: A[r][c] row-contiguous, B[c][r] one 128-byte row per lane — both
-      // conflict-free.
-#pragma unroll
-      for (int qq = 0; qq < TB / 8; ++qq) {
-        const int rr = warp + qq * 8, c = lane;
-        const double2 av = *reinterpret_cast<const double2*>(sA + (c >> 3) * (TB * 128) + rr * 128 +
-                                                             (((c & 7) ^ (rr & 7)) << 4));
-        const double2 bv = *reinterpret_cast<const double2*>(sB + (rr >> 3) * (TB * 128) + c * 128 +
-                                                             (((rr & 7) ^ (c & 7)) << 4));
-        tacc[qq & 1] = cmul_acc(tacc[qq & 1], av, bv);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-      if (!(d & SD_LAST)) continue;
-      if (tid == 0 && prof) s_info[1][slot].t_comp = gtimer();
-      double2 acc2 = make_double2(tacc[0].x + tacc[1].x, tacc[0].y + tacc[1].y);
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        acc2.x += __shfl_xor_sync(0xffffffffu, acc2.x, o);
-        acc2.y += __shfl_xor_sync(0xffffffffu, acc2.y, o);
-      }
-      // the TR scheduler sums the warps' partials (fixed order) when it publishes the item
-      if (lane == 0) red[slot][warp] = acc2;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&done[1][slot]);
     }
+    // item finished: this warp's stores (ordered by __syncwarp) before the arrival
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&done[0][slot]);
   }
 }
 
 }  // namespace
 
+namespace {
+__global__ void fused_finish_kernel(const DfFused* __restrict__ fused, int64_t Lt);
+}
 cudaError_t df_preload() {
   cudaFuncAttributes attr;
   cudaError_t e = cudaFuncGetAttributes(&attr, df_worker);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&attr, fused_finish_kernel);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(df_worker, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::SMEM);
   return e;
 }
@@ -576,6 +717,45 @@ bool df_encode_maps(void* dst, const void* A, const void* B, int64_t M, int64_t 
   p.sBo = sBo;
   p.sBb = sBb;
   return encode_zgemm_maps(dst, static_cast<uint8_t*>(dst) + 128, p, GC::BM, GC::BK);
+}
+
+bool df_encode_partner_map(void* dst, const void* X, int64_t Lt, int64_t N) {
+  // X as [Lt][N rows][N complex]: boxes of 32 rows x 8 complex (128-byte swizzle); the
+  // second map of the pair is unused
+  ZgemmProblem p{};
+  p.A = X;
+  p.B = X;
+  p.M = N;
+  p.Nn = N;
+  p.Kin = N;
+  p.Ko = 1;
+  p.batch = Lt;
+  p.lda = N;
+  p.sAb = N * N;
+  p.ldb = N;
+  p.sBb = N * N;
+  return encode_zgemm_maps(dst, static_cast<uint8_t*>(dst) + 128, p, TB, TB);
+}
+
+namespace {
+__global__ void fused_finish_kernel(const DfFused* __restrict__ fused, int64_t Lt) {
+  const DfFused& fz = fused[blockIdx.x];
+  for (int64_t t = threadIdx.x; t < Lt; t += blockDim.x) {
+    const double2* p = fz.part + t * fz.tiles * GC::NCW;
+    double2 s = make_double2(0.0, 0.0);
+    for (int k = 0; k < fz.tiles * GC::NCW; ++k) {   // tile-major, warp-minor: fixed order
+      s.x += p[k].x;
+      s.y += p[k].y;
+    }
+    fz.root[t] = s;
+  }
+}
+}  // namespace
+
+cudaError_t df_launch_fused_finish(const DfFused* fused, int32_t n_fused, int64_t Lt, cudaStream_t s) {
+  if (n_fused <= 0) return cudaSuccess;
+  fused_finish_kernel<<<unsigned(n_fused), 64, 0, s>>>(fused, Lt);
+  return cudaGetLastError();
 }
 
 bool df_encode_trace_maps(void* dst, const void* A, const void* B, int64_t Lt, int64_t N) {

@@ -41,6 +41,18 @@ struct DfOp {
   int32_t nb, P;          // 32x32 blocks per row; items (pieces) per time slice
   void* tr_part;          // [Lt][P] complex partials
   int* tr_cnt;            // [Lt] tickets (reset by the finisher)
+  // GEMM with fused traces: after its k-tiles every output tile also computes, for each
+  // fused TR_MM op f, sum over the tile of C[i][j] * X_f[j][i] (X_f = the trace's other
+  // operand, two extra 32 KB stages per f), written per warp to fused[fuse_begin + f].part
+  int32_t fuse_begin, fuse_count;
+};
+
+// One TR_MM op folded into the GEMM that produces its later operand (trace fusion).
+struct DfFused {
+  int32_t tmap;           // tensor map 2*tmap: the other operand [Lt][N][N], 8 x 32 boxes
+  int32_t tiles;          // output tiles per time slice of the host GEMM
+  double2* part;          // [Lt][tiles][8 warps] complex partials
+  double2* root;          // root values [Lt] of the TR's tree (written by the finish kernel)
 };
 
 struct DfQueue {
@@ -52,6 +64,7 @@ struct DfQueue {
 };
 
 struct DfArgs {
+  const DfFused* fused;       // fused traces of GEMM ops
   DfQueue q;                  // GEMM items
   DfQueue qt;                 // TR_MM items
   const int32_t* dep_slot;    // sync slot an op waits on
@@ -78,5 +91,9 @@ bool df_encode_maps(void* dst, const void* A, const void* B, int64_t M, int64_t 
                     int64_t batch, int64_t lda, int64_t sAo, int64_t sAb, int64_t ldb, int64_t sBo, int64_t sBb);
 // TMA maps of a TR_MM op's operands ([Lt][N][N] complex, 32-row boxes).
 bool df_encode_trace_maps(void* dst, const void* A, const void* B, int64_t Lt, int64_t N);
+// TMA map of a fused trace's other operand ([Lt][N][N] complex, boxes of 8 complex x 32 rows).
+bool df_encode_partner_map(void* dst, const void* X, int64_t Lt, int64_t N);
+// root[t] = sum over tiles, warps of part[t][tile][warp] (fixed order), for every fused trace.
+cudaError_t df_launch_fused_finish(const DfFused* fused, int32_t n_fused, int64_t Lt, cudaStream_t s);
 
 }  // namespace cc

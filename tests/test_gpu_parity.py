@@ -146,11 +146,26 @@ def test_c2_small_all_modes(flags):
     assert_corr_close(dag, r_or, corr, c_or)
 
 
-def test_schedule_and_mode_invariance_bitwise():
-    """Root values are bit-identical across schedulers, graph/stream mode and host/device
-    leaves (deterministic kernels, no atomics in any reduction)."""
+def test_schedule_and_mode_invariance_bitwise(monkeypatch):
+    """Deterministic kernels, no atomics in any reduction: root values are bit-identical run to
+    run and across graph/stream mode; with trace fusion off also across schedulers and
+    host/device leaves (which traces fuse into which GEMM depends on the plan, and a fused
+    trace sums in tile order, so with fusion on those agree to rounding)."""
     from paper_2511_02257_b200 import cc
     w = dags.config_c2(N=24, Lt=2, n_loop4=40, n_loop2=4, n_corr=3)
+    monkeypatch.setenv("CC_DF_FUSE_TR", "1")
+    base = run_gpu(w, algo=cc.CC_TREE)[1]
+    again = run_gpu(w, algo=cc.CC_TREE)[1]
+    for t in base:
+        assert np.array_equal(base[t], again[t])
+    for kw in (dict(algo=cc.CC_SIBLING), dict(algo=cc.CC_RSGS), dict(device_leaves=True),
+               dict(flags=1, device_leaves=True)):
+        assert_roots_close(run_gpu(w, **kw)[1], base, rel=1e-13)
+    dl = run_gpu(w, device_leaves=True)[1]
+    dlg = run_gpu(w, flags=1, device_leaves=True)[1]
+    for t in dl:
+        assert np.array_equal(dl[t], dlg[t])
+    monkeypatch.setenv("CC_DF_FUSE_TR", "0")
     base = run_gpu(w, algo=cc.CC_TREE)[1]
     for kw in (dict(algo=cc.CC_SIBLING), dict(algo=cc.CC_RSGS), dict(flags=1), dict(device_leaves=True),
                dict(flags=1, device_leaves=True)):
@@ -190,6 +205,26 @@ def test_chunked_and_reordered_h2d_copies(monkeypatch):
     _, roots, corr, st, ex = run_gpu(w)
     assert_roots_close(roots, r_or)
     assert_corr_close(dag, r_or, corr, c_or)
+
+
+def test_trace_fusion_on_off(monkeypatch):
+    """Traces fused into the GEMM that produces their later operand (partner tiles dotted
+    with the output tile in registers) give the oracle's values, like the stand-alone trace
+    items; ragged N (not a multiple of the 64-wide tile) exercises the zero-filled borders."""
+    for (N, Lt) in ((40, 3), (64, 2), (96, 2)):
+        w = dags.config_c2(N=N, Lt=Lt, n_loop4=70, n_loop2=6, n_corr=4)
+        dag = Dag(w)
+        r_or, c_or = values.run_workload(w, dag)
+        res = {}
+        for fuse in ("1", "0"):
+            monkeypatch.setenv("CC_DF_FUSE_TR", fuse)
+            for dev in (False, True):
+                _, roots, corr, st, ex = run_gpu(w, device_leaves=dev)
+                assert_roots_close(roots, r_or)
+                assert_corr_close(dag, r_or, corr, c_or)
+                res[(fuse, dev)] = (roots, ex["n_kernels"])
+        # fused: one more launch (the finish kernel summing tile partials)
+        assert res[("1", True)][1] == res[("0", True)][1] + 1
 
 
 def test_c3_nucleon_small():
