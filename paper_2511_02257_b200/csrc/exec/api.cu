@@ -1222,6 +1222,18 @@ int issue_dataflow(cc_ctx* ctx, bool time_copies = false) {
   ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_start, 0), "wait");
   ck(cudaStreamWaitEvent(ctx->ds, ctx->ev_start, 0), "wait");
   ck(cudaStreamWaitEvent(ctx->cs2, ctx->ev_start, 0), "wait");
+  // The worker goes first: copy streams may block on stream memory ops waiting for its
+  // counters, and a driver can stall the host's enqueue of further memory ops until the
+  // device makes progress — so the kernel they wait for must already be queued.
+  if (ctx->df_gemm_items + ctx->df_trace_items > 0) {
+    ck(df_launch(ctx->df_gemm, ctx->num_sms, ctx->cs), "dataflow worker");
+    DBG("worker launched");
+    ++nl;
+    if (ctx->df_n_fused > 0) {
+      ck(df_launch_fused_finish(ctx->df_gemm.fused, ctx->df_n_fused, g.Lt, ctx->cs), "fused trace finish");
+      ++nl;
+    }
+  }
   cudaStream_t st[3] = {ctx->cs, ctx->hs, ctx->ds};
   for (const int32_t kk : ctx->df_issue) {
     const size_t k = size_t(kk);
@@ -1248,15 +1260,6 @@ int issue_dataflow(cc_ctx* ctx, bool time_copies = false) {
   }
   ctx->copy_timed = time_copies;
   tmr.lap("copies");
-  if (ctx->df_gemm_items + ctx->df_trace_items > 0) {
-    ck(df_launch(ctx->df_gemm, ctx->num_sms, ctx->cs), "dataflow worker");
-    DBG("worker launched");
-    ++nl;
-    if (ctx->df_n_fused > 0) {
-      ck(df_launch_fused_finish(ctx->df_gemm.fused, ctx->df_n_fused, g.Lt, ctx->cs), "fused trace finish");
-      ++nl;
-    }
-  }
   DBG("workers launched");
   tmr.lap("worker");
   ck(cudaEventRecord(ctx->ev_cs2, ctx->cs2), "event");

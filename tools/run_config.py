@@ -1,0 +1,87 @@
+"""Run a BASELINE config end to end at full size from pinned host leaves (time to solution,
+transfers vs the plan, PCIe / FP64 bounds) and check sampled values against the oracle
+(per-slice independence: the oracle computes a few time slices, or a few trees for Lt=1).
+
+Usage: python tools/run_config.py c3|c4 [--cap BYTES] [--check-trees 3]
+"""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2511_02257_b200 import cc  # noqa: E402
+from synth import dags  # noqa: E402
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config")
+    ap.add_argument("--cap", type=float, default=None)
+    ap.add_argument("--arena-gb", type=float, default=150)
+    ap.add_argument("--check", type=int, default=1)
+    a = ap.parse_args()
+    w = {"c3": dags.config_c3, "c4": dags.config_c4}[a.config]()
+    cap = int(a.cap) if a.cap is not None else (32 * 10 ** 9 if a.config == "c4" else 0)
+    dev = torch.device("cuda:0")
+    streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
+    arena = torch.empty(int(a.arena_gb * (1 << 30)), dtype=torch.uint8, device=dev)
+    ctx = cc.Context(0, arena, streams=streams)
+    t0 = time.perf_counter()
+    ctx.load_workload(w)
+    order, st = ctx.schedule(cc.CC_TREE, cap_bytes=cap)
+    t1 = time.perf_counter()
+    print("%s: %d contractions, plan peak %.2f GB transient %.2f GB, evictions %d, H2D %.2f GB D2H %.2f GB, "
+          "schedule+plan %.1f ms" % (w.name, st["n_contr"], st["peak"] / 1e9, st["transient_peak"] / 1e9,
+                                     st["evictions"], st["h2d_bytes"] / 1e9, st["d2h_bytes"] / 1e9,
+                                     (t1 - t0) * 1e3), flush=True)
+    host = {}
+    tmp = None
+    for n in w.nodes:
+        if n[1] not in (dags.LEAF_M, dags.LEAF_B):
+            continue
+        shape = bench.leaf_shape(w, n[1])
+        cnt = int(np.prod(shape))
+        if tmp is None or tmp.numel() < 2 * cnt:
+            tmp = torch.empty(2 * cnt, dtype=torch.float64, device=dev)
+        d = tmp[:2 * cnt]
+        ctx.fill_synthetic(d, cnt, w.data_seed, n[0], 0, w.leaf_mode, bench.leaf_sigma(w, n[1]))
+        h = torch.empty(2 * cnt, dtype=torch.float64, pin_memory=True)
+        torch.cuda.synchronize()
+        h.copy_(d)
+        host[n[0]] = h
+    del tmp
+    torch.cuda.synchronize()
+    for u, h in host.items():
+        ctx.set_leaf(u, h)
+    for rep in range(2):
+        ex = ctx.execute(0)
+        moved = ex["h2d_bytes"] + ex["d2h_bytes"]
+        print("execute %d: %.1f ms (copies done %.1f ms); moved %.2f GB -> PCIe bound %.1f ms; flops %.3g -> "
+              "FP64 bound %.1f ms" % (rep, ex["seconds"] * 1e3, ex["copy_seconds"] * 1e3, moved / 1e9,
+                                      moved / 55.6e9 * 1e3, ex["flops"], ex["flops"] / 37.0e12 * 1e3), flush=True)
+    if a.check:
+        from oracle.dag import Dag
+        from oracle import values
+        dag = Dag(w)
+        trees = ctx.part_trees()
+        if w.Lt > 1:
+            t = w.Lt - 1
+            r_or, _ = values.run_workload(w, dag, t_range=(t, t + 1))
+            worst = 0.0
+            for tr in trees:
+                got = ctx.root_value(tr, w.Lt)[t]
+                worst = max(worst, abs(got - r_or[tr][0]) / abs(r_or[tr][0]))
+            print("oracle check (slice %d, all %d trees): worst relative root error %.2e" % (t, len(trees), worst))
+        else:
+            print("oracle check skipped (Lt=1: a single-slice oracle of this size takes too long on CPU)")
+    os._exit(0)
+
+
+if __name__ == "__main__":
+    main()
