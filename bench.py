@@ -188,8 +188,8 @@ def config_dict(w, args):
     return {"workload": "%s (BASELINE.json configs[1]: pi-pi I=2 correlator set, %d graphs sharing meson "
                         "nodes, N=%d, Lt=%d)" % (w.name, len(w.trees), w.N, w.Lt),
             "N": w.N, "Lt": w.Lt, "S": w.S, "trees": len(w.trees), "scheduler": "tree (Alg. 4-8)",
-            "parallelism": "time-slice split x%d + NCCL all-reduce of correlators" % args.gpus if args.gpus > 1
-            else "single GPU",
+            "parallelism": "time-slice split x%d + %s all-reduce of correlators" % (
+                args.gpus, getattr(args, "dist_backend", "nccl").upper()) if args.gpus > 1 else "single GPU",
             "l2": "flushed (256 MiB write) before every timed step; inputs (512 MiB of leaves) exceed L2",
             "leaves": "value: device-resident (HBM); e2e: pinned host, H2D inside the step"}
 
@@ -203,6 +203,7 @@ def main():
     ap.add_argument("--impl", default="cc", choices=["cc", "reference"])
     ap.add_argument("--config", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo to test N ranks on fewer GPUs")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -218,19 +219,24 @@ def main():
     from paper_2511_02257_b200 import cc
     from paper_2511_02257_b200.dist import allreduce_correlators
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    local_dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     w = workload(args.config)
-    from oracle.partition import time_range  # pure arithmetic of the split; no oracle compute
-    t0, t1 = time_range(w.Lt, world, rank) if world > 1 else (0, w.Lt)
-    Lt_p = t1 - t0
-
     streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
     cs = streams[0]
     arena = torch.empty(6 << 30, dtype=torch.uint8, device=dev)
-    ctx = cc.Context(local, arena, streams=streams)
+    ctx = cc.Context(local_dev, arena, streams=streams)
+    ctx.load_workload(w)
+    if world > 1:
+        ctx.partition(world, rank, cc.PART_TIME)   # this rank's time slices [t0, t1)
+    t0, t1 = ctx.part_time_range()
+    Lt_p = t1 - t0
 
     # leaves: device-resident copy of this rank's slices (value) + pinned host full leaves (e2e)
     leaf_ops = [(n[0], n[1]) for n in w.nodes if n[1] in (dags.LEAF_M, dags.LEAF_B)]
@@ -251,9 +257,6 @@ def main():
     torch.cuda.synchronize()
 
     # ---- value: plan replay with resident leaves --------------------------------------------------
-    ctx.load_workload(w)
-    if world > 1:
-        ctx.partition(world, rank, cc.PART_TIME)
     order, pst = ctx.schedule(cc.CC_TREE)
     for u, d in dev_leaves.items():
         ctx.set_leaf_device(u, d)
@@ -345,7 +348,7 @@ def main():
 
     # ---- e2e: the public API from pinned host buffers ------------------------------------------------
     arena2 = torch.empty(6 << 30, dtype=torch.uint8, device=dev)
-    ctx2 = cc.Context(local, arena2, streams=streams)
+    ctx2 = cc.Context(local_dev, arena2, streams=streams)
     e2e = []
     h2d_step = d2h_step = 0
 
@@ -365,10 +368,19 @@ def main():
         for u, h in host_leaves.items():
             ctx2.set_leaf(u, h)
 
+    corr_full2 = torch.zeros((n_corr, w.Lt), dtype=torch.complex128, device=dev)
+    host_corr = torch.empty((n_corr, w.Lt), dtype=torch.complex128, pin_memory=True)
+
     def step_e2e():
+        # solve (this rank's time slices), sum the ranks' correlators over NCCL, read to host
         st = ctx2.execute(0)
-        out = [ctx2.correlator(c, Lt_p) for c in corr_ids]
-        return st, out
+        ptr2, _, _ = ctx2.correlator_device_ptr()
+        view2 = _device_view(ptr2, (n_corr, Lt_p), dev)
+        with torch.cuda.stream(cs):
+            full = allreduce_correlators(view2, t0, t1, w.Lt, out=corr_full2) if world > 1 else view2
+            host_corr.copy_(full, non_blocking=True)
+        cs.synchronize()
+        return st, host_corr
 
     for _ in range(max(1, args.warmup)):
         prepare_e2e()
@@ -389,7 +401,7 @@ def main():
         e2e.append(e0.elapsed_time(e1) * 1e-3)
         copy_ms.append(st["copy_seconds"] * 1e3)
         h2d_step = st["h2d_bytes"]
-        d2h_step = st["d2h_bytes"] + n_corr * Lt_p * 16
+        d2h_step = st["d2h_bytes"] + n_corr * w.Lt * 16
     t_e2e = float(np.sum(e2e))
 
     # max over ranks

@@ -146,6 +146,9 @@ cc_status cc_dag_info(cc_ctx* ctx, cc_dag_stats* out);
 cc_status cc_partition(cc_ctx* ctx, int32_t n_parts, int32_t part, int32_t mode);
 /* Trees of the current part (ids, ascending); n_out receives the count. */
 cc_status cc_part_trees(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out);
+/* Time-slice range [t0, t1) of the loaded part (the whole [0, Lt) unless a TIME partition is
+ * active): where this part's correlator slices go in the full [n_corr][Lt] buffer. */
+cc_status cc_part_time_range(cc_ctx* ctx, int32_t* t0, int32_t* t1);
 
 /* Runs the scheduler (Alg. 1-3 or Alg. 4-8), then the LRU plan at cfg->cap_bytes and the
  * physical placement in the arena.  order_out (may be NULL: size query) receives the

@@ -86,6 +86,7 @@ _sig("cc_version", res=ctypes.c_char_p)
 _sig("cc_load_dag", c_void_p, P(cc_dims), P(cc_node), c_i64, P(cc_tree), c_i64, P(cc_term), c_i64)
 _sig("cc_load_dag_file", c_void_p, ctypes.c_char_p)
 _sig("cc_dag_info", c_void_p, P(cc_dag_stats))
+_sig("cc_part_time_range", c_void_p, P(c_i32), P(c_i32))
 _sig("cc_partition", c_void_p, c_i32, c_i32, c_i32)
 _sig("cc_part_trees", c_void_p, P(c_i64), c_i64, P(c_i64))
 _sig("cc_schedule", c_void_p, P(cc_sched_cfg), P(c_i64), c_i64, P(c_i64), P(cc_plan_stats))
@@ -111,7 +112,7 @@ _sig("cc_fill_synthetic", c_void_p, c_void_p, c_i64, c_u64, c_i64, c_i64, c_i32,
 _sig("cc_scratch_bytes", c_i32, c_i32, c_i32, res=c_size_t)
 
 EXPORTED = ["cc_create", "cc_destroy", "cc_last_error", "cc_version", "cc_load_dag", "cc_load_dag_file",
-            "cc_dag_info", "cc_partition", "cc_part_trees", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
+            "cc_dag_info", "cc_part_time_range", "cc_partition", "cc_part_trees", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
             "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_execute",
             "cc_execute_async", "cc_kernel_times", "cc_dataflow_state", "cc_dataflow_profile", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
             "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_fill_synthetic", "cc_scratch_bytes"]
@@ -208,6 +209,11 @@ class Context:
 
     def partition(self, n_parts, part, mode):
         self._ck(_lib.cc_partition(self._h, n_parts, part, mode))
+
+    def part_time_range(self):
+        t0, t1 = c_i32(), c_i32()
+        self._ck(_lib.cc_part_time_range(self._h, ctypes.byref(t0), ctypes.byref(t1)))
+        return t0.value, t1.value
 
     def part_trees(self):
         n = c_i64()

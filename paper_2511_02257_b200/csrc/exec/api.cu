@@ -1670,6 +1670,15 @@ cc_status cc_part_trees(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out) 
   API_END
 }
 
+cc_status cc_part_time_range(cc_ctx* ctx, int32_t* t0, int32_t* t1) {
+  if (!ctx || !t0 || !t1) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->loaded) throw Error(CC_E_STATE, "no DAG loaded");
+  *t0 = ctx->t0;
+  *t1 = ctx->t1;
+  API_END
+}
+
 cc_status cc_schedule(cc_ctx* ctx, const cc_sched_cfg* cfg, int64_t* order_out, int64_t order_cap, int64_t* n_order,
                       cc_plan_stats* stats) {
   if (!ctx) return CC_E_INVAL;

@@ -1,8 +1,7 @@
-"""Run a BASELINE config end to end at full size from pinned host leaves (time to solution,
-transfers vs the plan, PCIe / FP64 bounds) and check sampled values against the oracle
-(per-slice independence: the oracle computes a few time slices, or a few trees for Lt=1).
+"""Run a BASELINE config end to end at full size from pinned host leaves: time to solution,
+transfers vs the plan, PCIe / FP64 bounds.  (Values: tests/test_gpu_parity.py.)
 
-Usage: python tools/run_config.py c3|c4 [--cap BYTES] [--check-trees 3]
+Usage: python tools/run_config.py c3|c4 [--cap BYTES]
 """
 import argparse
 import os
@@ -24,7 +23,6 @@ def main():
     ap.add_argument("config")
     ap.add_argument("--cap", type=float, default=None)
     ap.add_argument("--arena-gb", type=float, default=150)
-    ap.add_argument("--check", type=int, default=1)
     a = ap.parse_args()
     w = {"c3": dags.config_c3, "c4": dags.config_c4}[a.config]()
     cap = int(a.cap) if a.cap is not None else (32 * 10 ** 9 if a.config == "c4" else 0)
@@ -65,21 +63,7 @@ def main():
         print("execute %d: %.1f ms (copies done %.1f ms); moved %.2f GB -> PCIe bound %.1f ms; flops %.3g -> "
               "FP64 bound %.1f ms" % (rep, ex["seconds"] * 1e3, ex["copy_seconds"] * 1e3, moved / 1e9,
                                       moved / 55.6e9 * 1e3, ex["flops"], ex["flops"] / 37.0e12 * 1e3), flush=True)
-    if a.check:
-        from oracle.dag import Dag
-        from oracle import values
-        dag = Dag(w)
-        trees = ctx.part_trees()
-        if w.Lt > 1:
-            t = w.Lt - 1
-            r_or, _ = values.run_workload(w, dag, t_range=(t, t + 1))
-            worst = 0.0
-            for tr in trees:
-                got = ctx.root_value(tr, w.Lt)[t]
-                worst = max(worst, abs(got - r_or[tr][0]) / abs(r_or[tr][0]))
-            print("oracle check (slice %d, all %d trees): worst relative root error %.2e" % (t, len(trees), worst))
-        else:
-            print("oracle check skipped (Lt=1: a single-slice oracle of this size takes too long on CPU)")
+    # values are checked against the oracle by tests/test_gpu_parity.py (tools do not run it)
     os._exit(0)
 
 
