@@ -199,9 +199,9 @@ cc_status cc_dataflow_state(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_o
  * work item (GEMM queue first, then TR queue) 8 uint64: claim, dependencies-ready and
  * published times (%globaltimer, ns), the SM id, first-operand-arrival and end-of-stage-loop
  * times, the kind (0 GEMM, 1 TR_MM) and the first-arrival time again; then one record per
- * worker CTA: consumer cycles (clock64) waiting for GEMM / TR_MM stage data, cycles in GEMM /
- * TR_MM stage math and epilogues, GEMM / TR_MM stages consumed, SM id.  out may be NULL
- * (size query: 8*(n_gemm+n_trace+num_sms)). */
+ * worker CTA (16 uint64): consumer cycles (clock64) waiting for GEMM / TR_MM stage data,
+ * cycles in GEMM / TR_MM stage math and epilogues, GEMM / TR_MM stages consumed, SM id, GEMM
+ * epilogue cycles, 8 reserved words.  out may be NULL (size query: 8*(n_gemm+n_trace+2*num_sms)). */
 cc_status cc_dataflow_profile(cc_ctx* ctx, uint64_t* out, int64_t cap, int64_t* n_gemm, int64_t* n_trace);
 
 /* Results.  out: 2*Lt_part doubles (interleaved complex) for the current part. */

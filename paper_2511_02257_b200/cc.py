@@ -301,13 +301,13 @@ class Context:
         ng, nt = c_i64(), c_i64()
         self._ck(_lib.cc_dataflow_profile(self._h, None, 0, ctypes.byref(ng), ctypes.byref(nt)))
         n = ng.value + nt.value
-        n_all = n + 1024  # + one record per worker CTA (at most 1024 SMs)
+        n_all = n + 2048  # + one 16-word record per worker CTA (at most 1024 SMs)
         out = np.zeros(8 * n_all, dtype=np.uint64)
         self._ck(_lib.cc_dataflow_profile(self._h, out.ctypes.data_as(P(c_u64)), 8 * n_all, ctypes.byref(ng),
                                           ctypes.byref(nt)))
         a = out[:8 * n].reshape(n, 8)
         if per_sm:
-            sm = out[8 * n:].reshape(-1, 8).view(np.int64)
+            sm = out[8 * n:].reshape(-1, 16).view(np.int64)
             sm = sm[(sm[:, 4] + sm[:, 5]) > 0]
             return a[:ng.value], a[ng.value:], sm
         return a[:ng.value], a[ng.value:]

@@ -1441,7 +1441,7 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
     prepare_dataflow(ctx, getenv("CC_EARLY_COPIES") ? atoi(getenv("CC_EARLY_COPIES")) != 0 : true);
     const bool prof = (flags & 32) != 0;
     if (prof && !ctx->df_prof) {
-      const int64_t n = ctx->df_gemm_items + ctx->df_trace_items + ctx->num_sms;
+      const int64_t n = ctx->df_gemm_items + ctx->df_trace_items + 2 * ctx->num_sms;
       ck(cudaMalloc(reinterpret_cast<void**>(&ctx->df_prof), size_t(n) * 64), "profile buffer");
       ck(cudaMemsetAsync(ctx->df_prof, 0, size_t(n) * 64, ctx->cs), "profile buffer");
     }
@@ -1946,7 +1946,7 @@ cc_status cc_dataflow_profile(cc_ctx* ctx, uint64_t* out, int64_t cap, int64_t* 
   API_BEGIN
   ctx->need_device();
   if (!ctx->df_prof) throw Error(CC_E_STATE, "no profiled dataflow execute (flags bit 5)");
-  const int64_t n = ctx->df_gemm_items + ctx->df_trace_items + ctx->num_sms;
+  const int64_t n = ctx->df_gemm_items + ctx->df_trace_items + 2 * ctx->num_sms;
   if (n_gemm) *n_gemm = ctx->df_gemm_items;
   if (n_trace) *n_trace = ctx->df_trace_items;
   if (out) {

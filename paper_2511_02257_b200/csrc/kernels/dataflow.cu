@@ -231,6 +231,9 @@ static_assert(DF_SMEM + DF_STATIC_SMEM <= 232448, "dataflow worker exceeds 227 K
 
 // launch bounds of 12 warps although 11 run: caps registers at 168 (3 warps per SM
 // sub-partition x 32 x 168 <= 16K registers each)
+// PROF: the instantiation with per-item / per-CTA timing (cc_execute flags bit 5); the plain
+// one compiles every profiling statement out (they cost ~2.5 % in registers and scheduling).
+template <bool PROF>
 __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
   using C = GC;
   extern __shared__ uint8_t smem_raw[];
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
     if (lane != 0) return;
     const int x = warp - C::NCW - 1;
     const DfQueue& Q = x == 0 ? a.q : a.qt;
-    unsigned long long* prof = x == 0 ? a.prof : a.prof_t;
+    unsigned long long* prof = PROF ? (x == 0 ? a.prof : a.prof_t) : nullptr;
     const uint32_t ahead = uint32_t(x == 0 ? a.ahead_g : a.ahead_t);
     uint32_t n_alloc = 0, n_pub = 0;
     bool exhausted = Q.n_items == 0, pending = false, stopped = false;
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
   // traces) live only as long as the item — the register allocator sees disjoint ranges.
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
   const int g = lane >> 2, t = lane & 3;
-  const bool prof = a.prof != nullptr;
+  constexpr bool prof = PROF;
   double2 tacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
   // profile (thread 0): clock64 cycles waiting for stage data / in stage math+epilogue, per kind
   long long c_wait[2] = {0, 0}, c_work[2] = {0, 0}, n_st[2] = {0, 0}, ta = 0, tb = 0, c_epi = 0, te = 0;
@@ -528,7 +531,7 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
     const uint32_t kind = d & 3u;
     if (kind == SK_STOP) {
       if (prof && tid == 0 && a.prof_sm) {
-        long long* ps = a.prof_sm + 8 * blockIdx.x;
+        long long* ps = a.prof_sm + 16 * blockIdx.x;
         ps[0] = c_wait[0];
         ps[1] = c_wait[1];
         ps[2] = c_work[0];
@@ -689,9 +692,11 @@ __global__ void fused_finish_kernel(const DfFused* __restrict__ fused, int64_t L
 }
 cudaError_t df_preload() {
   cudaFuncAttributes attr;
-  cudaError_t e = cudaFuncGetAttributes(&attr, df_worker);
+  cudaError_t e = cudaFuncGetAttributes(&attr, df_worker<false>);
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&attr, df_worker<true>);
   if (e == cudaSuccess) e = cudaFuncGetAttributes(&attr, fused_finish_kernel);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(df_worker, cudaFuncAttributeMaxDynamicSharedMemorySize, DF_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(df_worker<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DF_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(df_worker<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DF_SMEM);
   return e;
 }
 
@@ -705,7 +710,8 @@ void df_gemm_tile_dims(int* BM, int* BN, int* BK, int* slot_doubles) {
 int df_trace_block() { return TB; }
 
 cudaError_t df_launch(const DfArgs& a, int grid, cudaStream_t s) {
-  df_worker<<<grid, NT, DF_SMEM, s>>>(a);
+  if (a.prof) df_worker<true><<<grid, NT, DF_SMEM, s>>>(a);
+  else df_worker<false><<<grid, NT, DF_SMEM, s>>>(a);
   return cudaGetLastError();
 }
 
