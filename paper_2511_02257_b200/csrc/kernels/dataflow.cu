@@ -575,17 +575,27 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
     double2* out = static_cast<double2*>(op.C) + int64_t(cur.b) * op.sCb;
     // complex results C[row0 + 8i + g][col0 + 8j + 2t + e] = gauss3m_combine(acc, i, j, e)
     if (op.n_chunks == 1) {
+      // lane (g, t) holds the adjacent complex columns 2t, 2t+1 of each 8-column block: one
+      // 32-byte store (full sectors) when the row is 32-byte aligned and both columns exist
+      const bool wide = (op.ldc & 1) == 0 && (op.sCb & 1) == 0 && (reinterpret_cast<uintptr_t>(op.C) & 31) == 0;
 #pragma unroll
       for (int i = 0; i < C::MI; ++i) {
         const int64_t row = int64_t(cur.tm) * C::BM + wm * C::WM + i * 8 + g;
         if (row >= op.M) continue;
 #pragma unroll
-        for (int j = 0; j < C::NJ; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int64_t col = int64_t(cur.tn) * C::BN + wn * C::WN + j * 8 + 2 * t + e;
-            if (col < op.Nn) out[row * op.ldc + col] = gauss3m_combine<C>(acc, i, j, e);
+        for (int j = 0; j < C::NJ; ++j) {
+          const int64_t col = int64_t(cur.tn) * C::BN + wn * C::WN + j * 8 + 2 * t;
+          const double2 v0 = gauss3m_combine<C>(acc, i, j, 0), v1 = gauss3m_combine<C>(acc, i, j, 1);
+          double2* p = out + row * op.ldc + col;
+          if (wide && col + 1 < op.Nn) {
+            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v0.x), "d"(v0.y), "d"(v1.x),
+                         "d"(v1.y)
+                         : "memory");
+          } else {
+            if (col < op.Nn) p[0] = v0;
+            if (col + 1 < op.Nn) p[1] = v1;
           }
+        }
       }
     } else {
       // publish this chunk's partial; the CTA completing the tile's last chunk sums them
