@@ -1191,7 +1191,16 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       const char* v = getenv(k);
       return std::min(std::max(v ? atoi(v) : dflt, lo), hi);
     };
-    da.tr_ratio = env_int("CC_DF_TR_RATIO", 2, 0, 64);
+    // TR_MM stages the issuer may put between GEMM k-tiles (fixed point, 1/8): by default
+    // 1.12 x the plan's trace-stage / k-tile-stage ratio, so the traces keep pace with the
+    // GEMMs (c2: 1.56 -> 1.75; measured on c2: 1.5 / 1.75 / 2 / 2.5 -> 4.45 / 4.38 / 4.43 /
+    // 4.62 ms); CC_DF_TR_RATIO overrides
+    double g_st = 0, t_st = 0;
+    for (const auto& o : gops) g_st += double(o.n_items / std::max(o.n_chunks, 1)) * o.KT;
+    for (const auto& o : tops) t_st += double(o.Lt) * o.nb * o.nb;
+    const double auto_ratio = g_st > 0 && t_st > 0 ? std::min(std::max(1.12 * t_st / g_st, 0.25), 8.0) : 2.0;
+    const char* rv = getenv("CC_DF_TR_RATIO");
+    da.tr_ratio8 = std::min(std::max(int(std::lround((rv ? atof(rv) : auto_ratio) * 8.0)), 0), 512);
     da.Lt = int32_t(Lt);
     da.ahead_g = env_int("CC_DF_AHEAD_G", 2, 1, 4);
     da.ahead_t = env_int("CC_DF_AHEAD_T", 2, 1, 4);

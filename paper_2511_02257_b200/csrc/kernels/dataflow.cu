@@ -298,8 +298,9 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
         __nanosleep(20);
         continue;
       }
-      const int x = (have[1] && (!have[0] || credit > 0)) ? 1 : 0;
-      if (have[0]) credit = x ? credit - 1 : min(credit + a.tr_ratio, 2 * a.tr_ratio);
+      // credit in 1/8 stages: a GEMM k-tile earns tr_ratio8, a TR_MM stage costs 8
+      const int x = (have[1] && (!have[0] || credit >= 8)) ? 1 : 0;
+      if (have[0]) credit = x ? credit - 8 : min(credit + a.tr_ratio8, 2 * a.tr_ratio8);
       const ItemInfo& inf = s_info[x][slot_of[x]];
       const int k = k_of[x];
       const int st = int(pos % C::STAGES);

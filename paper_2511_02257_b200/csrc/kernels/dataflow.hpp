@@ -75,7 +75,7 @@ struct DfArgs {
   unsigned long long* prof;   // optional: per GEMM item {claim, ready, end, smid, first data, loop end, kind, -}
   unsigned long long* prof_t; // optional: the same per TR_MM item
   long long* prof_sm;         // optional: per CTA {wait cycles G/T, work cycles G/T, stages G/T, smid, -}
-  int32_t tr_ratio;           // TR_MM stages the issuer may interleave per GEMM k-tile
+  int32_t tr_ratio8;          // TR_MM stages the issuer may interleave per GEMM k-tile, x 8
   int32_t ahead_g, ahead_t;   // items a CTA may hold claimed-but-unpublished per queue (<= 4)
   int32_t Lt;                 // time slices (chunked-copy targets)
 };
