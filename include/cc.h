@@ -210,6 +210,10 @@ cc_status cc_root_value(cc_ctx* ctx, int64_t tree_id, double* out, int32_t Lt);
 /* Device buffer [n_corr][Lt_part] complex128 of all correlators (corr ids ascending), for
  * a torch / NCCL all-reduce; corr_ids (may be NULL) receives the ids in buffer order. */
 cc_status cc_correlator_device_ptr(cc_ctx* ctx, void** dev_ptr, int64_t* n_corr, int64_t* corr_ids);
+/* All correlators of the current part, [n_corr][Lt_part] interleaved complex (corr ids
+ * ascending, as cc_correlator_device_ptr), into host memory `out` (cap doubles) with one copy
+ * ordered after the last execute; pinned `out` makes it a DMA. */
+cc_status cc_correlators(cc_ctx* ctx, double* out, int64_t cap);
 
 /* Kernel entry points (the contraction kernels alone; used by the element-wise parity
  * tests and the roofline measurement).  All pointers are device pointers in the layouts

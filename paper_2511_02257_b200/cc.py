@@ -87,6 +87,7 @@ _sig("cc_load_dag", c_void_p, P(cc_dims), P(cc_node), c_i64, P(cc_tree), c_i64, 
 _sig("cc_load_dag_file", c_void_p, ctypes.c_char_p)
 _sig("cc_dag_info", c_void_p, P(cc_dag_stats))
 _sig("cc_part_time_range", c_void_p, P(c_i32), P(c_i32))
+_sig("cc_correlators", c_void_p, P(c_dbl), c_i64)
 _sig("cc_partition", c_void_p, c_i32, c_i32, c_i32)
 _sig("cc_part_trees", c_void_p, P(c_i64), c_i64, P(c_i64))
 _sig("cc_schedule", c_void_p, P(cc_sched_cfg), P(c_i64), c_i64, P(c_i64), P(cc_plan_stats))
@@ -112,7 +113,7 @@ _sig("cc_fill_synthetic", c_void_p, c_void_p, c_i64, c_u64, c_i64, c_i64, c_i32,
 _sig("cc_scratch_bytes", c_i32, c_i32, c_i32, res=c_size_t)
 
 EXPORTED = ["cc_create", "cc_destroy", "cc_last_error", "cc_version", "cc_load_dag", "cc_load_dag_file",
-            "cc_dag_info", "cc_part_time_range", "cc_partition", "cc_part_trees", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
+            "cc_dag_info", "cc_part_time_range", "cc_correlators", "cc_partition", "cc_part_trees", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
             "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_execute",
             "cc_execute_async", "cc_kernel_times", "cc_dataflow_state", "cc_dataflow_profile", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
             "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_fill_synthetic", "cc_scratch_bytes"]
@@ -316,6 +317,21 @@ class Context:
         out = np.empty(2 * Lt, dtype=np.float64)
         self._ck(_lib.cc_correlator(self._h, corr_id, out.ctypes.data_as(P(c_dbl)), Lt))
         return out[0::2] + 1j * out[1::2]
+
+    def correlators(self, out=None):
+        """All correlators [n_corr, Lt_part] complex128 (corr ids ascending) with one copy; `out`
+        may be a preallocated (pinned) complex128 array / CPU tensor of that shape."""
+        n = c_i64()
+        self._ck(_lib.cc_correlator_device_ptr(self._h, None, ctypes.byref(n), None))
+        t0, t1 = self.part_time_range()
+        if out is None:
+            out = np.empty((n.value, t1 - t0), dtype=np.complex128)
+        if hasattr(out, "data_ptr"):
+            ptr, numel = out.data_ptr(), out.numel() * 2
+        else:
+            ptr, numel = out.ctypes.data, out.size * 2
+        self._ck(_lib.cc_correlators(self._h, ctypes.cast(ptr, P(c_dbl)), numel))
+        return out
 
     def root_value(self, tree_id, Lt):
         out = np.empty(2 * Lt, dtype=np.float64)

@@ -1925,6 +1925,19 @@ cc_status cc_correlator_device_ptr(cc_ctx* ctx, void** dev_ptr, int64_t* n_corr,
   API_END
 }
 
+cc_status cc_correlators(cc_ctx* ctx, double* out, int64_t cap) {
+  if (!ctx || !out) return CC_E_INVAL;
+  API_BEGIN
+  ctx->need_device();
+  if (!ctx->executed) throw Error(CC_E_STATE, "before cc_execute");
+  const Dag& g = *ctx->dag;
+  const int64_t n = int64_t(g.corr_ids.size()) * g.Lt * 2;
+  if (cap < n) throw Error(CC_E_BUFFER_TOO_SMALL, "buffer too small");
+  ck(cudaMemcpyAsync(out, ctx->corr, size_t(n) * 8, cudaMemcpyDeviceToHost, ctx->cs), "correlators D2H");
+  ck(cudaStreamSynchronize(ctx->cs), "correlators D2H");
+  API_END
+}
+
 cc_status cc_dataflow_state(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out) {
   if (!ctx) return CC_E_INVAL;
   API_BEGIN

@@ -146,6 +146,19 @@ def test_c2_small_all_modes(flags):
     assert_corr_close(dag, r_or, corr, c_or)
 
 
+def test_correlators_bulk_read():
+    """cc_correlators (one copy of every correlator) == cc_correlator per id, also on a TIME part."""
+    from paper_2511_02257_b200 import cc
+    w = dags.config_c2(N=24, Lt=4, n_loop4=30, n_loop2=4, n_corr=5)
+    for part in (None, (2, 1, cc.PART_TIME)):
+        ctx, roots, corr, st, ex = run_gpu(w, part=part)
+        allc = ctx.correlators()
+        _, n, ids = ctx.correlator_device_ptr()
+        assert allc.shape[0] == n
+        for k, c in enumerate(ids):
+            assert np.array_equal(allc[k], corr[c])
+
+
 def test_schedule_and_mode_invariance_bitwise(monkeypatch):
     """Deterministic kernels, no atomics in any reduction: root values are bit-identical run to
     run and across graph/stream mode; with trace fusion off also across schedulers and
