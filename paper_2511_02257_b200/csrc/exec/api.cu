@@ -599,6 +599,145 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   const int64_t Lt = g.Lt, N = g.N;
   const int32_t n_ops = int32_t(ops.size());
   const int64_t per_t_m = 16LL * g.N * g.N;
+  // sync slots (done counters of compute ops, flags of copies) and H2D chunk counts
+  std::vector<int32_t> slot(size_t(n_ops), -1), target(size_t(n_ops), 0), df_index(size_t(n_ops), -1);
+  int32_t n_sync = 0;
+  // CC_H2D_CHUNK_MB: H2D copies in time-slice chunks of about that size (default off: every
+  // chunk costs a stream memory operation, measured ~8 us of copy-engine idle each on B200)
+  const double chunk_mb = getenv("CC_H2D_CHUNK_MB") ? atof(getenv("CC_H2D_CHUNK_MB")) : 0.0;
+  const int64_t h2d_chunk = chunk_mb > 0 ? std::max<int64_t>(4096, int64_t(chunk_mb * 1048576.0)) : INT64_MAX;
+  for (int32_t i = 0; i < n_ops; ++i) {
+    const PhysOp& op = ops[size_t(i)];
+    if (op.stream == S_NONE) continue;
+    slot[size_t(i)] = n_sync++;
+    if (op.kind != OP_CONTRACT) {
+      // consumers of a copy in C > 1 time-slice chunks wait only for the chunk holding their
+      // slice (target -C); else the flag reaches 1
+      target[size_t(i)] = 1;
+      if (op.kind == OP_H2D && op.stream == S_H2D && Lt > 1 && op.bytes % Lt == 0) {
+        const int64_t C = std::min<int64_t>(Lt, std::max<int64_t>(1, op.bytes / h2d_chunk + (op.bytes % h2d_chunk != 0)));
+        if (C > 1) target[size_t(i)] = -int32_t(C);
+      }
+    }
+  }
+  // The sync area (2 queue heads + n_sync ints), zeroed before every launch, sits at the top
+  // of the pool (above the plan's high-water mark); the rest of the metadata goes below it.
+  const size_t sz_sync = round_up(16 + int64_t(n_sync) * 4, 256);
+  {
+    const int64_t sync_off = (ctx->pool_bytes - int64_t(sz_sync)) / 256 * 256;
+    if (sync_off < ctx->pp.pool_high_water) throw Error(CC_E_NOMEM, "arena too small for the dataflow sync area");
+    ctx->df_sync_base = ctx->arena + sync_off;
+    ctx->df_sync = reinterpret_cast<int*>(ctx->df_sync_base + 16);
+    ctx->df_sync_bytes = sz_sync;
+  }
+  // 0b. early H2D copies.  A leaf H2D whose device range lies above everything the plan
+  // touched before it (fresh pool memory) waits on nothing and nothing earlier depends on it:
+  // it may be issued first, before the dependency analysis, so the copy engine starts while
+  // the host builds the rest.  These copies are ordered greedily by the work they enable:
+  // next = the leaf that completes the leaf set (closure in the DAG) of the most estimated
+  // compute time, so the GEMMs — most of the step — start early and little is left once the
+  // last leaf lands.  CC_COPY_REORDER=0 keeps plan order.
+  std::vector<int32_t> early_seq;
+  std::vector<uint8_t> is_early(size_t(n_ops), 0);
+  {
+    int64_t touched_end = 0;
+    auto touch = [&](int64_t off, int64_t bytes) {
+      if (off >= 0) touched_end = std::max(touched_end, off + bytes);
+    };
+    for (int32_t i = 0; i < n_ops; ++i) {
+      const PhysOp& op = ops[size_t(i)];
+      const Node& n = g.nodes[size_t(op.node)];
+      const int64_t rb = round_up(n.size, ALIGN);
+      if (op.kind == OP_H2D && op.stream == S_H2D && n.leaf() && op.dev_off >= touched_end) {
+        is_early[size_t(i)] = 1;
+        early_seq.push_back(i);
+      }
+      if (op.kind == OP_H2D || op.kind == OP_D2H) touch(op.dev_off, rb);
+      if (op.kind == OP_CONTRACT) {
+        if (op.loc_a == LOC_POOL) touch(op.off_a, round_up(g.nodes[size_t(n.l)].size, ALIGN));
+        if (op.loc_b == LOC_POOL) touch(op.off_b, round_up(g.nodes[size_t(n.r)].size, ALIGN));
+        touch(op.dev_off, rb);
+      }
+    }
+    const int reorder = getenv("CC_COPY_REORDER") ? atoi(getenv("CC_COPY_REORDER")) : 1;
+    if (reorder && early_seq.size() > 1) {
+      // leaf closure of every contraction (memoised over nodes), restricted to early leaves
+      std::vector<int32_t> early_of_node(g.nodes.size(), -1);
+      for (size_t k = 0; k < early_seq.size(); ++k) early_of_node[size_t(ops[size_t(early_seq[k])].node)] = int32_t(k);
+      std::vector<std::vector<int32_t>> leaves(g.nodes.size());
+      std::vector<uint8_t> blocked(g.nodes.size(), 0);   // needs a leaf that is not early
+      for (int32_t u : g.topo) {
+        const Node& n = g.nodes[size_t(u)];
+        if (n.leaf()) {
+          if (early_of_node[size_t(u)] >= 0) leaves[size_t(u)] = {early_of_node[size_t(u)]};
+          else blocked[size_t(u)] = 1;
+          continue;
+        }
+        auto& v = leaves[size_t(u)];
+        v = leaves[size_t(n.l)];
+        v.insert(v.end(), leaves[size_t(n.r)].begin(), leaves[size_t(n.r)].end());
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        blocked[size_t(u)] = blocked[size_t(n.l)] | blocked[size_t(n.r)];
+      }
+      std::vector<int32_t> contr;
+      std::vector<double> cost;
+      for (int32_t i = 0; i < n_ops; ++i) {
+        const PhysOp& op = ops[size_t(i)];
+        if (op.kind != OP_CONTRACT || blocked[size_t(op.node)]) continue;
+        const Node& n = g.nodes[size_t(op.node)];
+        contr.push_back(op.node);
+        cost.push_back(node_flops(n, g.Lt, g.N, g.S) / 37e12 + node_hbm_bytes(n, g.Lt, g.N, g.S) / 6.5e12);
+      }
+      const size_t ne = early_seq.size();
+      std::vector<std::vector<int32_t>> users(ne);
+      std::vector<int32_t> missing(contr.size());
+      for (size_t c = 0; c < contr.size(); ++c) {
+        missing[c] = int32_t(leaves[size_t(contr[c])].size());
+        for (int32_t e : leaves[size_t(contr[c])]) users[size_t(e)].push_back(int32_t(c));
+      }
+      std::vector<double> score(ne, 0.0);
+      for (size_t e = 0; e < ne; ++e)
+        for (int32_t c : users[e])
+          if (missing[size_t(c)] == 1) score[e] += cost[size_t(c)];
+      std::vector<uint8_t> taken(ne, 0);
+      std::vector<int32_t> out;
+      for (size_t step = 0; step < ne; ++step) {
+        size_t best = ne;
+        for (size_t e = 0; e < ne; ++e)
+          if (!taken[e] && (best == ne || score[e] > score[best])) best = e;
+        taken[best] = 1;
+        out.push_back(early_seq[best]);
+        for (int32_t c : users[best]) {
+          if (--missing[size_t(c)] == 1)
+            for (int32_t e : leaves[size_t(contr[size_t(c)])])
+              if (!taken[size_t(e)]) score[size_t(e)] += cost[size_t(c)];
+        }
+      }
+      early_seq.swap(out);
+    }
+  }
+  // early copies: zero the sync area on the H2D stream, then start the early copies, each
+  // followed by its flag write, so they overlap the rest of the host-side preparation; the
+  // compute stream waits for the zeroing only.
+  ctx->df_early.assign(size_t(n_ops), 0);
+  ctx->df_early_active = false;
+  if (early && !early_seq.empty()) {
+    ck(cudaEventRecord(ctx->ev_pre, ctx->cs), "event");        // after all earlier work on cs
+    ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_pre, 0), "wait");
+    ck(cudaMemsetAsync(ctx->df_sync_base, 0, sz_sync, ctx->hs), "memset");
+    ck(cudaEventRecord(ctx->ev_pre, ctx->hs), "event");
+    ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_pre, 0), "wait");
+    for (int32_t i : early_seq) {
+      const PhysOp& op = ops[size_t(i)];
+      const auto ep = copy_endpoints(ctx, op);
+      enqueue_copy(ctx, ctx->hs, ep.first, ep.second, size_t(op.bytes), cudaMemcpyHostToDevice,
+                   target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
+      ctx->df_early[size_t(i)] = 1;
+    }
+    ctx->df_early_active = true;
+  }
+  tmr.lap("early copies");
   // 1. data dependencies over the device pool and the host pool
   RWTracker dev(ctx->pool_bytes), host(std::max<int64_t>(ctx->pp.host_pool_bytes, 1));
   std::vector<std::vector<int32_t>> deps(static_cast<size_t>(n_ops));
@@ -672,146 +811,18 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
     }
   }
   tmr.lap("rw deps");
-  // 1b. copy issue order per stream (plan op indices).  A copy stream runs its copies in
-  // order.  Within a run of H2D copies that wait on nothing (fresh pool memory), the copies
-  // may be reordered without risking a deadlock (a wait-free copy blocks on nothing, so
-  // moving it earlier only completes it sooner for whoever needs it; the run's end — a copy
-  // that waits — keeps its place).  The run is ordered greedily by the work it enables: next
-  // = the copy that completes the input set (transitively, through compute ops) of the most
-  // estimated compute time, so the GEMMs — most of the step — can start early and the work
-  // left after the last copy lands is small.  CC_COPY_REORDER=0 keeps plan order.
+  // 1b. copy issue order per stream: the early H2D copies (chosen and possibly already
+  // enqueued in step 0) first, in their order, then the other copies in plan order.
   std::vector<int32_t> copy_seq[3];
   std::vector<int64_t> copy_pos(size_t(n_ops), 0);   // H2D issue position (0 for non-copies)
   {
-    for (int32_t i = 0; i < n_ops; ++i)
-      if (ops[size_t(i)].stream == S_H2D || ops[size_t(i)].stream == S_D2H)
-        copy_seq[ops[size_t(i)].stream].push_back(i);
-    const int reorder = getenv("CC_COPY_REORDER") ? atoi(getenv("CC_COPY_REORDER")) : 1;
-    auto& h = copy_seq[S_H2D];
-    if (reorder && h.size() > 1) {
-      // weight of op i towards a missing input while m inputs are missing: mode 1 counts
-      // only ops completed by the copy (m == 1); mode 2 spreads cost / m^2 over the missing
-      // inputs, so a copy also earns credit for bringing trees (root traces need four
-      // leaves) closer to completion
-      auto w = [&](int32_t m) { return m <= 0 ? 0.0 : (reorder == 1 ? (m == 1 ? 1.0 : 0.0) : 1.0 / (double(m) * m)); };
-      // leaf-copy inputs of every compute op (transitively), and its estimated time
-      std::vector<std::vector<int32_t>> need(static_cast<size_t>(n_ops));
-      std::vector<double> cost(size_t(n_ops), 0.0);
-      const double tr_weight = getenv("CC_COPY_TR_WEIGHT") ? atof(getenv("CC_COPY_TR_WEIGHT")) : 1.0;
-      for (int32_t i = 0; i < n_ops; ++i) {
-        const PhysOp& op = ops[size_t(i)];
-        if (op.kind != OP_CONTRACT) continue;
-        const Node& n = g.nodes[size_t(op.node)];
-        cost[size_t(i)] = node_flops(n, g.Lt, g.N, g.S) / 37e12 + node_hbm_bytes(n, g.Lt, g.N, g.S) / 6.5e12;
-        if (n.op == CC_TR_MM) cost[size_t(i)] *= tr_weight;
-        auto& v = need[size_t(i)];
-        for (int32_t j : deps[size_t(i)]) {
-          const PhysOp& oj = ops[size_t(j)];
-          if (oj.stream == S_H2D) v.push_back(j);
-          else if (oj.kind == OP_CONTRACT) v.insert(v.end(), need[size_t(j)].begin(), need[size_t(j)].end());
-        }
-        std::sort(v.begin(), v.end());
-        v.erase(std::unique(v.begin(), v.end()), v.end());
-      }
-      std::vector<std::vector<int32_t>> users(static_cast<size_t>(n_ops));
-      for (int32_t i = 0; i < n_ops; ++i)
-        for (int32_t j : need[size_t(i)]) users[size_t(j)].push_back(i);
-      std::vector<int32_t> missing(size_t(n_ops), 0);
-      for (int32_t i = 0; i < n_ops; ++i) missing[size_t(i)] = int32_t(need[size_t(i)].size());
-      std::vector<uint8_t> loaded(size_t(n_ops), 0);
-      auto wait_free = [&](int32_t i) { return deps[size_t(i)].empty(); };
-      // copies issued before a run count as loaded when the run is ordered
-      size_t a = 0;
-      while (a < h.size()) {
-        size_t b = a;
-        while (b < h.size() && wait_free(h[b])) ++b;
-        // greedy over h[a, b): score(c) = time of ops whose only missing input is c
-        std::vector<int32_t> run(h.begin() + int64_t(a), h.begin() + int64_t(b)), out;
-        std::vector<double> score(size_t(n_ops), 0.0);
-        std::vector<uint8_t> in_run(size_t(n_ops), 0);
-        for (int32_t c : run) in_run[size_t(c)] = 1;
-        for (int32_t c : run)
-          for (int32_t i : users[size_t(c)]) score[size_t(c)] += cost[size_t(i)] * w(missing[size_t(i)]);
-        std::vector<uint8_t> taken(run.size(), 0);
-        for (size_t step = 0; step < run.size(); ++step) {
-          size_t best = run.size();
-          for (size_t q = 0; q < run.size(); ++q)
-            if (!taken[q] && (best == run.size() || score[size_t(run[q])] > score[size_t(run[best])])) best = q;
-          taken[best] = 1;
-          const int32_t c = run[best];
-          out.push_back(c);
-          loaded[size_t(c)] = 1;
-          for (int32_t i : users[size_t(c)]) {
-            const int32_t m = missing[size_t(i)]--;
-            const double d = cost[size_t(i)] * (w(m - 1) - w(m));
-            if (d != 0.0)
-              for (int32_t j : need[size_t(i)])
-                if (!loaded[size_t(j)] && in_run[size_t(j)]) score[size_t(j)] += d;
-          }
-        }
-        std::copy(out.begin(), out.end(), h.begin() + int64_t(a));
-        // the run's closing copy (waits on something) keeps its place
-        if (b < h.size()) {
-          const int32_t c = h[b];
-          loaded[size_t(c)] = 1;
-          for (int32_t i : users[size_t(c)]) --missing[size_t(i)];
-        }
-        a = b + 1;
-      }
+    copy_seq[S_H2D] = early_seq;
+    for (int32_t i = 0; i < n_ops; ++i) {
+      const int st = ops[size_t(i)].stream;
+      if ((st == S_H2D && !is_early[size_t(i)]) || st == S_D2H) copy_seq[st].push_back(i);
     }
+    const auto& h = copy_seq[S_H2D];
     for (size_t k = 0; k < h.size(); ++k) copy_pos[size_t(h[k])] = int64_t(k) + 1;
-  }
-  // sync slots (done counters of compute ops, flags of copies) and H2D chunk counts
-  std::vector<int32_t> slot(size_t(n_ops), -1), target(size_t(n_ops), 0), df_index(size_t(n_ops), -1);
-  int32_t n_sync = 0;
-  // CC_H2D_CHUNK_MB: H2D copies in time-slice chunks of about that size (default off: every
-  // chunk costs a stream memory operation, measured ~8 us of copy-engine idle each on B200)
-  const double chunk_mb = getenv("CC_H2D_CHUNK_MB") ? atof(getenv("CC_H2D_CHUNK_MB")) : 0.0;
-  const int64_t h2d_chunk = chunk_mb > 0 ? std::max<int64_t>(4096, int64_t(chunk_mb * 1048576.0)) : INT64_MAX;
-  for (int32_t i = 0; i < n_ops; ++i) {
-    const PhysOp& op = ops[size_t(i)];
-    if (op.stream == S_NONE) continue;
-    slot[size_t(i)] = n_sync++;
-    if (op.kind != OP_CONTRACT) {
-      // consumers of a copy in C > 1 time-slice chunks wait only for the chunk holding their
-      // slice (target -C); else the flag reaches 1
-      target[size_t(i)] = 1;
-      if (op.kind == OP_H2D && op.stream == S_H2D && Lt > 1 && op.bytes % Lt == 0) {
-        const int64_t C = std::min<int64_t>(Lt, std::max<int64_t>(1, op.bytes / h2d_chunk + (op.bytes % h2d_chunk != 0)));
-        if (C > 1) target[size_t(i)] = -int32_t(C);
-      }
-    }
-  }
-  // The sync area (2 queue heads + n_sync ints), zeroed before every launch, sits at the top
-  // of the pool (above the plan's high-water mark); the rest of the metadata goes below it.
-  const size_t sz_sync = round_up(16 + int64_t(n_sync) * 4, 256);
-  {
-    const int64_t sync_off = (ctx->pool_bytes - int64_t(sz_sync)) / 256 * 256;
-    if (sync_off < ctx->pp.pool_high_water) throw Error(CC_E_NOMEM, "arena too small for the dataflow sync area");
-    ctx->df_sync_base = ctx->arena + sync_off;
-    ctx->df_sync = reinterpret_cast<int*>(ctx->df_sync_base + 16);
-    ctx->df_sync_bytes = sz_sync;
-  }
-  // early copies: zero the sync area on the H2D stream, then start the wait-free H2D copies at
-  // the head of the copy order, each followed by its flag write, so they overlap the rest of
-  // the host-side preparation; the compute stream waits for the zeroing only.
-  ctx->df_early.assign(size_t(n_ops), 0);
-  ctx->df_early_active = false;
-  if (early && !copy_seq[S_H2D].empty() && deps[size_t(copy_seq[S_H2D][0])].empty()) {
-    ck(cudaEventRecord(ctx->ev_pre, ctx->cs), "event");        // after all earlier work on cs
-    ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_pre, 0), "wait");
-    ck(cudaMemsetAsync(ctx->df_sync_base, 0, sz_sync, ctx->hs), "memset");
-    ck(cudaEventRecord(ctx->ev_pre, ctx->hs), "event");
-    ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_pre, 0), "wait");
-    for (int32_t i : copy_seq[S_H2D]) {
-      if (!deps[size_t(i)].empty()) break;
-      const PhysOp& op = ops[size_t(i)];
-      const auto ep = copy_endpoints(ctx, op);
-      enqueue_copy(ctx, ctx->hs, ep.first, ep.second, size_t(op.bytes), cudaMemcpyHostToDevice,
-                   target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
-      ctx->df_early[size_t(i)] = 1;
-    }
-    ctx->df_early_active = true;
   }
   // 2. work items
   std::vector<DfOp> gops, tops;
