@@ -25,7 +25,8 @@ def _sources():
 
 
 def _headers():
-    return glob.glob(os.path.join(CSRC, "**", "*.hpp"), recursive=True) + [os.path.join(ROOT, "include", "cc.h")]
+    return glob.glob(os.path.join(CSRC, "**", "*.hpp"), recursive=True) + \
+        glob.glob(os.path.join(CSRC, "**", "*.cuh"), recursive=True) + [os.path.join(ROOT, "include", "cc.h")]
 
 
 def _compile(src, hdr_mtime):

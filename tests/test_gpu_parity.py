@@ -333,3 +333,55 @@ def test_stream_k_repeatable_bitwise(ctx):
         g1, g2 = to_numpy_c(C1, shape), to_numpy_c(C2, shape)
         assert np.array_equal(g1, g2)
         assert np.all(np.abs(g1 - want) <= 1e-13 * scale)
+
+
+def _oracle_tree_roots(w, dag, tree_ids, t):
+    """Oracle roots of the given trees at time slice t only (their sub-DAGs, per-slice
+    independence is exact)."""
+    ops = {u: n.op for u, n in dag.nodes.items()}
+    memo = {}
+
+    def val(u):
+        if u not in memo:
+            n = dag.nodes[u]
+            if not n.child:
+                memo[u] = values.synthetic_leaf(w, u, ops[u], (t, t + 1))
+            else:
+                memo[u] = values.KERNELS[n.op](val(n.child[0]), val(n.child[1]))
+        return memo[u]
+    return {tr: val(dag.trees[tr][0]) for tr in tree_ids}
+
+
+@pytest.mark.parametrize("N,n_pairs,n_trees", [(256, 120, 600), (512, 60, 200), (1024, 24, 60)])
+def test_c5_large_N_time_part(N, n_pairs, n_trees):
+    """c5 (MxM sweep, Lt=128) at N = 256 / 512 / 1024 as one rank's TIME part of an 8-GPU run
+    (16 slices), leaves generated on the device by the bit-exact generator, bench launch
+    configuration (graph replay); the oracle computes sampled trees at two of the part's slices."""
+    from paper_2511_02257_b200 import cc
+    w = dags.config_c5(N=N, Lt=128, n_pairs=n_pairs, n_trees=n_trees, n_corr=8)
+    dag = Dag(w)
+    arena = torch.empty(96 << 30, dtype=torch.uint8, device="cuda")
+    ctx = cc.Context(0, arena)
+    ctx.load_workload(w)
+    ctx.partition(8, 5, cc.PART_TIME)
+    t0, t1 = ctx.part_time_range()
+    order, st = ctx.schedule(cc.CC_TREE)
+    keep = []
+    for u, n in dag.nodes.items():
+        if n.child:
+            continue
+        per_t = N * N
+        d = torch.empty(2 * (t1 - t0) * per_t, dtype=torch.float64, device="cuda")
+        ctx.fill_synthetic(d, (t1 - t0) * per_t, w.data_seed, u, t0 * per_t, w.leaf_mode, srng.meson_sigma(N))
+        keep.append(d)
+        ctx.set_leaf_device(u, d)
+    ctx.execute(1)
+    ctx.execute(1)
+    trees = ctx.part_trees()
+    sample = trees[:: max(1, len(trees) // 6)][:6]
+    for t in (t0, t1 - 1):
+        want = _oracle_tree_roots(w, dag, sample, t)
+        got = {tr: ctx.root_value(tr, t1 - t0)[t - t0:t - t0 + 1] for tr in sample}
+        assert_roots_close(got, want)
+    del arena
+    torch.cuda.empty_cache()

@@ -1,7 +1,9 @@
 """Run a BASELINE config end to end at full size from pinned host leaves: time to solution,
 transfers vs the plan, PCIe / FP64 bounds.  (Values: tests/test_gpu_parity.py.)
 
-Usage: python tools/run_config.py c3|c4 [--cap BYTES]
+Usage: python tools/run_config.py c3|c4|c5 [--cap BYTES] [--N N] [--parts P --part p] [--device-leaves]
+c5 at N=512/1024 runs one rank's TIME part of the 8-GPU partition (--parts 8) with device-resident
+leaves (the full pinned host set would be 32 / 128 GiB).
 """
 import argparse
 import os
@@ -23,8 +25,12 @@ def main():
     ap.add_argument("config")
     ap.add_argument("--cap", type=float, default=None)
     ap.add_argument("--arena-gb", type=float, default=150)
+    ap.add_argument("--N", type=int, default=256)
+    ap.add_argument("--parts", type=int, default=1)
+    ap.add_argument("--part", type=int, default=0)
+    ap.add_argument("--device-leaves", action="store_true")
     a = ap.parse_args()
-    w = {"c3": dags.config_c3, "c4": dags.config_c4}[a.config]()
+    w = {"c3": dags.config_c3, "c4": dags.config_c4, "c5": lambda: dags.config_c5(N=a.N)}[a.config]()
     cap = int(a.cap) if a.cap is not None else (32 * 10 ** 9 if a.config == "c4" else 0)
     dev = torch.device("cuda:0")
     streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
@@ -32,6 +38,9 @@ def main():
     ctx = cc.Context(0, arena, streams=streams)
     t0 = time.perf_counter()
     ctx.load_workload(w)
+    if a.parts > 1:
+        ctx.partition(a.parts, a.part, cc.PART_TIME)
+    pt0, pt1 = ctx.part_time_range()
     order, st = ctx.schedule(cc.CC_TREE, cap_bytes=cap)
     t1 = time.perf_counter()
     print("%s: %d contractions, plan peak %.2f GB transient %.2f GB, evictions %d, H2D %.2f GB D2H %.2f GB, "
@@ -44,6 +53,13 @@ def main():
         if n[1] not in (dags.LEAF_M, dags.LEAF_B):
             continue
         shape = bench.leaf_shape(w, n[1])
+        if a.device_leaves:
+            per_t = int(np.prod(shape[1:]))
+            d = torch.empty(2 * (pt1 - pt0) * per_t, dtype=torch.float64, device=dev)
+            ctx.fill_synthetic(d, (pt1 - pt0) * per_t, w.data_seed, n[0], pt0 * per_t, w.leaf_mode,
+                               bench.leaf_sigma(w, n[1]))
+            host[n[0]] = d
+            continue
         cnt = int(np.prod(shape))
         if tmp is None or tmp.numel() < 2 * cnt:
             tmp = torch.empty(2 * cnt, dtype=torch.float64, device=dev)
@@ -56,7 +72,11 @@ def main():
     del tmp
     torch.cuda.synchronize()
     for u, h in host.items():
-        ctx.set_leaf(u, h)
+        if a.device_leaves:
+            ctx.set_leaf_device(u, h)
+        else:
+            ctx.set_leaf(u, h)
+    print("part %d/%d: time slices [%d, %d), %d trees" % (a.part, a.parts, pt0, pt1, len(ctx.part_trees())), flush=True)
     for rep in range(2):
         ex = ctx.execute(0)
         moved = ex["h2d_bytes"] + ex["d2h_bytes"]
