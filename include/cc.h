@@ -222,6 +222,22 @@ cc_status cc_mm1(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt,
 cc_status cc_bm1(cc_ctx* ctx, const void* A, const void* M, void* C, int32_t Lt, int32_t N, int32_t S);
 cc_status cc_bb2(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt, int32_t N, int32_t S);
 cc_status cc_tr_mm(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t Lt, int32_t N);
+/* MM1 on the tcgen05 INT8 tensor cores by Ozaki splitting (DESIGN reading
+ * V-6).  Same operation and layouts as cc_mm1 (C[t,i,k] = sum_j A[t,i,j] B[t,j,k], complex128
+ * interleaved, [Lt][N][N], device pointers).  Each operand is split into n_slices (4..8) INT8
+ * slices of 7 bits under a per-row (A) / per-column (B) power-of-two scale; the pairs (i, j)
+ * with i + j <= n_slices - 1 are multiplied exactly (INT32 accumulation in TMEM) and summed in
+ * FP64, so |C - AB| <= ~(n_slices + 2) 2^(4 - 7 n_slices) sum_j |A[i,:]|max |B[:,k]|max.
+ * workspace: caller-owned device memory of cc_mm1_ozaki_workspace_bytes(Lt, N, n_slices) bytes
+ * (0 = invalid arguments).  Runs on the ctx compute stream, does not synchronise.  Errors:
+ * CC_E_INVAL (bad sizes / null pointers, N > 8192), CC_E_BUFFER_TOO_SMALL, CC_E_CUDA. */
+size_t cc_mm1_ozaki_workspace_bytes(int32_t Lt, int32_t N, int32_t n_slices);
+cc_status cc_mm1_ozaki(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt, int32_t N, int32_t n_slices,
+                       void* workspace, size_t workspace_bytes);
+/* The INT8 tcgen05 GEMM alone (pins the UMMA descriptors bit-exactly in the tests):
+ * C[m][n] = sum_k A[m][k] B[n][k]; A int8 [M][K], B int8 [Nn][K] row-major, C int32 [M][Nn];
+ * M % 128 == 0, Nn % 64 == 0, K % 64 == 0, K <= 2^17 (no INT32 overflow). */
+cc_status cc_i8gemm_tn(cc_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C, int32_t M, int32_t Nn, int32_t K);
 /* Synthetic leaf values (input generation, not the method; same recipe as synth/rng.py):
  * n complex elements starting at flat element e0 of leaf `leaf_id`, written to dev. */
 cc_status cc_fill_synthetic(cc_ctx* ctx, void* dev, int64_t n, uint64_t seed, int64_t leaf_id,

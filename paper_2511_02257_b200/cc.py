@@ -109,6 +109,9 @@ _sig("cc_mm1", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32)
 _sig("cc_bm1", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32)
 _sig("cc_bb2", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32)
 _sig("cc_tr_mm", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32)
+_sig("cc_mm1_ozaki", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, c_void_p, ctypes.c_size_t)
+_sig("cc_mm1_ozaki_workspace_bytes", c_i32, c_i32, c_i32, res=ctypes.c_size_t)
+_sig("cc_i8gemm_tn", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32)
 _sig("cc_fill_synthetic", c_void_p, c_void_p, c_i64, c_u64, c_i64, c_i64, c_i32, c_dbl)
 _sig("cc_scratch_bytes", c_i32, c_i32, c_i32, res=c_size_t)
 
@@ -116,7 +119,7 @@ EXPORTED = ["cc_create", "cc_destroy", "cc_last_error", "cc_version", "cc_load_d
             "cc_dag_info", "cc_part_time_range", "cc_correlators", "cc_partition", "cc_part_trees", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
             "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_execute",
             "cc_execute_async", "cc_kernel_times", "cc_dataflow_state", "cc_dataflow_profile", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
-            "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_fill_synthetic", "cc_scratch_bytes"]
+            "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_mm1_ozaki", "cc_mm1_ozaki_workspace_bytes", "cc_i8gemm_tn", "cc_fill_synthetic", "cc_scratch_bytes"]
 
 
 class CCError(RuntimeError):
@@ -145,6 +148,10 @@ def cc_version():
 
 def cc_scratch_bytes(Lt, N, S):
     return int(_lib.cc_scratch_bytes(Lt, N, S))
+
+
+def cc_mm1_ozaki_workspace_bytes(Lt, N, n_slices):
+    return int(_lib.cc_mm1_ozaki_workspace_bytes(Lt, N, n_slices))
 
 
 class Context:
@@ -355,6 +362,13 @@ class Context:
 
     def bb2(self, A, B, C, Lt, N, S):
         self._ck(_lib.cc_bb2(self._h, _ptr(A), _ptr(B), _ptr(C), Lt, N, S))
+
+    def mm1_ozaki(self, A, B, C, Lt, N, n_slices, workspace):
+        self._ck(_lib.cc_mm1_ozaki(self._h, _ptr(A), _ptr(B), _ptr(C), Lt, N, n_slices, _ptr(workspace),
+                                   workspace.numel() * workspace.element_size()))
+
+    def i8gemm_tn(self, A, B, C, M, Nn, K):
+        self._ck(_lib.cc_i8gemm_tn(self._h, _ptr(A), _ptr(B), _ptr(C), M, Nn, K))
 
     def tr_mm(self, A, B, c, Lt, N):
         self._ck(_lib.cc_tr_mm(self._h, _ptr(A), _ptr(B), _ptr(c), Lt, N))

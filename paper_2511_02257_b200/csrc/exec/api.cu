@@ -2035,6 +2035,34 @@ cc_status cc_tr_mm(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t L
   API_END
 }
 
+size_t cc_mm1_ozaki_workspace_bytes(int32_t Lt, int32_t N, int32_t n_slices) {
+  if (Lt <= 0 || N <= 0 || n_slices < 4 || n_slices > 8) return 0;
+  return ozaki_mm1_workspace_bytes(Lt, N, n_slices);
+}
+
+cc_status cc_mm1_ozaki(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt, int32_t N, int32_t n_slices,
+                       void* workspace, size_t workspace_bytes) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  ctx->need_device();
+  if (!A || !B || !C || !workspace || Lt <= 0 || N <= 0 || N > 8192 || n_slices < 4 || n_slices > 8)
+    throw Error(CC_E_INVAL, "bad kernel arguments");
+  if (workspace_bytes < ozaki_mm1_workspace_bytes(Lt, N, n_slices))
+    throw Error(CC_E_BUFFER_TOO_SMALL, "ozaki workspace too small");
+  ck(launch_ozaki_mm1(A, B, C, Lt, N, n_slices, workspace, workspace_bytes, ctx->cs), "Ozaki MM1");
+  API_END
+}
+
+cc_status cc_i8gemm_tn(cc_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C, int32_t M, int32_t Nn, int32_t K) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  ctx->need_device();
+  if (!A || !B || !C || M <= 0 || Nn <= 0 || K <= 0 || M % 128 || Nn % 64 || K % 64)
+    throw Error(CC_E_INVAL, "bad kernel arguments (M % 128, Nn % 64, K % 64)");
+  ck(launch_i8gemm_tn(A, B, C, M, Nn, K, ctx->cs), "int8 tcgen05 GEMM");
+  API_END
+}
+
 cc_status cc_fill_synthetic(cc_ctx* ctx, void* dev, int64_t n, uint64_t seed, int64_t leaf_id, int64_t e0, int32_t mode,
                             double sigma) {
   if (!ctx) return CC_E_INVAL;

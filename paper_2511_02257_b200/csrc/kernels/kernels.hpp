@@ -51,6 +51,15 @@ cudaError_t launch_upload(void* dst, const void* src_pinned, size_t bytes, int n
 cudaError_t zgemm_preload();
 cudaError_t trace_preload();
 
+// MM1 by Ozaki splitting on tcgen05 INT8 tensor cores (ozaki.cu): C[t] = A[t] B[t], complex128
+// [Lt][N][N], n_slices in 4..8 INT8 slices per operand; workspace holds the slices + scales.
+size_t ozaki_mm1_workspace_bytes(int64_t Lt, int64_t N, int slices);
+cudaError_t launch_ozaki_mm1(const void* A, const void* B, void* C, int64_t Lt, int64_t N, int slices, void* ws,
+                             size_t ws_bytes, cudaStream_t stream);
+// Plain INT8 GEMM on the same tcgen05 machinery: C[m][n] = sum_k A[m][k] B[n][k] (int32).
+cudaError_t launch_i8gemm_tn(const int8_t* A, const int8_t* B, int32_t* C, int64_t M, int64_t Nn, int64_t K,
+                             cudaStream_t stream);
+
 // Synthetic leaf values (input generation; same recipe as synth/rng.py).
 cudaError_t launch_fill_synthetic(void* dev, int64_t n, uint64_t seed, int64_t leaf_id, int64_t e0, int mode,
                                   double sigma, cudaStream_t stream);

@@ -1,0 +1,492 @@
+// MM1 on the 5th-generation tensor cores: complex-double C = A B per time slice by Ozaki
+// splitting into INT8 slices, tcgen05.mma kind::i8 with INT32 accumulators in TMEM, and an
+// FP64 epilogue (reading V-6 in DESIGN.md).
+//
+// Why: sm_100a has no tcgen05 f64 kind (probed), so FP64 DMMA caps MM1 at 37 TF/s.  An INT8
+// tcgen05 MMA is exact (integer products, INT32 accumulation), so a product of s-slice
+// splittings reproduces the FP64 product to ~2^-7s relative to the row/column scale.
+//
+// Splitting (per time slice t):
+//   A_cat = [Ar | Ai]              (N x 2N, row i scaled by 2^-eA[i], eA = max-exponent of row i)
+//   B_cat = [[Br, Bi], [-Bi, Br]]  (2N x 2N, column c scaled by 2^-fB[c])
+//   so that A_cat B_cat = [Cr | Ci]  (the real embedding of the complex product, 4M form)
+//   x * 2^-e = sum_{k=0}^{s-1} 2^{-7(k+1)} x_k + r,  x_k in [-127, 127] (truncation, exact in
+//   FP64), |r| < 2^-7s.
+//   C ~= 2^{eA+fB} sum_{i+j <= s-1} 2^{-7(i+j+2)} (A_i B_j)      (pairs below the anti-diagonal
+//   cut are dropped, the standard Ozaki truncation)
+// Every (i, j) with i + j = d accumulates into one INT32 TMEM accumulator d (|acc| <= s 127^2 K
+// < 2^31 for K = 2N <= 2^14), so the epilogue sees s accumulators per output, converts each
+// exactly to FP64 and sums them from the least significant one up.
+//
+// Layouts (device workspace, caller-owned):
+//   SA int8 [s][Lt][Mp][Kp]   K-major rows of A_cat, Mp = roundup(N,128), Kp = 2 Nc,
+//                             Nc = roundup(N,32); K index: Re part at j, Im part at Nc + j
+//   SB int8 [s][Lt][2Nc][Kp]  K-major rows of B_cat^T; rows grouped per 32 output columns:
+//                             row 64g + w, w < 32 -> Cr column 32g + w, w >= 32 -> Ci column
+//   eA int32 [Lt][Mp], fB int32 [Lt][Nc]
+// GEMM CTA: 128 rows x (32 complex output columns = 64 B_cat^T rows), K streamed in 64-byte
+// stages (SWIZZLE_64B TMA boxes, all s slices of A and B per stage), one lane issues the
+// tcgen05.mma's, 4 warps drain TMEM.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace cc {
+namespace oz {
+
+constexpr int BM = 128;     // CTA rows (UMMA M)
+constexpr int BN = 64;      // CTA B_cat^T rows (UMMA N) = 32 complex output columns
+constexpr int BKB = 64;     // K bytes per stage (one SWIZZLE_64B row)
+constexpr int UK = 32;      // K per kind::i8 MMA
+constexpr int A_TILE = BM * BKB;    // 8 KB
+constexpr int B_TILE = BN * BKB;    // 4 KB
+constexpr int SMEM_BUDGET = 222 * 1024;
+
+template <int S>
+struct Cfg {
+  static constexpr int STAGE = S * (A_TILE + B_TILE);
+  static constexpr int STAGES = (SMEM_BUDGET / STAGE) > 4 ? 4 : (SMEM_BUDGET / STAGE);
+  static constexpr int SMEM = STAGES * STAGE + 1024;
+  static_assert(STAGES >= 2, "too many slices for the stage budget");
+  static_assert(S * BN <= 512, "accumulators exceed TMEM");
+};
+
+struct Params {
+  int Lt, N, Mp, Nc, Kp, Brows;   // Brows = rows of SB per (slice, t) = 2 Nc
+  const int* eA;
+  const int* fB;
+  double* C;                      // complex128 [Lt][N][N] (interleaved)
+  int* Craw;                      // RAW mode: int32 [Mp][Brows]
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          dev::smem_u32(dst)),
+      "l"(map), "r"(dev::smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_64B: 8-row core-matrix groups 512 B apart
+// (SBO), LBO unused for swizzled K-major, version 1 (sm_100), layout type 4 = SWIZZLE_64B.
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+  uint64_t d = uint64_t((saddr & 0x3FFFF) >> 4);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(512 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(4) << 61;
+  return d;
+}
+
+// Instruction descriptor kind::i8: D = S32 (bits 4-5 = 2), A, B signed (bits 7-9, 10-12 = 1),
+// both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28.
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(dev::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------------------
+// Splitting kernels
+
+// x in (-1, 1) -> S int8 slices (truncation; every step exact in FP64)
+template <int S>
+__device__ __forceinline__ void split_value(double x, int8_t (&q)[S]) {
+#pragma unroll
+  for (int k = 0; k < S; ++k) {
+    const double y = x * 128.0;
+    const double d = trunc(y);
+    q[k] = int8_t(int(d));
+    x = y - d;
+  }
+}
+
+__device__ __forceinline__ int scale_exponent(double m) {
+  // smallest e with m < 2^e (m > 0); 0 for an all-zero row / column
+  return m > 0.0 ? ilogb(m) + 1 : 0;
+}
+
+// One warp per row (t, i) of A: A_cat row slices + eA.
+template <int S>
+__global__ void __launch_bounds__(256) split_rows_kernel(const double2* __restrict__ A, int8_t* __restrict__ SA,
+                                                         int* __restrict__ eA, int Lt, int N, int Mp, int Nc) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + warp;
+  const int t = blockIdx.y;
+  if (i >= Mp) return;
+  const int Kp = 2 * Nc;
+  const size_t slice_stride = size_t(Lt) * Mp * Kp;
+  int8_t* row = SA + (size_t(t) * Mp + i) * Kp;
+  const double2* src = A + (size_t(t) * N + (i < N ? i : 0)) * N;
+  double m = 0.0;
+  if (i < N)
+    for (int j = lane; j < N; j += 32) {
+      const double2 v = src[j];
+      m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+    }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const int e = scale_exponent(m);
+  if (lane == 0) eA[size_t(t) * Mp + i] = e;
+  for (int j0 = lane * 4; j0 < Nc; j0 += 128) {
+    uint32_t wr[S], wi[S];
+#pragma unroll
+    for (int k = 0; k < S; ++k) wr[k] = wi[k] = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u;
+      double2 v = make_double2(0.0, 0.0);
+      if (i < N && j < N) v = src[j];
+      int8_t qr[S], qi[S];
+      split_value<S>(ldexp(v.x, -e), qr);
+      split_value<S>(ldexp(v.y, -e), qi);
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        wr[k] |= uint32_t(uint8_t(qr[k])) << (8 * u);
+        wi[k] |= uint32_t(uint8_t(qi[k])) << (8 * u);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      *reinterpret_cast<uint32_t*>(row + k * slice_stride + j0) = wr[k];
+      *reinterpret_cast<uint32_t*>(row + k * slice_stride + Nc + j0) = wi[k];
+    }
+  }
+}
+
+// One CTA per (32-column group g, t) of B: B_cat^T row slices + fB.
+template <int S>
+__global__ void __launch_bounds__(256) split_cols_kernel(const double2* __restrict__ B, int8_t* __restrict__ SB,
+                                                         int* __restrict__ fB, int Lt, int N, int Nc) {
+  __shared__ double2 tile[32][33];
+  __shared__ double red[8][32];
+  __shared__ int ecol[32];
+  const int tid = threadIdx.x;
+  const int g = blockIdx.x, t = blockIdx.y;
+  const int c0 = 32 * g;
+  const int Kp = 2 * Nc, Brows = 2 * Nc;
+  const size_t slice_stride = size_t(Lt) * Brows * Kp;
+  const double2* src = B + size_t(t) * N * N;
+  {
+    const int c = tid & 31, r0 = tid >> 5;
+    double m = 0.0;
+    if (c0 + c < N)
+      for (int k = r0; k < N; k += 8) {
+        const double2 v = src[size_t(k) * N + c0 + c];
+        m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+      }
+    red[r0][c] = m;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    double m = red[0][tid];
+#pragma unroll
+    for (int r = 1; r < 8; ++r) m = fmax(m, red[r][tid]);
+    ecol[tid] = scale_exponent(m);
+    fB[size_t(t) * Nc + c0 + tid] = ecol[tid];
+  }
+  int8_t* rows = SB + (size_t(t) * Brows + 64 * g) * Kp;
+  for (int k0 = 0; k0 < Nc; k0 += 32) {
+    __syncthreads();
+    for (int idx = tid; idx < 1024; idx += 256) {
+      const int kr = idx >> 5, c = idx & 31;
+      double2 v = make_double2(0.0, 0.0);
+      if (k0 + kr < N && c0 + c < N) v = src[size_t(k0 + kr) * N + c0 + c];
+      tile[kr][c] = v;
+    }
+    __syncthreads();
+    for (int item = tid; item < 512; item += 256) {
+      const int kq = item & 3, h = (item >> 2) & 1, rT = item >> 3;
+      const int c = rT & 31, part = rT >> 5;
+      const int e = ecol[c];
+      uint32_t lo[S], hi[S];
+#pragma unroll
+      for (int k = 0; k < S; ++k) lo[k] = hi[k] = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double2 v = tile[kq * 8 + u][c];
+        // part 0 (Cr column): [Br; -Bi]; part 1 (Ci column): [Bi; Br]
+        const double x = part == 0 ? (h == 0 ? v.x : -v.y) : (h == 0 ? v.y : v.x);
+        int8_t q[S];
+        split_value<S>(ldexp(x, -e), q);
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+          if (u < 4)
+            lo[k] |= uint32_t(uint8_t(q[k])) << (8 * u);
+          else
+            hi[k] |= uint32_t(uint8_t(q[k])) << (8 * (u - 4));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < S; ++k)
+        *reinterpret_cast<uint2*>(rows + k * slice_stride + size_t(rT) * Kp + h * Nc + k0 + kq * 8) =
+            make_uint2(lo[k], hi[k]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// The tcgen05 GEMM: grid (Brows / 64, Mp / 128, Lt), 128 threads.
+template <int S, bool RAW>
+__global__ void __launch_bounds__(128, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
+                                                            const __grid_constant__ CUtensorMap mapB, Params p) {
+  using C = Cfg<S>;
+  extern __shared__ __align__(1024) uint8_t dsm[];
+  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], tfull;
+  __shared__ uint32_t tmem_slot;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = blockIdx.x, mb = blockIdx.y, t = blockIdx.z;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dev::smem_u32(&tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      dev::mbar_init(&full[s], 1);
+      dev::mbar_init(&empty[s], 1);
+    }
+    dev::mbar_init(&tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int nk = p.Kp / BKB;
+
+  if (warp == 0 && lane == 0) {
+    // TMA producer: all S slices of A and B for one 64-byte K stage per ring slot
+    const int rowA = t * p.Mp + mb * BM;
+    const int rowB = t * p.Brows + nb * BN;
+    for (int kc = 0; kc < nk; ++kc) {
+      const int st = kc % C::STAGES;
+      if (kc >= C::STAGES) dev::mbar_wait(&empty[st], ((kc / C::STAGES) - 1) & 1);
+      dev::mbar_expect_tx(&full[st], C::STAGE);
+      uint8_t* sa = smem + st * C::STAGE;
+      uint8_t* sb = sa + S * A_TILE;
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        tma_load_2d(sa + i * A_TILE, &mapA, &full[st], kc * BKB, i * p.Lt * p.Mp + rowA);
+        tma_load_2d(sb + i * B_TILE, &mapB, &full[st], kc * BKB, i * p.Lt * p.Brows + rowB);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // MMA issuer: pair (i, j), i + j = d <= S-1, accumulates into TMEM columns [64 d, 64 d + 64)
+    uint32_t started = 0;
+    for (int kc = 0; kc < nk; ++kc) {
+      const int st = kc % C::STAGES;
+      dev::mbar_wait(&full[st], (kc / C::STAGES) & 1);
+      tc_fence_after();
+      const uint32_t sa = dev::smem_u32(smem + st * C::STAGE);
+      const uint32_t sb = sa + S * A_TILE;
+#pragma unroll
+      for (int i = 0; i < S; ++i)
+#pragma unroll
+        for (int j = 0; j < S - i; ++j) {
+          const int d = i + j;
+#pragma unroll
+          for (int ks = 0; ks < BKB / UK; ++ks) {
+            mma_i8(tmem + uint32_t(d * BN), sw64_desc(sa + i * A_TILE + ks * UK), sw64_desc(sb + j * B_TILE + ks * UK),
+                   (started >> d) & 1u);
+            started |= 1u << d;
+          }
+        }
+      mma_commit(&empty[st]);
+    }
+    mma_commit(&tfull);
+  }
+  __syncwarp();
+  dev::mbar_wait(&tfull, 0);
+  tc_fence_after();
+
+  const int r = mb * BM + warp * 32 + lane;                 // row of this thread (TMEM lane)
+  const uint32_t tl = tmem + (uint32_t(warp * 32) << 16);
+  if constexpr (RAW) {
+#pragma unroll
+    for (int q = 0; q < BN / 16; ++q) {
+      int v[16];
+      tmem_ld16(tl + q * 16, v);
+      tmem_wait_ld();
+      int* dst = p.Craw + size_t(r) * p.Brows + nb * BN + q * 16;
+#pragma unroll
+      for (int u = 0; u < 16; u += 4) *reinterpret_cast<int4*>(dst + u) = make_int4(v[u], v[u + 1], v[u + 2], v[u + 3]);
+    }
+  } else {
+    const int e = p.eA[size_t(t) * p.Mp + r];
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      double ar[16], ai[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) ar[q] = ai[q] = 0.0;
+#pragma unroll 1
+      for (int d = S - 1; d >= 0; --d) {      // least significant accumulator first
+        int vr[16], vi[16];
+        tmem_ld16(tl + uint32_t(d * BN + h * 16), vr);
+        tmem_ld16(tl + uint32_t(d * BN + 32 + h * 16), vi);
+        tmem_wait_ld();
+        const double w = ldexp(1.0, -7 * (d + 2));
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          ar[q] = fma(double(vr[q]), w, ar[q]);
+          ai[q] = fma(double(vi[q]), w, ai[q]);
+        }
+      }
+      if (r < p.N) {
+        const int cbase = nb * 32 + h * 16;
+        double* dst = p.C + (size_t(t) * p.N + r) * p.N * 2;
+        const int* f = p.fB + size_t(t) * p.Nc + cbase;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int c = cbase + q;
+          if (c < p.N) {
+            const int sc = e + f[q];
+            *reinterpret_cast<double2*>(dst + 2 * c) = make_double2(ldexp(ar[q], sc), ldexp(ai[q], sc));
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult r;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &r) == cudaSuccess &&
+        r == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(q);
+  });
+  return fn;
+}
+
+bool map_i8(CUtensorMap* map, const void* base, uint64_t kp, uint64_t rows, uint32_t box_rows) {
+  auto enc = encoder();
+  if (!enc) return false;
+  cuuint64_t gd[2] = {kp, rows};
+  cuuint64_t gs[1] = {kp};
+  cuuint32_t box[2] = {uint32_t(BKB), box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), gd, gs, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct Geometry {
+  int Mp, Nc, Kp, Brows;
+  size_t sa, sb, ea, fb, total;
+};
+
+Geometry geometry(int Lt, int N, int S) {
+  Geometry g;
+  g.Mp = (N + BM - 1) / BM * BM;
+  g.Nc = (N + 31) / 32 * 32;
+  g.Kp = 2 * g.Nc;
+  g.Brows = 2 * g.Nc;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  g.sa = 0;
+  g.sb = al(size_t(S) * Lt * g.Mp * g.Kp);
+  g.ea = g.sb + al(size_t(S) * Lt * g.Brows * g.Kp);
+  g.fb = g.ea + al(size_t(Lt) * g.Mp * 4);
+  g.total = g.fb + al(size_t(Lt) * g.Nc * 4);
+  return g;
+}
+
+template <int S, bool RAW>
+cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t stream) {
+  using C = Cfg<S>;
+  auto k = ozaki_gemm_kernel<S, RAW>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (e != cudaSuccess) return e;
+  dim3 grid(p.Brows / BN, p.Mp / BM, RAW ? 1 : p.Lt);
+  k<<<grid, 128, C::SMEM, stream>>>(ma, mb, p);
+  return cudaGetLastError();
+}
+
+template <int S>
+cudaError_t run_mm1(const void* A, const void* B, void* Cout, int Lt, int N, void* ws, size_t ws_bytes,
+                    cudaStream_t stream) {
+  const Geometry g = geometry(Lt, N, S);
+  if (ws_bytes < g.total) return cudaErrorInvalidValue;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  int8_t* SA = reinterpret_cast<int8_t*>(w + g.sa);
+  int8_t* SB = reinterpret_cast<int8_t*>(w + g.sb);
+  int* eA = reinterpret_cast<int*>(w + g.ea);
+  int* fB = reinterpret_cast<int*>(w + g.fb);
+  split_rows_kernel<S><<<dim3(g.Mp / 8, Lt), 256, 0, stream>>>(static_cast<const double2*>(A), SA, eA, Lt, N, g.Mp,
+                                                               g.Nc);
+  split_cols_kernel<S><<<dim3(g.Nc / 32, Lt), 256, 0, stream>>>(static_cast<const double2*>(B), SB, fB, Lt, N, g.Nc);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  CUtensorMap ma, mb;
+  if (!map_i8(&ma, SA, g.Kp, uint64_t(S) * Lt * g.Mp, BM) || !map_i8(&mb, SB, g.Kp, uint64_t(S) * Lt * g.Brows, BN))
+    return cudaErrorInvalidValue;
+  Params p{Lt, N, g.Mp, g.Nc, g.Kp, g.Brows, eA, fB, static_cast<double*>(Cout), nullptr};
+  return launch_gemm<S, false>(ma, mb, p, stream);
+}
+
+}  // namespace oz
+
+size_t ozaki_mm1_workspace_bytes(int64_t Lt, int64_t N, int slices) {
+  return oz::geometry(int(Lt), int(N), slices).total;
+}
+
+cudaError_t launch_ozaki_mm1(const void* A, const void* B, void* C, int64_t Lt, int64_t N, int slices, void* ws,
+                             size_t ws_bytes, cudaStream_t stream) {
+  switch (slices) {
+    case 4: return oz::run_mm1<4>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
+    case 5: return oz::run_mm1<5>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
+    case 6: return oz::run_mm1<6>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
+    case 7: return oz::run_mm1<7>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
+    case 8: return oz::run_mm1<8>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_i8gemm_tn(const int8_t* A, const int8_t* B, int32_t* C, int64_t M, int64_t Nn, int64_t K,
+                             cudaStream_t stream) {
+  if (M % oz::BM || Nn % oz::BN || K % oz::BKB) return cudaErrorInvalidValue;
+  CUtensorMap ma, mb;
+  if (!oz::map_i8(&ma, A, uint64_t(K), uint64_t(M), oz::BM) || !oz::map_i8(&mb, B, uint64_t(K), uint64_t(Nn), oz::BN))
+    return cudaErrorInvalidValue;
+  oz::Params p{1, 0, int(M), 0, int(K), int(Nn), nullptr, nullptr, nullptr, C};
+  return oz::launch_gemm<1, true>(ma, mb, p, stream);
+}
+
+}  // namespace cc

@@ -1,0 +1,90 @@
+"""GPU parity of the tcgen05 INT8 path (DESIGN reading V-6).
+
+- cc_i8gemm_tn: the UMMA descriptor / TMEM machinery alone, bit-exact against an integer
+  matmul (numpy int64).
+- cc_mm1_ozaki: MM1 by Ozaki splitting, against the oracle's MM1 (oracle/values.py, numpy
+  complex128): phase-limited data within 1e-10 relative per element (north_star), random-phase
+  data within 1e-10 of the |A||B| error scale (V-4), all-ones closed form exactly (N J).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from synth import rng as srng  # noqa: E402
+from oracle import values  # noqa: E402
+from gpu_helpers import device_from, to_numpy_c  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2511_02257_b200 import cc
+    return cc.Context(0, torch.empty(64 << 20, dtype=torch.uint8, device="cuda"))
+
+
+@pytest.mark.parametrize("M,Nn,K", [(128, 64, 64), (256, 128, 192), (128, 256, 512), (384, 64, 1024)])
+def test_i8gemm_bit_exact(ctx, M, Nn, K):
+    g = np.random.default_rng(M * 7 + Nn + K)
+    A = g.integers(-127, 128, size=(M, K), dtype=np.int8)
+    B = g.integers(-127, 128, size=(Nn, K), dtype=np.int8)
+    A[0, :] = 127                      # extreme rows/cols: |sum| = 127^2 K
+    B[0, :] = -127
+    dA = torch.from_numpy(A).cuda()
+    dB = torch.from_numpy(B).cuda()
+    dC = torch.zeros((M, Nn), dtype=torch.int32, device="cuda")
+    ctx.i8gemm_tn(dA, dB, dC, M, Nn, K)
+    want = A.astype(np.int64) @ B.astype(np.int64).T
+    got = dC.cpu().numpy().astype(np.int64)
+    assert np.array_equal(got, want)
+
+
+def _phase_limited(shape, seed):
+    n = int(np.prod(shape))
+    return srng.leaf_values(seed, 3000 + seed, 0, n, 1.0).reshape(shape)
+
+
+def _random_phase(shape, seed):
+    n = int(np.prod(shape))
+    return srng.leaf_values(seed, 4000 + seed, 0, n, 1.0, srng.MODE_RANDOM_PHASE).reshape(shape)
+
+
+def _run(ctx, A, B, Lt, N, s):
+    from paper_2511_02257_b200 import cc
+    ws = torch.empty(cc.cc_mm1_ozaki_workspace_bytes(Lt, N, s), dtype=torch.uint8, device="cuda")
+    C = torch.full((Lt * N * N * 2,), float("nan"), dtype=torch.float64, device="cuda")
+    ctx.mm1_ozaki(device_from(A), device_from(B), C, Lt, N, s, ws)
+    torch.cuda.synchronize()
+    return to_numpy_c(C, (Lt, N, N))
+
+
+@pytest.mark.parametrize("Lt,N", [(1, 8), (2, 33), (3, 64), (2, 100), (4, 128), (1, 200), (2, 256), (1, 512)])
+@pytest.mark.parametrize("s", [6, 7])
+def test_mm1_ozaki_phase_limited(ctx, Lt, N, s):
+    A = _phase_limited((Lt, N, N), 1 + N)
+    B = _phase_limited((Lt, N, N), 2 + N)
+    got = _run(ctx, A, B, Lt, N, s)
+    want = values.mm1(A, B)
+    err = float(np.max(np.abs(got - want) / np.abs(want)))
+    assert err <= 1e-10, err
+
+
+@pytest.mark.parametrize("Lt,N", [(2, 48), (1, 130), (1, 256)])
+def test_mm1_ozaki_random_phase_scale(ctx, Lt, N):
+    A = _random_phase((Lt, N, N), 5)
+    B = _random_phase((Lt, N, N), 6)
+    A[0, 3, :] *= 1e-3                   # a row and a column far below the others' scale
+    B[0, :, 5] *= 1e6
+    got = _run(ctx, A, B, Lt, N, 7)
+    want = values.mm1(A, B)
+    scale = np.matmul(np.abs(A), np.abs(B))
+    assert np.all(np.abs(got - want) <= 1e-10 * scale)
+
+
+def test_mm1_ozaki_closed_form_all_ones(ctx):
+    Lt, N = 2, 96
+    J = np.ones((Lt, N, N), dtype=np.complex128)
+    got = _run(ctx, J, J, Lt, N, 6)
+    assert np.array_equal(got, N * J)
+    Z = np.zeros_like(J)                 # a zero operand (exponent 0, all-zero slices)
+    assert np.array_equal(_run(ctx, Z, J, Lt, N, 6), Z)
