@@ -181,7 +181,8 @@ cc_status cc_set_leaf_device(cc_ctx* ctx, int64_t leaf_id, const void* dev, size
  * (average launch duration for the roofline, without host launch overhead).  The default
  * executor is the dataflow one (persistent DMMA-tile and trace workers, kernels/dataflow.hpp);
  * bit 4 selects op-by-op launches instead; bit 5 records the per-item timeline
- * (cc_dataflow_profile). */
+ * (cc_dataflow_profile); bit 6 runs every MM1 on the tcgen05 INT8 Ozaki engine (cc_mm1_ozaki,
+ * 6 slices; implies op-by-op launches; the other kinds stay on FP64 DMMA). */
 cc_status cc_execute(cc_ctx* ctx, int32_t flags, cc_exec_stats* stats);
 /* Enqueue-only variant (no host sync): work is ordered on the compute stream. */
 cc_status cc_execute_async(cc_ctx* ctx, int32_t flags);

@@ -50,6 +50,9 @@ struct PhaseTimer {
 namespace {
 
 constexpr int64_t ALIGN = 1024;
+// INT8 slices per operand of the Ozaki MM1 engine (reading V-6: 6 x 7 bits keep the error of
+// a phase-limited MM1 below ~4e-12 relative, inside the north_star's 1e-10).
+constexpr int OZAKI_SLICES = 6;
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 void ck(cudaError_t e, const char* what) {
@@ -65,6 +68,7 @@ struct KindTimes {
 
 struct cc_ctx {
   int device = -1;
+  bool mm1_ozaki = false;     // execute flags bit 6: MM1 on the tcgen05 Ozaki engine (op-by-op)
   bool host_only = true;
   char* arena = nullptr;
   int64_t arena_bytes = 0;
@@ -363,6 +367,7 @@ void prepare_phys(cc_ctx* ctx) {
   for (const auto& n : g.nodes) has[n.op] = true;
   for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)})
     if (has[op]) gemm_ws = std::max(gemm_ws, zgemm_workspace_bytes(problem_for(op, Lt, N, S, nullptr, nullptr, nullptr), ctx->num_sms));
+  if (has[CC_MM1] && N <= 8192) gemm_ws = std::max(gemm_ws, ozaki_mm1_workspace_bytes(Lt, N, OZAKI_SLICES));
   const size_t trace_ws = trace_workspace_bytes(Lt, N);
   const int64_t n_trees = int64_t(g.trees.size()), n_corr = int64_t(g.corr_ids.size()), n_terms = int64_t(g.terms.size());
   const int64_t sz_gemm = round_up(int64_t(gemm_ws), ALIGN), sz_trace = round_up(int64_t(trace_ws), ALIGN);
@@ -1303,6 +1308,11 @@ void launch_contract(cc_ctx* ctx, const Node& n, const void* a, const void* b, v
     ++*nl;
     return;
   }
+  if (n.op == CC_MM1 && ctx->mm1_ozaki) {
+    ck(launch_ozaki_mm1(a, b, out, g.Lt, g.N, OZAKI_SLICES, ctx->gemm_ws, ctx->gemm_ws_bytes, ctx->cs), "Ozaki MM1");
+    *nl += 5;   // memset + colmax + 2 splits + GEMM
+    return;
+  }
   ZgemmProblem p = problem_for(n.op, g.Lt, g.N, g.S, a, b, out);
   ck(launch_zgemm(p, ctx->gemm_ws, ctx->gemm_ws_bytes, ctx->num_sms, ctx->cs, nl), "contraction kernel");
 }
@@ -1444,12 +1454,13 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   if (!ctx->scheduled) throw Error(CC_E_STATE, "cc_execute before cc_schedule");
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
   prepare_phys(ctx);
+  ctx->mm1_ozaki = (flags & 64) != 0;
   if (flags & 12) {
     kernel_only(ctx, (flags & 4) ? 0 : 1, stats);
     return;
   }
   const bool use_graph = (flags & 1) != 0;
-  const bool legacy = (flags & 16) != 0 || (flags & 2) != 0;
+  const bool legacy = (flags & 16) != 0 || (flags & 2) != 0 || (flags & 64) != 0;
   const bool time_kernels = (flags & 2) != 0 && !use_graph;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;
   std::vector<int> kev_kind;

@@ -114,16 +114,23 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // ---------------------------------------------------------------------------------------
 // Splitting kernels
 
-// x in (-1, 1) -> S int8 slices (truncation; every step exact in FP64)
+// x in (-1, 1) -> S int8 slices of 7 bits, truncated toward zero (sign-magnitude: every slice
+// has the sign of x).  |x| 2^56 < 2^56 is converted exactly up to the bits below 2^-56, which
+// lie beyond the last slice (S <= 8: 7 S <= 56); slice k = bits [49-7k, 56-7k) of |x| 2^56.
 template <int S>
 __device__ __forceinline__ void split_value(double x, int8_t (&q)[S]) {
+  const long long m = __double2ll_rz(x * 72057594037927936.0);   // 2^56
+  const unsigned long long a = static_cast<unsigned long long>(m < 0 ? -m : m);
 #pragma unroll
   for (int k = 0; k < S; ++k) {
-    const double y = x * 128.0;
-    const double d = trunc(y);
-    q[k] = int8_t(int(d));
-    x = y - d;
+    const int v = int((a >> (49 - 7 * k)) & 127ull);
+    q[k] = int8_t(m < 0 ? -v : v);
   }
+}
+
+// 2^k for |k| <= 1000 (exact; the exponents here come from ilogb of finite data)
+__device__ __forceinline__ double pow2(int k) {
+  return __longlong_as_double(static_cast<long long>(1023 + k) << 52);
 }
 
 __device__ __forceinline__ int scale_exponent(double m) {
@@ -153,6 +160,7 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double2* __restri
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   const int e = scale_exponent(m);
   if (lane == 0) eA[size_t(t) * Mp + i] = e;
+  const double sc = pow2(-e);
   for (int j0 = lane * 4; j0 < Nc; j0 += 128) {
     uint32_t wr[S], wi[S];
 #pragma unroll
@@ -163,8 +171,8 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double2* __restri
       double2 v = make_double2(0.0, 0.0);
       if (i < N && j < N) v = src[j];
       int8_t qr[S], qi[S];
-      split_value<S>(ldexp(v.x, -e), qr);
-      split_value<S>(ldexp(v.y, -e), qi);
+      split_value<S>(v.x * sc, qr);
+      split_value<S>(v.y * sc, qi);
 #pragma unroll
       for (int k = 0; k < S; ++k) {
         wr[k] |= uint32_t(uint8_t(qr[k])) << (8 * u);
@@ -179,12 +187,38 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double2* __restri
   }
 }
 
-// One CTA per (32-column group g, t) of B: B_cat^T row slices + fB.
+// Column scale exponents of B: grid (Nc/32, Lt, ceil(N/128)); fB preset to INT_MIN (bytes 0x80),
+// each CTA folds the max-exponent of its 128-row chunk in with atomicMax (exponents are
+// monotone in the magnitude, so the max of the chunk exponents is the column's exponent).
+__global__ void __launch_bounds__(256) colmax_kernel(const double2* __restrict__ B, int* __restrict__ fB, int N, int Nc) {
+  __shared__ double red[8][32];
+  const int tid = threadIdx.x, c = tid & 31, r0 = tid >> 5;
+  const int c0 = 32 * blockIdx.x, t = blockIdx.y, k0 = 128 * blockIdx.z;
+  const double2* src = B + size_t(t) * N * N;
+  double m = 0.0;
+  if (c0 + c < N) {
+    const int k1 = min(N, k0 + 128);
+    for (int k = k0 + r0; k < k1; k += 8) {
+      const double2 v = src[size_t(k) * N + c0 + c];
+      m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+    }
+  }
+  red[r0][c] = m;
+  __syncthreads();
+  if (tid < 32) {
+#pragma unroll
+    for (int r = 1; r < 8; ++r) m = fmax(m, red[r][tid]);
+    m = fmax(m, red[0][tid]);
+    if (m > 0.0) atomicMax(&fB[size_t(t) * Nc + c0 + tid], scale_exponent(m));
+  }
+}
+
+// B_cat^T row slices: grid (Nc/32, Lt, Nc/128), one CTA per (32-column group g, t, 128-row
+// chunk of k).  A column left at INT_MIN by colmax_kernel is all zero (exponent 0).
 template <int S>
 __global__ void __launch_bounds__(256) split_cols_kernel(const double2* __restrict__ B, int8_t* __restrict__ SB,
-                                                         int* __restrict__ fB, int Lt, int N, int Nc) {
+                                                         const int* __restrict__ fB, int Lt, int N, int Nc) {
   __shared__ double2 tile[32][33];
-  __shared__ double red[8][32];
   __shared__ int ecol[32];
   const int tid = threadIdx.x;
   const int g = blockIdx.x, t = blockIdx.y;
@@ -192,26 +226,13 @@ __global__ void __launch_bounds__(256) split_cols_kernel(const double2* __restri
   const int Kp = 2 * Nc, Brows = 2 * Nc;
   const size_t slice_stride = size_t(Lt) * Brows * Kp;
   const double2* src = B + size_t(t) * N * N;
-  {
-    const int c = tid & 31, r0 = tid >> 5;
-    double m = 0.0;
-    if (c0 + c < N)
-      for (int k = r0; k < N; k += 8) {
-        const double2 v = src[size_t(k) * N + c0 + c];
-        m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
-      }
-    red[r0][c] = m;
-  }
-  __syncthreads();
   if (tid < 32) {
-    double m = red[0][tid];
-#pragma unroll
-    for (int r = 1; r < 8; ++r) m = fmax(m, red[r][tid]);
-    ecol[tid] = scale_exponent(m);
-    fB[size_t(t) * Nc + c0 + tid] = ecol[tid];
+    const int e = fB[size_t(t) * Nc + c0 + tid];
+    ecol[tid] = e < -100000 ? 0 : e;
   }
   int8_t* rows = SB + (size_t(t) * Brows + 64 * g) * Kp;
-  for (int k0 = 0; k0 < Nc; k0 += 32) {
+  const int kend = min(Nc, 128 * int(blockIdx.z + 1));
+  for (int k0 = 128 * blockIdx.z; k0 < kend; k0 += 32) {
     __syncthreads();
     for (int idx = tid; idx < 1024; idx += 256) {
       const int kr = idx >> 5, c = idx & 31;
@@ -223,7 +244,7 @@ __global__ void __launch_bounds__(256) split_cols_kernel(const double2* __restri
     for (int item = tid; item < 512; item += 256) {
       const int kq = item & 3, h = (item >> 2) & 1, rT = item >> 3;
       const int c = rT & 31, part = rT >> 5;
-      const int e = ecol[c];
+      const double sc = pow2(-ecol[c]);
       uint32_t lo[S], hi[S];
 #pragma unroll
       for (int k = 0; k < S; ++k) lo[k] = hi[k] = 0;
@@ -233,7 +254,7 @@ __global__ void __launch_bounds__(256) split_cols_kernel(const double2* __restri
         // part 0 (Cr column): [Br; -Bi]; part 1 (Ci column): [Bi; Br]
         const double x = part == 0 ? (h == 0 ? v.x : -v.y) : (h == 0 ? v.y : v.x);
         int8_t q[S];
-        split_value<S>(ldexp(x, -e), q);
+        split_value<S>(x * sc, q);
 #pragma unroll
         for (int k = 0; k < S; ++k) {
           if (u < 4)
@@ -251,17 +272,26 @@ __global__ void __launch_bounds__(256) split_cols_kernel(const double2* __restri
 }
 
 // ---------------------------------------------------------------------------------------
-// The tcgen05 GEMM: grid (Brows / 64, Mp / 128, Lt), 128 threads.
+// The tcgen05 GEMM, persistent: grid = min(tiles, SMs), 192 threads.
+//   warps 0-3: epilogue (warp w drains TMEM lanes 32w..32w+31)
+//   warp 4 lane 0: TMA producer, runs ahead across tiles through the stage ring
+//   warp 5 lane 0: MMA issuer
+// Tiles in (t, row block, column block) order, column blocks fastest (consecutive tiles of a
+// CTA share the A slices in L2).  The S diagonal accumulators use S*64 of the 512 TMEM
+// columns; the epilogue drains them in order d = 0..S-1 and releases each one (drained[d])
+// as soon as it is in registers, so the next tile's MMAs into diagonal d start while the
+// epilogue is still converting and storing.
 template <int S, bool RAW>
-__global__ void __launch_bounds__(128, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
+__global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                                                             const __grid_constant__ CUtensorMap mapB, Params p) {
   using C = Cfg<S>;
   extern __shared__ __align__(1024) uint8_t dsm[];
-  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], tfull;
+  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], tfull, drained[S];
   __shared__ uint32_t tmem_slot;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nb = blockIdx.x, mb = blockIdx.y, t = blockIdx.z;
+  const int ntn = p.Brows / BN, ntm = p.Mp / BM;
+  const int ntiles = ntn * ntm * (RAW ? 1 : p.Lt);
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dev::smem_u32(&tmem_slot))
@@ -274,6 +304,7 @@ __global__ void __launch_bounds__(128, 1) ozaki_gemm_kernel(const __grid_constan
       dev::mbar_init(&empty[s], 1);
     }
     dev::mbar_init(&tfull, 1);
+    for (int d = 0; d < S; ++d) dev::mbar_init(&drained[d], 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -283,93 +314,113 @@ __global__ void __launch_bounds__(128, 1) ozaki_gemm_kernel(const __grid_constan
   const uint32_t tmem = tmem_slot;
   const int nk = p.Kp / BKB;
 
-  if (warp == 0 && lane == 0) {
-    // TMA producer: all S slices of A and B for one 64-byte K stage per ring slot
-    const int rowA = t * p.Mp + mb * BM;
-    const int rowB = t * p.Brows + nb * BN;
-    for (int kc = 0; kc < nk; ++kc) {
-      const int st = kc % C::STAGES;
-      if (kc >= C::STAGES) dev::mbar_wait(&empty[st], ((kc / C::STAGES) - 1) & 1);
-      dev::mbar_expect_tx(&full[st], C::STAGE);
-      uint8_t* sa = smem + st * C::STAGE;
-      uint8_t* sb = sa + S * A_TILE;
+  if (warp == 4) {
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int nb = tile % ntn, mb = (tile / ntn) % ntm, t = tile / (ntn * ntm);
+        const int rowA = t * p.Mp + mb * BM;
+        const int rowB = t * p.Brows + nb * BN;
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int st = it % C::STAGES;
+          if (it >= C::STAGES) dev::mbar_wait(&empty[st], ((it / C::STAGES) - 1) & 1);
+          dev::mbar_expect_tx(&full[st], C::STAGE);
+          uint8_t* sa = smem + st * C::STAGE;
+          uint8_t* sb = sa + S * A_TILE;
 #pragma unroll
-      for (int i = 0; i < S; ++i) {
-        tma_load_2d(sa + i * A_TILE, &mapA, &full[st], kc * BKB, i * p.Lt * p.Mp + rowA);
-        tma_load_2d(sb + i * B_TILE, &mapB, &full[st], kc * BKB, i * p.Lt * p.Brows + rowB);
-      }
-    }
-  } else if (warp == 1 && lane == 0) {
-    // MMA issuer: pair (i, j), i + j = d <= S-1, accumulates into TMEM columns [64 d, 64 d + 64)
-    uint32_t started = 0;
-    for (int kc = 0; kc < nk; ++kc) {
-      const int st = kc % C::STAGES;
-      dev::mbar_wait(&full[st], (kc / C::STAGES) & 1);
-      tc_fence_after();
-      const uint32_t sa = dev::smem_u32(smem + st * C::STAGE);
-      const uint32_t sb = sa + S * A_TILE;
-#pragma unroll
-      for (int i = 0; i < S; ++i)
-#pragma unroll
-        for (int j = 0; j < S - i; ++j) {
-          const int d = i + j;
-#pragma unroll
-          for (int ks = 0; ks < BKB / UK; ++ks) {
-            mma_i8(tmem + uint32_t(d * BN), sw64_desc(sa + i * A_TILE + ks * UK), sw64_desc(sb + j * B_TILE + ks * UK),
-                   (started >> d) & 1u);
-            started |= 1u << d;
+          for (int i = 0; i < S; ++i) {
+            tma_load_2d(sa + i * A_TILE, &mapA, &full[st], kc * BKB, i * p.Lt * p.Mp + rowA);
+            tma_load_2d(sb + i * B_TILE, &mapB, &full[st], kc * BKB, i * p.Lt * p.Brows + rowB);
           }
         }
-      mma_commit(&empty[st]);
+      }
     }
-    mma_commit(&tfull);
-  }
-  __syncwarp();
-  dev::mbar_wait(&tfull, 0);
-  tc_fence_after();
-
-  const int r = mb * BM + warp * 32 + lane;                 // row of this thread (TMEM lane)
-  const uint32_t tl = tmem + (uint32_t(warp * 32) << 16);
-  if constexpr (RAW) {
+  } else if (warp == 5) {
+    if (lane == 0) {
+      int it = 0, n = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++n) {
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int st = it % C::STAGES;
+          dev::mbar_wait(&full[st], (it / C::STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = dev::smem_u32(smem + st * C::STAGE);
+          const uint32_t sb = sa + S * A_TILE;
 #pragma unroll
-    for (int q = 0; q < BN / 16; ++q) {
-      int v[16];
-      tmem_ld16(tl + q * 16, v);
-      tmem_wait_ld();
-      int* dst = p.Craw + size_t(r) * p.Brows + nb * BN + q * 16;
+          for (int d = 0; d < S; ++d) {
+            if (kc == 0 && n > 0) {
+              dev::mbar_wait(&drained[d], (n - 1) & 1);     // previous tile's diagonal d is in registers
+              tc_fence_after();
+            }
 #pragma unroll
-      for (int u = 0; u < 16; u += 4) *reinterpret_cast<int4*>(dst + u) = make_int4(v[u], v[u + 1], v[u + 2], v[u + 3]);
+            for (int i = 0; i <= d; ++i)
+#pragma unroll
+              for (int ks = 0; ks < BKB / UK; ++ks)
+                mma_i8(tmem + uint32_t(d * BN), sw64_desc(sa + i * A_TILE + ks * UK),
+                       sw64_desc(sb + (d - i) * B_TILE + ks * UK), (kc | i | ks) != 0);
+          }
+          mma_commit(&empty[st]);
+        }
+        mma_commit(&tfull);
+      }
     }
   } else {
-    const int e = p.eA[size_t(t) * p.Mp + r];
-#pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      double ar[16], ai[16];
+    int n = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++n) {
+      const int nb = tile % ntn, mb = (tile / ntn) % ntm, t = tile / (ntn * ntm);
+      dev::mbar_wait(&tfull, n & 1);
+      tc_fence_after();
+      const int r = mb * BM + warp * 32 + lane;                 // row of this thread (TMEM lane)
+      const uint32_t tl = tmem + (uint32_t(warp * 32) << 16);
+      if constexpr (RAW) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) ar[q] = ai[q] = 0.0;
-#pragma unroll 1
-      for (int d = S - 1; d >= 0; --d) {      // least significant accumulator first
-        int vr[16], vi[16];
-        tmem_ld16(tl + uint32_t(d * BN + h * 16), vr);
-        tmem_ld16(tl + uint32_t(d * BN + 32 + h * 16), vi);
-        tmem_wait_ld();
-        const double w = ldexp(1.0, -7 * (d + 2));
+        for (int q = 0; q < BN / 16; ++q) {
+          int v[16];
+          tmem_ld16(tl + q * 16, v);
+          tmem_wait_ld();
+          if (q == BN / 16 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) dev::mbar_arrive(&drained[0]);
+          }
+          int* dst = p.Craw + size_t(r) * p.Brows + nb * BN + q * 16;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          ar[q] = fma(double(vr[q]), w, ar[q]);
-          ai[q] = fma(double(vi[q]), w, ai[q]);
+          for (int u = 0; u < 16; u += 4)
+            *reinterpret_cast<int4*>(dst + u) = make_int4(v[u], v[u + 1], v[u + 2], v[u + 3]);
         }
-      }
-      if (r < p.N) {
-        const int cbase = nb * 32 + h * 16;
-        double* dst = p.C + (size_t(t) * p.N + r) * p.N * 2;
-        const int* f = p.fB + size_t(t) * p.Nc + cbase;
+      } else {
+        double ar[32], ai[32];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int c = cbase + q;
-          if (c < p.N) {
-            const int sc = e + f[q];
-            *reinterpret_cast<double2*>(dst + 2 * c) = make_double2(ldexp(ar[q], sc), ldexp(ai[q], sc));
+        for (int q = 0; q < 32; ++q) ar[q] = ai[q] = 0.0;
+#pragma unroll 1
+        for (int d = 0; d < S; ++d) {          // most significant accumulator first (fixed order)
+          int vr[32], vi[32];
+          tmem_ld16(tl + uint32_t(d * BN), *reinterpret_cast<int(*)[16]>(&vr[0]));
+          tmem_ld16(tl + uint32_t(d * BN + 16), *reinterpret_cast<int(*)[16]>(&vr[16]));
+          tmem_ld16(tl + uint32_t(d * BN + 32), *reinterpret_cast<int(*)[16]>(&vi[0]));
+          tmem_ld16(tl + uint32_t(d * BN + 48), *reinterpret_cast<int(*)[16]>(&vi[16]));
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) dev::mbar_arrive(&drained[d]);
+          const double w = pow2(-7 * (d + 2));
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            ar[q] = fma(double(vr[q]), w, ar[q]);
+            ai[q] = fma(double(vi[q]), w, ai[q]);
+          }
+        }
+        if (r < p.N) {
+          const double se = pow2(p.eA[size_t(t) * p.Mp + r]);
+          const int cbase = nb * 32;
+          double* dst = p.C + (size_t(t) * p.N + r) * p.N * 2;
+          const int* f = p.fB + size_t(t) * p.Nc + cbase;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const int c = cbase + q;
+            if (c < p.N) {
+              const double sf = se * pow2(f[q] < -100000 ? 0 : f[q]);   // exact: a power of two
+              *reinterpret_cast<double2*>(dst + 2 * c) = make_double2(ar[q] * sf, ai[q] * sf);
+            }
           }
         }
       }
@@ -428,14 +479,25 @@ Geometry geometry(int Lt, int N, int S) {
   return g;
 }
 
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
 template <int S, bool RAW>
 cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t stream) {
   using C = Cfg<S>;
   auto k = ozaki_gemm_kernel<S, RAW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
-  dim3 grid(p.Brows / BN, p.Mp / BM, RAW ? 1 : p.Lt);
-  k<<<grid, 128, C::SMEM, stream>>>(ma, mb, p);
+  const int64_t tiles = int64_t(p.Brows / BN) * (p.Mp / BM) * (RAW ? 1 : p.Lt);
+  const int grid = int(tiles < num_sms() ? tiles : num_sms());
+  k<<<grid, 192, C::SMEM, stream>>>(ma, mb, p);
   return cudaGetLastError();
 }
 
@@ -451,8 +513,12 @@ cudaError_t run_mm1(const void* A, const void* B, void* Cout, int Lt, int N, voi
   int* fB = reinterpret_cast<int*>(w + g.fb);
   split_rows_kernel<S><<<dim3(g.Mp / 8, Lt), 256, 0, stream>>>(static_cast<const double2*>(A), SA, eA, Lt, N, g.Mp,
                                                                g.Nc);
-  split_cols_kernel<S><<<dim3(g.Nc / 32, Lt), 256, 0, stream>>>(static_cast<const double2*>(B), SB, fB, Lt, N, g.Nc);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = cudaMemsetAsync(fB, 0x80, size_t(Lt) * g.Nc * 4, stream);   // INT_MIN-like
+  if (e != cudaSuccess) return e;
+  colmax_kernel<<<dim3(g.Nc / 32, Lt, (N + 127) / 128), 256, 0, stream>>>(static_cast<const double2*>(B), fB, N, g.Nc);
+  split_cols_kernel<S><<<dim3(g.Nc / 32, Lt, (g.Nc + 127) / 128), 256, 0, stream>>>(static_cast<const double2*>(B), SB,
+                                                                                    fB, Lt, N, g.Nc);
+  e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CUtensorMap ma, mb;
   if (!map_i8(&ma, SA, g.Kp, uint64_t(S) * Lt * g.Mp, BM) || !map_i8(&mb, SB, g.Kp, uint64_t(S) * Lt * g.Brows, BN))

@@ -88,3 +88,37 @@ def test_mm1_ozaki_closed_form_all_ones(ctx):
     assert np.array_equal(got, N * J)
     Z = np.zeros_like(J)                 # a zero operand (exponent 0, all-zero slices)
     assert np.array_equal(_run(ctx, Z, J, Lt, N, 6), Z)
+
+
+@pytest.mark.parametrize("flags", [64, 65])
+def test_executor_ozaki_mm1_c2_small(flags):
+    """cc_execute with every MM1 on the Ozaki engine (flags bit 6; +bit 0 = CUDA graph):
+    roots within 1e-10 of the oracle, correlators within 1e-10 of sum|coef root|."""
+    from synth import dags
+    from oracle.dag import Dag
+    from gpu_helpers import run_gpu, assert_roots_close, assert_corr_close
+    w = dags.config_c2(N=72, Lt=3, n_loop4=60, n_loop2=6, n_corr=4)
+    dag = Dag(w)
+    _, roots, corr, st, ex = run_gpu(w, flags=flags)
+    r_or, c_or = values.run_workload(w, dag)
+    assert_roots_close(roots, r_or)
+    assert_corr_close(dag, r_or, corr, c_or)
+
+
+def test_executor_ozaki_mm1_c5_time_part_deterministic():
+    """c5-shaped DAG (N=256) on one TIME part with the Ozaki MM1 engine: oracle parity and
+    bit-identical roots over two executes (fixed-order reductions, no atomics on values)."""
+    from synth import dags
+    from oracle.dag import Dag
+    from oracle.partition import time_range
+    from paper_2511_02257_b200 import cc
+    from gpu_helpers import run_gpu, assert_roots_close
+    w = dags.config_c5(N=256, Lt=8, n_pairs=40, n_trees=120, n_corr=4)
+    dag = Dag(w)
+    ctx, roots, corr, st, ex = run_gpu(w, flags=64, part=(4, 1, cc.PART_TIME), arena_mb=2048, device_leaves=True)
+    t0, t1 = time_range(w.Lt, 4, 1)
+    r_or, _ = values.run_workload(w, dag, t_range=(t0, t1))
+    assert_roots_close({k: roots[k] for k in r_or}, r_or)
+    ctx.execute(64)
+    again = {t: ctx.root_value(t, t1 - t0) for t in roots}
+    assert all(np.array_equal(again[t], roots[t]) for t in roots)

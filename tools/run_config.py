@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--parts", type=int, default=1)
     ap.add_argument("--part", type=int, default=0)
     ap.add_argument("--device-leaves", action="store_true")
+    ap.add_argument("--ozaki", action="store_true", help="MM1 on the tcgen05 INT8 Ozaki engine (execute flags bit 6)")
     a = ap.parse_args()
     w = {"c3": dags.config_c3, "c4": dags.config_c4, "c5": lambda: dags.config_c5(N=a.N)}[a.config]()
     cap = int(a.cap) if a.cap is not None else (32 * 10 ** 9 if a.config == "c4" else 0)
@@ -78,10 +79,10 @@ def main():
             ctx.set_leaf(u, h)
     print("part %d/%d: time slices [%d, %d), %d trees" % (a.part, a.parts, pt0, pt1, len(ctx.part_trees())), flush=True)
     for rep in range(2):
-        ex = ctx.execute(0)
+        ex = ctx.execute(cc.EXEC_OZAKI_MM1 if a.ozaki else 0)
         moved = ex["h2d_bytes"] + ex["d2h_bytes"]
-        print("execute %d: %.1f ms (copies done %.1f ms); moved %.2f GB -> PCIe bound %.1f ms; flops %.3g -> "
-              "FP64 bound %.1f ms" % (rep, ex["seconds"] * 1e3, ex["copy_seconds"] * 1e3, moved / 1e9,
+        print("execute %d%s: %.1f ms (copies done %.1f ms); moved %.2f GB -> PCIe bound %.1f ms; flops %.3g -> "
+              "FP64 bound %.1f ms" % (rep, " (Ozaki MM1, op-by-op)" if a.ozaki else "", ex["seconds"] * 1e3, ex["copy_seconds"] * 1e3, moved / 1e9,
                                       moved / 55.6e9 * 1e3, ex["flops"], ex["flops"] / 37.0e12 * 1e3), flush=True)
     # values are checked against the oracle by tests/test_gpu_parity.py (tools do not run it)
     os._exit(0)
