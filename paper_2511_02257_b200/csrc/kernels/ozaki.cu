@@ -19,14 +19,16 @@
 // exactly to FP64 and sums them from the least significant one up.
 //
 // Layouts (device workspace, caller-owned):
-//   SA int8 [s][Lt][Mp][Kp]   K-major rows of A_cat, Mp = roundup(N,128), Kp = 2 Nc,
-//                             Nc = roundup(N,32); K index: Re part at j, Im part at Nc + j
-//   SB int8 [s][Lt][2Nc][Kp]  K-major rows of B_cat^T; rows grouped per 32 output columns:
-//                             row 64g + w, w < 32 -> Cr column 32g + w, w >= 32 -> Ci column
+//   SA int8: K-major rows of A_cat (Mp = roundup(N,128) rows, Kp = 2 Nc bytes, Nc =
+//            roundup(N,32); K index: Re part at j, Im part at Nc + j), stored tile-contiguous
+//            and pre-swizzled as [t][row block of 128][64-byte k chunk][slice][128][64]
+//   SB int8: K-major rows of B_cat^T (2 Nc rows; rows grouped per 32 output columns: row
+//            64g + w, w < 32 -> Cr column 32g + w, w >= 32 -> Ci column), same tiling with
+//            64-row blocks
 //   eA int32 [Lt][Mp], fB int32 [Lt][Nc]
-// GEMM CTA: 128 rows x (32 complex output columns = 64 B_cat^T rows), K streamed in 64-byte
-// stages (SWIZZLE_64B TMA boxes, all s slices of A and B per stage), one lane issues the
-// tcgen05.mma's, 4 warps drain TMEM.
+// GEMM CTA (persistent): tiles of 128 rows x (32 complex output columns = 64 B_cat^T rows);
+// a stage = all s slices of A and B for one 64-byte k chunk = two contiguous bulk copies;
+// one lane issues the tcgen05.mma's, 4 warps drain TMEM.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -42,7 +44,7 @@ namespace oz {
 
 constexpr int BM = 128;     // CTA rows (UMMA M)
 constexpr int BN = 64;      // CTA B_cat^T rows (UMMA N) = 32 complex output columns
-constexpr int BKB = 64;     // K bytes per stage (one SWIZZLE_64B row)
+constexpr int BKB = 64;     // K bytes per stage = one SWIZZLE_64B smem row (SW32 measured slower)
 constexpr int UK = 32;      // K per kind::i8 MMA
 constexpr int A_TILE = BM * BKB;    // 8 KB
 constexpr int B_TILE = BN * BKB;    // 4 KB
@@ -63,6 +65,8 @@ struct Params {
   const int* fB;
   double* C;                      // complex128 [Lt][N][N] (interleaved)
   int* Craw;                      // RAW mode: int32 [Mp][Brows]
+  const int8_t* SA;               // tiled slices (tiled_off); RAW mode reads through the maps
+  const int8_t* SB;
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -82,6 +86,24 @@ __device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
   d |= uint64_t(1) << 46;
   d |= uint64_t(4) << 61;
   return d;
+}
+
+// Slice layout of the Ozaki GEMM: tile-contiguous and pre-swizzled, [t][row block][k chunk]
+// [slice][R rows][64 B], so one stage (all S slices of a k chunk) is one contiguous bulk copy
+// (R = 128 for A, 64 for B).  Within a 64-byte row the 16-byte chunk index is XORed with
+// (row >> 1) & 3: the SWIZZLE_64B pattern (byte-offset bits [4,6) ^= bits [7,9)) that TMA
+// writes and UMMA reads.
+template <int S, int R>
+__device__ __forceinline__ size_t tiled_off(int t, int row, int kbyte, int nblk, int nk) {
+  const int blk = row / R, r = row % R, kc = kbyte >> 6, c = kbyte & 63;
+  return ((((size_t(t) * nblk + blk) * nk + kc) * S) * R + r) * 64 + ((((c >> 4) ^ ((r >> 1) & 3)) << 4) | (c & 15));
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dev::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(dev::smem_u32(bar))
+               : "memory");
 }
 
 // Instruction descriptor kind::i8: D = S32 (bits 4-5 = 2), A, B signed (bits 7-9, 10-12 = 1),
@@ -147,8 +169,7 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double2* __restri
   const int t = blockIdx.y;
   if (i >= Mp) return;
   const int Kp = 2 * Nc;
-  const size_t slice_stride = size_t(Lt) * Mp * Kp;
-  int8_t* row = SA + (size_t(t) * Mp + i) * Kp;
+  const int nk = Kp / 64, nblk = Mp / 128;
   const double2* src = A + (size_t(t) * N + (i < N ? i : 0)) * N;
   double m = 0.0;
   if (i < N)
@@ -181,8 +202,8 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double2* __restri
     }
 #pragma unroll
     for (int k = 0; k < S; ++k) {
-      *reinterpret_cast<uint32_t*>(row + k * slice_stride + j0) = wr[k];
-      *reinterpret_cast<uint32_t*>(row + k * slice_stride + Nc + j0) = wi[k];
+      *reinterpret_cast<uint32_t*>(SA + tiled_off<S, 128>(t, i, j0, nblk, nk) + k * A_TILE) = wr[k];
+      *reinterpret_cast<uint32_t*>(SA + tiled_off<S, 128>(t, i, Nc + j0, nblk, nk) + k * A_TILE) = wi[k];
     }
   }
 }
@@ -224,13 +245,12 @@ __global__ void __launch_bounds__(256) split_cols_kernel(const double2* __restri
   const int g = blockIdx.x, t = blockIdx.y;
   const int c0 = 32 * g;
   const int Kp = 2 * Nc, Brows = 2 * Nc;
-  const size_t slice_stride = size_t(Lt) * Brows * Kp;
+  const int nk = Kp / 64, nblk = Brows / 64;
   const double2* src = B + size_t(t) * N * N;
   if (tid < 32) {
     const int e = fB[size_t(t) * Nc + c0 + tid];
     ecol[tid] = e < -100000 ? 0 : e;
   }
-  int8_t* rows = SB + (size_t(t) * Brows + 64 * g) * Kp;
   const int kend = min(Nc, 128 * int(blockIdx.z + 1));
   for (int k0 = 128 * blockIdx.z; k0 < kend; k0 += 32) {
     __syncthreads();
@@ -265,8 +285,8 @@ __global__ void __launch_bounds__(256) split_cols_kernel(const double2* __restri
       }
 #pragma unroll
       for (int k = 0; k < S; ++k)
-        *reinterpret_cast<uint2*>(rows + k * slice_stride + size_t(rT) * Kp + h * Nc + k0 + kq * 8) =
-            make_uint2(lo[k], hi[k]);
+        *reinterpret_cast<uint2*>(SB + tiled_off<S, 64>(t, 64 * g + rT, h * Nc + k0 + kq * 8, nblk, nk) +
+                                  k * B_TILE) = make_uint2(lo[k], hi[k]);
     }
   }
 }
@@ -327,10 +347,12 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
           dev::mbar_expect_tx(&full[st], C::STAGE);
           uint8_t* sa = smem + st * C::STAGE;
           uint8_t* sb = sa + S * A_TILE;
-#pragma unroll
-          for (int i = 0; i < S; ++i) {
-            tma_load_2d(sa + i * A_TILE, &mapA, &full[st], kc * BKB, i * p.Lt * p.Mp + rowA);
-            tma_load_2d(sb + i * B_TILE, &mapB, &full[st], kc * BKB, i * p.Lt * p.Brows + rowB);
+          if constexpr (RAW) {
+            tma_load_2d(sa, &mapA, &full[st], kc * BKB, rowA);
+            tma_load_2d(sb, &mapB, &full[st], kc * BKB, rowB);
+          } else {
+            bulk_load(sa, p.SA + ((size_t(t) * ntm + mb) * nk + kc) * (S * A_TILE), S * A_TILE, &full[st]);
+            bulk_load(sb, p.SB + ((size_t(t) * ntn + nb) * nk + kc) * (S * B_TILE), S * B_TILE, &full[st]);
           }
         }
       }
@@ -520,10 +542,8 @@ cudaError_t run_mm1(const void* A, const void* B, void* Cout, int Lt, int N, voi
                                                                                     fB, Lt, N, g.Nc);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  CUtensorMap ma, mb;
-  if (!map_i8(&ma, SA, g.Kp, uint64_t(S) * Lt * g.Mp, BM) || !map_i8(&mb, SB, g.Kp, uint64_t(S) * Lt * g.Brows, BN))
-    return cudaErrorInvalidValue;
-  Params p{Lt, N, g.Mp, g.Nc, g.Kp, g.Brows, eA, fB, static_cast<double*>(Cout), nullptr};
+  CUtensorMap ma{}, mb{};   // unused: the slices are tile-contiguous, read by bulk copies
+  Params p{Lt, N, g.Mp, g.Nc, g.Kp, g.Brows, eA, fB, static_cast<double*>(Cout), nullptr, SA, SB};
   return launch_gemm<S, false>(ma, mb, p, stream);
 }
 
@@ -551,7 +571,7 @@ cudaError_t launch_i8gemm_tn(const int8_t* A, const int8_t* B, int32_t* C, int64
   CUtensorMap ma, mb;
   if (!oz::map_i8(&ma, A, uint64_t(K), uint64_t(M), oz::BM) || !oz::map_i8(&mb, B, uint64_t(K), uint64_t(Nn), oz::BN))
     return cudaErrorInvalidValue;
-  oz::Params p{1, 0, int(M), 0, int(K), int(Nn), nullptr, nullptr, nullptr, C};
+  oz::Params p{1, 0, int(M), 0, int(K), int(Nn), nullptr, nullptr, nullptr, C, nullptr, nullptr};
   return oz::launch_gemm<1, true>(ma, mb, p, stream);
 }
 

@@ -1,5 +1,6 @@
 """Build an experiment variant of libcc.so with extra nvcc defines (e.g. -DDF_STAGES=5) into
-variants/<name>.so; select it with CC_LIB=variants/<name>.so.  Usage: build_variant.py name -DX=1 ..."""
+variants/<name>.so; select it with CC_LIB=variants/<name>.so.  Usage: build_variant.py name -DX=1 ...
+VARIANT_SRC (comma list, default "dataflow") selects the sources compiled with the defines."""
 import os
 import subprocess
 import sys
@@ -15,7 +16,7 @@ objs = []
 for src in B._sources():
     rel = os.path.relpath(src, B.CSRC).replace(os.sep, "_")
     obj = os.path.join(B.OBJ, rel + ".o")
-    if src.endswith(".cu") and "dataflow" in src:
+    if src.endswith(".cu") and any(k in src for k in os.environ.get("VARIANT_SRC", "dataflow").split(",")):
         obj = os.path.join(out_dir, name + "_" + rel + ".o")
         subprocess.run([B.NVCC] + B.ARCH + B.FLAGS + defs + ["-c", src, "-o", obj], check=True)
     objs.append(obj)
