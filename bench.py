@@ -345,6 +345,7 @@ def main():
     Lt_k, N = Lt_p, w.N
     mm1_flops = 8.0 * Lt_k * N ** 3
     step_mean = t_value / args.steps
+    ozaki = ozaki_component(ctx, cs, flush, dev, [(Lt_k, N), (2, 1024)]) if rank == 0 else None
 
     # ---- e2e: the public API from pinned host buffers ------------------------------------------------
     arena2 = torch.empty(6 << 30, dtype=torch.uint8, device=dev)
@@ -456,6 +457,7 @@ def main():
                              "tr_mm_alone": {"avg_us": tr_avg * 1e6,
                                              "gbs": 32.0 * Lt_k * N * N / tr_avg / 1e9,
                                              "frac": 32.0 * Lt_k * N * N / tr_avg / 1e9 / hbm_peak},
+                             "mm1_ozaki_tcgen05": ozaki,
                              "how": "op-by-op path (cc_execute flags 4/8): the plan's MM1 / TR_MM launches of the "
                                     "stand-alone kernels replayed alone as CUDA graphs, L2 flushed before"}},
             "plan": {"peak_bytes": pst["peak"], "transient_peak_bytes": pst["transient_peak"],
@@ -481,6 +483,52 @@ def _device_view(ptr, shape, dev):
         __cuda_array_interface__ = {"shape": (n * 2,), "typestr": "<f8", "data": (ptr, False), "version": 2}
     t = torch.as_tensor(_Holder(), device=dev)
     return t.view(torch.complex128).view(*shape)
+
+
+def int8_peak():
+    """Dense INT8 tensor peak: measured bf16 (MEASURED_PEAKS.json, burst) x the guide's nominal
+    INT8/BF16 ratio of 2 (4.5 / 2.25 PFLOP/s)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return 2.0 * float(json.load(f)["bf16_tflops"]), "2 x measured bf16 (MEASURED_PEAKS.json)"
+    except (OSError, KeyError, ValueError):
+        return 4500.0, "nominal dense INT8 (B200_PROFILING.md)"
+
+
+def ozaki_component(ctx, cs, flush, dev, shapes, slices=6):
+    """MM1 on the tcgen05 INT8 Ozaki engine (cc_mm1_ozaki) at the given (Lt, N):
+    split + GEMM time from CUDA events on the compute stream (L2 flushed before each launch,
+    median of 5), FP64-equivalent TFLOP/s (8 per complex MAC) and INT8 tensor TOPS executed
+    (slices(slices+1)/2 pair products of the 4M real embedding, 2 x 4 N^3 ops per slice)."""
+    import torch
+    from paper_2511_02257_b200 import cc
+    out = []
+    pk, src = int8_peak()
+    for (Lt, N) in shapes:
+        A = torch.empty(Lt * N * N * 2, dtype=torch.float64, device=dev)
+        B = torch.empty_like(A)
+        C = torch.empty_like(A)
+        ctx.fill_synthetic(A, Lt * N * N, 11, 1, 0, 0, 1.0 / N)
+        ctx.fill_synthetic(B, Lt * N * N, 11, 2, 0, 0, 1.0 / N)
+        ws = torch.empty(cc.cc_mm1_ozaki_workspace_bytes(Lt, N, slices), dtype=torch.uint8, device=dev)
+        ts = []
+        for _ in range(7):
+            with torch.cuda.stream(cs):
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cs)
+            ctx.mm1_ozaki(A, B, C, Lt, N, slices, ws)
+            e1.record(cs)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        t = float(np.median(ts[2:]))
+        int8_ops = 2.0 * (slices * (slices + 1) // 2) * 4.0 * Lt * N ** 3
+        out.append({"Lt": Lt, "N": N, "slices": slices, "avg_us": t * 1e6,
+                    "tflops_fp64_equiv": 8.0 * Lt * N ** 3 / t / 1e12, "int8_tops": int8_ops / t / 1e12,
+                    "int8_frac": int8_ops / t / 1e12 / pk})
+        del A, B, C, ws
+    return {"runs": out, "int8_peak_tops": pk, "peak_source": src,
+            "note": "not on the bench step (c2 runs MM1 on FP64 DMMA in df_worker); split kernels included"}
 
 
 def fp64_peak():
