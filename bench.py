@@ -495,7 +495,7 @@ def int8_peak():
         return 4500.0, "nominal dense INT8 (B200_PROFILING.md)"
 
 
-def ozaki_component(ctx, cs, flush, dev, shapes, slices=6):
+def ozaki_component(ctx, cs, flush, dev, shapes, slices=5):
     """MM1 on the tcgen05 INT8 Ozaki engine (cc_mm1_ozaki) at the given (Lt, N):
     split + GEMM time from CUDA events on the compute stream (L2 flushed before each launch,
     median of 5), FP64-equivalent TFLOP/s (8 per complex MAC) and INT8 tensor TOPS executed

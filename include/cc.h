@@ -182,7 +182,7 @@ cc_status cc_set_leaf_device(cc_ctx* ctx, int64_t leaf_id, const void* dev, size
  * executor is the dataflow one (persistent DMMA-tile and trace workers, kernels/dataflow.hpp);
  * bit 4 selects op-by-op launches instead; bit 5 records the per-item timeline
  * (cc_dataflow_profile); bit 6 runs every MM1 on the tcgen05 INT8 Ozaki engine (cc_mm1_ozaki,
- * 6 slices; implies op-by-op launches; the other kinds stay on FP64 DMMA). */
+ * 5 slices, N <= 8192; implies op-by-op launches; the other kinds stay on FP64 DMMA). */
 cc_status cc_execute(cc_ctx* ctx, int32_t flags, cc_exec_stats* stats);
 /* Enqueue-only variant (no host sync): work is ordered on the compute stream. */
 cc_status cc_execute_async(cc_ctx* ctx, int32_t flags);
@@ -225,13 +225,15 @@ cc_status cc_bb2(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt,
 cc_status cc_tr_mm(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t Lt, int32_t N);
 /* MM1 on the tcgen05 INT8 tensor cores by Ozaki splitting (DESIGN reading
  * V-6).  Same operation and layouts as cc_mm1 (C[t,i,k] = sum_j A[t,i,j] B[t,j,k], complex128
- * interleaved, [Lt][N][N], device pointers).  Each operand is split into n_slices (4..8) INT8
- * slices of 7 bits under a per-row (A) / per-column (B) power-of-two scale; the pairs (i, j)
+ * interleaved, [Lt][N][N], device pointers).  Each operand is scaled per row (A) / column (B)
+ * by a power of two and split into n_slices (4..7) signed INT8 slices (balanced base-256
+ * digits of a fixed-point value with 6 + 8 (n_slices - 1) fractional bits); the pairs (i, j)
  * with i + j <= n_slices - 1 are multiplied exactly (INT32 accumulation in TMEM) and summed in
- * FP64, so |C - AB| <= ~(n_slices + 2) 2^(4 - 7 n_slices) sum_j |A[i,:]|max |B[:,k]|max.
- * workspace: caller-owned device memory of cc_mm1_ozaki_workspace_bytes(Lt, N, n_slices) bytes
- * (0 = invalid arguments).  Runs on the ctx compute stream, does not synchronise.  Errors:
- * CC_E_INVAL (bad sizes / null pointers, N > 8192), CC_E_BUFFER_TOO_SMALL, CC_E_CUDA. */
+ * FP64: |C - AB| <~ n_slices 2^(2 - 8 n_slices) 2N max_j|A[i,:]| max_k|B[:,k]| worst case,
+ * ~sqrt(2N) times less typically (zero-mean digits).  workspace: caller-owned device memory of
+ * cc_mm1_ozaki_workspace_bytes(Lt, N, n_slices) bytes (0 = invalid arguments).  Runs on the
+ * ctx compute stream, does not synchronise.  Errors: CC_E_INVAL (bad sizes / null pointers,
+ * N > 8192: INT32 accumulator bound), CC_E_BUFFER_TOO_SMALL, CC_E_CUDA. */
 size_t cc_mm1_ozaki_workspace_bytes(int32_t Lt, int32_t N, int32_t n_slices);
 cc_status cc_mm1_ozaki(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt, int32_t N, int32_t n_slices,
                        void* workspace, size_t workspace_bytes);

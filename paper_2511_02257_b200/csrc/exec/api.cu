@@ -50,9 +50,10 @@ struct PhaseTimer {
 namespace {
 
 constexpr int64_t ALIGN = 1024;
-// INT8 slices per operand of the Ozaki MM1 engine (reading V-6: 6 x 7 bits keep the error of
-// a phase-limited MM1 below ~4e-12 relative, inside the north_star's 1e-10).
-constexpr int OZAKI_SLICES = 6;
+// INT8 slices per operand of the Ozaki MM1 engine (reading V-6: 5 balanced base-256 digits,
+// 38 bits; measured error of phase-limited MM1s ~1e-12 relative, inside the north_star's 1e-10).
+constexpr int OZAKI_SLICES = 5;
+constexpr int64_t OZAKI_MAX_N = 8192;   // INT32 accumulators: s 2^14 2N < 2^31
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 void ck(cudaError_t e, const char* what) {
@@ -367,7 +368,7 @@ void prepare_phys(cc_ctx* ctx) {
   for (const auto& n : g.nodes) has[n.op] = true;
   for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)})
     if (has[op]) gemm_ws = std::max(gemm_ws, zgemm_workspace_bytes(problem_for(op, Lt, N, S, nullptr, nullptr, nullptr), ctx->num_sms));
-  if (has[CC_MM1] && N <= 8192) gemm_ws = std::max(gemm_ws, ozaki_mm1_workspace_bytes(Lt, N, OZAKI_SLICES));
+  if (has[CC_MM1] && N <= OZAKI_MAX_N) gemm_ws = std::max(gemm_ws, ozaki_mm1_workspace_bytes(Lt, N, OZAKI_SLICES));
   const size_t trace_ws = trace_workspace_bytes(Lt, N);
   const int64_t n_trees = int64_t(g.trees.size()), n_corr = int64_t(g.corr_ids.size()), n_terms = int64_t(g.terms.size());
   const int64_t sz_gemm = round_up(int64_t(gemm_ws), ALIGN), sz_trace = round_up(int64_t(trace_ws), ALIGN);
@@ -1308,7 +1309,7 @@ void launch_contract(cc_ctx* ctx, const Node& n, const void* a, const void* b, v
     ++*nl;
     return;
   }
-  if (n.op == CC_MM1 && ctx->mm1_ozaki) {
+  if (n.op == CC_MM1 && ctx->mm1_ozaki && g.N <= OZAKI_MAX_N) {
     ck(launch_ozaki_mm1(a, b, out, g.Lt, g.N, OZAKI_SLICES, ctx->gemm_ws, ctx->gemm_ws_bytes, ctx->cs), "Ozaki MM1");
     *nl += 5;   // memset + colmax + 2 splits + GEMM
     return;
@@ -2047,7 +2048,7 @@ cc_status cc_tr_mm(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t L
 }
 
 size_t cc_mm1_ozaki_workspace_bytes(int32_t Lt, int32_t N, int32_t n_slices) {
-  if (Lt <= 0 || N <= 0 || n_slices < 4 || n_slices > 8) return 0;
+  if (Lt <= 0 || N <= 0 || N > 8192 || n_slices < 4 || n_slices > 7) return 0;
   return ozaki_mm1_workspace_bytes(Lt, N, n_slices);
 }
 
@@ -2056,7 +2057,7 @@ cc_status cc_mm1_ozaki(cc_ctx* ctx, const void* A, const void* B, void* C, int32
   if (!ctx) return CC_E_INVAL;
   API_BEGIN
   ctx->need_device();
-  if (!A || !B || !C || !workspace || Lt <= 0 || N <= 0 || N > 8192 || n_slices < 4 || n_slices > 8)
+  if (!A || !B || !C || !workspace || Lt <= 0 || N <= 0 || N > 8192 || n_slices < 4 || n_slices > 7)
     throw Error(CC_E_INVAL, "bad kernel arguments");
   if (workspace_bytes < ozaki_mm1_workspace_bytes(Lt, N, n_slices))
     throw Error(CC_E_BUFFER_TOO_SMALL, "ozaki workspace too small");

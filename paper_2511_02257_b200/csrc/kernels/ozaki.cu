@@ -10,13 +10,13 @@
 //   A_cat = [Ar | Ai]              (N x 2N, row i scaled by 2^-eA[i], eA = max-exponent of row i)
 //   B_cat = [[Br, Bi], [-Bi, Br]]  (2N x 2N, column c scaled by 2^-fB[c])
 //   so that A_cat B_cat = [Cr | Ci]  (the real embedding of the complex product, 4M form)
-//   x * 2^-e = sum_{k=0}^{s-1} 2^{-7(k+1)} x_k + r,  x_k in [-127, 127] (truncation, exact in
-//   FP64), |r| < 2^-7s.
-//   C ~= 2^{eA+fB} sum_{i+j <= s-1} 2^{-7(i+j+2)} (A_i B_j)      (pairs below the anti-diagonal
-//   cut are dropped, the standard Ozaki truncation)
-// Every (i, j) with i + j = d accumulates into one INT32 TMEM accumulator d (|acc| <= s 127^2 K
-// < 2^31 for K = 2N <= 2^14), so the epilogue sees s accumulators per output, converts each
-// exactly to FP64 and sums them from the least significant one up.
+//   x * 2^-e = sum_{k=0}^{s-1} 2^{-6-8k} x_k + r   (balanced base-256 digits of the fixed-point
+//   value round(x 2^{6+8(s-1)})): x_0 in [-65, 65], x_k in [-128, 127], |r| <= 2^{-7-8(s-1)}.
+//   C ~= 2^{eA+fB} sum_{i+j <= s-1} 2^{-12-8(i+j)} (A_i B_j)    (pairs below the anti-diagonal
+//   cut are dropped, the standard Ozaki truncation); each pair is one signed kind::i8 MMA.
+// Every (i, j) with i + j = d accumulates into one INT32 TMEM accumulator d (|acc| <= s 2^14 K
+// < 2^31 for K = 2N <= 16384, s <= 7), so the epilogue sees s accumulators per output, converts
+// each exactly to FP64 and sums them, most significant first.
 //
 // Layouts (device workspace, caller-owned):
 //   SA int8: K-major rows of A_cat (Mp = roundup(N,128) rows, Kp = 2 Nc bytes, Nc =
@@ -136,18 +136,23 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // ---------------------------------------------------------------------------------------
 // Splitting kernels
 
-// x in (-1, 1) -> S int8 slices of 7 bits, truncated toward zero (sign-magnitude: every slice
-// has the sign of x).  |x| 2^56 < 2^56 is converted exactly up to the bits below 2^-56, which
-// lie beyond the last slice (S <= 8: 7 S <= 56); slice k = bits [49-7k, 56-7k) of |x| 2^56.
+// x in (-1, 1) -> S signed slices (balanced base-256 digits) of m = round(x 2^F), F = 6 + 8 (S-1):
+// from the least significant end, digit = low byte read as int8 (in [-128, 127]) and
+// m = (m - digit) / 256 (exact); the top digit is what remains, |top| <= 2^6 + 1.  All slices
+// are signed and zero-mean, so the truncated pair products (i + j >= S) and the rounding of x
+// (|x - m 2^-F| <= 2^-F-1) add incoherently.  x 2^F is an exact power-of-two scaling.
 template <int S>
 __device__ __forceinline__ void split_value(double x, int8_t (&q)[S]) {
-  const long long m = __double2ll_rz(x * 72057594037927936.0);   // 2^56
-  const unsigned long long a = static_cast<unsigned long long>(m < 0 ? -m : m);
+  constexpr int F = 6 + 8 * (S - 1);
+  static_assert(F <= 62, "slices exceed int64");
+  long long r = __double2ll_rn(x * static_cast<double>(1ll << F));
 #pragma unroll
-  for (int k = 0; k < S; ++k) {
-    const int v = int((a >> (49 - 7 * k)) & 127ull);
-    q[k] = int8_t(m < 0 ? -v : v);
+  for (int k = S - 1; k >= 1; --k) {
+    const int dgt = int(int8_t(uint8_t(r & 255)));
+    q[k] = int8_t(dgt);
+    r = (r - dgt) >> 8;
   }
+  q[0] = int8_t(r);
 }
 
 // 2^k for |k| <= 1000 (exact; the exponents here come from ilogb of finite data)
@@ -424,7 +429,7 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
           tc_fence_before();
           __syncwarp();
           if (lane == 0) dev::mbar_arrive(&drained[d]);
-          const double w = pow2(-7 * (d + 2));
+          const double w = pow2(-12 - 8 * d);
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
             ar[q] = fma(double(vr[q]), w, ar[q]);
@@ -560,7 +565,6 @@ cudaError_t launch_ozaki_mm1(const void* A, const void* B, void* C, int64_t Lt, 
     case 5: return oz::run_mm1<5>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
     case 6: return oz::run_mm1<6>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
     case 7: return oz::run_mm1<7>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
-    case 8: return oz::run_mm1<8>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -15,7 +15,7 @@ for Lt, N in sizes:
     A = torch.rand(Lt * N * N * 2, dtype=torch.float64, device=dev) + 0.5
     B = torch.rand(Lt * N * N * 2, dtype=torch.float64, device=dev) + 0.5
     C = torch.empty_like(A)
-    ws = torch.empty(cc.cc_mm1_ozaki_workspace_bytes(Lt, N, 6), dtype=torch.uint8, device=dev)
+    ws = torch.empty(cc.cc_mm1_ozaki_workspace_bytes(Lt, N, 5), dtype=torch.uint8, device=dev)
     for _ in range(2):
-        ctx.mm1_ozaki(A, B, C, Lt, N, 6, ws)
+        ctx.mm1_ozaki(A, B, C, Lt, N, 5, ws)
     torch.cuda.synchronize()
