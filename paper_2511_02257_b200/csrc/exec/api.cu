@@ -51,7 +51,7 @@ namespace {
 
 constexpr int64_t ALIGN = 1024;
 // INT8 slices per operand of the Ozaki MM1 engine (reading V-6: 5 balanced base-256 digits,
-// 38 bits; measured error of phase-limited MM1s ~1e-12 relative, inside the north_star's 1e-10).
+// 38 bits; phase-limited MM1 errors <= 1e-11 relative in the tests, inside the 1e-10 bar).
 constexpr int OZAKI_SLICES = 5;
 constexpr int64_t OZAKI_MAX_N = 8192;   // INT32 accumulators: s 2^14 2N < 2^31
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }

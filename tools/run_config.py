@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--part", type=int, default=0)
     ap.add_argument("--device-leaves", action="store_true")
     ap.add_argument("--ozaki", action="store_true", help="MM1 on the tcgen05 INT8 Ozaki engine (execute flags bit 6)")
+    ap.add_argument("--breakdown", action="store_true",
+                    help="one more op-by-op execute with every kernel timed (flags bit 1): time per op kind")
     a = ap.parse_args()
     w = {"c3": dags.config_c3, "c4": dags.config_c4, "c5": lambda: dags.config_c5(N=a.N)}[a.config]()
     cap = int(a.cap) if a.cap is not None else (32 * 10 ** 9 if a.config == "c4" else 0)
@@ -84,6 +86,19 @@ def main():
         print("execute %d%s: %.1f ms (copies done %.1f ms); moved %.2f GB -> PCIe bound %.1f ms; flops %.3g -> "
               "FP64 bound %.1f ms" % (rep, " (Ozaki MM1, op-by-op)" if a.ozaki else "", ex["seconds"] * 1e3, ex["copy_seconds"] * 1e3, moved / 1e9,
                                       moved / 55.6e9 * 1e3, ex["flops"], ex["flops"] / 37.0e12 * 1e3), flush=True)
+    if a.breakdown:
+        ctx.execute(cc.EXEC_TIME_KERNELS | (cc.EXEC_OZAKI_MM1 if a.ozaki else 0))
+        secs, cnts = ctx.kernel_times()
+        Lt_p, N = pt1 - pt0, w.N
+        names = {2: "MM1", 3: "BM1", 4: "BB2", 5: "TR_MM"}
+        for k, nm in names.items():
+            if cnts[k]:
+                extra = ""
+                if k == 2:
+                    extra = ", %.1f TF/s (8 flop/cMAC)" % (8.0 * Lt_p * N ** 3 * cnts[k] / secs[k] / 1e12)
+                if k == 5:
+                    extra = ", %.0f GB/s algorithmic" % (32.0 * Lt_p * N * N * cnts[k] / secs[k] / 1e9)
+                print("  %s: %d launches, %.1f ms%s" % (nm, cnts[k], secs[k] * 1e3, extra), flush=True)
     # values are checked against the oracle by tests/test_gpu_parity.py (tools do not run it)
     os._exit(0)
 
