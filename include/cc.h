@@ -245,7 +245,8 @@ cc_status cc_i8gemm_tn(cc_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C
  * n complex elements starting at flat element e0 of leaf `leaf_id`, written to dev. */
 cc_status cc_fill_synthetic(cc_ctx* ctx, void* dev, int64_t n, uint64_t seed, int64_t leaf_id,
                             int64_t e0, int32_t mode, double sigma);
-/* Bytes of kernel workspace the ctx reserves at the top of the arena. */
+/* Bytes of kernel workspace the ctx reserves at the top of the arena (plus, for DAGs with MM1
+ * ops, the Ozaki leaf-form cache of execute flags bit 6 when it needs at most 1/8 of the arena). */
 size_t cc_scratch_bytes(int32_t Lt, int32_t N, int32_t S);
 
 #ifdef __cplusplus

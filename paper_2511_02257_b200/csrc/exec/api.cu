@@ -70,6 +70,15 @@ struct KindTimes {
 struct cc_ctx {
   int device = -1;
   bool mm1_ozaki = false;     // execute flags bit 6: MM1 on the tcgen05 Ozaki engine (op-by-op)
+  // Ozaki leaf-form cache: INT8 slices of leaves, split once per execute and shared by every
+  // MM1 reading that leaf in the same role, placed in the pool above the plan's high water
+  struct {
+    std::vector<OzakiForm> form[2];
+    std::vector<char> have[2];
+    int64_t off = 0, end = 0;
+  } oz;
+  char* oz_scratch = nullptr;          // reserved leaf-form cache (scratch), may be empty
+  int64_t oz_scratch_bytes = 0;
   bool host_only = true;
   char* arena = nullptr;
   int64_t arena_bytes = 0;
@@ -369,6 +378,22 @@ void prepare_phys(cc_ctx* ctx) {
   for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)})
     if (has[op]) gemm_ws = std::max(gemm_ws, zgemm_workspace_bytes(problem_for(op, Lt, N, S, nullptr, nullptr, nullptr), ctx->num_sms));
   if (has[CC_MM1] && N <= OZAKI_MAX_N) gemm_ws = std::max(gemm_ws, ozaki_mm1_workspace_bytes(Lt, N, OZAKI_SLICES));
+  // Ozaki leaf-form cache (execute flags bit 6): one A-form per leaf read as a left MM1
+  // operand, one B-form per leaf read as a right one; reserved when it takes at most 1/8 of
+  // the arena (else the cache uses whatever pool space the plan leaves free)
+  int64_t sz_ozc = 0;
+  if (has[CC_MM1] && N <= OZAKI_MAX_N) {
+    std::vector<char> role(g.nodes.size(), 0);
+    for (const auto& n : g.nodes)
+      if (n.op == CC_MM1) {
+        if (g.nodes[size_t(n.l)].leaf()) role[size_t(n.l)] |= 1;
+        if (g.nodes[size_t(n.r)].leaf()) role[size_t(n.r)] |= 2;
+      }
+    const int64_t fa = round_up(int64_t(ozaki_form_bytes(Lt, N, OZAKI_SLICES, false)), ALIGN);
+    const int64_t fb = round_up(int64_t(ozaki_form_bytes(Lt, N, OZAKI_SLICES, true)), ALIGN);
+    for (char r : role) sz_ozc += ((r & 1) ? fa : 0) + ((r & 2) ? fb : 0);
+    if (sz_ozc > ctx->arena_bytes / 8) sz_ozc = 0;
+  }
   const size_t trace_ws = trace_workspace_bytes(Lt, N);
   const int64_t n_trees = int64_t(g.trees.size()), n_corr = int64_t(g.corr_ids.size()), n_terms = int64_t(g.terms.size());
   const int64_t sz_gemm = round_up(int64_t(gemm_ws), ALIGN), sz_trace = round_up(int64_t(trace_ws), ALIGN);
@@ -392,7 +417,7 @@ void prepare_phys(cc_ctx* ctx) {
   ctx->df_trace_slot = round_up(Lt * df_trace_pieces(Lt, N) * 16, ALIGN) + round_up(Lt * 4, ALIGN);
   const int64_t sz_df_chunk = DF_CHUNK_RING * (ctx->df_chunk_slot + ctx->df_chunk_cnt_slot);
   const int64_t sz_df_trace = DF_TRACE_RING * ctx->df_trace_slot;
-  const int64_t scratch = sz_gemm + sz_trace + sz_roots + sz_corr + sz_ts + sz_tt + sz_tc + sz_df_chunk + sz_df_trace;
+  const int64_t scratch = sz_gemm + sz_trace + sz_roots + sz_corr + sz_ts + sz_tt + sz_tc + sz_df_chunk + sz_df_trace + sz_ozc;
   const int64_t pool = (ctx->arena_bytes - scratch) / ALIGN * ALIGN;
   if (pool <= 0) throw Error(CC_E_NOMEM, "arena too small for the kernel workspace (" + std::to_string(scratch) + " B)");
   ctx->pool_bytes = pool;
@@ -406,6 +431,7 @@ void prepare_phys(cc_ctx* ctx) {
   ctx->term_coef = reinterpret_cast<double*>(s); s += sz_tc;
   ctx->df_chunk_ws = s; s += sz_df_chunk;
   ctx->df_trace_ws = s; s += sz_df_trace;
+  ctx->oz_scratch = s; ctx->oz_scratch_bytes = sz_ozc; s += sz_ozc;
   // every upload / clear is ordered on the compute stream (the copy streams may already be
   // busy; a legacy-stream cudaMemcpy from pageable memory can return before its DMA lands)
   if (sz_df_chunk > 0) ck(cudaMemsetAsync(ctx->df_chunk_ws, 0, size_t(sz_df_chunk), ctx->cs), "dataflow workspace");
@@ -1301,6 +1327,46 @@ int issue_dataflow(cc_ctx* ctx, bool time_copies = false) {
   return nl;
 }
 
+// Resets the Ozaki leaf-form cache for one execute (or one kernel-only capture): the free
+// pool range above the plan's high water, below any dataflow metadata / sync area placed at
+// the top of the pool.  CC_OZAKI_LEAF_CACHE=0 disables it.
+void oz_cache_reset(cc_ctx* ctx) {
+  const size_t n = ctx->dag->nodes.size();
+  for (int k = 0; k < 2; ++k) {
+    ctx->oz.form[k].assign(n, OzakiForm{nullptr, nullptr});
+    ctx->oz.have[k].assign(n, 0);
+  }
+  int64_t end = ctx->pool_bytes;
+  if (ctx->df_sync_base) end = std::min<int64_t>(end, ctx->df_sync_base - ctx->arena);
+  if (ctx->df_meta && !ctx->df_meta_owned) end = std::min<int64_t>(end, ctx->df_meta - ctx->arena);
+  if (ctx->df_fpart && !ctx->df_fpart_owned) end = std::min<int64_t>(end, reinterpret_cast<char*>(ctx->df_fpart) - ctx->arena);
+  const char* env = getenv("CC_OZAKI_LEAF_CACHE");
+  const bool off = env && atoi(env) == 0;
+  if (ctx->oz_scratch_bytes > 0) {            // offsets relative to the arena base
+    ctx->oz.off = ctx->oz_scratch - ctx->arena;
+    ctx->oz.end = off ? ctx->oz.off : ctx->oz.off + ctx->oz_scratch_bytes;
+  } else {
+    ctx->oz.off = round_up(ctx->pp.pool_high_water, ALIGN);
+    ctx->oz.end = off ? ctx->oz.off : end;
+  }
+}
+
+// The A-form (as_b false) or B-form of operand node `u` if it is a leaf with room in the
+// cache (made now, on the compute stream, at its first use), else nullptr.
+const OzakiForm* oz_leaf_form(cc_ctx* ctx, int32_t u, const void* x, bool as_b) {
+  const Dag& g = *ctx->dag;
+  if (u < 0 || !g.nodes[size_t(u)].leaf()) return nullptr;
+  const int k = as_b ? 1 : 0;
+  if (ctx->oz.have[k][size_t(u)]) return &ctx->oz.form[k][size_t(u)];
+  const int64_t bytes = round_up(int64_t(ozaki_form_bytes(g.Lt, g.N, OZAKI_SLICES, as_b)), ALIGN);
+  if (ctx->oz.off + bytes > ctx->oz.end) return nullptr;
+  ck(launch_ozaki_form(x, g.Lt, g.N, OZAKI_SLICES, as_b, ctx->arena + ctx->oz.off, &ctx->oz.form[k][size_t(u)], ctx->cs),
+     "Ozaki leaf split");
+  ctx->oz.off += bytes;
+  ctx->oz.have[k][size_t(u)] = 1;
+  return &ctx->oz.form[k][size_t(u)];
+}
+
 void launch_contract(cc_ctx* ctx, const Node& n, const void* a, const void* b, void* out, int64_t root_slot,
                      int* nl) {
   const Dag& g = *ctx->dag;
@@ -1310,8 +1376,11 @@ void launch_contract(cc_ctx* ctx, const Node& n, const void* a, const void* b, v
     return;
   }
   if (n.op == CC_MM1 && ctx->mm1_ozaki && g.N <= OZAKI_MAX_N) {
-    ck(launch_ozaki_mm1(a, b, out, g.Lt, g.N, OZAKI_SLICES, ctx->gemm_ws, ctx->gemm_ws_bytes, ctx->cs), "Ozaki MM1");
-    *nl += 5;   // memset + colmax + 2 splits + GEMM
+    const OzakiForm* fa = oz_leaf_form(ctx, n.l, a, false);
+    const OzakiForm* fb = oz_leaf_form(ctx, n.r, b, true);
+    ck(launch_ozaki_mm1(a, b, out, g.Lt, g.N, OZAKI_SLICES, ctx->gemm_ws, ctx->gemm_ws_bytes, ctx->cs, fa, fb),
+       "Ozaki MM1");
+    *nl += 5;   // (memset + colmax + 2 splits, or cached leaf forms made once) + GEMM
     return;
   }
   ZgemmProblem p = problem_for(n.op, g.Lt, g.N, g.S, a, b, out);
@@ -1456,6 +1525,7 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
   prepare_phys(ctx);
   ctx->mm1_ozaki = (flags & 64) != 0;
+  if (ctx->mm1_ozaki) oz_cache_reset(ctx);
   if (flags & 12) {
     kernel_only(ctx, (flags & 4) ? 0 : 1, stats);
     return;

@@ -54,8 +54,20 @@ cudaError_t trace_preload();
 // MM1 by Ozaki splitting on tcgen05 INT8 tensor cores (ozaki.cu): C[t] = A[t] B[t], complex128
 // [Lt][N][N], n_slices in 4..8 INT8 slices per operand; workspace holds the slices + scales.
 size_t ozaki_mm1_workspace_bytes(int64_t Lt, int64_t N, int slices);
+// A pre-split operand: INT8 slices (tile-contiguous) + power-of-two exponents, in the A-form
+// (rows of A_cat) or the B-form (columns of B_cat); made once and shared by every MM1 that
+// reads the same tensor in the same role.
+struct OzakiForm {
+  const void* slices;
+  const int* exps;
+};
+size_t ozaki_form_bytes(int64_t Lt, int64_t N, int slices, bool as_b);
+cudaError_t launch_ozaki_form(const void* X, int64_t Lt, int64_t N, int slices, bool as_b, void* dst,
+                              OzakiForm* form, cudaStream_t stream);
+// fa / fb: pre-split operands (nullptr: split A / B into the workspace first).
 cudaError_t launch_ozaki_mm1(const void* A, const void* B, void* C, int64_t Lt, int64_t N, int slices, void* ws,
-                             size_t ws_bytes, cudaStream_t stream);
+                             size_t ws_bytes, cudaStream_t stream, const OzakiForm* fa = nullptr,
+                             const OzakiForm* fb = nullptr);
 // Plain INT8 GEMM on the same tcgen05 machinery: C[m][n] = sum_k A[m][k] B[n][k] (int32).
 cudaError_t launch_i8gemm_tn(const int8_t* A, const int8_t* B, int32_t* C, int64_t M, int64_t Nn, int64_t K,
                              cudaStream_t stream);

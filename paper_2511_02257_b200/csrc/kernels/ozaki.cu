@@ -529,27 +529,66 @@ cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const Para
 }
 
 template <int S>
-cudaError_t run_mm1(const void* A, const void* B, void* Cout, int Lt, int N, void* ws, size_t ws_bytes,
-                    cudaStream_t stream) {
-  const Geometry g = geometry(Lt, N, S);
-  if (ws_bytes < g.total) return cudaErrorInvalidValue;
-  uint8_t* w = static_cast<uint8_t*>(ws);
-  int8_t* SA = reinterpret_cast<int8_t*>(w + g.sa);
-  int8_t* SB = reinterpret_cast<int8_t*>(w + g.sb);
-  int* eA = reinterpret_cast<int*>(w + g.ea);
-  int* fB = reinterpret_cast<int*>(w + g.fb);
+void split_a(const void* A, int8_t* SA, int* eA, int Lt, int N, const Geometry& g, cudaStream_t stream) {
   split_rows_kernel<S><<<dim3(g.Mp / 8, Lt), 256, 0, stream>>>(static_cast<const double2*>(A), SA, eA, Lt, N, g.Mp,
                                                                g.Nc);
+}
+
+template <int S>
+cudaError_t split_b(const void* B, int8_t* SB, int* fB, int Lt, int N, const Geometry& g, cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(fB, 0x80, size_t(Lt) * g.Nc * 4, stream);   // INT_MIN-like
   if (e != cudaSuccess) return e;
   colmax_kernel<<<dim3(g.Nc / 32, Lt, (N + 127) / 128), 256, 0, stream>>>(static_cast<const double2*>(B), fB, N, g.Nc);
   split_cols_kernel<S><<<dim3(g.Nc / 32, Lt, (g.Nc + 127) / 128), 256, 0, stream>>>(static_cast<const double2*>(B), SB,
                                                                                     fB, Lt, N, g.Nc);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+template <int S>
+cudaError_t gemm(const int8_t* SA, const int* eA, const int8_t* SB, const int* fB, void* Cout, int Lt, int N,
+                 const Geometry& g, cudaStream_t stream) {
   CUtensorMap ma{}, mb{};   // unused: the slices are tile-contiguous, read by bulk copies
   Params p{Lt, N, g.Mp, g.Nc, g.Kp, g.Brows, eA, fB, static_cast<double*>(Cout), nullptr, SA, SB};
   return launch_gemm<S, false>(ma, mb, p, stream);
+}
+
+template <int S>
+cudaError_t run_mm1(const void* A, const void* B, void* Cout, int Lt, int N, void* ws, size_t ws_bytes,
+                    const OzakiForm* fa, const OzakiForm* fb, cudaStream_t stream) {
+  const Geometry g = geometry(Lt, N, S);
+  if (ws_bytes < g.total) return cudaErrorInvalidValue;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  const int8_t* SA = reinterpret_cast<int8_t*>(w + g.sa);
+  const int8_t* SB = reinterpret_cast<int8_t*>(w + g.sb);
+  const int* eA = reinterpret_cast<int*>(w + g.ea);
+  const int* fB = reinterpret_cast<int*>(w + g.fb);
+  if (fa) {
+    SA = static_cast<const int8_t*>(fa->slices);
+    eA = fa->exps;
+  } else {
+    split_a<S>(A, reinterpret_cast<int8_t*>(w + g.sa), reinterpret_cast<int*>(w + g.ea), Lt, N, g, stream);
+  }
+  if (fb) {
+    SB = static_cast<const int8_t*>(fb->slices);
+    fB = fb->exps;
+  } else {
+    cudaError_t e = split_b<S>(B, reinterpret_cast<int8_t*>(w + g.sb), reinterpret_cast<int*>(w + g.fb), Lt, N, g, stream);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return gemm<S>(SA, eA, SB, fB, Cout, Lt, N, g, stream);
+}
+
+template <int S>
+cudaError_t make_form(const void* X, int Lt, int N, bool as_b, void* dst, cudaStream_t stream) {
+  const Geometry g = geometry(Lt, N, S);
+  uint8_t* d = static_cast<uint8_t*>(dst);
+  if (!as_b) {
+    split_a<S>(X, reinterpret_cast<int8_t*>(d), reinterpret_cast<int*>(d + (g.sb - g.sa)), Lt, N, g, stream);
+    return cudaGetLastError();
+  }
+  return split_b<S>(X, reinterpret_cast<int8_t*>(d), reinterpret_cast<int*>(d + (g.ea - g.sb)), Lt, N, g, stream);
 }
 
 }  // namespace oz
@@ -558,13 +597,34 @@ size_t ozaki_mm1_workspace_bytes(int64_t Lt, int64_t N, int slices) {
   return oz::geometry(int(Lt), int(N), slices).total;
 }
 
-cudaError_t launch_ozaki_mm1(const void* A, const void* B, void* C, int64_t Lt, int64_t N, int slices, void* ws,
-                             size_t ws_bytes, cudaStream_t stream) {
+// A-form (row slices + row exponents) / B-form (column slices + column exponents) of one
+// operand, as one buffer: slices first, exponents after (256-byte aligned).
+size_t ozaki_form_bytes(int64_t Lt, int64_t N, int slices, bool as_b) {
+  const oz::Geometry g = oz::geometry(int(Lt), int(N), slices);
+  return as_b ? (g.ea - g.sb) + (g.total - g.fb) : (g.sb - g.sa) + (g.fb - g.ea);
+}
+
+cudaError_t launch_ozaki_form(const void* X, int64_t Lt, int64_t N, int slices, bool as_b, void* dst,
+                              OzakiForm* form, cudaStream_t stream) {
+  const oz::Geometry g = oz::geometry(int(Lt), int(N), slices);
+  form->slices = dst;
+  form->exps = reinterpret_cast<const int*>(static_cast<uint8_t*>(dst) + (as_b ? (g.ea - g.sb) : (g.sb - g.sa)));
   switch (slices) {
-    case 4: return oz::run_mm1<4>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
-    case 5: return oz::run_mm1<5>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
-    case 6: return oz::run_mm1<6>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
-    case 7: return oz::run_mm1<7>(A, B, C, int(Lt), int(N), ws, ws_bytes, stream);
+    case 4: return oz::make_form<4>(X, int(Lt), int(N), as_b, dst, stream);
+    case 5: return oz::make_form<5>(X, int(Lt), int(N), as_b, dst, stream);
+    case 6: return oz::make_form<6>(X, int(Lt), int(N), as_b, dst, stream);
+    case 7: return oz::make_form<7>(X, int(Lt), int(N), as_b, dst, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_ozaki_mm1(const void* A, const void* B, void* C, int64_t Lt, int64_t N, int slices, void* ws,
+                             size_t ws_bytes, cudaStream_t stream, const OzakiForm* fa, const OzakiForm* fb) {
+  switch (slices) {
+    case 4: return oz::run_mm1<4>(A, B, C, int(Lt), int(N), ws, ws_bytes, fa, fb, stream);
+    case 5: return oz::run_mm1<5>(A, B, C, int(Lt), int(N), ws, ws_bytes, fa, fb, stream);
+    case 6: return oz::run_mm1<6>(A, B, C, int(Lt), int(N), ws, ws_bytes, fa, fb, stream);
+    case 7: return oz::run_mm1<7>(A, B, C, int(Lt), int(N), ws, ws_bytes, fa, fb, stream);
     default: return cudaErrorInvalidValue;
   }
 }

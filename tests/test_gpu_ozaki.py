@@ -139,3 +139,21 @@ def test_mm1_ozaki_error_margin_large_N(ctx):
     err4 = float(np.max(np.abs(_run(ctx, A, B, Lt, N, 4) - want) / np.abs(want)))
     assert err5 <= 1e-11, err5
     assert err4 > 10 * err5, (err4, err5)
+
+
+def test_executor_ozaki_leaf_form_cache_bitwise(monkeypatch):
+    """Leaves split once per execute and shared by their MM1s (cache in the free pool above the
+    plan's high water) give bit-identical roots to splitting per MM1 (CC_OZAKI_LEAF_CACHE=0):
+    the slices are a deterministic function of the leaf."""
+    from synth import dags
+    from oracle.dag import Dag
+    from gpu_helpers import run_gpu, assert_roots_close
+    w = dags.config_c2(N=64, Lt=4, n_loop4=50, n_loop2=4, n_corr=3)
+    dag = Dag(w)
+    ctx, roots, corr, st, ex = run_gpu(w, flags=64, arena_mb=512)
+    r_or, _ = values.run_workload(w, dag)
+    assert_roots_close(roots, r_or)
+    monkeypatch.setenv("CC_OZAKI_LEAF_CACHE", "0")
+    ctx.execute(64)
+    again = {t: ctx.root_value(t, w.Lt) for t in roots}
+    assert all(np.array_equal(again[t], roots[t]) for t in roots)
