@@ -15,6 +15,9 @@
 namespace cc {
 namespace {
 
+#ifndef TR_MINB
+#define TR_MINB 2
+#endif
 constexpr int TB = 32;          // block edge (complex elements)
 constexpr int TR_THREADS = 256; // 8 warps; warp w owns rows w, w+8, w+16, w+24 of a block
 constexpr int RPW = TB / 8;     // rows per warp
@@ -42,7 +45,7 @@ __device__ __forceinline__ void load_unit(const double2* __restrict__ At, const 
   }
 }
 
-__global__ void __launch_bounds__(TR_THREADS, 2)
+__global__ void __launch_bounds__(TR_THREADS, TR_MINB)
     trace_kernel(const double2* __restrict__ A, const double2* __restrict__ B, double2* __restrict__ out, int64_t N,
                  int nb, int P, double2* __restrict__ partials, int* __restrict__ counters) {
   __shared__ double2 sB[TB][TB + 1];
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(TR_THREADS, 2)
 
 int trace_pieces(int64_t Lt, int64_t N) {
   const int64_t nb = (N + TB - 1) / TB, U = nb * nb;
-  int64_t P = (2 * 148) / Lt;   // all CTAs resident at 2 per SM
+  int64_t P = (TR_MINB * 148) / Lt;   // all CTAs resident at TR_MINB per SM
   if (P > U) P = U;
   if (P < 1) P = 1;
   return int(P);

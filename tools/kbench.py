@@ -39,6 +39,7 @@ def timeit(fn, stream, reps=10, warm=3, flush=None, inner=20):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default=None, help="run only cases of this kind (MM1, BM1, BB2, TR)")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     streams = [torch.cuda.Stream() for _ in range(3)]
@@ -54,7 +55,9 @@ def main():
     cases = [("MM1", 64, 128, 1), ("MM1", 128, 256, 1), ("MM1", 128, 512, 1)]
     if not a.quick:
         cases += [("MM1", 4, 32, 1), ("MM1", 128, 1024, 1), ("BM1", 32, 64, 64), ("BB2", 32, 64, 64),
-                  ("BM1", 1, 128, 64), ("BB2", 1, 128, 64), ("TR", 64, 128, 1), ("TR", 128, 1024, 1)]
+                  ("BM1", 1, 128, 64), ("BB2", 1, 128, 64), ("TR", 64, 128, 1), ("TR", 128, 1024, 1), ("TR", 8, 1024, 1), ("TR", 16, 512, 1)]
+    if a.only:
+        cases = [c for c in cases if c[0] == a.only]
     for kind, Lt, N, S in cases:
         if kind == "MM1":
             A, B, C = rnd(Lt * N * N), rnd(Lt * N * N), rnd(Lt * N * N)
