@@ -75,9 +75,14 @@ typedef struct { int64_t corr_id; int64_t tree_id; double re, im; } cc_term;
  * RS-GS comparison of §IV) under DESIGN.md readings R-1..R-4. */
 typedef enum { CC_SIBLING = 0, CC_TREE = 1, CC_GIVEN = 2, CC_RSGS = 3 } cc_algo;
 
+/* cc_sched_cfg.flags bit 0: evict by next use instead of LRU (reading E-9; the
+ * whole schedule is known offline, so the victim is the resident non-operand whose next read
+ * is farthest away, ties to the least recently used). */
+#define CC_EVICT_NEXT_USE 1
+
 typedef struct {
   int32_t algo;               /* cc_algo                                                   */
-  int32_t flags;              /* reserved, 0                                               */
+  int32_t flags;              /* CC_EVICT_NEXT_USE or 0 (LRU)                              */
   uint64_t seed;              /* reserved (reading S-1 pins the "random leaf" to lowest id) */
   int64_t cap_bytes;          /* device pool capacity for the LRU plan; <= 0: unbounded     */
   const int64_t* given_order; /* CC_GIVEN: contraction order (node ids), n_given entries    */

@@ -15,6 +15,11 @@ follows DESIGN.md readings E-1..E-8:
   E-5 #transfers = h2d_count + d2h_count.
   E-8 tensors nothing depends on are released at once (never "evicted").
 Leaves are fetched lazily at first use (G-6).  Release follows §II-C.
+
+policy="next_use" (reading E-9; SURVEY f3 "Belady/next-use eviction, since the whole
+schedule is known offline"): the victim is the resident non-operand of c_i whose next use
+(the first later contraction that reads it) is farthest away; ties go to the least recently
+used (E-2 clock).  Everything else (E-1..E-8) is unchanged.
 """
 
 
@@ -22,8 +27,18 @@ class InfeasibleError(Exception):
     pass
 
 
-def plan(dag, order, cap=None):
-    """Replay `order` on a device of `cap` bytes (None or <= 0: unbounded).
+def _next_uses(dag, order):
+    """uses[x] = ascending list of the steps i whose contraction reads x."""
+    uses = {}
+    for i, u in enumerate(order):
+        for x in dag.nodes[u].child:
+            uses.setdefault(x, []).append(i)
+    return uses
+
+
+def plan(dag, order, cap=None, policy="lru"):
+    """Replay `order` on a device of `cap` bytes (None or <= 0: unbounded); policy "lru"
+    (E-1) or "next_use" (E-9).
 
     Returns dict: ops [(kind, node)], kinds in {"D2H","DROP","H2D","CONTRACT","FREE"}
     ("D2H" = eviction with a copy to host, "DROP" = eviction without copy),
@@ -45,7 +60,13 @@ def plan(dag, order, cap=None):
               peak=0, transient_peak=0, host_peak_bytes=0)
     ops = []
     used_trace = [0]
-    for u in order:
+    uses = _next_uses(dag, order)
+    ptr = {x: 0 for x in uses}          # uses[x][ptr[x]] = next step reading x
+
+    def next_use(x):
+        return uses[x][ptr[x]]
+
+    for i, u in enumerate(order):
         n = nodes[u]
         operands = list(n.child)
         work = sum(nodes[x].size for x in operands) + n.size
@@ -53,7 +74,11 @@ def plan(dag, order, cap=None):
             raise InfeasibleError("contraction %d needs %d bytes > cap %d" % (u, work, cap))
         need = sum(nodes[x].size for x in operands if x not in resident) + n.size
         while cap is not None and used + need > cap:          # E-1
-            victim = min((x for x in resident if x not in operands), key=lambda x: lru[x])
+            cands = [x for x in resident if x not in operands]
+            if policy == "next_use":                              # E-9: farthest next use
+                victim = max(cands, key=lambda x: (next_use(x), -lru[x]))
+            else:
+                victim = min(cands, key=lambda x: lru[x])
             st["evictions"] += 1
             if nodes[victim].child and victim not in host_copy:   # E-4 first eviction
                 st["d2h_count"] += 1
@@ -66,6 +91,8 @@ def plan(dag, order, cap=None):
                 ops.append(("DROP", victim))
             resident.discard(victim)
             used -= nodes[victim].size
+        for x in operands:                                         # this step's use is consumed
+            ptr[x] += 1
         for x in operands:                                         # fetch + touch (E-2)
             if x not in resident:
                 st["h2d_count"] += 1

@@ -25,6 +25,7 @@ CC_SIBLING, CC_TREE, CC_GIVEN, CC_RSGS = range(4)
 PART_TIME, PART_TREES = 0, 1
 EXEC_GRAPH, EXEC_TIME_KERNELS, EXEC_ONLY_GEMM, EXEC_ONLY_TRACE, EXEC_OP_BY_OP, EXEC_PROFILE = 1, 2, 4, 8, 16, 32
 EXEC_OZAKI_MM1 = 64
+CC_EVICT_NEXT_USE = 1       # cc_sched_cfg.flags: next-use (Belady) eviction, reading E-9
 STATUS = {0: "OK", -1: "INVAL", -2: "PARSE", -3: "CYCLE", -4: "INCONSISTENT", -5: "MULTIROOT",
           -6: "UNKNOWN_NODE", -7: "NOT_CLOSED", -8: "INFEASIBLE", -9: "STATE", -10: "BUFFER_TOO_SMALL",
           -11: "CUDA", -12: "NOMEM"}
@@ -232,9 +233,10 @@ class Context:
         return list(out[:n.value])
 
     # --- schedule / plan -----------------------------------------------------------------
-    def schedule(self, algo=CC_TREE, cap_bytes=0, given=None):
+    def schedule(self, algo=CC_TREE, cap_bytes=0, given=None, evict_next_use=False):
         cfg = cc_sched_cfg()
         cfg.algo = algo
+        cfg.flags = CC_EVICT_NEXT_USE if evict_next_use else 0
         cfg.cap_bytes = int(cap_bytes or 0)
         if given is not None:
             g = (c_i64 * max(len(given), 1))(*given)

@@ -1813,7 +1813,7 @@ cc_status cc_schedule(cc_ctx* ctx, const cc_sched_cfg* cfg, int64_t* order_out, 
   auto t1 = std::chrono::steady_clock::now();
   check_order(g, order);
   ctx->mt = simulate_model(g, order);
-  ctx->lp = lru_plan(g, order, cfg->cap_bytes);
+  ctx->lp = lru_plan(g, order, cfg->cap_bytes, (cfg->flags & CC_EVICT_NEXT_USE) ? EVICT_NEXT_USE : EVICT_LRU);
   auto t2 = std::chrono::steady_clock::now();
   ctx->order = std::move(order);
   ctx->tree_order = std::move(tree_order);

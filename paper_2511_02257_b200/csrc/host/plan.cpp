@@ -3,7 +3,9 @@
 // simulate_model: §II-C: for c_i (i) load the leaf operands not in
 //   memory, (ii) produce the output, (iii) release tensors no remaining contraction needs,
 //   including a ROOT output; M_i after (iii), transient after (ii) (reading G-5).
-// lru_plan: MemHC-style "pre-protected LRU" eviction to host, readings E-1..E-8:
+// lru_plan: MemHC-style "pre-protected LRU" eviction to host, readings E-1..E-8,
+// or (policy EVICT_NEXT_USE, reading E-9) Belady-style: the victim is the resident non-operand
+// whose next use in the known schedule is farthest away, ties to the least recently used:
 //   before c_i evict least-recently-used non-operand tensors until operands + output fit;
 //   leaves are dropped (no D2H), an intermediate is copied to host on its first eviction
 //   and the host copy is kept until release; fetches are touches; LRU ties cannot occur
@@ -72,24 +74,43 @@ ModelTrace simulate_model(const Dag& g, const std::vector<int32_t>& order) {
   return tr;
 }
 
-LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap) {
+LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap, EvictPolicy policy) {
   const bool bounded = cap > 0;
+  const bool next_use = policy == EVICT_NEXT_USE;
   const size_t n = g.nodes.size();
   LruPlan p;
   std::vector<int32_t> remaining(n);
   std::vector<uint8_t> resident(n, 0), host_copy(n, 0);
   std::vector<int64_t> stamp(n, 0);
   for (size_t u = 0; u < n; ++u) remaining[u] = int32_t(g.nodes[u].parents.size());
-  // resident tensors ordered by last touch: (stamp, node)
-  std::set<std::pair<int64_t, int32_t>> lru;
+  // E-9: the steps reading each tensor, in order (CSR), and a cursor to its next use
+  std::vector<int32_t> use_start(n + 1, 0), use_step, cursor(n, 0);
+  if (next_use) {
+    for (int32_t u : order) {
+      ++use_start[size_t(g.nodes[u].l) + 1];
+      ++use_start[size_t(g.nodes[u].r) + 1];
+    }
+    for (size_t x = 0; x < n; ++x) use_start[x + 1] += use_start[x];
+    use_step.resize(size_t(use_start[n]));
+    std::vector<int32_t> fill(use_start.begin(), use_start.end() - 1);
+    for (size_t i = 0; i < order.size(); ++i) {
+      const Node& nd = g.nodes[size_t(order[i])];
+      use_step[size_t(fill[size_t(nd.l)]++)] = int32_t(i);
+      use_step[size_t(fill[size_t(nd.r)]++)] = int32_t(i);
+    }
+  }
+  auto nxt = [&](int32_t x) -> int64_t { return use_step[size_t(use_start[size_t(x)] + cursor[size_t(x)])]; };
+  // resident tensors in eviction order: LRU (E-1): (stamp, node); next use (E-9):
+  // (-next use, stamp) with the node in the second slot of a tuple-like key
+  auto key = [&](int32_t x) -> std::pair<int64_t, int64_t> {
+    return next_use ? std::make_pair(-nxt(x), stamp[x]) : std::make_pair(stamp[x], int64_t(0));
+  };
+  std::set<std::pair<std::pair<int64_t, int64_t>, int32_t>> lru;
   int64_t clock = 0, used = 0, host = 0;
   p.used.reserve(order.size() + 1);
   p.used.push_back(0);
-  auto touch = [&](int32_t x) {
-    if (resident[x]) lru.erase({stamp[x], x});
-    stamp[x] = ++clock;
-    lru.insert({stamp[x], x});
-  };
+  auto erase = [&](int32_t x) { lru.erase({key(x), x}); };
+  auto insert = [&](int32_t x) { lru.insert({key(x), x}); };
   for (int32_t u : order) {
     const Node& nd = g.nodes[u];
     const int32_t ops[2] = {nd.l, nd.r};
@@ -100,7 +121,7 @@ LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap) {
     int64_t need = nd.size;
     for (int32_t x : ops)
       if (!resident[x]) need += g.nodes[x].size;
-    while (bounded && used + need > cap) {          // E-1
+    while (bounded && used + need > cap) {          // E-1 (victim order: E-1 LRU or E-9 next use)
       auto it = lru.begin();
       while (it != lru.end() && (it->second == ops[0] || it->second == ops[1])) ++it;
       if (it == lru.end()) throw Error(CC_E_INFEASIBLE, "no evictable tensor");
@@ -120,28 +141,27 @@ LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap) {
       resident[v] = 0;
       used -= g.nodes[v].size;
     }
+    for (int32_t x : ops)                            // this step's use is consumed (keys change)
+      if (resident[x]) erase(x);
+    for (int32_t x : ops) ++cursor[size_t(x)];
     for (int32_t x : ops) {                          // fetch + touch, left then right (E-2)
       if (!resident[x]) {
         ++p.h2d_count;
         p.h2d_bytes += g.nodes[x].size;
         used += g.nodes[x].size;
         p.ops.push_back({OP_H2D, x});
-        stamp[x] = ++clock;
         resident[x] = 1;
-        lru.insert({stamp[x], x});
-      } else {
-        touch(x);
       }
+      stamp[x] = ++clock;
     }
+    // operands are (re-)inserted below only while they stay resident
     used += nd.size;                                  // output
     stamp[u] = ++clock;
     resident[u] = 1;
-    lru.insert({stamp[u], u});
     p.ops.push_back({OP_CONTRACT, u});
     p.transient_peak = std::max(p.transient_peak, used);
     for (int32_t x : ops)                             // release at last use (E-8)
       if (--remaining[x] == 0) {
-        lru.erase({stamp[x], x});
         resident[x] = 0;
         used -= g.nodes[x].size;
         if (host_copy[x]) {
@@ -150,11 +170,14 @@ LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap) {
         }
         p.ops.push_back({OP_FREE, x});
       }
+    for (int32_t x : ops)
+      if (resident[x]) insert(x);
     if (remaining[u] == 0) {                          // ROOT output released at once
-      lru.erase({stamp[u], u});
       resident[u] = 0;
       used -= nd.size;
       p.ops.push_back({OP_FREE, u});
+    } else {
+      insert(u);
     }
     p.peak = std::max(p.peak, used);
     p.used.push_back(used);

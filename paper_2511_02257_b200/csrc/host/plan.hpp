@@ -28,7 +28,8 @@ struct LruPlan {
   int64_t evictions = 0, h2d_count = 0, d2h_count = 0, h2d_bytes = 0, d2h_bytes = 0;
   int64_t peak = 0, transient_peak = 0, host_peak = 0;
 };
-LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap);
+enum EvictPolicy { EVICT_LRU = 0, EVICT_NEXT_USE = 1 };
+LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap, EvictPolicy policy = EVICT_LRU);
 
 // Allocator with coalescing over [0, capacity).  BEST_FIT packs tightly; NEXT_FIT takes
 // the first block that fits at or after a rotating cursor (wrapping once), so freed memory

@@ -111,6 +111,19 @@ def fixture_dstar():
     return w
 
 
+def fixture_next_use():
+    """Eviction-policy fixture (reading E-9): leaves a,b,c,d; roots (one tree each)
+    s1=(a,b), s2=(c,a), s3=(d,b), s4=(c,d), s5=(b,a); unit sizes; replayed in id order.
+    Ids: a=0 b=1 c=2 d=3 s1=4 .. s5=8."""
+    w = Workload("NextUse", 1, 1, 1)
+    for i in range(4):
+        w.nodes.append((i, LEAF_X, -1, -1, 1))
+    w.nodes += [(4, OP_X, 0, 1, 1), (5, OP_X, 2, 0, 1), (6, OP_X, 3, 1, 1), (7, OP_X, 2, 3, 1), (8, OP_X, 1, 0, 1)]
+    w.trees = [(k, 4 + k) for k in range(5)]
+    w.terms = [(0, k, 1.0, 0.0) for k in range(5)]
+    return w
+
+
 def fixture_f1():
     """SPEC.md fixture F1 (S:513-516): leaves a,b,l; e=(b,l); g=(e,a); h=(e,a);
     f=(a,b); T0=g-tree, T1=h-tree, T2=f-tree; unit sizes.

@@ -23,7 +23,7 @@ def to_numpy_c(t, shape):
 
 
 def run_gpu(w, algo=None, cap=0, flags=0, device_leaves=False, arena_mb=256, leaf_fn=None, ctx=None,
-            part=None):
+            part=None, evict_next_use=False):
     """Returns (ctx, roots{tree: [Lt]}, corr{c: [Lt]}, plan stats, exec stats)."""
     import torch
     from paper_2511_02257_b200 import cc
@@ -34,7 +34,7 @@ def run_gpu(w, algo=None, cap=0, flags=0, device_leaves=False, arena_mb=256, lea
     ctx.load_workload(w)
     if part is not None:
         ctx.partition(*part)
-    order, st = ctx.schedule(cc.CC_TREE if algo is None else algo, cap_bytes=cap)
+    order, st = ctx.schedule(cc.CC_TREE if algo is None else algo, cap_bytes=cap, evict_next_use=evict_next_use)
     keep = []
     Lt_part = w.Lt
     t0 = 0

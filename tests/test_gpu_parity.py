@@ -270,6 +270,25 @@ def test_c4_evictions_under_cap():
         assert_corr_close(dag, r_or, corr, c_or)
 
 
+def test_c4_next_use_evictions_under_cap():
+    """The same capped two-baryon DAG with next-use eviction (reading E-9): the executed plan
+    moves exactly the oracle's bytes (fewer than LRU) and the values still match."""
+    w = dags.config_c4(N=8, Lt=1, S=4, n_trees=120, n_corr=4)
+    dag = Dag(w)
+    cap = 7 * 16 * 4 * 8 ** 3
+    order = tree.schedule(dag)
+    p = lru.plan(dag, order, cap, policy="next_use")
+    assert p["evictions"] > 0
+    assert p["h2d_bytes"] + p["d2h_bytes"] <= lru.plan(dag, order, cap)["h2d_bytes"] + lru.plan(dag, order, cap)["d2h_bytes"]
+    r_or, c_or = values.run_workload(w, dag)
+    for flags in (0, 16):
+        _, roots, corr, st, ex = run_gpu(w, cap=cap, flags=flags, evict_next_use=True)
+        assert st["evictions"] == p["evictions"] and ex["h2d_bytes"] == p["h2d_bytes"]
+        assert ex["d2h_bytes"] == p["d2h_bytes"]
+        assert_roots_close(roots, r_or)
+        assert_corr_close(dag, r_or, corr, c_or)
+
+
 def test_partitions_sum_to_whole():
     from paper_2511_02257_b200 import cc
     w = dags.config_c2(N=16, Lt=6, n_loop4=60, n_loop2=6, n_corr=4)

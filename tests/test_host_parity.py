@@ -224,3 +224,50 @@ def test_rsgs_matches_oracle():
         _, st = c.schedule(cc.CC_RSGS, cap_bytes=cap or 0)
         for k in ("evictions", "h2d_count", "d2h_count", "h2d_bytes", "d2h_bytes", "peak", "transient_peak"):
             assert st[k] == p[k], (k, cap)
+
+
+def _check_next_use(w, caps):
+    """C++ next-use (E-9) plans == oracle plans: counters, bytes, peaks and the op queue."""
+    dag = Dag(w)
+    c = _ctx(w)
+    for algo, order in ((cc.CC_TREE, tree.schedule(dag)), (cc.CC_SIBLING, sibling.schedule(dag))):
+        for cap in caps:
+            try:
+                p = lru.plan(dag, order, cap, policy="next_use")
+            except lru.InfeasibleError:
+                with pytest.raises(cc.CCError):
+                    c.schedule(algo, cap_bytes=cap or 0, evict_next_use=True)
+                continue
+            _, st = c.schedule(algo, cap_bytes=cap or 0, evict_next_use=True)
+            for k in ("evictions", "h2d_count", "d2h_count", "h2d_bytes", "d2h_bytes", "peak",
+                      "transient_peak", "host_peak_bytes"):
+                assert st[k] == p[k], (k, cap)
+            assert [(k, n) for (k, n, _, _) in c.plan_ops()] == p["ops"]
+
+
+def test_next_use_plans_bit_exact():
+    w = dags.fixture_next_use()
+    dag = Dag(w)
+    c = _ctx(w)
+    _, st = c.schedule(cc.CC_GIVEN, given=[4, 5, 6, 7, 8], cap_bytes=4, evict_next_use=True)
+    assert (st["evictions"], st["h2d_count"]) == (1, 5)
+    assert [(k, n) for (k, n, _, _) in c.plan_ops()] == lru.plan(dag, [4, 5, 6, 7, 8], 4, policy="next_use")["ops"]
+    _check_next_use(dags.fixture_dstar(), caps=(None, 2, 3, 4, 5))
+    for seed in range(60):
+        w = dags.random_dag(seed, n_leaves=7, n_trees=7, share_p=0.6)
+        tp = lru.plan(Dag(w), tree.schedule(Dag(w)))["transient_peak"]
+        _check_next_use(w, caps=(None, tp, max(1, tp - 2), max(1, tp // 2)))
+    mes = 16 * 2 * 8 * 8
+    _check_next_use(dags.config_c2(N=8, Lt=2), caps=(6 * mes, 10 * mes))
+    _check_next_use(dags.config_c4(N=4, Lt=1, S=4, n_trees=300), caps=(16 * 4 * 64 * 6, 16 * 4 * 64 * 9))
+
+
+def test_next_use_c4_full_scale():
+    """c4 at full scale under its 32e9 B cap: bit-exact with the oracle, and fewer bytes over
+    PCIe than LRU (the point of E-9)."""
+    w = dags.config_c4()
+    _check_next_use(w, caps=(32 * 10 ** 9,))
+    c = _ctx(w)
+    _, lru_st = c.schedule(cc.CC_TREE, cap_bytes=32 * 10 ** 9)
+    _, nu_st = c.schedule(cc.CC_TREE, cap_bytes=32 * 10 ** 9, evict_next_use=True)
+    assert nu_st["h2d_bytes"] + nu_st["d2h_bytes"] < lru_st["h2d_bytes"] + lru_st["d2h_bytes"]

@@ -100,3 +100,105 @@ def test_monotone_in_capacity_uniform_sizes():
             ev = [lru.plan(dag, order, c)["evictions"] for c in range(lo, sim["transient_peak"] + 2)]
             assert all(a >= b for a, b in zip(ev, ev[1:]))
             assert ev[-1] == 0
+
+
+# ---- E-9: next-use (Belady) eviction ---------------------------------------------------------
+
+NU_ORDER = [4, 5, 6, 7, 8]
+
+
+def test_next_use_hand_trace():
+    """fixture_next_use at cap 4 (three unit leaves + the output).  Before s3=(d,b) the
+    non-operands a and c are resident: LRU evicts c (touched at s2 before a), which s4
+    needs next, and then a for s4, which s5 re-fetches: 2 evictions, 6 H2D.  Next use evicts
+    a (read again at s5, after c's read at s4): 1 eviction, 5 H2D (hand-derived)."""
+    dag = Dag(dags.fixture_next_use())
+    p = lru.plan(dag, NU_ORDER, 4)
+    assert (p["evictions"], p["h2d_count"]) == (2, 6)
+    q = lru.plan(dag, NU_ORDER, 4, policy="next_use")
+    assert (q["evictions"], q["h2d_count"]) == (1, 5)
+    kinds = [(k, u) for (k, u) in q["ops"] if k not in ("FREE",)]
+    assert kinds == [("H2D", 0), ("H2D", 1), ("CONTRACT", 4), ("H2D", 2), ("CONTRACT", 5),
+                     ("DROP", 0), ("H2D", 3), ("CONTRACT", 6), ("CONTRACT", 7),
+                     ("H2D", 0), ("CONTRACT", 8)]
+    for cap in (5, 100):
+        assert lru.plan(dag, NU_ORDER, cap, policy="next_use")["h2d_count"] == 4
+
+
+def _min_fetches(dag, order, cap):
+    """Brute force over every victim choice (E-1 mechanics, any resident non-operand may be
+    evicted): the minimum number of H2D fetches.  For root-only DAGs (only leaves are ever
+    resident between steps, unit sizes) this is the paging problem whose optimum Belady's
+    farthest-next-use rule attains."""
+    nodes = dag.nodes
+    best = [None]
+
+    def rec(i, resident, fetches):
+        if best[0] is not None and fetches >= best[0]:
+            return
+        if i == len(order):
+            best[0] = fetches
+            return
+        u = order[i]
+        ops = nodes[u].child
+        need = sum(1 for x in ops if x not in resident) + 1
+        if len(resident) + need > cap:
+            for v in sorted(resident - set(ops)):
+                rec(i, resident - {v}, fetches)
+            return
+        new = set(resident) | set(ops)
+        f = fetches + sum(1 for x in ops if x not in resident)
+        # leaves with no later reader are released (E-8)
+        later = set(x for w in order[i + 1:] for x in nodes[w].child)
+        rec(i + 1, frozenset(x for x in new if x in later), f)
+
+    rec(0, frozenset(), 0)
+    return best[0]
+
+
+def test_next_use_optimal_on_root_only_dags():
+    """Belady's theorem as a pin: on random root-only DAGs with unit sizes the next-use plan
+    fetches the minimum possible number of leaves (brute force over all victim choices), and
+    LRU never beats it."""
+    rng = np.random.default_rng(7)
+    checked = 0
+    for trial in range(120):
+        k = int(rng.integers(4, 7))
+        m = int(rng.integers(5, 10))
+        w = dags.Workload("ro%d" % trial, 1, 1, 1)
+        pairs = [tuple(int(x) for x in rng.choice(k, size=2, replace=False)) for _ in range(m)]
+        if len(set(x for pr in pairs for x in pr)) < k:
+            continue                       # every leaf must be read (no isolated nodes)
+        for i in range(k):
+            w.nodes.append((i, dags.LEAF_X, -1, -1, 1))
+        for j, (a, b) in enumerate(pairs):
+            w.nodes.append((k + j, dags.OP_X, a, b, 1))
+            w.trees.append((j, k + j))
+            w.terms.append((0, j, 1.0, 0.0))
+        dag = Dag(w)
+        order = [k + j for j in range(m)]
+        for cap in range(3, k + 2):
+            q = lru.plan(dag, order, cap, policy="next_use")
+            p = lru.plan(dag, order, cap)
+            opt = _min_fetches(dag, order, cap)
+            assert q["h2d_count"] == opt, (trial, cap)
+            assert p["h2d_count"] >= opt
+            checked += 1
+    assert checked > 80
+
+
+def test_next_use_accounting_on_random_dags():
+    """With intermediates (D2H on first eviction, E-4) the next-use plan keeps every E
+    accounting identity: final residency 0, every D2H re-fetched, unbounded == LRU."""
+    for seed in range(30):
+        dag = Dag(dags.random_dag(seed, n_leaves=6, n_trees=6, share_p=0.6))
+        order = tree.schedule(dag)
+        tp = lru.plan(dag, order)["transient_peak"]
+        assert lru.plan(dag, order, None, policy="next_use")["ops"] == lru.plan(dag, order)["ops"]
+        for cap in (tp, max(1, tp - 2), max(1, tp // 2)):
+            try:
+                q = lru.plan(dag, order, cap, policy="next_use")
+            except lru.InfeasibleError:
+                continue
+            h2d_inter = sum(1 for (kk, u) in q["ops"] if kk == "H2D" and dag.nodes[u].child)
+            assert h2d_inter >= q["d2h_count"]

@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--part", type=int, default=0)
     ap.add_argument("--device-leaves", action="store_true")
     ap.add_argument("--ozaki", action="store_true", help="MM1 on the tcgen05 INT8 Ozaki engine (execute flags bit 6)")
+    ap.add_argument("--next-use", action="store_true", help="next-use (Belady) eviction, reading E-9")
     ap.add_argument("--breakdown", action="store_true",
                     help="one more op-by-op execute with every kernel timed (flags bit 1): time per op kind")
     a = ap.parse_args()
@@ -44,10 +45,10 @@ def main():
     if a.parts > 1:
         ctx.partition(a.parts, a.part, cc.PART_TIME)
     pt0, pt1 = ctx.part_time_range()
-    order, st = ctx.schedule(cc.CC_TREE, cap_bytes=cap)
+    order, st = ctx.schedule(cc.CC_TREE, cap_bytes=cap, evict_next_use=a.next_use)
     t1 = time.perf_counter()
-    print("%s: %d contractions, plan peak %.2f GB transient %.2f GB, evictions %d, H2D %.2f GB D2H %.2f GB, "
-          "schedule+plan %.1f ms" % (w.name, st["n_contr"], st["peak"] / 1e9, st["transient_peak"] / 1e9,
+    print("%s%s: %d contractions, plan peak %.2f GB transient %.2f GB, evictions %d, H2D %.2f GB D2H %.2f GB, "
+          "schedule+plan %.1f ms" % (w.name, " (next-use eviction)" if a.next_use else "", st["n_contr"], st["peak"] / 1e9, st["transient_peak"] / 1e9,
                                      st["evictions"], st["h2d_bytes"] / 1e9, st["d2h_bytes"] / 1e9,
                                      (t1 - t0) * 1e3), flush=True)
     host = {}
