@@ -1,5 +1,6 @@
 """Scheduler comparison report (the paper's Fig. 6-7 / Table III-IV
-metrics on synthetic workloads): RS-GS-like baseline vs sibling vs tree.
+metrics on synthetic workloads): RS-GS-like baseline vs sibling vs tree
+(LRU eviction, E-1) and tree with next-use eviction (E-9, "tree+nu").
 
 For each workload and seed: logical peak and transient peak (§II-C), and under a device
 capacity (default: the workload's cap, else a fraction of the RS-GS peak) the LRU plan's
@@ -20,7 +21,8 @@ sys.path.insert(0, ROOT)
 from paper_2511_02257_b200 import cc  # noqa: E402
 from synth import dags  # noqa: E402
 
-ALGOS = (("rsgs-like", cc.CC_RSGS), ("sibling", cc.CC_SIBLING), ("tree", cc.CC_TREE))
+ALGOS = (("rsgs-like", cc.CC_RSGS, False), ("sibling", cc.CC_SIBLING, False), ("tree", cc.CC_TREE, False),
+         ("tree+nu", cc.CC_TREE, True))   # tree order, next-use eviction (reading E-9)
 
 
 def workloads(seed):
@@ -39,14 +41,14 @@ def run(seeds, cap_frac):
             c.load_workload(w)
             base = {}
             res = {}
-            for label, algo in ALGOS:
+            for label, algo, _ in ALGOS:
                 _, st = c.schedule(algo)
                 res[label] = {"peak": st["peak"], "transient_peak": st["transient_peak"],
                               "sched_ms": st["sched_seconds"] * 1e3}
             cap_b = cap if cap is not None else int(cap_frac * res["rsgs-like"]["transient_peak"])
-            for label, algo in ALGOS:
+            for label, algo, nu in ALGOS:
                 try:
-                    _, st = c.schedule(algo, cap_bytes=cap_b)
+                    _, st = c.schedule(algo, cap_bytes=cap_b, evict_next_use=nu)
                     res[label].update(evictions=st["evictions"], transfers=st["h2d_count"] + st["d2h_count"],
                                       moved_bytes=st["h2d_bytes"] + st["d2h_bytes"])
                 except cc.CCError as e:
@@ -62,7 +64,7 @@ def summarise(rows):
         rs = [r for r in rows if r["workload"] == name]
         line = {"workload": name, "seeds": len(rs)}
         for metric in ("peak", "transient_peak", "evictions", "transfers", "moved_bytes", "sched_ms"):
-            for label, _ in ALGOS[1:]:
+            for label, _, _ in ALGOS[1:]:
                 ratios = []
                 for r in rs:
                     b, v = r["results"]["rsgs-like"].get(metric), r["results"][label].get(metric)
@@ -90,7 +92,7 @@ def main():
                                                    "transfers", "bytes", "sched_t")
     print(hdr)
     for s in summ:
-        for label, _ in ALGOS[1:]:
+        for label, _, _ in ALGOS[1:]:
             def f(m):
                 v = s.get("%s/%s" % (label, m))
                 return "%.3f" % v if v is not None else "-"
