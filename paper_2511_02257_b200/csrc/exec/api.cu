@@ -748,6 +748,18 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       }
       early_seq.swap(out);
     }
+    // the last copies of the order gate the work left at the end: split them into time-slice
+    // chunks (each a flag value; their consumers wait only for the chunk holding their slice)
+    // so that work starts while the rest of the leaf is still in flight.  CC_H2D_TAIL copies
+    // x CC_H2D_TAIL_CHUNKS chunks (every chunk costs one stream memory operation).
+    const int tail = getenv("CC_H2D_TAIL") ? atoi(getenv("CC_H2D_TAIL")) : 0;
+    const int tail_c = getenv("CC_H2D_TAIL_CHUNKS") ? atoi(getenv("CC_H2D_TAIL_CHUNKS")) : 4;
+    for (int k = 0; k < tail && k < int(early_seq.size()) && tail_c > 1; ++k) {
+      const int32_t i = early_seq[early_seq.size() - 1 - size_t(k)];
+      const PhysOp& op = ops[size_t(i)];
+      const int64_t C = std::min<int64_t>(Lt, tail_c);
+      if (target[size_t(i)] == 1 && Lt > 1 && Lt % C == 0 && op.bytes % Lt == 0) target[size_t(i)] = -int32_t(C);
+    }
   }
   // early copies: zero the sync area on the H2D stream, then start the early copies, each
   // followed by its flag write, so they overlap the rest of the host-side preparation; the
