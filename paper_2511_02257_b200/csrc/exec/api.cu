@@ -171,6 +171,8 @@ struct cc_ctx {
   std::vector<cudaEvent_t> df_events;  // per copy (index into df_copies), when some copy waits on it
   cudaStream_t cs2 = nullptr;       // second compute stream (trace worker)
   cudaEvent_t ev_cs2 = nullptr;
+  cudaStream_t hs2 = nullptr;       // second H2D stream: wait-free leaf copies alternate with hs
+  cudaEvent_t ev_hs2 = nullptr;
   cudaGraphExec_t gexec_df = nullptr;
   int64_t df_gemm_items = 0, df_trace_items = 0;
   unsigned long long* df_prof = nullptr;   // per-item timeline (flags bit 5)
@@ -237,6 +239,10 @@ struct cc_ctx {
     df_meta_img_bytes = 0;
     if (cs2) cudaStreamDestroy(cs2);
     cs2 = nullptr;
+    if (hs2) cudaStreamDestroy(hs2);
+    hs2 = nullptr;
+    if (ev_hs2) cudaEventDestroy(ev_hs2);
+    ev_hs2 = nullptr;
     if (ev_cs2) cudaEventDestroy(ev_cs2);
     ev_cs2 = nullptr;
     if (direct_tr_ws) cudaFree(direct_tr_ws);
@@ -618,6 +624,21 @@ void enqueue_copy(cc_ctx* ctx, cudaStream_t s, const void* src, void* dst, size_
   }
 }
 
+// Wait-free H2D copies alternate between the H2D stream and a second one (CC_H2D_STREAMS=1
+// keeps one): each copy is followed by its flag write, a stream memory operation that idles
+// its stream's copy engine (~8 us measured), so the other stream's copy fills the gap.
+// Off by default: c2 e2e 10.86-10.89 ms with two streams vs 10.87-11.36 ms with one (noise).
+bool dual_h2d() {
+  static const int n = getenv("CC_H2D_STREAMS") ? atoi(getenv("CC_H2D_STREAMS")) : 1;
+  return n >= 2;
+}
+void ensure_hs2(cc_ctx* ctx) {
+  if (!ctx->hs2) {
+    ck(cudaStreamCreateWithFlags(&ctx->hs2, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&ctx->ev_hs2, cudaEventDisableTiming), "event");
+  }
+}
+
 // early: start the wait-free H2D copies at the head of the copy order on the H2D stream as
 // soon as that order is known, so they overlap the rest of the host-side preparation (queues,
 // tensor maps, upload); the next issue_dataflow only adds their flag writes.
@@ -772,12 +793,22 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
     ck(cudaMemsetAsync(ctx->df_sync_base, 0, sz_sync, ctx->hs), "memset");
     ck(cudaEventRecord(ctx->ev_pre, ctx->hs), "event");
     ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_pre, 0), "wait");
+    const bool dual = dual_h2d();
+    if (dual) {
+      ensure_hs2(ctx);
+      ck(cudaStreamWaitEvent(ctx->hs2, ctx->ev_pre, 0), "wait");
+    }
+    size_t q = 0;
     for (int32_t i : early_seq) {
       const PhysOp& op = ops[size_t(i)];
       const auto ep = copy_endpoints(ctx, op);
-      enqueue_copy(ctx, ctx->hs, ep.first, ep.second, size_t(op.bytes), cudaMemcpyHostToDevice,
-                   target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
+      enqueue_copy(ctx, (dual && (q++ & 1)) ? ctx->hs2 : ctx->hs, ep.first, ep.second, size_t(op.bytes),
+                   cudaMemcpyHostToDevice, target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
       ctx->df_early[size_t(i)] = 1;
+    }
+    if (dual) {                                   // rejoin: later hs work follows every early copy
+      ck(cudaEventRecord(ctx->ev_hs2, ctx->hs2), "event");
+      ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_hs2, 0), "wait");
     }
     ctx->df_early_active = true;
   }
@@ -1299,10 +1330,19 @@ int issue_dataflow(cc_ctx* ctx, bool time_copies = false) {
     }
   }
   cudaStream_t st[3] = {ctx->cs, ctx->hs, ctx->ds};
+  const bool dual = dual_h2d();
+  if (dual) {
+    ensure_hs2(ctx);
+    ck(cudaStreamWaitEvent(ctx->hs2, ctx->ev_start, 0), "wait");
+  }
+  size_t q = 0;
   for (const int32_t kk : ctx->df_issue) {
     const size_t k = size_t(kk);
     const auto& c = ctx->df_copies[k];
     cudaStream_t s = st[c.stream];
+    // wait-free H2D copies (no event / value waits) alternate with the second H2D stream; any
+    // copy that waits stays on hs, whose order the explicit waits already cover
+    if (dual && c.stream == S_H2D && c.wait_events.empty() && c.wait_values.empty() && (q++ & 1)) s = ctx->hs2;
     for (int32_t e : c.wait_events) ck(cudaStreamWaitEvent(s, ctx->df_events[size_t(e)], 0), "wait");
     for (const auto& wv : c.wait_values)
       if (df_wait_fn()(s, reinterpret_cast<CUdeviceptr>(ctx->df_sync + wv.first), cuuint32_t(wv.second),
@@ -1317,6 +1357,10 @@ int issue_dataflow(cc_ctx* ctx, bool time_copies = false) {
     if (c.source) ck(cudaEventRecord(ctx->df_events[k], s), "event");
   }
   DBG("copies enqueued");
+  if (dual) {
+    ck(cudaEventRecord(ctx->ev_hs2, ctx->hs2), "event");
+    ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_hs2, 0), "wait");
+  }
   ctx->df_early_active = false;   // later replays copy everything and zero the sync area on cs
   if (time_copies) {
     ck(cudaEventRecord(ctx->ev_copy_h, ctx->hs), "event");
