@@ -186,8 +186,8 @@ cc_status cc_set_leaf_device(cc_ctx* ctx, int64_t leaf_id, const void* dev, size
  * (average launch duration for the roofline, without host launch overhead).  The default
  * executor is the dataflow one (persistent DMMA-tile and trace workers, kernels/dataflow.hpp);
  * bit 4 selects op-by-op launches instead; bit 5 records the per-item timeline
- * (cc_dataflow_profile); bit 6 runs every MM1 on the tcgen05 INT8 Ozaki engine (cc_mm1_ozaki,
- * 5 slices, N <= 8192; implies op-by-op launches; the other kinds stay on FP64 DMMA). */
+ * (cc_dataflow_profile); bit 6 runs every MM1 / BM1 / BB2 on the tcgen05 INT8 Ozaki engine
+ * (cc_gemm_ozaki, 5 slices; leaves split once per execute; implies op-by-op launches). */
 cc_status cc_execute(cc_ctx* ctx, int32_t flags, cc_exec_stats* stats);
 /* Enqueue-only variant (no host sync): work is ordered on the compute stream. */
 cc_status cc_execute_async(cc_ctx* ctx, int32_t flags);
@@ -242,6 +242,15 @@ cc_status cc_tr_mm(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t L
 size_t cc_mm1_ozaki_workspace_bytes(int32_t Lt, int32_t N, int32_t n_slices);
 cc_status cc_mm1_ozaki(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt, int32_t N, int32_t n_slices,
                        void* workspace, size_t workspace_bytes);
+/* Any of the three contraction kinds on the Ozaki engine: op = CC_MM1 / CC_BM1 / CC_BB2 with
+ * the layouts of cc_mm1 / cc_bm1 / cc_bb2 (S ignored for MM1).  BM1 splits the baryon's rows
+ * (M = S N^2); BB2 contracts K = S N^2 in chunks of 8192 complex terms (INT32 bound), whose
+ * FP64 partials are summed in chunk order (deterministic).  Time slices are processed in
+ * batches that fit `workspace` (at least cc_gemm_ozaki_workspace_bytes(op, 1, N, S, s) bytes;
+ * the full-batch size is returned for Lt).  Errors as cc_mm1_ozaki. */
+size_t cc_gemm_ozaki_workspace_bytes(int32_t op, int32_t Lt, int32_t N, int32_t S, int32_t n_slices);
+cc_status cc_gemm_ozaki(cc_ctx* ctx, int32_t op, const void* A, const void* B, void* C, int32_t Lt, int32_t N,
+                        int32_t S, int32_t n_slices, void* workspace, size_t workspace_bytes);
 /* The INT8 tcgen05 GEMM alone (pins the UMMA descriptors bit-exactly in the tests):
  * C[m][n] = sum_k A[m][k] B[n][k]; A int8 [M][K], B int8 [Nn][K] row-major, C int32 [M][Nn];
  * M % 128 == 0, Nn % 64 == 0, K % 64 == 0, K <= 2^17 (no INT32 overflow). */

@@ -24,7 +24,8 @@ CC_LEAF_M, CC_LEAF_B, CC_MM1, CC_BM1, CC_BB2, CC_TR_MM, CC_LEAF_X, CC_OP_X = ran
 CC_SIBLING, CC_TREE, CC_GIVEN, CC_RSGS = range(4)
 PART_TIME, PART_TREES = 0, 1
 EXEC_GRAPH, EXEC_TIME_KERNELS, EXEC_ONLY_GEMM, EXEC_ONLY_TRACE, EXEC_OP_BY_OP, EXEC_PROFILE = 1, 2, 4, 8, 16, 32
-EXEC_OZAKI_MM1 = 64
+EXEC_OZAKI_MM1 = 64        # MM1 / BM1 / BB2 on the tcgen05 Ozaki engine (name kept from MM1-only)
+EXEC_OZAKI = 64
 CC_EVICT_NEXT_USE = 1       # cc_sched_cfg.flags: next-use (Belady) eviction, reading E-9
 STATUS = {0: "OK", -1: "INVAL", -2: "PARSE", -3: "CYCLE", -4: "INCONSISTENT", -5: "MULTIROOT",
           -6: "UNKNOWN_NODE", -7: "NOT_CLOSED", -8: "INFEASIBLE", -9: "STATE", -10: "BUFFER_TOO_SMALL",
@@ -114,6 +115,8 @@ _sig("cc_tr_mm", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32)
 _sig("cc_mm1_ozaki", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, c_void_p, ctypes.c_size_t)
 _sig("cc_mm1_ozaki_workspace_bytes", c_i32, c_i32, c_i32, res=ctypes.c_size_t)
 _sig("cc_i8gemm_tn", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32)
+_sig("cc_gemm_ozaki", c_void_p, c_i32, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, c_i32, c_void_p, ctypes.c_size_t)
+_sig("cc_gemm_ozaki_workspace_bytes", c_i32, c_i32, c_i32, c_i32, c_i32, res=ctypes.c_size_t)
 _sig("cc_fill_synthetic", c_void_p, c_void_p, c_i64, c_u64, c_i64, c_i64, c_i32, c_dbl)
 _sig("cc_scratch_bytes", c_i32, c_i32, c_i32, res=c_size_t)
 
@@ -121,7 +124,8 @@ EXPORTED = ["cc_create", "cc_destroy", "cc_last_error", "cc_version", "cc_load_d
             "cc_dag_info", "cc_part_time_range", "cc_correlators", "cc_partition", "cc_part_trees", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
             "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_execute",
             "cc_execute_async", "cc_kernel_times", "cc_dataflow_state", "cc_dataflow_profile", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
-            "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_mm1_ozaki", "cc_mm1_ozaki_workspace_bytes", "cc_i8gemm_tn", "cc_fill_synthetic", "cc_scratch_bytes"]
+            "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_mm1_ozaki", "cc_mm1_ozaki_workspace_bytes", "cc_i8gemm_tn", "cc_gemm_ozaki",
+            "cc_gemm_ozaki_workspace_bytes", "cc_fill_synthetic", "cc_scratch_bytes"]
 
 
 class CCError(RuntimeError):
@@ -154,6 +158,10 @@ def cc_scratch_bytes(Lt, N, S):
 
 def cc_mm1_ozaki_workspace_bytes(Lt, N, n_slices):
     return int(_lib.cc_mm1_ozaki_workspace_bytes(Lt, N, n_slices))
+
+
+def cc_gemm_ozaki_workspace_bytes(op, Lt, N, S, n_slices):
+    return int(_lib.cc_gemm_ozaki_workspace_bytes(op, Lt, N, S, n_slices))
 
 
 class Context:
@@ -369,6 +377,10 @@ class Context:
     def mm1_ozaki(self, A, B, C, Lt, N, n_slices, workspace):
         self._ck(_lib.cc_mm1_ozaki(self._h, _ptr(A), _ptr(B), _ptr(C), Lt, N, n_slices, _ptr(workspace),
                                    workspace.numel() * workspace.element_size()))
+
+    def gemm_ozaki(self, op, A, B, C, Lt, N, S, n_slices, workspace):
+        self._ck(_lib.cc_gemm_ozaki(self._h, op, _ptr(A), _ptr(B), _ptr(C), Lt, N, S, n_slices, _ptr(workspace),
+                                    workspace.numel() * workspace.element_size()))
 
     def i8gemm_tn(self, A, B, C, M, Nn, K):
         self._ck(_lib.cc_i8gemm_tn(self._h, _ptr(A), _ptr(B), _ptr(C), M, Nn, K))

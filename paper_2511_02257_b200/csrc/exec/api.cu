@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -53,7 +54,8 @@ constexpr int64_t ALIGN = 1024;
 // INT8 slices per operand of the Ozaki MM1 engine (reading V-6: 5 balanced base-256 digits,
 // 38 bits; phase-limited MM1 errors <= 1e-11 relative in the tests, inside the 1e-10 bar).
 constexpr int OZAKI_SLICES = 5;
-constexpr int64_t OZAKI_MAX_N = 8192;   // INT32 accumulators: s 2^14 2N < 2^31
+// kind index of a GEMM op for the Ozaki form cache (a leaf's form depends on the problem shape)
+inline int oz_kind(int op) { return op == CC_MM1 ? 0 : (op == CC_BM1 ? 1 : 2); }
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 void ck(cudaError_t e, const char* what) {
@@ -69,12 +71,12 @@ struct KindTimes {
 
 struct cc_ctx {
   int device = -1;
-  bool mm1_ozaki = false;     // execute flags bit 6: MM1 on the tcgen05 Ozaki engine (op-by-op)
+  bool mm1_ozaki = false;     // execute flags bit 6: MM1/BM1/BB2 on the tcgen05 Ozaki engine (op-by-op)
   // Ozaki leaf-form cache: INT8 slices of leaves, split once per execute and shared by every
   // MM1 reading that leaf in the same role, placed in the pool above the plan's high water
   struct {
-    std::vector<OzakiForm> form[2];
-    std::vector<char> have[2];
+    std::vector<OzakiForm> form[6];   // [2 * oz_kind + (B-form)]
+    std::vector<char> have[6];
     int64_t off = 0, end = 0;
   } oz;
   char* oz_scratch = nullptr;          // reserved leaf-form cache (scratch), may be empty
@@ -383,21 +385,36 @@ void prepare_phys(cc_ctx* ctx) {
   for (const auto& n : g.nodes) has[n.op] = true;
   for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)})
     if (has[op]) gemm_ws = std::max(gemm_ws, zgemm_workspace_bytes(problem_for(op, Lt, N, S, nullptr, nullptr, nullptr), ctx->num_sms));
-  if (has[CC_MM1] && N <= OZAKI_MAX_N) gemm_ws = std::max(gemm_ws, ozaki_mm1_workspace_bytes(Lt, N, OZAKI_SLICES));
-  // Ozaki leaf-form cache (execute flags bit 6): one A-form per leaf read as a left MM1
-  // operand, one B-form per leaf read as a right one; reserved when it takes at most 1/8 of
-  // the arena (else the cache uses whatever pool space the plan leaves free)
+  // Ozaki engine (execute flags bit 6): workspace for batches of time slices that fit in
+  // max(one slice, arena / 16)
+  for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)}) {
+    if (!has[op]) continue;
+    const ZgemmProblem q = problem_for(op, Lt, N, S, nullptr, nullptr, nullptr);
+    const size_t lim = std::max(ozaki_workspace_bytes(q, OZAKI_SLICES, 1), size_t(ctx->arena_bytes / 16));
+    int64_t bt = Lt;
+    while (bt > 1 && ozaki_workspace_bytes(q, OZAKI_SLICES, bt) > lim) bt = (bt + 1) / 2;
+    gemm_ws = std::max(gemm_ws, ozaki_workspace_bytes(q, OZAKI_SLICES, bt));
+  }
+  // Ozaki leaf-form cache: one form per (leaf, op kind, side) read by a GEMM op; reserved
+  // when it takes at most 1/8 of the arena (else the cache uses whatever pool space the plan
+  // leaves free)
   int64_t sz_ozc = 0;
-  if (has[CC_MM1] && N <= OZAKI_MAX_N) {
-    std::vector<char> role(g.nodes.size(), 0);
+  {
+    std::vector<std::array<char, 6>> role(g.nodes.size(), std::array<char, 6>{});
     for (const auto& n : g.nodes)
-      if (n.op == CC_MM1) {
-        if (g.nodes[size_t(n.l)].leaf()) role[size_t(n.l)] |= 1;
-        if (g.nodes[size_t(n.r)].leaf()) role[size_t(n.r)] |= 2;
+      if (n.op == CC_MM1 || n.op == CC_BM1 || n.op == CC_BB2) {
+        if (g.nodes[size_t(n.l)].leaf()) role[size_t(n.l)][size_t(2 * oz_kind(n.op))] = 1;
+        if (g.nodes[size_t(n.r)].leaf()) role[size_t(n.r)][size_t(2 * oz_kind(n.op) + 1)] = 1;
       }
-    const int64_t fa = round_up(int64_t(ozaki_form_bytes(Lt, N, OZAKI_SLICES, false)), ALIGN);
-    const int64_t fb = round_up(int64_t(ozaki_form_bytes(Lt, N, OZAKI_SLICES, true)), ALIGN);
-    for (char r : role) sz_ozc += ((r & 1) ? fa : 0) + ((r & 2) ? fb : 0);
+    int64_t fsz[6] = {0};
+    for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)}) {
+      if (!has[op]) continue;
+      const ZgemmProblem q = problem_for(op, Lt, N, S, nullptr, nullptr, nullptr);
+      fsz[2 * oz_kind(op)] = round_up(int64_t(ozaki_form_bytes(q, OZAKI_SLICES, false)), ALIGN);
+      fsz[2 * oz_kind(op) + 1] = round_up(int64_t(ozaki_form_bytes(q, OZAKI_SLICES, true)), ALIGN);
+    }
+    for (const auto& r : role)
+      for (int k = 0; k < 6; ++k) sz_ozc += r[size_t(k)] ? fsz[k] : 0;
     if (sz_ozc > ctx->arena_bytes / 8) sz_ozc = 0;
   }
   const size_t trace_ws = trace_workspace_bytes(Lt, N);
@@ -1388,7 +1405,7 @@ int issue_dataflow(cc_ctx* ctx, bool time_copies = false) {
 // the top of the pool.  CC_OZAKI_LEAF_CACHE=0 disables it.
 void oz_cache_reset(cc_ctx* ctx) {
   const size_t n = ctx->dag->nodes.size();
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 6; ++k) {
     ctx->oz.form[k].assign(n, OzakiForm{nullptr, nullptr});
     ctx->oz.have[k].assign(n, 0);
   }
@@ -1407,16 +1424,16 @@ void oz_cache_reset(cc_ctx* ctx) {
   }
 }
 
-// The A-form (as_b false) or B-form of operand node `u` if it is a leaf with room in the
-// cache (made now, on the compute stream, at its first use), else nullptr.
-const OzakiForm* oz_leaf_form(cc_ctx* ctx, int32_t u, const void* x, bool as_b) {
+// The A-form (as_b false) or B-form of operand node `u` of problem q (op kind `op`) if it is a
+// leaf with room in the cache (made now, on the compute stream, at its first use), else nullptr.
+const OzakiForm* oz_leaf_form(cc_ctx* ctx, int op, const ZgemmProblem& q, int32_t u, bool as_b) {
   const Dag& g = *ctx->dag;
   if (u < 0 || !g.nodes[size_t(u)].leaf()) return nullptr;
-  const int k = as_b ? 1 : 0;
+  const int k = 2 * oz_kind(op) + (as_b ? 1 : 0);
   if (ctx->oz.have[k][size_t(u)]) return &ctx->oz.form[k][size_t(u)];
-  const int64_t bytes = round_up(int64_t(ozaki_form_bytes(g.Lt, g.N, OZAKI_SLICES, as_b)), ALIGN);
+  const int64_t bytes = round_up(int64_t(ozaki_form_bytes(q, OZAKI_SLICES, as_b)), ALIGN);
   if (ctx->oz.off + bytes > ctx->oz.end) return nullptr;
-  ck(launch_ozaki_form(x, g.Lt, g.N, OZAKI_SLICES, as_b, ctx->arena + ctx->oz.off, &ctx->oz.form[k][size_t(u)], ctx->cs),
+  ck(launch_ozaki_form(q, OZAKI_SLICES, as_b, ctx->arena + ctx->oz.off, &ctx->oz.form[k][size_t(u)], ctx->cs),
      "Ozaki leaf split");
   ctx->oz.off += bytes;
   ctx->oz.have[k][size_t(u)] = 1;
@@ -1431,12 +1448,14 @@ void launch_contract(cc_ctx* ctx, const Node& n, const void* a, const void* b, v
     ++*nl;
     return;
   }
-  if (n.op == CC_MM1 && ctx->mm1_ozaki && g.N <= OZAKI_MAX_N) {
-    const OzakiForm* fa = oz_leaf_form(ctx, n.l, a, false);
-    const OzakiForm* fb = oz_leaf_form(ctx, n.r, b, true);
-    ck(launch_ozaki_mm1(a, b, out, g.Lt, g.N, OZAKI_SLICES, ctx->gemm_ws, ctx->gemm_ws_bytes, ctx->cs, fa, fb),
-       "Ozaki MM1");
-    *nl += 5;   // (memset + colmax + 2 splits, or cached leaf forms made once) + GEMM
+  if (ctx->mm1_ozaki) {
+    const ZgemmProblem q = problem_for(n.op, g.Lt, g.N, g.S, a, b, out);
+    // forms only when the whole batch fits the workspace (else the engine splits per batch)
+    const bool whole = ozaki_workspace_bytes(q, OZAKI_SLICES, g.Lt) <= ctx->gemm_ws_bytes;
+    const OzakiForm* fa = whole ? oz_leaf_form(ctx, n.op, q, n.l, false) : nullptr;
+    const OzakiForm* fb = whole ? oz_leaf_form(ctx, n.op, q, n.r, true) : nullptr;
+    ck(launch_ozaki_gemm(q, OZAKI_SLICES, ctx->gemm_ws, ctx->gemm_ws_bytes, ctx->cs, fa, fb), "Ozaki GEMM");
+    *nl += 6;   // (memset + colmax + 2 splits, or cached leaf forms made once) + GEMM (+ split-K reduce)
     return;
   }
   ZgemmProblem p = problem_for(n.op, g.Lt, g.N, g.S, a, b, out);
@@ -2170,6 +2189,26 @@ cc_status cc_tr_mm(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t L
   // counters must be zero; a previous direct call with another Lt may have left partials there
   ck(cudaMemsetAsync(ctx->direct_tr_ws, 0, size_t(Lt) * 4, ctx->cs), "memset");
   ck(launch_trace(A, B, c, Lt, N, ctx->direct_tr_ws, ctx->cs), "TR_MM kernel");
+  API_END
+}
+
+size_t cc_gemm_ozaki_workspace_bytes(int32_t op, int32_t Lt, int32_t N, int32_t S, int32_t n_slices) {
+  if ((op != CC_MM1 && op != CC_BM1 && op != CC_BB2) || Lt <= 0 || N <= 0 || S <= 0 || n_slices < 4 || n_slices > 7)
+    return 0;
+  return ozaki_workspace_bytes(problem_for(op, Lt, N, op == CC_MM1 ? 1 : S, nullptr, nullptr, nullptr), n_slices, Lt);
+}
+
+cc_status cc_gemm_ozaki(cc_ctx* ctx, int32_t op, const void* A, const void* B, void* C, int32_t Lt, int32_t N,
+                        int32_t S, int32_t n_slices, void* workspace, size_t workspace_bytes) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  ctx->need_device();
+  if ((op != CC_MM1 && op != CC_BM1 && op != CC_BB2) || !A || !B || !C || !workspace || Lt <= 0 || N <= 0 || S <= 0 ||
+      n_slices < 4 || n_slices > 7)
+    throw Error(CC_E_INVAL, "bad kernel arguments");
+  const ZgemmProblem q = problem_for(op, Lt, N, op == CC_MM1 ? 1 : S, A, B, C);
+  if (workspace_bytes < ozaki_workspace_bytes(q, n_slices, 1)) throw Error(CC_E_BUFFER_TOO_SMALL, "ozaki workspace too small");
+  ck(launch_ozaki_gemm(q, n_slices, workspace, workspace_bytes, ctx->cs), "Ozaki GEMM");
   API_END
 }
 

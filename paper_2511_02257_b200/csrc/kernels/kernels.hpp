@@ -61,9 +61,14 @@ struct OzakiForm {
   const void* slices;
   const int* exps;
 };
-size_t ozaki_form_bytes(int64_t Lt, int64_t N, int slices, bool as_b);
-cudaError_t launch_ozaki_form(const void* X, int64_t Lt, int64_t N, int slices, bool as_b, void* dst,
-                              OzakiForm* form, cudaStream_t stream);
+// Any MM1 / BM1 / BB2-shaped problem (ZgemmProblem layout, two-level K, batch = time
+// slices): workspace for batches of up to max_batch slices; forms of the full batch.
+size_t ozaki_workspace_bytes(const ZgemmProblem& q, int slices, int64_t max_batch);
+size_t ozaki_form_bytes(const ZgemmProblem& q, int slices, bool as_b);
+cudaError_t launch_ozaki_form(const ZgemmProblem& q, int slices, bool as_b, void* dst, OzakiForm* form,
+                              cudaStream_t stream);
+cudaError_t launch_ozaki_gemm(const ZgemmProblem& q, int slices, void* ws, size_t ws_bytes, cudaStream_t stream,
+                              const OzakiForm* fa = nullptr, const OzakiForm* fb = nullptr);
 // fa / fb: pre-split operands (nullptr: split A / B into the workspace first).
 cudaError_t launch_ozaki_mm1(const void* A, const void* B, void* C, int64_t Lt, int64_t N, int slices, void* ws,
                              size_t ws_bytes, cudaStream_t stream, const OzakiForm* fa = nullptr,

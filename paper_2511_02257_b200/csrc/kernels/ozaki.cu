@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <mutex>
 
@@ -60,10 +61,14 @@ struct Cfg {
 };
 
 struct Params {
-  int Lt, N, Mp, Nc, Kp, Brows;   // Brows = rows of SB per (slice, t) = 2 Nc
+  int Lt, Mp, Nc, Kp, Brows;      // Brows = rows of SB per (slice, t) = 2 Nc
+  int M, Nn;                      // real output rows / complex columns
+  int nch, kchs;                  // K chunks (split K for the INT32 bound) x stages per chunk
+  long long ldc, sCb;             // C(t, m, n) at C + t sCb + m ldc + n (complex elements)
   const int* eA;
   const int* fB;
-  double* C;                      // complex128 [Lt][N][N] (interleaved)
+  double* C;                      // complex128, interleaved
+  double* P;                      // nch > 1: FP64 partials [nch][Lt][Mp][Nc] complex
   int* Craw;                      // RAW mode: int32 [Mp][Brows]
   const int8_t* SA;               // tiled slices (tiled_off); RAW mode reads through the maps
   const int8_t* SB;
@@ -165,21 +170,33 @@ __device__ __forceinline__ int scale_exponent(double m) {
   return m > 0.0 ? ilogb(m) + 1 : 0;
 }
 
-// One warp per row (t, i) of A: A_cat row slices + eA.
+// Operand addressing of a (two-level K) problem, complex elements (ZgemmProblem layout):
+//   A(t, m, kk) = A + t sAb + (kk / Kin) sAo + m lda + kk % Kin
+//   B(t, kk, n) = B + t sBb + (kk / Kin) sBo + (kk % Kin) ldb + n
+__device__ __forceinline__ const double2* a_at(const ZgemmProblem& q, int t, int64_t m, int64_t kk) {
+  return static_cast<const double2*>(q.A) + t * q.sAb + (kk / q.Kin) * q.sAo + m * q.lda + kk % q.Kin;
+}
+__device__ __forceinline__ const double2* b_at(const ZgemmProblem& q, int t, int64_t kk, int64_t n) {
+  return static_cast<const double2*>(q.B) + t * q.sBb + (kk / q.Kin) * q.sBo + (kk % q.Kin) * q.ldb + n;
+}
+
+// One warp per row (t, m) of A: A_cat row slices + eA.  K index of A_cat: Re part of kk at kk,
+// Im part at Kc + kk (Kc = roundup(K, 32)); padding rows / columns are zero.
 template <int S>
-__global__ void __launch_bounds__(256) split_rows_kernel(const double2* __restrict__ A, int8_t* __restrict__ SA,
-                                                         int* __restrict__ eA, int Lt, int N, int Mp, int Nc) {
+__global__ void __launch_bounds__(256) split_rows_kernel(ZgemmProblem q, int8_t* __restrict__ SA,
+                                                         int* __restrict__ eA, int Mp, int Kc) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * 8 + warp;
+  const int64_t i = int64_t(blockIdx.x) * 8 + warp;
   const int t = blockIdx.y;
   if (i >= Mp) return;
-  const int Kp = 2 * Nc;
+  const int64_t K = q.Kin * q.Ko;
+  const bool live = i < q.M;
+  const int Kp = 2 * Kc;
   const int nk = Kp / 64, nblk = Mp / 128;
-  const double2* src = A + (size_t(t) * N + (i < N ? i : 0)) * N;
   double m = 0.0;
-  if (i < N)
-    for (int j = lane; j < N; j += 32) {
-      const double2 v = src[j];
+  if (live)
+    for (int64_t j = lane; j < K; j += 32) {
+      const double2 v = *a_at(q, t, i, j);
       m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
     }
 #pragma unroll
@@ -187,7 +204,7 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double2* __restri
   const int e = scale_exponent(m);
   if (lane == 0) eA[size_t(t) * Mp + i] = e;
   const double sc = pow2(-e);
-  for (int j0 = lane * 4; j0 < Nc; j0 += 128) {
+  for (int j0 = lane * 4; j0 < Kc; j0 += 128) {
     uint32_t wr[S], wi[S];
 #pragma unroll
     for (int k = 0; k < S; ++k) wr[k] = wi[k] = 0;
@@ -195,7 +212,7 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double2* __restri
     for (int u = 0; u < 4; ++u) {
       const int j = j0 + u;
       double2 v = make_double2(0.0, 0.0);
-      if (i < N && j < N) v = src[j];
+      if (live && j < K) v = *a_at(q, t, i, j);
       int8_t qr[S], qi[S];
       split_value<S>(v.x * sc, qr);
       split_value<S>(v.y * sc, qi);
@@ -207,25 +224,25 @@ __global__ void __launch_bounds__(256) split_rows_kernel(const double2* __restri
     }
 #pragma unroll
     for (int k = 0; k < S; ++k) {
-      *reinterpret_cast<uint32_t*>(SA + tiled_off<S, 128>(t, i, j0, nblk, nk) + k * A_TILE) = wr[k];
-      *reinterpret_cast<uint32_t*>(SA + tiled_off<S, 128>(t, i, Nc + j0, nblk, nk) + k * A_TILE) = wi[k];
+      *reinterpret_cast<uint32_t*>(SA + tiled_off<S, 128>(t, int(i), j0, nblk, nk) + k * A_TILE) = wr[k];
+      *reinterpret_cast<uint32_t*>(SA + tiled_off<S, 128>(t, int(i), Kc + j0, nblk, nk) + k * A_TILE) = wi[k];
     }
   }
 }
 
-// Column scale exponents of B: grid (Nc/32, Lt, ceil(N/128)); fB preset to INT_MIN (bytes 0x80),
+// Column scale exponents of B: grid (Nc/32, Lt, ceil(K/128)); fB preset to INT_MIN (bytes 0x80),
 // each CTA folds the max-exponent of its 128-row chunk in with atomicMax (exponents are
 // monotone in the magnitude, so the max of the chunk exponents is the column's exponent).
-__global__ void __launch_bounds__(256) colmax_kernel(const double2* __restrict__ B, int* __restrict__ fB, int N, int Nc) {
+__global__ void __launch_bounds__(256) colmax_kernel(ZgemmProblem q, int* __restrict__ fB, int Nc) {
   __shared__ double red[8][32];
   const int tid = threadIdx.x, c = tid & 31, r0 = tid >> 5;
-  const int c0 = 32 * blockIdx.x, t = blockIdx.y, k0 = 128 * blockIdx.z;
-  const double2* src = B + size_t(t) * N * N;
+  const int c0 = 32 * blockIdx.x, t = blockIdx.y;
+  const int64_t k0 = 128 * int64_t(blockIdx.z), K = q.Kin * q.Ko;
   double m = 0.0;
-  if (c0 + c < N) {
-    const int k1 = min(N, k0 + 128);
-    for (int k = k0 + r0; k < k1; k += 8) {
-      const double2 v = src[size_t(k) * N + c0 + c];
+  if (c0 + c < q.Nn) {
+    const int64_t k1 = k0 + 128 < K ? k0 + 128 : K;
+    for (int64_t k = k0 + r0; k < k1; k += 8) {
+      const double2 v = *b_at(q, t, k, c0 + c);
       m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
     }
   }
@@ -239,30 +256,30 @@ __global__ void __launch_bounds__(256) colmax_kernel(const double2* __restrict__
   }
 }
 
-// B_cat^T row slices: grid (Nc/32, Lt, Nc/128), one CTA per (32-column group g, t, 128-row
+// B_cat^T row slices: grid (Nc/32, Lt, Kc/128), one CTA per (32-column group g, t, 128-row
 // chunk of k).  A column left at INT_MIN by colmax_kernel is all zero (exponent 0).
 template <int S>
-__global__ void __launch_bounds__(256) split_cols_kernel(const double2* __restrict__ B, int8_t* __restrict__ SB,
-                                                         const int* __restrict__ fB, int Lt, int N, int Nc) {
+__global__ void __launch_bounds__(256) split_cols_kernel(ZgemmProblem q, int8_t* __restrict__ SB,
+                                                         const int* __restrict__ fB, int Nc, int Kc) {
   __shared__ double2 tile[32][33];
   __shared__ int ecol[32];
   const int tid = threadIdx.x;
   const int g = blockIdx.x, t = blockIdx.y;
   const int c0 = 32 * g;
-  const int Kp = 2 * Nc, Brows = 2 * Nc;
+  const int64_t K = q.Kin * q.Ko;
+  const int Kp = 2 * Kc, Brows = 2 * Nc;
   const int nk = Kp / 64, nblk = Brows / 64;
-  const double2* src = B + size_t(t) * N * N;
   if (tid < 32) {
     const int e = fB[size_t(t) * Nc + c0 + tid];
     ecol[tid] = e < -100000 ? 0 : e;
   }
-  const int kend = min(Nc, 128 * int(blockIdx.z + 1));
+  const int kend = min(Kc, 128 * int(blockIdx.z + 1));
   for (int k0 = 128 * blockIdx.z; k0 < kend; k0 += 32) {
     __syncthreads();
     for (int idx = tid; idx < 1024; idx += 256) {
       const int kr = idx >> 5, c = idx & 31;
       double2 v = make_double2(0.0, 0.0);
-      if (k0 + kr < N && c0 + c < N) v = src[size_t(k0 + kr) * N + c0 + c];
+      if (k0 + kr < K && c0 + c < q.Nn) v = *b_at(q, t, k0 + kr, c0 + c);
       tile[kr][c] = v;
     }
     __syncthreads();
@@ -278,21 +295,38 @@ __global__ void __launch_bounds__(256) split_cols_kernel(const double2* __restri
         const double2 v = tile[kq * 8 + u][c];
         // part 0 (Cr column): [Br; -Bi]; part 1 (Ci column): [Bi; Br]
         const double x = part == 0 ? (h == 0 ? v.x : -v.y) : (h == 0 ? v.y : v.x);
-        int8_t q[S];
-        split_value<S>(x * sc, q);
+        int8_t qv[S];
+        split_value<S>(x * sc, qv);
 #pragma unroll
         for (int k = 0; k < S; ++k) {
           if (u < 4)
-            lo[k] |= uint32_t(uint8_t(q[k])) << (8 * u);
+            lo[k] |= uint32_t(uint8_t(qv[k])) << (8 * u);
           else
-            hi[k] |= uint32_t(uint8_t(q[k])) << (8 * (u - 4));
+            hi[k] |= uint32_t(uint8_t(qv[k])) << (8 * (u - 4));
         }
       }
 #pragma unroll
       for (int k = 0; k < S; ++k)
-        *reinterpret_cast<uint2*>(SB + tiled_off<S, 64>(t, 64 * g + rT, h * Nc + k0 + kq * 8, nblk, nk) +
+        *reinterpret_cast<uint2*>(SB + tiled_off<S, 64>(t, 64 * g + rT, h * Kc + k0 + kq * 8, nblk, nk) +
                                   k * B_TILE) = make_uint2(lo[k], hi[k]);
     }
+  }
+}
+
+// Split-K reduction: C(t, m, n) = sum over chunks ch (in order) of P[ch][t][m][n].
+__global__ void ozaki_reduce_kernel(Params p) {
+  const int64_t total = int64_t(p.Lt) * p.M * p.Nn;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t n = e % p.Nn, m = (e / p.Nn) % p.M, t = e / (int64_t(p.Nn) * p.M);
+    const double2* src = reinterpret_cast<const double2*>(p.P) + (t * p.Mp + m) * p.Nc + n;
+    const int64_t stride = int64_t(p.Lt) * p.Mp * p.Nc;
+    double2 acc = src[0];
+    for (int ch = 1; ch < p.nch; ++ch) {
+      const double2 v = src[ch * stride];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    reinterpret_cast<double2*>(p.C)[t * p.sCb + m * p.ldc + n] = acc;
   }
 }
 
@@ -316,7 +350,7 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntn = p.Brows / BN, ntm = p.Mp / BM;
-  const int ntiles = ntn * ntm * (RAW ? 1 : p.Lt);
+  const int ntiles = ntn * ntm * (RAW ? 1 : p.Lt) * p.nch;   // (t, row block, column block, K chunk)
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dev::smem_u32(&tmem_slot))
@@ -338,15 +372,25 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   const int nk = p.Kp / BKB;
+  // tile -> (t, mb, nb, ch), K chunks fastest; chunk ch covers stages [ch kchs, kc1)
+  auto decode = [&](int tile, int& t, int& mb, int& nb, int& ch) {
+    ch = tile % p.nch;
+    const int r = tile / p.nch;
+    nb = r % ntn;
+    mb = (r / ntn) % ntm;
+    t = r / (ntn * ntm);
+  };
 
   if (warp == 4) {
     if (lane == 0) {
       int it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int nb = tile % ntn, mb = (tile / ntn) % ntm, t = tile / (ntn * ntm);
+        int t, mb, nb, ch;
+        decode(tile, t, mb, nb, ch);
         const int rowA = t * p.Mp + mb * BM;
         const int rowB = t * p.Brows + nb * BN;
-        for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int kc1 = min(nk, (ch + 1) * p.kchs);
+        for (int kc = ch * p.kchs; kc < kc1; ++kc, ++it) {
           const int st = it % C::STAGES;
           if (it >= C::STAGES) dev::mbar_wait(&empty[st], ((it / C::STAGES) - 1) & 1);
           dev::mbar_expect_tx(&full[st], C::STAGE);
@@ -366,7 +410,9 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
     if (lane == 0) {
       int it = 0, n = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++n) {
-        for (int kc = 0; kc < nk; ++kc, ++it) {
+        const int ch = tile % p.nch;
+        const int kc0 = ch * p.kchs, kc1 = min(nk, (ch + 1) * p.kchs);
+        for (int kc = kc0; kc < kc1; ++kc, ++it) {
           const int st = it % C::STAGES;
           dev::mbar_wait(&full[st], (it / C::STAGES) & 1);
           tc_fence_after();
@@ -374,7 +420,7 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
           const uint32_t sb = sa + S * A_TILE;
 #pragma unroll
           for (int d = 0; d < S; ++d) {
-            if (kc == 0 && n > 0) {
+            if (kc == kc0 && n > 0) {
               dev::mbar_wait(&drained[d], (n - 1) & 1);     // previous tile's diagonal d is in registers
               tc_fence_after();
             }
@@ -383,7 +429,7 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
 #pragma unroll
               for (int ks = 0; ks < BKB / UK; ++ks)
                 mma_i8(tmem + uint32_t(d * BN), sw64_desc(sa + i * A_TILE + ks * UK),
-                       sw64_desc(sb + (d - i) * B_TILE + ks * UK), (kc | i | ks) != 0);
+                       sw64_desc(sb + (d - i) * B_TILE + ks * UK), ((kc - kc0) | i | ks) != 0);
           }
           mma_commit(&empty[st]);
         }
@@ -393,7 +439,8 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
   } else {
     int n = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++n) {
-      const int nb = tile % ntn, mb = (tile / ntn) % ntm, t = tile / (ntn * ntm);
+      int t, mb, nb, ch;
+      decode(tile, t, mb, nb, ch);
       dev::mbar_wait(&tfull, n & 1);
       tc_fence_after();
       const int r = mb * BM + warp * 32 + lane;                 // row of this thread (TMEM lane)
@@ -436,15 +483,17 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
             ai[q] = fma(double(vi[q]), w, ai[q]);
           }
         }
-        if (r < p.N) {
+        if (r < p.M) {
           const double se = pow2(p.eA[size_t(t) * p.Mp + r]);
           const int cbase = nb * 32;
-          double* dst = p.C + (size_t(t) * p.N + r) * p.N * 2;
           const int* f = p.fB + size_t(t) * p.Nc + cbase;
+          // one K chunk: the tile itself; else this chunk's FP64 partial (reduced in order later)
+          double* dst = p.nch == 1 ? p.C + 2 * (size_t(t) * p.sCb + size_t(r) * p.ldc)
+                                   : p.P + 2 * (((size_t(ch) * p.Lt + t) * p.Mp + r) * p.Nc);
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
             const int c = cbase + q;
-            if (c < p.N) {
+            if (c < p.Nn) {
               const double sf = se * pow2(f[q] < -100000 ? 0 : f[q]);   // exact: a power of two
               *reinterpret_cast<double2*>(dst + 2 * c) = make_double2(ar[q] * sf, ai[q] * sf);
             }
@@ -486,23 +535,34 @@ bool map_i8(CUtensorMap* map, const void* base, uint64_t kp, uint64_t rows, uint
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Sizes of one problem's slices for a batch of Lt time slices.
 struct Geometry {
-  int Mp, Nc, Kp, Brows;
-  size_t sa, sb, ea, fb, total;
+  int Mp, Nc, Kc, Kp, Brows, nk, kchs, nch;
+  size_t sa, ea, sb, fb, part, total;   // offsets in the workspace: A slices, eA, B slices, fB, partials
+  size_t a_form() const { return (ea - sa) + (sb - ea); }     // A slices + eA
+  size_t b_form() const { return (fb - sb) + (part - fb); }   // B slices + fB
 };
 
-Geometry geometry(int Lt, int N, int S) {
+constexpr int KCH_BYTES = 16384;   // K bytes per chunk: |acc| <= 7 * 2^14 * 16384 < 2^31
+
+Geometry geometry(const ZgemmProblem& q, int64_t Lt, int S) {
   Geometry g;
-  g.Mp = (N + BM - 1) / BM * BM;
-  g.Nc = (N + 31) / 32 * 32;
-  g.Kp = 2 * g.Nc;
+  const int64_t K = q.Kin * q.Ko;
+  g.Mp = int((q.M + BM - 1) / BM * BM);
+  g.Nc = int((q.Nn + 31) / 32 * 32);
+  g.Kc = int((K + 31) / 32 * 32);
+  g.Kp = 2 * g.Kc;
   g.Brows = 2 * g.Nc;
+  g.nk = g.Kp / BKB;
+  g.kchs = std::min(g.nk, KCH_BYTES / BKB);
+  g.nch = (g.nk + g.kchs - 1) / g.kchs;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   g.sa = 0;
-  g.sb = al(size_t(S) * Lt * g.Mp * g.Kp);
-  g.ea = g.sb + al(size_t(S) * Lt * g.Brows * g.Kp);
-  g.fb = g.ea + al(size_t(Lt) * g.Mp * 4);
-  g.total = g.fb + al(size_t(Lt) * g.Nc * 4);
+  g.ea = al(size_t(S) * Lt * g.Mp * g.Kp);
+  g.sb = g.ea + al(size_t(Lt) * g.Mp * 4);
+  g.fb = g.sb + al(size_t(S) * Lt * g.Brows * g.Kp);
+  g.part = g.fb + al(size_t(Lt) * g.Nc * 4);
+  g.total = g.part + (g.nch > 1 ? al(size_t(g.nch) * Lt * g.Mp * g.Nc * 16) : 0);
   return g;
 }
 
@@ -522,111 +582,143 @@ cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const Para
   auto k = ozaki_gemm_kernel<S, RAW>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
-  const int64_t tiles = int64_t(p.Brows / BN) * (p.Mp / BM) * (RAW ? 1 : p.Lt);
+  const int64_t tiles = int64_t(p.Brows / BN) * (p.Mp / BM) * (RAW ? 1 : p.Lt) * p.nch;
   const int grid = int(tiles < num_sms() ? tiles : num_sms());
   k<<<grid, 192, C::SMEM, stream>>>(ma, mb, p);
   return cudaGetLastError();
 }
 
 template <int S>
-void split_a(const void* A, int8_t* SA, int* eA, int Lt, int N, const Geometry& g, cudaStream_t stream) {
-  split_rows_kernel<S><<<dim3(g.Mp / 8, Lt), 256, 0, stream>>>(static_cast<const double2*>(A), SA, eA, Lt, N, g.Mp,
-                                                               g.Nc);
+void split_a(const ZgemmProblem& q, int8_t* SA, int* eA, const Geometry& g, cudaStream_t stream) {
+  split_rows_kernel<S><<<dim3(g.Mp / 8, unsigned(q.batch)), 256, 0, stream>>>(q, SA, eA, g.Mp, g.Kc);
 }
 
 template <int S>
-cudaError_t split_b(const void* B, int8_t* SB, int* fB, int Lt, int N, const Geometry& g, cudaStream_t stream) {
-  cudaError_t e = cudaMemsetAsync(fB, 0x80, size_t(Lt) * g.Nc * 4, stream);   // INT_MIN-like
+cudaError_t split_b(const ZgemmProblem& q, int8_t* SB, int* fB, const Geometry& g, cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(fB, 0x80, size_t(q.batch) * g.Nc * 4, stream);   // INT_MIN-like
   if (e != cudaSuccess) return e;
-  colmax_kernel<<<dim3(g.Nc / 32, Lt, (N + 127) / 128), 256, 0, stream>>>(static_cast<const double2*>(B), fB, N, g.Nc);
-  split_cols_kernel<S><<<dim3(g.Nc / 32, Lt, (g.Nc + 127) / 128), 256, 0, stream>>>(static_cast<const double2*>(B), SB,
-                                                                                    fB, Lt, N, g.Nc);
+  const int64_t K = q.Kin * q.Ko;
+  colmax_kernel<<<dim3(g.Nc / 32, unsigned(q.batch), unsigned((K + 127) / 128)), 256, 0, stream>>>(q, fB, g.Nc);
+  split_cols_kernel<S><<<dim3(g.Nc / 32, unsigned(q.batch), unsigned((g.Kc + 127) / 128)), 256, 0, stream>>>(q, SB, fB,
+                                                                                                          g.Nc, g.Kc);
   return cudaGetLastError();
 }
 
+// One batch (q.batch time slices): split what is not pre-split, GEMM, split-K reduction.
 template <int S>
-cudaError_t gemm(const int8_t* SA, const int* eA, const int8_t* SB, const int* fB, void* Cout, int Lt, int N,
-                 const Geometry& g, cudaStream_t stream) {
-  CUtensorMap ma{}, mb{};   // unused: the slices are tile-contiguous, read by bulk copies
-  Params p{Lt, N, g.Mp, g.Nc, g.Kp, g.Brows, eA, fB, static_cast<double*>(Cout), nullptr, SA, SB};
-  return launch_gemm<S, false>(ma, mb, p, stream);
-}
-
-template <int S>
-cudaError_t run_mm1(const void* A, const void* B, void* Cout, int Lt, int N, void* ws, size_t ws_bytes,
-                    const OzakiForm* fa, const OzakiForm* fb, cudaStream_t stream) {
-  const Geometry g = geometry(Lt, N, S);
-  if (ws_bytes < g.total) return cudaErrorInvalidValue;
-  uint8_t* w = static_cast<uint8_t*>(ws);
+cudaError_t run_batch(const ZgemmProblem& q, uint8_t* w, const OzakiForm* fa, const OzakiForm* fb,
+                      cudaStream_t stream) {
+  const Geometry g = geometry(q, q.batch, S);
   const int8_t* SA = reinterpret_cast<int8_t*>(w + g.sa);
-  const int8_t* SB = reinterpret_cast<int8_t*>(w + g.sb);
   const int* eA = reinterpret_cast<int*>(w + g.ea);
+  const int8_t* SB = reinterpret_cast<int8_t*>(w + g.sb);
   const int* fB = reinterpret_cast<int*>(w + g.fb);
   if (fa) {
     SA = static_cast<const int8_t*>(fa->slices);
     eA = fa->exps;
   } else {
-    split_a<S>(A, reinterpret_cast<int8_t*>(w + g.sa), reinterpret_cast<int*>(w + g.ea), Lt, N, g, stream);
+    split_a<S>(q, reinterpret_cast<int8_t*>(w + g.sa), reinterpret_cast<int*>(w + g.ea), g, stream);
   }
   if (fb) {
     SB = static_cast<const int8_t*>(fb->slices);
     fB = fb->exps;
   } else {
-    cudaError_t e = split_b<S>(B, reinterpret_cast<int8_t*>(w + g.sb), reinterpret_cast<int*>(w + g.fb), Lt, N, g, stream);
+    cudaError_t e = split_b<S>(q, reinterpret_cast<int8_t*>(w + g.sb), reinterpret_cast<int*>(w + g.fb), g, stream);
     if (e != cudaSuccess) return e;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return gemm<S>(SA, eA, SB, fB, Cout, Lt, N, g, stream);
+  CUtensorMap ma{}, mb{};   // unused: the slices are tile-contiguous, read by bulk copies
+  Params p{};
+  p.Lt = int(q.batch); p.Mp = g.Mp; p.Nc = g.Nc; p.Kp = g.Kp; p.Brows = g.Brows;
+  p.M = int(q.M); p.Nn = int(q.Nn); p.nch = g.nch; p.kchs = g.kchs;
+  p.ldc = q.ldc; p.sCb = q.sCb;
+  p.eA = eA; p.fB = fB; p.C = static_cast<double*>(q.C);
+  p.P = g.nch > 1 ? reinterpret_cast<double*>(w + g.part) : nullptr;
+  p.SA = SA; p.SB = SB;
+  e = launch_gemm<S, false>(ma, mb, p, stream);
+  if (e != cudaSuccess || g.nch == 1) return e;
+  ozaki_reduce_kernel<<<num_sms() * 4, 256, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// The whole problem in batches of time slices that fit the workspace (pre-split forms only
+// when it fits in one batch).
+template <int S>
+cudaError_t run_gemm(const ZgemmProblem& q, void* ws, size_t ws_bytes, const OzakiForm* fa, const OzakiForm* fb,
+                     cudaStream_t stream) {
+  int64_t bt = q.batch;
+  while (bt > 1 && geometry(q, bt, S).total > ws_bytes) bt = (bt + 1) / 2;
+  if (geometry(q, bt, S).total > ws_bytes) return cudaErrorInvalidValue;
+  if (bt < q.batch) fa = fb = nullptr;
+  for (int64_t t0 = 0; t0 < q.batch; t0 += bt) {
+    ZgemmProblem b = q;
+    b.batch = std::min(bt, q.batch - t0);
+    b.A = static_cast<const double2*>(q.A) + t0 * q.sAb;
+    b.B = static_cast<const double2*>(q.B) + t0 * q.sBb;
+    b.C = static_cast<double2*>(q.C) + t0 * q.sCb;
+    cudaError_t e = run_batch<S>(b, static_cast<uint8_t*>(ws), fa, fb, stream);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 template <int S>
-cudaError_t make_form(const void* X, int Lt, int N, bool as_b, void* dst, cudaStream_t stream) {
-  const Geometry g = geometry(Lt, N, S);
+cudaError_t make_form(const ZgemmProblem& q, bool as_b, void* dst, OzakiForm* form, cudaStream_t stream) {
+  const Geometry g = geometry(q, q.batch, S);
   uint8_t* d = static_cast<uint8_t*>(dst);
+  form->slices = d;
   if (!as_b) {
-    split_a<S>(X, reinterpret_cast<int8_t*>(d), reinterpret_cast<int*>(d + (g.sb - g.sa)), Lt, N, g, stream);
+    form->exps = reinterpret_cast<const int*>(d + (g.ea - g.sa));
+    split_a<S>(q, reinterpret_cast<int8_t*>(d), reinterpret_cast<int*>(d + (g.ea - g.sa)), g, stream);
     return cudaGetLastError();
   }
-  return split_b<S>(X, reinterpret_cast<int8_t*>(d), reinterpret_cast<int*>(d + (g.ea - g.sb)), Lt, N, g, stream);
+  form->exps = reinterpret_cast<const int*>(d + (g.fb - g.sb));
+  return split_b<S>(q, reinterpret_cast<int8_t*>(d), reinterpret_cast<int*>(d + (g.fb - g.sb)), g, stream);
+}
+
+ZgemmProblem mm1_problem(const void* A, const void* B, void* C, int64_t Lt, int64_t N) {
+  ZgemmProblem q{};
+  q.A = A; q.B = B; q.C = C; q.batch = Lt;
+  q.M = N; q.Nn = N; q.Kin = N; q.Ko = 1;
+  q.lda = N; q.sAo = 0; q.sAb = N * N;
+  q.ldb = N; q.sBo = 0; q.sBb = N * N;
+  q.ldc = N; q.sCb = N * N;
+  return q;
 }
 
 }  // namespace oz
 
-size_t ozaki_mm1_workspace_bytes(int64_t Lt, int64_t N, int slices) {
-  return oz::geometry(int(Lt), int(N), slices).total;
-}
-
-// A-form (row slices + row exponents) / B-form (column slices + column exponents) of one
-// operand, as one buffer: slices first, exponents after (256-byte aligned).
-size_t ozaki_form_bytes(int64_t Lt, int64_t N, int slices, bool as_b) {
-  const oz::Geometry g = oz::geometry(int(Lt), int(N), slices);
-  return as_b ? (g.ea - g.sb) + (g.total - g.fb) : (g.sb - g.sa) + (g.fb - g.ea);
-}
-
-cudaError_t launch_ozaki_form(const void* X, int64_t Lt, int64_t N, int slices, bool as_b, void* dst,
-                              OzakiForm* form, cudaStream_t stream) {
-  const oz::Geometry g = oz::geometry(int(Lt), int(N), slices);
-  form->slices = dst;
-  form->exps = reinterpret_cast<const int*>(static_cast<uint8_t*>(dst) + (as_b ? (g.ea - g.sb) : (g.sb - g.sa)));
-  switch (slices) {
-    case 4: return oz::make_form<4>(X, int(Lt), int(N), as_b, dst, stream);
-    case 5: return oz::make_form<5>(X, int(Lt), int(N), as_b, dst, stream);
-    case 6: return oz::make_form<6>(X, int(Lt), int(N), as_b, dst, stream);
-    case 7: return oz::make_form<7>(X, int(Lt), int(N), as_b, dst, stream);
-    default: return cudaErrorInvalidValue;
+#define OZ_DISPATCH(fn, ...)                               \
+  switch (slices) {                                        \
+    case 4: return oz::fn<4>(__VA_ARGS__);                 \
+    case 5: return oz::fn<5>(__VA_ARGS__);                 \
+    case 6: return oz::fn<6>(__VA_ARGS__);                 \
+    case 7: return oz::fn<7>(__VA_ARGS__);                 \
+    default: return cudaErrorInvalidValue;                 \
   }
-}
 
+size_t ozaki_workspace_bytes(const ZgemmProblem& q, int slices, int64_t max_batch) {
+  return oz::geometry(q, std::max<int64_t>(1, std::min(max_batch, q.batch)), slices).total;
+}
+size_t ozaki_mm1_workspace_bytes(int64_t Lt, int64_t N, int slices) {
+  return ozaki_workspace_bytes(oz::mm1_problem(nullptr, nullptr, nullptr, Lt, N), slices, Lt);
+}
+size_t ozaki_form_bytes(const ZgemmProblem& q, int slices, bool as_b) {
+  const oz::Geometry g = oz::geometry(q, q.batch, slices);
+  return as_b ? g.b_form() : g.a_form();
+}
+cudaError_t launch_ozaki_form(const ZgemmProblem& q, int slices, bool as_b, void* dst, OzakiForm* form,
+                              cudaStream_t stream) {
+  OZ_DISPATCH(make_form, q, as_b, dst, form, stream)
+}
+cudaError_t launch_ozaki_gemm(const ZgemmProblem& q, int slices, void* ws, size_t ws_bytes, cudaStream_t stream,
+                              const OzakiForm* fa, const OzakiForm* fb) {
+  OZ_DISPATCH(run_gemm, q, ws, ws_bytes, fa, fb, stream)
+}
 cudaError_t launch_ozaki_mm1(const void* A, const void* B, void* C, int64_t Lt, int64_t N, int slices, void* ws,
                              size_t ws_bytes, cudaStream_t stream, const OzakiForm* fa, const OzakiForm* fb) {
-  switch (slices) {
-    case 4: return oz::run_mm1<4>(A, B, C, int(Lt), int(N), ws, ws_bytes, fa, fb, stream);
-    case 5: return oz::run_mm1<5>(A, B, C, int(Lt), int(N), ws, ws_bytes, fa, fb, stream);
-    case 6: return oz::run_mm1<6>(A, B, C, int(Lt), int(N), ws, ws_bytes, fa, fb, stream);
-    case 7: return oz::run_mm1<7>(A, B, C, int(Lt), int(N), ws, ws_bytes, fa, fb, stream);
-    default: return cudaErrorInvalidValue;
-  }
+  return launch_ozaki_gemm(oz::mm1_problem(A, B, C, Lt, N), slices, ws, ws_bytes, stream, fa, fb);
 }
 
 cudaError_t launch_i8gemm_tn(const int8_t* A, const int8_t* B, int32_t* C, int64_t M, int64_t Nn, int64_t K,
@@ -635,7 +727,10 @@ cudaError_t launch_i8gemm_tn(const int8_t* A, const int8_t* B, int32_t* C, int64
   CUtensorMap ma, mb;
   if (!oz::map_i8(&ma, A, uint64_t(K), uint64_t(M), oz::BM) || !oz::map_i8(&mb, B, uint64_t(K), uint64_t(Nn), oz::BN))
     return cudaErrorInvalidValue;
-  oz::Params p{1, 0, int(M), 0, int(K), int(Nn), nullptr, nullptr, nullptr, C, nullptr, nullptr};
+  oz::Params p{};
+  p.Lt = 1; p.Mp = int(M); p.Nc = int(Nn / 2); p.Kp = int(K); p.Brows = int(Nn);
+  p.M = int(M); p.Nn = int(Nn); p.nch = 1; p.kchs = int(K / oz::BKB);
+  p.Craw = C;
   return oz::launch_gemm<1, true>(ma, mb, p, stream);
 }
 

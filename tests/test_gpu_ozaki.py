@@ -157,3 +157,78 @@ def test_executor_ozaki_leaf_form_cache_bitwise(monkeypatch):
     ctx.execute(64)
     again = {t: ctx.root_value(t, w.Lt) for t in roots}
     assert all(np.array_equal(again[t], roots[t]) for t in roots)
+
+
+def _run_gemm(ctx, op, A, B, Lt, N, S, s, out_shape, ws_bytes=None):
+    from paper_2511_02257_b200 import cc
+    full = cc.cc_gemm_ozaki_workspace_bytes(op, Lt, N, S, s)
+    ws = torch.empty(ws_bytes or full, dtype=torch.uint8, device="cuda")
+    C = torch.full((int(np.prod(out_shape)) * 2,), float("nan"), dtype=torch.float64, device="cuda")
+    ctx.gemm_ozaki(op, device_from(A), device_from(B), C, Lt, N, S, s, ws)
+    torch.cuda.synchronize()
+    return to_numpy_c(C, out_shape)
+
+
+@pytest.mark.parametrize("Lt,N,S", [(2, 8, 4), (1, 12, 64), (2, 16, 8), (1, 33, 2), (3, 24, 16)])
+def test_bm1_ozaki(ctx, Lt, N, S):
+    """BM1 (baryon x meson, M = S N^2 rows) on the Ozaki engine vs the oracle's BM1."""
+    from paper_2511_02257_b200 import cc
+    A = _phase_limited((Lt, S, N, N, N), 10 + N)
+    M = _phase_limited((Lt, N, N), 20 + N)
+    got = _run_gemm(ctx, cc.CC_BM1, A, M, Lt, N, S, 5, (Lt, S, N, N, N))
+    want = values.bm1(A, M)
+    err = float(np.max(np.abs(got - want) / np.abs(want)))
+    assert err <= 1e-10, err
+
+
+@pytest.mark.parametrize("Lt,N,S", [(2, 8, 4), (1, 12, 64), (2, 16, 64), (1, 24, 64), (1, 33, 8), (2, 20, 3)])
+def test_bb2_ozaki_split_k(ctx, Lt, N, S):
+    """BB2 (K = S N^2 up to 36864 complex terms: 1..5 split-K chunks of 8192, FP64 partials
+    summed in chunk order) vs the oracle's BB2; bit-identical on a repeat (deterministic)."""
+    from paper_2511_02257_b200 import cc
+    A = _phase_limited((Lt, S, N, N, N), 30 + N)
+    B = _phase_limited((Lt, S, N, N, N), 40 + N)
+    got = _run_gemm(ctx, cc.CC_BB2, A, B, Lt, N, S, 5, (Lt, N, N))
+    want = values.bb2(A, B)
+    err = float(np.max(np.abs(got - want) / np.abs(want)))
+    assert err <= 1e-10, err
+    again = _run_gemm(ctx, cc.CC_BB2, A, B, Lt, N, S, 5, (Lt, N, N))
+    assert np.array_equal(got, again)
+
+
+def test_gemm_ozaki_time_batches(ctx):
+    """A workspace that holds one time slice only: the engine runs the problem slice by slice,
+    same values as with the full workspace."""
+    from paper_2511_02257_b200 import cc
+    Lt, N, S = 4, 16, 8
+    A = _phase_limited((Lt, S, N, N, N), 51)
+    B = _phase_limited((Lt, S, N, N, N), 52)
+    one = cc.cc_gemm_ozaki_workspace_bytes(cc.CC_BB2, 1, N, S, 5)
+    got = _run_gemm(ctx, cc.CC_BB2, A, B, Lt, N, S, 5, (Lt, N, N), ws_bytes=one)
+    full = _run_gemm(ctx, cc.CC_BB2, A, B, Lt, N, S, 5, (Lt, N, N))
+    assert np.array_equal(got, full)
+
+
+def test_executor_ozaki_baryon_dags():
+    """c3 (nucleon) and c4 (two-baryon, capped pool with evictions) DAGs with every GEMM kind
+    on the Ozaki engine (flags bit 6): roots and correlators within 1e-10 of the oracle."""
+    from synth import dags
+    from oracle.dag import Dag
+    from oracle import lru, tree
+    from gpu_helpers import run_gpu, assert_roots_close, assert_corr_close
+    w = dags.config_c3(N=12, Lt=2, S=64)
+    dag = Dag(w)
+    _, roots, corr, st, ex = run_gpu(w, flags=64, arena_mb=1024)
+    r_or, c_or = values.run_workload(w, dag)
+    assert_roots_close(roots, r_or)
+    assert_corr_close(dag, r_or, corr, c_or)
+    w = dags.config_c4(N=8, Lt=1, S=4, n_trees=120, n_corr=4)
+    dag = Dag(w)
+    cap = 7 * 16 * 4 * 8 ** 3
+    for nu in (False, True):
+        _, roots, corr, st, ex = run_gpu(w, cap=cap, flags=64, evict_next_use=nu)
+        p = lru.plan(dag, tree.schedule(dag), cap, policy="next_use" if nu else "lru")
+        assert ex["h2d_bytes"] == p["h2d_bytes"] and ex["d2h_bytes"] == p["d2h_bytes"]
+        r_or, c_or = values.run_workload(w, dag)
+        assert_roots_close(roots, r_or)
+        assert_corr_close(dag, r_or, corr, c_or)
