@@ -173,38 +173,57 @@ __device__ __forceinline__ int scale_exponent(double m) {
 // Operand addressing of a (two-level K) problem, complex elements (ZgemmProblem layout):
 //   A(t, m, kk) = A + t sAb + (kk / Kin) sAo + m lda + kk % Kin
 //   B(t, kk, n) = B + t sBb + (kk / Kin) sBo + (kk % Kin) ldb + n
-__device__ __forceinline__ const double2* a_at(const ZgemmProblem& q, int t, int64_t m, int64_t kk) {
-  return static_cast<const double2*>(q.A) + t * q.sAb + (kk / q.Kin) * q.sAo + m * q.lda + kk % q.Kin;
+// (K = Ko Kin < 2^31: 32-bit index arithmetic)
+__device__ __forceinline__ const double2* a_at(const ZgemmProblem& q, int t, int64_t m, int kk) {
+  if (q.Ko == 1) return static_cast<const double2*>(q.A) + t * q.sAb + m * q.lda + kk;
+  const int ko = kk / int(q.Kin), ki = kk - ko * int(q.Kin);
+  return static_cast<const double2*>(q.A) + t * q.sAb + ko * q.sAo + m * q.lda + ki;
 }
-__device__ __forceinline__ const double2* b_at(const ZgemmProblem& q, int t, int64_t kk, int64_t n) {
-  return static_cast<const double2*>(q.B) + t * q.sBb + (kk / q.Kin) * q.sBo + (kk % q.Kin) * q.ldb + n;
+__device__ __forceinline__ const double2* b_at(const ZgemmProblem& q, int t, int kk, int64_t n) {
+  if (q.Ko == 1) return static_cast<const double2*>(q.B) + t * q.sBb + int64_t(kk) * q.ldb + n;
+  const int ko = kk / int(q.Kin), ki = kk - ko * int(q.Kin);
+  return static_cast<const double2*>(q.B) + t * q.sBb + ko * q.sBo + int64_t(ki) * q.ldb + n;
 }
 
-// One warp per row (t, m) of A: A_cat row slices + eA.  K index of A_cat: Re part of kk at kk,
-// Im part at Kc + kk (Kc = roundup(K, 32)); padding rows / columns are zero.
+constexpr int KSEG = 4096;   // K elements per warp in the row kernels (long BB2 rows in parallel)
+
+// Row scale exponents of A: grid (Mp/8, Lt, ceil(K/KSEG)), one warp per (row, K segment);
+// eA preset to INT_MIN (bytes 0x80), segments folded in with atomicMax.
+__global__ void __launch_bounds__(256) rowmax_kernel(ZgemmProblem q, int* __restrict__ eA, int Mp) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t i = int64_t(blockIdx.x) * 8 + warp;
+  const int t = blockIdx.y;
+  if (i >= q.M) return;
+  const int K = int(q.Kin * q.Ko);
+  const int k0 = int(blockIdx.z) * KSEG, k1 = min(K, k0 + KSEG);
+  double m = 0.0;
+  for (int j = k0 + lane; j < k1; j += 32) {
+    const double2 v = *a_at(q, t, i, j);
+    m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0 && m > 0.0) atomicMax(&eA[size_t(t) * Mp + i], scale_exponent(m));
+}
+
+// A_cat row slices: grid (Mp/8, Lt, ceil(Kc/KSEG)), one warp per (row, K segment).  K index
+// of A_cat: Re part of kk at kk, Im part at Kc + kk (Kc = roundup(K, 32)); padding rows /
+// columns are zero; a row left at INT_MIN by rowmax_kernel is all zero (exponent 0).
 template <int S>
 __global__ void __launch_bounds__(256) split_rows_kernel(ZgemmProblem q, int8_t* __restrict__ SA,
-                                                         int* __restrict__ eA, int Mp, int Kc) {
+                                                         const int* __restrict__ eA, int Mp, int Kc) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t i = int64_t(blockIdx.x) * 8 + warp;
   const int t = blockIdx.y;
   if (i >= Mp) return;
-  const int64_t K = q.Kin * q.Ko;
+  const int K = int(q.Kin * q.Ko);
   const bool live = i < q.M;
   const int Kp = 2 * Kc;
   const int nk = Kp / 64, nblk = Mp / 128;
-  double m = 0.0;
-  if (live)
-    for (int64_t j = lane; j < K; j += 32) {
-      const double2 v = *a_at(q, t, i, j);
-      m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
-    }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  const int e = scale_exponent(m);
-  if (lane == 0) eA[size_t(t) * Mp + i] = e;
-  const double sc = pow2(-e);
-  for (int j0 = lane * 4; j0 < Kc; j0 += 128) {
+  const int e0 = eA[size_t(t) * Mp + i];
+  const double sc = pow2(e0 < -100000 ? 0 : -e0);
+  const int j1 = min(Kc, int(blockIdx.z + 1) * KSEG);
+  for (int j0 = int(blockIdx.z) * KSEG + lane * 4; j0 < j1; j0 += 128) {
     uint32_t wr[S], wi[S];
 #pragma unroll
     for (int k = 0; k < S; ++k) wr[k] = wi[k] = 0;
@@ -237,11 +256,11 @@ __global__ void __launch_bounds__(256) colmax_kernel(ZgemmProblem q, int* __rest
   __shared__ double red[8][32];
   const int tid = threadIdx.x, c = tid & 31, r0 = tid >> 5;
   const int c0 = 32 * blockIdx.x, t = blockIdx.y;
-  const int64_t k0 = 128 * int64_t(blockIdx.z), K = q.Kin * q.Ko;
+  const int k0 = 128 * int(blockIdx.z), K = int(q.Kin * q.Ko);
   double m = 0.0;
   if (c0 + c < q.Nn) {
-    const int64_t k1 = k0 + 128 < K ? k0 + 128 : K;
-    for (int64_t k = k0 + r0; k < k1; k += 8) {
+    const int k1 = min(K, k0 + 128);
+    for (int k = k0 + r0; k < k1; k += 8) {
       const double2 v = *b_at(q, t, k, c0 + c);
       m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
     }
@@ -266,7 +285,7 @@ __global__ void __launch_bounds__(256) split_cols_kernel(ZgemmProblem q, int8_t*
   const int tid = threadIdx.x;
   const int g = blockIdx.x, t = blockIdx.y;
   const int c0 = 32 * g;
-  const int64_t K = q.Kin * q.Ko;
+  const int K = int(q.Kin * q.Ko);
   const int Kp = 2 * Kc, Brows = 2 * Nc;
   const int nk = Kp / 64, nblk = Brows / 64;
   if (tid < 32) {
@@ -484,7 +503,8 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
           }
         }
         if (r < p.M) {
-          const double se = pow2(p.eA[size_t(t) * p.Mp + r]);
+          const int ea = p.eA[size_t(t) * p.Mp + r];
+          const double se = pow2(ea < -100000 ? 0 : ea);        // INT_MIN: an all-zero row
           const int cbase = nb * 32;
           const int* f = p.fB + size_t(t) * p.Nc + cbase;
           // one K chunk: the tile itself; else this chunk's FP64 partial (reduced in order later)
@@ -589,8 +609,14 @@ cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const Para
 }
 
 template <int S>
-void split_a(const ZgemmProblem& q, int8_t* SA, int* eA, const Geometry& g, cudaStream_t stream) {
-  split_rows_kernel<S><<<dim3(g.Mp / 8, unsigned(q.batch)), 256, 0, stream>>>(q, SA, eA, g.Mp, g.Kc);
+cudaError_t split_a(const ZgemmProblem& q, int8_t* SA, int* eA, const Geometry& g, cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(eA, 0x80, size_t(q.batch) * g.Mp * 4, stream);   // INT_MIN-like
+  if (e != cudaSuccess) return e;
+  const int64_t K = q.Kin * q.Ko;
+  rowmax_kernel<<<dim3(g.Mp / 8, unsigned(q.batch), unsigned((K + KSEG - 1) / KSEG)), 256, 0, stream>>>(q, eA, g.Mp);
+  split_rows_kernel<S><<<dim3(g.Mp / 8, unsigned(q.batch), unsigned((g.Kc + KSEG - 1) / KSEG)), 256, 0, stream>>>(
+      q, SA, eA, g.Mp, g.Kc);
+  return cudaGetLastError();
 }
 
 template <int S>
@@ -617,7 +643,8 @@ cudaError_t run_batch(const ZgemmProblem& q, uint8_t* w, const OzakiForm* fa, co
     SA = static_cast<const int8_t*>(fa->slices);
     eA = fa->exps;
   } else {
-    split_a<S>(q, reinterpret_cast<int8_t*>(w + g.sa), reinterpret_cast<int*>(w + g.ea), g, stream);
+    cudaError_t e = split_a<S>(q, reinterpret_cast<int8_t*>(w + g.sa), reinterpret_cast<int*>(w + g.ea), g, stream);
+    if (e != cudaSuccess) return e;
   }
   if (fb) {
     SB = static_cast<const int8_t*>(fb->slices);
@@ -670,8 +697,7 @@ cudaError_t make_form(const ZgemmProblem& q, bool as_b, void* dst, OzakiForm* fo
   form->slices = d;
   if (!as_b) {
     form->exps = reinterpret_cast<const int*>(d + (g.ea - g.sa));
-    split_a<S>(q, reinterpret_cast<int8_t*>(d), reinterpret_cast<int*>(d + (g.ea - g.sa)), g, stream);
-    return cudaGetLastError();
+    return split_a<S>(q, reinterpret_cast<int8_t*>(d), reinterpret_cast<int*>(d + (g.ea - g.sa)), g, stream);
   }
   form->exps = reinterpret_cast<const int*>(d + (g.fb - g.sb));
   return split_b<S>(q, reinterpret_cast<int8_t*>(d), reinterpret_cast<int*>(d + (g.fb - g.sb)), g, stream);
