@@ -175,6 +175,8 @@ struct cc_ctx {
   cudaEvent_t ev_cs2 = nullptr;
   cudaStream_t hs2 = nullptr;       // second H2D stream: wait-free leaf copies alternate with hs
   cudaEvent_t ev_hs2 = nullptr;
+  cudaStream_t hsx[3] = {nullptr, nullptr, nullptr};   // op-by-op: extra H2D streams
+  cudaEvent_t ev_hsx[3] = {nullptr, nullptr, nullptr};
   cudaGraphExec_t gexec_df = nullptr;
   int64_t df_gemm_items = 0, df_trace_items = 0;
   unsigned long long* df_prof = nullptr;   // per-item timeline (flags bit 5)
@@ -243,6 +245,12 @@ struct cc_ctx {
     cs2 = nullptr;
     if (hs2) cudaStreamDestroy(hs2);
     hs2 = nullptr;
+    for (int k = 0; k < 3; ++k) {
+      if (hsx[k]) cudaStreamDestroy(hsx[k]);
+      if (ev_hsx[k]) cudaEventDestroy(ev_hsx[k]);
+      hsx[k] = nullptr;
+      ev_hsx[k] = nullptr;
+    }
     if (ev_hs2) cudaEventDestroy(ev_hs2);
     ev_hs2 = nullptr;
     if (ev_cs2) cudaEventDestroy(ev_cs2);
@@ -1469,13 +1477,32 @@ int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cud
   const int64_t per_t_m = 16LL * g.N * g.N;
   cudaStream_t st[3] = {ctx->cs, ctx->hs, ctx->ds};
   int nl = 0;
+  // CC_OPBYOP_H2D_STREAMS (1..4, default 1; c4 measured no gain: its copies wait for freed pool
+  // memory, not behind each other): H2D copies round-robin over that many streams, with
+  // their same-stream dependencies made explicit (op.same_deps), so a copy that waits for
+  // memory to be freed does not hold back later copies that could already run
+  static const int n_h2d = std::max(1, std::min(4, getenv("CC_OPBYOP_H2D_STREAMS") ? atoi(getenv("CC_OPBYOP_H2D_STREAMS")) : 1));
+  cudaStream_t h2d[4] = {ctx->hs, nullptr, nullptr, nullptr};
+  for (int k = 1; k < n_h2d; ++k) {
+    if (!ctx->hsx[k - 1]) {
+      ck(cudaStreamCreateWithFlags(&ctx->hsx[k - 1], cudaStreamNonBlocking), "stream");
+      ck(cudaEventCreateWithFlags(&ctx->ev_hsx[k - 1], cudaEventDisableTiming), "event");
+    }
+    h2d[k] = ctx->hsx[k - 1];
+  }
   ck(cudaEventRecord(ctx->ev_start, ctx->cs), "event");
   ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_start, 0), "wait");
   ck(cudaStreamWaitEvent(ctx->ds, ctx->ev_start, 0), "wait");
+  for (int k = 1; k < n_h2d; ++k) ck(cudaStreamWaitEvent(h2d[k], ctx->ev_start, 0), "wait");
+  size_t rr = 0;
   for (size_t i = 0; i < ctx->pp.ops.size(); ++i) {
     const PhysOp& op = ctx->pp.ops[i];
     if (op.stream == S_NONE) continue;
     cudaStream_t s = st[op.stream];
+    if (op.stream == S_H2D && n_h2d > 1) {
+      s = h2d[rr++ % size_t(n_h2d)];
+      for (int32_t d : op.same_deps) ck(cudaStreamWaitEvent(s, ctx->events[size_t(d)], 0), "wait");
+    }
     for (int32_t d : op.deps) ck(cudaStreamWaitEvent(s, ctx->events[size_t(d)], 0), "wait");
     const Node& n = g.nodes[size_t(op.node)];
     switch (op.kind) {
@@ -1525,6 +1552,10 @@ int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cud
                       ctx->term_coef, ctx->cs),
      "correlate kernel");
   ++nl;
+  for (int k = 1; k < n_h2d; ++k) {                 // join the extra H2D streams
+    ck(cudaEventRecord(ctx->ev_hsx[k - 1], h2d[k]), "event");
+    ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_hsx[k - 1], 0), "wait");
+  }
   ck(cudaEventRecord(ctx->ev_h_end, ctx->hs), "event");
   ck(cudaEventRecord(ctx->ev_d_end, ctx->ds), "event");
   ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_h_end, 0), "wait");

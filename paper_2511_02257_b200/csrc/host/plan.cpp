@@ -277,12 +277,14 @@ void RangeTracker::split(int64_t at) {
   pieces_[at] = hi;
 }
 
-void RangeTracker::access(int64_t off, int64_t bytes, int stream, int32_t op, std::vector<int32_t>& deps) {
+void RangeTracker::access(int64_t off, int64_t bytes, int stream, int32_t op, std::vector<int32_t>& deps,
+                          std::vector<int32_t>* same) {
   split(off);
   split(off + bytes);
   for (auto it = pieces_.find(off); it != pieces_.end() && it->first < off + bytes; ++it) {
     for (int s = 0; s < 3; ++s)
       if (s != stream && it->second.last[s] >= 0) deps.push_back(it->second.last[s]);
+    if (same && it->second.last[stream] >= 0) same->push_back(it->second.last[stream]);
     it->second.last[stream] = op;
   }
 }
@@ -319,11 +321,11 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
         dev_off[x] = off;
         op.stream = S_H2D;
         op.dev_off = off;
-        dtr.access(off, rb, S_H2D, me, op.deps);
+        dtr.access(off, rb, S_H2D, me, op.deps, &op.same_deps);
         if (!nd.leaf()) {                                       // re-fetch of an evicted intermediate
           op.host_off = host_off[x];
           if (d2h_op[x] >= 0) op.deps.push_back(d2h_op[x]);
-          htr.access(host_off[x], rb, S_H2D, me, op.deps);
+          htr.access(host_off[x], rb, S_H2D, me, op.deps, &op.same_deps);
         }
         ready[x] = me;
         ready_stream[x] = S_H2D;
@@ -398,10 +400,14 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
     }
     std::sort(op.deps.begin(), op.deps.end());
     op.deps.erase(std::unique(op.deps.begin(), op.deps.end()), op.deps.end());
+    std::sort(op.same_deps.begin(), op.same_deps.end());
+    op.same_deps.erase(std::unique(op.same_deps.begin(), op.same_deps.end()), op.same_deps.end());
     pp.ops.push_back(std::move(op));
   }
-  for (auto& op : pp.ops)
+  for (auto& op : pp.ops) {
     for (int32_t d : op.deps) pp.ops[size_t(d)].source = true;
+    for (int32_t d : op.same_deps) pp.ops[size_t(d)].source = true;
+  }
   pp.pool_high_water = dev.high_water();
   pp.host_pool_bytes = host_cap;
   return pp;

@@ -58,7 +58,8 @@ class RangeTracker {
  public:
   explicit RangeTracker(int64_t capacity = 0);
   // ops that a new access by `op` on `stream` must wait for (other streams only)
-  void access(int64_t off, int64_t bytes, int stream, int32_t op, std::vector<int32_t>& deps);
+  void access(int64_t off, int64_t bytes, int stream, int32_t op, std::vector<int32_t>& deps,
+              std::vector<int32_t>* same = nullptr);
  private:
   struct Piece { int64_t end; int32_t last[3]; };
   std::map<int64_t, Piece> pieces_;
@@ -80,6 +81,8 @@ struct PhysOp {
   int32_t loc_a = LOC_POOL, loc_b = LOC_POOL;
   int64_t off_a = -1, off_b = -1;    // operand pool offsets (CONTRACT)
   std::vector<int32_t> deps;         // ops on other streams that must complete first
+  std::vector<int32_t> same_deps;    // H2D ops: earlier H2D ops it depends on (implicit in a single
+                                     // H2D stream; explicit when H2D copies use several streams)
   bool source = false;               // some later op waits on this one (record an event)
 };
 

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--device-leaves", action="store_true")
     ap.add_argument("--ozaki", action="store_true", help="MM1 on the tcgen05 INT8 Ozaki engine (execute flags bit 6)")
     ap.add_argument("--next-use", action="store_true", help="next-use (Belady) eviction, reading E-9")
+    ap.add_argument("--op-by-op", action="store_true", help="op-by-op executor (execute flags bit 4)")
     ap.add_argument("--breakdown", action="store_true",
                     help="one more op-by-op execute with every kernel timed (flags bit 1): time per op kind")
     a = ap.parse_args()
@@ -82,7 +83,7 @@ def main():
             ctx.set_leaf(u, h)
     print("part %d/%d: time slices [%d, %d), %d trees" % (a.part, a.parts, pt0, pt1, len(ctx.part_trees())), flush=True)
     for rep in range(2):
-        ex = ctx.execute(cc.EXEC_OZAKI_MM1 if a.ozaki else 0)
+        ex = ctx.execute((cc.EXEC_OZAKI_MM1 if a.ozaki else 0) | (cc.EXEC_OP_BY_OP if a.op_by_op else 0))
         moved = ex["h2d_bytes"] + ex["d2h_bytes"]
         print("execute %d%s: %.1f ms (copies done %.1f ms); moved %.2f GB -> PCIe bound %.1f ms; flops %.3g -> "
               "FP64 bound %.1f ms" % (rep, " (Ozaki MM1, op-by-op)" if a.ozaki else "", ex["seconds"] * 1e3, ex["copy_seconds"] * 1e3, moved / 1e9,
