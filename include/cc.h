@@ -253,7 +253,8 @@ cc_status cc_gemm_ozaki(cc_ctx* ctx, int32_t op, const void* A, const void* B, v
                         int32_t S, int32_t n_slices, void* workspace, size_t workspace_bytes);
 /* The INT8 tcgen05 GEMM alone (pins the UMMA descriptors bit-exactly in the tests):
  * C[m][n] = sum_k A[m][k] B[n][k]; A int8 [M][K], B int8 [Nn][K] row-major, C int32 [M][Nn];
- * M % 128 == 0, Nn % 64 == 0, K % 64 == 0, K <= 2^17 (no INT32 overflow). */
+ * M % 128 == 0, Nn % 192 == 0 (a multiple of the tile width, 64 or 96 by build), K % 64 == 0,
+ * K <= 2^17 (no INT32 overflow). */
 cc_status cc_i8gemm_tn(cc_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C, int32_t M, int32_t Nn, int32_t K);
 /* Synthetic leaf values (input generation, not the method; same recipe as synth/rng.py):
  * n complex elements starting at flat element e0 of leaf `leaf_id`, written to dev. */

@@ -2265,8 +2265,8 @@ cc_status cc_i8gemm_tn(cc_ctx* ctx, const int8_t* A, const int8_t* B, int32_t* C
   if (!ctx) return CC_E_INVAL;
   API_BEGIN
   ctx->need_device();
-  if (!A || !B || !C || M <= 0 || Nn <= 0 || K <= 0 || M % 128 || Nn % 64 || K % 64)
-    throw Error(CC_E_INVAL, "bad kernel arguments (M % 128, Nn % 64, K % 64)");
+  if (!A || !B || !C || M <= 0 || Nn <= 0 || K <= 0 || M % 128 || Nn % 192 || K % 64)
+    throw Error(CC_E_INVAL, "bad kernel arguments (M % 128, Nn % 192, K % 64)");
   ck(launch_i8gemm_tn(A, B, C, M, Nn, K, ctx->cs), "int8 tcgen05 GEMM");
   API_END
 }

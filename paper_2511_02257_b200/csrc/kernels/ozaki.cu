@@ -44,20 +44,35 @@ namespace cc {
 namespace oz {
 
 constexpr int BM = 128;     // CTA rows (UMMA M)
-constexpr int BN = 64;      // CTA B_cat^T rows (UMMA N) = 32 complex output columns
 constexpr int BKB = 64;     // K bytes per stage = one SWIZZLE_64B smem row (SW32 measured slower)
 constexpr int UK = 32;      // K per kind::i8 MMA
 constexpr int A_TILE = BM * BKB;    // 8 KB
-constexpr int B_TILE = BN * BKB;    // 4 KB
+
+// Tile width: BN B_cat^T rows per tile (UMMA N) = BN/2 complex output columns (Cr | Ci).
+// 64 for small problems, 96 for wide ones (pick_bn): 1.5x the MACs per MMA instruction, the
+// S diagonal accumulators then fill S*96 of the 512 TMEM columns (S <= 5).
+template <int BN_>
+struct Tile {
+  static constexpr int BN = BN_;
+  static constexpr int CG = BN_ / 2;                   // complex output columns per tile
+  static constexpr int NEPI = BN_ > 64 ? 8 : 4;        // epilogue warps: lane quarters x column halves
+  static constexpr int CPW = CG / (NEPI / 4);          // complex columns per epilogue warp
+  static constexpr int B_TILE = BN_ * BKB;             // 4 / 6 KB
+  // instruction descriptor kind::i8: D = S32 (bits 4-5 = 2), A, B signed (bits 7-9, 10-12 =
+  // 1), both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28
+  static constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN_ >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+  static_assert(BN_ == 64 || BN_ == 96, "tile width");
+};
 constexpr int SMEM_BUDGET = 222 * 1024;
 
-template <int S>
+template <int S, int BN>
 struct Cfg {
-  static constexpr int STAGE = S * (A_TILE + B_TILE);
+  static constexpr int STAGE = S * (A_TILE + Tile<BN>::B_TILE);
   static constexpr int STAGES = (SMEM_BUDGET / STAGE) > 4 ? 4 : (SMEM_BUDGET / STAGE);
   static constexpr int SMEM = STAGES * STAGE + 1024;
   static_assert(STAGES >= 2, "too many slices for the stage budget");
   static_assert(S * BN <= 512, "accumulators exceed TMEM");
+  static_assert(BN == 64 || BN == 96, "tile width");
 };
 
 struct Params {
@@ -111,15 +126,11 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                : "memory");
 }
 
-// Instruction descriptor kind::i8: D = S32 (bits 4-5 = 2), A, B signed (bits 7-9, 10-12 = 1),
-// both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28.
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
-
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t acc) {
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(acc)
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -135,6 +146,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
         "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -271,40 +287,41 @@ __global__ void __launch_bounds__(256) colmax_kernel(ZgemmProblem q, int* __rest
 #pragma unroll
     for (int r = 1; r < 8; ++r) m = fmax(m, red[r][tid]);
     m = fmax(m, red[0][tid]);
-    if (m > 0.0) atomicMax(&fB[size_t(t) * Nc + c0 + tid], scale_exponent(m));
+    if (m > 0.0 && c0 + tid < Nc) atomicMax(&fB[size_t(t) * Nc + c0 + tid], scale_exponent(m));
   }
 }
 
-// B_cat^T row slices: grid (Nc/32, Lt, Kc/128), one CTA per (32-column group g, t, 128-row
+// B_cat^T row slices: grid (Nc/CG, Lt, Kc/128), one CTA per (CG-column group g, t, 128-row
 // chunk of k).  A column left at INT_MIN by colmax_kernel is all zero (exponent 0).
-template <int S>
+template <int S, int BN>
 __global__ void __launch_bounds__(256) split_cols_kernel(ZgemmProblem q, int8_t* __restrict__ SB,
                                                          const int* __restrict__ fB, int Nc, int Kc) {
-  __shared__ double2 tile[32][33];
-  __shared__ int ecol[32];
+  constexpr int CG = Tile<BN>::CG, B_TILE = Tile<BN>::B_TILE;
+  __shared__ double2 tile[32][CG + 1];
+  __shared__ int ecol[CG];
   const int tid = threadIdx.x;
   const int g = blockIdx.x, t = blockIdx.y;
-  const int c0 = 32 * g;
+  const int c0 = CG * g;
   const int K = int(q.Kin * q.Ko);
   const int Kp = 2 * Kc, Brows = 2 * Nc;
-  const int nk = Kp / 64, nblk = Brows / 64;
-  if (tid < 32) {
+  const int nk = Kp / 64, nblk = Brows / BN;
+  if (tid < CG) {
     const int e = fB[size_t(t) * Nc + c0 + tid];
     ecol[tid] = e < -100000 ? 0 : e;
   }
   const int kend = min(Kc, 128 * int(blockIdx.z + 1));
   for (int k0 = 128 * blockIdx.z; k0 < kend; k0 += 32) {
     __syncthreads();
-    for (int idx = tid; idx < 1024; idx += 256) {
-      const int kr = idx >> 5, c = idx & 31;
+    for (int idx = tid; idx < 32 * CG; idx += 256) {
+      const int kr = idx / CG, c = idx % CG;
       double2 v = make_double2(0.0, 0.0);
       if (k0 + kr < K && c0 + c < q.Nn) v = *b_at(q, t, k0 + kr, c0 + c);
       tile[kr][c] = v;
     }
     __syncthreads();
-    for (int item = tid; item < 512; item += 256) {
+    for (int item = tid; item < 16 * CG; item += 256) {
       const int kq = item & 3, h = (item >> 2) & 1, rT = item >> 3;
-      const int c = rT & 31, part = rT >> 5;
+      const int c = rT % CG, part = rT / CG;
       const double sc = pow2(-ecol[c]);
       uint32_t lo[S], hi[S];
 #pragma unroll
@@ -326,7 +343,7 @@ __global__ void __launch_bounds__(256) split_cols_kernel(ZgemmProblem q, int8_t*
       }
 #pragma unroll
       for (int k = 0; k < S; ++k)
-        *reinterpret_cast<uint2*>(SB + tiled_off<S, 64>(t, 64 * g + rT, h * Kc + k0 + kq * 8, nblk, nk) +
+        *reinterpret_cast<uint2*>(SB + tiled_off<S, BN>(t, BN * g + rT, h * Kc + k0 + kq * 8, nblk, nk) +
                                   k * B_TILE) = make_uint2(lo[k], hi[k]);
     }
   }
@@ -359,10 +376,12 @@ __global__ void ozaki_reduce_kernel(Params p) {
 // columns; the epilogue drains them in order d = 0..S-1 and releases each one (drained[d])
 // as soon as it is in registers, so the next tile's MMAs into diagonal d start while the
 // epilogue is still converting and storing.
-template <int S, bool RAW>
-__global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
+template <int S, bool RAW, int BN>
+__global__ void __launch_bounds__((Tile<BN>::NEPI + 2) * 32, 1) ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                                                             const __grid_constant__ CUtensorMap mapB, Params p) {
-  using C = Cfg<S>;
+  using C = Cfg<S, BN>;
+  constexpr int CG = Tile<BN>::CG, NEPI = Tile<BN>::NEPI, CPW = Tile<BN>::CPW, B_TILE = Tile<BN>::B_TILE;
+  constexpr uint32_t IDESC = Tile<BN>::IDESC;
   extern __shared__ __align__(1024) uint8_t dsm[];
   __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES], tfull, drained[S];
   __shared__ uint32_t tmem_slot;
@@ -382,7 +401,7 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
       dev::mbar_init(&empty[s], 1);
     }
     dev::mbar_init(&tfull, 1);
-    for (int d = 0; d < S; ++d) dev::mbar_init(&drained[d], 4);
+    for (int d = 0; d < S; ++d) dev::mbar_init(&drained[d], NEPI);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -400,7 +419,7 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
     t = r / (ntn * ntm);
   };
 
-  if (warp == 4) {
+  if (warp == NEPI) {
     if (lane == 0) {
       int it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -425,7 +444,7 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == NEPI + 1) {
     if (lane == 0) {
       int it = 0, n = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++n) {
@@ -448,7 +467,7 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
 #pragma unroll
               for (int ks = 0; ks < BKB / UK; ++ks)
                 mma_i8(tmem + uint32_t(d * BN), sw64_desc(sa + i * A_TILE + ks * UK),
-                       sw64_desc(sb + (d - i) * B_TILE + ks * UK), ((kc - kc0) | i | ks) != 0);
+                       sw64_desc(sb + (d - i) * B_TILE + ks * UK), IDESC, ((kc - kc0) | i | ks) != 0);
           }
           mma_commit(&empty[st]);
         }
@@ -462,42 +481,44 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
       decode(tile, t, mb, nb, ch);
       dev::mbar_wait(&tfull, n & 1);
       tc_fence_after();
-      const int r = mb * BM + warp * 32 + lane;                 // row of this thread (TMEM lane)
-      const uint32_t tl = tmem + (uint32_t(warp * 32) << 16);
+      const int quarter = warp & 3, half = warp >> 2;            // TMEM lane quarter, column half
+      const int r = mb * BM + quarter * 32 + lane;                // row of this thread (TMEM lane)
+      const uint32_t tl = tmem + (uint32_t(quarter * 32) << 16);
       if constexpr (RAW) {
+        if (half == 0) {
 #pragma unroll
-        for (int q = 0; q < BN / 16; ++q) {
-          int v[16];
-          tmem_ld16(tl + q * 16, v);
-          tmem_wait_ld();
-          if (q == BN / 16 - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) dev::mbar_arrive(&drained[0]);
+          for (int q = 0; q < BN / 16; ++q) {
+            int v[16];
+            tmem_ld16(tl + q * 16, v);
+            tmem_wait_ld();
+            if (q == BN / 16 - 1) tc_fence_before();
+            int* dst = p.Craw + size_t(r) * p.Brows + nb * BN + q * 16;
+#pragma unroll
+            for (int u = 0; u < 16; u += 4)
+              *reinterpret_cast<int4*>(dst + u) = make_int4(v[u], v[u + 1], v[u + 2], v[u + 3]);
           }
-          int* dst = p.Craw + size_t(r) * p.Brows + nb * BN + q * 16;
-#pragma unroll
-          for (int u = 0; u < 16; u += 4)
-            *reinterpret_cast<int4*>(dst + u) = make_int4(v[u], v[u + 1], v[u + 2], v[u + 3]);
         }
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&drained[0]);
       } else {
-        double ar[32], ai[32];
+        double ar[CPW], ai[CPW];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) ar[q] = ai[q] = 0.0;
+        for (int q = 0; q < CPW; ++q) ar[q] = ai[q] = 0.0;
 #pragma unroll 1
         for (int d = 0; d < S; ++d) {          // most significant accumulator first (fixed order)
-          int vr[32], vi[32];
-          tmem_ld16(tl + uint32_t(d * BN), *reinterpret_cast<int(*)[16]>(&vr[0]));
-          tmem_ld16(tl + uint32_t(d * BN + 16), *reinterpret_cast<int(*)[16]>(&vr[16]));
-          tmem_ld16(tl + uint32_t(d * BN + 32), *reinterpret_cast<int(*)[16]>(&vi[0]));
-          tmem_ld16(tl + uint32_t(d * BN + 48), *reinterpret_cast<int(*)[16]>(&vi[16]));
+          int vr[CPW], vi[CPW];
+#pragma unroll
+          for (int q = 0; q < CPW; q += 8) {
+            tmem_ld8(tl + uint32_t(d * BN + half * CPW + q), &vr[q]);
+            tmem_ld8(tl + uint32_t(d * BN + CG + half * CPW + q), &vi[q]);
+          }
           tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) dev::mbar_arrive(&drained[d]);
           const double w = pow2(-12 - 8 * d);
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
+          for (int q = 0; q < CPW; ++q) {
             ar[q] = fma(double(vr[q]), w, ar[q]);
             ai[q] = fma(double(vi[q]), w, ai[q]);
           }
@@ -505,13 +526,13 @@ __global__ void __launch_bounds__(192, 1) ozaki_gemm_kernel(const __grid_constan
         if (r < p.M) {
           const int ea = p.eA[size_t(t) * p.Mp + r];
           const double se = pow2(ea < -100000 ? 0 : ea);        // INT_MIN: an all-zero row
-          const int cbase = nb * 32;
+          const int cbase = nb * CG + half * CPW;
           const int* f = p.fB + size_t(t) * p.Nc + cbase;
           // one K chunk: the tile itself; else this chunk's FP64 partial (reduced in order later)
           double* dst = p.nch == 1 ? p.C + 2 * (size_t(t) * p.sCb + size_t(r) * p.ldc)
                                    : p.P + 2 * (((size_t(ch) * p.Lt + t) * p.Mp + r) * p.Nc);
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
+          for (int q = 0; q < CPW; ++q) {
             const int c = cbase + q;
             if (c < p.Nn) {
               const double sf = se * pow2(f[q] < -100000 ? 0 : f[q]);   // exact: a power of two
@@ -565,11 +586,15 @@ struct Geometry {
 
 constexpr int KCH_BYTES = 16384;   // K bytes per chunk: |acc| <= 7 * 2^14 * 16384 < 2^31
 
-Geometry geometry(const ZgemmProblem& q, int64_t Lt, int S) {
+// Tile width for a problem: 96 when the output is wide enough that padding to 48 columns
+// costs <= 3 % and the S accumulators fit TMEM (S <= 5), else 64.
+int pick_bn(const ZgemmProblem& q, int S) { return q.Nn >= 512 && S * 96 <= 512 ? 96 : 64; }
+
+Geometry geometry(const ZgemmProblem& q, int64_t Lt, int S, int BN) {
   Geometry g;
   const int64_t K = q.Kin * q.Ko;
   g.Mp = int((q.M + BM - 1) / BM * BM);
-  g.Nc = int((q.Nn + 31) / 32 * 32);
+  g.Nc = int((q.Nn + BN / 2 - 1) / (BN / 2) * (BN / 2));
   g.Kc = int((K + 31) / 32 * 32);
   g.Kp = 2 * g.Kc;
   g.Brows = 2 * g.Nc;
@@ -596,15 +621,15 @@ int num_sms() {
   return n;
 }
 
-template <int S, bool RAW>
+template <int S, bool RAW, int BN>
 cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t stream) {
-  using C = Cfg<S>;
-  auto k = ozaki_gemm_kernel<S, RAW>;
+  using C = Cfg<S, BN>;
+  auto k = ozaki_gemm_kernel<S, RAW, BN>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   const int64_t tiles = int64_t(p.Brows / BN) * (p.Mp / BM) * (RAW ? 1 : p.Lt) * p.nch;
   const int grid = int(tiles < num_sms() ? tiles : num_sms());
-  k<<<grid, 192, C::SMEM, stream>>>(ma, mb, p);
+  k<<<grid, (Tile<BN>::NEPI + 2) * 32, C::SMEM, stream>>>(ma, mb, p);
   return cudaGetLastError();
 }
 
@@ -619,22 +644,22 @@ cudaError_t split_a(const ZgemmProblem& q, int8_t* SA, int* eA, const Geometry& 
   return cudaGetLastError();
 }
 
-template <int S>
+template <int S, int BN>
 cudaError_t split_b(const ZgemmProblem& q, int8_t* SB, int* fB, const Geometry& g, cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(fB, 0x80, size_t(q.batch) * g.Nc * 4, stream);   // INT_MIN-like
   if (e != cudaSuccess) return e;
   const int64_t K = q.Kin * q.Ko;
-  colmax_kernel<<<dim3(g.Nc / 32, unsigned(q.batch), unsigned((K + 127) / 128)), 256, 0, stream>>>(q, fB, g.Nc);
-  split_cols_kernel<S><<<dim3(g.Nc / 32, unsigned(q.batch), unsigned((g.Kc + 127) / 128)), 256, 0, stream>>>(q, SB, fB,
+  colmax_kernel<<<dim3((g.Nc + 31) / 32, unsigned(q.batch), unsigned((K + 127) / 128)), 256, 0, stream>>>(q, fB, g.Nc);
+  split_cols_kernel<S, BN><<<dim3(g.Nc / Tile<BN>::CG, unsigned(q.batch), unsigned((g.Kc + 127) / 128)), 256, 0, stream>>>(q, SB, fB,
                                                                                                           g.Nc, g.Kc);
   return cudaGetLastError();
 }
 
 // One batch (q.batch time slices): split what is not pre-split, GEMM, split-K reduction.
-template <int S>
+template <int S, int BN>
 cudaError_t run_batch(const ZgemmProblem& q, uint8_t* w, const OzakiForm* fa, const OzakiForm* fb,
                       cudaStream_t stream) {
-  const Geometry g = geometry(q, q.batch, S);
+  const Geometry g = geometry(q, q.batch, S, BN);
   const int8_t* SA = reinterpret_cast<int8_t*>(w + g.sa);
   const int* eA = reinterpret_cast<int*>(w + g.ea);
   const int8_t* SB = reinterpret_cast<int8_t*>(w + g.sb);
@@ -650,7 +675,7 @@ cudaError_t run_batch(const ZgemmProblem& q, uint8_t* w, const OzakiForm* fa, co
     SB = static_cast<const int8_t*>(fb->slices);
     fB = fb->exps;
   } else {
-    cudaError_t e = split_b<S>(q, reinterpret_cast<int8_t*>(w + g.sb), reinterpret_cast<int*>(w + g.fb), g, stream);
+    cudaError_t e = split_b<S, BN>(q, reinterpret_cast<int8_t*>(w + g.sb), reinterpret_cast<int*>(w + g.fb), g, stream);
     if (e != cudaSuccess) return e;
   }
   cudaError_t e = cudaGetLastError();
@@ -663,7 +688,7 @@ cudaError_t run_batch(const ZgemmProblem& q, uint8_t* w, const OzakiForm* fa, co
   p.eA = eA; p.fB = fB; p.C = static_cast<double*>(q.C);
   p.P = g.nch > 1 ? reinterpret_cast<double*>(w + g.part) : nullptr;
   p.SA = SA; p.SB = SB;
-  e = launch_gemm<S, false>(ma, mb, p, stream);
+  e = launch_gemm<S, false, BN>(ma, mb, p, stream);
   if (e != cudaSuccess || g.nch == 1) return e;
   ozaki_reduce_kernel<<<num_sms() * 4, 256, 0, stream>>>(p);
   return cudaGetLastError();
@@ -671,12 +696,12 @@ cudaError_t run_batch(const ZgemmProblem& q, uint8_t* w, const OzakiForm* fa, co
 
 // The whole problem in batches of time slices that fit the workspace (pre-split forms only
 // when it fits in one batch).
-template <int S>
+template <int S, int BN>
 cudaError_t run_gemm(const ZgemmProblem& q, void* ws, size_t ws_bytes, const OzakiForm* fa, const OzakiForm* fb,
                      cudaStream_t stream) {
   int64_t bt = q.batch;
-  while (bt > 1 && geometry(q, bt, S).total > ws_bytes) bt = (bt + 1) / 2;
-  if (geometry(q, bt, S).total > ws_bytes) return cudaErrorInvalidValue;
+  while (bt > 1 && geometry(q, bt, S, BN).total > ws_bytes) bt = (bt + 1) / 2;
+  if (geometry(q, bt, S, BN).total > ws_bytes) return cudaErrorInvalidValue;
   if (bt < q.batch) fa = fb = nullptr;
   for (int64_t t0 = 0; t0 < q.batch; t0 += bt) {
     ZgemmProblem b = q;
@@ -684,15 +709,15 @@ cudaError_t run_gemm(const ZgemmProblem& q, void* ws, size_t ws_bytes, const Oza
     b.A = static_cast<const double2*>(q.A) + t0 * q.sAb;
     b.B = static_cast<const double2*>(q.B) + t0 * q.sBb;
     b.C = static_cast<double2*>(q.C) + t0 * q.sCb;
-    cudaError_t e = run_batch<S>(b, static_cast<uint8_t*>(ws), fa, fb, stream);
+    cudaError_t e = run_batch<S, BN>(b, static_cast<uint8_t*>(ws), fa, fb, stream);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
-template <int S>
+template <int S, int BN>
 cudaError_t make_form(const ZgemmProblem& q, bool as_b, void* dst, OzakiForm* form, cudaStream_t stream) {
-  const Geometry g = geometry(q, q.batch, S);
+  const Geometry g = geometry(q, q.batch, S, BN);
   uint8_t* d = static_cast<uint8_t*>(dst);
   form->slices = d;
   if (!as_b) {
@@ -700,7 +725,7 @@ cudaError_t make_form(const ZgemmProblem& q, bool as_b, void* dst, OzakiForm* fo
     return split_a<S>(q, reinterpret_cast<int8_t*>(d), reinterpret_cast<int*>(d + (g.ea - g.sa)), g, stream);
   }
   form->exps = reinterpret_cast<const int*>(d + (g.fb - g.sb));
-  return split_b<S>(q, reinterpret_cast<int8_t*>(d), reinterpret_cast<int*>(d + (g.fb - g.sb)), g, stream);
+  return split_b<S, BN>(q, reinterpret_cast<int8_t*>(d), reinterpret_cast<int*>(d + (g.fb - g.sb)), g, stream);
 }
 
 ZgemmProblem mm1_problem(const void* A, const void* B, void* C, int64_t Lt, int64_t N) {
@@ -715,32 +740,39 @@ ZgemmProblem mm1_problem(const void* A, const void* B, void* C, int64_t Lt, int6
 
 }  // namespace oz
 
-#define OZ_DISPATCH(fn, ...)                               \
-  switch (slices) {                                        \
-    case 4: return oz::fn<4>(__VA_ARGS__);                 \
-    case 5: return oz::fn<5>(__VA_ARGS__);                 \
-    case 6: return oz::fn<6>(__VA_ARGS__);                 \
-    case 7: return oz::fn<7>(__VA_ARGS__);                 \
-    default: return cudaErrorInvalidValue;                 \
+// slice counts whose S diagonal accumulators fit the 512 TMEM columns at the problem's tile width
+#define OZ_CASE(k, bn, fn, ...) \
+  case k:                       \
+    if constexpr (k * bn <= 512) return oz::fn<k, bn>(__VA_ARGS__); else return cudaErrorInvalidValue;
+#define OZ_SWITCH(bn, fn, ...)                  \
+  switch (slices) {                             \
+    OZ_CASE(4, bn, fn, __VA_ARGS__)             \
+    OZ_CASE(5, bn, fn, __VA_ARGS__)             \
+    OZ_CASE(6, bn, fn, __VA_ARGS__)             \
+    OZ_CASE(7, bn, fn, __VA_ARGS__)             \
+    default: return cudaErrorInvalidValue;      \
   }
+#define OZ_DISPATCH(q, fn, ...)                                   \
+  if (oz::pick_bn(q, slices) == 96) { OZ_SWITCH(96, fn, __VA_ARGS__) }    \
+  else { OZ_SWITCH(64, fn, __VA_ARGS__) }
 
 size_t ozaki_workspace_bytes(const ZgemmProblem& q, int slices, int64_t max_batch) {
-  return oz::geometry(q, std::max<int64_t>(1, std::min(max_batch, q.batch)), slices).total;
+  return oz::geometry(q, std::max<int64_t>(1, std::min(max_batch, q.batch)), slices, oz::pick_bn(q, slices)).total;
 }
 size_t ozaki_mm1_workspace_bytes(int64_t Lt, int64_t N, int slices) {
   return ozaki_workspace_bytes(oz::mm1_problem(nullptr, nullptr, nullptr, Lt, N), slices, Lt);
 }
 size_t ozaki_form_bytes(const ZgemmProblem& q, int slices, bool as_b) {
-  const oz::Geometry g = oz::geometry(q, q.batch, slices);
+  const oz::Geometry g = oz::geometry(q, q.batch, slices, oz::pick_bn(q, slices));
   return as_b ? g.b_form() : g.a_form();
 }
 cudaError_t launch_ozaki_form(const ZgemmProblem& q, int slices, bool as_b, void* dst, OzakiForm* form,
                               cudaStream_t stream) {
-  OZ_DISPATCH(make_form, q, as_b, dst, form, stream)
+  OZ_DISPATCH(q, make_form, q, as_b, dst, form, stream)
 }
 cudaError_t launch_ozaki_gemm(const ZgemmProblem& q, int slices, void* ws, size_t ws_bytes, cudaStream_t stream,
                               const OzakiForm* fa, const OzakiForm* fb) {
-  OZ_DISPATCH(run_gemm, q, ws, ws_bytes, fa, fb, stream)
+  OZ_DISPATCH(q, run_gemm, q, ws, ws_bytes, fa, fb, stream)
 }
 cudaError_t launch_ozaki_mm1(const void* A, const void* B, void* C, int64_t Lt, int64_t N, int slices, void* ws,
                              size_t ws_bytes, cudaStream_t stream, const OzakiForm* fa, const OzakiForm* fb) {
@@ -749,15 +781,17 @@ cudaError_t launch_ozaki_mm1(const void* A, const void* B, void* C, int64_t Lt, 
 
 cudaError_t launch_i8gemm_tn(const int8_t* A, const int8_t* B, int32_t* C, int64_t M, int64_t Nn, int64_t K,
                              cudaStream_t stream) {
-  if (M % oz::BM || Nn % oz::BN || K % oz::BKB) return cudaErrorInvalidValue;
+  // tile width 96 when M % 256 == 0, else 64 (both widths pinned by the bit-exact tests)
+  const int bn = (M % 256 == 0 && Nn % 96 == 0) ? 96 : 64;
+  if (M % oz::BM || Nn % bn || K % oz::BKB) return cudaErrorInvalidValue;
   CUtensorMap ma, mb;
-  if (!oz::map_i8(&ma, A, uint64_t(K), uint64_t(M), oz::BM) || !oz::map_i8(&mb, B, uint64_t(K), uint64_t(Nn), oz::BN))
+  if (!oz::map_i8(&ma, A, uint64_t(K), uint64_t(M), oz::BM) || !oz::map_i8(&mb, B, uint64_t(K), uint64_t(Nn), uint32_t(bn)))
     return cudaErrorInvalidValue;
   oz::Params p{};
   p.Lt = 1; p.Mp = int(M); p.Nc = int(Nn / 2); p.Kp = int(K); p.Brows = int(Nn);
   p.M = int(M); p.Nn = int(Nn); p.nch = 1; p.kchs = int(K / oz::BKB);
   p.Craw = C;
-  return oz::launch_gemm<1, true>(ma, mb, p, stream);
+  return bn == 96 ? oz::launch_gemm<1, true, 96>(ma, mb, p, stream) : oz::launch_gemm<1, true, 64>(ma, mb, p, stream);
 }
 
 }  // namespace cc

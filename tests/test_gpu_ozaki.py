@@ -23,7 +23,7 @@ def ctx():
     return cc.Context(0, torch.empty(64 << 20, dtype=torch.uint8, device="cuda"))
 
 
-@pytest.mark.parametrize("M,Nn,K", [(128, 64, 64), (256, 128, 192), (128, 256, 512), (384, 64, 1024)])
+@pytest.mark.parametrize("M,Nn,K", [(128, 192, 64), (256, 192, 192), (128, 384, 512), (384, 192, 1024)])
 def test_i8gemm_bit_exact(ctx, M, Nn, K):
     g = np.random.default_rng(M * 7 + Nn + K)
     A = g.integers(-127, 128, size=(M, K), dtype=np.int8)

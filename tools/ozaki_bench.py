@@ -44,14 +44,14 @@ def main():
             t = timeit(lambda: ctx.mm1(A, B, C, Lt, N), s, flush)
             row["dmma_us"] = t * 1e6
             row["dmma_tflops"] = fl / t / 1e12
-            for ns in (5, 6):
+            for ns in (5,):
                 ws = torch.empty(cc.cc_mm1_ozaki_workspace_bytes(Lt, N, ns), dtype=torch.uint8, device=dev)
                 t = timeit(lambda: ctx.mm1_ozaki(A, B, C, Lt, N, ns, ws), s, flush)
                 row["ozaki%d_us" % ns] = t * 1e6
                 row["ozaki%d_tflops_equiv" % ns] = fl / t / 1e12
         print(json.dumps(row), flush=True)
         out.append(row)
-    for (M, Nn, K) in ((8192, 8192, 8192), (16384, 8192, 4096)):
+    for (M, Nn, K) in ((8192, 8064, 8192), (16384, 8064, 4096)):
         a = torch.randint(-127, 128, (M, K), dtype=torch.int8, device=dev)
         b = torch.randint(-127, 128, (Nn, K), dtype=torch.int8, device=dev)
         c = torch.empty((M, Nn), dtype=torch.int32, device=dev)
