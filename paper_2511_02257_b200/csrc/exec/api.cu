@@ -1495,9 +1495,49 @@ int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cud
   ck(cudaStreamWaitEvent(ctx->ds, ctx->ev_start, 0), "wait");
   for (int k = 1; k < n_h2d; ++k) ck(cudaStreamWaitEvent(h2d[k], ctx->ev_start, 0), "wait");
   size_t rr = 0;
+  // consecutive TR_MM contractions share one batched trace launch (CC_TR_BATCH=0: one each);
+  // the batch is launched before any other op is issued, and its source events right after
+  static const bool tr_batch = !(getenv("CC_TR_BATCH") && atoi(getenv("CC_TR_BATCH")) == 0);
+  std::vector<const void*> ta, tb;
+  std::vector<void*> tout;
+  std::vector<size_t> tops;
+  auto flush_tr = [&]() {
+    if (tops.empty()) return;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (time_kernels) {
+      ck(cudaEventCreate(&e0), "event");
+      ck(cudaEventCreate(&e1), "event");
+      ck(cudaEventRecord(e0, ctx->cs), "event");
+    }
+    ck(launch_trace_batch(ta.data(), tb.data(), tout.data(), int(tops.size()), g.Lt, g.N, ctx->trace_ws, ctx->cs),
+       "TR_MM batch");
+    ++nl;
+    if (time_kernels) {
+      ck(cudaEventRecord(e1, ctx->cs), "event");
+      kev->push_back({e0, e1});
+      kev_kind->push_back(CC_TR_MM);
+    }
+    for (size_t k : tops)
+      if (ctx->pp.ops[k].source) ck(cudaEventRecord(ctx->events[k], ctx->cs), "event");
+    ta.clear();
+    tb.clear();
+    tout.clear();
+    tops.clear();
+  };
   for (size_t i = 0; i < ctx->pp.ops.size(); ++i) {
     const PhysOp& op = ctx->pp.ops[i];
     if (op.stream == S_NONE) continue;
+    if (tr_batch && op.kind == OP_CONTRACT && g.nodes[size_t(op.node)].op == CC_TR_MM) {
+      const Node& n = g.nodes[size_t(op.node)];
+      for (int32_t d : op.deps) ck(cudaStreamWaitEvent(ctx->cs, ctx->events[size_t(d)], 0), "wait");
+      ta.push_back(op.loc_a == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.l)] : ctx->arena + op.off_a);
+      tb.push_back(op.loc_b == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.r)] : ctx->arena + op.off_b);
+      tout.push_back(ctx->roots + g.tree_of_root[size_t(op.node)] * g.Lt);
+      tops.push_back(i);
+      if (int(tops.size()) == trace_batch_max()) flush_tr();
+      continue;
+    }
+    flush_tr();
     cudaStream_t s = st[op.stream];
     if (op.stream == S_H2D && n_h2d > 1) {
       s = h2d[rr++ % size_t(n_h2d)];
@@ -1548,6 +1588,7 @@ int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cud
     }
     if (op.source) ck(cudaEventRecord(ctx->events[i], s), "event");
   }
+  flush_tr();
   ck(launch_correlate(ctx->roots, ctx->corr, int64_t(g.corr_ids.size()), g.Lt, ctx->term_start, ctx->term_tree,
                       ctx->term_coef, ctx->cs),
      "correlate kernel");

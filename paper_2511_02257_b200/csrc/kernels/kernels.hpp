@@ -36,6 +36,10 @@ cudaError_t launch_zgemm(const ZgemmProblem& p, void* workspace, size_t ws_bytes
 size_t trace_workspace_bytes(int64_t Lt, int64_t N);
 cudaError_t launch_trace(const void* A, const void* B, void* out, int64_t Lt, int64_t N, void* workspace,
                          cudaStream_t stream);
+// n <= trace_batch_max() traces of the same shape in one launch (out[k] = Lt complex128 each).
+int trace_batch_max();
+cudaError_t launch_trace_batch(const void* const* A, const void* const* B, void* const* out, int n, int64_t Lt,
+                               int64_t N, void* workspace, cudaStream_t stream);
 
 // corr[c][t] = sum over the terms of correlator c (in input order) of coef * roots[tree][t].
 // term_start: n_corr+1 offsets into (term_tree, term_coef).

@@ -19,6 +19,7 @@ namespace {
 #define TR_MINB 2
 #endif
 constexpr int TB = 32;          // block edge (complex elements)
+constexpr int TRB = 32;         // traces per batched launch
 constexpr int TR_THREADS = 256; // 8 warps; warp w owns rows w, w+8, w+16, w+24 of a block
 constexpr int RPW = TB / 8;     // rows per warp
 
@@ -45,13 +46,26 @@ __device__ __forceinline__ void load_unit(const double2* __restrict__ At, const 
   }
 }
 
+// Up to TRB traces per launch (blockIdx.z): consecutive TR_MM ops of a plan share one launch,
+// so the ramp-up and tail of a launch are paid once per batch.
+struct TraceBatch {
+  const double2* A[TRB];
+  const double2* B[TRB];
+  double2* out[TRB];
+};
+
 __global__ void __launch_bounds__(TR_THREADS, TR_MINB)
-    trace_kernel(const double2* __restrict__ A, const double2* __restrict__ B, double2* __restrict__ out, int64_t N,
-                 int nb, int P, double2* __restrict__ partials, int* __restrict__ counters) {
+    trace_kernel(const __grid_constant__ TraceBatch tb, int64_t N, int nb, int P, double2* __restrict__ partials,
+                 int* __restrict__ counters) {
   __shared__ double2 sB[TB][TB + 1];
   __shared__ double2 red[TR_THREADS / 32];
   __shared__ int is_last;
-  const int t = blockIdx.y, p = blockIdx.x;
+  const int t = blockIdx.y, p = blockIdx.x, z = blockIdx.z;
+  const double2* __restrict__ A = tb.A[z];
+  const double2* __restrict__ B = tb.B[z];
+  double2* __restrict__ out = tb.out[z];
+  partials += int64_t(z) * gridDim.y * P;
+  counters += int64_t(z) * gridDim.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int U = nb * nb;
   const int u0 = int((int64_t(p) * U) / P), u1 = int((int64_t(p + 1) * U) / P);
@@ -123,9 +137,9 @@ __global__ void __launch_bounds__(TR_THREADS, TR_MINB)
   }
 }
 
-int trace_pieces(int64_t Lt, int64_t N) {
+int trace_pieces(int64_t Lt, int64_t N, int n_traces = 1) {
   const int64_t nb = (N + TB - 1) / TB, U = nb * nb;
-  int64_t P = (TR_MINB * 148) / Lt;   // all CTAs resident at TR_MINB per SM
+  int64_t P = (TR_MINB * 148) / (Lt * n_traces);   // all CTAs resident at TR_MINB per SM
   if (P > U) P = U;
   if (P < 1) P = 1;
   return int(P);
@@ -205,22 +219,36 @@ cudaError_t trace_preload() {
   return e;
 }
 
+// layout: counters (TRB x Lt ints, left at zero by every launch) then the unit partials (the
+// most a batch of n traces needs: n Lt P_n <= TRB Lt P_1)
 size_t trace_workspace_bytes(int64_t Lt, int64_t N) {
-  return size_t(Lt * trace_pieces(Lt, N)) * 16 + ((size_t(Lt) * 4 + 255) / 256) * 256;
+  return size_t(TRB) * size_t(Lt * trace_pieces(Lt, N)) * 16 + ((size_t(TRB) * Lt * 4 + 255) / 256) * 256;
+}
+
+int trace_batch_max() { return TRB; }
+
+cudaError_t launch_trace_batch(const void* const* A, const void* const* B, void* const* out, int n, int64_t Lt,
+                               int64_t N, void* workspace, cudaStream_t stream) {
+  if (Lt <= 0 || N <= 0 || Lt > 65535 || n <= 0 || n > TRB) return cudaErrorInvalidValue;
+  const int nb = int((N + TB - 1) / TB);
+  const int P = trace_pieces(Lt, N, n);
+  int* counters = static_cast<int*>(workspace);
+  double2* partials =
+      reinterpret_cast<double2*>(static_cast<char*>(workspace) + ((size_t(TRB) * Lt * 4 + 255) / 256) * 256);
+  TraceBatch tb{};
+  for (int k = 0; k < n; ++k) {
+    tb.A[k] = static_cast<const double2*>(A[k]);
+    tb.B[k] = static_cast<const double2*>(B[k]);
+    tb.out[k] = static_cast<double2*>(out[k]);
+  }
+  dim3 grid{unsigned(P), unsigned(Lt), unsigned(n)};
+  trace_kernel<<<grid, TR_THREADS, 0, stream>>>(tb, N, nb, P, partials, counters);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_trace(const void* A, const void* B, void* out, int64_t Lt, int64_t N, void* workspace,
                          cudaStream_t stream) {
-  if (Lt <= 0 || N <= 0 || Lt > 65535) return cudaErrorInvalidValue;
-  const int nb = int((N + TB - 1) / TB);
-  const int P = trace_pieces(Lt, N);
-  // layout: counters (Lt ints, left at zero by every launch) then the unit partials
-  int* counters = static_cast<int*>(workspace);
-  double2* partials = reinterpret_cast<double2*>(static_cast<char*>(workspace) + ((size_t(Lt) * 4 + 255) / 256) * 256);
-  dim3 grid{unsigned(P), unsigned(Lt), 1u};
-  trace_kernel<<<grid, TR_THREADS, 0, stream>>>(static_cast<const double2*>(A), static_cast<const double2*>(B),
-                                               static_cast<double2*>(out), N, nb, P, partials, counters);
-  return cudaGetLastError();
+  return launch_trace_batch(&A, &B, &out, 1, Lt, N, workspace, stream);
 }
 
 cudaError_t launch_correlate(const void* roots, void* corr, int64_t n_corr, int64_t Lt, const int32_t* term_start,

@@ -98,8 +98,9 @@ def main():
                 extra = ""
                 if k == 2:
                     extra = ", %.1f TF/s (8 flop/cMAC)" % (8.0 * Lt_p * N ** 3 * cnts[k] / secs[k] / 1e12)
-                if k == 5:
-                    extra = ", %.0f GB/s algorithmic" % (32.0 * Lt_p * N * N * cnts[k] / secs[k] / 1e9)
+                if k == 5:   # batched trace launches: count the TR_MM ops of the plan, not the launches
+                    n_tr = sum(1 for nd in w.nodes if nd[1] == dags.TR_MM)
+                    extra = ", %d traces, %.0f GB/s algorithmic" % (n_tr, 32.0 * Lt_p * N * N * n_tr / secs[k] / 1e9)
                 print("  %s: %d launches, %.1f ms%s" % (nm, cnts[k], secs[k] * 1e3, extra), flush=True)
     # values are checked against the oracle by tests/test_gpu_parity.py (tools do not run it)
     os._exit(0)
