@@ -271,3 +271,20 @@ def test_next_use_c4_full_scale():
     _, lru_st = c.schedule(cc.CC_TREE, cap_bytes=32 * 10 ** 9)
     _, nu_st = c.schedule(cc.CC_TREE, cap_bytes=32 * 10 ** 9, evict_next_use=True)
     assert nu_st["h2d_bytes"] + nu_st["d2h_bytes"] < lru_st["h2d_bytes"] + lru_st["d2h_bytes"]
+
+
+def test_ozaki_workspace_sizes_host_only():
+    """The Ozaki engine's workspace queries are host functions (no GPU): 0 for invalid
+    arguments, the full-batch size grows with Lt and with the slice count, BB2's K chunks add
+    split-K partials, MM1 via the generic query equals the MM1-specific one."""
+    assert cc.cc_mm1_ozaki_workspace_bytes(0, 128, 5) == 0
+    assert cc.cc_mm1_ozaki_workspace_bytes(4, 128, 3) == 0
+    assert cc.cc_gemm_ozaki_workspace_bytes(cc.CC_TR_MM, 4, 128, 1, 5) == 0
+    a = cc.cc_gemm_ozaki_workspace_bytes(cc.CC_MM1, 4, 128, 1, 5)
+    assert a == cc.cc_mm1_ozaki_workspace_bytes(4, 128, 5) > 0
+    assert cc.cc_gemm_ozaki_workspace_bytes(cc.CC_MM1, 8, 128, 1, 5) > a
+    assert cc.cc_gemm_ozaki_workspace_bytes(cc.CC_MM1, 4, 128, 1, 6) > a
+    # BB2 N=16 S=64: K = 16384 complex -> Kp = 32768 bytes -> 2 chunks of 16 KB (partials)
+    one = cc.cc_gemm_ozaki_workspace_bytes(cc.CC_BB2, 1, 16, 64, 5)
+    slices = 5 * 128 * 32768 + 5 * 64 * 32768           # A slices (Mp=128) + B slices (2*32 rows)
+    assert one >= slices + 2 * 128 * 32 * 16            # + 2 chunks of [Mp][Nc] complex partials
