@@ -10,6 +10,8 @@
 // is reduced in a fixed order (shuffle tree, then warps in order) into partials[t][p]; the
 // last CTA of slice t (ticket counter) sums the P partials in order.  No floating-point
 // atomics: the result is bit-identical from run to run.
+#include <algorithm>
+
 #include "kernels.hpp"
 
 namespace cc {
@@ -137,9 +139,24 @@ __global__ void __launch_bounds__(TR_THREADS, TR_MINB)
   }
 }
 
+// Pieces per time slice: from P0 = slots / slices (one wave) upwards, the smallest P whose CTAs
+// fill whole waves to within 5 % while each CTA keeps >= 16 units (else the least wasteful);
+// e.g. 512 slices in 512 CTAs is a 1.7-wave launch that idles a third of its last wave.
 int trace_pieces(int64_t Lt, int64_t N, int n_traces = 1) {
   const int64_t nb = (N + TB - 1) / TB, U = nb * nb;
-  int64_t P = (TR_MINB * 148) / (Lt * n_traces);   // all CTAs resident at TR_MINB per SM
+  const int64_t slots = int64_t(TR_MINB) * 148, X = Lt * n_traces;
+  const int64_t P0 = std::max<int64_t>(1, slots / X);
+  int64_t P = P0;
+  double best_waste = 1e9;
+  for (int64_t q = P0; q <= P0 + 64 && (q == P0 || q * 16 <= U); ++q) {
+    const int64_t ctas = X * q;
+    const double waste = double((ctas + slots - 1) / slots * slots) / double(ctas) - 1.0;
+    if (waste < best_waste - 1e-12) {
+      P = q;
+      best_waste = waste;
+    }
+    if (waste < 0.05) break;
+  }
   if (P > U) P = U;
   if (P < 1) P = 1;
   return int(P);
@@ -220,9 +237,11 @@ cudaError_t trace_preload() {
 }
 
 // layout: counters (TRB x Lt ints, left at zero by every launch) then the unit partials (the
-// most a batch of n traces needs: n Lt P_n <= TRB Lt P_1)
+// most any batch of n <= TRB traces needs, n Lt P_n)
 size_t trace_workspace_bytes(int64_t Lt, int64_t N) {
-  return size_t(TRB) * size_t(Lt * trace_pieces(Lt, N)) * 16 + ((size_t(TRB) * Lt * 4 + 255) / 256) * 256;
+  size_t parts = 0;
+  for (int n = 1; n <= TRB; ++n) parts = std::max(parts, size_t(n) * size_t(Lt * trace_pieces(Lt, N, n)));
+  return parts * 16 + ((size_t(TRB) * Lt * 4 + 255) / 256) * 256;
 }
 
 int trace_batch_max() { return TRB; }
