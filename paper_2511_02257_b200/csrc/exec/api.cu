@@ -652,7 +652,8 @@ void enqueue_copy(cc_ctx* ctx, cudaStream_t s, const void* src, void* dst, size_
 // Wait-free H2D copies alternate between the H2D stream and a second one (CC_H2D_STREAMS=1
 // keeps one): each copy is followed by its flag write, a stream memory operation that idles
 // its stream's copy engine (~8 us measured), so the other stream's copy fills the gap.
-// Off by default: c2 e2e 10.86-10.89 ms with two streams vs 10.87-11.36 ms with one (noise).
+// Off by default: 4 alternating c2 runs each: copies land 80 us earlier with two streams but
+// e2e is 10.82-10.84 ms vs 10.74-10.75 ms with one (the leaves arrive in a less useful order).
 bool dual_h2d() {
   static const int n = getenv("CC_H2D_STREAMS") ? atoi(getenv("CC_H2D_STREAMS")) : 1;
   return n >= 2;
