@@ -187,7 +187,11 @@ cc_status cc_set_leaf_device(cc_ctx* ctx, int64_t leaf_id, const void* dev, size
  * executor is the dataflow one (persistent DMMA-tile and trace workers, kernels/dataflow.hpp);
  * bit 4 selects op-by-op launches instead; bit 5 records the per-item timeline
  * (cc_dataflow_profile); bit 6 runs every MM1 / BM1 / BB2 on the tcgen05 INT8 Ozaki engine
- * (cc_gemm_ozaki, 5 slices; leaves split once per execute; implies op-by-op launches). */
+ * (cc_gemm_ozaki, 5 slices; leaves split once per execute; implies op-by-op launches); bit 7
+ * (CC_EXEC_AUTO) chooses bit 6 or the dataflow worker by the measured rule of DESIGN §7 (the
+ * Ozaki engine for GEMMs with N >= 256, or baryon GEMMs with N >= 128). */
+#define CC_EXEC_OZAKI 64
+#define CC_EXEC_AUTO 128
 cc_status cc_execute(cc_ctx* ctx, int32_t flags, cc_exec_stats* stats);
 /* Enqueue-only variant (no host sync): work is ordered on the compute stream. */
 cc_status cc_execute_async(cc_ctx* ctx, int32_t flags);

@@ -26,6 +26,7 @@ PART_TIME, PART_TREES = 0, 1
 EXEC_GRAPH, EXEC_TIME_KERNELS, EXEC_ONLY_GEMM, EXEC_ONLY_TRACE, EXEC_OP_BY_OP, EXEC_PROFILE = 1, 2, 4, 8, 16, 32
 EXEC_OZAKI_MM1 = 64        # MM1 / BM1 / BB2 on the tcgen05 Ozaki engine (name kept from MM1-only)
 EXEC_OZAKI = 64
+EXEC_AUTO = 128             # Ozaki engine or dataflow worker by the measured rule
 CC_EVICT_NEXT_USE = 1       # cc_sched_cfg.flags: next-use (Belady) eviction, reading E-9
 STATUS = {0: "OK", -1: "INVAL", -2: "PARSE", -3: "CYCLE", -4: "INCONSISTENT", -5: "MULTIROOT",
           -6: "UNKNOWN_NODE", -7: "NOT_CLOSED", -8: "INFEASIBLE", -9: "STATE", -10: "BUFFER_TOO_SMALL",

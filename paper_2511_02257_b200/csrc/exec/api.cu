@@ -1672,6 +1672,18 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   if (!ctx->scheduled) throw Error(CC_E_STATE, "cc_execute before cc_schedule");
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
   prepare_phys(ctx);
+  if (flags & 128) {
+    // CC_EXEC_AUTO: the Ozaki engine (bit 6) where it measured faster than the dataflow worker
+    // (DESIGN §7): GEMMs with N >= 256, or baryon GEMMs with N >= 128
+    const Dag& gd = *ctx->dag;
+    bool gemm = false, baryon = false;
+    for (const auto& n : gd.nodes) {
+      gemm |= n.op == CC_MM1 || n.op == CC_BM1 || n.op == CC_BB2;
+      baryon |= n.op == CC_BM1 || n.op == CC_BB2;
+    }
+    if (gemm && (gd.N >= 256 || (baryon && gd.N >= 128))) flags |= 64;
+    flags &= ~128;
+  }
   ctx->mm1_ozaki = (flags & 64) != 0;
   if (ctx->mm1_ozaki) oz_cache_reset(ctx);
   if (flags & 12) {
