@@ -510,8 +510,10 @@ void prepare_phys(cc_ctx* ctx) {
   // writer of a byte range rarely has to wait for its last reader — the dataflow executor
   // overlaps more).  With a capacity cap the physical pool is held to 1.25 x cap so the
   // physical footprint follows the logical one; the logical plan is unchanged either way.
+  // (CC_PHYS_SLACK: the slack fraction over the cap, default 0.25)
   int64_t phys_limit = pool;
-  if (ctx->cap > 0) phys_limit = std::min(pool, round_up(ctx->cap + ctx->cap / 4, ALIGN));
+  static const double slack = getenv("CC_PHYS_SLACK") ? atof(getenv("CC_PHYS_SLACK")) : 0.25;
+  if (ctx->cap > 0) phys_limit = std::min(pool, round_up(ctx->cap + int64_t(double(ctx->cap) * slack), ALIGN));
   try {
     ctx->pp = build_phys(g, ctx->lp, on_dev, phys_limit, ALIGN, RangeAlloc::NEXT_FIT);
   } catch (const Error& e) {
