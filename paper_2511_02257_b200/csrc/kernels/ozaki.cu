@@ -1,4 +1,4 @@
-// MM1 on the 5th-generation tensor cores: complex-double C = A B per time slice by Ozaki
+// MM1 / BM1 / BB2 on the 5th-generation tensor cores: complex-double C = A B per time slice by Ozaki
 // splitting into INT8 slices, tcgen05.mma kind::i8 with INT32 accumulators in TMEM, and an
 // FP64 epilogue (reading V-6 in DESIGN.md).
 //
@@ -26,9 +26,12 @@
 //            64g + w, w < 32 -> Cr column 32g + w, w >= 32 -> Ci column), same tiling with
 //            64-row blocks
 //   eA int32 [Lt][Mp], fB int32 [Lt][Nc]
-// GEMM CTA (persistent): tiles of 128 rows x (32 complex output columns = 64 B_cat^T rows);
-// a stage = all s slices of A and B for one 64-byte k chunk = two contiguous bulk copies;
-// one lane issues the tcgen05.mma's, 4 warps drain TMEM.
+// GEMM CTA (persistent): tiles of 128 rows x BN B_cat^T rows (BN = 64, or 96 for outputs >= 512
+// columns: BN/2 complex output columns); a stage = all s slices of A and B for one 64-byte k
+// chunk = contiguous bulk copies; one lane issues the tcgen05.mma's, 4 or 8 warps drain TMEM.
+// BM1 / BB2 use the same kernels on their (two-level K) operand layouts; K is cut into chunks
+// of 8192 complex terms (INT32 bound) whose FP64 partials are summed in order.  An opt-in
+// CTA-pair variant (cta_group::2, CC_OZ_PAIR=1) runs M = 256 per instruction.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
