@@ -19,12 +19,12 @@
 // each exactly to FP64 and sums them, most significant first.
 //
 // Layouts (device workspace, caller-owned):
-//   SA int8: K-major rows of A_cat (Mp = roundup(N,128) rows, Kp = 2 Nc bytes, Nc =
-//            roundup(N,32); K index: Re part at j, Im part at Nc + j), stored tile-contiguous
+//   SA int8: K-major rows of A_cat (Mp = roundup(M,128) rows, Kp = 2 Kc bytes, Kc =
+//            roundup(K,32); K index: Re part at k, Im part at Kc + k), stored tile-contiguous
 //            and pre-swizzled as [t][row block of 128][64-byte k chunk][slice][128][64]
-//   SB int8: K-major rows of B_cat^T (2 Nc rows; rows grouped per 32 output columns: row
-//            64g + w, w < 32 -> Cr column 32g + w, w >= 32 -> Ci column), same tiling with
-//            64-row blocks
+//   SB int8: K-major rows of B_cat^T (2 Nc rows, Nc = roundup(Nn, BN/2); rows grouped per BN/2
+//            output columns: row BN g + w, w < BN/2 -> Cr column (BN/2) g + w, else Ci), same
+//            tiling with BN-row blocks
 //   eA int32 [Lt][Mp], fB int32 [Lt][Nc]
 // GEMM CTA (persistent): tiles of 128 rows x BN B_cat^T rows (BN = 64, or 96 for outputs >= 512
 // columns: BN/2 complex output columns); a stage = all s slices of A and B for one 64-byte k
