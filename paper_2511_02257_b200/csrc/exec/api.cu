@@ -720,6 +720,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   // last leaf lands.  CC_COPY_REORDER=0 keeps plan order.
   std::vector<int32_t> early_seq;
   std::vector<uint8_t> is_early(size_t(n_ops), 0);
+  int32_t first_issued = -1;                           // early copy already enqueued
   {
     int64_t touched_end = 0;
     auto touch = [&](int64_t off, int64_t bytes) {
@@ -741,6 +742,18 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       }
     }
     const int reorder = getenv("CC_COPY_REORDER") ? atoi(getenv("CC_COPY_REORDER")) : 1;
+    // the plan's first leaf copy starts now, before the ordering of the others is computed
+    // (it heads the order either way), so the copy engine starts ~0.2 ms earlier
+    if (early && !early_seq.empty()) {
+      ck(cudaEventRecord(ctx->ev_pre, ctx->cs), "event");        // after all earlier work on cs
+      ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_pre, 0), "wait");
+      ck(cudaMemsetAsync(ctx->df_sync_base, 0, sz_sync, ctx->hs), "memset");
+      const int32_t i = early_seq[0];
+      const auto ep = copy_endpoints(ctx, ops[size_t(i)]);
+      enqueue_copy(ctx, ctx->hs, ep.first, ep.second, size_t(ops[size_t(i)].bytes), cudaMemcpyHostToDevice,
+                   target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
+      first_issued = i;
+    }
     if (reorder && early_seq.size() > 1) {
       // leaf closure of every contraction (memoised over nodes), restricted to early leaves
       std::vector<int32_t> early_of_node(g.nodes.size(), -1);
@@ -785,8 +798,12 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       std::vector<int32_t> out;
       for (size_t step = 0; step < ne; ++step) {
         size_t best = ne;
-        for (size_t e = 0; e < ne; ++e)
-          if (!taken[e] && (best == ne || score[e] > score[best])) best = e;
+        if (step == 0 && first_issued >= 0) {
+          best = 0;                                   // early_seq[0], already on its way
+        } else {
+          for (size_t e = 0; e < ne; ++e)
+            if (!taken[e] && (best == ne || score[e] > score[best])) best = e;
+        }
         taken[best] = 1;
         out.push_back(early_seq[best]);
         for (int32_t c : users[best]) {
@@ -816,10 +833,12 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   ctx->df_early.assign(size_t(n_ops), 0);
   ctx->df_early_active = false;
   if (early && !early_seq.empty()) {
-    ck(cudaEventRecord(ctx->ev_pre, ctx->cs), "event");        // after all earlier work on cs
-    ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_pre, 0), "wait");
-    ck(cudaMemsetAsync(ctx->df_sync_base, 0, sz_sync, ctx->hs), "memset");
-    ck(cudaEventRecord(ctx->ev_pre, ctx->hs), "event");
+    if (first_issued < 0) {
+      ck(cudaEventRecord(ctx->ev_pre, ctx->cs), "event");        // after all earlier work on cs
+      ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_pre, 0), "wait");
+      ck(cudaMemsetAsync(ctx->df_sync_base, 0, sz_sync, ctx->hs), "memset");
+    }
+    ck(cudaEventRecord(ctx->ev_pre, ctx->hs), "event");          // after the zeroing (and copy 0)
     ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_pre, 0), "wait");
     const bool dual = dual_h2d();
     if (dual) {
@@ -829,10 +848,11 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
     size_t q = 0;
     for (int32_t i : early_seq) {
       const PhysOp& op = ops[size_t(i)];
+      ctx->df_early[size_t(i)] = 1;
+      if (i == first_issued) continue;
       const auto ep = copy_endpoints(ctx, op);
       enqueue_copy(ctx, (dual && (q++ & 1)) ? ctx->hs2 : ctx->hs, ep.first, ep.second, size_t(op.bytes),
                    cudaMemcpyHostToDevice, target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
-      ctx->df_early[size_t(i)] = 1;
     }
     if (dual) {                                   // rejoin: later hs work follows every early copy
       ck(cudaEventRecord(ctx->ev_hs2, ctx->hs2), "event");
