@@ -72,6 +72,8 @@ struct KindTimes {
 struct cc_ctx {
   int device = -1;
   bool mm1_ozaki = false;     // execute flags bit 6: MM1/BM1/BB2 on the tcgen05 Ozaki engine (op-by-op)
+  bool pre_copied = false;    // the plan's first leaf copy was started before the physical plan
+  cudaEvent_t ev_precopy = nullptr;
   // Ozaki leaf-form cache: INT8 slices of leaves, split once per execute and shared by every
   // MM1 reading that leaf in the same role, placed in the pool above the plan's high water
   struct {
@@ -231,7 +233,8 @@ struct cc_ctx {
   void release_device() {
     if (host_only) return;
     release_phys();
-    for (cudaEvent_t* e : {&ev_start, &ev_end, &ev_h_end, &ev_d_end, &ev_copy_h, &ev_copy_d, &ev_pre, &ev_meta})
+    for (cudaEvent_t* e : {&ev_start, &ev_end, &ev_h_end, &ev_d_end, &ev_copy_h, &ev_copy_d, &ev_pre, &ev_meta,
+                           &ev_precopy})
       if (*e) {
         cudaEventDestroy(*e);
         *e = nullptr;
@@ -749,11 +752,21 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_pre, 0), "wait");
       ck(cudaMemsetAsync(ctx->df_sync_base, 0, sz_sync, ctx->hs), "memset");
       const int32_t i = early_seq[0];
-      const auto ep = copy_endpoints(ctx, ops[size_t(i)]);
-      enqueue_copy(ctx, ctx->hs, ep.first, ep.second, size_t(ops[size_t(i)].bytes), cudaMemcpyHostToDevice,
-                   target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
+      if (ctx->pre_copied && i == 0 && target[0] == 1) {
+        // copied during execute() before the plan was built (hs order: copy, memset, flag)
+        if (df_write_fn()(ctx->hs, reinterpret_cast<CUdeviceptr>(ctx->df_sync + slot[0]), 1u, 0) != CUDA_SUCCESS)
+          throw Error(CC_E_CUDA, "cuStreamWriteValue32 failed");
+      } else {
+        if (ctx->pre_copied) ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_precopy, 0), "wait");
+        const auto ep = copy_endpoints(ctx, ops[size_t(i)]);
+        enqueue_copy(ctx, ctx->hs, ep.first, ep.second, size_t(ops[size_t(i)].bytes), cudaMemcpyHostToDevice,
+                     target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
+      }
       first_issued = i;
+    } else if (ctx->pre_copied) {
+      ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_precopy, 0), "wait");
     }
+    ctx->pre_copied = false;
     if (reorder && early_seq.size() > 1) {
       // leaf closure of every contraction (memoised over nodes), restricted to early leaves
       std::vector<int32_t> early_of_node(g.nodes.size(), -1);
@@ -1693,7 +1706,40 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   ctx->need_device();
   if (!ctx->scheduled) throw Error(CC_E_STATE, "cc_execute before cc_schedule");
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaEvent_t t_begin, t_end;
+  ck(cudaEventCreate(&t_begin), "event");
+  ck(cudaEventCreate(&t_end), "event");
+  ck(cudaEventRecord(t_begin, ctx->cs), "event");   // before any preparation: seconds = time to solution
+  // A plan that is about to be (re)built starts with a host leaf's H2D into an empty pool:
+  // next-fit places it at offset 0, so its copy can start before the physical plan exists
+  // (prepare_dataflow checks the placement and adds the flag write; dataflow executor only).
+  ctx->pre_copied = false;
+  if (!(getenv("CC_PRECOPY") && atoi(getenv("CC_PRECOPY")) == 0) && !ctx->phys_valid &&
+      !(flags & (2 | 4 | 8 | 16 | 64 | 128)) && !getenv("CC_H2D_CHUNK_MB") &&
+      !getenv("CC_H2D_TAIL") && !(getenv("CC_EARLY_COPIES") && atoi(getenv("CC_EARLY_COPIES")) == 0) &&
+      !ctx->lp.ops.empty() && ctx->lp.ops[0].kind == OP_H2D) {
+    const Dag& g0 = *ctx->dag;
+    const int32_t u = ctx->lp.ops[0].node;
+    const Node& n0 = g0.nodes[size_t(u)];
+    if (n0.leaf() && !ctx->leaf_dev[size_t(u)] && ctx->leaf_host[size_t(u)]) {
+      if (!ctx->ev_precopy) ck(cudaEventCreateWithFlags(&ctx->ev_precopy, cudaEventDisableTiming), "event");
+      const int64_t per_t_m = 16LL * g0.N * g0.N;
+      const int64_t per_t = n0.op == CC_LEAF_M ? per_t_m : per_t_m * g0.S * g0.N;
+      const char* src = static_cast<const char*>(ctx->leaf_host[size_t(u)]) + int64_t(ctx->t0) * per_t;
+      ck(cudaEventRecord(ctx->ev_precopy, ctx->cs), "event");   // after all earlier work on cs
+      ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_precopy, 0), "wait");
+      ck(cudaMemcpyAsync(ctx->arena, src, size_t(n0.size), cudaMemcpyHostToDevice, ctx->hs), "H2D");
+      ck(cudaEventRecord(ctx->ev_precopy, ctx->hs), "event");
+      ctx->pre_copied = true;
+    }
+  }
   prepare_phys(ctx);
+  if (ctx->pre_copied && (ctx->pp.ops.empty() || ctx->pp.ops[0].kind != OP_H2D || ctx->pp.ops[0].dev_off != 0)) {
+    // placement differs: the early path copies the leaf again; nothing may touch [0, size)
+    // on the compute stream before the stray copy is done
+    ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_precopy, 0), "wait");
+    ctx->pre_copied = false;
+  }
   if (flags & 128) {
     // CC_EXEC_AUTO: the Ozaki engine (bit 6) where it measured faster than the dataflow worker
     // (DESIGN §7): GEMMs with N >= 256, or baryon GEMMs with N >= 128
@@ -1717,10 +1763,6 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   const bool time_kernels = (flags & 2) != 0 && !use_graph;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;
   std::vector<int> kev_kind;
-  cudaEvent_t t_begin, t_end;
-  ck(cudaEventCreate(&t_begin), "event");
-  ck(cudaEventCreate(&t_end), "event");
-  ck(cudaEventRecord(t_begin, ctx->cs), "event");   // before any preparation: seconds = time to solution
   if (!legacy) {
     prepare_dataflow(ctx, getenv("CC_EARLY_COPIES") ? atoi(getenv("CC_EARLY_COPIES")) != 0 : true);
     const bool prof = (flags & 32) != 0;
