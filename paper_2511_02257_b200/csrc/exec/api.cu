@@ -72,7 +72,7 @@ struct KindTimes {
 struct cc_ctx {
   int device = -1;
   bool mm1_ozaki = false;     // execute flags bit 6: MM1/BM1/BB2 on the tcgen05 Ozaki engine (op-by-op)
-  bool pre_copied = false;    // the plan's first leaf copy was started before the physical plan
+  int pre_n = 0;              // the plan's first pre_n leaf copies were started before the physical plan
   cudaEvent_t ev_precopy = nullptr;
   // Ozaki leaf-form cache: INT8 slices of leaves, split once per execute and shared by every
   // MM1 reading that leaf in the same role, placed in the pool above the plan's high water
@@ -723,7 +723,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   // last leaf lands.  CC_COPY_REORDER=0 keeps plan order.
   std::vector<int32_t> early_seq;
   std::vector<uint8_t> is_early(size_t(n_ops), 0);
-  int32_t first_issued = -1;                           // early copy already enqueued
+  int32_t n_first = 0;                                 // early copies already enqueued (plan ops 0..n-1)
   {
     int64_t touched_end = 0;
     auto touch = [&](int64_t off, int64_t bytes) {
@@ -745,28 +745,34 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       }
     }
     const int reorder = getenv("CC_COPY_REORDER") ? atoi(getenv("CC_COPY_REORDER")) : 1;
-    // the plan's first leaf copy starts now, before the ordering of the others is computed
-    // (it heads the order either way), so the copy engine starts ~0.2 ms earlier
+    // the plan's first leaf copies start now, before the ordering of the others is computed
+    // (they head the order either way); the first pre_n of them were even started by
+    // execute() before the physical plan existed, and only get their flag writes here
     if (early && !early_seq.empty()) {
       ck(cudaEventRecord(ctx->ev_pre, ctx->cs), "event");        // after all earlier work on cs
       ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_pre, 0), "wait");
       ck(cudaMemsetAsync(ctx->df_sync_base, 0, sz_sync, ctx->hs), "memset");
-      const int32_t i = early_seq[0];
-      if (ctx->pre_copied && i == 0 && target[0] == 1) {
-        // copied during execute() before the plan was built (hs order: copy, memset, flag)
-        if (df_write_fn()(ctx->hs, reinterpret_cast<CUdeviceptr>(ctx->df_sync + slot[0]), 1u, 0) != CUDA_SUCCESS)
+      int pre = ctx->pre_n;
+      for (int j = 0; j < pre; ++j)
+        if (size_t(j) >= early_seq.size() || early_seq[size_t(j)] != j || target[size_t(j)] != 1) pre = 0;
+      if (pre == 0 && ctx->pre_n > 0) ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_precopy, 0), "wait");
+      for (int j = 0; j < pre; ++j)   // hs order: copies, memset, flags
+        if (df_write_fn()(ctx->hs, reinterpret_cast<CUdeviceptr>(ctx->df_sync + slot[size_t(j)]), 1u, 0) != CUDA_SUCCESS)
           throw Error(CC_E_CUDA, "cuStreamWriteValue32 failed");
-      } else {
-        if (ctx->pre_copied) ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_precopy, 0), "wait");
+      if (pre == 0) {
+        const int32_t i = early_seq[0];
         const auto ep = copy_endpoints(ctx, ops[size_t(i)]);
         enqueue_copy(ctx, ctx->hs, ep.first, ep.second, size_t(ops[size_t(i)].bytes), cudaMemcpyHostToDevice,
                      target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
+        n_first = 1;
+        if (i != early_seq[0]) n_first = 0;
+      } else {
+        n_first = pre;
       }
-      first_issued = i;
-    } else if (ctx->pre_copied) {
+    } else if (ctx->pre_n > 0) {
       ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_precopy, 0), "wait");
     }
-    ctx->pre_copied = false;
+    ctx->pre_n = 0;
     if (reorder && early_seq.size() > 1) {
       // leaf closure of every contraction (memoised over nodes), restricted to early leaves
       std::vector<int32_t> early_of_node(g.nodes.size(), -1);
@@ -811,8 +817,8 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       std::vector<int32_t> out;
       for (size_t step = 0; step < ne; ++step) {
         size_t best = ne;
-        if (step == 0 && first_issued >= 0) {
-          best = 0;                                   // early_seq[0], already on its way
+        if (step < size_t(n_first)) {
+          best = step;                                // early_seq[step], already on its way
         } else {
           for (size_t e = 0; e < ne; ++e)
             if (!taken[e] && (best == ne || score[e] > score[best])) best = e;
@@ -846,7 +852,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   ctx->df_early.assign(size_t(n_ops), 0);
   ctx->df_early_active = false;
   if (early && !early_seq.empty()) {
-    if (first_issued < 0) {
+    if (n_first == 0) {
       ck(cudaEventRecord(ctx->ev_pre, ctx->cs), "event");        // after all earlier work on cs
       ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_pre, 0), "wait");
       ck(cudaMemsetAsync(ctx->df_sync_base, 0, sz_sync, ctx->hs), "memset");
@@ -858,11 +864,11 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       ensure_hs2(ctx);
       ck(cudaStreamWaitEvent(ctx->hs2, ctx->ev_pre, 0), "wait");
     }
-    size_t q = 0;
+    size_t q = 0, q_issued = 0;
     for (int32_t i : early_seq) {
       const PhysOp& op = ops[size_t(i)];
       ctx->df_early[size_t(i)] = 1;
-      if (i == first_issued) continue;
+      if (q_issued++ < size_t(n_first)) continue;     // enqueued before the ordering
       const auto ep = copy_endpoints(ctx, op);
       enqueue_copy(ctx, (dual && (q++ & 1)) ? ctx->hs2 : ctx->hs, ep.first, ep.second, size_t(op.bytes),
                    cudaMemcpyHostToDevice, target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
@@ -1710,35 +1716,52 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   ck(cudaEventCreate(&t_begin), "event");
   ck(cudaEventCreate(&t_end), "event");
   ck(cudaEventRecord(t_begin, ctx->cs), "event");   // before any preparation: seconds = time to solution
-  // A plan that is about to be (re)built starts with a host leaf's H2D into an empty pool:
-  // next-fit places it at offset 0, so its copy can start before the physical plan exists
-  // (prepare_dataflow checks the placement and adds the flag write; dataflow executor only).
-  ctx->pre_copied = false;
+  // A plan that is about to be (re)built starts with host-leaf H2Ds into an empty pool: next-fit
+  // places them back to back from offset 0, so up to 4 of those copies start before the
+  // physical plan exists (prepare_dataflow checks the placement and adds the flag writes;
+  // dataflow executor only; CC_PRECOPY=0 disables).
+  ctx->pre_n = 0;
+  std::vector<int64_t> pre_off;
   if (!(getenv("CC_PRECOPY") && atoi(getenv("CC_PRECOPY")) == 0) && !ctx->phys_valid &&
       !(flags & (2 | 4 | 8 | 16 | 64 | 128)) && !getenv("CC_H2D_CHUNK_MB") &&
-      !getenv("CC_H2D_TAIL") && !(getenv("CC_EARLY_COPIES") && atoi(getenv("CC_EARLY_COPIES")) == 0) &&
-      !ctx->lp.ops.empty() && ctx->lp.ops[0].kind == OP_H2D) {
+      !getenv("CC_H2D_TAIL") && !(getenv("CC_EARLY_COPIES") && atoi(getenv("CC_EARLY_COPIES")) == 0)) {
     const Dag& g0 = *ctx->dag;
-    const int32_t u = ctx->lp.ops[0].node;
-    const Node& n0 = g0.nodes[size_t(u)];
-    if (n0.leaf() && !ctx->leaf_dev[size_t(u)] && ctx->leaf_host[size_t(u)]) {
+    int64_t off = 0;
+    for (size_t j = 0; j < ctx->lp.ops.size() && j < 4; ++j) {
+      const auto& lop = ctx->lp.ops[j];
+      if (lop.kind != OP_H2D) break;
+      const int32_t u = lop.node;
+      const Node& n0 = g0.nodes[size_t(u)];
+      if (!n0.leaf() || ctx->leaf_dev[size_t(u)] || !ctx->leaf_host[size_t(u)]) break;
       if (!ctx->ev_precopy) ck(cudaEventCreateWithFlags(&ctx->ev_precopy, cudaEventDisableTiming), "event");
+      if (j == 0) {
+        ck(cudaEventRecord(ctx->ev_precopy, ctx->cs), "event");   // after all earlier work on cs
+        ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_precopy, 0), "wait");
+      }
       const int64_t per_t_m = 16LL * g0.N * g0.N;
       const int64_t per_t = n0.op == CC_LEAF_M ? per_t_m : per_t_m * g0.S * g0.N;
       const char* src = static_cast<const char*>(ctx->leaf_host[size_t(u)]) + int64_t(ctx->t0) * per_t;
-      ck(cudaEventRecord(ctx->ev_precopy, ctx->cs), "event");   // after all earlier work on cs
-      ck(cudaStreamWaitEvent(ctx->hs, ctx->ev_precopy, 0), "wait");
-      ck(cudaMemcpyAsync(ctx->arena, src, size_t(n0.size), cudaMemcpyHostToDevice, ctx->hs), "H2D");
+      ck(cudaMemcpyAsync(ctx->arena + off, src, size_t(n0.size), cudaMemcpyHostToDevice, ctx->hs), "H2D");
+      pre_off.push_back(off);
+      off += round_up(n0.size, ALIGN);
+    }
+    if (!pre_off.empty()) {
       ck(cudaEventRecord(ctx->ev_precopy, ctx->hs), "event");
-      ctx->pre_copied = true;
+      ctx->pre_n = int(pre_off.size());
     }
   }
   prepare_phys(ctx);
-  if (ctx->pre_copied && (ctx->pp.ops.empty() || ctx->pp.ops[0].kind != OP_H2D || ctx->pp.ops[0].dev_off != 0)) {
-    // placement differs: the early path copies the leaf again; nothing may touch [0, size)
-    // on the compute stream before the stray copy is done
-    ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_precopy, 0), "wait");
-    ctx->pre_copied = false;
+  for (int j = 0; j < ctx->pre_n; ++j) {
+    const bool ok = size_t(j) < ctx->pp.ops.size() && ctx->pp.ops[size_t(j)].kind == OP_H2D &&
+                    ctx->pp.ops[size_t(j)].dev_off == pre_off[size_t(j)] &&
+                    ctx->pp.ops[size_t(j)].node == ctx->lp.ops[size_t(j)].node;
+    if (!ok) {
+      // placement differs: the early path copies those leaves again; nothing may touch the
+      // pre-copied ranges on the compute stream before the stray copies are done
+      ck(cudaStreamWaitEvent(ctx->cs, ctx->ev_precopy, 0), "wait");
+      ctx->pre_n = 0;
+      break;
+    }
   }
   if (flags & 128) {
     // CC_EXEC_AUTO: the Ozaki engine (bit 6) where it measured faster than the dataflow worker
