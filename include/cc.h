@@ -147,7 +147,9 @@ cc_status cc_dag_info(cc_ctx* ctx, cc_dag_stats* out);
  * mode 0 TIME: time slices [part*Lt/n, (part+1)*Lt/n) of every tensor (no replication);
  * mode 1 TREES: a contiguous, flop-balanced chunk of the trees in tree-scheduler
  *   selection order, with the sub-DAG they need (shared nodes replicated).
- * Call after cc_load_dag, before cc_schedule.  n_parts == 1 restores the full DAG. */
+ * Call after cc_load_dag, before cc_schedule.  n_parts == 1 restores the full DAG.  Errors:
+ * CC_E_INVAL for part outside [0, n_parts), an unknown mode, or a TIME part that owns no time
+ * slice (n_parts > Lt), CC_E_STATE before cc_load_dag. */
 cc_status cc_partition(cc_ctx* ctx, int32_t n_parts, int32_t part, int32_t mode);
 /* Trees of the current part (ids, ascending); n_out receives the count. */
 cc_status cc_part_trees(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out);
