@@ -686,6 +686,10 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   // sync slots (done counters of compute ops, flags of copies) and H2D chunk counts
   std::vector<int32_t> slot(size_t(n_ops), -1), target(size_t(n_ops), 0), df_index(size_t(n_ops), -1);
   int32_t n_sync = 0;
+  // per-time-slice done counters of GEMMs with meson outputs [Lt, N, N] (MM1, BB2): a trace of
+  // slice t waits only for that slice's tiles (CC_SLICE_DEPS=0: for the whole GEMM)
+  std::vector<int32_t> slice_slot(size_t(n_ops), -1), items_per_slice(size_t(n_ops), 0);
+  static const bool slice_deps = !(getenv("CC_SLICE_DEPS") && atoi(getenv("CC_SLICE_DEPS")) == 0);
   // CC_H2D_CHUNK_MB: H2D copies in time-slice chunks of about that size (default off: every
   // chunk costs a stream memory operation, measured ~8 us of copy-engine idle each on B200)
   const double chunk_mb = getenv("CC_H2D_CHUNK_MB") ? atof(getenv("CC_H2D_CHUNK_MB")) : 0.0;
@@ -694,6 +698,11 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
     const PhysOp& op = ops[size_t(i)];
     if (op.stream == S_NONE) continue;
     slot[size_t(i)] = n_sync++;
+    if (slice_deps && op.kind == OP_CONTRACT && Lt > 1 &&
+        (g.nodes[size_t(op.node)].op == CC_MM1 || g.nodes[size_t(op.node)].op == CC_BB2)) {
+      slice_slot[size_t(i)] = n_sync;
+      n_sync += int32_t(Lt);
+    }
     if (op.kind != OP_CONTRACT) {
       // consumers of a copy in C > 1 time-slice chunks wait only for the chunk holding their
       // slice (target -C); else the flag reaches 1
@@ -988,6 +997,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
     if (fuse_host[size_t(i)] >= 0) continue;   // fused TR: computed by its host GEMM's tiles
     DfOp d{};
     d.sync_id = slot[size_t(i)];
+    d.slice_sync = -1;
     if (n.op == CC_TR_MM) {
       const int64_t P = df_trace_pieces(Lt, N);
       d.kind = 1;
@@ -1016,6 +1026,10 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       df_gemm_geometry(p, tiles, KT, chunks, ctx->num_sms);
       d.kind = 0;
       d.n_items = int32_t(tiles * chunks);
+      if (slice_slot[size_t(i)] >= 0 && p.batch == Lt && d.n_items % Lt == 0) {
+        d.slice_sync = slice_slot[size_t(i)];
+        items_per_slice[size_t(i)] = int32_t(d.n_items / Lt);
+      }
       d.first_item = g_items;
       d.tiles_m = int32_t((p.M + BM - 1) / BM);
       d.tiles_n = int32_t((p.Nn + BN - 1) / BN);
@@ -1172,7 +1186,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
   tmr.lap("queue order");
   // 4. dependency lists of compute ops, wait lists of copies
   std::vector<int32_t> dep_slot, dep_target;
-  auto fill_deps = [&](std::vector<DfOp>& v, const std::vector<int32_t>& plan) {
+  auto fill_deps = [&](std::vector<DfOp>& v, const std::vector<int32_t>& plan, bool traces) {
     for (size_t k = 0; k < v.size(); ++k) {
       const int32_t i = plan[k];
       v[k].dep_begin = int32_t(dep_slot.size());
@@ -1182,14 +1196,19 @@ void prepare_dataflow(cc_ctx* ctx, bool early = false) {
       all.erase(std::unique(all.begin(), all.end()), all.end());
       for (int32_t j : all) {
         if (slot[size_t(j)] < 0) continue;
+        if (traces && items_per_slice[size_t(j)] > 0) {   // a trace reads slice t of this GEMM's output
+          dep_slot.push_back(slice_slot[size_t(j)]);
+          dep_target.push_back(-(1 << 20) - items_per_slice[size_t(j)]);
+          continue;
+        }
         dep_slot.push_back(slot[size_t(j)]);
         dep_target.push_back(target[size_t(j)]);
       }
       v[k].dep_count = int32_t(dep_slot.size()) - v[k].dep_begin;
     }
   };
-  fill_deps(gops, gplan);
-  fill_deps(tops, tplan);
+  fill_deps(gops, gplan, false);
+  fill_deps(tops, tplan, true);
   ctx->df_copies.clear();
   std::vector<int32_t> copy_index(static_cast<size_t>(n_ops), -1);
   for (int32_t i = 0; i < n_ops; ++i) {

@@ -154,15 +154,21 @@ __device__ __forceinline__ void decode_item(const DfQueue& q, int64_t item, Item
 }
 
 // Non-blocking dependency poll of an item working on time slice `slice`: advances *dep past
-// satisfied dependencies.  A chunked copy (target -C) is needed only up to the chunk holding
+// satisfied dependencies.  A per-slice GEMM counter (target <= -2^20) is read at slot + slice.  A chunked copy (target -C) is needed only up to the chunk holding
 // the slice: chunk k covers slices [k*Lt/C, (k+1)*Lt/C), so slice s is in chunk
 // floor(((s+1)*C - 1) / Lt).
 __device__ __forceinline__ bool deps_ready(const DfArgs& a, const DfOp& op, int slice, int* dep) {
   while (*dep < op.dep_count) {
     const int k = op.dep_begin + *dep;
     int target = a.dep_target[k];
-    if (target < 0) target = int((int64_t(slice + 1) * (-target) - 1) / a.Lt) + 1;
-    if (ld_acquire(a.sync + a.dep_slot[k]) < target) return false;
+    int slot = a.dep_slot[k];
+    if (target <= -(1 << 20)) {
+      slot += slice;
+      target = -target - (1 << 20);
+    } else if (target < 0) {
+      target = int((int64_t(slice + 1) * (-target) - 1) / a.Lt) + 1;
+    }
+    if (ld_acquire(a.sync + slot) < target) return false;
     ++*dep;
   }
   return true;
@@ -377,6 +383,7 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
         }
         __threadfence();
         atomicAdd(a.sync + op.sync_id, 1);
+        if (x == 0 && op.slice_sync >= 0) atomicAdd(a.sync + op.slice_sync + cur.b, 1);
         if (prof) {
           unsigned long long* pr = prof + 8 * cur.item;
           pr[0] = cur.t_disp;

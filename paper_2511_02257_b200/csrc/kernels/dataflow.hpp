@@ -25,6 +25,9 @@ struct DfOp {
   int32_t n_items;
   int64_t first_item;     // index of the op's first item in its queue
   int32_t sync_id;        // done counter (sync[sync_id] reaches n_items)
+  int32_t slice_sync;     // GEMM with a [Lt, ...] output: per-time-slice done counters
+                          // sync[slice_sync + t] (-1: none), so a trace of slice t waits only
+                          // for that slice's tiles
   int32_t dep_begin, dep_count;
   // GEMM: C[b][m][n] = sum_k A[b][m][k] B[b][k][n] (zgemm semantics, kernels.hpp)
   int32_t tmap;           // tensor maps 2*tmap (A) and 2*tmap+1 (B)
@@ -69,7 +72,9 @@ struct DfArgs {
   DfQueue qt;                 // TR_MM items
   const int32_t* dep_slot;    // sync slot an op waits on
   const int32_t* dep_target;  // value the slot must reach; -C: a copy in C time-slice chunks,
-                              // the item needs the chunk holding its slice (value chunk+1)
+                              // the item needs the chunk holding its slice (value chunk+1);
+                              // <= -2^20: per-slice GEMM counter, slot + slice must reach
+                              // -target - 2^20 (the op's items per time slice)
   const void* tmaps;          // CUtensorMap array (64-byte aligned, global memory)
   int* sync;                  // done counters + copy flags (zeroed per launch)
   unsigned long long* prof;   // optional: per GEMM item {claim, ready, end, smid, first data, loop end, kind, -}
