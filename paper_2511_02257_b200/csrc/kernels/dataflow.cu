@@ -39,6 +39,10 @@ using namespace dev;
 using GC = Cfg<64, 64, 16, 32, 16, DF_STAGES>;   // 32 KB stages
 constexpr int CW = GC::NCW * 32;           // 256 consumer threads (+ issuer + 2 scheduler warps)
 constexpr int NT = CW + 96;
+#ifndef DF_CREDIT_CAP
+#define DF_CREDIT_CAP 2   // trace credit saved while no trace item is ready, in k-tiles' worth
+                          // (c2: 2 -> 4.39 ms, 4 -> 4.41, 8 -> 4.55, 32 -> 4.96)
+#endif
 constexpr int TB = 32;                     // trace block edge (complex)
 #ifndef PREFETCH_PARTNERS
 #define PREFETCH_PARTNERS 0
@@ -306,7 +310,7 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
       }
       // credit in 1/8 stages: a GEMM k-tile earns tr_ratio8, a TR_MM stage costs 8
       const int x = (have[1] && (!have[0] || credit >= 8)) ? 1 : 0;
-      if (have[0]) credit = x ? credit - 8 : min(credit + a.tr_ratio8, 2 * a.tr_ratio8);
+      if (have[0]) credit = x ? credit - 8 : min(credit + a.tr_ratio8, DF_CREDIT_CAP * a.tr_ratio8);
       const ItemInfo& inf = s_info[x][slot_of[x]];
       const int k = k_of[x];
       const int st = int(pos % C::STAGES);
