@@ -283,3 +283,17 @@ print('pair ok')
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "pair ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_bb2_ozaki_random_phase_scale(ctx):
+    """BB2 with random-phase data (terms of both signs, cancellation) across 2 split-K chunks:
+    within 1e-10 of the |A||B| error scale (V-4), like the FP64 DMMA path."""
+    from paper_2511_02257_b200 import cc
+    Lt, N, S = 1, 16, 64
+    A = _random_phase((Lt, S, N, N, N), 61)
+    B = _random_phase((Lt, S, N, N, N), 62)
+    got = _run_gemm(ctx, cc.CC_BB2, A, B, Lt, N, S, 5, (Lt, N, N))
+    want = values.bb2(A, B)
+    scale = sum(np.matmul(np.abs(A[:, s]).reshape(Lt, N, N * N), np.abs(B[:, s]).reshape(Lt, N * N, N))
+                for s in range(S))
+    assert np.all(np.abs(got - want) <= 1e-10 * scale)
