@@ -206,6 +206,9 @@ __device__ __forceinline__ const double2* b_at(const ZgemmProblem& q, int t, int
 }
 
 constexpr int KSEG = 4096;   // K elements per warp in the row kernels (long BB2 rows in parallel)
+#ifndef SPLIT_COLS_ROWS
+#define SPLIT_COLS_ROWS 32   // k rows per split_cols CTA (a multiple of 32; more CTAs for small N)
+#endif
 
 // Row scale exponents of A: grid (Mp/8, Lt, ceil(K/KSEG)), one warp per (row, K segment);
 // eA preset to INT_MIN (bytes 0x80), segments folded in with atomicMax.
@@ -295,8 +298,8 @@ __global__ void __launch_bounds__(256) colmax_kernel(ZgemmProblem q, int* __rest
   }
 }
 
-// B_cat^T row slices: grid (Nc/CG, Lt, Kc/128), one CTA per (CG-column group g, t, 128-row
-// chunk of k).  A column left at INT_MIN by colmax_kernel is all zero (exponent 0).
+// B_cat^T row slices: grid (Nc/CG, Lt, Kc/SPLIT_COLS_ROWS), one CTA per (CG-column group g, t,
+// chunk of k rows).  A column left at INT_MIN by colmax_kernel is all zero (exponent 0).
 template <int S, int BN>
 __global__ void __launch_bounds__(256) split_cols_kernel(ZgemmProblem q, int8_t* __restrict__ SB,
                                                          const int* __restrict__ fB, int Nc, int Kc) {
@@ -313,8 +316,8 @@ __global__ void __launch_bounds__(256) split_cols_kernel(ZgemmProblem q, int8_t*
     const int e = fB[size_t(t) * Nc + c0 + tid];
     ecol[tid] = e < -100000 ? 0 : e;
   }
-  const int kend = min(Kc, 128 * int(blockIdx.z + 1));
-  for (int k0 = 128 * blockIdx.z; k0 < kend; k0 += 32) {
+  const int kend = min(Kc, SPLIT_COLS_ROWS * int(blockIdx.z + 1));
+  for (int k0 = SPLIT_COLS_ROWS * blockIdx.z; k0 < kend; k0 += 32) {
     __syncthreads();
     for (int idx = tid; idx < 32 * CG; idx += 256) {
       const int kr = idx / CG, c = idx % CG;
@@ -903,7 +906,7 @@ cudaError_t split_b(const ZgemmProblem& q, int8_t* SB, int* fB, const Geometry& 
   if (e != cudaSuccess) return e;
   const int64_t K = q.Kin * q.Ko;
   colmax_kernel<<<dim3((g.Nc + 31) / 32, unsigned(q.batch), unsigned((K + 127) / 128)), 256, 0, stream>>>(q, fB, g.Nc);
-  split_cols_kernel<S, BN><<<dim3(g.Nc / Tile<BN>::CG, unsigned(q.batch), unsigned((g.Kc + 127) / 128)), 256, 0, stream>>>(q, SB, fB,
+  split_cols_kernel<S, BN><<<dim3(g.Nc / Tile<BN>::CG, unsigned(q.batch), unsigned((g.Kc + SPLIT_COLS_ROWS - 1) / SPLIT_COLS_ROWS)), 256, 0, stream>>>(q, SB, fB,
                                                                                                           g.Nc, g.Kc);
   return cudaGetLastError();
 }
