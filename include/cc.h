@@ -195,8 +195,36 @@ cc_status cc_set_leaf_device(cc_ctx* ctx, int64_t leaf_id, const void* dev, size
 #define CC_EXEC_OZAKI 64
 #define CC_EXEC_AUTO 128
 cc_status cc_execute(cc_ctx* ctx, int32_t flags, cc_exec_stats* stats);
-/* Enqueue-only variant (no host sync): work is ordered on the compute stream. */
+/* Enqueue-only variant (no host sync): work is ordered on the compute stream.  Takes the same
+ * flags as cc_execute except bits 1 (per-kernel timing), 2 / 3 (kernel-only replays) and 5
+ * (profiling), which need a host sync: CC_E_INVAL. */
 cc_status cc_execute_async(cc_ctx* ctx, int32_t flags);
+
+/* Executor options of one context (defaults in brackets; cc_get_options returns the current
+ * values).  They change how the plan is executed, never what it computes: results are
+ * bit-identical across copy_reorder / early_copies / precopy / h2d_chunk_bytes /
+ * ozaki_leaf_cache, and equal within V-4's tolerance across trace_fusion (a fused trace sums
+ * in tile order).  Setting options drops cached graphs and dataflow metadata.
+ *   trace_fusion      dataflow: compute a TR_MM inside the GEMM producing its later operand [0]
+ *   copy_reorder      dataflow: order wait-free leaf H2D copies by the work they enable [1]
+ *   early_copies      dataflow: start wait-free leaf copies while the metadata is built [1]
+ *   precopy           dataflow: start up to 4 leading leaf copies before the physical plan [1]
+ *   ozaki_leaf_cache  Ozaki engine: split every leaf once per execute [1]
+ *   ozaki_slices      Ozaki engine: INT8 slices per operand, 4..7 [5]
+ *   h2d_chunk_bytes   dataflow: H2D copies in time-slice chunks of about this size, each with its
+ *                     own completion flag; 0: whole tensors [0]
+ *   tr_ratio          dataflow: TR_MM stages the issuer interleaves per GEMM k-tile; 0: 1.12 x the
+ *                     plan's trace/k-tile stage ratio [0]
+ *   debug             bit 0: executor trace on stderr; bit 1: host phase timings on stderr [0]
+ * Errors: CC_E_INVAL for out-of-range values. */
+typedef struct {
+  int32_t trace_fusion, copy_reorder, early_copies, precopy, ozaki_leaf_cache, ozaki_slices;
+  int64_t h2d_chunk_bytes;
+  double tr_ratio;
+  int32_t debug, pad_;
+} cc_options;
+cc_status cc_get_options(cc_ctx* ctx, cc_options* out);
+cc_status cc_set_options(cc_ctx* ctx, const cc_options* opt);
 
 /* Per-kind contraction-kernel time of the last cc_execute with flags bit 1 (kernels timed
  * with CUDA events on the compute stream): seconds[op], counts[op] for op = cc_op (8 each). */

@@ -71,6 +71,12 @@ class cc_plan_op(ctypes.Structure):
     _fields_ = [("kind", c_i32), ("pad_", c_i32), ("node", c_i64), ("bytes", c_i64), ("offset", c_i64)]
 
 
+class cc_options(ctypes.Structure):
+    _fields_ = [(n, c_i32) for n in ("trace_fusion", "copy_reorder", "early_copies", "precopy", "ozaki_leaf_cache",
+                                     "ozaki_slices")] + \
+               [("h2d_chunk_bytes", c_i64), ("tr_ratio", c_dbl), ("debug", c_i32), ("pad_", c_i32)]
+
+
 class cc_dag_stats(ctypes.Structure):
     _fields_ = [(n, c_i64) for n in ("V", "E", "k", "n_contr", "n_leaves", "max_rank", "n_corr")] + \
                [("F_v", c_dbl), ("F_e", c_dbl)]
@@ -104,6 +110,8 @@ _sig("cc_set_leaf_device", c_void_p, c_i64, c_void_p, c_size_t)
 _sig("cc_execute", c_void_p, c_i32, P(cc_exec_stats))
 _sig("cc_execute_async", c_void_p, c_i32)
 _sig("cc_kernel_times", c_void_p, P(c_dbl), P(c_i64))
+_sig("cc_get_options", c_void_p, P(cc_options))
+_sig("cc_set_options", c_void_p, P(cc_options))
 _sig("cc_dataflow_state", c_void_p, P(c_i64), c_i64, P(c_i64))
 _sig("cc_dataflow_profile", c_void_p, P(c_u64), c_i64, P(c_i64), P(c_i64))
 _sig("cc_correlator", c_void_p, c_i64, P(c_dbl), c_i32)
@@ -124,7 +132,7 @@ _sig("cc_scratch_bytes", c_i32, c_i32, c_i32, res=c_size_t)
 EXPORTED = ["cc_create", "cc_destroy", "cc_last_error", "cc_version", "cc_load_dag", "cc_load_dag_file",
             "cc_dag_info", "cc_part_time_range", "cc_correlators", "cc_partition", "cc_part_trees", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
             "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_execute",
-            "cc_execute_async", "cc_kernel_times", "cc_dataflow_state", "cc_dataflow_profile", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
+            "cc_execute_async", "cc_get_options", "cc_set_options", "cc_kernel_times", "cc_dataflow_state", "cc_dataflow_profile", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
             "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_mm1_ozaki", "cc_mm1_ozaki_workspace_bytes", "cc_i8gemm_tn", "cc_gemm_ozaki",
             "cc_gemm_ozaki_workspace_bytes", "cc_fill_synthetic", "cc_scratch_bytes"]
 
@@ -301,6 +309,21 @@ class Context:
 
     def execute_async(self, flags=0):
         self._ck(_lib.cc_execute_async(self._h, flags))
+
+    def options(self):
+        o = cc_options()
+        self._ck(_lib.cc_get_options(self._h, ctypes.byref(o)))
+        return {f: getattr(o, f) for f, _ in cc_options._fields_ if f != "pad_"}
+
+    def set_options(self, **kw):
+        """Change executor options (cc.h cc_options); unnamed ones keep their current value."""
+        o = cc_options()
+        self._ck(_lib.cc_get_options(self._h, ctypes.byref(o)))
+        for k, v in kw.items():
+            if k not in dict(cc_options._fields_) or k == "pad_":
+                raise KeyError(k)
+            setattr(o, k, v)
+        self._ck(_lib.cc_set_options(self._h, ctypes.byref(o)))
 
     def kernel_times(self):
         s = (c_dbl * 8)()

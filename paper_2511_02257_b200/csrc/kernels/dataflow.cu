@@ -44,12 +44,6 @@ constexpr int NT = CW + 96;
                           // (c2: 2 -> 4.39 ms, 4 -> 4.41, 8 -> 4.55, 32 -> 4.96)
 #endif
 constexpr int TB = 32;                     // trace block edge (complex)
-#ifndef PREFETCH_PARTNERS
-#define PREFETCH_PARTNERS 0
-#endif
-#ifndef PREFETCH_TRACE
-#define PREFETCH_TRACE 0
-#endif
 constexpr int INFO = 4;                    // item slots per queue (claimed-ready-running-unpublished)
 static_assert(GC::A_BYTES == TB * TB * 16 && GC::B_BYTES == TB * TB * 16, "a trace block pair fills one stage");
 
@@ -60,12 +54,6 @@ __device__ __forceinline__ void tma_load_4d_g(void* dst, const void* map, uint64
           smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
-}
-
-__device__ __forceinline__ void tma_prefetch_4d(const void* map, int c0, int c1, int c2, int c3) {
-  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(map), "r"(c0), "r"(c1),
-               "r"(c2), "r"(c3)
-               : "memory");
 }
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
@@ -197,16 +185,6 @@ __device__ __forceinline__ void gemm_stage_loads(const ItemInfo& inf, int k, uin
       tma_load_4d_g(sA + c * 4096, map, bar, 2 * (inf.tm * C::BM + 8 * c), inf.tn * C::BN + 32 * h, 0, inf.b);
     return;
   }
-  if (k == 0 && inf.fc > 0 && PREFETCH_PARTNERS) {
-    // warm L2 with the item's partner tiles while its k-tiles run
-    for (int f = 0; f < inf.fc; ++f) {
-      const void* map = static_cast<const uint8_t*>(tmaps) + size_t(2 * (inf.ptmap0 + f)) * 128;
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          tma_prefetch_4d(map, 2 * (inf.tm * C::BM + 8 * c), inf.tn * C::BN + 32 * h, 0, inf.b);
-    }
-  }
   uint8_t* sB = sA + C::A_BYTES;
   const int kk = inf.k0 + k;
   const int ko = kk / inf.kt_per_o;
@@ -310,7 +288,8 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
       }
       // credit in 1/8 stages: a GEMM k-tile earns tr_ratio8, a TR_MM stage costs 8
       const int x = (have[1] && (!have[0] || credit >= 8)) ? 1 : 0;
-      if (have[0]) credit = x ? credit - 8 : min(credit + a.tr_ratio8, DF_CREDIT_CAP * a.tr_ratio8);
+      // (the cap is at least one trace stage, so a low ratio still interleaves)
+      if (have[0]) credit = x ? credit - 8 : min(credit + a.tr_ratio8, max(8, DF_CREDIT_CAP * a.tr_ratio8));
       const ItemInfo& inf = s_info[x][slot_of[x]];
       const int k = k_of[x];
       const int st = int(pos % C::STAGES);
@@ -426,18 +405,6 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
             asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(
                              static_cast<const uint8_t*>(a.tmaps) + size_t(2 * (inf.ptmap0 + f)) * 128)
                          : "memory");
-        if (x == 1 && PREFETCH_TRACE) {
-          // warm L2 with the trace item's block pairs (the scheduler is off the issue path)
-          for (int k = 0; k < inf.npos; ++k) {
-            const int u = inf.u0 + k;
-            const int I = u / inf.nb, J = u - I * inf.nb;
-#pragma unroll
-            for (int ch = 0; ch < TB / 8; ++ch) {
-              tma_prefetch_4d(inf.tA, 2 * (J * TB + 8 * ch), I * TB, 0, inf.t);
-              tma_prefetch_4d(inf.tB, 2 * (I * TB + 8 * ch), J * TB, 0, inf.t);
-            }
-          }
-        }
         inf.t_ready = prof ? gtimer() : 0ull;
         const int s = int(n_alloc % INFO);
         s_info[x][s] = inf;

@@ -30,8 +30,8 @@
 // columns: BN/2 complex output columns); a stage = all s slices of A and B for one 64-byte k
 // chunk = contiguous bulk copies; one lane issues the tcgen05.mma's, 4 or 8 warps drain TMEM.
 // BM1 / BB2 use the same kernels on their (two-level K) operand layouts; K is cut into chunks
-// of 8192 complex terms (INT32 bound) whose FP64 partials are summed in order.  An opt-in
-// CTA-pair variant (cta_group::2, CC_OZ_PAIR=1) runs M = 256 per instruction.
+// of 8192 complex terms (INT32 bound) whose FP64 partials are summed in order.  (A CTA-pair
+// variant, cta_group::2 with M = 256 per instruction, measured slower in round 1: removed.)
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -556,230 +556,6 @@ __global__ void __launch_bounds__((Tile<BN>::NEPI + 2) * 32, 1) ozaki_gemm_kerne
 }
 
 // ---------------------------------------------------------------------------------------
-// The same GEMM on CTA pairs (cta_group::2, cluster of 2): one tcgen05.mma.cta_group::2 covers
-// M = 256 rows (128 per CTA, each CTA's own A block) x BN columns (each CTA holds BN/2 rows of
-// B_cat^T), so every instruction does twice the MACs and each SM reads half the B tile.
-// Synchronisation: each CTA's producer fills its own ring slot; the peer (rank 1) forwards
-// "my slot is full" to the leader's pfull barrier; the leader issues the MMAs and its commits
-// arrive on both CTAs' empty / tfull barriers (multicast); both CTAs drain their own TMEM and
-// release each diagonal on the leader's drained barrier (2 x NEPI arrivals).
-template <int S, int BN>
-struct Cfg2 {
-  static constexpr int HB_TILE = (BN / 2) * BKB;
-  static constexpr int STAGE = S * (A_TILE + HB_TILE);
-  static constexpr int STAGES = (SMEM_BUDGET / STAGE) > 4 ? 4 : (SMEM_BUDGET / STAGE);
-  static constexpr int SMEM = STAGES * STAGE + 1024;
-  static_assert(STAGES >= 2 && S * BN <= 512, "pair config");
-};
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t mapa_rank0(const void* p) {
-  uint32_t a;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(a) : "r"(dev::smem_u32(p)));
-  return a;
-}
-__device__ __forceinline__ void remote_arrive(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nW_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra W_%=;\n}\n" ::"r"(dev::smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void mma2_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(0u)
-      : "memory");
-}
-__device__ __forceinline__ void commit2_both(uint64_t* bar) {
-  asm volatile(
-      "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n" ::"r"(
-          dev::smem_u32(bar))
-      : "memory");
-}
-
-template <int S, int BN>
-__global__ void __launch_bounds__((Tile<BN>::NEPI + 2) * 32, 1) ozaki_gemm2_kernel(Params p) {
-  using C = Cfg2<S, BN>;
-  constexpr int CG = Tile<BN>::CG, NEPI = Tile<BN>::NEPI, CPW = Tile<BN>::CPW, B_TILE = Tile<BN>::B_TILE;
-  constexpr int HB_TILE = C::HB_TILE;
-  constexpr uint32_t IDESC = (Tile<BN>::IDESC & ~(31u << 24)) | (uint32_t(256 >> 4) << 24);   // M = 256
-  extern __shared__ __align__(1024) uint8_t dsm[];
-  __shared__ __align__(8) uint64_t full[C::STAGES], pfull[C::STAGES], empty[C::STAGES], tfull, drained[S];
-  __shared__ uint32_t tmem_slot;
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-  const int ntn = p.Brows / BN, ntm = p.Mp / BM, ntm2 = ntm / 2;
-  const int ntiles = ntn * ntm2 * p.Lt * p.nch;
-
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dev::smem_u32(&tmem_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  if (threadIdx.x == 32) {
-    for (int s = 0; s < C::STAGES; ++s) {
-      dev::mbar_init(&full[s], 1);
-      dev::mbar_init(&pfull[s], 1);
-      dev::mbar_init(&empty[s], 1);
-    }
-    dev::mbar_init(&tfull, 1);
-    for (int d = 0; d < S; ++d) dev::mbar_init(&drained[d], 2 * NEPI);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();
-  tc_fence_after();
-  const uint32_t tmem = tmem_slot;
-  const int nk = p.Kp / BKB;
-  auto decode = [&](int tile, int& t, int& mb2, int& nb, int& ch) {
-    ch = tile % p.nch;
-    const int r = tile / p.nch;
-    nb = r % ntn;
-    mb2 = (r / ntn) % ntm2;
-    t = r / (ntn * ntm2);
-  };
-
-  if (warp == NEPI) {
-    if (lane == 0) {
-      int it = 0;
-      for (int tile = cid; tile < ntiles; tile += ncl) {
-        int t, mb2, nb, ch;
-        decode(tile, t, mb2, nb, ch);
-        const int mb = 2 * mb2 + int(rank);
-        const int kc1 = min(nk, (ch + 1) * p.kchs);
-        for (int kc = ch * p.kchs; kc < kc1; ++kc, ++it) {
-          const int st = it % C::STAGES;
-          if (it >= C::STAGES) dev::mbar_wait(&empty[st], ((it / C::STAGES) - 1) & 1);
-          dev::mbar_expect_tx(&full[st], C::STAGE);
-          uint8_t* sa = smem + st * C::STAGE;
-          uint8_t* sb = sa + S * A_TILE;
-          bulk_load(sa, p.SA + ((size_t(t) * ntm + mb) * nk + kc) * (S * A_TILE), S * A_TILE, &full[st]);
-          const int8_t* srcb = p.SB + ((size_t(t) * ntn + nb) * nk + kc) * (S * B_TILE) + rank * HB_TILE;
-#pragma unroll
-          for (int j = 0; j < S; ++j) bulk_load(sb + j * HB_TILE, srcb + j * B_TILE, HB_TILE, &full[st]);
-        }
-      }
-    }
-  } else if (warp == NEPI + 1) {
-    if (lane == 0 && rank == 1) {
-      // the peer forwards the arrival of each of its ring slots to the leader
-      int it = 0;
-      for (int tile = cid; tile < ntiles; tile += ncl) {
-        const int ch = tile % p.nch;
-        const int kc1 = min(nk, (ch + 1) * p.kchs);
-        for (int kc = ch * p.kchs; kc < kc1; ++kc, ++it) {
-          const int st = it % C::STAGES;
-          dev::mbar_wait(&full[st], (it / C::STAGES) & 1);
-          remote_arrive(mapa_rank0(&pfull[st]));
-        }
-      }
-    } else if (lane == 0) {
-      int it = 0, n = 0;
-      for (int tile = cid; tile < ntiles; tile += ncl, ++n) {
-        const int ch = tile % p.nch;
-        const int kc0 = ch * p.kchs, kc1 = min(nk, (ch + 1) * p.kchs);
-        for (int kc = kc0; kc < kc1; ++kc, ++it) {
-          const int st = it % C::STAGES;
-          dev::mbar_wait(&full[st], (it / C::STAGES) & 1);
-          mbar_wait_cluster(&pfull[st], (it / C::STAGES) & 1);
-          tc_fence_after();
-          const uint32_t sa = dev::smem_u32(smem + st * C::STAGE);
-          const uint32_t sb = sa + S * A_TILE;
-#pragma unroll
-          for (int d = 0; d < S; ++d) {
-            if (kc == kc0 && n > 0) {
-              mbar_wait_cluster(&drained[d], (n - 1) & 1);
-              tc_fence_after();
-            }
-#pragma unroll
-            for (int i = 0; i <= d; ++i)
-#pragma unroll
-              for (int ks = 0; ks < BKB / UK; ++ks)
-                mma2_i8(tmem + uint32_t(d * BN), sw64_desc(sa + i * A_TILE + ks * UK),
-                        sw64_desc(sb + (d - i) * HB_TILE + ks * UK), IDESC, ((kc - kc0) | i | ks) != 0);
-          }
-          commit2_both(&empty[st]);
-        }
-        commit2_both(&tfull);
-      }
-    }
-  } else {
-    const uint32_t leader_drained0 = mapa_rank0(&drained[0]);
-    int n = 0;
-    for (int tile = cid; tile < ntiles; tile += ncl, ++n) {
-      int t, mb2, nb, ch;
-      decode(tile, t, mb2, nb, ch);
-      const int mb = 2 * mb2 + int(rank);
-      dev::mbar_wait(&tfull, n & 1);
-      tc_fence_after();
-      const int quarter = warp & 3, half = warp >> 2;
-      const int r = mb * BM + quarter * 32 + lane;
-      const uint32_t tl = tmem + (uint32_t(quarter * 32) << 16);
-      double ar[CPW], ai[CPW];
-#pragma unroll
-      for (int q = 0; q < CPW; ++q) ar[q] = ai[q] = 0.0;
-#pragma unroll 1
-      for (int d = 0; d < S; ++d) {
-        int vr[CPW], vi[CPW];
-#pragma unroll
-        for (int q = 0; q < CPW; q += 8) {
-          tmem_ld8(tl + uint32_t(d * BN + half * CPW + q), &vr[q]);
-          tmem_ld8(tl + uint32_t(d * BN + CG + half * CPW + q), &vi[q]);
-        }
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) remote_arrive(leader_drained0 + uint32_t(d * 8));
-        const double w = pow2(-12 - 8 * d);
-#pragma unroll
-        for (int q = 0; q < CPW; ++q) {
-          ar[q] = fma(double(vr[q]), w, ar[q]);
-          ai[q] = fma(double(vi[q]), w, ai[q]);
-        }
-      }
-      if (r < p.M) {
-        const int ea = p.eA[size_t(t) * p.Mp + r];
-        const double se = pow2(ea < -100000 ? 0 : ea);
-        const int cbase = nb * CG + half * CPW;
-        const int* f = p.fB + size_t(t) * p.Nc + cbase;
-        double* dst = p.nch == 1 ? p.C + 2 * (size_t(t) * p.sCb + size_t(r) * p.ldc)
-                                 : p.P + 2 * (((size_t(ch) * p.Lt + t) * p.Mp + r) * p.Nc);
-#pragma unroll
-        for (int q = 0; q < CPW; ++q) {
-          const int c = cbase + q;
-          if (c < p.Nn) {
-            const double sf = se * pow2(f[q] < -100000 ? 0 : f[q]);
-            *reinterpret_cast<double2*>(dst + 2 * c) = make_double2(ar[q] * sf, ai[q] * sf);
-          }
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync_all();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-}
-
-// ---------------------------------------------------------------------------------------
 // host side
 
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
@@ -864,31 +640,6 @@ cudaError_t launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const Para
   return cudaGetLastError();
 }
 
-template <int S, int BN>
-cudaError_t launch_gemm2(const Params& p, cudaStream_t stream) {
-  using C = Cfg2<S, BN>;
-  auto k = ozaki_gemm2_kernel<S, BN>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  if (e != cudaSuccess) return e;
-  const int64_t tiles = int64_t(p.Brows / BN) * (p.Mp / BM / 2) * p.Lt * p.nch;
-  const int pairs = int(std::min<int64_t>(tiles, num_sms() / 2));
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(unsigned(2 * pairs));
-  cfg.blockDim = dim3(unsigned((Tile<BN>::NEPI + 2) * 32));
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, k, p);
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
-}
-
 template <int S>
 cudaError_t split_a(const ZgemmProblem& q, int8_t* SA, int* eA, const Geometry& g, cudaStream_t stream) {
   cudaError_t e = cudaMemsetAsync(eA, 0x80, size_t(q.batch) * g.Mp * 4, stream);   // INT_MIN-like
@@ -944,12 +695,7 @@ cudaError_t run_batch(const ZgemmProblem& q, uint8_t* w, const OzakiForm* fa, co
   p.eA = eA; p.fB = fB; p.C = static_cast<double*>(q.C);
   p.P = g.nch > 1 ? reinterpret_cast<double*>(w + g.part) : nullptr;
   p.SA = SA; p.SB = SB;
-  // CTA pairs (cta_group::2) when CC_OZ_PAIR=1 and the rows come in whole pairs of 128-row blocks
-  static const bool pair_env = getenv("CC_OZ_PAIR") && atoi(getenv("CC_OZ_PAIR")) != 0;
-  if (pair_env && (g.Mp / BM) % 2 == 0)
-    e = launch_gemm2<S, BN>(p, stream);
-  else
-    e = launch_gemm<S, false, BN>(ma, mb, p, stream);
+  e = launch_gemm<S, false, BN>(ma, mb, p, stream);
   if (e != cudaSuccess || g.nch == 1) return e;
   ozaki_reduce_kernel<<<num_sms() * 4, 256, 0, stream>>>(p);
   return cudaGetLastError();

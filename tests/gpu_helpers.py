@@ -23,14 +23,17 @@ def to_numpy_c(t, shape):
 
 
 def run_gpu(w, algo=None, cap=0, flags=0, device_leaves=False, arena_mb=256, leaf_fn=None, ctx=None,
-            part=None, evict_next_use=False):
-    """Returns (ctx, roots{tree: [Lt]}, corr{c: [Lt]}, plan stats, exec stats)."""
+            part=None, evict_next_use=False, options=None):
+    """Returns (ctx, roots{tree: [Lt]}, corr{c: [Lt]}, plan stats, exec stats).
+    options: executor options for cc_set_options (cc.h cc_options), e.g. {"trace_fusion": 1}."""
     import torch
     from paper_2511_02257_b200 import cc
     dag = Dag(w)
     if ctx is None:
         arena = torch.empty(arena_mb << 20, dtype=torch.uint8, device="cuda")
         ctx = cc.Context(0, arena)
+    if options:
+        ctx.set_options(**options)
     ctx.load_workload(w)
     if part is not None:
         ctx.partition(*part)

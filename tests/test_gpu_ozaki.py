@@ -141,9 +141,9 @@ def test_mm1_ozaki_error_margin_large_N(ctx):
     assert err4 > 10 * err5, (err4, err5)
 
 
-def test_executor_ozaki_leaf_form_cache_bitwise(monkeypatch):
+def test_executor_ozaki_leaf_form_cache_bitwise():
     """Leaves split once per execute and shared by their MM1s (cache in the free pool above the
-    plan's high water) give bit-identical roots to splitting per MM1 (CC_OZAKI_LEAF_CACHE=0):
+    plan's high water) give bit-identical roots to splitting per MM1 (option ozaki_leaf_cache=0):
     the slices are a deterministic function of the leaf."""
     from synth import dags
     from oracle.dag import Dag
@@ -153,7 +153,7 @@ def test_executor_ozaki_leaf_form_cache_bitwise(monkeypatch):
     ctx, roots, corr, st, ex = run_gpu(w, flags=64, arena_mb=512)
     r_or, _ = values.run_workload(w, dag)
     assert_roots_close(roots, r_or)
-    monkeypatch.setenv("CC_OZAKI_LEAF_CACHE", "0")
+    ctx.set_options(ozaki_leaf_cache=0)
     ctx.execute(64)
     again = {t: ctx.root_value(t, w.Lt) for t in roots}
     assert all(np.array_equal(again[t], roots[t]) for t in roots)
@@ -250,39 +250,6 @@ def test_executor_auto_flag():
     _, roots, _, _, ex = run_gpu(w, flags=cc.EXEC_AUTO, arena_mb=2048)
     assert ex["n_kernels"] > 10
     assert_roots_close(roots, values.run_workload(w, Dag(w))[0])
-
-
-def test_pair_variant_cta_group_2():
-    """The CTA-pair GEMM (tcgen05.mma.cta_group::2, M = 256 per instruction; CC_OZ_PAIR=1, read
-    once per process, hence the subprocess) gives the same values as the single-CTA engine."""
-    import os
-    import subprocess
-    import sys
-    code = r"""
-import numpy as np, torch, sys
-sys.path.insert(0, 'tests')
-from synth import rng as srng
-from oracle import values
-from paper_2511_02257_b200 import cc
-from gpu_helpers import device_from, to_numpy_c
-ctx = cc.Context(0, torch.empty(64 << 20, dtype=torch.uint8, device='cuda'))
-for (Lt, N) in ((2, 256), (1, 640)):
-    A = srng.leaf_values(3, 900 + N, 0, Lt * N * N, 1.0).reshape(Lt, N, N)
-    B = srng.leaf_values(3, 950 + N, 0, Lt * N * N, 1.0).reshape(Lt, N, N)
-    ws = torch.empty(cc.cc_mm1_ozaki_workspace_bytes(Lt, N, 5), dtype=torch.uint8, device='cuda')
-    C = torch.empty(Lt * N * N * 2, dtype=torch.float64, device='cuda')
-    ctx.mm1_ozaki(device_from(A), device_from(B), C, Lt, N, 5, ws)
-    torch.cuda.synchronize()
-    got = to_numpy_c(C, (Lt, N, N))
-    want = values.mm1(A, B)
-    err = float(np.max(np.abs(got - want) / np.abs(want)))
-    assert err <= 1e-10, err
-print('pair ok')
-"""
-    env = dict(os.environ, CC_OZ_PAIR="1")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0 and "pair ok" in r.stdout, r.stdout + r.stderr
 
 
 def test_bb2_ozaki_random_phase_scale(ctx):

@@ -159,29 +159,29 @@ def test_correlators_bulk_read():
             assert np.array_equal(allc[k], corr[c])
 
 
-def test_schedule_and_mode_invariance_bitwise(monkeypatch):
+def test_schedule_and_mode_invariance_bitwise():
     """Deterministic kernels, no atomics in any reduction: root values are bit-identical run to
     run and across graph/stream mode; with trace fusion off also across schedulers and
     host/device leaves (which traces fuse into which GEMM depends on the plan, and a fused
     trace sums in tile order, so with fusion on those agree to rounding)."""
     from paper_2511_02257_b200 import cc
     w = dags.config_c2(N=24, Lt=2, n_loop4=40, n_loop2=4, n_corr=3)
-    monkeypatch.setenv("CC_DF_FUSE_TR", "1")
-    base = run_gpu(w, algo=cc.CC_TREE)[1]
-    again = run_gpu(w, algo=cc.CC_TREE)[1]
+    fz = {"trace_fusion": 1}
+    base = run_gpu(w, algo=cc.CC_TREE, options=fz)[1]
+    again = run_gpu(w, algo=cc.CC_TREE, options=fz)[1]
     for t in base:
         assert np.array_equal(base[t], again[t])
     for kw in (dict(algo=cc.CC_SIBLING), dict(algo=cc.CC_RSGS), dict(device_leaves=True),
                dict(flags=1, device_leaves=True)):
-        assert_roots_close(run_gpu(w, **kw)[1], base, rel=1e-13)
-    dl = run_gpu(w, device_leaves=True)[1]
-    dlg = run_gpu(w, flags=1, device_leaves=True)[1]
+        assert_roots_close(run_gpu(w, options=fz, **kw)[1], base, rel=1e-13)
+    dl = run_gpu(w, device_leaves=True, options=fz)[1]
+    dlg = run_gpu(w, flags=1, device_leaves=True, options=fz)[1]
     for t in dl:
         assert np.array_equal(dl[t], dlg[t])
-    monkeypatch.setenv("CC_DF_FUSE_TR", "0")
     base = run_gpu(w, algo=cc.CC_TREE)[1]
     for kw in (dict(algo=cc.CC_SIBLING), dict(algo=cc.CC_RSGS), dict(flags=1), dict(device_leaves=True),
-               dict(flags=1, device_leaves=True)):
+               dict(flags=1, device_leaves=True), dict(options={"precopy": 0}), dict(options={"early_copies": 0}),
+               dict(options={"copy_reorder": 0, "tr_ratio": 0.5})):
         other = run_gpu(w, **kw)[1]
         for t in base:
             assert np.array_equal(base[t], other[t]), kw
@@ -190,7 +190,7 @@ def test_schedule_and_mode_invariance_bitwise(monkeypatch):
     assert_roots_close(legacy, base, rel=1e-13)
 
 
-def test_chunked_and_reordered_h2d_copies(monkeypatch):
+def test_chunked_and_reordered_h2d_copies():
     """Host leaves copied in time-slice chunks (items wait only for the chunk holding their
     slice) and wait-free copies moved ahead in queue order: same values as the oracle and
     bit-identical to whole-tensor copies in plan order (the copy schedule never changes
@@ -198,29 +198,25 @@ def test_chunked_and_reordered_h2d_copies(monkeypatch):
     w = dags.config_c2(N=40, Lt=8, n_loop4=60, n_loop2=6, n_corr=4)
     dag = Dag(w)
     r_or, c_or = values.run_workload(w, dag)
-    monkeypatch.setenv("CC_H2D_CHUNK_MB", "100")
-    monkeypatch.setenv("CC_COPY_REORDER", "0")
-    base = run_gpu(w)[1]
-    for chunk_mb, reorder in (("0.0625", "0"), ("0.0625", "1"), ("0.01", "1"), ("100", "1")):
-        monkeypatch.setenv("CC_H2D_CHUNK_MB", chunk_mb)
-        monkeypatch.setenv("CC_COPY_REORDER", reorder)
+    base = run_gpu(w, options={"h2d_chunk_bytes": 100 << 20, "copy_reorder": 0})[1]
+    for chunk, reorder in ((65536, 0), (65536, 1), (10 << 10, 1), (100 << 20, 1)):
+        opt = {"h2d_chunk_bytes": chunk, "copy_reorder": reorder}
         for flags in (0, 1):
-            _, roots, corr, st, ex = run_gpu(w, flags=flags)
+            _, roots, corr, st, ex = run_gpu(w, flags=flags, options=opt)
             assert_roots_close(roots, r_or)
             assert_corr_close(dag, r_or, corr, c_or)
             for t in base:
-                assert np.array_equal(base[t], roots[t]), (chunk_mb, reorder, flags)
+                assert np.array_equal(base[t], roots[t]), (chunk, reorder, flags)
     # baryon leaves (Lt=2 -> at most 2 chunks)
-    monkeypatch.setenv("CC_H2D_CHUNK_MB", "0.0625")
     w = dags.config_c3(N=12, Lt=2, S=64)
     dag = Dag(w)
     r_or, c_or = values.run_workload(w, dag)
-    _, roots, corr, st, ex = run_gpu(w)
+    _, roots, corr, st, ex = run_gpu(w, options={"h2d_chunk_bytes": 65536})
     assert_roots_close(roots, r_or)
     assert_corr_close(dag, r_or, corr, c_or)
 
 
-def test_trace_fusion_on_off(monkeypatch):
+def test_trace_fusion_on_off():
     """Traces fused into the GEMM that produces their later operand (partner tiles dotted
     with the output tile in registers) give the oracle's values, like the stand-alone trace
     items; ragged N (not a multiple of the 64-wide tile) exercises the zero-filled borders."""
@@ -229,15 +225,14 @@ def test_trace_fusion_on_off(monkeypatch):
         dag = Dag(w)
         r_or, c_or = values.run_workload(w, dag)
         res = {}
-        for fuse in ("1", "0"):
-            monkeypatch.setenv("CC_DF_FUSE_TR", fuse)
+        for fuse in (1, 0):
             for dev in (False, True):
-                _, roots, corr, st, ex = run_gpu(w, device_leaves=dev)
+                _, roots, corr, st, ex = run_gpu(w, device_leaves=dev, options={"trace_fusion": fuse})
                 assert_roots_close(roots, r_or)
                 assert_corr_close(dag, r_or, corr, c_or)
                 res[(fuse, dev)] = (roots, ex["n_kernels"])
         # fused: one more launch (the finish kernel summing tile partials)
-        assert res[("1", True)][1] == res[("0", True)][1] + 1
+        assert res[(1, True)][1] == res[(0, True)][1] + 1
 
 
 def test_c3_nucleon_small():
