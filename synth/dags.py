@@ -221,11 +221,22 @@ def config_c1(N=32, Lt=4):
     return b.w
 
 
-def config_c2(N=128, Lt=64, n_src=16, n_snk=16, n_loop4=384, n_loop2=16, n_corr=10, seed=1):
+# Gaussian-integer term coefficients (coefs="complex"): exact in FP64, both signs, both parts
+COMPLEX_COEFS = [(1.0, 2.0), (-1.0, 1.0), (2.0, -1.0), (0.0, -3.0), (-2.0, 0.0), (1.0, -1.0)]
+
+
+def draw_coef(rng, coefs):
+    """One term coefficient: +-1 ("pm1") or a Gaussian integer from COMPLEX_COEFS ("complex")."""
+    if coefs == "complex":
+        return COMPLEX_COEFS[int(rng.integers(len(COMPLEX_COEFS)))]
+    return (float(rng.choice([1.0, -1.0])), 0.0)
+
+
+def config_c2(N=128, Lt=64, n_src=16, n_snk=16, n_loop4=384, n_loop2=16, n_corr=10, seed=1, coefs="pm1"):
     """c2: pi-pi I=2 correlator set.  4-meson loops TR_MM(MM1(src_a,snk_c), MM1(src_b,snk_d))
     with a<b, c!=d sampled without replacement; MM1 pairs shared across trees;
     plus 2-meson loops TR_MM(src_a, snk_c).  Each tree enters one or two of
-    n_corr correlators with coefficient +-1."""
+    n_corr correlators with coefficient +-1 (coefs="complex": Gaussian integers)."""
     rng = np.random.default_rng(seed)
     b = Builder("c2_pipi_set_N%d_Lt%d" % (N, Lt), Lt, N, 1)
     src = [b.leaf(LEAF_M) for _ in range(n_src)]
@@ -252,7 +263,7 @@ def config_c2(N=128, Lt=64, n_src=16, n_snk=16, n_loop4=384, n_loop2=16, n_corr=
     for t in trees:
         cs = rng.choice(n_corr, size=int(rng.integers(1, 3)), replace=False)
         for c in sorted(int(x) for x in cs):
-            b.term(c, t, float(rng.choice([1.0, -1.0])), 0.0)
+            b.term(c, t, *draw_coef(rng, coefs))
     _prune(b.w)
     return b.w
 

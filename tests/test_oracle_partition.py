@@ -1,0 +1,68 @@
+"""Pins of oracle/partition.py (reading M-1; partitioning is future work
+in the paper) against hand-derived parts and properties the rule must satisfy:
+contiguity in tree-scheduler selection order, first-execution weights computed as set
+differences of tree closures, total weight = the DAG's contraction weight, and balance
+|W_p - W/n| <= max_t w_t (midpoint rule)."""
+import pytest
+
+from synth import dags
+from oracle import partition, tree as tree_sched
+from oracle.dag import Dag
+
+
+def _selection(dag):
+    s = tree_sched.TreeScheduler(dag)
+    s.run()
+    return s.tree_order
+
+
+def test_dstar_hand_parts():
+    """D* (Table I DAG, unit weights: abstract contractions weigh 1).  The tree scheduler selects
+    T0 (f), T1 (g), T2 (h) (SURVEY §8(c) O4 hand trace); first-execution weights: T0 {f} = 1,
+    T1 {e, g} = 2, T2 {h} = 1, W = 4.  Midpoints 0.5, 2, 3.5 -> n = 2: floor(2 mid / 4) = 0, 1, 1;
+    n = 3: floor(3 mid / 4) = 0, 1, 2."""
+    dag = Dag(dags.fixture_dstar())
+    assert _selection(dag) == [0, 1, 2]
+    assert partition.tree_parts(dag, 2) == {0: 0, 1: 1, 2: 1}
+    assert partition.tree_parts(dag, 3) == {0: 0, 1: 1, 2: 2}
+    assert partition.tree_parts(dag, 1) == {0: 0, 1: 0, 2: 0}
+
+
+def _weight(w, op):
+    # flops / 8 of one contraction: MM1 Lt N^3, BM1 / BB2 Lt S N^4, TR_MM Lt N^2
+    return {dags.MM1: w.Lt * w.N ** 3, dags.BM1: w.Lt * w.S * w.N ** 4, dags.BB2: w.Lt * w.S * w.N ** 4,
+            dags.TR_MM: w.Lt * w.N ** 2, dags.OP_X: 1}[op]
+
+
+@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("n", [2, 3, 5])
+def test_partition_properties(seed, n):
+    typed = seed % 3 != 0
+    w = dags.random_dag(seed, n_leaves=6, n_trees=9, max_ops_per_tree=4, share_p=0.6, typed=typed, N=3, Lt=2)
+    dag = Dag(w)
+    ops = {x[0]: x[1] for x in w.nodes}
+    sel = _selection(dag)
+    parts = partition.tree_parts(dag, n)
+    # contiguous and non-decreasing along the selection order, every tree assigned
+    seq = [parts[t] for t in sel]
+    assert sorted(parts) == sorted(dag.tree_ids)
+    assert seq == sorted(seq) and all(0 <= p < n for p in seq)
+    # first-execution weights as set differences of closures (members of a tree not in any
+    # earlier-selected tree's closure, contractions only)
+    seen, wt = set(), {}
+    for t in sel:
+        members = set(dag.trees[t][1])
+        new = [u for u in members - seen if dag.nodes[u].child]
+        wt[t] = sum(_weight(w, ops[u]) for u in new)
+        seen |= members
+    W = sum(wt.values())
+    assert W == sum(_weight(w, ops[u]) for u, nd in dag.nodes.items() if nd.child)
+    wmax = max(wt.values())
+    for p in range(n):
+        Wp = sum(wt[t] for t in sel if parts[t] == p)
+        assert abs(n * Wp - W) <= n * wmax, (p, Wp, W, wmax)
+    # the assignment is the midpoint rule on these weights
+    P = 0
+    for t in sel:
+        assert parts[t] == min(n - 1, (n * (2 * P + wt[t])) // (2 * W))
+        P += wt[t]

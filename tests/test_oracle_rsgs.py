@@ -91,7 +91,7 @@ def test_greedy_chain_matches_brute_force(seed):
     dag = Dag(w)
     assert rsgs.tree_chain(dag) == _brute_chain(dag)
     order = rsgs.schedule(dag)
-    check_schedule(dag, order)
+    assert check_schedule(dag, order) == []
     assert sorted(order) == sorted(u for u, n in dag.nodes.items() if n.child)
 
 
@@ -109,4 +109,4 @@ def test_configs_valid():
     for w in (dags.config_c2(N=8, Lt=1), dags.config_c4(N=4, Lt=1, S=2, n_trees=300)):
         dag = Dag(w)
         order = rsgs.schedule(dag)
-        check_schedule(dag, order)
+        assert check_schedule(dag, order) == []

@@ -134,6 +134,57 @@ def test_correlator_sum_of_terms():
         np.testing.assert_allclose(corr[c], want, rtol=1e-15)
 
 
+def scaled_ones_scalars(w):
+    """Closed form for leaves c_u * J (J the all-ones matrix, c_u = scaled_ones_factor(u)):
+    MM1(xJ, yJ) = x y N J and TR_MM(xJ, yJ) = x y N^2 (sum of N^2 equal entries), so every node
+    is (scalar) * J and every root an integer; returns {node: scalar} in Python integers."""
+    nodes = {n[0]: n for n in w.nodes}
+    memo = {}
+
+    def sc(u):
+        if u not in memo:
+            (_, op, a, b, _) = nodes[u]
+            if op == dags.LEAF_M:
+                memo[u] = scaled_ones_factor(u)
+            elif op == dags.MM1:
+                memo[u] = sc(a) * sc(b) * w.N
+            elif op == dags.TR_MM:
+                memo[u] = sc(a) * sc(b) * w.N * w.N
+            else:
+                raise ValueError(op)
+        return memo[u]
+    return {u: sc(u) for u in nodes}
+
+
+def scaled_ones_factor(u):
+    return (u % 5) - 2 or 3          # small nonzero integers of both signs
+
+
+def test_correlator_closed_form_scaled_ones():
+    """Pins values.correlators (and the MM1 / TR_MM chain) against exact integers: with leaves
+    c_u J every root is an integer (scaled_ones_scalars) and, with Gaussian-integer coefficients,
+    every correlator entry C_c[t] = sum over c's terms of coef * root is an exact Gaussian integer
+    (P:54), summed here in Python integers from the DAG structure alone."""
+    N, Lt = 6, 3
+    w = dags.config_c2(N=N, Lt=Lt, n_loop4=40, n_loop2=5, n_corr=4, coefs="complex")
+    assert any(im != 0 for (_, _, _, im) in w.terms)
+    dag = Dag(w)
+    sc = scaled_ones_scalars(w)
+    roots = values.evaluate(dag, lambda u: scaled_ones_factor(u) * np.ones((Lt, N, N), complex))
+    corr = values.correlators(dag, roots)
+    root_of = dict(w.trees)
+    want = {}
+    for (c, t, re, im) in w.terms:
+        r = sc[root_of[t]]
+        pre, pim = want.get(c, (0, 0))
+        want[c] = (pre + int(re) * r, pim + int(im) * r)
+    assert set(corr) == set(want)
+    for c, (re, im) in want.items():
+        np.testing.assert_array_equal(corr[c], np.full(Lt, complex(re, im)))
+    for t, r in root_of.items():
+        np.testing.assert_array_equal(roots[t], np.full(Lt, complex(sc[r], 0)))
+
+
 def test_generator_phase_bound_and_determinism():
     v = srng.leaf_values(1, 7, 0, 4096, 0.5, srng.MODE_PHASE_LIMITED)
     assert np.all(np.abs(np.angle(v)) <= np.arctan(0.125 / 0.75) + 1e-15)
