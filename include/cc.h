@@ -106,7 +106,9 @@ typedef struct {
   double kernel_seconds;      /* sum of contraction-kernel durations (0 unless profiled)    */
   double flops;               /* algorithmic flops: MM1 8LtN^3, BM1/BB2 8LtSN^4, TR 8LtN^2   */
   double hbm_bytes;           /* algorithmic HBM bytes of the kernels                       */
-  int64_t h2d_bytes, d2h_bytes; /* bytes actually copied (device-resident leaves: 0)         */
+  int64_t h2d_bytes, d2h_bytes; /* bytes copied, counted as the executor enqueues each copy (a
+                                   dropped or duplicated copy shows here; the plan's own counts
+                                   are cc_plan_stats; device-resident leaves: 0)           */
   int64_t n_kernels;          /* kernel launches issued by this execute                     */
   double copy_seconds;        /* start -> last H2D/D2H copy done (blocking stream-mode
                                  dataflow execute with copies; else 0)                     */

@@ -112,6 +112,7 @@ void enqueue_copy(cc_ctx* ctx, cudaStream_t s, const void* src, void* dst, size_
     const size_t t1 = chunks == 1 ? 0 : size_t(int64_t(ch + 1) * g.Lt / chunks);
     const size_t off = t0 * per_t, len = chunks == 1 ? bytes : (t1 - t0) * per_t;
     ck(cudaMemcpyAsync(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len, kind, s), "copy");
+    ctx->count_copy(kind == cudaMemcpyHostToDevice, int64_t(len));
     if (df_write_fn()(s, reinterpret_cast<CUdeviceptr>(ctx->df_sync + flag_slot), cuuint32_t(ch + 1), 0) != CUDA_SUCCESS)
       throw Error(CC_E_CUDA, "cuStreamWriteValue32 failed");
   }

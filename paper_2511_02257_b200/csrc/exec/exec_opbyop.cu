@@ -132,9 +132,11 @@ int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cud
           src = ctx->host_pool + op.host_off;
         }
         ck(cudaMemcpyAsync(ctx->arena + op.dev_off, src, size_t(op.bytes), cudaMemcpyHostToDevice, s), "H2D");
+        ctx->count_copy(true, op.bytes);
         break;
       }
       case OP_D2H:
+        ctx->count_copy(false, op.bytes);
         ck(cudaMemcpyAsync(ctx->host_pool + op.host_off, ctx->arena + op.dev_off, size_t(op.bytes),
                            cudaMemcpyDeviceToHost, s),
            "D2H");

@@ -19,6 +19,7 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   // land in scratch or outside the arena; if preparation fails, the compute stream is ordered
   // after the stray copies before the error returns.
   ctx->pre_n = 0;
+  ctx->run_h2d = ctx->run_d2h = 0;
   std::vector<int64_t> pre_off;
   if (ctx->opt.precopy && ctx->opt.early_copies && ctx->opt.h2d_chunk_bytes == 0 && !ctx->phys_valid &&
       !ctx->dag->abstract && !(flags & (2 | 4 | 8 | 16 | 64 | 128))) {
@@ -42,6 +43,7 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
       const int64_t per_t = n0.op == CC_LEAF_M ? per_t_m : per_t_m * g0.S * g0.N;
       const char* src = static_cast<const char*>(ctx->leaf_host[size_t(u)]) + int64_t(ctx->t0) * per_t;
       ck(cudaMemcpyAsync(ctx->arena + off, src, size_t(n0.size), cudaMemcpyHostToDevice, ctx->hs), "H2D");
+      ctx->count_copy(true, n0.size);
       pre_off.push_back(off);
       off += round_up(n0.size, ALIGN);
     }
@@ -140,6 +142,11 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
       ck(cudaStreamEndCapture(ctx->cs, &graph), "graph capture");
       ck(cudaGraphInstantiate(&ctx->gexec, graph, 0), "graph instantiate");
       cudaGraphDestroy(graph);
+      ctx->graph_h2d = ctx->run_h2d;     // the copies the graph carries
+      ctx->graph_d2h = ctx->run_d2h;
+    } else {
+      ctx->run_h2d = ctx->graph_h2d;
+      ctx->run_d2h = ctx->graph_d2h;
     }
     ck(cudaGraphLaunch(ctx->gexec, ctx->cs), "graph launch");
   } else {
@@ -170,8 +177,8 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
         stats->flops += node_flops(g.nodes[size_t(op.node)], g.Lt, g.N, g.S);
         stats->hbm_bytes += node_hbm_bytes(g.nodes[size_t(op.node)], g.Lt, g.N, g.S);
       }
-    stats->h2d_bytes = ctx->pp.h2d_bytes;
-    stats->d2h_bytes = ctx->pp.d2h_bytes;
+    stats->h2d_bytes = ctx->run_h2d;      // counted as enqueued (the plan's: cc_plan_stats)
+    stats->d2h_bytes = ctx->run_d2h;
     stats->n_kernels = ctx->last_n_kernels;
   }
   ctx->ktimes = KindTimes{};

@@ -135,6 +135,11 @@ struct cc_ctx {
   bool executed = false;
   KindTimes ktimes;
   int64_t last_n_kernels = 0;
+  // plan copies counted as they are enqueued (cc_exec_stats h2d/d2h: runtime counts, not the
+  // plan's): the current execute's, and those baked into each cached graph
+  int64_t run_h2d = 0, run_d2h = 0;
+  int64_t graph_h2d = 0, graph_d2h = 0;   // gexec (op-by-op graph)
+  void count_copy(bool h2d, int64_t bytes) { (h2d ? run_h2d : run_d2h) += bytes; }
 
   // dataflow execution (persistent workers): device metadata + per-launch sync area
   bool df_valid = false;

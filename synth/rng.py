@@ -2,8 +2,8 @@
 
 This module is INPUT GENERATION ONLY: it holds none of the method's arithmetic
 (no contraction, no schedule, no memory model).  The CUDA library carries an
-independent implementation of the same generator (csrc/kernels/synth_fill.cu,
-entry point `cc_fill_synthetic`); a GPU test checks the two bit for bit.  The
+independent implementation of the same generator (csrc/kernels/trace.cu,
+`fill_synthetic_kernel`, entry point `cc_fill_synthetic`); a GPU test checks the two bit for bit.  The
 recipe is DESIGN.md §"Input recipe":
 
   key(seed, leaf)   = splitmix64(splitmix64(seed) XOR leaf)
@@ -84,3 +84,21 @@ def leaf_tensor(seed, leaf_id, shape, sigma, mode=MODE_PHASE_LIMITED, t_range=No
     t0, t1 = (0, shape[0]) if t_range is None else t_range
     vals = leaf_values(seed, leaf_id, t0 * per_t, (t1 - t0) * per_t, sigma, mode)
     return vals.reshape((t1 - t0,) + tuple(shape[1:]))
+
+
+def leaf_values_into(out, seed, leaf_id, e0, sigma, mode=MODE_PHASE_LIMITED, chunk=1 << 22, workers=None):
+    """leaf_values(seed, leaf_id, e0, out.size, sigma, mode) written into the complex128 array
+    `out` in chunks on a thread pool (numpy releases the GIL in its loops): the same values,
+    for multi-GiB leaves at full config sizes."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    flat = out.reshape(-1)
+    n = flat.size
+    workers = workers or max(1, min(32, len(os.sched_getaffinity(0))))
+
+    def work(a):
+        b = min(n, a + chunk)
+        flat[a:b] = leaf_values(seed, leaf_id, e0 + a, b - a, sigma, mode)
+    with ThreadPoolExecutor(workers) as ex:
+        list(ex.map(work, range(0, n, chunk)))
+    return out

@@ -49,6 +49,11 @@ def run_gpu(w, algo=None, cap=0, flags=0, device_leaves=False, arena_mb=256, lea
         if n.child:
             continue
         v = leaf_fn(u, n.op) if leaf_fn else values.synthetic_leaf(w, u, n.op)
+        if hasattr(v, "data_ptr"):          # a ready pinned host tensor of the full leaf
+            assert not device_leaves and part is None
+            keep.append(v)
+            ctx.set_leaf(u, v)
+            continue
         if device_leaves:
             d = device_from(v[t0:t0 + Lt_part])
             keep.append(d)
