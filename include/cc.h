@@ -47,18 +47,27 @@ typedef enum {
   CC_E_NOMEM = -12            /* arena / host allocation failed                       */
 } cc_status;
 
-/* Node kinds.  Index semantics (reading V-1):
- *   CC_MM1   (meson A, meson B)   C[t,i,k]     = sum_j A[t,i,j] B[t,j,k]          O(N^3)
- *   CC_BM1   (baryon A, meson M)  C[t,s,i,j,l] = sum_k A[t,s,i,j,k] M[t,k,l]      O(N^4)
- *   CC_BB2   (baryon A, baryon B) C[t,i,l]     = sum_s sum_{j,k} A[t,s,i,j,k] B[t,s,j,k,l]
- *   CC_TR_MM (meson A, meson B)   c[t]         = sum_{i,j} A[t,i,j] B[t,j,i]   (root only:
+/* Node kinds.  Index semantics (readings V-1 and T4-1..T4-4; P:120, P:806-813,
+ * P:867):
+ *   CC_MM1   (meson A, meson B)   C[t,i,k]       = sum_j A[t,i,j] B[t,j,k]          O(N^3)
+ *   CC_BM1   (baryon A, meson M)  C[t,s,i,j,l]   = sum_k A[t,s,i,j,k] M[t,k,l]      O(N^4)
+ *   CC_BB2   (baryon A, baryon B) C[t,i,l]       = sum_s sum_{j,k} A[t,s,i,j,k] B[t,s,j,k,l]
+ *   CC_TR_MM (meson A, meson B)   c[t]           = sum_{i,j} A[t,i,j] B[t,j,i]   (root only:
  *                                  "contract all")
+ *   BxBxB (tritium class, Table II P:813 O(N^5); sizes O(N^2)/O(N^3)/O(N^4)):
+ *   CC_BB1   (baryon A, baryon B) T[t,i,j,l,m]   = sum_s sum_k A[t,s,i,j,k] B[t,s,k,l,m]
+ *                                  -> tetraquark node [Lt][N][N][N][N], O(S N^5)
+ *   CC_BT2   (baryon A, tetra X)  C[t,s,m,i,j]   = sum_{k,l} A[t,s,m,k,l] X[t,k,l,i,j]
+ *                                  -> baryon node, O(S N^5)
+ *   CC_BB3   (baryon A, baryon B) c[t]           = sum_s sum_{i,j,k} A[t,s,i,j,k] B[t,s,k,j,i]
+ *                                  (root only: baryon x baryon "contract all", O(S N^3))
  * CC_LEAF_X / CC_OP_X are abstract nodes of explicit size for scheduling-only DAGs
  * (e.g. Table I); a DAG containing them can be scheduled/planned, not executed. */
 typedef enum {
   CC_LEAF_M = 0, CC_LEAF_B = 1, CC_MM1 = 2, CC_BM1 = 3, CC_BB2 = 4, CC_TR_MM = 5,
-  CC_LEAF_X = 6, CC_OP_X = 7
+  CC_LEAF_X = 6, CC_OP_X = 7, CC_BB1 = 8, CC_BT2 = 9, CC_BB3 = 10
 } cc_op;
+#define CC_N_OPS 11
 
 typedef struct { int32_t Lt, N, S; } cc_dims;
 
@@ -229,7 +238,7 @@ cc_status cc_get_options(cc_ctx* ctx, cc_options* out);
 cc_status cc_set_options(cc_ctx* ctx, const cc_options* opt);
 
 /* Per-kind contraction-kernel time of the last cc_execute with flags bit 1 (kernels timed
- * with CUDA events on the compute stream): seconds[op], counts[op] for op = cc_op (8 each). */
+ * with CUDA events on the compute stream): seconds[op], counts[op] for op = cc_op (CC_N_OPS each). */
 cc_status cc_kernel_times(cc_ctx* ctx, double* seconds, int64_t* counts);
 
 /* Progress of the dataflow executor (diagnostics; readable while a replay runs): out[0], out[1]
@@ -264,6 +273,11 @@ cc_status cc_mm1(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt,
 cc_status cc_bm1(cc_ctx* ctx, const void* A, const void* M, void* C, int32_t Lt, int32_t N, int32_t S);
 cc_status cc_bb2(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt, int32_t N, int32_t S);
 cc_status cc_tr_mm(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t Lt, int32_t N);
+/* BxBxB kinds alone (FP64 DMMA; layouts of the CC_BB1 / CC_BT2 / CC_BB3 definitions above):
+ * A, B baryon [Lt][S][N][N][N]; T tetra [Lt][N][N][N][N]; C baryon; c [Lt]. */
+cc_status cc_bb1(cc_ctx* ctx, const void* A, const void* B, void* T, int32_t Lt, int32_t N, int32_t S);
+cc_status cc_bt2(cc_ctx* ctx, const void* A, const void* X, void* C, int32_t Lt, int32_t N, int32_t S);
+cc_status cc_bb3(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t Lt, int32_t N, int32_t S);
 /* MM1 on the tcgen05 INT8 tensor cores by Ozaki splitting (DESIGN reading
  * V-6).  Same operation and layouts as cc_mm1 (C[t,i,k] = sum_j A[t,i,j] B[t,j,k], complex128
  * interleaved, [Lt][N][N], device pointers).  Each operand is scaled per row (A) / column (B)

@@ -7,12 +7,15 @@ Node fields follow P:162-183: child (ordered left/right), parents, type in
 {LEAF, INTERIOR, ROOT} by degree, size.  A tree is the
 closure of its root under operands (DESIGN reading T-5: trees are closed).
 """
-from synth.dags import LEAF_M, LEAF_B, MM1, BM1, BB2, TR_MM, LEAF_X, OP_X, LEAF_OPS
+from synth.dags import LEAF_M, LEAF_B, MM1, BM1, BB2, TR_MM, LEAF_X, OP_X, BB1, BT2, BB3, N_OPS, LEAF_OPS
 
 LEAF, INTERIOR, ROOT = "LEAF", "INTERIOR", "ROOT"
 
 MESON_KINDS = (LEAF_M, MM1, BB2)
-BARYON_KINDS = (LEAF_B, BM1)
+BARYON_KINDS = (LEAF_B, BM1, BT2)
+TETRA_KINDS = (BB1,)                     # reading T4-1: [Lt, N, N, N, N], no spin index
+CONTRACT_ALL = (TR_MM, BB3)              # root-only kinds ("contract all", P:867)
+GEMM_KINDS = (MM1, BM1, BB2, BB1, BT2)   # interior kinds ("exterior contract", P:867)
 
 
 class OracleError(Exception):
@@ -50,12 +53,16 @@ class Node:
 
 def tensor_size(op, Lt, N, S):
     """Bytes of the tensor a node of kind `op` holds (complex128 = 16 B):
-    meson [Lt,N,N], baryon [Lt,S,N,N,N], TR_MM root [Lt] scalars (P:59 pins 16 B/element)."""
+    meson [Lt,N,N], baryon [Lt,S,N,N,N], tetra [Lt,N,N,N,N] (reading T4-1; the O(N^2) /
+    O(N^3) / O(N^4) size classes of P:871-872), contract-all root [Lt] scalars (P:59 pins 16
+    B/element)."""
     if op in MESON_KINDS:
         return 16 * Lt * N * N
     if op in BARYON_KINDS:
         return 16 * Lt * S * N ** 3
-    if op == TR_MM:
+    if op in TETRA_KINDS:
+        return 16 * Lt * N ** 4
+    if op in CONTRACT_ALL:
         return 16 * Lt
     raise OracleError("abstract node needs an explicit size")
 
@@ -69,7 +76,7 @@ class Dag:
         for (nid, op, a, b, size) in w.nodes:
             if nid in self.nodes:
                 raise InconsistentError("duplicate node id %d" % nid)
-            if op not in range(8):
+            if op not in range(N_OPS):
                 raise OracleError("bad op %r" % (op,))
             abstract = op in (LEAF_X, OP_X)
             if abstract:
@@ -166,7 +173,9 @@ class Dag:
         return order
 
     def _check_shapes(self):
-        """Operand kinds per DESIGN reading V-1: MM1(M,M) BM1(B,M) BB2(B,B) TR_MM(M,M), TR_MM only as root."""
+        """Operand kinds per DESIGN readings V-1, T4-1..T4-3: MM1(M,M) BM1(B,M) BB2(B,B) TR_MM(M,M)
+        BB1(B,B) BT2(B,T) BB3(B,B); the contract-all kinds (TR_MM, BB3) only as roots, the others
+        never as roots."""
         for v in self.nodes.values():
             if v.op in LEAF_OPS:
                 continue
@@ -177,16 +186,18 @@ class Dag:
                 ok = all(k in MESON_KINDS for k in kinds)
             elif v.op == BM1:
                 ok = kinds[0] in BARYON_KINDS and kinds[1] in MESON_KINDS
-            elif v.op == BB2:
+            elif v.op in (BB2, BB1, BB3):
                 ok = all(k in BARYON_KINDS for k in kinds)
+            elif v.op == BT2:
+                ok = kinds[0] in BARYON_KINDS and kinds[1] in TETRA_KINDS
             else:
                 ok = False
             if not ok:
                 raise InconsistentError("node %d: operand kinds %r do not fit op %d" % (v.id, kinds, v.op))
-            if v.op == TR_MM and v.parents:
-                raise InconsistentError("TR_MM node %d must be a root" % v.id)
-            if v.op in (MM1, BM1, BB2) and not v.parents:
-                raise InconsistentError("root %d must be a TR_MM (contract-all)" % v.id)
+            if v.op in CONTRACT_ALL and v.parents:
+                raise InconsistentError("contract-all node %d must be a root" % v.id)
+            if v.op in GEMM_KINDS and not v.parents:
+                raise InconsistentError("root %d must be a contract-all (TR_MM / BB3)" % v.id)
 
     def _ranks(self):
         """Eq. (1): rank(leaf)=0, else 1 + max child rank."""

@@ -3,11 +3,12 @@ work).  TEST INFRASTRUCTURE (see oracle/__init__.py).
 
 TIME: part p of n owns time slices [p*Lt//n, (p+1)*Lt//n) — every op is per-slice.
 TREES: trees in tree-scheduler selection order (O4); tree weight = flops/8 of the
-contractions first executed while processing it (MM1 Lt N^3, BM1/BB2 Lt S N^4, TR Lt N^2;
+contractions first executed while processing it (MM1 Lt N^3, BM1/BB2 Lt S N^4, TR Lt N^2,
+BB1/BT2 Lt S N^5, BB3 Lt S N^3;
 abstract DAGs: 1 per contraction); tree i with prefix weight P_i, weight w_i, total W goes
 to part min(n-1, floor(n (2 P_i + w_i) / (2 W))).
 """
-from synth.dags import MM1, BM1, BB2, TR_MM, Workload
+from synth.dags import MM1, BM1, BB2, TR_MM, BB1, BT2, BB3, Workload
 from .dag import Dag
 from . import tree as tree_sched
 
@@ -24,6 +25,10 @@ def _weight(dag, u):
         return dag.Lt * dag.S * dag.N ** 4
     if n.op == TR_MM:
         return dag.Lt * dag.N ** 2
+    if n.op in (BB1, BT2):
+        return dag.Lt * dag.S * dag.N ** 5
+    if n.op == BB3:
+        return dag.Lt * dag.S * dag.N ** 3
     return 1
 
 

@@ -12,12 +12,16 @@ DESIGN.md): "exterior contract" for interior nodes and "contract all" for roots
   TR_MM(A,B)[t]       = sum_{i,j} A[t,i,j] B[t,j,i]              (contract all)
 Correlator (reading V-2): C_c[t] = sum over terms (c, T, coef) of coef * root_T[t],
 summed in term input order.
+BxBxB kinds (tritium class, Table II O(N^5) P:813; size classes P:871-872; readings T4-1..T4-4):
+  BB1(A,B)[t,i,j,l,m] = sum_s sum_k A[t,s,i,j,k] B[t,s,k,l,m]      (baryon x baryon -> tetra)
+  BT2(A,X)[t,s,m,i,j] = sum_{k,l} A[t,s,m,k,l] X[t,k,l,i,j]        (baryon x tetra -> baryon)
+  BB3(A,B)[t]         = sum_s sum_{i,j,k} A[t,s,i,j,k] B[t,s,k,j,i] (baryon x baryon contract all)
 Precision: complex128 throughout (P:59 pins 16 B per element; reading V-3).
 """
 import numpy as np
 
 from synth import rng as srng
-from synth.dags import LEAF_M, LEAF_B, MM1, BM1, BB2, TR_MM
+from synth.dags import LEAF_M, LEAF_B, MM1, BM1, BB2, TR_MM, BB1, BT2, BB3
 
 
 def mm1(A, B):
@@ -42,7 +46,25 @@ def tr_mm(A, B):
     return (A * np.swapaxes(B, 1, 2)).sum(axis=(1, 2))
 
 
-KERNELS = {MM1: mm1, BM1: bm1, BB2: bb2, TR_MM: tr_mm}
+def bb1(A, B):
+    Lt, S, N = A.shape[0], A.shape[1], A.shape[2]
+    T = np.zeros((Lt, N * N, N * N), dtype=np.complex128)
+    for s in range(S):                       # sum over the spin index s
+        T += np.matmul(A[:, s].reshape(Lt, N * N, N), B[:, s].reshape(Lt, N, N * N))
+    return T.reshape(Lt, N, N, N, N)
+
+
+def bt2(A, X):
+    Lt, S, N = A.shape[0], A.shape[1], A.shape[2]
+    C = np.matmul(A.reshape(Lt, S * N, N * N), X.reshape(Lt, N * N, N * N))
+    return C.reshape(Lt, S, N, N, N)
+
+
+def bb3(A, B):
+    return (A * np.transpose(B, (0, 1, 4, 3, 2))).sum(axis=(1, 2, 3, 4))
+
+
+KERNELS = {MM1: mm1, BM1: bm1, BB2: bb2, TR_MM: tr_mm, BB1: bb1, BT2: bt2, BB3: bb3}
 
 
 def leaf_shape(op, Lt, N, S):

@@ -20,7 +20,8 @@ c_i32, c_i64, c_u64, c_dbl, c_void_p, c_size_t = (ctypes.c_int32, ctypes.c_int64
                                                   ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t)
 P = ctypes.POINTER
 
-CC_LEAF_M, CC_LEAF_B, CC_MM1, CC_BM1, CC_BB2, CC_TR_MM, CC_LEAF_X, CC_OP_X = range(8)
+CC_LEAF_M, CC_LEAF_B, CC_MM1, CC_BM1, CC_BB2, CC_TR_MM, CC_LEAF_X, CC_OP_X, CC_BB1, CC_BT2, CC_BB3 = range(11)
+CC_N_OPS = 11
 CC_SIBLING, CC_TREE, CC_GIVEN, CC_RSGS = range(4)
 PART_TIME, PART_TREES = 0, 1
 EXEC_GRAPH, EXEC_TIME_KERNELS, EXEC_ONLY_GEMM, EXEC_ONLY_TRACE, EXEC_OP_BY_OP, EXEC_PROFILE = 1, 2, 4, 8, 16, 32
@@ -121,6 +122,9 @@ _sig("cc_mm1", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32)
 _sig("cc_bm1", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32)
 _sig("cc_bb2", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32)
 _sig("cc_tr_mm", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32)
+_sig("cc_bb1", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32)
+_sig("cc_bt2", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32)
+_sig("cc_bb3", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32)
 _sig("cc_mm1_ozaki", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, c_void_p, ctypes.c_size_t)
 _sig("cc_mm1_ozaki_workspace_bytes", c_i32, c_i32, c_i32, res=ctypes.c_size_t)
 _sig("cc_i8gemm_tn", c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32)
@@ -133,7 +137,7 @@ EXPORTED = ["cc_create", "cc_destroy", "cc_last_error", "cc_version", "cc_load_d
             "cc_dag_info", "cc_part_time_range", "cc_correlators", "cc_partition", "cc_part_trees", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
             "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_execute",
             "cc_execute_async", "cc_get_options", "cc_set_options", "cc_kernel_times", "cc_dataflow_state", "cc_dataflow_profile", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
-            "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_mm1_ozaki", "cc_mm1_ozaki_workspace_bytes", "cc_i8gemm_tn", "cc_gemm_ozaki",
+            "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_bb1", "cc_bt2", "cc_bb3", "cc_mm1_ozaki", "cc_mm1_ozaki_workspace_bytes", "cc_i8gemm_tn", "cc_gemm_ozaki",
             "cc_gemm_ozaki_workspace_bytes", "cc_fill_synthetic", "cc_scratch_bytes"]
 
 
@@ -326,8 +330,8 @@ class Context:
         self._ck(_lib.cc_set_options(self._h, ctypes.byref(o)))
 
     def kernel_times(self):
-        s = (c_dbl * 8)()
-        c = (c_i64 * 8)()
+        s = (c_dbl * CC_N_OPS)()
+        c = (c_i64 * CC_N_OPS)()
         self._ck(_lib.cc_kernel_times(self._h, s, c))
         return list(s), list(c)
 
@@ -411,6 +415,15 @@ class Context:
 
     def tr_mm(self, A, B, c, Lt, N):
         self._ck(_lib.cc_tr_mm(self._h, _ptr(A), _ptr(B), _ptr(c), Lt, N))
+
+    def bb1(self, A, B, T, Lt, N, S):
+        self._ck(_lib.cc_bb1(self._h, _ptr(A), _ptr(B), _ptr(T), Lt, N, S))
+
+    def bt2(self, A, X, C, Lt, N, S):
+        self._ck(_lib.cc_bt2(self._h, _ptr(A), _ptr(X), _ptr(C), Lt, N, S))
+
+    def bb3(self, A, B, c, Lt, N, S):
+        self._ck(_lib.cc_bb3(self._h, _ptr(A), _ptr(B), _ptr(c), Lt, N, S))
 
     def fill_synthetic(self, dev, n, seed, leaf_id, e0, mode, sigma):
         self._ck(_lib.cc_fill_synthetic(self._h, _ptr(dev), n, seed, leaf_id, e0, mode, sigma))

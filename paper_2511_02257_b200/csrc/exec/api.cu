@@ -482,7 +482,7 @@ cc_status cc_dataflow_profile(cc_ctx* ctx, uint64_t* out, int64_t cap, int64_t* 
 cc_status cc_kernel_times(cc_ctx* ctx, double* seconds, int64_t* counts) {
   if (!ctx) return CC_E_INVAL;
   API_BEGIN
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < CC_N_OPS; ++k) {
     if (seconds) seconds[k] = ctx->ktimes.seconds[k];
     if (counts) counts[k] = ctx->ktimes.count[k];
   }
@@ -513,20 +513,38 @@ cc_status cc_bb2(cc_ctx* ctx, const void* A, const void* B, void* C, int32_t Lt,
   if (!ctx) return CC_E_INVAL;
   return direct_gemm(ctx, CC_BB2, A, B, C, Lt, N, S);
 }
-cc_status cc_tr_mm(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t Lt, int32_t N) {
-  if (!ctx) return CC_E_INVAL;
+static cc_status direct_trace(cc_ctx* ctx, int op, const void* A, const void* B, void* c, int32_t Lt, int32_t N,
+                              int32_t S) {
   API_BEGIN
   ctx->need_device();
-  if (!A || !B || !c || Lt <= 0 || N <= 0) throw Error(CC_E_INVAL, "bad kernel arguments");
-  ensure_ws(ctx->direct_tr_ws, ctx->direct_tr_ws_bytes, trace_workspace_bytes(Lt, N));
+  if (!A || !B || !c || Lt <= 0 || N <= 0 || S <= 0) throw Error(CC_E_INVAL, "bad kernel arguments");
+  const TraceShape sh = trace_shape(op, N, S);
+  ensure_ws(ctx->direct_tr_ws, ctx->direct_tr_ws_bytes, trace_workspace_bytes(Lt, sh));
   // counters must be zero; a previous direct call with another Lt may have left partials there
-  ck(cudaMemsetAsync(ctx->direct_tr_ws, 0, size_t(Lt) * 4, ctx->cs), "memset");
-  ck(launch_trace(A, B, c, Lt, N, ctx->direct_tr_ws, ctx->cs), "TR_MM kernel");
+  ck(cudaMemsetAsync(ctx->direct_tr_ws, 0, size_t(Lt) * 4 * 32, ctx->cs), "memset");
+  ck(launch_trace(A, B, c, Lt, sh, ctx->direct_tr_ws, ctx->cs), "contract-all kernel");
   API_END
 }
 
+cc_status cc_tr_mm(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t Lt, int32_t N) {
+  if (!ctx) return CC_E_INVAL;
+  return direct_trace(ctx, CC_TR_MM, A, B, c, Lt, N, 1);
+}
+cc_status cc_bb1(cc_ctx* ctx, const void* A, const void* B, void* T, int32_t Lt, int32_t N, int32_t S) {
+  if (!ctx) return CC_E_INVAL;
+  return direct_gemm(ctx, CC_BB1, A, B, T, Lt, N, S);
+}
+cc_status cc_bt2(cc_ctx* ctx, const void* A, const void* X, void* C, int32_t Lt, int32_t N, int32_t S) {
+  if (!ctx) return CC_E_INVAL;
+  return direct_gemm(ctx, CC_BT2, A, X, C, Lt, N, S);
+}
+cc_status cc_bb3(cc_ctx* ctx, const void* A, const void* B, void* c, int32_t Lt, int32_t N, int32_t S) {
+  if (!ctx) return CC_E_INVAL;
+  return direct_trace(ctx, CC_BB3, A, B, c, Lt, N, S);
+}
+
 size_t cc_gemm_ozaki_workspace_bytes(int32_t op, int32_t Lt, int32_t N, int32_t S, int32_t n_slices) {
-  if ((op != CC_MM1 && op != CC_BM1 && op != CC_BB2) || Lt <= 0 || N <= 0 || S <= 0 || n_slices < 4 || n_slices > 7)
+  if (!is_gemm_kind(op) || Lt <= 0 || N <= 0 || S <= 0 || n_slices < 4 || n_slices > 7)
     return 0;
   return ozaki_workspace_bytes(problem_for(op, Lt, N, op == CC_MM1 ? 1 : S, nullptr, nullptr, nullptr), n_slices, Lt);
 }
@@ -536,7 +554,7 @@ cc_status cc_gemm_ozaki(cc_ctx* ctx, int32_t op, const void* A, const void* B, v
   if (!ctx) return CC_E_INVAL;
   API_BEGIN
   ctx->need_device();
-  if ((op != CC_MM1 && op != CC_BM1 && op != CC_BB2) || !A || !B || !C || !workspace || Lt <= 0 || N <= 0 || S <= 0 ||
+  if (!is_gemm_kind(op) || !A || !B || !C || !workspace || Lt <= 0 || N <= 0 || S <= 0 ||
       n_slices < 4 || n_slices > 7)
     throw Error(CC_E_INVAL, "bad kernel arguments");
   const ZgemmProblem q = problem_for(op, Lt, N, op == CC_MM1 ? 1 : S, A, B, C);
@@ -586,9 +604,11 @@ cc_status cc_fill_synthetic(cc_ctx* ctx, void* dev, int64_t n, uint64_t seed, in
 size_t cc_scratch_bytes(int32_t Lt, int32_t N, int32_t S) {
   // upper bound of prepare_phys's scratch for DAGs with up to 2^16 trees/terms/correlators
   size_t ws = 0;
-  for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)})
+  for (int op : GEMM_OPS)
     ws = std::max(ws, zgemm_workspace_bytes(problem_for(op, Lt, N, S, nullptr, nullptr, nullptr), 148));
-  return ws + trace_workspace_bytes(Lt, N) + size_t(Lt) * 16 * 3 * 65536 + (size_t(16) << 20);
+  size_t tws = 0;
+  for (int op : TRACE_OPS) tws = std::max(tws, trace_workspace_bytes(Lt, trace_shape(op, N, S)));
+  return ws + tws + size_t(Lt) * 16 * 3 * 65536 + (size_t(16) << 20);
 }
 
 }  // extern "C"

@@ -419,8 +419,9 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     DfOp d{};
     d.sync_id = slot[size_t(i)];
     d.slice_sync = -1;
-    if (n.op == CC_TR_MM) {
-      const int64_t P = df_trace_pieces(Lt, N);
+    if (is_root_kind(n.op)) {
+      const TraceShape sh = trace_shape(n.op, N, g.S);
+      const int64_t P = df_trace_pieces(sh);
       d.kind = 1;
       d.n_items = int32_t(Lt * P);
       d.first_item = g_items;
@@ -431,11 +432,15 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
       d.Lt = Lt;
       d.nb = int32_t((N + 31) / 32);
       d.P = int32_t(P);
+      d.tr_G = sh.G;
+      d.tr_Gj = n.op == CC_BB3 ? sh.Gj : 0;
+      d.tr_S = n.op == CC_BB3 ? int32_t(g.S) : 1;
       // partial slots (P > 1) come from a ring assigned in queue order below
       d.tmap = int32_t(tmaps.size() / 256);
       tmaps.resize(tmaps.size() + 256);
-      if (!df_encode_trace_maps(tmaps.data() + size_t(d.tmap) * 256, a, b, Lt, N))
-        throw Error(CC_E_CUDA, "TMA descriptor encoding failed");
+      const bool ok = n.op == CC_BB3 ? df_encode_bb3_maps(tmaps.data() + size_t(d.tmap) * 256, a, b, Lt, N, g.S)
+                                     : df_encode_trace_maps(tmaps.data() + size_t(d.tmap) * 256, a, b, Lt, N);
+      if (!ok) throw Error(CC_E_CUDA, "TMA descriptor encoding failed");
       g_items += d.n_items;
       df_index[size_t(i)] = int32_t(gops.size());
       gops.push_back(d);
@@ -538,7 +543,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     // priority: inputs' availability first (copy issue order), then plan rank (+ the TR delay)
     auto key = [&](int32_t i) {
       const PhysOp& op = ops[size_t(i)];
-      const bool tr = op.kind == OP_CONTRACT && g.nodes[size_t(op.node)].op == CC_TR_MM;
+      const bool tr = op.kind == OP_CONTRACT && is_root_kind(g.nodes[size_t(op.node)].op);
       return avail[size_t(i)] * (int64_t(n_ops) + delay + 1) + int64_t(rank[size_t(i)]) + (tr ? delay : 0);
     };
     std::priority_queue<std::pair<int64_t, int32_t>, std::vector<std::pair<int64_t, int32_t>>, std::greater<>> ready;
@@ -786,7 +791,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     // 4.62 ms); opt.tr_ratio > 0 overrides
     double g_st = 0, t_st = 0;
     for (const auto& o : gops) g_st += double(o.n_items / std::max(o.n_chunks, 1)) * o.KT;
-    for (const auto& o : tops) t_st += double(o.Lt) * o.nb * o.nb;
+    for (const auto& o : tops) t_st += double(o.Lt) * o.tr_G * o.nb * o.nb;
     const double auto_ratio = g_st > 0 && t_st > 0 ? std::min(std::max(1.12 * t_st / g_st, 0.25), 8.0) : 2.0;
     const double ratio = ctx->opt.tr_ratio > 0 ? ctx->opt.tr_ratio : auto_ratio;
     da.tr_ratio8 = std::min(std::max(int(std::lround(ratio * 8.0)), 1), 512);

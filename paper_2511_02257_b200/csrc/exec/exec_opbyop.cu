@@ -6,10 +6,10 @@ namespace ccx {
 
 // Resets the Ozaki leaf-form cache for one execute (or one kernel-only capture): the free
 // pool range above the plan's high water, below any dataflow metadata / sync area placed at
-// the top of the pool.  CC_OZAKI_LEAF_CACHE=0 disables it.
+// the top of the pool.  Option ozaki_leaf_cache = 0 disables it.
 void oz_cache_reset(cc_ctx* ctx) {
   const size_t n = ctx->dag->nodes.size();
-  for (int k = 0; k < 6; ++k) {
+  for (int k = 0; k < 2 * OZ_KINDS; ++k) {
     ctx->oz.form[k].assign(n, OzakiForm{nullptr, nullptr});
     ctx->oz.have[k].assign(n, 0);
   }
@@ -46,8 +46,9 @@ const OzakiForm* oz_leaf_form(cc_ctx* ctx, int op, const ZgemmProblem& q, int32_
 void launch_contract(cc_ctx* ctx, const Node& n, const void* a, const void* b, void* out, int64_t root_slot,
                      int* nl) {
   const Dag& g = *ctx->dag;
-  if (n.op == CC_TR_MM) {
-    ck(launch_trace(a, b, ctx->roots + root_slot * g.Lt, g.Lt, g.N, ctx->trace_ws, ctx->cs), "TR_MM kernel");
+  if (is_root_kind(n.op)) {
+    ck(launch_trace(a, b, ctx->roots + root_slot * g.Lt, g.Lt, trace_shape(n.op, g.N, g.S), ctx->trace_ws, ctx->cs),
+       "contract-all kernel");
     ++*nl;
     return;
   }
@@ -77,6 +78,7 @@ int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cud
   ck(cudaStreamWaitEvent(ctx->ds, ctx->ev_start, 0), "wait");
   // consecutive TR_MM contractions share one batched trace launch; the batch is launched
   // before any other op is issued, and its source events right after
+  int tr_kind = CC_TR_MM;                 // kind of the pending batch
   std::vector<const void*> ta, tb;
   std::vector<void*> tout;
   std::vector<size_t> tops;
@@ -88,13 +90,14 @@ int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cud
       ck(cudaEventCreate(&e1), "event");
       ck(cudaEventRecord(e0, ctx->cs), "event");
     }
-    ck(launch_trace_batch(ta.data(), tb.data(), tout.data(), int(tops.size()), g.Lt, g.N, ctx->trace_ws, ctx->cs),
-       "TR_MM batch");
+    ck(launch_trace_batch(ta.data(), tb.data(), tout.data(), int(tops.size()), g.Lt, trace_shape(tr_kind, g.N, g.S),
+                          ctx->trace_ws, ctx->cs),
+       "contract-all batch");
     ++nl;
     if (time_kernels) {
       ck(cudaEventRecord(e1, ctx->cs), "event");
       kev->push_back({e0, e1});
-      kev_kind->push_back(CC_TR_MM);
+      kev_kind->push_back(tr_kind);
     }
     for (size_t k : tops)
       if (ctx->pp.ops[k].source) ck(cudaEventRecord(ctx->events[k], ctx->cs), "event");
@@ -106,8 +109,10 @@ int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cud
   for (size_t i = 0; i < ctx->pp.ops.size(); ++i) {
     const PhysOp& op = ctx->pp.ops[i];
     if (op.stream == S_NONE) continue;
-    if (op.kind == OP_CONTRACT && g.nodes[size_t(op.node)].op == CC_TR_MM) {
+    if (op.kind == OP_CONTRACT && is_root_kind(g.nodes[size_t(op.node)].op)) {
       const Node& n = g.nodes[size_t(op.node)];
+      if (!tops.empty() && n.op != tr_kind) flush_tr();   // a batch holds one shape
+      tr_kind = n.op;
       for (int32_t d : op.deps) ck(cudaStreamWaitEvent(ctx->cs, ctx->events[size_t(d)], 0), "wait");
       ta.push_back(op.loc_a == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.l)] : ctx->arena + op.off_a);
       tb.push_back(op.loc_b == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.r)] : ctx->arena + op.off_b);
@@ -190,7 +195,7 @@ void kernel_only(cc_ctx* ctx, int cls, cc_exec_stats* stats) {
   for (const auto& op : ctx->pp.ops) {
     if (op.kind != OP_CONTRACT) continue;
     const Node& n = g.nodes[size_t(op.node)];
-    if ((n.op == CC_TR_MM) != (cls == 1)) continue;
+    if (is_root_kind(n.op) != (cls == 1)) continue;
     ++nl;
     flops += node_flops(n, g.Lt, g.N, g.S);
     bytes += node_hbm_bytes(n, g.Lt, g.N, g.S);
@@ -203,7 +208,7 @@ void kernel_only(cc_ctx* ctx, int cls, cc_exec_stats* stats) {
       for (const auto& op : ctx->pp.ops) {
         if (op.kind != OP_CONTRACT) continue;
         const Node& n = g.nodes[size_t(op.node)];
-        if ((n.op == CC_TR_MM) != (cls == 1)) continue;
+        if (is_root_kind(n.op) != (cls == 1)) continue;
         const void* a = op.loc_a == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.l)] : ctx->arena + op.off_a;
         const void* b = op.loc_b == LOC_DEVLEAF ? ctx->leaf_dev[size_t(n.r)] : ctx->arena + op.off_b;
         if (!a || !b) throw Error(CC_E_STATE, "kernel-only replay: operand without a device address");

@@ -77,8 +77,8 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
     const Dag& gd = *ctx->dag;
     bool gemm = false, baryon = false;
     for (const auto& n : gd.nodes) {
-      gemm |= n.op == CC_MM1 || n.op == CC_BM1 || n.op == CC_BB2;
-      baryon |= n.op == CC_BM1 || n.op == CC_BB2;
+      gemm |= is_gemm_kind(n.op);
+      baryon |= is_gemm_kind(n.op) && n.op != CC_MM1;
     }
     if (gemm && (gd.N >= 256 || (baryon && gd.N >= 128))) flags |= 64;
     flags &= ~128;
@@ -192,7 +192,7 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   }
   if (stats) {
     double ks = 0;
-    for (int k = 0; k < 8; ++k) ks += ctx->ktimes.seconds[k];
+    for (int k = 0; k < CC_N_OPS; ++k) ks += ctx->ktimes.seconds[k];
     stats->kernel_seconds = ks;
   }
   cudaEventDestroy(t_begin);

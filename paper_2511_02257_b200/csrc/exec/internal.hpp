@@ -53,7 +53,12 @@ struct PhaseTimer {
 };
 constexpr int64_t ALIGN = 1024;
 // kind index of a GEMM op for the Ozaki form cache (a leaf's form depends on the problem shape)
-inline int oz_kind(int op) { return op == CC_MM1 ? 0 : (op == CC_BM1 ? 1 : 2); }
+constexpr int OZ_KINDS = 5;   // MM1, BM1, BB2, BB1, BT2
+inline int oz_kind(int op) {
+  return op == CC_MM1 ? 0 : op == CC_BM1 ? 1 : op == CC_BB2 ? 2 : op == CC_BB1 ? 3 : 4;
+}
+constexpr int GEMM_OPS[5] = {CC_MM1, CC_BM1, CC_BB2, CC_BB1, CC_BT2};
+constexpr int TRACE_OPS[2] = {CC_TR_MM, CC_BB3};
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 inline void ck(cudaError_t e, const char* what) {
@@ -61,8 +66,8 @@ inline void ck(cudaError_t e, const char* what) {
 }
 
 struct KindTimes {
-  double seconds[8] = {0};
-  int64_t count[8] = {0};
+  double seconds[CC_N_OPS] = {0};
+  int64_t count[CC_N_OPS] = {0};
 };
 constexpr int64_t DF_CHUNK_RING = 4;   // GEMM ops split in k that may be in flight at once
 constexpr int64_t DF_TRACE_RING = 16;  // TR ops that may be in flight at once
@@ -78,8 +83,8 @@ struct cc_ctx {
   // Ozaki leaf-form cache: INT8 slices of leaves, split once per execute and shared by every
   // MM1 reading that leaf in the same role, placed in the pool above the plan's high water
   struct {
-    std::vector<OzakiForm> form[6];   // [2 * oz_kind + (B-form)]
-    std::vector<char> have[6];
+    std::vector<OzakiForm> form[2 * OZ_KINDS];   // [2 * oz_kind + (B-form)]
+    std::vector<char> have[2 * OZ_KINDS];
     int64_t off = 0, end = 0;
   } oz;
   char* oz_scratch = nullptr;          // reserved leaf-form cache (scratch), may be empty
@@ -261,7 +266,7 @@ namespace ccx {
 void rebuild_dag(cc_ctx* ctx);
 ZgemmProblem problem_for(int op, int64_t Lt, int64_t N, int64_t S, const void* a, const void* b, void* c);
 void df_gemm_geometry(const ZgemmProblem& p, int64_t& tiles, int64_t& KT, int64_t& chunks, int num_sms);
-int64_t df_trace_pieces(int64_t Lt, int64_t N);
+int64_t df_trace_pieces(const TraceShape& sh);
 struct ScratchSizes {
   int64_t sz_gemm = 0, sz_trace = 0, sz_roots = 0, sz_corr = 0, sz_ts = 0, sz_tt = 0, sz_tc = 0, sz_df_chunk = 0,
           sz_df_trace = 0, sz_ozc = 0, total = 0;

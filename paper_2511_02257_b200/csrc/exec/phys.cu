@@ -55,11 +55,23 @@ ZgemmProblem problem_for(int op, int64_t Lt, int64_t N, int64_t S, const void* a
     p.lda = N; p.sAo = 0; p.sAb = S * N * N * N;
     p.ldb = N; p.sBo = 0; p.sBb = N * N;
     p.ldc = N; p.sCb = S * N * N * N;
-  } else {  // CC_BB2
+  } else if (op == CC_BB2) {
     p.M = N; p.Nn = N; p.Kin = N * N; p.Ko = S;
     p.lda = N * N; p.sAo = N * N * N; p.sAb = S * N * N * N;
     p.ldb = N; p.sBo = N * N * N; p.sBb = S * N * N * N;
     p.ldc = N; p.sCb = N * N;
+  } else if (op == CC_BB1) {
+    // T[t,(i,j),(l,m)] = sum_{s,k} A[t,s,(i,j),k] B[t,s,k,(l,m)]: M = N^2, Nn = N^2, K = (s, k)
+    p.M = N * N; p.Nn = N * N; p.Kin = N; p.Ko = S;
+    p.lda = N; p.sAo = N * N * N; p.sAb = S * N * N * N;
+    p.ldb = N * N; p.sBo = N * N * N; p.sBb = S * N * N * N;
+    p.ldc = N * N; p.sCb = N * N * N * N;
+  } else {  // CC_BT2
+    // C[t,(s,m),(i,j)] = sum_{(k,l)} A[t,(s,m),(k,l)] X[t,(k,l),(i,j)]: M = S N, Nn = N^2, K = N^2
+    p.M = S * N; p.Nn = N * N; p.Kin = N * N; p.Ko = 1;
+    p.lda = N * N; p.sAo = 0; p.sAb = S * N * N * N;
+    p.ldb = N * N; p.sBo = 0; p.sBb = N * N * N * N;
+    p.ldc = N * N; p.sCb = S * N * N * N;
   }
   return p;
 }
@@ -81,10 +93,9 @@ void df_gemm_geometry(const ZgemmProblem& p, int64_t& tiles, int64_t& KT, int64_
 }
 
 // Pieces per time slice of a TR op: ~DF_TR_UNITS blocks of 32x32 (32 KB each) per item.
-int64_t df_trace_pieces(int64_t Lt, int64_t N) {
+int64_t df_trace_pieces(const TraceShape& sh) {
   constexpr int64_t units = 16;
-  const int64_t nb = (N + 31) / 32, U = nb * nb;
-  (void)Lt;
+  const int64_t nb = (sh.N + 31) / 32, U = int64_t(sh.G) * nb * nb;
   return std::max<int64_t>(1, (U + units - 1) / units);
 }
 
@@ -96,13 +107,13 @@ ScratchSizes scratch_sizes(cc_ctx* ctx) {
   ScratchSizes z;
   // scratch layout
   size_t gemm_ws = 0;
-  bool has[8] = {false};
+  bool has[CC_N_OPS] = {false};
   for (const auto& n : g.nodes) has[n.op] = true;
-  for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)})
+  for (int op : GEMM_OPS)
     if (has[op]) gemm_ws = std::max(gemm_ws, zgemm_workspace_bytes(problem_for(op, Lt, N, S, nullptr, nullptr, nullptr), ctx->num_sms));
   // Ozaki engine (execute flags bit 6): workspace for batches of time slices that fit in
   // max(one slice, arena / 16)
-  for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)}) {
+  for (int op : GEMM_OPS) {
     if (!has[op]) continue;
     const ZgemmProblem q = problem_for(op, Lt, N, S, nullptr, nullptr, nullptr);
     const size_t lim = std::max(ozaki_workspace_bytes(q, ctx->opt.ozaki_slices, 1), size_t(ctx->arena_bytes / 16));
@@ -115,24 +126,26 @@ ScratchSizes scratch_sizes(cc_ctx* ctx) {
   // leaves free)
   int64_t sz_ozc = 0;
   {
-    std::vector<std::array<char, 6>> role(g.nodes.size(), std::array<char, 6>{});
+    std::vector<std::array<char, 2 * OZ_KINDS>> role(g.nodes.size(), std::array<char, 2 * OZ_KINDS>{});
     for (const auto& n : g.nodes)
-      if (n.op == CC_MM1 || n.op == CC_BM1 || n.op == CC_BB2) {
+      if (is_gemm_kind(n.op)) {
         if (g.nodes[size_t(n.l)].leaf()) role[size_t(n.l)][size_t(2 * oz_kind(n.op))] = 1;
         if (g.nodes[size_t(n.r)].leaf()) role[size_t(n.r)][size_t(2 * oz_kind(n.op) + 1)] = 1;
       }
-    int64_t fsz[6] = {0};
-    for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)}) {
+    int64_t fsz[2 * OZ_KINDS] = {0};
+    for (int op : GEMM_OPS) {
       if (!has[op]) continue;
       const ZgemmProblem q = problem_for(op, Lt, N, S, nullptr, nullptr, nullptr);
       fsz[2 * oz_kind(op)] = round_up(int64_t(ozaki_form_bytes(q, ctx->opt.ozaki_slices, false)), ALIGN);
       fsz[2 * oz_kind(op) + 1] = round_up(int64_t(ozaki_form_bytes(q, ctx->opt.ozaki_slices, true)), ALIGN);
     }
     for (const auto& r : role)
-      for (int k = 0; k < 6; ++k) sz_ozc += r[size_t(k)] ? fsz[k] : 0;
+      for (int k = 0; k < 2 * OZ_KINDS; ++k) sz_ozc += r[size_t(k)] ? fsz[k] : 0;
     if (sz_ozc > ctx->arena_bytes / 8) sz_ozc = 0;
   }
-  const size_t trace_ws = trace_workspace_bytes(Lt, N);
+  size_t trace_ws = 0;
+  for (int op : TRACE_OPS)
+    if (has[op] || op == CC_TR_MM) trace_ws = std::max(trace_ws, trace_workspace_bytes(Lt, trace_shape(op, N, S)));
   const int64_t n_trees = int64_t(g.trees.size()), n_corr = int64_t(g.corr_ids.size()), n_terms = int64_t(g.terms.size());
   z.sz_gemm = round_up(int64_t(gemm_ws), ALIGN);
   z.sz_trace = round_up(int64_t(trace_ws), ALIGN);
@@ -144,7 +157,7 @@ ScratchSizes scratch_sizes(cc_ctx* ctx) {
   // dataflow workspaces: rings of chunk-partial slots (GEMM ops split in k) and of trace
   // partial slots (per-op tickets and [Lt][P] partials)
   ctx->df_chunk_slot = ctx->df_chunk_cnt_slot = 0;
-  for (int op : {int(CC_MM1), int(CC_BM1), int(CC_BB2)}) {
+  for (int op : GEMM_OPS) {
     if (!has[op]) continue;
     int64_t tiles, KT, chunks;
     df_gemm_geometry(problem_for(op, Lt, N, S, nullptr, nullptr, nullptr), tiles, KT, chunks, ctx->num_sms);
@@ -155,7 +168,10 @@ ScratchSizes scratch_sizes(cc_ctx* ctx) {
       ctx->df_chunk_cnt_slot = std::max(ctx->df_chunk_cnt_slot, round_up(tiles * 4, ALIGN));
     }
   }
-  ctx->df_trace_slot = round_up(Lt * df_trace_pieces(Lt, N) * 16, ALIGN) + round_up(Lt * 4, ALIGN);
+  int64_t pieces = 1;
+  for (int op : TRACE_OPS)
+    if (has[op]) pieces = std::max(pieces, df_trace_pieces(trace_shape(op, N, S)));
+  ctx->df_trace_slot = round_up(Lt * pieces * 16, ALIGN) + round_up(Lt * 4, ALIGN);
   z.sz_df_chunk = DF_CHUNK_RING * (ctx->df_chunk_slot + ctx->df_chunk_cnt_slot);
   z.sz_df_trace = DF_TRACE_RING * ctx->df_trace_slot;
   z.sz_ozc = sz_ozc;

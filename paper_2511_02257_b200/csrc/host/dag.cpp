@@ -13,7 +13,8 @@ int64_t tensor_bytes(int op, int64_t Lt, int64_t N, int64_t S) {
   // complex128 = 16 B per element: meson [Lt,N,N], baryon [Lt,S,N,N,N], root [Lt]
   if (is_meson_kind(op)) return 16 * Lt * N * N;
   if (is_baryon_kind(op)) return 16 * Lt * S * N * N * N;
-  if (op == CC_TR_MM) return 16 * Lt;
+  if (is_tetra_kind(op)) return 16 * Lt * N * N * N * N;
+  if (is_root_kind(op)) return 16 * Lt;
   throw Error(CC_E_INVAL, "abstract node needs an explicit size");
 }
 
@@ -25,6 +26,9 @@ double node_flops(const Node& n, int64_t Lt, int64_t N, int64_t S) {
     case CC_BM1:
     case CC_BB2: return 8.0 * lt * s * nn * nn * nn * nn;
     case CC_TR_MM: return 8.0 * lt * nn * nn;
+    case CC_BB1:
+    case CC_BT2: return 8.0 * lt * s * nn * nn * nn * nn * nn;
+    case CC_BB3: return 8.0 * lt * s * nn * nn * nn;
     default: return 0.0;
   }
 }
@@ -36,6 +40,9 @@ double node_hbm_bytes(const Node& n, int64_t Lt, int64_t N, int64_t S) {
     case CC_BM1:
     case CC_BB2: return 16.0 * lt * (2.0 * s * nn * nn * nn + nn * nn);
     case CC_TR_MM: return 32.0 * lt * nn * nn;
+    case CC_BB1: return 16.0 * lt * (2.0 * s * nn * nn * nn + nn * nn * nn * nn);     // 2 baryons in, tetra out
+    case CC_BT2: return 16.0 * lt * (2.0 * s * nn * nn * nn + nn * nn * nn * nn);     // baryon + tetra in, baryon out
+    case CC_BB3: return 32.0 * lt * s * nn * nn * nn;
     default: return 0.0;
   }
 }
@@ -63,7 +70,7 @@ Dag::Dag(const Input& in, int32_t Lt_override, const std::vector<int64_t>* keep_
   std::unordered_map<int64_t, const cc_node*> byid;
   byid.reserve(in.nodes.size() * 2);
   for (const auto& n : in.nodes) {
-    if (n.op < 0 || n.op > 7) throw Error(CC_E_INVAL, "bad op for node " + S_(n.id));
+    if (n.op < 0 || n.op >= CC_N_OPS) throw Error(CC_E_INVAL, "bad op for node " + S_(n.id));
     if (!byid.emplace(n.id, &n).second) throw Error(CC_E_INCONSISTENT, "duplicate node id " + S_(n.id));
   }
   std::vector<int64_t> ids;
@@ -177,14 +184,17 @@ Dag::Dag(const Input& in, int32_t Lt_override, const std::vector<int64_t>* keep_
       case CC_MM1:
       case CC_TR_MM: ok = is_meson_kind(ka) && is_meson_kind(kb); break;
       case CC_BM1: ok = is_baryon_kind(ka) && is_meson_kind(kb); break;
-      case CC_BB2: ok = is_baryon_kind(ka) && is_baryon_kind(kb); break;
+      case CC_BB2:
+      case CC_BB1:
+      case CC_BB3: ok = is_baryon_kind(ka) && is_baryon_kind(kb); break;
+      case CC_BT2: ok = is_baryon_kind(ka) && is_tetra_kind(kb); break;
       default: ok = false;
     }
     if (!ok) throw Error(CC_E_INCONSISTENT, "node " + S_(n.id) + ": operand kinds do not fit its op");
-    if (n.op == CC_TR_MM && !n.parents.empty())
-      throw Error(CC_E_INCONSISTENT, "TR_MM node " + S_(n.id) + " must be a root");
-    if ((n.op == CC_MM1 || n.op == CC_BM1 || n.op == CC_BB2) && n.parents.empty())
-      throw Error(CC_E_INCONSISTENT, "root " + S_(n.id) + " must be a TR_MM (contract-all)");
+    if (is_root_kind(n.op) && !n.parents.empty())
+      throw Error(CC_E_INCONSISTENT, "contract-all node " + S_(n.id) + " must be a root");
+    if (is_gemm_kind(n.op) && n.parents.empty())
+      throw Error(CC_E_INCONSISTENT, "root " + S_(n.id) + " must be a contract-all (TR_MM / BB3)");
   }
 
   // --- ranks, Eq. (1) ---------------------------------------------------------------------
@@ -290,7 +300,8 @@ cc_dag_stats Dag::stats() const {
 Input parse_text_file(const std::string& path) {
   std::ifstream f(path);
   if (!f) throw Error(CC_E_PARSE, "cannot open " + path);
-  static const char* names[8] = {"leafM", "leafB", "MM1", "BM1", "BB2", "TR_MM", "leafX", "OPX"};
+  static const char* names[CC_N_OPS] = {"leafM", "leafB", "MM1", "BM1", "BB2", "TR_MM", "leafX", "OPX",
+                                         "BB1", "BT2", "BB3"};
   Input in;
   bool have_dims = false;
   std::string line;
@@ -322,7 +333,7 @@ Input parse_text_file(const std::string& path) {
     } else if (tok[0] == "node") {
       if (tok.size() < 3) fail("missing field");
       int op = -1;
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < CC_N_OPS; ++i)
         if (tok[2] == names[i]) op = i;
       if (op < 0) fail("unknown op " + tok[2]);
       cc_node n{num(1), op, 0, -1, -1, 0};

@@ -21,7 +21,12 @@ enum NodeType : uint8_t { LEAF = 0, INTERIOR = 1, ROOT = 2 };
 
 inline bool is_leaf_op(int op) { return op == CC_LEAF_M || op == CC_LEAF_B || op == CC_LEAF_X; }
 inline bool is_meson_kind(int op) { return op == CC_LEAF_M || op == CC_MM1 || op == CC_BB2; }
-inline bool is_baryon_kind(int op) { return op == CC_LEAF_B || op == CC_BM1; }
+inline bool is_baryon_kind(int op) { return op == CC_LEAF_B || op == CC_BM1 || op == CC_BT2; }
+inline bool is_tetra_kind(int op) { return op == CC_BB1; }
+inline bool is_root_kind(int op) { return op == CC_TR_MM || op == CC_BB3; }   // "contract all"
+inline bool is_gemm_kind(int op) {
+  return op == CC_MM1 || op == CC_BM1 || op == CC_BB2 || op == CC_BB1 || op == CC_BT2;
+}
 
 struct Node {
   int64_t id = 0;

@@ -35,6 +35,9 @@ std::vector<int32_t> tree_parts(const Dag& g, int32_t n_parts, std::vector<int32
         case CC_BM1:
         case CC_BB2: f = lt * s * nn * nn * nn * nn; break;
         case CC_TR_MM: f = lt * nn * nn; break;
+        case CC_BB1:
+        case CC_BT2: f = lt * s * nn * nn * nn * nn * nn; break;
+        case CC_BB3: f = lt * s * nn * nn * nn; break;
         default: f = 1;
       }
     }

@@ -100,6 +100,7 @@ struct ItemInfo {
   int32_t kt, fb, fc, ptmap0, rr;           // GEMM: k-tile stages, fused traces [fb, fb+fc) with
                                             // partner maps ptmap0.., tile index within its slice
   int32_t t, u0, nb, piece;                 // TRACE
+  int32_t gj, gs;                           // TRACE: BB3 j extent and spin count (gj = 0: TR_MM)
   unsigned long long t_disp, t_ready;       // profiling (producer)
   unsigned long long t_first, t_comp;       // profiling (consumers)
 };
@@ -136,10 +137,12 @@ __device__ __forceinline__ void decode_item(const DfQueue& q, int64_t item, Item
     inf.npos = inf.kt + 2 * op.fuse_count;   // + two partner stages per fused trace
   } else {
     const int t = int(local / op.P), p = int(local - int64_t(t) * op.P);
-    const int U = op.nb * op.nb;
+    const int U = op.tr_G * op.nb * op.nb;
     inf.t = t;
     inf.piece = p;
     inf.nb = op.nb;
+    inf.gj = op.tr_Gj;
+    inf.gs = op.tr_S;
     inf.u0 = int((int64_t(p) * U) / op.P);
     inf.npos = int((int64_t(p + 1) * U) / op.P) - inf.u0;
   }
@@ -200,11 +203,23 @@ __device__ __forceinline__ void gemm_stage_loads(const ItemInfo& inf, int k, uin
 __device__ __forceinline__ void trace_stage_loads(const ItemInfo& inf, int k, uint8_t* sA, uint64_t* bar) {
   uint8_t* sB = sA + GC::A_BYTES;
   const int u = inf.u0 + k;
-  const int I = u / inf.nb, J = u - I * inf.nb;
+  const int nb2 = inf.nb * inf.nb;
+  const int g = u / nb2, rem = u - g * nb2;
+  const int I = rem / inf.nb, J = rem - I * inf.nb;
+  if (inf.gj == 0) {
 #pragma unroll
-  for (int ch = 0; ch < TB / 8; ++ch) {  // A[t, I*32 + r, J*32 + 8ch + s] and B[t, J*32 + r, I*32 + 8ch + s]
-    tma_load_4d_g(sA + ch * TB * 128, inf.tA, bar, 2 * (J * TB + 8 * ch), I * TB, 0, inf.t);
-    tma_load_4d_g(sB + ch * TB * 128, inf.tB, bar, 2 * (I * TB + 8 * ch), J * TB, 0, inf.t);
+    for (int ch = 0; ch < TB / 8; ++ch) {  // A[t, I*32 + r, J*32 + 8ch + s] and B[t, J*32 + r, I*32 + 8ch + s]
+      tma_load_4d_g(sA + ch * TB * 128, inf.tA, bar, 2 * (J * TB + 8 * ch), I * TB, 0, inf.t);
+      tma_load_4d_g(sB + ch * TB * 128, inf.tB, bar, 2 * (I * TB + 8 * ch), J * TB, 0, inf.t);
+    }
+  } else {
+    // BB3 sub-matrix g = (s, j): maps (k, j, row, t S + s) — the same 32 x 32 block pair layout
+    const int j = g % inf.gj, ts = inf.t * inf.gs + g / inf.gj;
+#pragma unroll
+    for (int ch = 0; ch < TB / 8; ++ch) {
+      tma_load_4d_g(sA + ch * TB * 128, inf.tA, bar, 2 * (J * TB + 8 * ch), j, I * TB, ts);
+      tma_load_4d_g(sB + ch * TB * 128, inf.tB, bar, 2 * (I * TB + 8 * ch), j, J * TB, ts);
+    }
   }
 }
 
@@ -760,6 +775,14 @@ cudaError_t df_launch_fused_finish(const DfFused* fused, int32_t n_fused, int64_
   if (n_fused <= 0) return cudaSuccess;
   fused_finish_kernel<<<unsigned(n_fused), 64, 0, s>>>(fused, Lt);
   return cudaGetLastError();
+}
+
+bool df_encode_bb3_maps(void* dst, const void* A, const void* B, int64_t Lt, int64_t N, int64_t S) {
+  // X[t,s,r,j,c] (r = row of the sub-matrix, c = column) as dims (2N doubles of c, j, r, t S + s)
+  const uint64_t dims[4] = {uint64_t(2 * N), uint64_t(N), uint64_t(N), uint64_t(Lt * S)};
+  const uint64_t strides[3] = {uint64_t(N) * 16, uint64_t(N * N) * 16, uint64_t(N * N * N) * 16};
+  const uint32_t box[4] = {16, 1, uint32_t(TB), 1};
+  return encode_map_4d(dst, A, dims, strides, box) && encode_map_4d(static_cast<uint8_t*>(dst) + 128, B, dims, strides, box);
 }
 
 bool df_encode_trace_maps(void* dst, const void* A, const void* B, int64_t Lt, int64_t N) {

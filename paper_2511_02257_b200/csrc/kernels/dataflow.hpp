@@ -36,12 +36,15 @@ struct DfOp {
   void* C;
   void* part;             // chunked: partial tiles [tile][chunk][slot]
   int* tile_cnt;          // chunked: per-tile finished-chunk counters (reset by the finisher)
-  // TRACE: out[t] = sum_{i,j} A[t,i,j] B[t,j,i]
+  // TRACE: out[t] = sum_g sum_{i,j} A_g[t,i,j] B_g[t,j,i] over G sub-matrices per slice:
+  // TR_MM G = 1; BB3 (reading T4-3) G = S N, g = (s, j) (kernels.hpp TraceShape)
   const void* A;
   const void* B;
   void* out;
   int64_t N, Lt;
   int32_t nb, P;          // 32x32 blocks per row; items (pieces) per time slice
+  int32_t tr_G, tr_Gj;    // sub-matrices per slice; BB3: j extent (0 for TR_MM: 3-dim maps)
+  int32_t tr_S, pad_;     // BB3: spin components (time-spin index of the maps: t S + s)
   void* tr_part;          // [Lt][P] complex partials
   int* tr_cnt;            // [Lt] tickets (reset by the finisher)
   // GEMM with fused traces: after its k-tiles every output tile also computes, for each
@@ -96,6 +99,9 @@ bool df_encode_maps(void* dst, const void* A, const void* B, int64_t M, int64_t 
                     int64_t batch, int64_t lda, int64_t sAo, int64_t sAb, int64_t ldb, int64_t sBo, int64_t sBb);
 // TMA maps of a TR_MM op's operands ([Lt][N][N] complex, 32-row boxes).
 bool df_encode_trace_maps(void* dst, const void* A, const void* B, int64_t Lt, int64_t N);
+// TMA maps of a BB3 op's operands (baryons [Lt][S][N][N][N] as 4-d tensors (k, j, i, t S + s):
+// boxes of 8 complex x 1 x 32 rows, so a stage holds the same 32x32 sub-matrix block pair).
+bool df_encode_bb3_maps(void* dst, const void* A, const void* B, int64_t Lt, int64_t N, int64_t S);
 // TMA map of a fused trace's other operand ([Lt][N][N] complex, boxes of 8 complex x 32 rows).
 bool df_encode_partner_map(void* dst, const void* X, int64_t Lt, int64_t N);
 // root[t] = sum over tiles, warps of part[t][tile][warp] (fixed order), for every fused trace.

@@ -25,21 +25,35 @@ struct ZgemmProblem {
 // with 128-byte swizzle, as the DMMA kernels read them.
 bool encode_zgemm_maps(void* mapA, void* mapB, const ZgemmProblem& p, int BM, int BK);
 
+// A 4-d FP64 tensor map (dims[0] innermost, strides in bytes of dims 1..3, box extents),
+// 128-byte swizzle.
+bool encode_map_4d(void* map, const void* base, const uint64_t dims[4], const uint64_t strides_bytes[3],
+                   const uint32_t box[4]);
+
 // Workspace bytes a problem needs for its deterministic split-K partials.
 size_t zgemm_workspace_bytes(const ZgemmProblem& p, int num_sms);
 cudaError_t launch_zgemm(const ZgemmProblem& p, void* workspace, size_t ws_bytes, int num_sms,
                          cudaStream_t stream, int* n_launches);
 
-// c[t] = sum_{i,j} A[t,i,j] B[t,j,i]; out[t] (complex128) written with a fixed-order
-// reduction.  counters: Lt ints, zero on entry, zero again on exit.  partials: Lt*ceil(N/32)
-// complex128.
-size_t trace_workspace_bytes(int64_t Lt, int64_t N);
-cudaError_t launch_trace(const void* A, const void* B, void* out, int64_t Lt, int64_t N, void* workspace,
+// "Contract all" of two nodes as a sum of traces of G strided N x N sub-matrices per time
+// slice: c[t] = sum_g sum_{i,k} A[t](g)[i][k] B[t](g)[k][i] with X[t](g)[r][c] at
+// X + t sT + (g / Gj) sGo + (g % Gj) sGi + r ld + c (complex elements).
+//   TR_MM: G = 1, ld = N, sT = N^2.   BB3 (reading T4-3): g = (s, j), G = S N, Gj = N,
+//   sGo = N^3, sGi = N, ld = N^2, sT = S N^3 (A_sj[i][k] = A[t,s,i,j,k], B_sj[k][i] = B[t,s,k,j,i]).
+struct TraceShape {
+  int64_t N, ld, sT, sGo, sGi;
+  int32_t G, Gj;
+};
+TraceShape trace_shape(int op, int64_t N, int64_t S);   // op = CC_TR_MM or CC_BB3
+// out[t] (complex128) written with a fixed-order reduction.  Workspace: counters (zero on entry,
+// zero again on exit) + unit partials.
+size_t trace_workspace_bytes(int64_t Lt, const TraceShape& sh);
+cudaError_t launch_trace(const void* A, const void* B, void* out, int64_t Lt, const TraceShape& sh, void* workspace,
                          cudaStream_t stream);
 // n <= trace_batch_max() traces of the same shape in one launch (out[k] = Lt complex128 each).
 int trace_batch_max();
 cudaError_t launch_trace_batch(const void* const* A, const void* const* B, void* const* out, int n, int64_t Lt,
-                               int64_t N, void* workspace, cudaStream_t stream);
+                               const TraceShape& sh, void* workspace, cudaStream_t stream);
 
 // corr[c][t] = sum over the terms of correlator c (in input order) of coef * roots[tree][t].
 // term_start: n_corr+1 offsets into (term_tree, term_coef).

@@ -1,7 +1,11 @@
 // "Contract all" for tree roots and the correlator sums.
 //
 // TR_MM: c[t] = sum_{i,j} A[t,i,j] * B[t,j,i]  (reading V-1).  HBM/L2-bound (0.25 flop/B).
-// Work unit = (t, I, J): the 32x32 complex block A[t, I, J] and its transpose partner
+// BB3 (reading T4-3): c[t] = sum_s sum_{i,j,k} A[t,s,i,j,k] B[t,s,k,j,i] is the same operation
+// over G = S N strided sub-matrices per slice: for each (s, j), A_sj[i][k] = A[t,s,i,j,k] and
+// B_sj[k][i] = B[t,s,k,j,i] are N x N matrices with row stride N^2, and c[t] = sum over (s, j)
+// of tr(A_sj B_sj) (TraceShape, kernels.hpp).
+// Work unit = (t, g, I, J): the 32x32 complex block A[t, I, J] of sub-matrix g and its transpose partner
 // B[t, J, I] (16 KB each, coalesced 512-byte row segments).  Slice t is split into P
 // pieces of consecutive units (P chosen so Lt*P ~ 2 CTAs per SM); CTA (t, p) walks its
 // units with the next unit's eight 16-byte loads per thread issued before the current
@@ -12,6 +16,7 @@
 // atomics: the result is bit-identical from run to run.
 #include <algorithm>
 
+#include "cc.h"
 #include "kernels.hpp"
 
 namespace cc {
@@ -33,18 +38,22 @@ __device__ __forceinline__ double2 cmul_acc(double2 acc, double2 a, double2 b) {
   return acc;
 }
 
-__device__ __forceinline__ void load_unit(const double2* __restrict__ At, const double2* __restrict__ Bt, int64_t N,
-                                          int nb, int unit, int warp, int lane, double2 (&a)[RPW],
-                                          double2 (&b)[RPW]) {
-  const int I = unit / nb, J = unit - I * nb;
+__device__ __forceinline__ void load_unit(const double2* __restrict__ At, const double2* __restrict__ Bt,
+                                          const TraceShape& sh, int nb, int unit, int warp, int lane,
+                                          double2 (&a)[RPW], double2 (&b)[RPW]) {
+  const int nb2 = nb * nb;
+  const int g = unit / nb2, rem = unit - g * nb2;
+  const int I = rem / nb, J = rem - I * nb;
+  const int64_t N = sh.N, ld = sh.ld;
+  const int64_t goff = int64_t(g / sh.Gj) * sh.sGo + int64_t(g % sh.Gj) * sh.sGi;   // sub-matrix g
   const int64_t i0 = int64_t(I) * TB, j0 = int64_t(J) * TB;
 #pragma unroll
   for (int rr = 0; rr < RPW; ++rr) {
     const int r = warp + rr * 8;
-    const int64_t ia = i0 + r, ja = j0 + lane;   // A[t, I0 + r, J0 + lane]
-    const int64_t jb = j0 + r, ib = i0 + lane;   // B[t, J0 + r, I0 + lane]
-    a[rr] = (ia < N && ja < N) ? __ldg(At + ia * N + ja) : make_double2(0.0, 0.0);
-    b[rr] = (jb < N && ib < N) ? __ldg(Bt + jb * N + ib) : make_double2(0.0, 0.0);
+    const int64_t ia = i0 + r, ja = j0 + lane;   // A_g[I0 + r, J0 + lane]
+    const int64_t jb = j0 + r, ib = i0 + lane;   // B_g[J0 + r, I0 + lane]
+    a[rr] = (ia < N && ja < N) ? __ldg(At + goff + ia * ld + ja) : make_double2(0.0, 0.0);
+    b[rr] = (jb < N && ib < N) ? __ldg(Bt + goff + jb * ld + ib) : make_double2(0.0, 0.0);
   }
 }
 
@@ -57,8 +66,8 @@ struct TraceBatch {
 };
 
 __global__ void __launch_bounds__(TR_THREADS, TR_MINB)
-    trace_kernel(const __grid_constant__ TraceBatch tb, int64_t N, int nb, int P, double2* __restrict__ partials,
-                 int* __restrict__ counters) {
+    trace_kernel(const __grid_constant__ TraceBatch tb, const TraceShape sh, int nb, int P,
+                 double2* __restrict__ partials, int* __restrict__ counters) {
   __shared__ double2 sB[TB][TB + 1];
   __shared__ double2 red[TR_THREADS / 32];
   __shared__ int is_last;
@@ -69,15 +78,15 @@ __global__ void __launch_bounds__(TR_THREADS, TR_MINB)
   partials += int64_t(z) * gridDim.y * P;
   counters += int64_t(z) * gridDim.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int U = nb * nb;
+  const int U = sh.G * nb * nb;
   const int u0 = int((int64_t(p) * U) / P), u1 = int((int64_t(p + 1) * U) / P);
-  const double2* At = A + int64_t(t) * N * N;
-  const double2* Bt = B + int64_t(t) * N * N;
+  const double2* At = A + int64_t(t) * sh.sT;
+  const double2* Bt = B + int64_t(t) * sh.sT;
   double2 acc = make_double2(0.0, 0.0);
   double2 a[RPW], b[RPW], an[RPW], bn[RPW];
-  if (u0 < u1) load_unit(At, Bt, N, nb, u0, warp, lane, a, b);
+  if (u0 < u1) load_unit(At, Bt, sh, nb, u0, warp, lane, a, b);
   for (int u = u0; u < u1; ++u) {
-    if (u + 1 < u1) load_unit(At, Bt, N, nb, u + 1, warp, lane, an, bn);
+    if (u + 1 < u1) load_unit(At, Bt, sh, nb, u + 1, warp, lane, an, bn);
 #pragma unroll
     for (int rr = 0; rr < RPW; ++rr) sB[warp + rr * 8][lane] = b[rr];
     __syncthreads();
@@ -142,8 +151,8 @@ __global__ void __launch_bounds__(TR_THREADS, TR_MINB)
 // Pieces per time slice: from P0 = slots / slices (one wave) upwards, the smallest P whose CTAs
 // fill whole waves to within 5 % while each CTA keeps >= 16 units (else the least wasteful);
 // e.g. 512 slices in 512 CTAs is a 1.7-wave launch that idles a third of its last wave.
-int trace_pieces(int64_t Lt, int64_t N, int n_traces = 1) {
-  const int64_t nb = (N + TB - 1) / TB, U = nb * nb;
+int trace_pieces(int64_t Lt, const TraceShape& sh, int n_traces = 1) {
+  const int64_t nb = (sh.N + TB - 1) / TB, U = int64_t(sh.G) * nb * nb;
   const int64_t slots = int64_t(TR_MINB) * 148, X = Lt * n_traces;
   const int64_t P0 = std::max<int64_t>(1, slots / X);
   int64_t P = P0;
@@ -238,19 +247,25 @@ cudaError_t trace_preload() {
 
 // layout: counters (TRB x Lt ints, left at zero by every launch) then the unit partials (the
 // most any batch of n <= TRB traces needs, n Lt P_n)
-size_t trace_workspace_bytes(int64_t Lt, int64_t N) {
+TraceShape trace_shape(int op, int64_t N, int64_t S) {
+  if (op == CC_BB3) return TraceShape{N, N * N, S * N * N * N, N * N * N, N, int32_t(S * N), int32_t(N)};
+  return TraceShape{N, N, N * N, 0, 0, 1, 1};
+}
+
+size_t trace_workspace_bytes(int64_t Lt, const TraceShape& sh) {
   size_t parts = 0;
-  for (int n = 1; n <= TRB; ++n) parts = std::max(parts, size_t(n) * size_t(Lt * trace_pieces(Lt, N, n)));
+  for (int n = 1; n <= TRB; ++n) parts = std::max(parts, size_t(n) * size_t(Lt * trace_pieces(Lt, sh, n)));
   return parts * 16 + ((size_t(TRB) * Lt * 4 + 255) / 256) * 256;
 }
 
 int trace_batch_max() { return TRB; }
 
 cudaError_t launch_trace_batch(const void* const* A, const void* const* B, void* const* out, int n, int64_t Lt,
-                               int64_t N, void* workspace, cudaStream_t stream) {
-  if (Lt <= 0 || N <= 0 || Lt > 65535 || n <= 0 || n > TRB) return cudaErrorInvalidValue;
-  const int nb = int((N + TB - 1) / TB);
-  const int P = trace_pieces(Lt, N, n);
+                               const TraceShape& sh, void* workspace, cudaStream_t stream) {
+  if (Lt <= 0 || sh.N <= 0 || sh.G <= 0 || sh.Gj <= 0 || Lt > 65535 || n <= 0 || n > TRB) return cudaErrorInvalidValue;
+  const int nb = int((sh.N + TB - 1) / TB);
+  if (int64_t(sh.G) * nb * nb >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+  const int P = trace_pieces(Lt, sh, n);
   int* counters = static_cast<int*>(workspace);
   double2* partials =
       reinterpret_cast<double2*>(static_cast<char*>(workspace) + ((size_t(TRB) * Lt * 4 + 255) / 256) * 256);
@@ -261,13 +276,13 @@ cudaError_t launch_trace_batch(const void* const* A, const void* const* B, void*
     tb.out[k] = static_cast<double2*>(out[k]);
   }
   dim3 grid{unsigned(P), unsigned(Lt), unsigned(n)};
-  trace_kernel<<<grid, TR_THREADS, 0, stream>>>(tb, N, nb, P, partials, counters);
+  trace_kernel<<<grid, TR_THREADS, 0, stream>>>(tb, sh, nb, P, partials, counters);
   return cudaGetLastError();
 }
 
-cudaError_t launch_trace(const void* A, const void* B, void* out, int64_t Lt, int64_t N, void* workspace,
+cudaError_t launch_trace(const void* A, const void* B, void* out, int64_t Lt, const TraceShape& sh, void* workspace,
                          cudaStream_t stream) {
-  return launch_trace_batch(&A, &B, &out, 1, Lt, N, workspace, stream);
+  return launch_trace_batch(&A, &B, &out, 1, Lt, sh, workspace, stream);
 }
 
 cudaError_t launch_correlate(const void* roots, void* corr, int64_t n_corr, int64_t Lt, const int32_t* term_start,

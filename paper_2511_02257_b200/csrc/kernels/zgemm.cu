@@ -271,18 +271,24 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-bool make_map(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint64_t strides_bytes[3],
-              uint32_t box1) {
+bool make_map_box(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint64_t strides_bytes[3],
+                  const uint32_t box_in[4]) {
   auto enc = get_encode();
   if (!enc) return false;
   cuuint64_t gd[4] = {dims[0], dims[1], dims[2], dims[3]};
   cuuint64_t gs[3] = {strides_bytes[0], strides_bytes[1], strides_bytes[2]};
-  cuuint32_t box[4] = {16, box1, 1, 1};
+  cuuint32_t box[4] = {box_in[0], box_in[1], box_in[2], box_in[3]};
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), gd, gs, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+bool make_map(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint64_t strides_bytes[3],
+              uint32_t box1) {
+  const uint32_t box[4] = {16, box1, 1, 1};
+  return make_map_box(map, base, dims, strides_bytes, box);
 }
 
 
@@ -350,6 +356,11 @@ cudaError_t launch_cfg(const ZgemmProblem& p, void* ws, size_t ws_size, int num_
 }
 
 }  // namespace
+
+bool encode_map_4d(void* map, const void* base, const uint64_t dims[4], const uint64_t strides_bytes[3],
+                   const uint32_t box[4]) {
+  return make_map_box(static_cast<CUtensorMap*>(map), base, dims, strides_bytes, box);
+}
 
 bool encode_zgemm_maps(void* mapA, void* mapB, const ZgemmProblem& p, int BM, int BK) {
   const uint64_t sAo = p.Ko > 1 ? p.sAo : p.lda * p.M;

@@ -12,6 +12,10 @@ DESIGN.md reading V-1:
   BM1(A,M)[t,s,i,j,l] = sum_k A[t,s,i,j,k] M[t,k,l]             baryon x meson
   BB2(A,B)[t,i,l]     = sum_s sum_{j,k} A[t,s,i,j,k] B[t,s,j,k,l] baryon x baryon
   TR_MM(A,B)[t]       = sum_{i,j} A[t,i,j] B[t,j,i]              contract-all (root)
+BxBxB kinds (tritium class, readings T4-1..T4-4):
+  BB1(A,B)[t,i,j,l,m] = sum_s sum_k A[t,s,i,j,k] B[t,s,k,l,m]    baryon x baryon -> tetra
+  BT2(A,X)[t,s,m,i,j] = sum_{k,l} A[t,s,m,k,l] X[t,k,l,i,j]      baryon x tetra -> baryon
+  BB3(A,B)[t]         = sum_s sum_{i,j,k} A[t,s,i,j,k] B[t,s,k,j,i]  contract-all (root)
 LEAF_X / OP_X are abstract nodes with explicit sizes (scheduling-only DAGs,
 e.g. the Table I example); they carry no tensor semantics.
 
@@ -20,8 +24,9 @@ Recipes of the five BASELINE.json configs are DESIGN.md §"Input recipe".
 from dataclasses import dataclass, field
 import numpy as np
 
-LEAF_M, LEAF_B, MM1, BM1, BB2, TR_MM, LEAF_X, OP_X = range(8)
-OP_NAMES = ["leafM", "leafB", "MM1", "BM1", "BB2", "TR_MM", "leafX", "OPX"]
+LEAF_M, LEAF_B, MM1, BM1, BB2, TR_MM, LEAF_X, OP_X, BB1, BT2, BB3 = range(11)
+OP_NAMES = ["leafM", "leafB", "MM1", "BM1", "BB2", "TR_MM", "leafX", "OPX", "BB1", "BT2", "BB3"]
+N_OPS = len(OP_NAMES)
 LEAF_OPS = (LEAF_M, LEAF_B, LEAF_X)
 
 
@@ -349,5 +354,48 @@ def config_c5(N=256, Lt=128, n_mes=64, n_pairs=2000, n_trees=20000, zipf=1.1, n_
         trees.append(b.tree(b.op(TR_MM, x, y, share=False)))
     for t in trees:
         b.term(int(rng.integers(n_corr)), t, float(rng.choice([1.0, -1.0])), 0.0)
+    _prune(b.w)
+    return b.w
+
+
+def config_c6(N=32, Lt=8, S=64, n_snk=4, n_src=4, n_trees=200, p_meson=0.3, n_corr=4, seed=1, coefs="pm1"):
+    """c6: tritium-like BxBxB system (Table II 'tritium': N = 32, O(N^5),
+    8 leaves, every size class O(N^2) / O(N^3) / O(N^4)).  Each tree takes 3
+    sink and 3 source baryon leaves and eliminates quark lines one contraction at a time
+     through a tetraquark intermediate (reading T4-1..T4-4):
+      X1 = BB1(snk_a, src_b)   [tetra]        Y1 = BT2(snk_c, X1)   [baryon]
+      family A: X2 = BB1(Y1, src_d), Y2 = BT2(snk_e, X2), root = BB3(Y2, src_f)
+      family B (prob. p_meson): M1 = BB2(Y1, src_d), M2 = BB2(snk_e, src_f), root = TR_MM(M1, M2)
+    Identical contractions are shared across trees (prefixes X1, Y1 recur), duplicate trees are
+    redrawn; each tree enters one correlator."""
+    rng = np.random.default_rng(seed)
+    b = Builder("c6_tritium_N%d_Lt%d_S%d_k%d" % (N, Lt, S, n_trees), Lt, N, S)
+    snk = [b.leaf(LEAF_B) for _ in range(n_snk)]
+    src = [b.leaf(LEAF_B) for _ in range(n_src)]
+    seen = set()
+    trees = []
+    tries = 0
+    while len(trees) < n_trees and tries < 50 * n_trees:
+        tries += 1
+        a, c, e = (int(rng.integers(n_snk)) for _ in range(3))
+        bb, d, f = (int(rng.integers(n_src)) for _ in range(3))
+        fam = 1 if rng.random() < p_meson else 0
+        key = (fam, a, bb, c, d, e, f)
+        if key in seen:
+            continue
+        seen.add(key)
+        x1 = b.op(BB1, snk[a], src[bb])
+        y1 = b.op(BT2, snk[c], x1)
+        if fam == 0:
+            x2 = b.op(BB1, y1, src[d])
+            y2 = b.op(BT2, snk[e], x2)
+            root = b.op(BB3, y2, src[f], share=False)
+        else:
+            m1 = b.op(BB2, y1, src[d])
+            m2 = b.op(BB2, snk[e], src[f])
+            root = b.op(TR_MM, m1, m2, share=False)
+        trees.append(b.tree(root))
+    for t in trees:
+        b.term(int(rng.integers(n_corr)), t, *draw_coef(rng, coefs))
     _prune(b.w)
     return b.w

@@ -87,6 +87,35 @@ def test_configs_small_scale():
     _check(dags.config_c2(N=8, Lt=2), caps=(None, 6 * mes, 10 * mes))
     _check(dags.config_c3(N=4, Lt=2, S=4), caps=(None,))
     _check(dags.config_c4(N=4, Lt=1, S=4, n_trees=300), caps=(None, 16 * 4 * 64 * 6, 16 * 4 * 64 * 9))
+    # tritium-like BxBxB (f4): baryon 16 Lt S N^3, tetra 16 Lt N^4, meson 16 Lt N^2 mixed
+    bary = 16 * 2 * 4 * 4 ** 3
+    _check(dags.config_c6(N=4, Lt=2, S=4, n_trees=150), caps=(None, 5 * bary, 8 * bary))
+
+
+def test_c6_sizes_flops_and_text_roundtrip(tmp_path):
+    """BxBxB node sizes / dag stats agree with the oracle, the text format knows the new kinds,
+    and a contract-all kind used as an interior node (or a GEMM kind as a root) is rejected."""
+    w = dags.config_c6(N=5, Lt=3, S=2, n_trees=40)
+    dag = Dag(w)
+    c = _ctx(w)
+    assert c.dag_info()["V"] == len(dag.nodes)
+    _, st = c.schedule(cc.CC_TREE)
+    assert st["model_peak"] == simulate(dag, tree.schedule(dag))["peak"]
+    p = tmp_path / "c6.txt"
+    p.write_text(w.to_text())
+    c2 = cc.Context(-1)
+    c2.load_dag_file(str(p))
+    assert c2.schedule(cc.CC_TREE)[0] == c.schedule(cc.CC_TREE)[0]
+    b = dags.Builder("bad", 1, 2, 2)
+    x, y = b.leaf(dags.LEAF_B), b.leaf(dags.LEAF_B)
+    r = b.op(dags.BB3, x, y)
+    b.tree(b.op(dags.BB3, r, y))
+    for w_bad in (b.w,):
+        with pytest.raises(OracleError):
+            Dag(w_bad)
+        with pytest.raises(cc.CCError) as ei:
+            _ctx(w_bad)
+        assert ei.value.code == "INCONSISTENT"
 
 
 @pytest.mark.slow

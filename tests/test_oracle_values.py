@@ -62,6 +62,60 @@ def test_all_ones_closed_forms():
     assert np.array_equal(roots[0], np.full(Lt, float(N) ** 4, complex))
 
 
+def test_bxbxb_brute_force_loops_tiny():
+    """BB1 / BT2 / BB3 (readings T4-1..T4-3) against plain index loops over every index."""
+    Lt, N, S = 2, 3, 2
+    A = _rand((Lt, S, N, N, N), 11)
+    B = _rand((Lt, S, N, N, N), 12)
+    X = _rand((Lt, N, N, N, N), 13)
+    R = range(N)
+    bb1 = np.zeros((Lt, N, N, N, N), complex)
+    bt2 = np.zeros((Lt, S, N, N, N), complex)
+    bb3 = np.zeros(Lt, complex)
+    for t in range(Lt):
+        for i, j, l, m in itertools.product(R, R, R, R):
+            bb1[t, i, j, l, m] = sum(A[t, s, i, j, k] * B[t, s, k, l, m] for s in range(S) for k in R)
+        for s, m, i, j in itertools.product(range(S), R, R, R):
+            bt2[t, s, m, i, j] = sum(A[t, s, m, k, l] * X[t, k, l, i, j] for k in R for l in R)
+        bb3[t] = sum(A[t, s, i, j, k] * B[t, s, k, j, i] for s in range(S) for i in R for j in R for k in R)
+    np.testing.assert_allclose(values.bb1(A, B), bb1, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(values.bt2(A, X), bt2, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(values.bb3(A, B), bb3, rtol=1e-13, atol=1e-13)
+    # numpy.einsum as a third opinion
+    np.testing.assert_allclose(np.einsum("tsijk,tsklm->tijlm", A, B), bb1, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(np.einsum("tsmkl,tklij->tsmij", A, X), bt2, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(np.einsum("tsijk,tskji->t", A, B), bb3, rtol=1e-13, atol=1e-13)
+
+
+def test_bxbxb_closed_forms():
+    """All-ones baryons J_B and tetra J_T: BB1(J_B, J_B) = S N J_T (sum over s, k), BT2(J_B, J_T)
+    = N^2 J_B (sum over k, l), BB3(J_B, J_B) = S N^3; a tritium-family tree of all-ones leaves
+    (c6 family A: BB3(BT2(J, BB1(BT2(J, BB1(J, J)), J)), J)) is then exactly
+    S N^3 (S N N^2)^2 = S^3 N^9; spin-separable baryons A = sa (x) a, B = sb (x) b factorise."""
+    Lt, N, S = 2, 4, 3
+    JB = np.ones((Lt, S, N, N, N), complex)
+    JT = np.ones((Lt, N, N, N, N), complex)
+    assert np.array_equal(values.bb1(JB, JB), S * N * JT)
+    assert np.array_equal(values.bt2(JB, JT), N * N * JB)
+    assert np.array_equal(values.bb3(JB, JB), np.full(Lt, S * N ** 3, complex))
+    w = dags.config_c6(N=N, Lt=Lt, S=S, n_trees=12, p_meson=0.0)
+    dag = Dag(w)
+    roots = values.evaluate(dag, lambda u: JB)
+    for t in dag.tree_ids:
+        np.testing.assert_array_equal(roots[t], np.full(Lt, float(S ** 3 * N ** 9), complex))
+    sa, sb = _rand((Lt, S), 21), _rand((Lt, S), 22)
+    a, b = _rand((Lt, N, N, N), 23), _rand((Lt, N, N, N), 24)
+    X = _rand((Lt, N, N, N, N), 25)
+    A = np.einsum("ts,tijk->tsijk", sa, a)
+    B = np.einsum("ts,tijk->tsijk", sb, b)
+    ss = np.einsum("ts,ts->t", sa, sb)
+    np.testing.assert_allclose(values.bb1(A, B), ss[:, None, None, None, None] * np.einsum("tijk,tklm->tijlm", a, b),
+                               rtol=1e-12)
+    np.testing.assert_allclose(values.bb3(A, B), ss * np.einsum("tijk,tkji->t", a, b), rtol=1e-12)
+    np.testing.assert_allclose(values.bt2(A, X), np.einsum("ts,tmij->tsmij", sa, np.einsum("tmkl,tklij->tmij", a, X)),
+                               rtol=1e-12)
+
+
 def test_identity_and_transpose_structure():
     Lt, N = 2, 5
     I = np.broadcast_to(np.eye(N, dtype=complex), (Lt, N, N))
