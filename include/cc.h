@@ -96,6 +96,15 @@ typedef struct {
   int64_t cap_bytes;          /* device pool capacity for the LRU plan; <= 0: unbounded     */
   const int64_t* given_order; /* CC_GIVEN: contraction order (node ids), n_given entries    */
   int64_t n_given;
+  /* Peer-HBM tier (readings E-10, E-11; NVLink instead of the PCIe
+   * bus the paper names as the bottleneck).  peer_cap_bytes > 0: a victim
+   * with no off-device copy (an intermediate's first eviction, or a leaf) is copied to a peer
+   * GPU's HBM while that many bytes remain, and re-fetched from there; the copy lives until
+   * release.  peer_leaves: ids of leaves whose home copy is in a peer GPU's HBM (cross-GPU
+   * leaf sharing: every fetch of them is a peer copy, never H2D).  0 / NULL: no peer tier. */
+  int64_t peer_cap_bytes;
+  const int64_t* peer_leaves;
+  int64_t n_peer_leaves;
 } cc_sched_cfg;
 
 /* Logical plan statistics (integers are bit-exact with the oracle).
@@ -107,6 +116,9 @@ typedef struct {
   double sched_seconds;       /* scheduler wall time only (Table IV analogue) */
   double plan_seconds;        /* LRU plan + physical placement                              */
   int64_t arena_high_water;   /* physical pool bytes used (>= peak; fragmentation headroom)  */
+  int64_t p2p_out_count, p2p_out_bytes, p2p_in_count, p2p_in_bytes, peer_peak_bytes;
+                              /* peer-tier copies (E-10, E-11): evictions copied to the peer
+                                 tier, fetches from a peer; bytes in the peer tier at most  */
 } cc_plan_stats;
 
 typedef struct {
@@ -121,10 +133,12 @@ typedef struct {
   int64_t n_kernels;          /* kernel launches issued by this execute                     */
   double copy_seconds;        /* start -> last H2D/D2H copy done (blocking stream-mode
                                  dataflow execute with copies; else 0)                     */
+  int64_t p2p_in_bytes, p2p_out_bytes; /* peer-tier copies, counted as enqueued             */
 } cc_exec_stats;
 
 /* One op of the physical plan (cc_plan_ops). kind: 0 H2D, 1 D2H (evict with copy),
- * 2 DROP (evict, no copy), 3 CONTRACT, 4 FREE (release at last use). */
+ * 2 DROP (evict, no copy), 3 CONTRACT, 4 FREE (release at last use), 5 P2P_OUT (evict with a
+ * copy to the peer tier), 6 P2P_IN (fetch from a peer GPU's HBM). */
 typedef struct { int32_t kind; int32_t pad_; int64_t node; int64_t bytes; int64_t offset; } cc_plan_op;
 
 typedef struct cc_ctx cc_ctx;
@@ -189,6 +203,18 @@ cc_status cc_plan_dump(cc_ctx* ctx, const char* csv_path);
  * a no-op).  bytes must equal the (full / part) leaf size. */
 cc_status cc_set_leaf(cc_ctx* ctx, int64_t leaf_id, const void* host, size_t bytes);
 cc_status cc_set_leaf_device(cc_ctx* ctx, int64_t leaf_id, const void* dev, size_t bytes);
+/* Peer-homed leaf (E-11): dev is the address, in this process, of the full leaf ([Lt_full,...])
+ * in a peer GPU's HBM (a CUDA IPC mapping of the owner rank's buffer, or any device pointer
+ * cudaMemcpyAsync(cudaMemcpyDefault) can read — a buffer on this GPU works the same way),
+ * caller-owned, valid and holding the data until the last cc_execute returns.  Required
+ * for every leaf named in cc_sched_cfg.peer_leaves; each P2P_IN copies the part's slices. */
+cc_status cc_set_leaf_peer(cc_ctx* ctx, int64_t leaf_id, const void* dev, size_t bytes);
+/* The peer-HBM eviction tier region (E-10): caller-owned device memory (normally a CUDA IPC
+ * mapping of a peer GPU's buffer; any device pointer works), at least the plan's
+ * peer_peak_bytes plus fragmentation.  P2P_OUT copies are placed in it best-fit; cc_execute
+ * fails with CC_E_NOMEM if they do not fit, CC_E_STATE if the plan has peer copies and no
+ * region is set.  dev NULL / bytes 0 removes it. */
+cc_status cc_set_peer_tier(cc_ctx* ctx, void* dev, size_t bytes);
 
 /* Replays the plan on the device: H2D / D2H on the copy streams, contractions on the
  * compute stream, event dependencies for RAW on data and WAR on reused memory; blocking.

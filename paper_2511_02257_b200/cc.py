@@ -32,7 +32,7 @@ CC_EVICT_NEXT_USE = 1       # cc_sched_cfg.flags: next-use (Belady) eviction, re
 STATUS = {0: "OK", -1: "INVAL", -2: "PARSE", -3: "CYCLE", -4: "INCONSISTENT", -5: "MULTIROOT",
           -6: "UNKNOWN_NODE", -7: "NOT_CLOSED", -8: "INFEASIBLE", -9: "STATE", -10: "BUFFER_TOO_SMALL",
           -11: "CUDA", -12: "NOMEM"}
-OP_KINDS = ["H2D", "D2H", "DROP", "CONTRACT", "FREE"]
+OP_KINDS = ["H2D", "D2H", "DROP", "CONTRACT", "FREE", "P2P_OUT", "P2P_IN"]
 
 
 class cc_dims(ctypes.Structure):
@@ -53,19 +53,23 @@ class cc_term(ctypes.Structure):
 
 class cc_sched_cfg(ctypes.Structure):
     _fields_ = [("algo", c_i32), ("flags", c_i32), ("seed", c_u64), ("cap_bytes", c_i64),
-                ("given_order", P(c_i64)), ("n_given", c_i64)]
+                ("given_order", P(c_i64)), ("n_given", c_i64),
+                ("peer_cap_bytes", c_i64), ("peer_leaves", P(c_i64)), ("n_peer_leaves", c_i64)]
 
 
 class cc_plan_stats(ctypes.Structure):
     _fields_ = [(n, c_i64) for n in ("n_contr", "peak", "transient_peak", "evictions", "h2d_count", "d2h_count",
                                      "h2d_bytes", "d2h_bytes", "host_peak_bytes", "model_peak",
                                      "model_transient_peak")] + \
-               [("sched_seconds", c_dbl), ("plan_seconds", c_dbl), ("arena_high_water", c_i64)]
+               [("sched_seconds", c_dbl), ("plan_seconds", c_dbl), ("arena_high_water", c_i64)] + \
+               [(n, c_i64) for n in ("p2p_out_count", "p2p_out_bytes", "p2p_in_count", "p2p_in_bytes",
+                                     "peer_peak_bytes")]
 
 
 class cc_exec_stats(ctypes.Structure):
     _fields_ = [("seconds", c_dbl), ("kernel_seconds", c_dbl), ("flops", c_dbl), ("hbm_bytes", c_dbl),
-                ("h2d_bytes", c_i64), ("d2h_bytes", c_i64), ("n_kernels", c_i64), ("copy_seconds", c_dbl)]
+                ("h2d_bytes", c_i64), ("d2h_bytes", c_i64), ("n_kernels", c_i64), ("copy_seconds", c_dbl),
+                ("p2p_in_bytes", c_i64), ("p2p_out_bytes", c_i64)]
 
 
 class cc_plan_op(ctypes.Structure):
@@ -108,6 +112,8 @@ _sig("cc_tree_order", c_void_p, P(c_i64), c_i64, P(c_i64))
 _sig("cc_plan_dump", c_void_p, ctypes.c_char_p)
 _sig("cc_set_leaf", c_void_p, c_i64, c_void_p, c_size_t)
 _sig("cc_set_leaf_device", c_void_p, c_i64, c_void_p, c_size_t)
+_sig("cc_set_leaf_peer", c_void_p, c_i64, c_void_p, c_size_t)
+_sig("cc_set_peer_tier", c_void_p, c_void_p, c_size_t)
 _sig("cc_execute", c_void_p, c_i32, P(cc_exec_stats))
 _sig("cc_execute_async", c_void_p, c_i32)
 _sig("cc_kernel_times", c_void_p, P(c_dbl), P(c_i64))
@@ -135,7 +141,7 @@ _sig("cc_scratch_bytes", c_i32, c_i32, c_i32, res=c_size_t)
 
 EXPORTED = ["cc_create", "cc_destroy", "cc_last_error", "cc_version", "cc_load_dag", "cc_load_dag_file",
             "cc_dag_info", "cc_part_time_range", "cc_correlators", "cc_partition", "cc_part_trees", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
-            "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_execute",
+            "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_set_leaf_peer", "cc_set_peer_tier", "cc_execute",
             "cc_execute_async", "cc_get_options", "cc_set_options", "cc_kernel_times", "cc_dataflow_state", "cc_dataflow_profile", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
             "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_bb1", "cc_bt2", "cc_bb3", "cc_mm1_ozaki", "cc_mm1_ozaki_workspace_bytes", "cc_i8gemm_tn", "cc_gemm_ozaki",
             "cc_gemm_ozaki_workspace_bytes", "cc_fill_synthetic", "cc_scratch_bytes"]
@@ -254,7 +260,9 @@ class Context:
         return list(out[:n.value])
 
     # --- schedule / plan -----------------------------------------------------------------
-    def schedule(self, algo=CC_TREE, cap_bytes=0, given=None, evict_next_use=False):
+    def schedule(self, algo=CC_TREE, cap_bytes=0, given=None, evict_next_use=False, peer_cap_bytes=0,
+                 peer_leaves=()):
+        """peer_cap_bytes / peer_leaves: the peer-HBM tier (readings E-10, E-11; cc.h)."""
         cfg = cc_sched_cfg()
         cfg.algo = algo
         cfg.flags = CC_EVICT_NEXT_USE if evict_next_use else 0
@@ -263,6 +271,12 @@ class Context:
             g = (c_i64 * max(len(given), 1))(*given)
             cfg.given_order = ctypes.cast(g, P(c_i64))
             cfg.n_given = len(given)
+        cfg.peer_cap_bytes = int(peer_cap_bytes or 0)
+        pl = sorted(int(x) for x in peer_leaves)
+        if pl:
+            parr = (c_i64 * len(pl))(*pl)
+            cfg.peer_leaves = ctypes.cast(parr, P(c_i64))
+            cfg.n_peer_leaves = len(pl)
         n = c_i64()
         stats = cc_plan_stats()
         self._ck(_lib.cc_schedule(self._h, ctypes.byref(cfg), None, 0, ctypes.byref(n), ctypes.byref(stats)))
@@ -305,6 +319,30 @@ class Context:
     def set_leaf_device(self, leaf_id, dev, nbytes=None):
         nbytes = nbytes if nbytes is not None else dev.numel() * dev.element_size()
         self._ck(_lib.cc_set_leaf_device(self._h, leaf_id, _ptr(dev), nbytes))
+
+    def set_leaf_peer(self, leaf_id, dev, nbytes=None):
+        """E-11: the leaf's full copy in (a peer GPU's) device memory; dev is a torch tensor or
+        an integer device address (e.g. a CUDA IPC mapping)."""
+        if isinstance(dev, int):
+            ptr = dev
+            assert nbytes is not None
+        else:
+            ptr = _ptr(dev)
+            nbytes = nbytes if nbytes is not None else dev.numel() * dev.element_size()
+        self._ck(_lib.cc_set_leaf_peer(self._h, leaf_id, ptr, nbytes))
+
+    def set_peer_tier(self, dev, nbytes=None):
+        """E-10: the peer-HBM eviction tier region (torch tensor or integer address; None: remove)."""
+        if dev is None:
+            self._ck(_lib.cc_set_peer_tier(self._h, None, 0))
+            return
+        if isinstance(dev, int):
+            ptr = dev
+            assert nbytes is not None
+        else:
+            ptr = _ptr(dev)
+            nbytes = nbytes if nbytes is not None else dev.numel() * dev.element_size()
+        self._ck(_lib.cc_set_peer_tier(self._h, ptr, nbytes))
 
     def execute(self, flags=0):
         s = cc_exec_stats()

@@ -197,7 +197,23 @@ cc_status cc_schedule(cc_ctx* ctx, const cc_sched_cfg* cfg, int64_t* order_out, 
   auto t1 = std::chrono::steady_clock::now();
   check_order(g, order);
   ctx->mt = simulate_model(g, order);
-  ctx->lp = lru_plan(g, order, cfg->cap_bytes, (cfg->flags & CC_EVICT_NEXT_USE) ? EVICT_NEXT_USE : EVICT_LRU);
+  if (cfg->peer_cap_bytes < 0 || cfg->n_peer_leaves < 0 || (cfg->n_peer_leaves > 0 && !cfg->peer_leaves))
+    throw Error(CC_E_INVAL, "bad peer tier configuration");
+  std::vector<uint8_t> peer_home(g.nodes.size(), 0);
+  for (int64_t i = 0; i < cfg->n_peer_leaves; ++i) {
+    auto it = g.index.find(cfg->peer_leaves[i]);
+    if (it == g.index.end()) {
+      bool other_part = false;   // a leaf of another TREES part: ignored
+      for (const auto& nn : ctx->input.nodes) other_part |= nn.id == cfg->peer_leaves[i];
+      if (!other_part) throw Error(CC_E_UNKNOWN_NODE, "unknown peer leaf " + std::to_string(cfg->peer_leaves[i]));
+      continue;
+    }
+    if (!g.nodes[size_t(it->second)].leaf()) throw Error(CC_E_INVAL, "peer leaf " + std::to_string(cfg->peer_leaves[i]) + " is not a leaf");
+    peer_home[size_t(it->second)] = 1;
+  }
+  ctx->lp = lru_plan(g, order, cfg->cap_bytes, (cfg->flags & CC_EVICT_NEXT_USE) ? EVICT_NEXT_USE : EVICT_LRU,
+                     cfg->peer_cap_bytes, &peer_home);
+  ctx->peer_home = std::move(peer_home);
   auto t2 = std::chrono::steady_clock::now();
   ctx->order = std::move(order);
   ctx->tree_order = std::move(tree_order);
@@ -213,6 +229,11 @@ cc_status cc_schedule(cc_ctx* ctx, const cc_sched_cfg* cfg, int64_t* order_out, 
   s.h2d_bytes = ctx->lp.h2d_bytes;
   s.d2h_bytes = ctx->lp.d2h_bytes;
   s.host_peak_bytes = ctx->lp.host_peak;
+  s.p2p_out_count = ctx->lp.p2p_out_count;
+  s.p2p_out_bytes = ctx->lp.p2p_out_bytes;
+  s.p2p_in_count = ctx->lp.p2p_in_count;
+  s.p2p_in_bytes = ctx->lp.p2p_in_bytes;
+  s.peer_peak_bytes = ctx->lp.peer_peak;
   s.model_peak = ctx->mt.peak;
   s.model_transient_peak = ctx->mt.transient_peak;
   s.sched_seconds = std::chrono::duration<double>(t1 - t0).count();
@@ -317,6 +338,38 @@ cc_status cc_set_leaf(cc_ctx* ctx, int64_t leaf_id, const void* host, size_t byt
     ctx->release_graph();
   }
   ctx->release_graph();  // host pointers are baked into a captured graph
+  API_END
+}
+
+cc_status cc_set_leaf_peer(cc_ctx* ctx, int64_t leaf_id, const void* dev, size_t bytes) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->loaded) throw Error(CC_E_STATE, "no DAG loaded");
+  const Dag& g = *ctx->dag;
+  auto it = g.index.find(leaf_id);
+  if (it == g.index.end()) {
+    for (const auto& n : ctx->input.nodes)
+      if (n.id == leaf_id) return CC_OK;   // a leaf of another TREES part
+    throw Error(CC_E_UNKNOWN_NODE, "unknown leaf " + std::to_string(leaf_id));
+  }
+  const Node& n = g.nodes[size_t(it->second)];
+  if (!n.leaf()) throw Error(CC_E_INVAL, "node " + std::to_string(leaf_id) + " is not a leaf");
+  const int64_t full = tensor_bytes(n.op, ctx->input.dims.Lt, g.N, g.S);
+  if (int64_t(bytes) != full) throw Error(CC_E_INVAL, "leaf " + std::to_string(leaf_id) + ": expected " + std::to_string(full) + " bytes");
+  if (!dev) throw Error(CC_E_INVAL, "null peer pointer");
+  ctx->leaf_peer[size_t(it->second)] = dev;
+  ctx->release_graph();  // copy sources are baked into a captured graph
+  API_END
+}
+
+cc_status cc_set_peer_tier(cc_ctx* ctx, void* dev, size_t bytes) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if ((dev == nullptr) != (bytes == 0)) throw Error(CC_E_INVAL, "peer tier: pointer and size must both be set or both be 0");
+  ctx->peer_tier = static_cast<char*>(dev);
+  ctx->peer_tier_bytes = int64_t(bytes);
+  ctx->phys_valid = false;
+  ctx->release_graph();
   API_END
 }
 

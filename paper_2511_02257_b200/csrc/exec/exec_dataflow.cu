@@ -97,13 +97,21 @@ std::pair<const void*, void*> copy_endpoints(cc_ctx* ctx, const PhysOp& op) {
     }
     return {ctx->host_pool + op.host_off, ctx->arena + op.dev_off};
   }
+  if (op.kind == OP_P2P_IN)   // peer tier (E-10) or a peer-homed leaf (E-11)
+    return {op.peer_off >= 0 ? static_cast<const void*>(ctx->peer_tier + op.peer_off) : peer_leaf_src(ctx, op.node),
+            ctx->arena + op.dev_off};
+  if (op.kind == OP_P2P_OUT) return {ctx->arena + op.dev_off, ctx->peer_tier + op.peer_off};
   return {ctx->arena + op.dev_off, ctx->host_pool + op.host_off};
+}
+cudaMemcpyKind copy_kind(int32_t op_kind) {
+  return op_kind == OP_H2D ? cudaMemcpyHostToDevice : op_kind == OP_D2H ? cudaMemcpyDeviceToHost : cudaMemcpyDefault;
 }
 
 // One plan copy on `s`: C time-slice chunks, each followed by a flag write (value = chunks
 // done) — the dataflow worker's items wait on the flag (chunk of their slice, kernels/dataflow.hpp).
-void enqueue_copy(cc_ctx* ctx, cudaStream_t s, const void* src, void* dst, size_t bytes, cudaMemcpyKind kind,
+void enqueue_copy(cc_ctx* ctx, cudaStream_t s, const void* src, void* dst, size_t bytes, int32_t op_kind,
                   int32_t chunks, int32_t flag_slot) {
+  const cudaMemcpyKind kind = copy_kind(op_kind);
   const Dag& g = *ctx->dag;
   const size_t per_t = bytes / size_t(std::max<int64_t>(g.Lt, 1));
   for (int32_t ch = 0; ch < chunks; ++ch) {
@@ -111,8 +119,11 @@ void enqueue_copy(cc_ctx* ctx, cudaStream_t s, const void* src, void* dst, size_
     const size_t t0 = chunks == 1 ? 0 : size_t(int64_t(ch) * g.Lt / chunks);
     const size_t t1 = chunks == 1 ? 0 : size_t(int64_t(ch + 1) * g.Lt / chunks);
     const size_t off = t0 * per_t, len = chunks == 1 ? bytes : (t1 - t0) * per_t;
+    // a device-to-device copy (peer tier, peer-homed leaf, kind Default) may run as a copy
+    // kernel, which could never start while the persistent worker holds every SM: the worker
+    // leaves one SM free when the plan has peer copies (issue_dataflow)
     ck(cudaMemcpyAsync(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, len, kind, s), "copy");
-    ctx->count_copy(kind == cudaMemcpyHostToDevice, int64_t(len));
+    ctx->count_op_copy(op_kind, int64_t(len));
     if (df_write_fn()(s, reinterpret_cast<CUdeviceptr>(ctx->df_sync + flag_slot), cuuint32_t(ch + 1), 0) != CUDA_SUCCESS)
       throw Error(CC_E_CUDA, "cuStreamWriteValue32 failed");
   }
@@ -194,7 +205,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
         is_early[size_t(i)] = 1;
         early_seq.push_back(i);
       }
-      if (op.kind == OP_H2D || op.kind == OP_D2H) touch(op.dev_off, rb);
+      if (op.kind == OP_H2D || op.kind == OP_D2H || op.kind == OP_P2P_IN || op.kind == OP_P2P_OUT) touch(op.dev_off, rb);
       if (op.kind == OP_CONTRACT) {
         if (op.loc_a == LOC_POOL) touch(op.off_a, round_up(g.nodes[size_t(n.l)].size, ALIGN));
         if (op.loc_b == LOC_POOL) touch(op.off_b, round_up(g.nodes[size_t(n.r)].size, ALIGN));
@@ -221,7 +232,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
       if (pre == 0) {
         const int32_t i = early_seq[0];
         const auto ep = copy_endpoints(ctx, ops[size_t(i)]);
-        enqueue_copy(ctx, ctx->hs, ep.first, ep.second, size_t(ops[size_t(i)].bytes), cudaMemcpyHostToDevice,
+        enqueue_copy(ctx, ctx->hs, ep.first, ep.second, size_t(ops[size_t(i)].bytes), OP_H2D,
                      target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
         n_first = 1;
       } else {
@@ -305,13 +316,14 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
       if (q_issued++ < size_t(n_first)) continue;     // enqueued before the ordering
       const auto ep = copy_endpoints(ctx, op);
       enqueue_copy(ctx, ctx->hs, ep.first, ep.second, size_t(op.bytes),
-                   cudaMemcpyHostToDevice, target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
+                   OP_H2D, target[size_t(i)] < 0 ? -target[size_t(i)] : 1, slot[size_t(i)]);
     }
     ctx->df_early_active = true;
   }
   tmr.lap("early copies");
   // 1. data dependencies over the device pool and the host pool
-  RWTracker dev(ctx->pool_bytes), host(std::max<int64_t>(ctx->pp.host_pool_bytes, 1));
+  RWTracker dev(ctx->pool_bytes), host(std::max<int64_t>(ctx->pp.host_pool_bytes, 1)),
+      peer(std::max<int64_t>(ctx->peer_tier_bytes, 1));
   std::vector<std::vector<int32_t>> deps(static_cast<size_t>(n_ops));
   // writers of contraction operands: pool writer op, -1 never written, -2 caller device leaf
   std::vector<int32_t> wr_a(size_t(n_ops), -1), wr_b(size_t(n_ops), -1);
@@ -326,6 +338,12 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     } else if (op.kind == OP_D2H) {
       dev.read(op.dev_off, rb, i, d);
       host.write(op.host_off, rb, i, d);
+    } else if (op.kind == OP_P2P_IN && op.stream != S_NONE) {
+      dev.write(op.dev_off, rb, i, d);
+      if (op.peer_off >= 0) peer.read(op.peer_off, rb, i, d);
+    } else if (op.kind == OP_P2P_OUT && op.stream != S_NONE) {
+      dev.read(op.dev_off, rb, i, d);
+      peer.write(op.peer_off, rb, i, d);
     } else if (op.kind == OP_CONTRACT) {
       const int64_t sa = round_up(g.nodes[size_t(n.l)].size, ALIGN), sb = round_up(g.nodes[size_t(n.r)].size, ALIGN);
       wr_a[size_t(i)] = op.loc_a == LOC_POOL ? dev.last_writer(op.off_a, sa) : (op.loc_a == LOC_DEVLEAF ? -2 : -1);
@@ -807,6 +825,8 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
   ctx->df_valid = true;
 }
 
+static int32_t ops_kind_of(cc_ctx* ctx, int32_t op) { return ctx->pp.ops[size_t(op)].kind; }
+
 // Enqueues one dataflow replay; returns the number of kernel launches.
 int issue_dataflow(cc_ctx* ctx, bool time_copies) {
   const Dag& g = *ctx->dag;
@@ -824,7 +844,9 @@ int issue_dataflow(cc_ctx* ctx, bool time_copies) {
   // counters, and a driver can stall the host's enqueue of further memory ops until the
   // device makes progress — so the kernel they wait for must already be queued.
   if (ctx->df_gemm_items + ctx->df_trace_items > 0) {
-    ck(df_launch(ctx->df_gemm, ctx->num_sms, ctx->cs), "dataflow worker");
+    // one SM stays free when the plan has peer (device-to-device) copies (see enqueue_copy)
+    const bool p2p = ctx->pp.p2p_in_bytes > 0 || ctx->pp.p2p_out_bytes > 0;
+    ck(df_launch(ctx->df_gemm, ctx->num_sms - (p2p ? 1 : 0), ctx->cs), "dataflow worker");
     DBG("worker launched");
     ++nl;
     if (ctx->df_n_fused > 0) {
@@ -845,8 +867,7 @@ int issue_dataflow(cc_ctx* ctx, bool time_copies) {
     DBG("copy %zu: stream %d bytes %zu waits %zu/%zu", k, c.stream, c.bytes, c.wait_values.size(), c.wait_events.size());
     // copies started during preparation (flags included) are skipped
     if (!(ctx->df_early_active && ctx->df_early[size_t(c.op)]))
-      enqueue_copy(ctx, s, c.src, c.dst, c.bytes, c.stream == S_H2D ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
-                   c.chunks, c.flag_slot);
+      enqueue_copy(ctx, s, c.src, c.dst, c.bytes, ops_kind_of(ctx, c.op), c.chunks, c.flag_slot);
     DBG("copy %zu enqueued", k);
     if (c.source) ck(cudaEventRecord(ctx->df_events[k], s), "event");
   }

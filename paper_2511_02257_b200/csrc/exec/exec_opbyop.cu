@@ -140,6 +140,19 @@ int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cud
         ctx->count_copy(true, op.bytes);
         break;
       }
+      case OP_P2P_IN: {
+        // from the peer tier (stashed tensor) or the leaf's peer home copy (E-10, E-11)
+        const void* src = op.peer_off >= 0 ? static_cast<const void*>(ctx->peer_tier + op.peer_off)
+                                           : peer_leaf_src(ctx, op.node);
+        ck(cudaMemcpyAsync(ctx->arena + op.dev_off, src, size_t(op.bytes), cudaMemcpyDefault, s), "P2P in");
+        ctx->count_op_copy(OP_P2P_IN, op.bytes);
+        break;
+      }
+      case OP_P2P_OUT:
+        ck(cudaMemcpyAsync(ctx->peer_tier + op.peer_off, ctx->arena + op.dev_off, size_t(op.bytes), cudaMemcpyDefault, s),
+           "P2P out");
+        ctx->count_op_copy(OP_P2P_OUT, op.bytes);
+        break;
       case OP_D2H:
         ctx->count_copy(false, op.bytes);
         ck(cudaMemcpyAsync(ctx->host_pool + op.host_off, ctx->arena + op.dev_off, size_t(op.bytes),

@@ -19,7 +19,7 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   // land in scratch or outside the arena; if preparation fails, the compute stream is ordered
   // after the stray copies before the error returns.
   ctx->pre_n = 0;
-  ctx->run_h2d = ctx->run_d2h = 0;
+  ctx->run_h2d = ctx->run_d2h = ctx->run_p2p_in = ctx->run_p2p_out = 0;
   std::vector<int64_t> pre_off;
   if (ctx->opt.precopy && ctx->opt.early_copies && ctx->opt.h2d_chunk_bytes == 0 && !ctx->phys_valid &&
       !ctx->dag->abstract && !(flags & (2 | 4 | 8 | 16 | 64 | 128))) {
@@ -144,9 +144,13 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
       cudaGraphDestroy(graph);
       ctx->graph_h2d = ctx->run_h2d;     // the copies the graph carries
       ctx->graph_d2h = ctx->run_d2h;
+      ctx->graph_p2p_in = ctx->run_p2p_in;
+      ctx->graph_p2p_out = ctx->run_p2p_out;
     } else {
       ctx->run_h2d = ctx->graph_h2d;
       ctx->run_d2h = ctx->graph_d2h;
+      ctx->run_p2p_in = ctx->graph_p2p_in;
+      ctx->run_p2p_out = ctx->graph_p2p_out;
     }
     ck(cudaGraphLaunch(ctx->gexec, ctx->cs), "graph launch");
   } else {
@@ -179,6 +183,8 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
       }
     stats->h2d_bytes = ctx->run_h2d;      // counted as enqueued (the plan's: cc_plan_stats)
     stats->d2h_bytes = ctx->run_d2h;
+    stats->p2p_in_bytes = ctx->run_p2p_in;
+    stats->p2p_out_bytes = ctx->run_p2p_out;
     stats->n_kernels = ctx->last_n_kernels;
   }
   ctx->ktimes = KindTimes{};

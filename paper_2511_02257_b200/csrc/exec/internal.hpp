@@ -111,6 +111,10 @@ struct cc_ctx {
   int64_t cap = 0;
 
   std::vector<const void*> leaf_host, leaf_dev;
+  std::vector<const void*> leaf_peer;   // peer-homed leaves' device copies (E-11), cc_set_leaf_peer
+  std::vector<uint8_t> peer_home;       // leaves the current plan fetches from a peer (E-11)
+  char* peer_tier = nullptr;            // peer-HBM eviction tier region (E-10), cc_set_peer_tier
+  int64_t peer_tier_bytes = 0;
 
   // physical state
   bool phys_valid = false;
@@ -142,9 +146,15 @@ struct cc_ctx {
   int64_t last_n_kernels = 0;
   // plan copies counted as they are enqueued (cc_exec_stats h2d/d2h: runtime counts, not the
   // plan's): the current execute's, and those baked into each cached graph
-  int64_t run_h2d = 0, run_d2h = 0;
-  int64_t graph_h2d = 0, graph_d2h = 0;   // gexec (op-by-op graph)
+  int64_t run_h2d = 0, run_d2h = 0, run_p2p_in = 0, run_p2p_out = 0;
+  int64_t graph_h2d = 0, graph_d2h = 0, graph_p2p_in = 0, graph_p2p_out = 0;   // gexec (op-by-op graph)
   void count_copy(bool h2d, int64_t bytes) { (h2d ? run_h2d : run_d2h) += bytes; }
+  // a plan copy of kind OP_H2D / OP_D2H / OP_P2P_IN / OP_P2P_OUT, counted as enqueued
+  void count_op_copy(int32_t kind, int64_t bytes) {
+    if (kind == OP_P2P_IN) run_p2p_in += bytes;
+    else if (kind == OP_P2P_OUT) run_p2p_out += bytes;
+    else count_copy(kind == OP_H2D, bytes);
+  }
 
   // dataflow execution (persistent workers): device metadata + per-launch sync area
   bool df_valid = false;
@@ -280,5 +290,15 @@ int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cud
           std::vector<int>* kev_kind);
 void kernel_only(cc_ctx* ctx, int cls, cc_exec_stats* stats);
 void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats);
+// Source of a P2P_IN of a peer-homed leaf (E-11): this part's time slices of the caller's copy.
+inline const void* peer_leaf_src(cc_ctx* ctx, int32_t u) {
+  const Dag& g = *ctx->dag;
+  const Node& n = g.nodes[size_t(u)];
+  const char* p = static_cast<const char*>(ctx->leaf_peer[size_t(u)]);
+  if (!p) throw Error(CC_E_STATE, "leaf " + std::to_string(n.id) + " has no peer copy (cc_set_leaf_peer)");
+  const int64_t per_t_m = 16LL * g.N * g.N;
+  const int64_t per_t = n.op == CC_LEAF_M ? per_t_m : per_t_m * g.S * g.N;
+  return p + int64_t(ctx->t0) * per_t;
+}
 }  // namespace ccx
 

@@ -33,6 +33,8 @@ void rebuild_dag(cc_ctx* ctx) {
   const size_t n = ctx->dag->nodes.size();
   ctx->leaf_host.assign(n, nullptr);
   ctx->leaf_dev.assign(n, nullptr);
+  ctx->leaf_peer.assign(n, nullptr);
+  ctx->peer_home.assign(n, 0);
   ctx->scheduled = false;
   ctx->executed = false;
   ctx->phys_valid = false;
@@ -258,11 +260,16 @@ void prepare_phys(cc_ctx* ctx) {
   // physical footprint follows the logical one; the logical plan is unchanged either way.
   int64_t phys_limit = pool;
   if (ctx->cap > 0) phys_limit = std::min(pool, round_up(ctx->cap + ctx->cap / 4, ALIGN));
+  if (ctx->lp.p2p_out_count > 0 && !ctx->peer_tier)
+    throw Error(CC_E_STATE, "the plan evicts to the peer tier and no region is set (cc_set_peer_tier)");
+  for (size_t u = 0; u < g.nodes.size(); ++u)
+    if (u < ctx->peer_home.size() && ctx->peer_home[u] && !on_dev[u] && !ctx->leaf_peer[u])
+      throw Error(CC_E_STATE, "peer-homed leaf " + std::to_string(g.nodes[u].id) + " has no peer copy (cc_set_leaf_peer)");
   try {
-    ctx->pp = build_phys(g, ctx->lp, on_dev, phys_limit, ALIGN, RangeAlloc::NEXT_FIT);
+    ctx->pp = build_phys(g, ctx->lp, on_dev, phys_limit, ALIGN, RangeAlloc::NEXT_FIT, ctx->peer_tier_bytes);
   } catch (const Error& e) {
     if (e.status != CC_E_NOMEM) throw;
-    ctx->pp = build_phys(g, ctx->lp, on_dev, pool, ALIGN, RangeAlloc::BEST_FIT);
+    ctx->pp = build_phys(g, ctx->lp, on_dev, pool, ALIGN, RangeAlloc::BEST_FIT, ctx->peer_tier_bytes);
   }
   ctx->stats.arena_high_water = ctx->pp.pool_high_water;
   pt.lap("build_phys");

@@ -10,6 +10,10 @@
 //   leaves are dropped (no D2H), an intermediate is copied to host on its first eviction
 //   and the host copy is kept until release; fetches are touches; LRU ties cannot occur
 //   (one clock tick per touch: operands left then right, then the output).
+//   Peer-HBM tier (readings E-10, E-11): a victim with no copy off the device other than a
+//   leaf's caller host copy goes to the peer tier (P2P_OUT) while peer_cap has room, and its
+//   re-fetches are P2P_IN; the peer copy lives until release.  Peer-homed leaves are always
+//   fetched P2P_IN and dropped on eviction.
 // build_phys: offline placement of every residency in the device pool (best fit) and the
 //   host pool, plus cross-stream event dependencies: RAW on data (ready op of each operand,
 //   D2H before a re-fetch) and WAR/WAW on reused byte ranges.
@@ -74,13 +78,16 @@ ModelTrace simulate_model(const Dag& g, const std::vector<int32_t>& order) {
   return tr;
 }
 
-LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap, EvictPolicy policy) {
+LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap, EvictPolicy policy, int64_t peer_cap,
+                 const std::vector<uint8_t>* peer_home) {
   const bool bounded = cap > 0;
   const bool next_use = policy == EVICT_NEXT_USE;
   const size_t n = g.nodes.size();
   LruPlan p;
   std::vector<int32_t> remaining(n);
-  std::vector<uint8_t> resident(n, 0), host_copy(n, 0);
+  std::vector<uint8_t> resident(n, 0), host_copy(n, 0), peer_copy(n, 0);
+  auto homed = [&](int32_t x) { return peer_home && (*peer_home)[size_t(x)] != 0; };
+  int64_t peer_used = 0;
   std::vector<int64_t> stamp(n, 0);
   for (size_t u = 0; u < n; ++u) remaining[u] = int32_t(g.nodes[u].parents.size());
   // E-9: the steps reading each tensor, in order (CSR), and a cursor to its next use
@@ -128,7 +135,16 @@ LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap, E
       const int32_t v = it->second;
       lru.erase(it);
       ++p.evictions;
-      if (!g.nodes[v].leaf() && !host_copy[v]) {    // E-4: first eviction copies to host
+      const int64_t vs = g.nodes[v].size;
+      const bool stash = !peer_copy[v] && !homed(v) && !host_copy[v];
+      if (stash && peer_used + vs <= peer_cap) {      // E-10: copy to the peer tier
+        ++p.p2p_out_count;
+        p.p2p_out_bytes += vs;
+        peer_copy[v] = 1;
+        peer_used += vs;
+        p.peer_peak = std::max(p.peer_peak, peer_used);
+        p.ops.push_back({OP_P2P_OUT, v});
+      } else if (!g.nodes[v].leaf() && stash) {       // E-4: first eviction copies to host
         ++p.d2h_count;
         p.d2h_bytes += g.nodes[v].size;
         host_copy[v] = 1;
@@ -146,10 +162,16 @@ LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap, E
     for (int32_t x : ops) ++cursor[size_t(x)];
     for (int32_t x : ops) {                          // fetch + touch, left then right (E-2)
       if (!resident[x]) {
-        ++p.h2d_count;
-        p.h2d_bytes += g.nodes[x].size;
+        if (peer_copy[x] || homed(x)) {              // E-10 / E-11: over NVLink
+          ++p.p2p_in_count;
+          p.p2p_in_bytes += g.nodes[x].size;
+          p.ops.push_back({OP_P2P_IN, x});
+        } else {
+          ++p.h2d_count;
+          p.h2d_bytes += g.nodes[x].size;
+          p.ops.push_back({OP_H2D, x});
+        }
         used += g.nodes[x].size;
-        p.ops.push_back({OP_H2D, x});
         resident[x] = 1;
       }
       stamp[x] = ++clock;
@@ -168,6 +190,10 @@ LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap, E
           host_copy[x] = 0;
           host -= g.nodes[x].size;
         }
+        if (peer_copy[x]) {
+          peer_copy[x] = 0;
+          peer_used -= g.nodes[x].size;
+        }
         p.ops.push_back({OP_FREE, x});
       }
     for (int32_t x : ops)
@@ -182,7 +208,7 @@ LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap, E
     p.peak = std::max(p.peak, used);
     p.used.push_back(used);
   }
-  if (used != 0 || host != 0) throw Error(CC_E_STATE, "plan: accounting did not return to zero");
+  if (used != 0 || host != 0 || peer_used != 0) throw Error(CC_E_STATE, "plan: accounting did not return to zero");
   return p;
 }
 
@@ -292,17 +318,17 @@ void RangeTracker::access(int64_t off, int64_t bytes, int stream, int32_t op, st
 static int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>& leaf_on_device,
-                    int64_t pool_bytes, int64_t align, RangeAlloc::Policy policy) {
+                    int64_t pool_bytes, int64_t align, RangeAlloc::Policy policy, int64_t peer_bytes) {
   PhysPlan pp;
   const size_t n = g.nodes.size();
   // host pool: sized for the worst case (sum of all D2H'd sizes), placed best-fit
   int64_t host_cap = 0;
   for (const auto& op : lp.ops)
     if (op.kind == OP_D2H) host_cap += round_up(g.nodes[op.node].size, align);
-  RangeAlloc dev(pool_bytes, policy), hostp(host_cap);
-  RangeTracker dtr(pool_bytes), htr(std::max<int64_t>(host_cap, 1));
-  std::vector<int64_t> dev_off(n, -1), host_off(n, -1);
-  std::vector<int32_t> ready(n, -1), ready_stream(n, -1), d2h_op(n, -1);
+  RangeAlloc dev(pool_bytes, policy), hostp(host_cap), peerp(peer_bytes);
+  RangeTracker dtr(pool_bytes), htr(std::max<int64_t>(host_cap, 1)), ptr(std::max<int64_t>(peer_bytes, 1));
+  std::vector<int64_t> dev_off(n, -1), host_off(n, -1), peer_off(n, -1);
+  std::vector<int32_t> ready(n, -1), ready_stream(n, -1), d2h_op(n, -1), p2p_op(n, -1);
   auto need_ready = [&](int32_t x, int stream, std::vector<int32_t>& deps) {
     if (ready[x] >= 0 && ready_stream[x] != stream) deps.push_back(ready[x]);
   };
@@ -330,6 +356,41 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
         ready[x] = me;
         ready_stream[x] = S_H2D;
         pp.h2d_bytes += nd.size;
+        break;
+      }
+      case OP_P2P_IN: {
+        if (nd.leaf() && leaf_on_device[x]) break;            // already in HBM: no copy
+        const int64_t off = dev.alloc(rb);
+        if (off < 0) throw Error(CC_E_NOMEM, "device pool fragmented/too small for node " + std::to_string(nd.id));
+        dev_off[x] = off;
+        op.stream = S_H2D;                                      // inbound copies share the H2D stream
+        op.dev_off = off;
+        dtr.access(off, rb, S_H2D, me, op.deps, &op.same_deps);
+        if (peer_off[x] >= 0) {                                 // stashed copy in the peer tier
+          op.peer_off = peer_off[x];
+          if (p2p_op[x] >= 0) op.deps.push_back(p2p_op[x]);
+          ptr.access(peer_off[x], rb, S_H2D, me, op.deps, &op.same_deps);
+        }
+        ready[x] = me;
+        ready_stream[x] = S_H2D;
+        pp.p2p_in_bytes += nd.size;
+        break;
+      }
+      case OP_P2P_OUT: {
+        if (nd.leaf() && leaf_on_device[x]) break;            // caller device leaf: nothing to move
+        const int64_t poff = peerp.alloc(rb);
+        if (poff < 0) throw Error(CC_E_NOMEM, "peer tier fragmented/too small for node " + std::to_string(nd.id));
+        peer_off[x] = poff;
+        op.stream = S_D2H;                                      // outbound copies share the D2H stream
+        op.dev_off = dev_off[x];
+        op.peer_off = poff;
+        need_ready(x, S_D2H, op.deps);
+        dtr.access(dev_off[x], rb, S_D2H, me, op.deps);
+        ptr.access(poff, rb, S_D2H, me, op.deps);
+        p2p_op[x] = me;
+        dev.free(dev_off[x], rb);
+        dev_off[x] = -1;
+        pp.p2p_out_bytes += nd.size;
         break;
       }
       case OP_D2H: {
@@ -395,6 +456,10 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
           hostp.free(host_off[x], rb);
           host_off[x] = -1;
         }
+        if (peer_off[x] >= 0) {
+          peerp.free(peer_off[x], rb);
+          peer_off[x] = -1;
+        }
         break;
       }
     }
@@ -410,6 +475,7 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
   }
   pp.pool_high_water = dev.high_water();
   pp.host_pool_bytes = host_cap;
+  pp.peer_high_water = peerp.high_water();
   return pp;
 }
 

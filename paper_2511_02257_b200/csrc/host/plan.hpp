@@ -18,7 +18,9 @@ ModelTrace simulate_model(const Dag& g, const std::vector<int32_t>& order);
 // Throws CC_E_INVAL when `order` is not a valid schedule of g.
 void check_order(const Dag& g, const std::vector<int32_t>& order);
 
-enum OpKind : int32_t { OP_H2D = 0, OP_D2H = 1, OP_DROP = 2, OP_CONTRACT = 3, OP_FREE = 4 };
+// OP_P2P_OUT: eviction copied to the peer-HBM tier; OP_P2P_IN: fetch from a peer GPU's HBM
+// (a stashed tensor or a peer-homed leaf) — readings E-10, E-11.
+enum OpKind : int32_t { OP_H2D = 0, OP_D2H = 1, OP_DROP = 2, OP_CONTRACT = 3, OP_FREE = 4, OP_P2P_OUT = 5, OP_P2P_IN = 6 };
 struct LogicalOp { int32_t kind; int32_t node; };
 
 // Capacity-limited LRU plan, readings E-1..E-8.
@@ -27,9 +29,13 @@ struct LruPlan {
   std::vector<int64_t> used;         // device bytes after each contraction's releases
   int64_t evictions = 0, h2d_count = 0, d2h_count = 0, h2d_bytes = 0, d2h_bytes = 0;
   int64_t peak = 0, transient_peak = 0, host_peak = 0;
+  int64_t p2p_out_count = 0, p2p_out_bytes = 0, p2p_in_count = 0, p2p_in_bytes = 0, peer_peak = 0;
 };
 enum EvictPolicy { EVICT_LRU = 0, EVICT_NEXT_USE = 1 };
-LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap, EvictPolicy policy = EVICT_LRU);
+// peer_cap: bytes of the peer-HBM eviction tier (E-10; 0: none); peer_home[u] != 0: leaf u's
+// home copy is in a peer GPU's HBM (E-11; nullptr: none).
+LruPlan lru_plan(const Dag& g, const std::vector<int32_t>& order, int64_t cap, EvictPolicy policy = EVICT_LRU,
+                 int64_t peer_cap = 0, const std::vector<uint8_t>* peer_home = nullptr);
 
 // Allocator with coalescing over [0, capacity).  BEST_FIT packs tightly; NEXT_FIT takes
 // the first block that fits at or after a rotating cursor (wrapping once), so freed memory
@@ -78,6 +84,8 @@ struct PhysOp {
   int64_t bytes = 0;
   int64_t dev_off = -1;              // pool offset of the tensor this op moves / produces
   int64_t host_off = -1;             // host-pool offset (evicted intermediates), -1: caller leaf
+  int64_t peer_off = -1;             // peer-tier offset (P2P_OUT / P2P_IN of a stashed tensor),
+                                     // -1: a peer-homed leaf (P2P_IN from the caller's peer copy)
   int32_t loc_a = LOC_POOL, loc_b = LOC_POOL;
   int64_t off_a = -1, off_b = -1;    // operand pool offsets (CONTRACT)
   std::vector<int32_t> deps;         // ops on other streams that must complete first
@@ -88,11 +96,14 @@ struct PhysOp {
 
 struct PhysPlan {
   std::vector<PhysOp> ops;
-  int64_t pool_high_water = 0, host_pool_bytes = 0;
-  int64_t h2d_bytes = 0, d2h_bytes = 0;   // bytes physically copied
+  int64_t pool_high_water = 0, host_pool_bytes = 0, peer_high_water = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0, p2p_in_bytes = 0, p2p_out_bytes = 0;   // bytes physically copied
 };
-// leaf_on_device[u]: the leaf is a caller device buffer (no H2D / no pool space).
+// leaf_on_device[u]: the leaf is a caller device buffer (no copy / no pool space).
+// peer_bytes: size of the peer-tier region P2P_OUT copies are placed in (best fit;
+// CC_E_NOMEM when fragmentation leaves no block).
 PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>& leaf_on_device,
-                    int64_t pool_bytes, int64_t align, RangeAlloc::Policy policy = RangeAlloc::BEST_FIT);
+                    int64_t pool_bytes, int64_t align, RangeAlloc::Policy policy = RangeAlloc::BEST_FIT,
+                    int64_t peer_bytes = 0);
 
 }  // namespace cc

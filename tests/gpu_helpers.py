@@ -23,9 +23,11 @@ def to_numpy_c(t, shape):
 
 
 def run_gpu(w, algo=None, cap=0, flags=0, device_leaves=False, arena_mb=256, leaf_fn=None, ctx=None,
-            part=None, evict_next_use=False, options=None):
+            part=None, evict_next_use=False, options=None, peer_cap=0, peer_leaves=(), peer_tier_mb=0):
     """Returns (ctx, roots{tree: [Lt]}, corr{c: [Lt]}, plan stats, exec stats).
-    options: executor options for cc_set_options (cc.h cc_options), e.g. {"trace_fusion": 1}."""
+    options: executor options for cc_set_options (cc.h cc_options), e.g. {"trace_fusion": 1}.
+    peer_cap / peer_leaves / peer_tier_mb: the peer-HBM tier (E-10, E-11) with its region and the
+    peer-homed leaves' copies as buffers on this GPU (a loopback stand-in for a peer GPU's HBM)."""
     import torch
     from paper_2511_02257_b200 import cc
     dag = Dag(w)
@@ -37,8 +39,13 @@ def run_gpu(w, algo=None, cap=0, flags=0, device_leaves=False, arena_mb=256, lea
     ctx.load_workload(w)
     if part is not None:
         ctx.partition(*part)
-    order, st = ctx.schedule(cc.CC_TREE if algo is None else algo, cap_bytes=cap, evict_next_use=evict_next_use)
+    order, st = ctx.schedule(cc.CC_TREE if algo is None else algo, cap_bytes=cap, evict_next_use=evict_next_use,
+                             peer_cap_bytes=peer_cap, peer_leaves=peer_leaves)
     keep = []
+    if peer_tier_mb:
+        tier = torch.empty(peer_tier_mb << 20, dtype=torch.uint8, device="cuda")
+        keep.append(tier)
+        ctx.set_peer_tier(tier)
     Lt_part = w.Lt
     t0 = 0
     if part is not None and part[2] == cc.PART_TIME:
@@ -53,6 +60,11 @@ def run_gpu(w, algo=None, cap=0, flags=0, device_leaves=False, arena_mb=256, lea
             assert not device_leaves and part is None
             keep.append(v)
             ctx.set_leaf(u, v)
+            continue
+        if u in peer_leaves:
+            d = device_from(v)                     # the full leaf, as a peer rank would hold it
+            keep.append(d)
+            ctx.set_leaf_peer(u, d)
             continue
         if device_leaves:
             d = device_from(v[t0:t0 + Lt_part])

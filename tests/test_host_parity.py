@@ -317,3 +317,55 @@ def test_ozaki_workspace_sizes_host_only():
     one = cc.cc_gemm_ozaki_workspace_bytes(cc.CC_BB2, 1, 16, 64, 5)
     slices = 5 * 128 * 32768 + 5 * 64 * 32768           # A slices (Mp=128) + B slices (2*32 rows)
     assert one >= slices + 2 * 128 * 32 * 16            # + 2 chunks of [Mp][Nc] complex partials
+
+
+PEER_KEYS = ("evictions", "h2d_count", "d2h_count", "h2d_bytes", "d2h_bytes", "peak", "transient_peak",
+             "host_peak_bytes", "p2p_out_count", "p2p_out_bytes", "p2p_in_count", "p2p_in_bytes", "peer_peak_bytes")
+
+
+def _check_peer(w, cap, peer_caps, homed_sets, algo=None):
+    dag = Dag(w)
+    c = _ctx(w)
+    order, _ = c.schedule(cc.CC_TREE if algo is None else algo)
+    for pol, nu in (("lru", False), ("next_use", True)):
+        for pc in peer_caps:
+            for homed in homed_sets:
+                try:
+                    p = lru.plan(dag, order, cap, policy=pol, peer_cap=pc, peer_leaves=homed)
+                except lru.InfeasibleError:
+                    continue
+                _, st = c.schedule(cc.CC_GIVEN, given=order, cap_bytes=cap or 0, evict_next_use=nu,
+                                   peer_cap_bytes=pc, peer_leaves=homed)
+                for k in PEER_KEYS:
+                    assert st[k] == p[k], (k, pol, pc)
+                assert [(k, n) for (k, n, _, _) in c.plan_ops()] == p["ops"]
+
+
+def test_peer_tier_plans_bit_exact():
+    """Peer-HBM tier (readings E-10, E-11): the C++ plan's op queue and counters equal the
+    oracle's on D*, random typed DAGs and small c2/c4 shapes, for LRU and next-use eviction."""
+    D = dict(zip("abcdefgh", range(8)))
+    _check_peer(dags.fixture_dstar(), 3, (0, 1, 2, 10), (set(), {D["a"]}, {D["a"], D["b"], D["d"]}))
+    for seed in range(40):
+        w = dags.random_dag(seed, n_leaves=7, n_trees=7, share_p=0.6, typed=True)
+        dag = Dag(w)
+        tp = lru.plan(dag, tree.schedule(dag))["transient_peak"]
+        leaves = sorted(u for u, n in dag.nodes.items() if not n.child)
+        for cap in (max(1, tp * 2 // 3), max(1, tp // 2)):
+            _check_peer(w, cap, (0, cap // 3, cap, 1 << 50), (set(), set(leaves[::2])))
+    w = dags.config_c4(N=4, Lt=1, S=4, n_trees=300)
+    baryon = 16 * 4 * 64
+    leaves = sorted(n[0] for n in w.nodes if n[1] in (dags.LEAF_M, dags.LEAF_B))
+    _check_peer(w, 9 * baryon, (0, 3 * baryon, 40 * baryon), (set(), set(leaves[:4])))
+
+
+def test_peer_tier_c4_full_scale():
+    """c4 at full scale (32e9 B cap) with a 32e9 B peer tier: bit-exact with the oracle, and the
+    PCIe bytes fall below the plain plan's (the point of E-10)."""
+    w = dags.config_c4()
+    _check_peer(w, 32 * 10 ** 9, (32 * 10 ** 9,), (set(),))
+    c = _ctx(w)
+    _, base = c.schedule(cc.CC_TREE, cap_bytes=32 * 10 ** 9, evict_next_use=True)
+    _, peer = c.schedule(cc.CC_TREE, cap_bytes=32 * 10 ** 9, evict_next_use=True, peer_cap_bytes=32 * 10 ** 9)
+    assert peer["h2d_bytes"] + peer["d2h_bytes"] < base["h2d_bytes"] + base["d2h_bytes"]
+    assert peer["h2d_count"] + peer["p2p_in_count"] == base["h2d_count"]
