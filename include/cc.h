@@ -10,7 +10,8 @@
  *
  * Conventions
  *  - Every function returns cc_status (0 = CC_OK, < 0 = error); no C++ exception crosses
- *    the ABI.  cc_last_error(ctx) gives a message for the last failing call on ctx.
+ *    the ABI.  cc_last_error(ctx) gives a message for the last failing call on ctx
+ *    (cc_last_error(NULL): the calling thread's last failing context-free call).
  *  - complex128 tensors are interleaved (re, im) doubles, row-major, time slice t
  *    outermost: meson node [Lt][N][N], baryon node [Lt][S][N][N][N] (S = spin
  *    components, 64 in P:59), root value [Lt].  Byte sizes 16*Lt*N^2, 16*Lt*S*N^3, 16*Lt.
@@ -176,6 +177,22 @@ cc_status cc_dag_info(cc_ctx* ctx, cc_dag_stats* out);
  * CC_E_INVAL for part outside [0, n_parts), an unknown mode, or a TIME part that owns no time
  * slice (n_parts > Lt), CC_E_STATE before cc_load_dag. */
 cc_status cc_partition(cc_ctx* ctx, int32_t n_parts, int32_t part, int32_t mode);
+/* GRID split (reading M-2): n_tree_parts TREES parts x n_time_parts TIME parts; part
+ * p in [0, n_tree_parts * n_time_parts) is TREES part p / n_time_parts restricted to the time
+ * slices of TIME part p % n_time_parts (e.g. c5 at N = 1024 over 8 GPUs: the per-GPU plan of a
+ * TIME-only split does not fit HBM).  Errors as cc_partition. */
+cc_status cc_partition_grid(cc_ctx* ctx, int32_t n_tree_parts, int32_t n_time_parts, int32_t part);
+/* Work of the current part (reading M-3; replicas "counted as overhead and
+ * reported"): work = sum of flops/8 of its contractions at its slice count (MM1 Lt N^3, ...,
+ * abstract: 1 each); replicated_* = the share of nodes whose owner (the part of the first
+ * selected tree containing them) is another part.  No partition: replicated = 0. */
+typedef struct { int64_t n_trees, n_contr, work, replicated_work, leaf_bytes, replicated_leaf_bytes; } cc_part_stats;
+cc_status cc_part_info(cc_ctx* ctx, cc_part_stats* out);
+/* Owner part of every leaf of the full DAG under the current TREES / GRID split (reading
+ * E-11: the rank that loads a shared leaf over PCIe; the others read its copy over NVLink
+ * with cc_set_leaf_peer).  leaf_ids / owners may be NULL (count query).  CC_E_STATE without a
+ * TREES / GRID partition. */
+cc_status cc_leaf_owners(cc_ctx* ctx, int64_t* leaf_ids, int32_t* owners, int64_t cap, int64_t* n_out);
 /* Trees of the current part (ids, ascending); n_out receives the count. */
 cc_status cc_part_trees(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out);
 /* Time-slice range [t0, t1) of the loaded part (the whole [0, Lt) unless a TIME partition is
@@ -215,6 +232,15 @@ cc_status cc_set_leaf_peer(cc_ctx* ctx, int64_t leaf_id, const void* dev, size_t
  * fails with CC_E_NOMEM if they do not fit, CC_E_STATE if the plan has peer copies and no
  * region is set.  dev NULL / bytes 0 removes it. */
 cc_status cc_set_peer_tier(cc_ctx* ctx, void* dev, size_t bytes);
+/* CUDA IPC plumbing between the one-process-per-GPU ranks (peer tier, leaf sharing):
+ * cc_ipc_export: a 64-byte handle of the device allocation holding dev (any address inside a
+ *   cudaMalloc'ed block, e.g. a torch tensor) and dev's offset in it; CC_E_INVAL if dev is not
+ *   device memory.
+ * cc_ipc_open: maps another process's handle (same GPU or a peer GPU), returns base + offset;
+ *   the mapping stays until cc_ipc_close(that pointer).  Context-free; thread-safe. */
+cc_status cc_ipc_export(const void* dev, uint8_t handle_out[64], uint64_t* offset_out);
+cc_status cc_ipc_open(const uint8_t handle[64], uint64_t offset, void** dev_out);
+cc_status cc_ipc_close(void* dev);
 
 /* Replays the plan on the device: H2D / D2H on the copy streams, contractions on the
  * compute stream, event dependencies for RAW on data and WAR on reused memory; blocking.

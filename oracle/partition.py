@@ -7,6 +7,13 @@ contractions first executed while processing it (MM1 Lt N^3, BM1/BB2 Lt S N^4, T
 BB1/BT2 Lt S N^5, BB3 Lt S N^3;
 abstract DAGs: 1 per contraction); tree i with prefix weight P_i, weight w_i, total W goes
 to part min(n-1, floor(n (2 P_i + w_i) / (2 W))).
+GRID (reading M-2): n_tree x n_time parts; part p is TREES part p // n_time restricted to
+TIME slices of part p % n_time (every op is per-slice, so the two splits compose).
+Replication (SURVEY §8(d) "replicas ... counted as overhead and reported", reading M-3): the
+owner of a node is the part of the first selected tree containing it; a part's replicated
+work / leaf bytes are those of its contractions / leaves owned by another part.
+Leaf owners (reading E-11): the same owner rule names the rank that loads a shared leaf over
+PCIe; the other parts using it read that copy over NVLink.
 """
 from synth.dags import MM1, BM1, BB2, TR_MM, BB1, BT2, BB3, Workload
 from .dag import Dag
@@ -32,8 +39,8 @@ def _weight(dag, u):
     return 1
 
 
-def tree_parts(dag, n_parts):
-    """{tree_id: part} for a TREES split."""
+def _owners(dag):
+    """(contraction order, tree selection order, {node: first selected tree containing it})."""
     s = tree_sched.TreeScheduler(dag)
     order = s.run()
     sel = s.tree_order
@@ -41,6 +48,12 @@ def tree_parts(dag, n_parts):
     for t in sel:
         for u in dag.trees[t][1]:
             owner.setdefault(u, t)
+    return order, sel, owner
+
+
+def tree_parts(dag, n_parts):
+    """{tree_id: part} for a TREES split."""
+    order, sel, owner = _owners(dag)
     w = {t: 0 for t in sel}
     for u in order:
         w[owner[u]] += _weight(dag, u)
@@ -66,3 +79,42 @@ def sub_workload(w, keep_trees):
                     trees=[t for t in w.trees if t[0] in keep],
                     terms=[x for x in w.terms if x[1] in keep],
                     data_seed=w.data_seed, leaf_mode=w.leaf_mode)
+
+
+def grid_part(n_tree, n_time, part):
+    """GRID part index -> (TREES part, TIME part) (reading M-2)."""
+    return part // n_time, part % n_time
+
+
+def part_stats(w, n_parts, part, n_time=1):
+    """Work (flops / 8, weights of _weight at this part's slice count) and leaf bytes of one
+    part of a TREES (n_time == 1) or GRID split, with the replicated share (reading M-3)."""
+    dag = Dag(w)
+    pt, ptm = grid_part(n_parts, n_time, part)
+    t0, t1 = time_range(w.Lt, n_time, ptm)
+    parts = tree_parts(dag, n_parts)
+    _, _, owner = _owners(dag)
+    keep = [t for t in dag.tree_ids if parts[t] == pt]
+    sub = Dag(sub_workload(w, keep))
+    scale = Dag(Workload(w.name, t1 - t0, w.N, w.S, nodes=w.nodes, trees=w.trees, terms=w.terms))
+    st = dict(n_trees=len(keep), n_contr=0, work=0, replicated_work=0, leaf_bytes=0, replicated_leaf_bytes=0)
+    for u, n in sub.nodes.items():
+        mine = parts[owner[u]] == pt
+        if n.child:
+            wu = _weight(scale, u)
+            st["n_contr"] += 1
+            st["work"] += wu
+            st["replicated_work"] += 0 if mine else wu
+        else:
+            b = n.size * (t1 - t0) // w.Lt
+            st["leaf_bytes"] += b
+            st["replicated_leaf_bytes"] += 0 if mine else b
+    return st
+
+
+def leaf_owners(w, n_parts):
+    """{leaf id: part that loads it over PCIe} for a TREES split (reading E-11)."""
+    dag = Dag(w)
+    parts = tree_parts(dag, n_parts)
+    _, _, owner = _owners(dag)
+    return {u: parts[owner[u]] for u, n in dag.nodes.items() if not n.child and u in owner}

@@ -82,6 +82,11 @@ class cc_options(ctypes.Structure):
                [("h2d_chunk_bytes", c_i64), ("tr_ratio", c_dbl), ("debug", c_i32), ("pad_", c_i32)]
 
 
+class cc_part_stats(ctypes.Structure):
+    _fields_ = [(n, c_i64) for n in ("n_trees", "n_contr", "work", "replicated_work", "leaf_bytes",
+                                     "replicated_leaf_bytes")]
+
+
 class cc_dag_stats(ctypes.Structure):
     _fields_ = [(n, c_i64) for n in ("V", "E", "k", "n_contr", "n_leaves", "max_rank", "n_corr")] + \
                [("F_v", c_dbl), ("F_e", c_dbl)]
@@ -105,6 +110,9 @@ _sig("cc_part_time_range", c_void_p, P(c_i32), P(c_i32))
 _sig("cc_correlators", c_void_p, P(c_dbl), c_i64)
 _sig("cc_partition", c_void_p, c_i32, c_i32, c_i32)
 _sig("cc_part_trees", c_void_p, P(c_i64), c_i64, P(c_i64))
+_sig("cc_partition_grid", c_void_p, c_i32, c_i32, c_i32)
+_sig("cc_part_info", c_void_p, P(cc_part_stats))
+_sig("cc_leaf_owners", c_void_p, P(c_i64), P(c_i32), c_i64, P(c_i64))
 _sig("cc_schedule", c_void_p, P(cc_sched_cfg), P(c_i64), c_i64, P(c_i64), P(cc_plan_stats))
 _sig("cc_memory_trace", c_void_p, P(c_i64), P(c_i64), c_i64, P(c_i64))
 _sig("cc_plan_ops", c_void_p, P(cc_plan_op), c_i64, P(c_i64))
@@ -114,6 +122,9 @@ _sig("cc_set_leaf", c_void_p, c_i64, c_void_p, c_size_t)
 _sig("cc_set_leaf_device", c_void_p, c_i64, c_void_p, c_size_t)
 _sig("cc_set_leaf_peer", c_void_p, c_i64, c_void_p, c_size_t)
 _sig("cc_set_peer_tier", c_void_p, c_void_p, c_size_t)
+_sig("cc_ipc_export", c_void_p, P(ctypes.c_uint8), P(c_u64))
+_sig("cc_ipc_open", P(ctypes.c_uint8), c_u64, P(c_void_p))
+_sig("cc_ipc_close", c_void_p)
 _sig("cc_execute", c_void_p, c_i32, P(cc_exec_stats))
 _sig("cc_execute_async", c_void_p, c_i32)
 _sig("cc_kernel_times", c_void_p, P(c_dbl), P(c_i64))
@@ -140,8 +151,8 @@ _sig("cc_fill_synthetic", c_void_p, c_void_p, c_i64, c_u64, c_i64, c_i64, c_i32,
 _sig("cc_scratch_bytes", c_i32, c_i32, c_i32, res=c_size_t)
 
 EXPORTED = ["cc_create", "cc_destroy", "cc_last_error", "cc_version", "cc_load_dag", "cc_load_dag_file",
-            "cc_dag_info", "cc_part_time_range", "cc_correlators", "cc_partition", "cc_part_trees", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
-            "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_set_leaf_peer", "cc_set_peer_tier", "cc_execute",
+            "cc_dag_info", "cc_part_time_range", "cc_correlators", "cc_partition", "cc_part_trees", "cc_partition_grid", "cc_part_info", "cc_leaf_owners", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
+            "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_set_leaf_peer", "cc_set_peer_tier", "cc_ipc_export", "cc_ipc_open", "cc_ipc_close", "cc_execute",
             "cc_execute_async", "cc_get_options", "cc_set_options", "cc_kernel_times", "cc_dataflow_state", "cc_dataflow_profile", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
             "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_bb1", "cc_bt2", "cc_bb3", "cc_mm1_ozaki", "cc_mm1_ozaki_workspace_bytes", "cc_i8gemm_tn", "cc_gemm_ozaki",
             "cc_gemm_ozaki_workspace_bytes", "cc_fill_synthetic", "cc_scratch_bytes"]
@@ -165,6 +176,31 @@ def _ptr(x):
     if isinstance(x, np.ndarray):
         return x.ctypes.data
     raise TypeError("cannot take the address of %r" % type(x))
+
+
+def _ck_free(st):
+    if st != 0:
+        raise CCError(st, _lib.cc_last_error(None).decode())
+
+
+def ipc_export(dev):
+    """(64-byte handle, offset) of a device buffer (torch tensor or address) for another rank."""
+    h = (ctypes.c_uint8 * 64)()
+    off = c_u64()
+    _ck_free(_lib.cc_ipc_export(_ptr(dev), h, ctypes.byref(off)))
+    return bytes(h), int(off.value)
+
+
+def ipc_open(handle, offset):
+    """Device address of another process's buffer (cc_ipc_open); close with ipc_close."""
+    h = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    p = c_void_p()
+    _ck_free(_lib.cc_ipc_open(h, offset, ctypes.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr):
+    _ck_free(_lib.cc_ipc_close(ptr))
 
 
 def cc_version():
@@ -246,6 +282,24 @@ class Context:
 
     def partition(self, n_parts, part, mode):
         self._ck(_lib.cc_partition(self._h, n_parts, part, mode))
+
+    def partition_grid(self, n_tree_parts, n_time_parts, part):
+        """GRID split (reading M-2): TREES part part // n_time_parts x TIME part part % n_time_parts."""
+        self._ck(_lib.cc_partition_grid(self._h, n_tree_parts, n_time_parts, part))
+
+    def part_info(self):
+        s = cc_part_stats()
+        self._ck(_lib.cc_part_info(self._h, ctypes.byref(s)))
+        return {f: getattr(s, f) for f, _ in cc_part_stats._fields_}
+
+    def leaf_owners(self):
+        """{leaf id: owner part} under the current TREES / GRID split (reading E-11)."""
+        n = c_i64()
+        self._ck(_lib.cc_leaf_owners(self._h, None, None, 0, ctypes.byref(n)))
+        ids = (c_i64 * max(n.value, 1))()
+        own = (c_i32 * max(n.value, 1))()
+        self._ck(_lib.cc_leaf_owners(self._h, ids, own, n.value, ctypes.byref(n)))
+        return {int(ids[i]): int(own[i]) for i in range(n.value)}
 
     def part_time_range(self):
         t0, t1 = c_i32(), c_i32()

@@ -2,8 +2,13 @@
 // work happens in the exec/ and host/ translation units.
 #include "internal.hpp"
 
+#include <mutex>
+
+static thread_local std::string g_err = "no error";   // context-free calls (ctx == NULL)
+
 static cc_status fail(cc_ctx* ctx, const Error& e) {
   if (ctx) ctx->err = e.what();
+  else g_err = e.what();
   return e.status;
 }
 
@@ -41,7 +46,7 @@ extern "C" {
 
 const char* cc_version(void) { return CC_VERSION; }
 
-const char* cc_last_error(const cc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+const char* cc_last_error(const cc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
 
 cc_status cc_create(cc_ctx** out, int device, void* dev_arena, size_t arena_bytes, void* compute_stream,
                     void* h2d_stream, void* d2h_stream) {
@@ -140,7 +145,76 @@ cc_status cc_partition(cc_ctx* ctx, int32_t n_parts, int32_t part, int32_t mode)
   ctx->n_parts = n_parts;
   ctx->part = part;
   ctx->mode = mode;
+  ctx->n_time_parts = 1;
   rebuild_dag(ctx);
+  API_END
+}
+
+cc_status cc_partition_grid(cc_ctx* ctx, int32_t n_tree_parts, int32_t n_time_parts, int32_t part) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->loaded) throw Error(CC_E_STATE, "no DAG loaded");
+  if (n_tree_parts < 1 || n_time_parts < 1 || part < 0 || int64_t(part) >= int64_t(n_tree_parts) * n_time_parts)
+    throw Error(CC_E_INVAL, "bad grid partition");
+  // a degenerate grid is a plain TIME (one tree part) or TREES (one time part) split
+  ctx->n_parts = n_tree_parts == 1 ? n_time_parts : n_tree_parts;
+  ctx->n_time_parts = n_tree_parts == 1 ? 1 : n_time_parts;
+  ctx->part = part;
+  ctx->mode = n_tree_parts == 1 ? 0 : (n_time_parts == 1 ? 1 : 2);
+  rebuild_dag(ctx);
+  API_END
+}
+
+cc_status cc_part_info(cc_ctx* ctx, cc_part_stats* out) {
+  if (!ctx || !out) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->loaded) throw Error(CC_E_STATE, "no DAG loaded");
+  Dag full(ctx->input);
+  std::vector<int32_t> owner;
+  const bool trees = ctx->n_parts > 1 && ctx->mode != 0;
+  std::vector<int32_t> parts = trees ? tree_parts(full, ctx->n_parts, nullptr, &owner) : std::vector<int32_t>();
+  const int32_t pt = trees ? ctx->part / (ctx->mode == 2 ? ctx->n_time_parts : 1) : 0;
+  const Dag& g = *ctx->dag;
+  const int64_t lt = ctx->t1 - ctx->t0;
+  cc_part_stats s{};
+  s.n_trees = int64_t(g.trees.size());
+  for (const Node& n : g.nodes) {
+    bool mine = true;
+    if (trees) {
+      const int32_t u = full.idx(n.id);
+      mine = owner[size_t(u)] >= 0 && parts[size_t(owner[size_t(u)])] == pt;
+    }
+    if (n.leaf()) {
+      s.leaf_bytes += n.size;
+      if (!mine) s.replicated_leaf_bytes += n.size;
+    } else {
+      const int64_t wu = contraction_weight(g, n, lt);
+      ++s.n_contr;
+      s.work += wu;
+      if (!mine) s.replicated_work += wu;
+    }
+  }
+  *out = s;
+  API_END
+}
+
+cc_status cc_leaf_owners(cc_ctx* ctx, int64_t* leaf_ids, int32_t* owners, int64_t cap, int64_t* n_out) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->loaded) throw Error(CC_E_STATE, "no DAG loaded");
+  if (ctx->n_parts <= 1 || ctx->mode == 0) throw Error(CC_E_STATE, "leaf owners need a TREES or GRID partition");
+  Dag full(ctx->input);
+  std::vector<int32_t> owner;
+  std::vector<int32_t> parts = tree_parts(full, ctx->n_parts, nullptr, &owner);
+  int64_t n = 0;
+  for (size_t u = 0; u < full.nodes.size(); ++u)
+    if (full.nodes[u].leaf() && owner[u] >= 0) {
+      if ((leaf_ids || owners) && n >= cap) throw Error(CC_E_BUFFER_TOO_SMALL, "buffer too small");
+      if (leaf_ids) leaf_ids[n] = full.nodes[u].id;
+      if (owners) owners[n] = parts[size_t(owner[u])];
+      ++n;
+    }
+  if (n_out) *n_out = n;
   API_END
 }
 
@@ -359,6 +433,68 @@ cc_status cc_set_leaf_peer(cc_ctx* ctx, int64_t leaf_id, const void* dev, size_t
   if (!dev) throw Error(CC_E_INVAL, "null peer pointer");
   ctx->leaf_peer[size_t(it->second)] = dev;
   ctx->release_graph();  // copy sources are baked into a captured graph
+  API_END
+}
+
+// ---- CUDA IPC plumbing for the peer tier / leaf sharing between rank processes ----------
+namespace {
+std::mutex g_ipc_mu;
+std::map<uintptr_t, void*> g_ipc_open;   // pointer handed out -> mapped base
+}  // namespace
+
+cc_status cc_ipc_export(const void* dev, uint8_t handle_out[64], uint64_t* offset_out) {
+  cc_ctx* ctx = nullptr;
+  if (!dev || !handle_out || !offset_out) return CC_E_INVAL;
+  API_BEGIN
+  using PFN_range = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static PFN_range range = nullptr;
+  if (!range) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      throw Error(CC_E_CUDA, "cuMemGetAddressRange unavailable");
+    range = reinterpret_cast<PFN_range>(p);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev)) != CUDA_SUCCESS)
+    throw Error(CC_E_INVAL, "cc_ipc_export: not a device allocation");
+  cudaIpcMemHandle_t h;
+  ck(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(handle_out, &h, 64);
+  *offset_out = uint64_t(reinterpret_cast<uintptr_t>(dev) - uintptr_t(base));
+  API_END
+}
+
+cc_status cc_ipc_open(const uint8_t handle[64], uint64_t offset, void** dev_out) {
+  cc_ctx* ctx = nullptr;
+  if (!handle || !dev_out) return CC_E_INVAL;
+  API_BEGIN
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  void* base = nullptr;
+  ck(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  void* p = static_cast<char*>(base) + offset;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  g_ipc_open[reinterpret_cast<uintptr_t>(p)] = base;
+  *dev_out = p;
+  API_END
+}
+
+cc_status cc_ipc_close(void* dev) {
+  cc_ctx* ctx = nullptr;
+  API_BEGIN
+  void* base = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto it = g_ipc_open.find(reinterpret_cast<uintptr_t>(dev));
+    if (it == g_ipc_open.end()) throw Error(CC_E_INVAL, "cc_ipc_close: not a pointer from cc_ipc_open");
+    base = it->second;
+    g_ipc_open.erase(it);
+  }
+  ck(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle");
   API_END
 }
 

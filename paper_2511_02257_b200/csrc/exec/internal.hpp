@@ -100,6 +100,7 @@ struct cc_ctx {
   Input input;
   bool loaded = false;
   int32_t n_parts = 1, part = 0, mode = 0, t0 = 0, t1 = 0;
+  int32_t n_time_parts = 1;            // GRID (mode 2): n_parts TREES parts x n_time_parts TIME parts
   std::vector<int64_t> part_trees;
   std::unique_ptr<Dag> dag;
 

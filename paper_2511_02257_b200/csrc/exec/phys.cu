@@ -19,15 +19,19 @@ void rebuild_dag(cc_ctx* ctx) {
     ctx->part_trees.clear();
     for (const auto& t : ctx->dag->trees) ctx->part_trees.push_back(t.tree_id);
   } else {
-    ctx->t0 = 0;
-    ctx->t1 = Lt;
+    // TREES (mode 1), or GRID (mode 2): TREES part part / n_time_parts, TIME part part % n_time_parts
+    const int32_t nt = ctx->mode == 2 ? ctx->n_time_parts : 1;
+    const int32_t pt = ctx->part / nt, ptm = ctx->part % nt;
+    ctx->t0 = int32_t(int64_t(ptm) * Lt / nt);
+    ctx->t1 = int32_t(int64_t(ptm + 1) * Lt / nt);
+    if (ctx->t1 <= ctx->t0) throw Error(CC_E_INVAL, "GRID partition: part has no time slices");
     Dag full(ctx->input);
     std::vector<int32_t> parts = tree_parts(full, ctx->n_parts, nullptr);
     std::vector<int64_t> keep;
     for (size_t t = 0; t < full.trees.size(); ++t)
-      if (parts[t] == ctx->part) keep.push_back(full.trees[t].tree_id);
+      if (parts[t] == pt) keep.push_back(full.trees[t].tree_id);
     if (keep.empty()) throw Error(CC_E_INVAL, "TREES partition: part has no trees");
-    ctx->dag = std::make_unique<Dag>(ctx->input, 0, &keep);
+    ctx->dag = std::make_unique<Dag>(ctx->input, nt > 1 ? ctx->t1 - ctx->t0 : 0, &keep);
     ctx->part_trees = keep;
   }
   const size_t n = ctx->dag->nodes.size();

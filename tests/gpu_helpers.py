@@ -38,7 +38,10 @@ def run_gpu(w, algo=None, cap=0, flags=0, device_leaves=False, arena_mb=256, lea
         ctx.set_options(**options)
     ctx.load_workload(w)
     if part is not None:
-        ctx.partition(*part)
+        if part[0] == "grid":               # ("grid", n_tree_parts, n_time_parts, part)
+            ctx.partition_grid(*part[1:])
+        else:
+            ctx.partition(*part)
     order, st = ctx.schedule(cc.CC_TREE if algo is None else algo, cap_bytes=cap, evict_next_use=evict_next_use,
                              peer_cap_bytes=peer_cap, peer_leaves=peer_leaves)
     keep = []
@@ -48,9 +51,8 @@ def run_gpu(w, algo=None, cap=0, flags=0, device_leaves=False, arena_mb=256, lea
         ctx.set_peer_tier(tier)
     Lt_part = w.Lt
     t0 = 0
-    if part is not None and part[2] == cc.PART_TIME:
-        from oracle.partition import time_range
-        t0, t1 = time_range(w.Lt, part[0], part[1])
+    if part is not None:
+        t0, t1 = ctx.part_time_range()
         Lt_part = t1 - t0
     for u, n in dag.nodes.items():
         if n.child:

@@ -303,6 +303,23 @@ def test_partitions_sum_to_whole():
         assert_corr_close(dag, r_or, total, c_or)
 
 
+@pytest.mark.parametrize("flags", [0, 16])
+def test_grid_parts_sum_to_whole(flags):
+    """GRID split (reading M-2, 2 tree parts x 3 time parts): each part's correlator slices,
+    placed at its time range and summed over tree parts, equal the whole DAG's."""
+    w = dags.config_c2(N=16, Lt=6, n_loop4=60, n_loop2=6, n_corr=4)
+    dag = Dag(w)
+    r_or, c_or = values.run_workload(w, dag)
+    total = {c: np.zeros(w.Lt, complex) for c in c_or}
+    for p in range(6):
+        ctx, roots, corr, st, ex = run_gpu(w, part=("grid", 2, 3, p), flags=flags)
+        t0, t1 = ctx.part_time_range()
+        assert (t0, t1) == partition.time_range(w.Lt, 3, p % 3)
+        for c in corr:
+            total[c][t0:t1] += corr[c]
+    assert_corr_close(dag, r_or, total, c_or)
+
+
 def test_c2_full_size_sampled_slices():
     """BASELINE configs[1] at full size (N=128, Lt=64, 400 trees) in the bench's launch
     configuration (graph, device-resident leaves); the oracle computes time slices

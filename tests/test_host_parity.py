@@ -369,3 +369,38 @@ def test_peer_tier_c4_full_scale():
     _, peer = c.schedule(cc.CC_TREE, cap_bytes=32 * 10 ** 9, evict_next_use=True, peer_cap_bytes=32 * 10 ** 9)
     assert peer["h2d_bytes"] + peer["d2h_bytes"] < base["h2d_bytes"] + base["d2h_bytes"]
     assert peer["h2d_count"] + peer["p2p_in_count"] == base["h2d_count"]
+
+
+def test_grid_partition_part_info_leaf_owners():
+    """GRID split (M-2), replication (M-3) and leaf owners (E-11): the C++ part's trees, time
+    range, work / replication counters and leaf owners equal the oracle's, and each part's
+    plan is bit-exact with the oracle on that part's sub-workload."""
+    cases = [(dags.config_c5(N=8, Lt=8, n_pairs=40, n_trees=200), 2, 2),
+             (dags.config_c5(N=8, Lt=8, n_pairs=40, n_trees=200), 3, 4),
+             (dags.config_c4(N=4, Lt=2, S=4, n_trees=120), 2, 2),
+             (dags.config_c6(N=4, Lt=2, S=4, n_trees=40), 2, 2),
+             (dags.fixture_dstar(), 2, 1)]
+    for w, nT, nL in cases:
+        dag = Dag(w)
+        parts = partition.tree_parts(dag, nT)
+        owners = partition.leaf_owners(w, nT)
+        for p in range(nT * nL):
+            c = _ctx(w)
+            c.partition_grid(nT, nL, p)
+            pt, ptm = partition.grid_part(nT, nL, p)
+            assert c.part_trees() == sorted(t for t in dag.tree_ids if parts[t] == pt)
+            if w.Lt > 1 or nL == 1:
+                assert c.part_time_range() == partition.time_range(w.Lt, nL, ptm)
+            assert c.part_info() == partition.part_stats(w, nT, p, n_time=nL)
+            assert c.leaf_owners() == owners
+            sub = partition.sub_workload(w, c.part_trees())
+            t0, t1 = partition.time_range(w.Lt, nL, ptm)
+            sub.Lt = t1 - t0
+            sd = Dag(sub)
+            order, st = c.schedule(cc.CC_TREE)
+            assert order == tree.schedule(sd)
+            assert st["peak"] == lru.plan(sd, order)["peak"]
+    c = _ctx(dags.config_c5(N=8, Lt=8, n_pairs=40, n_trees=200))
+    assert c.part_info()["replicated_work"] == 0
+    with pytest.raises(cc.CCError):
+        c.leaf_owners()

@@ -66,3 +66,56 @@ def test_partition_properties(seed, n):
     for t in sel:
         assert parts[t] == min(n - 1, (n * (2 * P + wt[t])) // (2 * W))
         P += wt[t]
+
+
+def test_dstar_part_stats_and_owners():
+    """D*, n = 2: part 0 = T0 = {f, a, b}, part 1 = T1 u T2 = {g, e, h, a, b, c, d} (unit sizes,
+    unit contraction weights).  Owners = part of the first selected tree containing the node:
+    a, b -> T0 (part 0); c, e, g -> T1; d, h -> T2 (part 1).  Part 1 replicates leaves a, b."""
+    w = dags.fixture_dstar()
+    assert partition.part_stats(w, 2, 0) == dict(n_trees=1, n_contr=1, work=1, replicated_work=0, leaf_bytes=2,
+                                                 replicated_leaf_bytes=0)
+    assert partition.part_stats(w, 2, 1) == dict(n_trees=2, n_contr=3, work=3, replicated_work=0, leaf_bytes=4,
+                                                 replicated_leaf_bytes=2)
+    assert partition.leaf_owners(w, 2) == {0: 0, 1: 0, 2: 1, 3: 1}
+
+
+@pytest.mark.parametrize("seed", range(20))
+@pytest.mark.parametrize("n,nt", [(2, 1), (3, 2), (2, 4)])
+def test_part_stats_properties(seed, n, nt):
+    """Replication by an independent formulation: a node's owner part is the smallest part
+    index among the trees whose closure holds it (parts are contiguous along the selection
+    order); sum over parts of (work - replicated) = the whole DAG's work; GRID time parts
+    split each TREES part's work and leaf bytes exactly by slice count."""
+    Lt = 4
+    w = dags.random_dag(seed, n_leaves=6, n_trees=9, max_ops_per_tree=4, share_p=0.6, typed=True, N=3, Lt=Lt)
+    dag = Dag(w)
+    ops = {x[0]: x[1] for x in w.nodes}
+    parts = partition.tree_parts(dag, n)
+    own = {}
+    for t in dag.tree_ids:
+        for u in dag.trees[t][1]:
+            own[u] = min(own.get(u, n), parts[t])
+    W = sum(_weight(w, ops[u]) for u, nd in dag.nodes.items() if nd.child)
+    used_leaf_bytes = sum(dag.nodes[u].size for u in own if not dag.nodes[u].child)
+    tot_unique, tot_leaf_unique = 0, 0
+    for pt in range(n):
+        rows = [partition.part_stats(w, n, pt * nt + k, n_time=nt) for k in range(nt)]
+        keep = [t for t in dag.tree_ids if parts[t] == pt]
+        members = set().union(*[dag.trees[t][1] for t in keep]) if keep else set()
+        contr = [u for u in members if dag.nodes[u].child]
+        work = sum(_weight(w, ops[u]) for u in contr)
+        rep = sum(_weight(w, ops[u]) for u in contr if own[u] != pt)
+        lb = sum(dag.nodes[u].size for u in members if not dag.nodes[u].child)
+        rlb = sum(dag.nodes[u].size for u in members if not dag.nodes[u].child and own[u] != pt)
+        t_slices = [partition.time_range(Lt, nt, k) for k in range(nt)]
+        for k, r in enumerate(rows):
+            frac = (t_slices[k][1] - t_slices[k][0])
+            assert r["n_trees"] == len(keep) and r["n_contr"] == len(contr)
+            assert r["work"] * Lt == work * frac and r["replicated_work"] * Lt == rep * frac
+            assert r["leaf_bytes"] * Lt == lb * frac and r["replicated_leaf_bytes"] * Lt == rlb * frac
+        tot_unique += work - rep
+        tot_leaf_unique += lb - rlb
+    assert tot_unique == W and tot_leaf_unique == used_leaf_bytes
+    lo = partition.leaf_owners(w, n)
+    assert lo == {u: p for u, p in own.items() if not dag.nodes[u].child}
