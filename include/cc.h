@@ -276,15 +276,19 @@ cc_status cc_execute_async(cc_ctx* ctx, int32_t flags);
  *   ozaki_slices      Ozaki engine: INT8 slices per operand, 4..7 [5]
  *   h2d_chunk_bytes   dataflow: H2D copies in time-slice chunks of about this size, each with its
  *                     own completion flag; 0: whole tensors [0]
- *   tr_ratio          dataflow: TR_MM stages the issuer interleaves per GEMM k-tile; 0: 1.12 x the
- *                     plan's trace/k-tile stage ratio [0]
+ *   tr_ratio          ignored (the dataflow worker's traces run in their own warps since round 2;
+ *                     the field keeps the struct layout) [0]
  *   debug             bit 0: executor trace on stderr; bit 1: host phase timings on stderr [0]
+ *   slice_major       dataflow: order the work items time slice by time slice within each group
+ *                     of ops whose inputs arrive together, so a slice's GEMM outputs are traced
+ *                     (and its leaves reused) while they are still in L2; applies when every
+ *                     dependency between contractions is per time slice [1]
  * Errors: CC_E_INVAL for out-of-range values. */
 typedef struct {
   int32_t trace_fusion, copy_reorder, early_copies, precopy, ozaki_leaf_cache, ozaki_slices;
   int64_t h2d_chunk_bytes;
   double tr_ratio;
-  int32_t debug, pad_;
+  int32_t debug, slice_major;
 } cc_options;
 cc_status cc_get_options(cc_ctx* ctx, cc_options* out);
 cc_status cc_set_options(cc_ctx* ctx, const cc_options* opt);

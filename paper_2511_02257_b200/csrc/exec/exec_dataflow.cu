@@ -147,8 +147,8 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
   // sync slots (done counters of compute ops, flags of copies) and H2D chunk counts
   std::vector<int32_t> slot(size_t(n_ops), -1), target(size_t(n_ops), 0), df_index(size_t(n_ops), -1);
   int32_t n_sync = 0;
-  // per-time-slice done counters of GEMMs with meson outputs [Lt, N, N] (MM1, BB2): a trace of
-  // slice t waits only for that slice's tiles
+  // per-time-slice done counters of GEMMs (every op is batched over time slices, reading V-1):
+  // a trace or GEMM reading slice t of a GEMM's output waits only for that slice's tiles
   std::vector<int32_t> slice_slot(size_t(n_ops), -1), items_per_slice(size_t(n_ops), 0);
   // opt.h2d_chunk_bytes: H2D copies in time-slice chunks of about that size (default off: every
   // chunk costs a stream memory operation, measured ~8 us of copy-engine idle each on B200)
@@ -157,8 +157,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     const PhysOp& op = ops[size_t(i)];
     if (op.stream == S_NONE) continue;
     slot[size_t(i)] = n_sync++;
-    if (op.kind == OP_CONTRACT && Lt > 1 &&
-        (g.nodes[size_t(op.node)].op == CC_MM1 || g.nodes[size_t(op.node)].op == CC_BB2)) {
+    if (op.kind == OP_CONTRACT && Lt > 1 && is_gemm_kind(g.nodes[size_t(op.node)].op)) {
       slice_slot[size_t(i)] = n_sync;
       n_sync += int32_t(Lt);
     }
@@ -527,6 +526,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     }
   tmr.lap("items+tmaps");
   std::vector<int64_t> qpos(size_t(n_ops), INT64_MAX);   // merged queue position of compute ops
+  std::vector<int64_t> avail(size_t(n_ops), 0);
   // 3. queue order: a topological order of the plan's ops (compute and copy; consecutive
   // copies on one stream are chained, since a copy stream runs in plan order) that delays each
   // TR_MM op by DF_TR_DELAY compute positions, so a trace item is usually claimed after its
@@ -540,7 +540,6 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     for (int st : {int(S_H2D), int(S_D2H)})
       for (size_t k = 1; k < copy_seq[st].size(); ++k) chain_prev[size_t(copy_seq[st][k])] = copy_seq[st][k - 1];
     // avail: the H2D issue position after which an op's inputs can all be there
-    std::vector<int64_t> avail(size_t(n_ops), 0);
     int32_t r = 0;
     for (int32_t i = 0; i < n_ops; ++i) {
       if (slot[size_t(i)] < 0) continue;
@@ -627,6 +626,65 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
       trace_ring_user[size_t(r)] = tplan[k];
     }
   }
+  // 3b. item order within each queue.  Op-major (an op's items contiguous, in queue order),
+  // or — option slice_major — time slice by time slice within each run of ops whose inputs
+  // become available at the same copy position (avail): all ops' items of slice 0, then of
+  // slice 1, ..., so the GEMM outputs of a slice are traced while still in L2 and a leaf
+  // slice is read by every GEMM using it back to back.  Requires every dependency between
+  // contractions to be a per-slice RAW on an operand (no memory-reuse or ring dependencies)
+  // and no fused traces; the merged order (segment by segment, slice by slice, GEMM items
+  // before trace items, ops in queue order) stays topological, so the dataflow stays
+  // deadlock-free (dataflow.hpp).
+  std::vector<int32_t> gitem_op, gitem_local, titem_op, titem_local;
+  {
+    auto ips_of = [&](int32_t i, const DfOp& d) -> int64_t {
+      return d.kind == 1 ? int64_t(d.P) : int64_t(items_per_slice[size_t(i)]);
+    };
+    bool sm = ctx->opt.slice_major != 0 && Lt > 1 && fusedv.empty();
+    for (int32_t i = 0; sm && i < n_ops; ++i) {
+      const PhysOp& op = ops[size_t(i)];
+      if (op.kind != OP_CONTRACT || slot[size_t(i)] < 0) continue;
+      if (!ring_deps[size_t(i)].empty()) sm = false;
+      if (df_index[size_t(i)] >= 0 && !is_root_kind(g.nodes[size_t(op.node)].op) && items_per_slice[size_t(i)] <= 0)
+        sm = false;
+      for (int32_t j : deps[size_t(i)]) {
+        if (ops[size_t(j)].kind != OP_CONTRACT) continue;
+        const bool raw = j == wr_a[size_t(i)] || j == wr_b[size_t(i)];
+        if (!raw || items_per_slice[size_t(j)] <= 0) sm = false;
+      }
+    }
+    auto build = [&](const std::vector<DfOp>& v, const std::vector<int32_t>& plan, std::vector<int32_t>& iop,
+                     std::vector<int32_t>& iloc) {
+      for (size_t k0 = 0; k0 < v.size();) {
+        size_t k1 = k0 + 1;
+        if (sm)
+          while (k1 < v.size() && avail[size_t(plan[k1])] == avail[size_t(plan[k0])]) ++k1;
+        if (!sm) {
+          for (int32_t x = 0; x < v[k0].n_items; ++x) {
+            iop.push_back(int32_t(k0));
+            iloc.push_back(x);
+          }
+        } else {
+          for (int64_t t = 0; t < Lt; ++t)
+            for (size_t k = k0; k < k1; ++k) {
+              const int64_t ips = ips_of(plan[k], v[k]);
+              for (int64_t x = t * ips; x < (t + 1) * ips; ++x) {
+                iop.push_back(int32_t(k));
+                iloc.push_back(int32_t(x));
+              }
+            }
+        }
+        k0 = k1;
+      }
+    };
+    build(gops, gplan, gitem_op, gitem_local);
+    build(tops, tplan, titem_op, titem_local);
+    if (int64_t(gitem_op.size()) != g_items || int64_t(titem_op.size()) != t_items)
+      throw Error(CC_E_STATE, "dataflow: item order lost items");
+    ctx->df_slice_major = sm;
+    if (gitem_op.empty()) { gitem_op.push_back(0); gitem_local.push_back(0); }
+    if (titem_op.empty()) { titem_op.push_back(0); titem_local.push_back(0); }
+  }
   tmr.lap("queue order");
   // 4. dependency lists of compute ops, wait lists of copies
   std::vector<int32_t> dep_slot, dep_target;
@@ -640,7 +698,10 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
       all.erase(std::unique(all.begin(), all.end()), all.end());
       for (int32_t j : all) {
         if (slot[size_t(j)] < 0) continue;
-        if (traces && items_per_slice[size_t(j)] > 0) {   // a trace reads slice t of this GEMM's output
+        // a trace, or a GEMM batched over the same time slices, reading slice t of this GEMM's
+        // output (RAW on an operand; reuse deps stay whole-op) waits for that slice only
+        const bool raw = j == wr_a[size_t(i)] || j == wr_b[size_t(i)];
+        if (items_per_slice[size_t(j)] > 0 && (traces || (raw && items_per_slice[size_t(i)] > 0))) {
           dep_slot.push_back(slice_slot[size_t(j)]);
           dep_target.push_back(-(1 << 20) - items_per_slice[size_t(j)]);
           continue;
@@ -717,14 +778,9 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
   const size_t sz_t = round_up(int64_t(std::max<size_t>(tops.size(), 1) * sizeof(DfOp)), 256);
   const size_t sz_d = round_up(int64_t(std::max<size_t>(dep_slot.size(), 1) * 4), 256);
   const size_t sz_m = round_up(int64_t(std::max<size_t>(tmaps.size(), 256)), 256);
-  std::vector<int32_t> gitem_op(size_t(std::max<int64_t>(g_items, 1)), 0), titem_op(size_t(std::max<int64_t>(t_items, 1)), 0);
-  for (size_t k = 0; k < gops.size(); ++k)
-    std::fill(gitem_op.begin() + gops[k].first_item, gitem_op.begin() + gops[k].first_item + gops[k].n_items, int32_t(k));
-  for (size_t k = 0; k < tops.size(); ++k)
-    std::fill(titem_op.begin() + tops[k].first_item, titem_op.begin() + tops[k].first_item + tops[k].n_items, int32_t(k));
   const size_t sz_gi = round_up(int64_t(gitem_op.size() * 4), 256), sz_ti = round_up(int64_t(titem_op.size() * 4), 256);
   const size_t sz_f = round_up(int64_t(std::max<size_t>(fusedv.size(), 1) * sizeof(DfFused)), 256);
-  const size_t total = sz_g + sz_t + 2 * sz_d + sz_m + sz_gi + sz_ti + sz_f;
+  const size_t total = sz_g + sz_t + 2 * sz_d + sz_m + 2 * sz_gi + 2 * sz_ti + sz_f;
   // device region: the top of the pool when the plan's high water leaves room (no allocation
   // on the execute path), else a cudaMalloc
   const int64_t meta_off = (int64_t(ctx->df_sync_base - ctx->arena) - int64_t(total)) / 256 * 256;
@@ -759,7 +815,9 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
   char* pm = pdt + sz_d;
   char* pgi = pm + sz_m;
   char* pti = pgi + sz_gi;
-  char* pf = pti + sz_ti;
+  char* pgl = pti + sz_ti;
+  char* ptl = pgl + sz_gi;
+  char* pf = ptl + sz_ti;
   {
     // one host image, one copy, ordered on the compute stream before the worker launch
     if (ctx->df_meta_img_bytes < total) {
@@ -781,6 +839,8 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     };
     put(pgi, gitem_op.data(), gitem_op.size() * 4);
     put(pti, titem_op.data(), titem_op.size() * 4);
+    put(pgl, gitem_local.data(), gitem_local.size() * 4);
+    put(ptl, titem_local.data(), titem_local.size() * 4);
     put(pg, gops.data(), gops.size() * sizeof(DfOp));
     put(pt, tops.data(), tops.size() * sizeof(DfOp));
     put(pds, dep_slot.data(), dep_slot.size() * 4);
@@ -798,21 +858,13 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
   da.sync = ctx->df_sync;
   da.fused = reinterpret_cast<const DfFused*>(pf);
   ctx->df_n_fused = int32_t(fusedv.size());
-  da.q = DfQueue{reinterpret_cast<const DfOp*>(pg), reinterpret_cast<const int32_t*>(pgi), int32_t(gops.size()),
+  da.q = DfQueue{reinterpret_cast<const DfOp*>(pg), reinterpret_cast<const int32_t*>(pgi),
+                 reinterpret_cast<const int32_t*>(pgl), int32_t(gops.size()),
                  g_items, heads};
-  da.qt = DfQueue{reinterpret_cast<const DfOp*>(pt), reinterpret_cast<const int32_t*>(pti), int32_t(tops.size()),
+  da.qt = DfQueue{reinterpret_cast<const DfOp*>(pt), reinterpret_cast<const int32_t*>(pti),
+                  reinterpret_cast<const int32_t*>(ptl), int32_t(tops.size()),
                   t_items, heads + 1};
   {
-    // TR_MM stages the issuer may put between GEMM k-tiles (fixed point, 1/8): by default
-    // 1.12 x the plan's trace-stage / k-tile-stage ratio, so the traces keep pace with the
-    // GEMMs (c2: 1.56 -> 1.75; measured on c2: 1.5 / 1.75 / 2 / 2.5 -> 4.45 / 4.38 / 4.43 /
-    // 4.62 ms); opt.tr_ratio > 0 overrides
-    double g_st = 0, t_st = 0;
-    for (const auto& o : gops) g_st += double(o.n_items / std::max(o.n_chunks, 1)) * o.KT;
-    for (const auto& o : tops) t_st += double(o.Lt) * o.tr_G * o.nb * o.nb;
-    const double auto_ratio = g_st > 0 && t_st > 0 ? std::min(std::max(1.12 * t_st / g_st, 0.25), 8.0) : 2.0;
-    const double ratio = ctx->opt.tr_ratio > 0 ? ctx->opt.tr_ratio : auto_ratio;
-    da.tr_ratio8 = std::min(std::max(int(std::lround(ratio * 8.0)), 1), 512);
     da.Lt = int32_t(Lt);
     da.ahead_g = 2;   // items a CTA's scheduler holds claimed-but-unpublished per queue
     da.ahead_t = 2;

@@ -76,7 +76,7 @@ using namespace ccx;
 
 struct cc_ctx {
   int device = -1;
-  cc_options opt{0, 1, 1, 1, 1, 5, 0, 0.0, 0, 0};   // cc_set_options (cc.h)
+  cc_options opt{0, 1, 1, 1, 1, 5, 0, 0.0, 0, 1};   // cc_set_options (cc.h)
   bool mm1_ozaki = false;     // execute flags bit 6: MM1/BM1/BB2 on the tcgen05 Ozaki engine (op-by-op)
   int pre_n = 0;              // the plan's first pre_n leaf copies were started before the physical plan
   cudaEvent_t ev_precopy = nullptr;
@@ -159,6 +159,7 @@ struct cc_ctx {
 
   // dataflow execution (persistent workers): device metadata + per-launch sync area
   bool df_valid = false;
+  bool df_slice_major = false;      // the current dataflow queues are in slice-major item order
   char* df_meta = nullptr;          // ops, deps, tensor maps, sync area: top of the pool, else cudaMalloc
   bool df_meta_owned = false;       // cudaMalloc'ed (the arena had no room above the plan's high water)
   char* df_fpart = nullptr;         // fused-trace partials (below the metadata, else cudaMalloc)

@@ -144,9 +144,11 @@ __device__ __forceinline__ void gauss3m_sums(const double (&ar)[MI], const doubl
         "d"(bi[0]), "d"(br[1]), "d"(bi[1]));
 }
 
-template <class C>
+// `between(q)` runs after the DMMA sweeps of k-quad q (0..BK/4-1): other work (the dataflow
+// worker's interleaved trace rows) issued while this warp's DMMAs drain from the FP64 pipe.
+template <class C, class F>
 __device__ __forceinline__ void dmma3m_ktile(const uint8_t* sA, const uint8_t* sB, int wm, int wn, int g, int t,
-                                             double (&p)[3][C::MI][C::NJ][2]) {
+                                             double (&p)[3][C::MI][C::NJ][2], F&& between) {
   static_assert(C::WM % 8 == 0 && C::WN % 8 == 0, "lane-constant swizzle keys need WM, WN % 8 == 0");
   const uint8_t* a_base = sA + (wm * C::WM + g) * 128;
   const uint8_t* b_base = sB + (wn * C::WN / 8) * (C::BK * 128);
@@ -182,8 +184,14 @@ __device__ __forceinline__ void dmma3m_ktile(const uint8_t* sA, const uint8_t* s
       for (int i = 0; i < C::MI; ++i)
 #pragma unroll
         for (int j = 0; j < C::NJ; ++j) dmma(p[2][i][j][0], p[2][i][j][1], as[i], bs[j]);
+      between(2 * kc + h);
     }
   }
+}
+template <class C>
+__device__ __forceinline__ void dmma3m_ktile(const uint8_t* sA, const uint8_t* sB, int wm, int wn, int g, int t,
+                                             double (&p)[3][C::MI][C::NJ][2]) {
+  dmma3m_ktile<C>(sA, sB, wm, wn, g, t, p, [](int) {});
 }
 // complex result of the 3M products of accumulator (i, j, e)
 template <class C>

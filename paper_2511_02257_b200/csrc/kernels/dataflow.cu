@@ -1,26 +1,24 @@
 // Persistent dataflow worker for a whole plan (see dataflow.hpp for the protocol).
 //
-// One CTA per SM, 11 warps:
-//   8 consumer warps  — DMMA k-tiles and trace block pairs, in ring order;
-//   1 issuer warp     — streams operands of ready items through a STAGES-deep TMA ring of
-//                       32 KB stages (shared memory only, never blocks on global memory):
-//     GEMM item (MM1/BM1/BB2 output tile, or one k-chunk of it): one stage per 16-complex
-//       k-tile (A 64x16 + B 16x64 complex), consumed by the FP64 DMMA k-tile step
-//       (common.cuh, 64 x 64 complex CTA tile, warp tile 32 x 16);
-//     TR_MM item (a range of 32x32 block pairs of one time slice): one stage per block pair
-//       (A[t,I,J] and B[t,J,I], 16 KB each, 128-byte swizzled), consumed with FP64 FMAs;
-//     TR_MM stages are interleaved between GEMM k-tiles (tr_ratio per k-tile), so the trace
-//     operands stream from HBM while the DMMAs run;
-//   2 scheduler warps — one per queue (GEMM, TR_MM): claim items, decode them, poll their
-//                       dependencies without blocking, hand ready items to the issuer, and
-//                       publish finished items (fence + done counter).
-// The trace math runs on the consumer warps between k-tiles because DMMA and DFMA share the
-// SM's FP64 datapath: a co-resident DFMA kernel is starved by DMMA issue (measured:
-// tools/microbench/dmma_dfma_share.cu).
+// One CTA per SM, 12 warps:
+//   8 consumer warps — DMMA k-tiles of GEMM items from the GEMM ring (common.cuh 3M k-tile,
+//                      64 x 64 complex CTA tile, warp tile 32 x 16), epilogue, fused traces;
+//   4 aux warps      — one per SM sub-partition; all lanes compute the TR_MM block pairs of
+//                      the trace ring (8 rows of each 32 x 32 pair per warp, FP64 FMAs), and
+//                      lane 0 of three of them carries a role:
+//     issuer: streams operands of ready items through two TMA rings of 32 KB stages (GEMM:
+//       one stage per 16-complex k-tile (A 64x16 + B 16x64 complex) or per half partner tile of
+//       a fused trace; trace: one 32x32 block pair A[t,I,J], B[t,J,I], 128-byte swizzled);
+//       shared memory only, never blocks on global memory or on one ring;
+//     GEMM / TR scheduler: claim items, decode them, poll their dependencies without
+//       blocking, hand ready items to the issuer, and publish finished items (fence + done
+//       counter).
+// DMMA and DFMA share a sub-partition's FP64 pipe; trace FMAs in the aux warps take only
+// their ~3 % share of it and never stall a warp that issues DMMAs.
 // Reductions are deterministic: a chunked tile is summed chunk by chunk by the CTA that
-// completes its last chunk (ticket); a TR_MM item's warp partials are summed in warp order by
-// the TR scheduler, and a slice's pieces in piece order by the CTA completing its last piece.
-// Completion: consumer warps arrive on the item's done mbarrier after their stores
+// completes its last chunk (ticket); a TR_MM item's aux-warp partials are summed in warp order
+// by the TR scheduler, and a slice's pieces in piece order by the CTA completing its last piece.
+// Completion: the warps that worked on an item arrive on its done mbarrier after their stores
 // (__syncwarp orders the lanes' stores first); the scheduler acquires it, fences at GPU scope
 // (cumulative) and increments the op's done counter; a dependent CTA's scheduler acquires the
 // counter (ld.acquire.gpu) and issues a proxy fence before TMA reads data other SMs wrote
@@ -33,16 +31,15 @@ namespace cc {
 namespace {
 using namespace dev;
 
-#ifndef DF_STAGES
-#define DF_STAGES 7
+#ifndef DF_GSTAGES
+#define DF_GSTAGES 4      // GEMM ring stages (32 KB)
 #endif
-using GC = Cfg<64, 64, 16, 32, 16, DF_STAGES>;   // 32 KB stages
-constexpr int CW = GC::NCW * 32;           // 256 consumer threads (+ issuer + 2 scheduler warps)
-constexpr int NT = CW + 96;
-#ifndef DF_CREDIT_CAP
-#define DF_CREDIT_CAP 2   // trace credit saved while no trace item is ready, in k-tiles' worth
-                          // (c2: 2 -> 4.39 ms, 4 -> 4.41, 8 -> 4.55, 32 -> 4.96)
+#ifndef DF_TSTAGES
+#define DF_TSTAGES 3      // trace ring stages (32 KB: one 32 x 32 complex block pair)
 #endif
+using GC = Cfg<64, 64, 16, 32, 16, DF_GSTAGES>;   // 32 KB stages
+constexpr int CW = GC::NCW * 32;           // 256 consumer threads
+constexpr int NT = CW + 256;           // + 4 trace warps + issuer, two schedulers, an idle warp
 constexpr int TB = 32;                     // trace block edge (complex)
 constexpr int INFO = 4;                    // item slots per queue (claimed-ready-running-unpublished)
 static_assert(GC::A_BYTES == TB * TB * 16 && GC::B_BYTES == TB * TB * 16, "a trace block pair fills one stage");
@@ -111,7 +108,7 @@ __device__ __forceinline__ void decode_item(const DfQueue& q, int64_t item, Item
   inf.item = item;
   const int oi = q.item_op[item];
   const DfOp& op = q.ops[oi];
-  const int64_t local = item - op.first_item;
+  const int64_t local = q.item_local[item];
   inf.op = oi;
   inf.kind = op.kind;
   inf.tA = static_cast<const uint8_t*>(tmaps) + size_t(2 * op.tmap) * 128;
@@ -170,7 +167,7 @@ __device__ __forceinline__ bool deps_ready(const DfArgs& a, const DfOp& op, int 
 }
 
 // Stage descriptor (producer -> consumers, one per ring stage)
-constexpr uint32_t SK_TRACE = 1, SK_STOP = 2;   // 0: GEMM k-tile
+constexpr uint32_t SK_STOP = 2;   // 0: data stage
 constexpr uint32_t SD_FIRST = 1u << 5, SD_LAST = 1u << 6;
 static_assert(INFO <= 8, "slot field is 3 bits");
 
@@ -223,62 +220,90 @@ __device__ __forceinline__ void trace_stage_loads(const ItemInfo& inf, int k, ui
   }
 }
 
-// Shared memory: the dynamic ring (+ barriers + alignment slack) and the static control arrays
-// (item slots, barriers, stage descriptors, trace partials) must fit 227 KB per CTA.  The
-// control arrays stay static: addressed through dynamic-region pointers they measured 2 %
+// Shared memory: the two dynamic rings (+ barriers + alignment slack) and the static control
+// arrays (item slots, barriers, stage descriptors, trace partials) must fit 227 KB per CTA.
+// The control arrays stay static: addressed through dynamic-region pointers they measured 2 %
 // slower (c2: 4.75 vs 4.64 ms at 6 stages).
-constexpr int DF_SMEM = GC::STAGES * GC::STAGE_BYTES + 2 * GC::STAGES * 8 + 1024;
+constexpr int GS = GC::STAGES;             // GEMM ring stages
+constexpr int TS = DF_TSTAGES;             // trace ring stages
+constexpr int STAGE = GC::STAGE_BYTES;     // 32 KB
+constexpr int DF_SMEM = (GS + TS) * STAGE + 2 * (GS + TS) * 8 + 1024;
 constexpr int DF_STATIC_SMEM =
-    int(2 * INFO * sizeof(ItemInfo)) + 4 * INFO * 8 + GC::STAGES * 4 + INFO * GC::NCW * 16 + 4;
+    int(2 * INFO * sizeof(ItemInfo)) + 4 * INFO * 8 + (GS + TS) * 4 + INFO * 4 * 16 + 4;
 static_assert(DF_SMEM + DF_STATIC_SMEM <= 232448, "dataflow worker exceeds 227 KB of shared memory");
 
-// launch bounds of 12 warps although 11 run: caps registers at 168 (3 warps per SM
-// sub-partition x 32 x 168 <= 16K registers each)
+// warp-uniform non-blocking mbarrier test (every lane tests; the warp agrees only when all see it)
+__device__ __forceinline__ bool mbar_ready_warp(uint64_t* bar, uint32_t parity) {
+  return __all_sync(0xffffffffu, mbar_test(bar, parity));
+}
+
+// Warps (16, four warpgroups): 8 consumer warps (DMMA k-tiles of the GEMM ring, warpgroups 0-1),
+// 4 trace warps (warpgroup 2, one per SM sub-partition: the TR_MM block pairs of the trace
+// ring, 8 rows of each 32 x 32 pair per warp) and warpgroup 3: issuer, GEMM scheduler, TR
+// scheduler (lane 0 each) and an idle warp.  DMMA and DFMA share a sub-partition's FP64 pipe,
+// so trace FMAs queue behind DMMAs: done by the consumer warps they stalled the warps issuing
+// DMMAs (trace stages were 18.6 % of consumer time; interleaving their FMAs between DMMA
+// k-quads, or running them in the role warps, measured slower still); in their own warps they
+// take only their ~3 % share of the pipe.  Registers: launched at 128 per thread (512
+// threads); setmaxnreg moves them to the consumers (184), from the trace warps (72) and the
+// role warps (72) (no spills; 184 / 88 / 56 spilled in the role code).
 // PROF: the instantiation with per-item / per-CTA timing (cc_execute flags bit 5); the plain
-// one compiles every profiling statement out (they cost ~2.5 % in registers and scheduling).
+// one compiles every profiling statement out.
+constexpr int NAUX = 4;
+static_assert(TB % NAUX == 0, "trace rows split evenly over the trace warps");
+constexpr int REG_MMA = 184, REG_TRACE = 72, REG_ROLE = 72;
+static_assert(8 * REG_MMA + 4 * REG_TRACE + 4 * REG_ROLE <= 16 * 128, "register file: 64K per SM");
 template <bool PROF>
-__global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
+__global__ void __launch_bounds__(CW + 256, 1) df_worker(DfArgs a) {
   using C = GC;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned stage base, derived from the __shared__ array by pointer arithmetic so
   // the compiler keeps the shared address space (LDS, not generic LD)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
+  uint8_t* tsmem = smem + GS * STAGE;        // trace ring
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (GS + TS) * STAGE);
+  uint64_t* empty = full + GS;
+  uint64_t* full_t = empty + GS;
+  uint64_t* empty_t = full_t + TS;
   __shared__ ItemInfo s_info[2][INFO];
   __shared__ uint64_t info_full[2][INFO], done[2][INFO];
-  __shared__ uint32_t s_desc[C::STAGES];
-  __shared__ double2 red[INFO][GC::NCW];    // TR_MM item partials per consumer warp, per slot
+  __shared__ uint32_t s_desc[GS], s_desc_t[TS];
+  __shared__ double2 red[INFO][NAUX];       // TR_MM item partials per trace warp, per slot
   __shared__ int s_flag;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < GS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NCW);
     }
-    for (int x = 0; x < 2; ++x)
-      for (int s = 0; s < INFO; ++s) {
-        mbar_init(&info_full[x][s], 1);     // scheduler -> issuer: item ready
-        mbar_init(&done[x][s], C::NCW);     // consumers -> scheduler: item finished
-      }
+    for (int s = 0; s < TS; ++s) {
+      mbar_init(&full_t[s], 1);
+      mbar_init(&empty_t[s], NAUX);
+    }
+    for (int s = 0; s < INFO; ++s) {
+      mbar_init(&info_full[0][s], 1);     // scheduler -> issuer: item ready
+      mbar_init(&info_full[1][s], 1);
+      mbar_init(&done[0][s], C::NCW);     // consumers -> GEMM scheduler: item finished
+      mbar_init(&done[1][s], NAUX);       // trace warps -> TR scheduler: trace item finished
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == C::NCW) {
-    // ----------------------------------- issuer -------------------------------------------
+  if (warp >= C::NCW + NAUX) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_ROLE));
+    const int role = warp - C::NCW - NAUX;   // 0 issuer, 1 GEMM scheduler, 2 TR scheduler, 3 idle
+    if (lane != 0 || role == 3) return;
+    // ---------------------------- issuer role (aux 0, lane 0) ------------------------------
     // Takes ready items of both kinds from the schedulers (shared memory only) and streams
-    // their operands through the one TMA ring: TR_MM stages go between GEMM k-tiles (up to
-    // tr_ratio per k-tile), so the trace operands arrive while the DMMAs run.  It never
-    // touches global memory itself and blocks only on a free ring stage.
-    if (lane != 0) return;
-    uint32_t nx[2] = {0u, 0u};
-    bool have[2] = {false, false}, ex[2] = {false, false};
+    // their operands through the two TMA rings (GEMM: k-tiles and fused-trace partner tiles;
+    // trace: block pairs); never blocks on global memory or on one ring while the other has
+    // room.  Returns true once both rings carry their stop marker.
+    uint32_t nx[2] = {0u, 0u}, pos[2] = {0u, 0u};
+    bool have[2] = {false, false}, ex[2] = {false, false}, stop_put[2] = {false, false};
     int slot_of[2] = {0, 0}, k_of[2] = {0, 0}, np_of[2] = {0, 0};
-    uint32_t pos = 0;
-    int credit = 0;
-    for (;;) {
+    auto issuer_step = [&]() -> bool {
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
         if (!have[x] && !ex[x]) {
@@ -296,66 +321,60 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
           }
         }
       }
-      if (ex[0] && ex[1]) break;
-      if (!have[0] && !have[1]) {
-        __nanosleep(20);
-        continue;
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        if (!have[x] && !(ex[x] && !stop_put[x])) continue;
+        const uint32_t nst = x ? uint32_t(TS) : uint32_t(GS);
+        const int st = int(pos[x] % nst);
+        if (!mbar_test(x ? &empty_t[st] : &empty[st], ((pos[x] / nst) & 1u) ^ 1u)) continue;
+        uint32_t* desc = x ? &s_desc_t[st] : &s_desc[st];
+        uint64_t* fb = x ? &full_t[st] : &full[st];
+        ++pos[x];
+        if (!have[x]) {                      // the queue is drained: the ring's stop marker
+          *desc = SK_STOP;
+          mbar_arrive(fb);
+          stop_put[x] = true;
+          continue;
+        }
+        const ItemInfo& inf = s_info[x][slot_of[x]];
+        const int k = k_of[x];
+        *desc = (uint32_t(slot_of[x]) << 2) | (k == 0 ? SD_FIRST : 0u) | (k == np_of[x] - 1 ? SD_LAST : 0u);
+        mbar_expect_tx(fb, STAGE);
+        if (x) trace_stage_loads(inf, k, tsmem + st * STAGE, fb);
+        else gemm_stage_loads(inf, k, smem + st * STAGE, fb, a.tmaps);
+        if (++k_of[x] == np_of[x]) have[x] = false;
       }
-      // credit in 1/8 stages: a GEMM k-tile earns tr_ratio8, a TR_MM stage costs 8
-      const int x = (have[1] && (!have[0] || credit >= 8)) ? 1 : 0;
-      // (the cap is at least one trace stage, so a low ratio still interleaves)
-      if (have[0]) credit = x ? credit - 8 : min(credit + a.tr_ratio8, max(8, DF_CREDIT_CAP * a.tr_ratio8));
-      const ItemInfo& inf = s_info[x][slot_of[x]];
-      const int k = k_of[x];
-      const int st = int(pos % C::STAGES);
-      mbar_wait(&empty[st], ((pos / C::STAGES) & 1u) ^ 1u);
-      s_desc[st] = uint32_t(x) | (uint32_t(slot_of[x]) << 2) | (k == 0 ? SD_FIRST : 0u) |
-                   (k == np_of[x] - 1 ? SD_LAST : 0u);
-      mbar_expect_tx(&full[st], C::STAGE_BYTES);
-      uint8_t* sA = smem + st * C::STAGE_BYTES;
-      if (x == 0) gemm_stage_loads(inf, k, sA, &full[st], a.tmaps);
-      else trace_stage_loads(inf, k, sA, &full[st]);
-      ++pos;
-      if (++k_of[x] == np_of[x]) have[x] = false;
-    }
-    const int st = int(pos % C::STAGES);
-    mbar_wait(&empty[st], ((pos / C::STAGES) & 1u) ^ 1u);
-    s_desc[st] = SK_STOP;
-    mbar_arrive(&full[st]);
-    return;
-  }
-  if (warp > C::NCW) {
-    // ------------------------------ schedulers / publishers -------------------------------
-    // Warp NCW+1 serves the GEMM queue, warp NCW+2 the TR_MM queue.  Each claims items (at
-    // most `ahead` unpublished), decodes them, polls their dependencies without blocking and
-    // hands ready items to the issuer in claim order; and it publishes finished items in the
-    // same order (the consumers finish the items of one kind in ring order): after the
-    // consumer warps' arrivals on done[slot] (acquiring their stores) it makes the stores
-    // visible at GPU scope (cumulative fence) and bumps the op's done counter, so neither the
-    // global-memory latency of claiming and polling nor the fence's drain sits on the
-    // issuer's or the consumers' path.
-    if (lane != 0) return;
-    const int x = warp - C::NCW - 1;
-    const DfQueue& Q = x == 0 ? a.q : a.qt;
-    unsigned long long* prof = PROF ? (x == 0 ? a.prof : a.prof_t) : nullptr;
-    const uint32_t ahead = uint32_t(x == 0 ? a.ahead_g : a.ahead_t);
+      return stop_put[0] && stop_put[1];
+    };
+    // ------------------ scheduler / publisher role (aux 1: GEMM, aux 2: TR, lane 0) --------
+    // Claims items (at most `ahead` unpublished), decodes them, polls their dependencies
+    // without blocking and hands ready items to the issuer in claim order; publishes finished
+    // items in the same order (items of one kind finish in ring order): after the arrivals
+    // on done[slot] (acquiring the stores) it makes the stores visible at GPU scope
+    // (cumulative fence) and bumps the op's done counter, so neither the global-memory
+    // latency of claiming and polling nor the fence's drain sits on the issuer's or the
+    // consumers' path.  Returns true once the queue is drained and published.
+    const int xq = role == 2 ? 1 : 0;
+    const DfQueue& Q = xq == 0 ? a.q : a.qt;
+    unsigned long long* prof = PROF ? (xq == 0 ? a.prof : a.prof_t) : nullptr;
+    const uint32_t ahead = uint32_t(xq == 0 ? a.ahead_g : a.ahead_t);
     uint32_t n_alloc = 0, n_pub = 0;
     bool exhausted = Q.n_items == 0, pending = false, stopped = false;
     ItemInfo inf;
     int dep = 0;
-    for (;;) {
-      bool idle = true;
+    auto sched_step = [&]() -> bool {
+      const int x = xq;
       while (n_pub < n_alloc && !(stopped && n_pub == n_alloc - 1)) {
         const int s = int(n_pub % INFO);
         if (!mbar_test(&done[x][s], (n_pub / INFO) & 1u)) break;
         const ItemInfo& cur = s_info[x][s];
         const DfOp& op = Q.ops[cur.op];
         if (x == 1) {
-          // TR_MM piece: fixed-order sum of the consumer warps' partials; a slice's pieces are
+          // TR_MM piece: fixed-order sum of the trace warps' partials; a slice's pieces are
           // summed in piece order by the CTA that completes its last piece (ticket)
           double2 v = red[s][0];
 #pragma unroll
-          for (int w = 1; w < C::NCW; ++w) {
+          for (int w = 1; w < NAUX; ++w) {
             v.x += red[s][w].x;
             v.y += red[s][w].y;
           }
@@ -394,11 +413,9 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
           pr[7] = cur.t_first;
         }
         ++n_pub;
-        idle = false;
       }
-      if (stopped) {
-        if (n_pub == n_alloc - 1) break;
-      } else if (!pending && !exhausted && n_alloc - n_pub < ahead) {
+      if (stopped) return n_pub == n_alloc - 1;
+      if (!pending && !exhausted && n_alloc - n_pub < ahead) {
         const unsigned long long t0 = prof ? gtimer() : 0ull;
         const int64_t it = int64_t(atomicAdd(Q.head, 1ull));
         if (it >= Q.n_items) {
@@ -409,7 +426,6 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
           pending = true;
           dep = 0;
         }
-        idle = false;
       }
       if (pending && deps_ready(a, Q.ops[inf.op], x == 0 ? inf.b : inf.t, &dep)) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -426,7 +442,6 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
         mbar_arrive(&info_full[x][s]);     // release: the item is visible to issuer and consumers
         ++n_alloc;
         pending = false;
-        idle = false;
       }
       if (!stopped && exhausted && !pending && n_alloc - n_pub < INFO) {
         const int s = int(n_alloc % INFO);
@@ -434,113 +449,126 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
         mbar_arrive(&info_full[x][s]);
         ++n_alloc;
         stopped = true;
-        idle = false;
       }
-      if (idle) __nanosleep(32);
+      return false;
+    };
+    if (role == 0) {
+      while (!issuer_step()) {}
+    } else {
+      while (!sched_step()) __nanosleep(32);
     }
     return;
   }
+  if (warp >= C::NCW) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_TRACE));
+    const int ax = warp - C::NCW;            // trace warp 0..3 (sub-partition ax)
+    // ------------------------------------ trace rows -----------------------------------------
+    // Rows ax, ax+4, ..., ax+28 of each 32 x 32 block pair, lane = column c: sum of
+    // A[r][c] * B[c][r].  Element (row, col) of a block: chunk col/8, 128-byte row `row`,
+    // 16-byte slot (col%8) ^ (row%8) (TMA 128-byte swizzle): A[r][c] row-contiguous, B[c][r]
+    // one 128-byte row per lane — both conflict-free.  16 partial sums (4 row groups x the 4
+    // real products of a complex MAC) keep the FMAs of one stage independent: they queue
+    // behind the sub-partition's DMMAs, and nothing waits on them until the next stage.
+    constexpr int RG = 4;                    // row groups of independent accumulators
+    double accp[RG][4];
+#pragma unroll
+    for (int q = 0; q < RG; ++q) accp[q][0] = accp[q][1] = accp[q][2] = accp[q][3] = 0.0;
+    uint32_t rt = 0;
+    bool t_stop = false;
+    long long n_tst = 0;
+    // one trace stage if it is there; false when nothing was done
+    auto trace_step = [&]() -> bool {
+      if (t_stop) return false;
+      const int st = int(rt % TS);
+      if (!mbar_ready_warp(&full_t[st], (rt / TS) & 1u)) return false;
+      const uint32_t d = s_desc_t[st];
+      if ((d & 3u) == SK_STOP) {
+        t_stop = true;
+        return false;
+      }
+      if (d & SD_FIRST) {
+#pragma unroll
+        for (int q = 0; q < RG; ++q) accp[q][0] = accp[q][1] = accp[q][2] = accp[q][3] = 0.0;
+        if (ax == 0 && lane == 0 && PROF) s_info[1][int((d >> 2) & 7u)].t_first = gtimer();
+      }
+      const uint8_t* sA = tsmem + st * STAGE;
+      const uint8_t* sB = sA + C::A_BYTES;
+      const int c = lane;
+#pragma unroll
+      for (int qq = 0; qq < TB / NAUX; ++qq) {
+        const int rr = ax + NAUX * qq;
+        const double2 av = *reinterpret_cast<const double2*>(sA + (c >> 3) * (TB * 128) + rr * 128 +
+                                                             (((c & 7) ^ (rr & 7)) << 4));
+        const double2 bv = *reinterpret_cast<const double2*>(sB + (rr >> 3) * (TB * 128) + c * 128 +
+                                                             (((rr & 7) ^ (c & 7)) << 4));
+        double* p = accp[qq % RG];
+        p[0] = fma(av.x, bv.x, p[0]);
+        p[1] = fma(av.y, bv.y, p[1]);
+        p[2] = fma(av.x, bv.y, p[2]);
+        p[3] = fma(av.y, bv.x, p[3]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_t[st]);
+      ++rt;
+      if (PROF) ++n_tst;
+      if (d & SD_LAST) {
+        const int slot = int((d >> 2) & 7u);
+        if (ax == 0 && lane == 0 && PROF) s_info[1][slot].t_comp = gtimer();
+        double re = 0.0, im = 0.0;
+#pragma unroll
+        for (int q = 0; q < RG; ++q) {
+          re += accp[q][0] - accp[q][1];
+          im += accp[q][2] + accp[q][3];
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          re += __shfl_xor_sync(0xffffffffu, re, o);
+          im += __shfl_xor_sync(0xffffffffu, im, o);
+        }
+        // the TR scheduler sums the trace warps' partials (fixed order) when it publishes
+        if (lane == 0) red[slot][ax] = make_double2(re, im);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done[1][slot]);
+      }
+      return true;
+    };
+    for (;;) {
+      if (!trace_step()) {
+        if (t_stop) break;
+        __nanosleep(20);
+      }
+    }
+    if (PROF && lane == 0 && a.prof_sm) a.prof_sm[16 * blockIdx.x + 8 + ax] = n_tst;
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_MMA));
 
   // ----------------------------------- consumers ---------------------------------------------
-  // Stages arrive in ring order.  A GEMM item's stages are contiguous in the GEMM subsequence
-  // (the issuer holds one GEMM item at a time), with TR_MM stages interleaved; the item is
-  // processed by one block scope so its accumulators (and the finished tile kept for fused
-  // traces) live only as long as the item — the register allocator sees disjoint ranges.
+  // GEMM stages arrive in ring order; an item's stages are contiguous (k-tiles, then partner
+  // stages of fused traces), and each item is processed by one block scope so its
+  // accumulators (and the finished tile kept for fused traces) live only as long as the item.
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
   const int g = lane >> 2, t = lane & 3;
   constexpr bool prof = PROF;
-  double2 tacc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-  // profile (thread 0): clock64 cycles waiting for stage data / in stage math+epilogue, per kind
-  long long c_wait[2] = {0, 0}, c_work[2] = {0, 0}, n_st[2] = {0, 0}, ta = 0, tb = 0, c_epi = 0, te = 0;
-  int lastk = 0;
+  // profile (thread 0): clock64 cycles waiting for stage data / in stage math, epilogue
+  long long c_wait = 0, c_work = 0, n_st = 0, c_epi = 0, ta = 0, te = 0;
   uint32_t r = 0;
-  // wait for ring position r, return its descriptor (stage index in st)
   auto next_stage = [&](int& st) -> uint32_t {
-    st = int(r % C::STAGES);
+    st = int(r % GS);
+    if (prof && tid == 0) ta = clock64();
+    mbar_wait(&full[st], (r / GS) & 1u);
     if (prof && tid == 0) {
-      ta = clock64();
-      if (r > 0) c_work[lastk] += ta - tb;
-    }
-    mbar_wait(&full[st], (r / C::STAGES) & 1u);
-    const uint32_t d = s_desc[st];
-    const uint32_t kind = d & 3u;
-    if (prof && tid == 0 && kind < 2) {
-      tb = clock64();
-      c_wait[kind] += tb - ta;
-      ++n_st[kind];
-      lastk = int(kind);
+      c_wait += clock64() - ta;
+      ++n_st;
     }
     ++r;
-    return d;
-  };
-  // one TR_MM block pair: sum of A[r][c] * B[c][r]
-  auto trace_stage = [&](uint32_t d, int st) {
-    const int slot = int((d >> 2) & 7u);
-    const uint8_t* sA = smem + st * C::STAGE_BYTES;
-    if (d & SD_FIRST) {
-      tacc[0] = tacc[1] = make_double2(0.0, 0.0);
-      if (tid == 0 && prof) s_info[1][slot].t_first = gtimer();
-    }
-    const uint8_t* sB = sA + C::A_BYTES;
-    // element (row, col) of a 32x32 block: chunk col/8, 128-byte row `row`, 16-byte slot
-    // (col%8) ^ (row%8) (TMA 128-byte swizzle); warp w takes rows w, w+8, w+16, w+24 of A,
-    // lane = column c: A[r][c] row-contiguous, B[c][r] one 128-byte row per lane — both
-    // conflict-free.
-#pragma unroll
-    for (int qq = 0; qq < TB / 8; ++qq) {
-      const int rr = warp + qq * 8, c = lane;
-      const double2 av = *reinterpret_cast<const double2*>(sA + (c >> 3) * (TB * 128) + rr * 128 +
-                                                           (((c & 7) ^ (rr & 7)) << 4));
-      const double2 bv = *reinterpret_cast<const double2*>(sB + (rr >> 3) * (TB * 128) + c * 128 +
-                                                           (((rr & 7) ^ (c & 7)) << 4));
-      tacc[qq & 1] = cmul_acc(tacc[qq & 1], av, bv);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-    if (!(d & SD_LAST)) return;
-    if (tid == 0 && prof) s_info[1][slot].t_comp = gtimer();
-    double2 acc2 = make_double2(tacc[0].x + tacc[1].x, tacc[0].y + tacc[1].y);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      acc2.x += __shfl_xor_sync(0xffffffffu, acc2.x, o);
-      acc2.y += __shfl_xor_sync(0xffffffffu, acc2.y, o);
-    }
-    // the TR scheduler sums the warps' partials (fixed order) when it publishes the item
-    if (lane == 0) red[slot][warp] = acc2;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&done[1][slot]);
-  };
-  // the next stage of the current GEMM item, running interleaved trace stages on the way
-  auto next_gemm_stage = [&](int& st) {
-    for (;;) {
-      const uint32_t d = next_stage(st);
-      if ((d & 3u) != SK_TRACE) return d;
-      trace_stage(d, st);
-    }
+    return s_desc[st];
   };
 
   for (;;) {
     int st;
     uint32_t d = next_stage(st);
-    const uint32_t kind = d & 3u;
-    if (kind == SK_STOP) {
-      if (prof && tid == 0 && a.prof_sm) {
-        long long* ps = a.prof_sm + 16 * blockIdx.x;
-        ps[0] = c_wait[0];
-        ps[1] = c_wait[1];
-        ps[2] = c_work[0];
-        ps[3] = c_work[1];
-        ps[4] = n_st[0];
-        ps[5] = n_st[1];
-        ps[6] = smid();
-        ps[7] = c_epi;
-      }
-      break;
-    }
-    if (kind == SK_TRACE) {
-      trace_stage(d, st);
-      continue;
-    }
+    if ((d & 3u) == SK_STOP) break;
     // ---------------- GEMM item: k-tiles, epilogue, then partner stages of fused traces ----------------
     const int slot = int((d >> 2) & 7u);
     const ItemInfo& cur = s_info[0][slot];
@@ -554,12 +582,14 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
 #pragma unroll
           for (int j = 0; j < C::NJ; ++j) acc[x][i][j][0] = acc[x][i][j][1] = 0.0;
       for (int k = 0;;) {
-        const uint8_t* sA = smem + st * C::STAGE_BYTES;
+        const uint8_t* sA = smem + st * STAGE;
+        if (prof && tid == 0) ta = clock64();
         dmma3m_ktile<C>(sA, sA + C::A_BYTES, wm, wn, g, t, acc);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
+        if (prof && tid == 0) c_work += clock64() - ta;
         if (++k == cur.kt) break;
-        d = next_gemm_stage(st);
+        d = next_stage(st);
       }
       if (prof && tid == 0) te = clock64();
       const DfOp& op = a.q.ops[cur.op];
@@ -646,14 +676,14 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
 #pragma unroll
             for (int e = 0; e < 2; ++e) v[i][j][e] = gauss3m_combine<C>(acc, i, j, e);
         for (int p = 0; p < 2 * cur.fc; ++p) {
-          d = next_gemm_stage(st);
+          d = next_stage(st);
           // partner stage (fused trace f, half h) holds X rows j in [32h, 32h+32): the warps
           // whose output columns j fall there (wn = 2h, 2h+1: one warp per SM sub-partition)
           // add C[i][j] * X[j][i]; X[j][i] sits in box i/8 = 4wm + mi, row j - 32h, 16-byte
           // slot (i%8) ^ (j%8) = g ^ (2t+e) — conflict-free across each quarter warp
           const int f = p >> 1, h = p & 1;
           if ((wn >> 1) == h) {
-            const uint8_t* sP = smem + st * C::STAGE_BYTES;
+            const uint8_t* sP = smem + st * STAGE;
             double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
 #pragma unroll
             for (int i = 0; i < C::MI; ++i)
@@ -686,6 +716,17 @@ __global__ void __launch_bounds__(CW + 128, 1) df_worker(DfArgs a) {
     // item finished: this warp's stores (ordered by __syncwarp) before the arrival
     __syncwarp();
     if (lane == 0) mbar_arrive(&done[0][slot]);
+  }
+  if (prof && tid == 0 && a.prof_sm) {
+    long long* ps = a.prof_sm + 16 * blockIdx.x;
+    ps[0] = c_wait;
+    ps[1] = 0;
+    ps[2] = c_work;
+    ps[3] = 0;
+    ps[4] = n_st;
+    ps[5] = 0;
+    ps[6] = smid();
+    ps[7] = c_epi;
   }
 }
 

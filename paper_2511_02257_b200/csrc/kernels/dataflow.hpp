@@ -23,7 +23,7 @@ namespace cc {
 struct DfOp {
   int32_t kind;           // 0 GEMM, 1 TRACE
   int32_t n_items;
-  int64_t first_item;     // index of the op's first item in its queue
+  int64_t first_item;     // queue position of the op's first item (informational)
   int32_t sync_id;        // done counter (sync[sync_id] reaches n_items)
   int32_t slice_sync;     // GEMM with a [Lt, ...] output: per-time-slice done counters
                           // sync[slice_sync + t] (-1: none), so a trace of slice t waits only
@@ -64,6 +64,7 @@ struct DfFused {
 struct DfQueue {
   const DfOp* ops;
   const int32_t* item_op;    // op index of each item
+  const int32_t* item_local; // index of each item within its op (queue order need not be op-major)
   int32_t n_ops;
   int64_t n_items;
   unsigned long long* head;  // atomic queue head (zeroed per launch)
@@ -83,7 +84,6 @@ struct DfArgs {
   unsigned long long* prof;   // optional: per GEMM item {claim, ready, end, smid, first data, loop end, kind, -}
   unsigned long long* prof_t; // optional: the same per TR_MM item
   long long* prof_sm;         // optional: per CTA {wait cycles G/T, work cycles G/T, stages G/T, smid, -}
-  int32_t tr_ratio8;          // TR_MM stages the issuer may interleave per GEMM k-tile, x 8
   int32_t ahead_g, ahead_t;   // items a CTA may hold claimed-but-unpublished per queue (<= 4)
   int32_t Lt;                 // time slices (chunked-copy targets)
 };
