@@ -251,7 +251,12 @@ __device__ __forceinline__ bool mbar_ready_warp(uint64_t* bar, uint32_t parity) 
 // one compiles every profiling statement out.
 constexpr int NAUX = 4;
 static_assert(TB % NAUX == 0, "trace rows split evenly over the trace warps");
-constexpr int REG_MMA = 184, REG_TRACE = 72, REG_ROLE = 72;
+#ifndef DF_REG_MMA
+#define DF_REG_MMA 184
+#define DF_REG_TRACE 72
+#define DF_REG_ROLE 72
+#endif
+constexpr int REG_MMA = DF_REG_MMA, REG_TRACE = DF_REG_TRACE, REG_ROLE = DF_REG_ROLE;
 static_assert(8 * REG_MMA + 4 * REG_TRACE + 4 * REG_ROLE <= 16 * 128, "register file: 64K per SM");
 template <bool PROF>
 __global__ void __launch_bounds__(CW + 256, 1) df_worker(DfArgs a) {
@@ -469,7 +474,10 @@ __global__ void __launch_bounds__(CW + 256, 1) df_worker(DfArgs a) {
     // one 128-byte row per lane — both conflict-free.  16 partial sums (4 row groups x the 4
     // real products of a complex MAC) keep the FMAs of one stage independent: they queue
     // behind the sub-partition's DMMAs, and nothing waits on them until the next stage.
-    constexpr int RG = 4;                    // row groups of independent accumulators
+#ifndef DF_TRG
+#define DF_TRG 4
+#endif
+    constexpr int RG = DF_TRG;               // row groups of independent accumulators
     double accp[RG][4];
 #pragma unroll
     for (int q = 0; q < RG; ++q) accp[q][0] = accp[q][1] = accp[q][2] = accp[q][3] = 0.0;

@@ -33,11 +33,11 @@ gp, tp, psm = ctx.dataflow_profile(per_sm=True)
 tot = psm[:, :4].sum(axis=1).astype(np.float64)
 print("GEMM epilogue (thread 0, included in work G): %.0f cycles per item, %.1f%% of consumer time"
       % (psm[:, 7].sum() / max(psm[:, 4].sum() / 8, 1), 100 * psm[:, 7].sum() / tot.sum()))
-print("per CTA (clock64): wait G %.1f%%  wait T %.1f%%  work G %.1f%%  work T %.1f%%;  stages G %d  T %d;"
-      "  per stage: G wait %.0f + work %.0f cyc, T wait %.0f + work %.0f cyc"
-      % tuple([100 * psm[:, k].sum() / tot.sum() for k in range(4)] + [psm[:, 4].sum(), psm[:, 5].sum()] +
-              [psm[:, 0].sum() / max(psm[:, 4].sum(), 1), psm[:, 2].sum() / max(psm[:, 4].sum(), 1),
-               psm[:, 1].sum() / max(psm[:, 5].sum(), 1), psm[:, 3].sum() / max(psm[:, 5].sum(), 1)]))
+print("consumer warps (thread 0, clock64): stage wait %.1f%%, stage math %.1f%%; %d GEMM stages: %.0f wait + %.0f "
+      "math cycles each; trace stages per trace warp (4 per CTA): %s"
+      % (100 * psm[:, 0].sum() / tot.sum(), 100 * psm[:, 2].sum() / tot.sum(), psm[:, 4].sum(),
+         psm[:, 0].sum() / max(psm[:, 4].sum(), 1), psm[:, 2].sum() / max(psm[:, 4].sum(), 1),
+         psm[:, 8:12].sum(axis=0).tolist()))
 g0 = np.vstack([gp, tp])
 g, t = g0[g0[:, 6] == 0], g0[g0[:, 6] == 1]
 t0 = min(g[:, 0].min() if len(g) else 2**63, t[:, 0].min() if len(t) else 2**63)
