@@ -434,7 +434,15 @@ def main():
         d2h_step = st["d2h_bytes"] + n_corr * w.Lt * 16
     t_e2e = float(np.sum(e2e))
     del ctx2, arena2
-    c4 = c4_record(dev, local_dev, streams, args.c4_steps, world, rank) if args.c4 else None
+    c4 = None
+    if args.c4:
+        if world == 1:
+            try:
+                c4 = c4_record(dev, local_dev, streams, args.c4_steps, world, rank)
+            except Exception as e:      # the c2 line stands; the record says what failed
+                c4 = {"error": "%s: %s" % (type(e).__name__, e)}
+        else:                           # collectives inside: an exception on one rank must end the job
+            c4 = c4_record(dev, local_dev, streams, args.c4_steps, world, rank)
 
     # max over ranks
     if world > 1:
@@ -514,29 +522,51 @@ C4_RUNS = [   # (label, scheduler, next-use eviction)
 ]
 
 
-def c4_record(dev, local_dev, streams, steps, world=1, rank=0, pcie_gbs=55.6):
+def c4_record(dev, local_dev, streams, steps, world=1, rank=0, pcie_gbs=55.6, pcie_d2h_gbs=57.2,
+              lend_bytes=24 * 10 ** 9):
     """The paper's thesis workload (BASELINE configs[3]): the two-baryon DAG
     (2000 trees, N=128, S=64, Lt=1: 2 GiB baryon nodes) with the device pool capped at
-    32e9 B so the plan evicts, leaves in pinned host memory.  For each scheduler (tree with
-    next-use and LRU eviction, sibling, the RS-GS-like baseline) one warm-up
-    (physical plan + pinned host pool built) and `steps` timed cc_execute calls (CC_EXEC_AUTO: the tcgen05 Ozaki engine for these baryon
-    GEMMs) from host leaves to correlators on the host; the bytes the executor enqueued are
-    compared with the oracle-parity plan's H2D / D2H bytes.  With N ranks each runs its TREES
-    part (§8(e): locality-ordered, flop-balanced) under its own 32e9 B cap; times are the max
-    over ranks, bytes / evictions the sum.  Returns the record (rank 0)."""
+    32e9 B so the plan evicts.  Each run: one warm-up (physical plan + pinned host pool built)
+    and `steps` timed executions from host leaves to correlators on the host
+    (CC_EXEC_AUTO: the tcgen05 Ozaki engine for these baryon GEMMs); the bytes the executor
+    enqueued are compared with the oracle-parity plan's.
+    N = 1: leaves in pinned host memory; tree scheduler with next-use and LRU eviction,
+    sibling, and the RS-GS-like baseline.
+    N > 1: each rank runs its TREES part (§8(e)) under its own 32e9 B cap with the peer-HBM
+    tier of DESIGN E-10 (it evicts into the next rank's lent HBM, lend_bytes) and cross-GPU
+    leaf sharing E-11 (each leaf crosses PCIe once per run, into its owner rank's HBM, inside
+    the timed region; the other ranks copy it over NVLink); times are the max over ranks,
+    bytes / evictions the sum.  Returns the record (rank 0)."""
     import torch
     from paper_2511_02257_b200 import cc
     w = dags.config_c4()
     cap = 32 * 10 ** 9
+    # device memory this needs (arena + owned-leaf staging + lent tier), checked on every rank
+    # before any collective so that no rank starts the record while another cannot
+    need = (48 << 30) + ((34 << 30) // world + lend_bytes if world > 1 else 0)
+    free = torch.tensor([float(torch.cuda.mem_get_info(dev)[0])], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(free, op=dist.ReduceOp.MIN)
+    if float(free[0]) < need:
+        return {"skipped": "needs %.1f GB of free device memory per rank, %.1f GB free" % (need / 1e9, float(free[0]) / 1e9)}
     arena = torch.empty(48 << 30, dtype=torch.uint8, device=dev)
     ctx = cc.Context(local_dev, arena, streams=streams)
+    ctx.load_workload(w)
+    owners = None
+    if world > 1:
+        ctx.partition(world, rank, cc.PART_TREES)
+        owners = ctx.leaf_owners()
     t_setup = time.perf_counter()
-    host = {}
+    host, leaf_bytes = {}, {}
     tmp = None
     for n in w.nodes:
         if n[1] not in (dags.LEAF_M, dags.LEAF_B):
             continue
         cnt = int(np.prod(leaf_shape(w, n[1])))
+        leaf_bytes[n[0]] = 16 * cnt
+        if owners is not None and owners.get(n[0]) != rank:
+            continue                               # another rank loads it (E-11)
         if tmp is None or tmp.numel() < 2 * cnt:
             tmp = torch.empty(2 * cnt, dtype=torch.float64, device=dev)
         d = tmp[:2 * cnt]
@@ -547,71 +577,103 @@ def c4_record(dev, local_dev, streams, steps, world=1, rank=0, pcie_gbs=55.6):
         host[n[0]] = h
     del tmp
     torch.cuda.synchronize()
+    shared, lent = None, None
+    if world > 1:
+        from paper_2511_02257_b200.dist import SharedLeaves, setup_peer_tier
+        shared = SharedLeaves(ctx, leaf_bytes, host, dev)
+        lent, tier_ptrs = setup_peer_tier(ctx, lend_bytes, dev)
     t_setup = time.perf_counter() - t_setup
     n_corr = len({t[0] for t in w.terms})
     host_corr = torch.empty((n_corr, w.Lt), dtype=torch.complex128, pin_memory=True)
     runs = {}
     flags = cc.EXEC_AUTO
-    for k, (label, algo, nu) in enumerate(C4_RUNS):
-        ctx.load_workload(w)
-        if world > 1:
-            ctx.partition(world, rank, cc.PART_TREES)
+    plan_runs = C4_RUNS if world == 1 else [("tree+next_use+peer_hbm", "CC_TREE", True)]
+    for k, (label, algo, nu) in enumerate(plan_runs):
         t0 = time.perf_counter()
-        _, st = ctx.schedule(getattr(cc, algo), cap_bytes=cap, evict_next_use=nu)
+        if world == 1:
+            _, st = ctx.schedule(getattr(cc, algo), cap_bytes=cap, evict_next_use=nu)
+            for u, h in host.items():
+                ctx.set_leaf(u, h)
+        else:
+            _, st = ctx.schedule(getattr(cc, algo), cap_bytes=cap, evict_next_use=nu, peer_cap_bytes=lend_bytes,
+                                 peer_leaves=shared.ids)
         sched_s = time.perf_counter() - t0
-        for u, h in host.items():
-            ctx.set_leaf(u, h)
         # warm-up of this plan: builds the physical plan and allocates its pinned host pool for
         # evicted intermediates (64 GB for the RS-GS-like plan), which a replay reuses
+        if shared is not None:
+            shared.stage()
         ctx.execute(flags)
-        ts, ex = [], None
+        ts, ex, staged = [], None, 0
         for _ in range(steps):
             torch.cuda.synchronize()
+            if world > 1:
+                import torch.distributed as dist
+                dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(streams[0])
+            if shared is not None:
+                staged = shared.stage()            # the owners' H2D of the shared leaves
             ex = ctx.execute(flags)
             ctx.correlators(host_corr)
             e1.record(streams[0])
             e1.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e-3)
         t = float(np.median(ts))
+        st = dict(st)
+        ex = dict(ex)
+        st["h2d_bytes"] += staged                  # leaf staging is PCIe traffic of the run
+        ex["h2d_bytes"] += staged
         if world > 1:
             import torch.distributed as dist
-            v = torch.tensor([t, st["evictions"], st["h2d_bytes"], st["d2h_bytes"], ex["h2d_bytes"], ex["d2h_bytes"]],
-                             dtype=torch.float64, device=dev)
+            keys = ("evictions", "h2d_bytes", "d2h_bytes", "p2p_in_bytes", "p2p_out_bytes")
+            v = torch.tensor([t] + [st[k] for k in keys] + [ex["h2d_bytes"], ex["d2h_bytes"], ex["p2p_in_bytes"],
+                                                           ex["p2p_out_bytes"]], dtype=torch.float64, device=dev)
             tmax = v[:1].clone()
             dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
             dist.all_reduce(v, op=dist.ReduceOp.SUM)
             t = float(tmax[0])
-            st = dict(st, evictions=int(v[1]), h2d_bytes=int(v[2]), d2h_bytes=int(v[3]))
-            ex = dict(ex, h2d_bytes=int(v[4]), d2h_bytes=int(v[5]))
-        moved = st["h2d_bytes"] + st["d2h_bytes"]
+            st.update({k: int(v[1 + i]) for i, k in enumerate(keys)})
+            ex.update(h2d_bytes=int(v[6]), d2h_bytes=int(v[7]), p2p_in_bytes=int(v[8]), p2p_out_bytes=int(v[9]))
+        # H2D and D2H use the two directions of the link (one link per GPU): the bound is the
+        # busier direction
+        pcie_bound = max(st["h2d_bytes"] / (pcie_gbs * 1e9), st["d2h_bytes"] / (pcie_d2h_gbs * 1e9)) / world
         runs[label] = {
             "e2e_s": t, "steps": steps, "sched_s": sched_s,
             "peak_bytes": st["peak"], "transient_peak_bytes": st["transient_peak"], "evictions": st["evictions"],
             "h2d_bytes": st["h2d_bytes"], "d2h_bytes": st["d2h_bytes"], "host_peak_bytes": st["host_peak_bytes"],
+            "p2p_in_bytes": st.get("p2p_in_bytes", 0), "p2p_out_bytes": st.get("p2p_out_bytes", 0),
             "runtime_h2d_bytes": int(ex["h2d_bytes"]), "runtime_d2h_bytes": int(ex["d2h_bytes"]),
-            "bytes_match_plan": int(ex["h2d_bytes"]) == st["h2d_bytes"] and int(ex["d2h_bytes"]) == st["d2h_bytes"],
-            "pcie_bound_s": moved / (pcie_gbs * 1e9 * world), "pcie_frac": moved / (pcie_gbs * 1e9 * world) / t,
+            "bytes_match_plan": int(ex["h2d_bytes"]) == st["h2d_bytes"] and int(ex["d2h_bytes"]) == st["d2h_bytes"]
+            and int(ex.get("p2p_in_bytes", 0)) == st.get("p2p_in_bytes", 0),
+            "pcie_bound_s": pcie_bound, "pcie_frac": pcie_bound / t,
             "fp64_flops": ex["flops"], "copies_done_s": ex["copy_seconds"]}
-    base = runs["rsgs_like+lru"]
     ratios = {}
-    for label in ("tree+next_use", "tree+lru", "sibling+lru"):
-        r = runs[label]
-        ratios[label] = {"time": base["e2e_s"] / r["e2e_s"],
-                         "evictions": base["evictions"] / max(r["evictions"], 1),
-                         "peak": base["peak_bytes"] / r["peak_bytes"],
-                         "bytes_moved": (base["h2d_bytes"] + base["d2h_bytes"]) / (r["h2d_bytes"] + r["d2h_bytes"])}
-    leaf_bytes = sum(h.numel() * 8 for h in host.values())
-    del ctx, arena, host
+    if "rsgs_like+lru" in runs:
+        base = runs["rsgs_like+lru"]
+        for label in ("tree+next_use", "tree+lru", "sibling+lru"):
+            r = runs[label]
+            ratios[label] = {"time": base["e2e_s"] / r["e2e_s"],
+                             "evictions": base["evictions"] / max(r["evictions"], 1),
+                             "peak": base["peak_bytes"] / r["peak_bytes"],
+                             "bytes_moved": (base["h2d_bytes"] + base["d2h_bytes"]) / (r["h2d_bytes"] + r["d2h_bytes"])}
+    if world > 1:
+        dist.barrier()                              # every rank's executes are done
+        shared.close()
+        from paper_2511_02257_b200.dist import close_buffers
+        close_buffers(tier_ptrs)
+    leaf_bytes_total = sum(leaf_bytes.values())
+    del ctx, arena, host, lent
     torch.cuda.empty_cache()
     return {"workload": "%s (BASELINE.json configs[3]: two-baryon system, %d graphs, N=%d, S=%d, Lt=%d; "
                         "device pool capped at 32e9 B)" % (w.name, len(w.trees), w.N, w.S, w.Lt),
-            "cap_bytes": cap, "ranks": world, "split": "TREES parts, one per rank" if world > 1 else "none",
+            "cap_bytes": cap, "ranks": world,
+            "split": "TREES parts, one per rank; peer-HBM tier (E-10, %d B lent per rank) + shared leaves (E-11)"
+                     % lend_bytes if world > 1 else "none",
             "engine": "CC_EXEC_AUTO (tcgen05 INT8 Ozaki GEMMs, op-by-op with copy streams)",
-            "leaves": "pinned host (%.1f GiB), H2D inside every timed execute" % (leaf_bytes / 2 ** 30),
-            "pcie_gbs_assumed": pcie_gbs, "setup_s": t_setup, "runs": runs,
-            "rsgs_over_ours": ratios,
+            "leaves": "pinned host (%.1f GiB), H2D inside every timed execution" % (leaf_bytes_total / 2 ** 30),
+            "pcie_gbs_measured": {"h2d": pcie_gbs, "d2h": pcie_d2h_gbs,
+                                  "source": "profiles/r01_microbench_fp64_pcie.txt (pinned cudaMemcpyAsync)"},
+            "setup_s": t_setup, "runs": runs, "rsgs_over_ours": ratios,
             "paper_context": "paper (Frontier/Summit-era GPUs, Redstar): up to 1.9x faster, 2.1x lower peak memory, "
                              "4.2x fewer evictions than RS-GS (P:31, P:944, P:979-982)"}
 

@@ -55,29 +55,45 @@ def setup_peer_tier(ctx, lend_bytes, device, group=None):
     return lent, ptrs
 
 
-def share_leaves(ctx, host_leaves, device, group=None):
-    """E-11 under a TREES split (rank = TREES part): the owner of each leaf (cc_leaf_owners)
-    copies it host -> its HBM once; every rank then points each leaf at the owner's copy
-    (cc_set_leaf_peer: a peer copy over NVLink, or a local device copy for its own leaves).
-    host_leaves: {leaf id: pinned host tensor of the full leaf}.  Returns (peer leaf ids for
-    cc_schedule's peer_leaves, own staging buffer, mapped addresses); the caller keeps the
-    buffers alive, and times the staging (H2D of the owned leaves) as part of the run."""
-    rank = dist.get_rank(group)
-    owners = ctx.leaf_owners()
-    mine = sorted(u for u, o in owners.items() if o == rank)
-    offs, total = {}, 0
-    for u in mine:
-        offs[u] = total
-        total += (host_leaves[u].numel() * host_leaves[u].element_size() + 255) // 256 * 256
-    buf = torch.empty(max(total, 256), dtype=torch.uint8, device=device)
-    for u in mine:
-        n = host_leaves[u].numel() * host_leaves[u].element_size()
-        buf[offs[u]:offs[u] + n].view(host_leaves[u].dtype).copy_(host_leaves[u], non_blocking=True)
-    all_offs = [None] * dist.get_world_size(group)
-    dist.all_gather_object(all_offs, offs, group=group)
-    torch.cuda.synchronize(device)
-    ptrs = exchange_buffers(buf, group)
-    dist.barrier(group)                     # every owner's copies have landed
-    for u, o in owners.items():
-        ctx.set_leaf_peer(u, ptrs[o] + all_offs[o][u], host_leaves[u].numel() * host_leaves[u].element_size())
-    return sorted(owners), buf, ptrs
+class SharedLeaves:
+    """E-11 under a TREES split (rank = TREES part): every leaf is held in the HBM of its owner
+    (cc_leaf_owners), which loads it over PCIe once per run (stage()); every rank points each
+    leaf at the owner's copy (cc_set_leaf_peer: a peer copy over NVLink, or a local device copy
+    for its own leaves) and schedules with peer_leaves = ids.
+    leaf_bytes: {leaf id: bytes of the full leaf}; host_owned: {leaf id: pinned host tensor}
+    for the leaves this rank owns.  Keep the object alive until every rank's last cc_execute
+    returned (barrier), then close()."""
+
+    def __init__(self, ctx, leaf_bytes, host_owned, device, group=None):
+        self.group = group
+        rank = dist.get_rank(group)
+        owners = ctx.leaf_owners()
+        self.mine = sorted(u for u, o in owners.items() if o == rank)
+        self.offs, total = {}, 0
+        for u in self.mine:
+            self.offs[u] = total
+            total += (leaf_bytes[u] + 255) // 256 * 256
+        self.buf = torch.empty(max(total, 256), dtype=torch.uint8, device=device)
+        self.host = host_owned
+        all_offs = [None] * dist.get_world_size(group)
+        dist.all_gather_object(all_offs, self.offs, group=group)
+        self.ptrs = exchange_buffers(self.buf, group)
+        for u, o in owners.items():
+            ctx.set_leaf_peer(u, self.ptrs[o] + all_offs[o][u], leaf_bytes[u])
+        self.ids = sorted(owners)
+
+    def stage(self):
+        """Owners copy their leaves host -> HBM (the run's only leaf PCIe traffic; current
+        stream); returns the bytes copied.  Ends with a barrier: every owner's copies landed."""
+        n = 0
+        for u in self.mine:
+            h = self.host[u]
+            nb = h.numel() * h.element_size()
+            self.buf[self.offs[u]:self.offs[u] + nb].view(h.dtype).copy_(h, non_blocking=True)
+            n += nb
+        torch.cuda.synchronize()
+        dist.barrier(self.group)
+        return n
+
+    def close(self):
+        close_buffers(self.ptrs, self.group)

@@ -22,7 +22,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 from synth import dags, rng as srng  # noqa: E402
 from paper_2511_02257_b200 import cc  # noqa: E402
-from paper_2511_02257_b200.dist import setup_peer_tier, share_leaves, close_buffers  # noqa: E402
+from paper_2511_02257_b200.dist import setup_peer_tier, SharedLeaves, close_buffers  # noqa: E402
 
 
 def main():
@@ -49,13 +49,17 @@ def main():
             ctx.fill_synthetic(d, cnt, w.data_seed, n[0], 0, w.leaf_mode, sigma)
             torch.cuda.synchronize(dev)      # the generator runs on the library's stream
             host[n[0]] = d.cpu().pin_memory()
-    tier_ptrs, leaf_ptrs, peer_leaves = [], [], []
+    tier_ptrs, peer_leaves = [], []
     if mode in ("tier", "both"):
         lent, tier_ptrs = setup_peer_tier(ctx, 8 << 20, dev)
     else:
         peer_cap = 0
+    shared = None
     if mode in ("leaves", "both"):
-        peer_leaves, buf, leaf_ptrs = share_leaves(ctx, host, dev)
+        sizes = {u: h.numel() * h.element_size() for u, h in host.items()}
+        shared = SharedLeaves(ctx, sizes, host, dev)
+        shared.stage()
+        peer_leaves = shared.ids
     else:
         for u, h in host.items():
             ctx.set_leaf(u, h)
@@ -70,8 +74,8 @@ def main():
     dist.barrier()                          # every rank's executes are done before unmapping
     if tier_ptrs:
         close_buffers(tier_ptrs)
-    if leaf_ptrs:
-        close_buffers(leaf_ptrs)
+    if shared is not None:
+        shared.close()
     if rank == 0:
         total = {}
         for p, *_ in allp:
