@@ -598,6 +598,7 @@ def c4_record(dev, local_dev, streams, steps, world=1, rank=0, pcie_gbs=55.6, pc
             _, st = ctx.schedule(getattr(cc, algo), cap_bytes=cap, evict_next_use=nu, peer_cap_bytes=lend_bytes,
                                  peer_leaves=shared.ids)
         sched_s = time.perf_counter() - t0
+        part = ctx.part_info()          # replicated share of a TREES part (reading M-3)
         # warm-up of this plan: builds the physical plan and allocates its pinned host pool for
         # evicted intermediates (64 GB for the RS-GS-like plan), which a replay reuses
         if shared is not None:
@@ -626,6 +627,11 @@ def c4_record(dev, local_dev, streams, steps, world=1, rank=0, pcie_gbs=55.6, pc
         if world > 1:
             import torch.distributed as dist
             keys = ("evictions", "h2d_bytes", "d2h_bytes", "p2p_in_bytes", "p2p_out_bytes")
+            pv = torch.tensor([part["work"], part["replicated_work"], part["leaf_bytes"], part["replicated_leaf_bytes"]],
+                              dtype=torch.float64, device=dev)
+            dist.all_reduce(pv, op=dist.ReduceOp.SUM)
+            part = dict(work=int(pv[0]), replicated_work=int(pv[1]), leaf_bytes=int(pv[2]),
+                        replicated_leaf_bytes=int(pv[3]))
             v = torch.tensor([t] + [st[k] for k in keys] + [ex["h2d_bytes"], ex["d2h_bytes"], ex["p2p_in_bytes"],
                                                            ex["p2p_out_bytes"]], dtype=torch.float64, device=dev)
             tmax = v[:1].clone()
@@ -646,7 +652,11 @@ def c4_record(dev, local_dev, streams, steps, world=1, rank=0, pcie_gbs=55.6, pc
             "bytes_match_plan": int(ex["h2d_bytes"]) == st["h2d_bytes"] and int(ex["d2h_bytes"]) == st["d2h_bytes"]
             and int(ex.get("p2p_in_bytes", 0)) == st.get("p2p_in_bytes", 0),
             "pcie_bound_s": pcie_bound, "pcie_frac": pcie_bound / t,
-            "fp64_flops": ex["flops"], "copies_done_s": ex["copy_seconds"]}
+            "fp64_flops": ex["flops"], "copies_done_s": ex["copy_seconds"],
+            "replication": {"work_flops_over_8": part["work"], "replicated_work": part["replicated_work"],
+                            "replicated_work_share": part["replicated_work"] / max(part["work"], 1),
+                            "leaf_bytes": part["leaf_bytes"], "replicated_leaf_bytes": part["replicated_leaf_bytes"],
+                            "note": "summed over ranks; reading M-3 (owner = part of the first selected tree)"}}
     ratios = {}
     if "rsgs_like+lru" in runs:
         base = runs["rsgs_like+lru"]

@@ -181,7 +181,8 @@ def test_schedule_and_mode_invariance_bitwise():
     base = run_gpu(w, algo=cc.CC_TREE)[1]
     for kw in (dict(algo=cc.CC_SIBLING), dict(algo=cc.CC_RSGS), dict(flags=1), dict(device_leaves=True),
                dict(flags=1, device_leaves=True), dict(options={"precopy": 0}), dict(options={"early_copies": 0}),
-               dict(options={"copy_reorder": 0, "tr_ratio": 0.5})):
+               dict(options={"copy_reorder": 0, "tr_ratio": 0.5}), dict(options={"slice_major": 0}),
+               dict(flags=1, device_leaves=True, options={"slice_major": 0})):
         other = run_gpu(w, **kw)[1]
         for t in base:
             assert np.array_equal(base[t], other[t]), kw
@@ -416,3 +417,20 @@ def test_c5_large_N_time_part(N, n_pairs, n_trees):
         assert_roots_close(got, want)
     del arena
     torch.cuda.empty_cache()
+
+
+def test_slice_major_baryon_chains_bitwise():
+    """Slice-major item order with per-slice GEMM -> GEMM dependencies (BM1 -> BB2 -> TR, c3 /
+    c4 shapes with Lt > 1, and the tritium chain BB1 -> BT2 -> BB1 -> BT2 -> BB3) gives values
+    bit-identical to the op-major order and within tolerance of the oracle."""
+    from paper_2511_02257_b200 import cc
+    for w in (dags.config_c3(N=12, Lt=3, S=4), dags.config_c4(N=8, Lt=3, S=4, n_trees=20),
+              dags.config_c6(N=8, Lt=3, S=4, n_trees=12)):
+        dag = Dag(w)
+        r_or = values.evaluate(dag, lambda u: values.synthetic_leaf(w, u, dag.nodes[u].op))
+        for flags in (0, 1):
+            a = run_gpu(w, flags=flags, device_leaves=bool(flags), options={"slice_major": 1})[1]
+            b = run_gpu(w, flags=flags, device_leaves=bool(flags), options={"slice_major": 0})[1]
+            for t in a:
+                assert np.array_equal(a[t], b[t]), (w.name, flags, t)
+            assert_roots_close(a, r_or)
