@@ -39,7 +39,10 @@ using namespace dev;
 #endif
 using GC = Cfg<64, 64, 16, 32, 16, DF_GSTAGES>;   // 32 KB stages
 constexpr int CW = GC::NCW * 32;           // 256 consumer threads
-constexpr int NT = CW + 256;           // + 4 trace warps + issuer, two schedulers, an idle warp
+#ifndef DF_NAUX
+#define DF_NAUX 4         // trace warps (a multiple of 4: whole warpgroups, equal per sub-partition)
+#endif
+constexpr int NT = CW + 32 * DF_NAUX + 128;   // + trace warps + issuer, two schedulers, an idle warp
 constexpr int TB = 32;                     // trace block edge (complex)
 constexpr int INFO = 4;                    // item slots per queue (claimed-ready-running-unpublished)
 static_assert(GC::A_BYTES == TB * TB * 16 && GC::B_BYTES == TB * TB * 16, "a trace block pair fills one stage");
@@ -229,7 +232,7 @@ constexpr int TS = DF_TSTAGES;             // trace ring stages
 constexpr int STAGE = GC::STAGE_BYTES;     // 32 KB
 constexpr int DF_SMEM = (GS + TS) * STAGE + 2 * (GS + TS) * 8 + 1024;
 constexpr int DF_STATIC_SMEM =
-    int(2 * INFO * sizeof(ItemInfo)) + 4 * INFO * 8 + (GS + TS) * 4 + INFO * 4 * 16 + 4;
+    int(2 * INFO * sizeof(ItemInfo)) + 4 * INFO * 8 + (GS + TS) * 4 + INFO * DF_NAUX * 16 + 4;
 static_assert(DF_SMEM + DF_STATIC_SMEM <= 232448, "dataflow worker exceeds 227 KB of shared memory");
 
 // warp-uniform non-blocking mbarrier test (every lane tests; the warp agrees only when all see it)
@@ -249,7 +252,7 @@ __device__ __forceinline__ bool mbar_ready_warp(uint64_t* bar, uint32_t parity) 
 // role warps (72) (no spills; 184 / 88 / 56 spilled in the role code).
 // PROF: the instantiation with per-item / per-CTA timing (cc_execute flags bit 5); the plain
 // one compiles every profiling statement out.
-constexpr int NAUX = 4;
+constexpr int NAUX = DF_NAUX;
 static_assert(TB % NAUX == 0, "trace rows split evenly over the trace warps");
 #ifndef DF_REG_MMA
 #define DF_REG_MMA 184
@@ -257,9 +260,14 @@ static_assert(TB % NAUX == 0, "trace rows split evenly over the trace warps");
 #define DF_REG_ROLE 72
 #endif
 constexpr int REG_MMA = DF_REG_MMA, REG_TRACE = DF_REG_TRACE, REG_ROLE = DF_REG_ROLE;
-static_assert(8 * REG_MMA + 4 * REG_TRACE + 4 * REG_ROLE <= 16 * 128, "register file: 64K per SM");
+// setmaxnreg moves registers only within the CTA's launch allocation (NT x the launch count,
+// a multiple of 8 per thread): the three budgets must fit in it, or setmaxnreg.inc never returns
+constexpr int LAUNCH_REGS = (65536 / NT) / 8 * 8;
+static_assert(8 * REG_MMA + NAUX * REG_TRACE + 4 * REG_ROLE <= (NT / 32) * LAUNCH_REGS,
+              "register budgets exceed the CTA's launch allocation");
+static_assert(NAUX % 4 == 0, "setmaxnreg works on whole warpgroups");
 template <bool PROF>
-__global__ void __launch_bounds__(CW + 256, 1) df_worker(DfArgs a) {
+__global__ void __launch_bounds__(NT, 1) df_worker(DfArgs a) {
   using C = GC;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned stage base, derived from the __shared__ array by pointer arithmetic so
