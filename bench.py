@@ -527,9 +527,9 @@ def c4_record(dev, local_dev, streams, steps, world=1, rank=0, pcie_gbs=55.6, pc
     """The paper's thesis workload (BASELINE configs[3]): the two-baryon DAG
     (2000 trees, N=128, S=64, Lt=1: 2 GiB baryon nodes) with the device pool capped at
     32e9 B so the plan evicts.  Each run: one warm-up (physical plan + pinned host pool built)
-    and `steps` timed executions from host leaves to correlators on the host
-    (CC_EXEC_AUTO: the tcgen05 Ozaki engine for these baryon GEMMs); the bytes the executor
-    enqueued are compared with the oracle-parity plan's.
+    and `steps` timed executions from host leaves to correlators on the host (the dataflow
+    worker: FP64 DMMA GEMMs, copies overlapped through the flag protocol); the bytes the
+    executor enqueued are compared with the oracle-parity plan's.
     N = 1: leaves in pinned host memory; tree scheduler with next-use and LRU eviction,
     sibling, and the RS-GS-like baseline.
     N > 1: each rank runs its TREES part (§8(e)) under its own 32e9 B cap with the peer-HBM
@@ -586,7 +586,9 @@ def c4_record(dev, local_dev, streams, steps, world=1, rank=0, pcie_gbs=55.6, pc
     n_corr = len({t[0] for t in w.terms})
     host_corr = torch.empty((n_corr, w.Lt), dtype=torch.complex128, pin_memory=True)
     runs = {}
-    flags = cc.EXEC_AUTO
+    # the DMMA dataflow worker (1.58 s on c4 at 48 GiB of arena; the Ozaki engine's leaf-form
+    # cache needs headroom beyond the cap: 1.42-1.55 s at 60-100 GiB, 1.79 s at 48 GiB)
+    flags = 0
     plan_runs = C4_RUNS if world == 1 else [("tree+next_use+peer_hbm", "CC_TREE", True)]
     for k, (label, algo, nu) in enumerate(plan_runs):
         t0 = time.perf_counter()
@@ -679,7 +681,7 @@ def c4_record(dev, local_dev, streams, steps, world=1, rank=0, pcie_gbs=55.6, pc
             "cap_bytes": cap, "ranks": world,
             "split": "TREES parts, one per rank; peer-HBM tier (E-10, %d B lent per rank) + shared leaves (E-11)"
                      % lend_bytes if world > 1 else "none",
-            "engine": "CC_EXEC_AUTO (tcgen05 INT8 Ozaki GEMMs, op-by-op with copy streams)",
+            "engine": "dataflow worker (FP64 DMMA 3M GEMMs; copies on their streams, flag-synchronised)",
             "leaves": "pinned host (%.1f GiB), H2D inside every timed execution" % (leaf_bytes_total / 2 ** 30),
             "pcie_gbs_measured": {"h2d": pcie_gbs, "d2h": pcie_d2h_gbs,
                                   "source": "profiles/r01_microbench_fp64_pcie.txt (pinned cudaMemcpyAsync)"},

@@ -244,6 +244,7 @@ cc_status cc_schedule(cc_ctx* ctx, const cc_sched_cfg* cfg, int64_t* order_out, 
   if (!ctx) return CC_E_INVAL;
   API_BEGIN
   if (!ctx->loaded) throw Error(CC_E_STATE, "cc_schedule before cc_load_dag");
+  NvtxRange nv("cc_schedule");
   if (!cfg) throw Error(CC_E_INVAL, "null config");
   const Dag& g = *ctx->dag;
   ctx->scheduled = false;

@@ -136,6 +136,7 @@ void enqueue_copy(cc_ctx* ctx, cudaStream_t s, const void* src, void* dst, size_
 // tensor maps, upload); the next issue_dataflow only adds their flag writes.
 void prepare_dataflow(cc_ctx* ctx, bool early) {
   if (ctx->df_valid) return;
+  NvtxRange nv("cc prepare_dataflow");
   if (ctx->opt.debug & 1) fprintf(stderr, "[cc] prepare_dataflow\n");
   prepare_phys(ctx);
   PhaseTimer tmr("prepare_dataflow", (ctx->opt.debug & 2) != 0);
@@ -881,6 +882,7 @@ static int32_t ops_kind_of(cc_ctx* ctx, int32_t op) { return ctx->pp.ops[size_t(
 
 // Enqueues one dataflow replay; returns the number of kernel launches.
 int issue_dataflow(cc_ctx* ctx, bool time_copies) {
+  NvtxRange nv("cc issue_dataflow");
   const Dag& g = *ctx->dag;
   int nl = 0;
   const bool dbg = (ctx->opt.debug & 1) != 0;

@@ -69,6 +69,7 @@ void launch_contract(cc_ctx* ctx, const Node& n, const void* a, const void* b, v
 // Issues the plan on the three streams.  Returns the number of kernel launches.
 int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* kev,
           std::vector<int>* kev_kind) {
+  NvtxRange nv("cc issue_opbyop");
   const Dag& g = *ctx->dag;
   const int64_t per_t_m = 16LL * g.N * g.N;
   cudaStream_t st[3] = {ctx->cs, ctx->hs, ctx->ds};

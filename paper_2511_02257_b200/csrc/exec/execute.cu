@@ -4,6 +4,7 @@
 namespace ccx {
 
 void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
+  NvtxRange nv("cc_execute");
   ctx->need_device();
   if (!ctx->scheduled) throw Error(CC_E_STATE, "cc_execute before cc_schedule");
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");

@@ -13,6 +13,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <array>
@@ -39,6 +40,15 @@ using namespace cc;
 #define CC_VERSION "cc-b200 0.2 (sm_100a; FP64 DMMA + TMA; tcgen05 INT8 Ozaki; sibling/tree/RS-GS schedulers; LRU/next-use plan)"
 
 namespace ccx {
+// NVTX range for the executor phases (header-only NVTX 3: a no-op unless a tool such as
+// nsys / ncu is attached), so a timeline shows schedule / plan / prepare / issue on the host
+// next to the copies and the worker on the device.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 // ctx->opt.debug bit 1: host-side phase times of plan preparation / issue on stderr
 struct PhaseTimer {
   const char* what;

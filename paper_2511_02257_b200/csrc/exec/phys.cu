@@ -189,6 +189,7 @@ ScratchSizes scratch_sizes(cc_ctx* ctx) {
 // events and the host pool.  Called lazily by cc_execute.
 void prepare_phys(cc_ctx* ctx) {
   if (ctx->phys_valid) return;
+  NvtxRange nv("cc prepare_phys");
   PhaseTimer pt("prepare_phys", (ctx->opt.debug & 2) != 0);
   ctx->release_phys();
   pt.lap("release");
