@@ -283,12 +283,16 @@ cc_status cc_execute_async(cc_ctx* ctx, int32_t flags);
  *                     of ops whose inputs arrive together, so a slice's GEMM outputs are traced
  *                     (and its leaves reused) while they are still in L2; applies when every
  *                     dependency between contractions is per time slice [1]
+ *   leaf_slots        unbounded plans: place every host leaf in a fixed slot of the pool so no
+ *                     leaf copy waits for freed memory (falls back when the pool cannot hold the
+ *                     leaves next to the plan's intermediates) [1]
  * Errors: CC_E_INVAL for out-of-range values. */
 typedef struct {
   int32_t trace_fusion, copy_reorder, early_copies, precopy, ozaki_leaf_cache, ozaki_slices;
   int64_t h2d_chunk_bytes;
   double tr_ratio;
   int32_t debug, slice_major;
+  int32_t leaf_slots, pad_;
 } cc_options;
 cc_status cc_get_options(cc_ctx* ctx, cc_options* out);
 cc_status cc_set_options(cc_ctx* ctx, const cc_options* opt);

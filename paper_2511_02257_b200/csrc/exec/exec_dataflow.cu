@@ -182,26 +182,41 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     ctx->df_sync = reinterpret_cast<int*>(ctx->df_sync_base + 16);
     ctx->df_sync_bytes = sz_sync;
   }
-  // 0b. early H2D copies.  A leaf H2D whose device range lies above everything the plan
-  // touched before it (fresh pool memory) waits on nothing and nothing earlier depends on it:
+  // 0b. early H2D copies.  A leaf H2D whose device range no earlier op of the plan touched
+  // (fresh pool memory, e.g. every leaf slot) waits on nothing and nothing earlier depends on it:
   // it may be issued first, before the dependency analysis, so the copy engine starts while
   // the host builds the rest.  These copies are ordered greedily by the work they enable:
   // next = the leaf that completes the leaf set (closure in the DAG) of the most estimated
   // compute time, so the GEMMs — most of the step — start early and little is left once the
-  // last leaf lands.  CC_COPY_REORDER=0 keeps plan order.
+  // last leaf lands.  Option copy_reorder = 0 keeps plan order.
   std::vector<int32_t> early_seq;
   std::vector<uint8_t> is_early(size_t(n_ops), 0);
   int32_t n_first = 0;                                 // early copies already enqueued (plan ops 0..n-1)
   {
-    int64_t touched_end = 0;
+    // byte ranges of the pool touched so far in plan order (merged intervals start -> end)
+    std::map<int64_t, int64_t> touched;
     auto touch = [&](int64_t off, int64_t bytes) {
-      if (off >= 0) touched_end = std::max(touched_end, off + bytes);
+      if (off < 0) return;
+      int64_t lo = off, hi = off + bytes;
+      auto it = touched.upper_bound(lo);
+      if (it != touched.begin() && std::prev(it)->second >= lo) --it;
+      while (it != touched.end() && it->first <= hi) {
+        lo = std::min(lo, it->first);
+        hi = std::max(hi, it->second);
+        it = touched.erase(it);
+      }
+      touched[lo] = hi;
+    };
+    auto fresh = [&](int64_t off, int64_t bytes) {
+      auto it = touched.upper_bound(off);
+      if (it != touched.end() && it->first < off + bytes) return false;
+      return it == touched.begin() || std::prev(it)->second <= off;
     };
     for (int32_t i = 0; i < n_ops; ++i) {
       const PhysOp& op = ops[size_t(i)];
       const Node& n = g.nodes[size_t(op.node)];
       const int64_t rb = round_up(n.size, ALIGN);
-      if (op.kind == OP_H2D && op.stream == S_H2D && n.leaf() && op.dev_off >= touched_end) {
+      if (op.kind == OP_H2D && op.stream == S_H2D && n.leaf() && fresh(op.dev_off, rb)) {
         is_early[size_t(i)] = 1;
         early_seq.push_back(i);
       }

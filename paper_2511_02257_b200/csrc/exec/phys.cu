@@ -270,11 +270,25 @@ void prepare_phys(cc_ctx* ctx) {
   for (size_t u = 0; u < g.nodes.size(); ++u)
     if (u < ctx->peer_home.size() && ctx->peer_home[u] && !on_dev[u] && !ctx->leaf_peer[u])
       throw Error(CC_E_STATE, "peer-homed leaf " + std::to_string(g.nodes[u].id) + " has no peer copy (cc_set_leaf_peer)");
-  try {
-    ctx->pp = build_phys(g, ctx->lp, on_dev, phys_limit, ALIGN, RangeAlloc::NEXT_FIT, ctx->peer_tier_bytes);
-  } catch (const Error& e) {
-    if (e.status != CC_E_NOMEM) throw;
-    ctx->pp = build_phys(g, ctx->lp, on_dev, pool, ALIGN, RangeAlloc::BEST_FIT, ctx->peer_tier_bytes);
+  // Unbounded plans first try fixed leaf slots (every leaf copy then lands in memory no earlier
+  // op touched, so all of them stream ahead at full PCIe rate instead of waiting, in plan
+  // order, for intermediates to free their space); a capped plan keeps its footprint.
+  bool placed = false;
+  if (ctx->cap <= 0 && ctx->opt.leaf_slots) {
+    try {
+      ctx->pp = build_phys(g, ctx->lp, on_dev, phys_limit, ALIGN, RangeAlloc::NEXT_FIT, ctx->peer_tier_bytes, true);
+      placed = true;
+    } catch (const Error& e) {
+      if (e.status != CC_E_NOMEM) throw;
+    }
+  }
+  if (!placed) {
+    try {
+      ctx->pp = build_phys(g, ctx->lp, on_dev, phys_limit, ALIGN, RangeAlloc::NEXT_FIT, ctx->peer_tier_bytes);
+    } catch (const Error& e) {
+      if (e.status != CC_E_NOMEM) throw;
+      ctx->pp = build_phys(g, ctx->lp, on_dev, pool, ALIGN, RangeAlloc::BEST_FIT, ctx->peer_tier_bytes);
+    }
   }
   ctx->stats.arena_high_water = ctx->pp.pool_high_water;
   pt.lap("build_phys");

@@ -318,14 +318,37 @@ void RangeTracker::access(int64_t off, int64_t bytes, int stream, int32_t op, st
 static int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>& leaf_on_device,
-                    int64_t pool_bytes, int64_t align, RangeAlloc::Policy policy, int64_t peer_bytes) {
+                    int64_t pool_bytes, int64_t align, RangeAlloc::Policy policy, int64_t peer_bytes, bool leaf_slots) {
   PhysPlan pp;
   const size_t n = g.nodes.size();
+  // fixed leaf slots: assigned in first-load order from offset 0; the intermediates share
+  // [leaf_region, pool) (the top of the pool stays free for the executor's metadata)
+  std::vector<int64_t> slot(n, -1);
+  int64_t leaf_region = 0;
+  if (leaf_slots) {
+    for (const auto& op : lp.ops)
+      if ((op.kind == OP_H2D || op.kind == OP_P2P_IN) && g.nodes[size_t(op.node)].leaf() &&
+          !leaf_on_device[size_t(op.node)] && slot[size_t(op.node)] < 0) {
+        slot[size_t(op.node)] = leaf_region;
+        leaf_region += round_up(g.nodes[size_t(op.node)].size, align);
+      }
+    if (leaf_region > pool_bytes) throw Error(CC_E_NOMEM, "leaf slots exceed the pool");
+  }
   // host pool: sized for the worst case (sum of all D2H'd sizes), placed best-fit
   int64_t host_cap = 0;
   for (const auto& op : lp.ops)
     if (op.kind == OP_D2H) host_cap += round_up(g.nodes[op.node].size, align);
-  RangeAlloc dev(pool_bytes, policy), hostp(host_cap), peerp(peer_bytes);
+  RangeAlloc dev0(pool_bytes - leaf_region, policy), hostp(host_cap), peerp(peer_bytes);
+  // the intermediates' allocator works on [leaf_region, pool)
+  struct Shifted {
+    RangeAlloc& a;
+    int64_t base;
+    int64_t alloc(int64_t b) {
+      const int64_t o = a.alloc(b);
+      return o < 0 ? o : o + base;
+    }
+    void free(int64_t o, int64_t b) { a.free(o - base, b); }
+  } dev{dev0, leaf_region};
   RangeTracker dtr(pool_bytes), htr(std::max<int64_t>(host_cap, 1)), ptr(std::max<int64_t>(peer_bytes, 1));
   std::vector<int64_t> dev_off(n, -1), host_off(n, -1), peer_off(n, -1);
   std::vector<int32_t> ready(n, -1), ready_stream(n, -1), d2h_op(n, -1), p2p_op(n, -1);
@@ -342,7 +365,7 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
     switch (lop.kind) {
       case OP_H2D: {
         if (nd.leaf() && leaf_on_device[x]) break;            // already in HBM: no copy
-        const int64_t off = dev.alloc(rb);
+        const int64_t off = slot[x] >= 0 ? slot[x] : dev.alloc(rb);
         if (off < 0) throw Error(CC_E_NOMEM, "device pool fragmented/too small for node " + std::to_string(nd.id));
         dev_off[x] = off;
         op.stream = S_H2D;
@@ -360,7 +383,7 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
       }
       case OP_P2P_IN: {
         if (nd.leaf() && leaf_on_device[x]) break;            // already in HBM: no copy
-        const int64_t off = dev.alloc(rb);
+        const int64_t off = slot[x] >= 0 ? slot[x] : dev.alloc(rb);
         if (off < 0) throw Error(CC_E_NOMEM, "device pool fragmented/too small for node " + std::to_string(nd.id));
         dev_off[x] = off;
         op.stream = S_H2D;                                      // inbound copies share the H2D stream
@@ -388,7 +411,7 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
         dtr.access(dev_off[x], rb, S_D2H, me, op.deps);
         ptr.access(poff, rb, S_D2H, me, op.deps);
         p2p_op[x] = me;
-        dev.free(dev_off[x], rb);
+        if (slot[x] < 0) dev.free(dev_off[x], rb);   // a leaf slot stays reserved
         dev_off[x] = -1;
         pp.p2p_out_bytes += nd.size;
         break;
@@ -404,14 +427,14 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
         dtr.access(dev_off[x], rb, S_D2H, me, op.deps);
         htr.access(hoff, rb, S_D2H, me, op.deps);
         d2h_op[x] = me;
-        dev.free(dev_off[x], rb);
+        if (slot[x] < 0) dev.free(dev_off[x], rb);   // a leaf slot stays reserved
         dev_off[x] = -1;
         pp.d2h_bytes += nd.size;
         break;
       }
       case OP_DROP: {
         if (dev_off[x] >= 0) {
-          dev.free(dev_off[x], rb);
+          if (slot[x] < 0) dev.free(dev_off[x], rb);   // a leaf slot stays reserved
           dev_off[x] = -1;
         }
         break;
@@ -449,7 +472,7 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
       }
       case OP_FREE: {
         if (dev_off[x] >= 0) {
-          dev.free(dev_off[x], rb);
+          if (slot[x] < 0) dev.free(dev_off[x], rb);   // a leaf slot stays reserved
           dev_off[x] = -1;
         }
         if (host_off[x] >= 0) {
@@ -473,7 +496,7 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
     for (int32_t d : op.deps) pp.ops[size_t(d)].source = true;
     for (int32_t d : op.same_deps) pp.ops[size_t(d)].source = true;
   }
-  pp.pool_high_water = dev.high_water();
+  pp.pool_high_water = leaf_region + dev0.high_water();
   pp.host_pool_bytes = host_cap;
   pp.peer_high_water = peerp.high_water();
   return pp;

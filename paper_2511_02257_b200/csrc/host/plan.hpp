@@ -102,8 +102,12 @@ struct PhysPlan {
 // leaf_on_device[u]: the leaf is a caller device buffer (no copy / no pool space).
 // peer_bytes: size of the peer-tier region P2P_OUT copies are placed in (best fit;
 // CC_E_NOMEM when fragmentation leaves no block).
+// leaf_slots: every host leaf gets a fixed slot at the top of the pool (in first-load order) and
+// the intermediates share the rest, so no leaf copy ever waits for memory to be freed — the copy
+// streams can run ahead at full PCIe rate (useful when the pool holds all leaves next to the
+// plan's intermediates; CC_E_NOMEM otherwise, and the caller falls back).
 PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>& leaf_on_device,
                     int64_t pool_bytes, int64_t align, RangeAlloc::Policy policy = RangeAlloc::BEST_FIT,
-                    int64_t peer_bytes = 0);
+                    int64_t peer_bytes = 0, bool leaf_slots = false);
 
 }  // namespace cc

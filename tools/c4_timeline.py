@@ -17,11 +17,16 @@ import bench  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--cap", type=float, default=32e9)
 ap.add_argument("--lru", action="store_true")
+ap.add_argument("--opt", action="append", default=[], help="executor option k=v (cc_set_options)")
 a = ap.parse_args()
 w = dags.config_c4()
 dev = torch.device("cuda:0")
 streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
 ctx = cc.Context(0, torch.empty(60 << 30, dtype=torch.uint8, device=dev), streams=streams)
+if a.opt:
+    o = ctx.options()
+    o.update({k: type(o[k])(float(v)) for k, v in (x.split("=") for x in a.opt)})
+    ctx.set_options(**o)
 ctx.load_workload(w)
 _, st = ctx.schedule(cc.CC_TREE, cap_bytes=int(a.cap), evict_next_use=not a.lru)
 host, tmp = {}, None
