@@ -385,7 +385,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     constexpr size_t MAX_FUSED = 16;
     // default off: on c2 the fused partner stages come in bursts the 6-stage ring cannot hide
     // (4.89 ms vs 4.64 ms unfused, profiles/r01 notes); kept for larger N and as an option
-    const bool fuse = ctx->opt.trace_fusion != 0;
+    const bool fuse = ctx->opt.trace_fusion != 0 && df_supports_fusion();
     for (int32_t i = 0; fuse && i < n_ops; ++i) {
       const PhysOp& op = ops[size_t(i)];
       if (op.kind != OP_CONTRACT || g.nodes[size_t(op.node)].op != CC_TR_MM) continue;

@@ -37,7 +37,8 @@ using namespace dev;
 #ifndef DF_TSTAGES
 #define DF_TSTAGES 3      // trace ring stages (32 KB: one 32 x 32 complex block pair)
 #endif
-using GC = Cfg<64, 64, 16, 32, 16, DF_GSTAGES>;   // 32 KB stages
+using GC = Cfg<64, 64, 16, 32, 16, DF_GSTAGES>;   // 32 KB stages (BK = 8: 16 KB stages with twice
+                                                   // the barrier traffic measured 4.64-4.74 ms on c2)
 constexpr int CW = GC::NCW * 32;           // 256 consumer threads
 #ifndef DF_NAUX
 #define DF_NAUX 4         // trace warps (a multiple of 4: whole warpgroups, equal per sub-partition)
@@ -45,7 +46,10 @@ constexpr int CW = GC::NCW * 32;           // 256 consumer threads
 constexpr int NT = CW + 32 * DF_NAUX + 128;   // + trace warps + issuer, two schedulers, an idle warp
 constexpr int TB = 32;                     // trace block edge (complex)
 constexpr int INFO = 4;                    // item slots per queue (claimed-ready-running-unpublished)
-static_assert(GC::A_BYTES == TB * TB * 16 && GC::B_BYTES == TB * TB * 16, "a trace block pair fills one stage");
+constexpr int TSTAGE = 2 * TB * TB * 16;   // a trace block pair: A and B 32 x 32 complex (32 KB)
+constexpr int TB_BYTES = TB * TB * 16;     // one operand block of a trace stage
+// fused-trace partner stages (two halves of a 64 x 64 tile) need 32 KB GEMM stages
+constexpr bool DF_FUSION = GC::STAGE_BYTES == TSTAGE;
 
 __device__ __forceinline__ void tma_load_4d_g(void* dst, const void* map, uint64_t* bar, int c0, int c1, int c2,
                                               int c3) {
@@ -201,7 +205,7 @@ __device__ __forceinline__ void gemm_stage_loads(const ItemInfo& inf, int k, uin
 }
 
 __device__ __forceinline__ void trace_stage_loads(const ItemInfo& inf, int k, uint8_t* sA, uint64_t* bar) {
-  uint8_t* sB = sA + GC::A_BYTES;
+  uint8_t* sB = sA + TB_BYTES;
   const int u = inf.u0 + k;
   const int nb2 = inf.nb * inf.nb;
   const int g = u / nb2, rem = u - g * nb2;
@@ -229,8 +233,8 @@ __device__ __forceinline__ void trace_stage_loads(const ItemInfo& inf, int k, ui
 // slower (c2: 4.75 vs 4.64 ms at 6 stages).
 constexpr int GS = GC::STAGES;             // GEMM ring stages
 constexpr int TS = DF_TSTAGES;             // trace ring stages
-constexpr int STAGE = GC::STAGE_BYTES;     // 32 KB
-constexpr int DF_SMEM = (GS + TS) * STAGE + 2 * (GS + TS) * 8 + 1024;
+constexpr int STAGE = GC::STAGE_BYTES;     // GEMM stage (32 KB at BK = 16)
+constexpr int DF_SMEM = GS * STAGE + TS * TSTAGE + 2 * (GS + TS) * 8 + 1024;
 constexpr int DF_STATIC_SMEM =
     int(2 * INFO * sizeof(ItemInfo)) + 4 * INFO * 8 + (GS + TS) * 4 + INFO * DF_NAUX * 16 + 4;
 static_assert(DF_SMEM + DF_STATIC_SMEM <= 232448, "dataflow worker exceeds 227 KB of shared memory");
@@ -274,7 +278,7 @@ __global__ void __launch_bounds__(NT, 1) df_worker(DfArgs a) {
   // the compiler keeps the shared address space (LDS, not generic LD)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* tsmem = smem + GS * STAGE;        // trace ring
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (GS + TS) * STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GS * STAGE + TS * TSTAGE);
   uint64_t* empty = full + GS;
   uint64_t* full_t = empty + GS;
   uint64_t* empty_t = full_t + TS;
@@ -352,8 +356,8 @@ __global__ void __launch_bounds__(NT, 1) df_worker(DfArgs a) {
         const ItemInfo& inf = s_info[x][slot_of[x]];
         const int k = k_of[x];
         *desc = (uint32_t(slot_of[x]) << 2) | (k == 0 ? SD_FIRST : 0u) | (k == np_of[x] - 1 ? SD_LAST : 0u);
-        mbar_expect_tx(fb, STAGE);
-        if (x) trace_stage_loads(inf, k, tsmem + st * STAGE, fb);
+        mbar_expect_tx(fb, x ? TSTAGE : STAGE);
+        if (x) trace_stage_loads(inf, k, tsmem + st * TSTAGE, fb);
         else gemm_stage_loads(inf, k, smem + st * STAGE, fb, a.tmaps);
         if (++k_of[x] == np_of[x]) have[x] = false;
       }
@@ -507,8 +511,8 @@ __global__ void __launch_bounds__(NT, 1) df_worker(DfArgs a) {
         for (int q = 0; q < RG; ++q) accp[q][0] = accp[q][1] = accp[q][2] = accp[q][3] = 0.0;
         if (ax == 0 && lane == 0 && PROF) s_info[1][int((d >> 2) & 7u)].t_first = gtimer();
       }
-      const uint8_t* sA = tsmem + st * STAGE;
-      const uint8_t* sB = sA + C::A_BYTES;
+      const uint8_t* sA = tsmem + st * TSTAGE;
+      const uint8_t* sB = sA + TB_BYTES;
       const int c = lane;
 #pragma unroll
       for (int qq = 0; qq < TB / NAUX; ++qq) {
@@ -769,6 +773,8 @@ void df_gemm_tile_dims(int* BM, int* BN, int* BK, int* slot_doubles) {
 }
 
 int df_trace_block() { return TB; }
+
+bool df_supports_fusion() { return DF_FUSION; }
 
 cudaError_t df_launch(const DfArgs& a, int grid, cudaStream_t s) {
   if (a.prof) df_worker<true><<<grid, NT, DF_SMEM, s>>>(a);

@@ -94,6 +94,8 @@ cudaError_t df_launch(const DfArgs& a, int grid, cudaStream_t s);
 // Tile / chunk geometry the builder needs (matches the worker's Cfg).
 void df_gemm_tile_dims(int* BM, int* BN, int* BK, int* slot_doubles);
 int df_trace_block();
+// fused traces need GEMM stages that hold a half partner tile (32 KB)
+bool df_supports_fusion();
 // Encode the TMA maps of one GEMM problem into dst[0] (A) and dst[1] (B).
 bool df_encode_maps(void* dst, const void* A, const void* B, int64_t M, int64_t Nn, int64_t Kin, int64_t Ko,
                     int64_t batch, int64_t lda, int64_t sAo, int64_t sAb, int64_t ldb, int64_t sBo, int64_t sBb);
