@@ -2,11 +2,17 @@
 work).  TEST INFRASTRUCTURE (see oracle/__init__.py).
 
 TIME: part p of n owns time slices [p*Lt//n, (p+1)*Lt//n) — every op is per-slice.
-TREES: trees in tree-scheduler selection order (O4); tree weight = flops/8 of the
-contractions first executed while processing it (MM1 Lt N^3, BM1/BB2 Lt S N^4, TR Lt N^2,
-BB1/BT2 Lt S N^5, BB3 Lt S N^3;
-abstract DAGs: 1 per contraction); tree i with prefix weight P_i, weight w_i, total W goes
-to part min(n-1, floor(n (2 P_i + w_i) / (2 W))).
+TREES (reading M-1, round 2): trees in tree-scheduler selection order (O4), cut into n
+contiguous chunks; a chunk's work is what its part executes: flops/8 of the distinct
+contractions in the union of its trees' closures, shared nodes replicated (MM1 Lt N^3,
+BM1/BB2 Lt S N^4, TR Lt N^2, BB1/BT2 Lt S N^5, BB3 Lt S N^3; abstract DAGs: 1 per
+contraction).  The cut minimises the largest chunk's work: T* = the smallest T for which the
+first-fit cut (extend the current chunk while its work stays <= T) needs at most n chunks
+(exact for min-max contiguous partitions: chunk work only grows when a chunk is extended);
+the parts are that first-fit cut at T*; while there are fewer than n chunks, the chunk of
+largest work with at least two trees (lowest index on ties) is split in half by tree count.
+(Round 1 balanced first-execution work, which ignores the replicas: on c4 at 8 parts the
+largest part executed 1.59x the mean.)
 GRID (reading M-2): n_tree x n_time parts; part p is TREES part p // n_time restricted to
 TIME slices of part p % n_time (every op is per-slice, so the two splits compose).
 Replication (SURVEY §8(d) "replicas ... counted as overhead and reported", reading M-3): the
@@ -51,20 +57,60 @@ def _owners(dag):
     return order, sel, owner
 
 
-def tree_parts(dag, n_parts):
-    """{tree_id: part} for a TREES split."""
-    order, sel, owner = _owners(dag)
-    w = {t: 0 for t in sel}
-    for u in order:
-        w[owner[u]] += _weight(dag, u)
-    W = sum(w.values())
-    parts = {}
-    P = 0
+def _closure_contractions(dag, t):
+    return [u for u in dag.trees[t][1] if dag.nodes[u].child]
+
+
+def chunk_work(dag, trees):
+    """Work (flops/8) of the distinct contractions in the union of the trees' closures."""
+    seen = set()
+    for t in trees:
+        seen.update(_closure_contractions(dag, t))
+    return sum(_weight(dag, u) for u in seen)
+
+
+def _first_fit(dag, sel, T):
+    """Chunks of the first-fit cut at work bound T, or None if one tree alone exceeds T."""
+    out, cur, seen, w = [], [], set(), 0
     for t in sel:
-        p = (n_parts * (2 * P + w[t])) // (2 * W) if W > 0 else 0
-        parts[t] = min(n_parts - 1, p)
-        P += w[t]
-    return parts
+        mem = _closure_contractions(dag, t)
+        add = sum(_weight(dag, u) for u in mem if u not in seen)
+        if cur and w + add > T:
+            out.append(cur)
+            cur, seen, w = [], set(), 0
+            add = sum(_weight(dag, u) for u in mem)
+        if add > T:
+            return None
+        cur.append(t)
+        seen.update(mem)
+        w += add
+    if cur:
+        out.append(cur)
+    return out
+
+
+def tree_parts(dag, n_parts):
+    """{tree_id: part} for a TREES split (reading M-1, module docstring)."""
+    _, sel, _ = _owners(dag)
+    lo = max([chunk_work(dag, [t]) for t in sel] + [0])
+    hi = chunk_work(dag, sel)
+    while lo < hi:                                  # smallest T with <= n first-fit chunks
+        mid = (lo + hi) // 2
+        c = _first_fit(dag, sel, mid)
+        if c is not None and len(c) <= n_parts:
+            hi = mid
+        else:
+            lo = mid + 1
+    chunks = _first_fit(dag, sel, lo) if sel else []
+    while len(chunks) < n_parts:
+        cand = [(chunk_work(dag, c), -k) for k, c in enumerate(chunks) if len(c) >= 2]
+        if not cand:
+            break
+        k = -max(cand)[1]
+        c = chunks[k]
+        h = len(c) // 2
+        chunks[k:k + 1] = [c[:h], c[h:]]
+    return {t: p for p, c in enumerate(chunks) for t in c}
 
 
 def sub_workload(w, keep_trees):

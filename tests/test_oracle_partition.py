@@ -1,8 +1,9 @@
-"""Pins of oracle/partition.py (reading M-1; partitioning is future work
-in the paper) against hand-derived parts and properties the rule must satisfy:
-contiguity in tree-scheduler selection order, first-execution weights computed as set
-differences of tree closures, total weight = the DAG's contraction weight, and balance
-|W_p - W/n| <= max_t w_t (midpoint rule)."""
+"""Pins of oracle/partition.py (readings M-1..M-3; partitioning is future
+work in the paper) against hand-derived parts (D*) and properties the rule must satisfy:
+contiguity in tree-scheduler selection order, non-empty parts, and a largest part work
+(replicas included) equal to the brute-force minimum over all contiguous cuts."""
+import itertools
+
 import pytest
 
 from synth import dags
@@ -18,14 +19,17 @@ def _selection(dag):
 
 def test_dstar_hand_parts():
     """D* (Table I DAG, unit weights: abstract contractions weigh 1).  The tree scheduler selects
-    T0 (f), T1 (g), T2 (h) (SURVEY §8(c) O4 hand trace); first-execution weights: T0 {f} = 1,
-    T1 {e, g} = 2, T2 {h} = 1, W = 4.  Midpoints 0.5, 2, 3.5 -> n = 2: floor(2 mid / 4) = 0, 1, 1;
-    n = 3: floor(3 mid / 4) = 0, 1, 2."""
+    T0 (f), T1 (g), T2 (h) (SURVEY §8(c) O4 hand trace).  Closure contractions: T0 {f},
+    T1 {e, g}, T2 {e, h}.  n = 2: bound 2 cuts [T0] | [T1] | [T2] (T0 + T1 would be 3) — three
+    chunks; bound 3: [T0, T1] (work 3) | [T2] (T2 adds h only while e is in the chunk, but
+    4 > 3 cuts it; alone it weighs 2) — two chunks, so T* = 3 and the parts are {0, 0, 1}.
+    n = 3: bound 2 gives the three singletons.  n = 1: one chunk."""
     dag = Dag(dags.fixture_dstar())
     assert _selection(dag) == [0, 1, 2]
-    assert partition.tree_parts(dag, 2) == {0: 0, 1: 1, 2: 1}
+    assert partition.tree_parts(dag, 2) == {0: 0, 1: 0, 2: 1}
     assert partition.tree_parts(dag, 3) == {0: 0, 1: 1, 2: 2}
     assert partition.tree_parts(dag, 1) == {0: 0, 1: 0, 2: 0}
+    assert partition.chunk_work(dag, [0, 1]) == 3 and partition.chunk_work(dag, [1, 2]) == 3
 
 
 def _weight(w, op):
@@ -34,50 +38,49 @@ def _weight(w, op):
             dags.TR_MM: w.Lt * w.N ** 2, dags.OP_X: 1}[op]
 
 
-@pytest.mark.parametrize("seed", range(30))
-@pytest.mark.parametrize("n", [2, 3, 5])
-def test_partition_properties(seed, n):
+def _work(dag, ops, w, trees):
+    """Independent restatement: distinct contractions of the trees' closures, weighted."""
+    nodes = set()
+    for t in trees:
+        nodes |= {u for u in dag.trees[t][1] if dag.nodes[u].child}
+    return sum(_weight(w, ops[u]) for u in nodes)
+
+
+@pytest.mark.parametrize("seed", range(25))
+@pytest.mark.parametrize("n", [2, 3])
+def test_partition_min_max_by_brute_force(seed, n):
+    """The parts are contiguous in the selection order, all non-empty, and their largest work
+    (replicas included) equals the brute-force minimum over every cut of the selection order
+    into n non-empty contiguous chunks."""
     typed = seed % 3 != 0
-    w = dags.random_dag(seed, n_leaves=6, n_trees=9, max_ops_per_tree=4, share_p=0.6, typed=typed, N=3, Lt=2)
+    w = dags.random_dag(seed, n_leaves=6, n_trees=7, max_ops_per_tree=4, share_p=0.6, typed=typed, N=3, Lt=2)
     dag = Dag(w)
     ops = {x[0]: x[1] for x in w.nodes}
     sel = _selection(dag)
     parts = partition.tree_parts(dag, n)
-    # contiguous and non-decreasing along the selection order, every tree assigned
     seq = [parts[t] for t in sel]
     assert sorted(parts) == sorted(dag.tree_ids)
-    assert seq == sorted(seq) and all(0 <= p < n for p in seq)
-    # first-execution weights as set differences of closures (members of a tree not in any
-    # earlier-selected tree's closure, contractions only)
-    seen, wt = set(), {}
-    for t in sel:
-        members = set(dag.trees[t][1])
-        new = [u for u in members - seen if dag.nodes[u].child]
-        wt[t] = sum(_weight(w, ops[u]) for u in new)
-        seen |= members
-    W = sum(wt.values())
-    assert W == sum(_weight(w, ops[u]) for u, nd in dag.nodes.items() if nd.child)
-    wmax = max(wt.values())
-    for p in range(n):
-        Wp = sum(wt[t] for t in sel if parts[t] == p)
-        assert abs(n * Wp - W) <= n * wmax, (p, Wp, W, wmax)
-    # the assignment is the midpoint rule on these weights
-    P = 0
-    for t in sel:
-        assert parts[t] == min(n - 1, (n * (2 * P + wt[t])) // (2 * W))
-        P += wt[t]
+    assert seq == sorted(seq) and set(seq) == set(range(min(n, len(sel))))
+    got = max(_work(dag, ops, w, [t for t in sel if parts[t] == p]) for p in set(seq))
+    best = None
+    for cuts in itertools.combinations(range(1, len(sel)), min(n, len(sel)) - 1):
+        bounds = [0, *cuts, len(sel)]
+        m = max(_work(dag, ops, w, sel[bounds[k]:bounds[k + 1]]) for k in range(len(bounds) - 1))
+        best = m if best is None else min(best, m)
+    assert got == best
 
 
 def test_dstar_part_stats_and_owners():
-    """D*, n = 2: part 0 = T0 = {f, a, b}, part 1 = T1 u T2 = {g, e, h, a, b, c, d} (unit sizes,
-    unit contraction weights).  Owners = part of the first selected tree containing the node:
-    a, b -> T0 (part 0); c, e, g -> T1; d, h -> T2 (part 1).  Part 1 replicates leaves a, b."""
+    """D*, n = 2: part 0 = T0 u T1 = {f, g, e, a, b, c}, part 1 = T2 = {h, e, d, b, c} (unit
+    sizes, unit contraction weights).  Owners = part of the first selected tree containing the
+    node: a, b, f -> T0, c, e, g -> T1 (part 0); d, h -> T2 (part 1).  Part 1 replicates the
+    contraction e and the leaves b, c."""
     w = dags.fixture_dstar()
-    assert partition.part_stats(w, 2, 0) == dict(n_trees=1, n_contr=1, work=1, replicated_work=0, leaf_bytes=2,
+    assert partition.part_stats(w, 2, 0) == dict(n_trees=2, n_contr=3, work=3, replicated_work=0, leaf_bytes=3,
                                                  replicated_leaf_bytes=0)
-    assert partition.part_stats(w, 2, 1) == dict(n_trees=2, n_contr=3, work=3, replicated_work=0, leaf_bytes=4,
+    assert partition.part_stats(w, 2, 1) == dict(n_trees=1, n_contr=2, work=2, replicated_work=1, leaf_bytes=3,
                                                  replicated_leaf_bytes=2)
-    assert partition.leaf_owners(w, 2) == {0: 0, 1: 0, 2: 1, 3: 1}
+    assert partition.leaf_owners(w, 2) == {0: 0, 1: 0, 2: 0, 3: 1}
 
 
 @pytest.mark.parametrize("seed", range(20))
