@@ -475,6 +475,9 @@ def main():
                          "kernel": "df_worker (one persistent dataflow launch per step: every MM1 tile and "
                                    "TR_MM block pair of the plan; FP64 DMMA + DFMA)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "frac_note": "achieved counts the algorithmic 8 flops per complex MAC; the GEMMs execute the "
+                                      "3M form (6), so frac can exceed 1 — the FP64 pipe's executed fraction is "
+                                      "fp64_pipe.frac",
                          "traffic": ncu_traffic(), "peak_source": peak_src,
                          "algorithmic": {"flops_per_launch": step_flops, "hbm_bytes_per_launch": step_hbm},
                          "launch_ms": worker_t * 1e3,
