@@ -434,3 +434,26 @@ def test_slice_major_baryon_chains_bitwise():
             for t in a:
                 assert np.array_equal(a[t], b[t]), (w.name, flags, t)
             assert_roots_close(a, r_or)
+
+
+def test_leaf_slots_placement_and_fallback():
+    """Leaf slots (option leaf_slots): values bit-identical with and without, on the dataflow and
+    op-by-op executors; a pool too small to hold every leaf next to the intermediates falls back
+    to the shared placement (still exact)."""
+    w = dags.config_c2(N=40, Lt=3, n_loop4=40, n_loop2=4, n_corr=3)
+    dag = Dag(w)
+    r_or = values.evaluate(dag, lambda u: values.synthetic_leaf(w, u, dag.nodes[u].op))
+    for flags in (0, 16):
+        a = run_gpu(w, flags=flags, options={"leaf_slots": 1})[1]
+        b = run_gpu(w, flags=flags, options={"leaf_slots": 0})[1]
+        for t in a:
+            assert np.array_equal(a[t], b[t]), (flags, t)
+        assert_roots_close(a, r_or)
+    # an arena that holds the plan's peak but not every leaf slot next to it
+    leaf_bytes = sum(dag.nodes[u].size for u, n in dag.nodes.items() if not n.child)
+    from paper_2511_02257_b200 import cc
+    scratch = cc.cc_scratch_bytes(w.Lt, w.N, w.S)
+    peak = lru.plan(dag, tree.schedule(dag))["transient_peak"]
+    arena_mb = max(1, int((scratch + peak + leaf_bytes // 2) * 1.05) >> 20) + 1
+    ctx, roots, _, _, _ = run_gpu(w, arena_mb=arena_mb, options={"leaf_slots": 1})
+    assert_roots_close(roots, r_or)
