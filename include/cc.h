@@ -130,11 +130,16 @@ typedef struct {
   double hbm_bytes;           /* algorithmic HBM bytes of the kernels                       */
   int64_t h2d_bytes, d2h_bytes; /* bytes copied, counted as the executor enqueues each copy (a
                                    dropped or duplicated copy shows here; the plan's own counts
-                                   are cc_plan_stats; device-resident leaves: 0)           */
+                                   are cc_plan_stats; device-resident leaves: 0).  Includes the
+                                   up to 4 early leaf copies a first dataflow execute starts
+                                   before its physical plan exists, when that plan then places
+                                   them elsewhere or runs op by op (compaction)            */
   int64_t n_kernels;          /* kernel launches issued by this execute                     */
   double copy_seconds;        /* start -> last H2D/D2H copy done (blocking stream-mode
                                  dataflow execute with copies; else 0)                     */
   int64_t p2p_in_bytes, p2p_out_bytes; /* peer-tier copies, counted as enqueued             */
+  int64_t move_bytes;         /* compaction device-to-device moves (physical plan), enqueued  */
+  int64_t pad_;
 } cc_exec_stats;
 
 /* One op of the physical plan (cc_plan_ops). kind: 0 H2D, 1 D2H (evict with copy),
@@ -210,6 +215,22 @@ cc_status cc_memory_trace(cc_ctx* ctx, int64_t* m_out, int64_t* transient_out, i
 cc_status cc_plan_ops(cc_ctx* ctx, cc_plan_op* out, int64_t cap, int64_t* n_out);
 /* Tree order of the last CC_TREE (selection order) or CC_RSGS (similarity chain) schedule (tree ids). */
 cc_status cc_tree_order(cc_ctx* ctx, int64_t* out, int64_t cap, int64_t* n_out);
+/* Host-side placement query (no device needed): the physical plan of the current schedule over a
+ * pool of pool_bytes.  flags bit 0: an allocation that finds no free block clears a window by
+ * device-to-device moves of small resident tensors (what cc_execute falls back to when next fit
+ * and best fit both fail; such plans execute op by op); bit 1: next fit instead of best fit.
+ * CC_E_NOMEM if it does not fit. */
+typedef struct { int64_t pool_high_water, n_moves, move_bytes, host_pool_bytes; } cc_phys_stats;
+cc_status cc_phys_plan(cc_ctx* ctx, int64_t pool_bytes, int32_t flags, cc_phys_stats* out);
+/* The ops of the last cc_phys_plan, compaction moves inline before the op that needs them:
+ * kind as cc_plan_op, 7 = MOVE (offset = source, dst = destination); offset = the op's pool
+ * offset (copy target / output), off_a / off_b = a contraction's operand offsets (-1 for a
+ * caller device leaf or when not a contraction). */
+typedef struct { int32_t kind; int32_t pad_; int64_t node; int64_t bytes; int64_t offset, dst, off_a, off_b; } cc_phys_op;
+cc_status cc_phys_ops(cc_ctx* ctx, cc_phys_op* out, int64_t cap, int64_t* n_out);
+/* Exact bytes cc_execute reserves at the top of the arena for kernel workspace and tables with
+ * the current DAG and options (the pool is the rest, rounded down to 1 KiB). */
+cc_status cc_scratch_of(cc_ctx* ctx, int64_t* out);
 /* Per-step op queue as CSV (step, op, node, bytes, offset, device_used). */
 cc_status cc_plan_dump(cc_ctx* ctx, const char* csv_path);
 

@@ -69,7 +69,7 @@ class cc_plan_stats(ctypes.Structure):
 class cc_exec_stats(ctypes.Structure):
     _fields_ = [("seconds", c_dbl), ("kernel_seconds", c_dbl), ("flops", c_dbl), ("hbm_bytes", c_dbl),
                 ("h2d_bytes", c_i64), ("d2h_bytes", c_i64), ("n_kernels", c_i64), ("copy_seconds", c_dbl),
-                ("p2p_in_bytes", c_i64), ("p2p_out_bytes", c_i64)]
+                ("p2p_in_bytes", c_i64), ("p2p_out_bytes", c_i64), ("move_bytes", c_i64), ("pad_", c_i64)]
 
 
 class cc_plan_op(ctypes.Structure):
@@ -86,6 +86,15 @@ class cc_options(ctypes.Structure):
 class cc_part_stats(ctypes.Structure):
     _fields_ = [(n, c_i64) for n in ("n_trees", "n_contr", "work", "replicated_work", "leaf_bytes",
                                      "replicated_leaf_bytes")]
+
+
+class cc_phys_stats(ctypes.Structure):
+    _fields_ = [(n, c_i64) for n in ("pool_high_water", "n_moves", "move_bytes", "host_pool_bytes")]
+
+
+class cc_phys_op(ctypes.Structure):
+    _fields_ = [("kind", c_i32), ("pad_", c_i32), ("node", c_i64), ("bytes", c_i64), ("offset", c_i64),
+                ("dst", c_i64), ("off_a", c_i64), ("off_b", c_i64)]
 
 
 class cc_dag_stats(ctypes.Structure):
@@ -117,6 +126,9 @@ _sig("cc_leaf_owners", c_void_p, P(c_i64), P(c_i32), c_i64, P(c_i64))
 _sig("cc_schedule", c_void_p, P(cc_sched_cfg), P(c_i64), c_i64, P(c_i64), P(cc_plan_stats))
 _sig("cc_memory_trace", c_void_p, P(c_i64), P(c_i64), c_i64, P(c_i64))
 _sig("cc_plan_ops", c_void_p, P(cc_plan_op), c_i64, P(c_i64))
+_sig("cc_phys_plan", c_void_p, c_i64, c_i32, P(cc_phys_stats))
+_sig("cc_phys_ops", c_void_p, P(cc_phys_op), c_i64, P(c_i64))
+_sig("cc_scratch_of", c_void_p, P(c_i64))
 _sig("cc_tree_order", c_void_p, P(c_i64), c_i64, P(c_i64))
 _sig("cc_plan_dump", c_void_p, ctypes.c_char_p)
 _sig("cc_set_leaf", c_void_p, c_i64, c_void_p, c_size_t)
@@ -152,7 +164,7 @@ _sig("cc_fill_synthetic", c_void_p, c_void_p, c_i64, c_u64, c_i64, c_i64, c_i32,
 _sig("cc_scratch_bytes", c_i32, c_i32, c_i32, res=c_size_t)
 
 EXPORTED = ["cc_create", "cc_destroy", "cc_last_error", "cc_version", "cc_load_dag", "cc_load_dag_file",
-            "cc_dag_info", "cc_part_time_range", "cc_correlators", "cc_partition", "cc_part_trees", "cc_partition_grid", "cc_part_info", "cc_leaf_owners", "cc_schedule", "cc_memory_trace", "cc_plan_ops",
+            "cc_dag_info", "cc_part_time_range", "cc_correlators", "cc_partition", "cc_part_trees", "cc_partition_grid", "cc_part_info", "cc_leaf_owners", "cc_schedule", "cc_memory_trace", "cc_plan_ops", "cc_phys_plan", "cc_phys_ops", "cc_scratch_of",
             "cc_tree_order", "cc_plan_dump", "cc_set_leaf", "cc_set_leaf_device", "cc_set_leaf_peer", "cc_set_peer_tier", "cc_ipc_export", "cc_ipc_open", "cc_ipc_close", "cc_execute",
             "cc_execute_async", "cc_get_options", "cc_set_options", "cc_kernel_times", "cc_dataflow_state", "cc_dataflow_profile", "cc_correlator", "cc_root_value", "cc_correlator_device_ptr",
             "cc_mm1", "cc_bm1", "cc_bb2", "cc_tr_mm", "cc_bb1", "cc_bt2", "cc_bb3", "cc_mm1_ozaki", "cc_mm1_ozaki_workspace_bytes", "cc_i8gemm_tn", "cc_gemm_ozaki",
@@ -355,6 +367,26 @@ class Context:
         self._ck(_lib.cc_plan_ops(self._h, out, n.value, ctypes.byref(n)))
         return [(OP_KINDS[o.kind], o.node, o.bytes, o.offset) for o in out[:n.value]]
 
+    def phys_plan(self, pool_bytes, compact=False, next_fit=False):
+        """Host-side placement of the current plan (cc_phys_plan): stats dict."""
+        st = cc_phys_stats()
+        self._ck(_lib.cc_phys_plan(self._h, int(pool_bytes), (1 if compact else 0) | (2 if next_fit else 0),
+                                   ctypes.byref(st)))
+        return {f: getattr(st, f) for f, _ in cc_phys_stats._fields_}
+
+    def scratch_of(self):
+        n = c_i64()
+        self._ck(_lib.cc_scratch_of(self._h, ctypes.byref(n)))
+        return int(n.value)
+
+    def phys_ops(self):
+        """[(kind, node, bytes, offset, dst, off_a, off_b)] of the last phys_plan (kind 7: MOVE)."""
+        n = c_i64()
+        self._ck(_lib.cc_phys_ops(self._h, None, 0, ctypes.byref(n)))
+        out = (cc_phys_op * max(n.value, 1))()
+        self._ck(_lib.cc_phys_ops(self._h, out, n.value, ctypes.byref(n)))
+        return [(o.kind, o.node, o.bytes, o.offset, o.dst, o.off_a, o.off_b) for o in out[:n.value]]
+
     def tree_order(self):
         n = c_i64()
         self._ck(_lib.cc_tree_order(self._h, None, 0, ctypes.byref(n)))
@@ -402,7 +434,7 @@ class Context:
     def execute(self, flags=0):
         s = cc_exec_stats()
         self._ck(_lib.cc_execute(self._h, flags, ctypes.byref(s)))
-        return {f: getattr(s, f) for f, _ in cc_exec_stats._fields_}
+        return {f: getattr(s, f) for f, _ in cc_exec_stats._fields_ if f != "pad_"}
 
     def execute_async(self, flags=0):
         self._ck(_lib.cc_execute_async(self._h, flags))

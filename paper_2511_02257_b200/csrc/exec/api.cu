@@ -340,6 +340,56 @@ cc_status cc_memory_trace(cc_ctx* ctx, int64_t* m_out, int64_t* transient_out, i
   API_END
 }
 
+cc_status cc_phys_plan(cc_ctx* ctx, int64_t pool_bytes, int32_t compact, cc_phys_stats* out) {  // compact = flags
+  if (!ctx || pool_bytes <= 0) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->scheduled) throw Error(CC_E_STATE, "no schedule");
+  const Dag& g = *ctx->dag;
+  std::vector<uint8_t> on_dev(g.nodes.size(), 0);
+  for (size_t u = 0; u < g.nodes.size() && u < ctx->leaf_dev.size(); ++u) on_dev[u] = ctx->leaf_dev[u] != nullptr;
+  PhysPlan pp = build_phys(g, ctx->lp, on_dev, pool_bytes, ALIGN, (compact & 2) ? RangeAlloc::NEXT_FIT : RangeAlloc::BEST_FIT,
+                           ctx->peer_tier_bytes, false, (compact & 1) != 0);
+  if (out) {
+    *out = cc_phys_stats{};
+    out->pool_high_water = pp.pool_high_water;
+    out->n_moves = pp.n_moves;
+    out->move_bytes = pp.move_bytes;
+    out->host_pool_bytes = pp.host_pool_bytes;
+  }
+  ctx->phys_probe = std::move(pp);
+  API_END
+}
+
+cc_status cc_scratch_of(cc_ctx* ctx, int64_t* out) {
+  if (!ctx || !out) return CC_E_INVAL;
+  API_BEGIN
+  if (!ctx->scheduled) throw Error(CC_E_STATE, "no schedule");
+  *out = scratch_sizes(ctx).total;
+  API_END
+}
+
+cc_status cc_phys_ops(cc_ctx* ctx, cc_phys_op* out, int64_t cap, int64_t* n_out) {
+  if (!ctx) return CC_E_INVAL;
+  API_BEGIN
+  const auto& ops = ctx->phys_probe.ops;
+  const Dag& g = *ctx->dag;
+  int64_t n = 0;
+  for (const auto& op : ops) n += 1 + int64_t(op.pre_moves.size());
+  if (n_out) *n_out = n;
+  if (out) {
+    if (cap < n) throw Error(CC_E_BUFFER_TOO_SMALL, "buffer too small");
+    int64_t k = 0;
+    for (const auto& op : ops) {
+      for (const auto& m : op.pre_moves)
+        out[k++] = cc_phys_op{7, 0, g.nodes[size_t(m.node)].id, m.bytes, m.src, m.dst, -1, -1};
+      const Node& nd = g.nodes[size_t(op.node)];
+      out[k++] = cc_phys_op{op.kind, 0, nd.id, op.bytes, op.dev_off, -1, op.kind == OP_CONTRACT ? op.off_a : -1,
+                            op.kind == OP_CONTRACT ? op.off_b : -1};
+    }
+  }
+  API_END
+}
+
 cc_status cc_plan_ops(cc_ctx* ctx, cc_plan_op* out, int64_t cap, int64_t* n_out) {
   if (!ctx) return CC_E_INVAL;
   API_BEGIN

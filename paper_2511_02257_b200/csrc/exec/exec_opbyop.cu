@@ -125,6 +125,10 @@ int issue(cc_ctx* ctx, bool time_kernels, std::vector<std::pair<cudaEvent_t, cud
     flush_tr();
     cudaStream_t s = st[op.stream];
     for (int32_t d : op.deps) ck(cudaStreamWaitEvent(s, ctx->events[size_t(d)], 0), "wait");
+    for (const Move& m : op.pre_moves) {      // compaction (physical plan): non-overlapping D2D moves
+      ck(cudaMemcpyAsync(ctx->arena + m.dst, ctx->arena + m.src, size_t(m.bytes), cudaMemcpyDeviceToDevice, s), "move");
+      ctx->run_moves += m.bytes;
+    }
     const Node& n = g.nodes[size_t(op.node)];
     switch (op.kind) {
       case OP_H2D: {

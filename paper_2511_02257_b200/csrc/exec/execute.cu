@@ -20,7 +20,7 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   // land in scratch or outside the arena; if preparation fails, the compute stream is ordered
   // after the stray copies before the error returns.
   ctx->pre_n = 0;
-  ctx->run_h2d = ctx->run_d2h = ctx->run_p2p_in = ctx->run_p2p_out = 0;
+  ctx->run_h2d = ctx->run_d2h = ctx->run_p2p_in = ctx->run_p2p_out = ctx->run_moves = 0;
   std::vector<int64_t> pre_off;
   if (ctx->opt.precopy && ctx->opt.early_copies && ctx->opt.h2d_chunk_bytes == 0 && !ctx->phys_valid &&
       !ctx->dag->abstract && !(flags & (2 | 4 | 8 | 16 | 64 | 128))) {
@@ -91,7 +91,8 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
     return;
   }
   const bool use_graph = (flags & 1) != 0;
-  const bool legacy = (flags & 16) != 0 || (flags & 2) != 0 || (flags & 64) != 0;
+  // a plan with compaction moves runs op by op (the moves are copies on the allocating op's stream)
+  const bool legacy = (flags & 16) != 0 || (flags & 2) != 0 || (flags & 64) != 0 || ctx->pp.n_moves > 0;
   const bool time_kernels = (flags & 2) != 0 && !use_graph;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;
   std::vector<int> kev_kind;
@@ -147,11 +148,13 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
       ctx->graph_d2h = ctx->run_d2h;
       ctx->graph_p2p_in = ctx->run_p2p_in;
       ctx->graph_p2p_out = ctx->run_p2p_out;
+      ctx->graph_moves = ctx->run_moves;
     } else {
       ctx->run_h2d = ctx->graph_h2d;
       ctx->run_d2h = ctx->graph_d2h;
       ctx->run_p2p_in = ctx->graph_p2p_in;
       ctx->run_p2p_out = ctx->graph_p2p_out;
+      ctx->run_moves = ctx->graph_moves;
     }
     ck(cudaGraphLaunch(ctx->gexec, ctx->cs), "graph launch");
   } else {
@@ -186,6 +189,7 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
     stats->d2h_bytes = ctx->run_d2h;
     stats->p2p_in_bytes = ctx->run_p2p_in;
     stats->p2p_out_bytes = ctx->run_p2p_out;
+    stats->move_bytes = ctx->run_moves;
     stats->n_kernels = ctx->last_n_kernels;
   }
   ctx->ktimes = KindTimes{};

@@ -129,6 +129,7 @@ struct cc_ctx {
 
   // physical state
   bool phys_valid = false;
+  PhysPlan phys_probe;                  // cc_phys_plan (host-side placement query)
   PhysPlan pp;
   int64_t pool_bytes = 0;
   char* scratch = nullptr;
@@ -157,8 +158,8 @@ struct cc_ctx {
   int64_t last_n_kernels = 0;
   // plan copies counted as they are enqueued (cc_exec_stats h2d/d2h: runtime counts, not the
   // plan's): the current execute's, and those baked into each cached graph
-  int64_t run_h2d = 0, run_d2h = 0, run_p2p_in = 0, run_p2p_out = 0;
-  int64_t graph_h2d = 0, graph_d2h = 0, graph_p2p_in = 0, graph_p2p_out = 0;   // gexec (op-by-op graph)
+  int64_t run_h2d = 0, run_d2h = 0, run_p2p_in = 0, run_p2p_out = 0, run_moves = 0;
+  int64_t graph_h2d = 0, graph_d2h = 0, graph_p2p_in = 0, graph_p2p_out = 0, graph_moves = 0;   // gexec (op-by-op graph)
   void count_copy(bool h2d, int64_t bytes) { (h2d ? run_h2d : run_d2h) += bytes; }
   // a plan copy of kind OP_H2D / OP_D2H / OP_P2P_IN / OP_P2P_OUT, counted as enqueued
   void count_op_copy(int32_t kind, int64_t bytes) {

@@ -287,7 +287,13 @@ void prepare_phys(cc_ctx* ctx) {
       ctx->pp = build_phys(g, ctx->lp, on_dev, phys_limit, ALIGN, RangeAlloc::NEXT_FIT, ctx->peer_tier_bytes);
     } catch (const Error& e) {
       if (e.status != CC_E_NOMEM) throw;
-      ctx->pp = build_phys(g, ctx->lp, on_dev, pool, ALIGN, RangeAlloc::BEST_FIT, ctx->peer_tier_bytes);
+      try {
+        ctx->pp = build_phys(g, ctx->lp, on_dev, pool, ALIGN, RangeAlloc::BEST_FIT, ctx->peer_tier_bytes);
+      } catch (const Error& e2) {
+        if (e2.status != CC_E_NOMEM) throw;
+        // fragmentation: compact with device-to-device moves (op-by-op executor)
+        ctx->pp = build_phys(g, ctx->lp, on_dev, pool, ALIGN, RangeAlloc::BEST_FIT, ctx->peer_tier_bytes, false, true);
+      }
     }
   }
   ctx->stats.arena_high_water = ctx->pp.pool_high_water;

@@ -269,6 +269,32 @@ int64_t RangeAlloc::alloc(int64_t bytes) {
   return take(it->second, it->first, bytes);
 }
 
+bool RangeAlloc::take_range(int64_t off, int64_t bytes) {
+  auto it = by_off_.upper_bound(off);
+  if (it == by_off_.begin()) return false;
+  --it;
+  if (it->first > off || it->first + it->second < off + bytes) return false;
+  const int64_t b = it->first, size = it->second;
+  by_size_.erase({size, b});
+  by_off_.erase(it);
+  if (off > b) {
+    by_off_[b] = off - b;
+    by_size_.insert({off - b, b});
+  }
+  if (b + size > off + bytes) {
+    by_off_[off + bytes] = b + size - off - bytes;
+    by_size_.insert({b + size - off - bytes, off + bytes});
+  }
+  high_ = std::max(high_, off + bytes);
+  return true;
+}
+
+int64_t RangeAlloc::free_bytes() const {
+  int64_t t = 0;
+  for (const auto& kv : by_off_) t += kv.second;
+  return t;
+}
+
 void RangeAlloc::free(int64_t off, int64_t bytes) {
   auto next = by_off_.lower_bound(off);
   if (next != by_off_.end() && next->first == off + bytes) {
@@ -318,7 +344,8 @@ void RangeTracker::access(int64_t off, int64_t bytes, int stream, int32_t op, st
 static int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>& leaf_on_device,
-                    int64_t pool_bytes, int64_t align, RangeAlloc::Policy policy, int64_t peer_bytes, bool leaf_slots) {
+                    int64_t pool_bytes, int64_t align, RangeAlloc::Policy policy, int64_t peer_bytes, bool leaf_slots,
+                    bool compact) {
   PhysPlan pp;
   const size_t n = g.nodes.size();
   // fixed leaf slots: assigned in first-load order from offset 0; the intermediates share
@@ -348,12 +375,82 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
       return o < 0 ? o : o + base;
     }
     void free(int64_t o, int64_t b) { a.free(o - base, b); }
+    bool take_range(int64_t o, int64_t b) { return a.take_range(o - base, b); }
   } dev{dev0, leaf_region};
   RangeTracker dtr(pool_bytes), htr(std::max<int64_t>(host_cap, 1)), ptr(std::max<int64_t>(peer_bytes, 1));
   std::vector<int64_t> dev_off(n, -1), host_off(n, -1), peer_off(n, -1);
   std::vector<int32_t> ready(n, -1), ready_stream(n, -1), d2h_op(n, -1), p2p_op(n, -1);
   auto need_ready = [&](int32_t x, int stream, std::vector<int32_t>& deps) {
     if (ready[x] >= 0 && ready_stream[x] != stream) deps.push_back(ready[x]);
+  };
+  // tensors placed in the shared region (not leaf slots): offset -> node, for compaction
+  std::map<int64_t, int32_t> placed;
+  // allocation for op `me` on `stream`: a free block, else (compact) a cleared window
+  auto alloc_for = [&](int64_t rb, int stream, int32_t me, PhysOp& op, int32_t self) -> int64_t {
+    int64_t off = dev.alloc(rb);
+    if (off >= 0 || !compact) return off;
+    // windows start at a free block's start or right after a placed tensor; the cheapest has
+    // the fewest bytes of resident tensors, each at most half the request (so they fit
+    // elsewhere) and none of them an operand the op is about to read
+    std::vector<int64_t> starts;
+    for (const auto& kv : dev0.free_blocks()) starts.push_back(kv.first + leaf_region);
+    for (const auto& kv : placed) starts.push_back(kv.first + round_up(g.nodes[size_t(kv.second)].size, align));
+    const Node& me_node = g.nodes[size_t(self)];
+    int64_t best = -1, best_cost = INT64_MAX;
+    for (int64_t w0 : starts) {
+      if (w0 < leaf_region || w0 + rb > pool_bytes) continue;
+      int64_t cost = 0;
+      bool ok = true;
+      auto it = placed.upper_bound(w0);
+      if (it != placed.begin()) --it;
+      for (; it != placed.end() && it->first < w0 + rb; ++it) {
+        const int32_t y = it->second;
+        const int64_t ys = round_up(g.nodes[size_t(y)].size, align);
+        if (it->first + ys <= w0) continue;
+        if (ys * 2 > rb || (op.kind == OP_CONTRACT && (y == me_node.l || y == me_node.r))) {
+          ok = false;
+          break;
+        }
+        cost += ys;
+      }
+      if (ok && cost < best_cost && dev0.free_bytes() - (rb - cost) >= cost) {
+        best = w0;
+        best_cost = cost;
+      }
+    }
+    if (best < 0) return -1;
+    // reserve the window's free pieces, move its tensors out, then allocate it whole
+    std::vector<std::pair<int64_t, int64_t>> reserved;
+    for (const auto& kv : std::map<int64_t, int64_t>(dev0.free_blocks())) {
+      const int64_t a = std::max(kv.first + leaf_region, best), b = std::min(kv.first + leaf_region + kv.second, best + rb);
+      if (b > a && dev.take_range(a, b - a)) reserved.push_back({a, b - a});
+    }
+    std::vector<int32_t> movers;
+    for (auto it = placed.lower_bound(0); it != placed.end(); ++it) {
+      const int64_t ys = round_up(g.nodes[size_t(it->second)].size, align);
+      if (it->first < best + rb && it->first + ys > best) movers.push_back(it->second);
+    }
+    for (int32_t y : movers) {
+      const int64_t ys = round_up(g.nodes[size_t(y)].size, align);
+      const int64_t src = dev_off[size_t(y)];
+      const int64_t dst = dev.alloc(ys);
+      if (dst < 0) throw Error(CC_E_NOMEM, "compaction: no room to relocate node " + std::to_string(g.nodes[size_t(y)].id));
+      need_ready(y, stream, op.deps);
+      dtr.access(src, ys, stream, me, op.deps);         // read the old range (after its writer)
+      dtr.access(dst, ys, stream, me, op.deps);         // write the new range (after its readers)
+      op.pre_moves.push_back(Move{y, src, dst, g.nodes[size_t(y)].size});
+      ++pp.n_moves;
+      pp.move_bytes += g.nodes[size_t(y)].size;
+      placed.erase(src);
+      placed[dst] = y;
+      dev_off[size_t(y)] = dst;
+      ready[size_t(y)] = me;
+      ready_stream[size_t(y)] = stream;
+      reserved.push_back({src, ys});                    // its old range is inside the window
+    }
+    for (const auto& r : reserved) dev.free(r.first, r.second);
+    if (!dev.take_range(best, rb)) throw Error(CC_E_STATE, "compaction: window not free");
+    return best;
   };
   for (const auto& lop : lp.ops) {
     const int32_t x = lop.node;
@@ -365,9 +462,10 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
     switch (lop.kind) {
       case OP_H2D: {
         if (nd.leaf() && leaf_on_device[x]) break;            // already in HBM: no copy
-        const int64_t off = slot[x] >= 0 ? slot[x] : dev.alloc(rb);
+        const int64_t off = slot[x] >= 0 ? slot[x] : alloc_for(rb, S_H2D, me, op, x);
         if (off < 0) throw Error(CC_E_NOMEM, "device pool fragmented/too small for node " + std::to_string(nd.id));
         dev_off[x] = off;
+        if (slot[x] < 0) placed[off] = x;
         op.stream = S_H2D;
         op.dev_off = off;
         dtr.access(off, rb, S_H2D, me, op.deps, &op.same_deps);
@@ -383,9 +481,10 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
       }
       case OP_P2P_IN: {
         if (nd.leaf() && leaf_on_device[x]) break;            // already in HBM: no copy
-        const int64_t off = slot[x] >= 0 ? slot[x] : dev.alloc(rb);
+        const int64_t off = slot[x] >= 0 ? slot[x] : alloc_for(rb, S_H2D, me, op, x);
         if (off < 0) throw Error(CC_E_NOMEM, "device pool fragmented/too small for node " + std::to_string(nd.id));
         dev_off[x] = off;
+        if (slot[x] < 0) placed[off] = x;
         op.stream = S_H2D;                                      // inbound copies share the H2D stream
         op.dev_off = off;
         dtr.access(off, rb, S_H2D, me, op.deps, &op.same_deps);
@@ -411,7 +510,10 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
         dtr.access(dev_off[x], rb, S_D2H, me, op.deps);
         ptr.access(poff, rb, S_D2H, me, op.deps);
         p2p_op[x] = me;
-        if (slot[x] < 0) dev.free(dev_off[x], rb);   // a leaf slot stays reserved
+        if (slot[x] < 0) {                            // a leaf slot stays reserved
+          dev.free(dev_off[x], rb);
+          placed.erase(dev_off[x]);
+        }
         dev_off[x] = -1;
         pp.p2p_out_bytes += nd.size;
         break;
@@ -427,14 +529,20 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
         dtr.access(dev_off[x], rb, S_D2H, me, op.deps);
         htr.access(hoff, rb, S_D2H, me, op.deps);
         d2h_op[x] = me;
-        if (slot[x] < 0) dev.free(dev_off[x], rb);   // a leaf slot stays reserved
+        if (slot[x] < 0) {                            // a leaf slot stays reserved
+          dev.free(dev_off[x], rb);
+          placed.erase(dev_off[x]);
+        }
         dev_off[x] = -1;
         pp.d2h_bytes += nd.size;
         break;
       }
       case OP_DROP: {
         if (dev_off[x] >= 0) {
-          if (slot[x] < 0) dev.free(dev_off[x], rb);   // a leaf slot stays reserved
+          if (slot[x] < 0) {                            // a leaf slot stays reserved
+          dev.free(dev_off[x], rb);
+          placed.erase(dev_off[x]);
+        }
           dev_off[x] = -1;
         }
         break;
@@ -460,10 +568,11 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
         if (nd.type == ROOT) {
           op.dev_off = -1;                                      // root values buffer
         } else {
-          const int64_t off = dev.alloc(rb);
+          const int64_t off = alloc_for(rb, S_COMPUTE, me, op, x);
           if (off < 0) throw Error(CC_E_NOMEM, "device pool fragmented/too small for node " + std::to_string(nd.id));
           dev_off[x] = off;
           op.dev_off = off;
+          placed[off] = x;
           dtr.access(off, rb, S_COMPUTE, me, op.deps);
         }
         ready[x] = me;
@@ -472,7 +581,10 @@ PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>&
       }
       case OP_FREE: {
         if (dev_off[x] >= 0) {
-          if (slot[x] < 0) dev.free(dev_off[x], rb);   // a leaf slot stays reserved
+          if (slot[x] < 0) {                            // a leaf slot stays reserved
+          dev.free(dev_off[x], rb);
+          placed.erase(dev_off[x]);
+        }
           dev_off[x] = -1;
         }
         if (host_off[x] >= 0) {

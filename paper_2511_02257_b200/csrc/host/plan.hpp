@@ -48,6 +48,10 @@ class RangeAlloc {
   explicit RangeAlloc(int64_t capacity = 0, Policy policy = BEST_FIT);
   int64_t alloc(int64_t bytes);      // -1 if no block fits
   void free(int64_t off, int64_t bytes);
+  // allocate exactly [off, off + bytes) if it lies inside one free block; false otherwise
+  bool take_range(int64_t off, int64_t bytes);
+  const std::map<int64_t, int64_t>& free_blocks() const { return by_off_; }   // offset -> size
+  int64_t free_bytes() const;
   int64_t high_water() const { return high_; }
  private:
   std::map<int64_t, int64_t> by_off_;
@@ -77,6 +81,13 @@ enum Stream : int32_t { S_COMPUTE = 0, S_H2D = 1, S_D2H = 2, S_NONE = -1 };
 // Where an operand lives at a given op.
 enum Loc : int32_t { LOC_POOL = 0, LOC_DEVLEAF = 1, LOC_ROOTS = 2 };
 
+// Compaction move (physical only: the logical plan is unchanged): before the op that needs the
+// space, resident tensor `node` is copied device-to-device from src to dst (non-overlapping).
+struct Move {
+  int32_t node;
+  int64_t src, dst, bytes;
+};
+
 struct PhysOp {
   int32_t kind;                      // OpKind
   int32_t node;
@@ -92,22 +103,29 @@ struct PhysOp {
   std::vector<int32_t> same_deps;    // H2D ops: earlier H2D ops it depends on (implicit in a single
                                      // H2D stream; explicit when H2D copies use several streams)
   bool source = false;               // some later op waits on this one (record an event)
+  std::vector<Move> pre_moves;       // compaction moves issued on this op's stream before it
 };
 
 struct PhysPlan {
   std::vector<PhysOp> ops;
   int64_t pool_high_water = 0, host_pool_bytes = 0, peer_high_water = 0;
   int64_t h2d_bytes = 0, d2h_bytes = 0, p2p_in_bytes = 0, p2p_out_bytes = 0;   // bytes physically copied
+  int64_t n_moves = 0, move_bytes = 0;   // compaction (device-to-device) moves
 };
 // leaf_on_device[u]: the leaf is a caller device buffer (no copy / no pool space).
 // peer_bytes: size of the peer-tier region P2P_OUT copies are placed in (best fit;
 // CC_E_NOMEM when fragmentation leaves no block).
+// compact: when no free block fits an allocation, compact instead of failing — pick the window
+// of the needed size whose resident tensors (each at most half the request) are fewest bytes,
+// move them device-to-device into free blocks outside it (PhysOp::pre_moves, issued on the
+// allocating op's stream with their own dependencies) and allocate the window; CC_E_NOMEM only
+// when no window can be cleared.
 // leaf_slots: every host leaf gets a fixed slot at the top of the pool (in first-load order) and
 // the intermediates share the rest, so no leaf copy ever waits for memory to be freed — the copy
 // streams can run ahead at full PCIe rate (useful when the pool holds all leaves next to the
 // plan's intermediates; CC_E_NOMEM otherwise, and the caller falls back).
 PhysPlan build_phys(const Dag& g, const LruPlan& lp, const std::vector<uint8_t>& leaf_on_device,
                     int64_t pool_bytes, int64_t align, RangeAlloc::Policy policy = RangeAlloc::BEST_FIT,
-                    int64_t peer_bytes = 0, bool leaf_slots = false);
+                    int64_t peer_bytes = 0, bool leaf_slots = false, bool compact = false);
 
 }  // namespace cc
