@@ -273,6 +273,22 @@ def config_c2(N=128, Lt=64, n_src=16, n_snk=16, n_loop4=384, n_loop2=16, n_corr=
     return b.w
 
 
+def config_traces(N=128, Lt=64, n_mes=128, n_traces=400, seed=1):
+    """Diagnostic (not a BASELINE config): c2's trace stage alone — n_traces TR_MM of random
+    distinct pairs of n_mes meson leaves (c2 traces 384 pairs of its 128 MM1 outputs)."""
+    rng = np.random.default_rng(seed)
+    b = Builder("traces_N%d_Lt%d_k%d" % (N, Lt, n_traces), Lt, N, 1)
+    mes = [b.leaf(LEAF_M) for _ in range(n_mes)]
+    seen = set()
+    while len(seen) < n_traces:
+        x, y = (int(v) for v in rng.choice(n_mes, size=2, replace=False))
+        if (x, y) in seen:
+            continue
+        seen.add((x, y))
+        b.term(len(seen) % 4, b.tree(b.op(TR_MM, mes[x], mes[y], share=False)))
+    return b.w
+
+
 def config_c3(N=64, Lt=32, S=64):
     """c3: single nucleon correlator: P = BM1(B_snk, tau1); X = BB2(P, B_src);
     root = TR_MM(X, tau2)."""
