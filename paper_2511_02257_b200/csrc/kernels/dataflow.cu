@@ -6,9 +6,9 @@
 //   4 aux warps      — one per SM sub-partition; all lanes compute the TR_MM block pairs of
 //                      the trace ring (8 rows of each 32 x 32 pair per warp, FP64 FMAs), and
 //                      lane 0 of three of them carries a role:
-//     issuer: streams operands of ready items through two TMA rings of 32 KB stages (GEMM:
-//       one stage per 16-complex k-tile (A 64x16 + B 16x64 complex) or per half partner tile of
-//       a fused trace; trace: one 32x32 block pair A[t,I,J], B[t,J,I], 128-byte swizzled);
+//     issuer: streams operands of ready items through two TMA rings (GEMM, 64 KB stages: one
+//       stage per 32-complex k-tile (A 64x32 + B 32x64 complex) or per partner tile of a fused
+//       trace; trace, 32 KB stages: one 32x32 block pair A[t,I,J], B[t,J,I], 128-byte swizzled);
 //       shared memory only, never blocks on global memory or on one ring;
 //     GEMM / TR scheduler: claim items, decode them, poll their dependencies without
 //       blocking, hand ready items to the issuer, and publish finished items (fence + done
@@ -32,13 +32,17 @@ namespace {
 using namespace dev;
 
 #ifndef DF_GSTAGES
-#define DF_GSTAGES 4      // GEMM ring stages (32 KB)
+#define DF_GSTAGES 2      // GEMM ring stages (64 KB at BK = 32)
 #endif
 #ifndef DF_TSTAGES
 #define DF_TSTAGES 3      // trace ring stages (32 KB: one 32 x 32 complex block pair)
 #endif
-using GC = Cfg<64, 64, 16, 32, 16, DF_GSTAGES>;   // 32 KB stages (BK = 8: 16 KB stages with twice
-                                                   // the barrier traffic measured 4.64-4.74 ms on c2)
+#ifndef DF_BK
+#define DF_BK 32          // complex k per GEMM stage: 64 KB stages (12 TMA boxes per 64 KB instead
+                          // of 10 per 32 KB at BK = 16; c2 3.73 -> 3.68 ms, c4 / c5 -1 to -2 %)
+#endif
+using GC = Cfg<64, 64, DF_BK, 32, 16, DF_GSTAGES>;   // (BK = 8: 16 KB stages with twice the barrier
+                                                      // traffic measured 4.64-4.74 ms on c2; BK = 24 pads K = 128)
 constexpr int CW = GC::NCW * 32;           // 256 consumer threads
 #ifndef DF_NAUX
 #define DF_NAUX 4         // trace warps (a multiple of 4: whole warpgroups, equal per sub-partition)
@@ -48,8 +52,10 @@ constexpr int TB = 32;                     // trace block edge (complex)
 constexpr int INFO = 4;                    // item slots per queue (claimed-ready-running-unpublished)
 constexpr int TSTAGE = 2 * TB * TB * 16;   // a trace block pair: A and B 32 x 32 complex (32 KB)
 constexpr int TB_BYTES = TB * TB * 16;     // one operand block of a trace stage
-// fused-trace partner stages (two halves of a 64 x 64 tile) need 32 KB GEMM stages
-constexpr bool DF_FUSION = GC::STAGE_BYTES == TSTAGE;
+// fused-trace partner stages (two halves of a 64 x 64 tile) need 32 or 64 KB GEMM stages
+constexpr bool DF_FUSION = GC::STAGE_BYTES == TSTAGE || GC::STAGE_BYTES == 2 * TSTAGE;
+constexpr int PHALF = GC::STAGE_BYTES / TSTAGE;       // partner-tile halves per GEMM stage (1 or 2)
+constexpr int PSTAGES = PHALF >= 2 ? 1 : 2;           // GEMM stages per fused trace
 
 __device__ __forceinline__ void tma_load_4d_g(void* dst, const void* map, uint64_t* bar, int c0, int c1, int c2,
                                               int c3) {
@@ -138,7 +144,7 @@ __device__ __forceinline__ void decode_item(const DfQueue& q, int64_t item, Item
     inf.fb = op.fuse_begin;
     inf.fc = op.fuse_count;
     inf.ptmap0 = op.fuse_count > 0 ? fused[op.fuse_begin].tmap : 0;
-    inf.npos = inf.kt + 2 * op.fuse_count;   // + two partner stages per fused trace
+    inf.npos = inf.kt + PSTAGES * op.fuse_count;   // + the partner stages of the fused traces
   } else {
     const int t = int(local / op.P), p = int(local - int64_t(t) * op.P);
     const int U = op.tr_G * op.nb * op.nb;
@@ -185,11 +191,14 @@ __device__ __forceinline__ void gemm_stage_loads(const ItemInfo& inf, int k, uin
     // partner stage of fused trace f, half h: X[b, tn*64 + 32h + (0..31), tm*64 + (0..63)] as 8
     // boxes of 8 complex x 32 rows (row = j - 32h of the output tile, box c = columns i in
     // 8c..8c+7)
-    const int f = (k - inf.kt) >> 1, h = (k - inf.kt) & 1;
+    // (a 64 KB stage holds both halves: h at byte offset h * 32 KB)
+    const int f = (k - inf.kt) / PSTAGES;
     const void* map = static_cast<const uint8_t*>(tmaps) + size_t(2 * (inf.ptmap0 + f)) * 128;
+    for (int h = PHALF >= 2 ? 0 : (k - inf.kt) & 1, hn = 0; hn < (PHALF >= 2 ? 2 : 1); ++h, ++hn)
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-      tma_load_4d_g(sA + c * 4096, map, bar, 2 * (inf.tm * C::BM + 8 * c), inf.tn * C::BN + 32 * h, 0, inf.b);
+      for (int c = 0; c < 8; ++c)
+        tma_load_4d_g(sA + hn * TSTAGE + c * 4096, map, bar, 2 * (inf.tm * C::BM + 8 * c), inf.tn * C::BN + 32 * h, 0,
+                      inf.b);
     return;
   }
   uint8_t* sB = sA + C::A_BYTES;
@@ -233,7 +242,7 @@ __device__ __forceinline__ void trace_stage_loads(const ItemInfo& inf, int k, ui
 // slower (c2: 4.75 vs 4.64 ms at 6 stages).
 constexpr int GS = GC::STAGES;             // GEMM ring stages
 constexpr int TS = DF_TSTAGES;             // trace ring stages
-constexpr int STAGE = GC::STAGE_BYTES;     // GEMM stage (32 KB at BK = 16)
+constexpr int STAGE = GC::STAGE_BYTES;     // GEMM stage (64 KB at BK = 32)
 constexpr int DF_SMEM = GS * STAGE + TS * TSTAGE + 2 * (GS + TS) * 8 + 1024;
 constexpr int DF_STATIC_SMEM =
     int(2 * INFO * sizeof(ItemInfo)) + 4 * INFO * 8 + (GS + TS) * 4 + INFO * DF_NAUX * 16 + 4;
@@ -695,15 +704,15 @@ __global__ void __launch_bounds__(NT, 1) df_worker(DfArgs a) {
           for (int j = 0; j < C::NJ; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) v[i][j][e] = gauss3m_combine<C>(acc, i, j, e);
-        for (int p = 0; p < 2 * cur.fc; ++p) {
+        for (int p = 0; p < PSTAGES * cur.fc; ++p) {
           d = next_stage(st);
-          // partner stage (fused trace f, half h) holds X rows j in [32h, 32h+32): the warps
+          // partner half h (a 32 KB stage each, or both in one 64 KB stage) holds X rows j in [32h, 32h+32): the warps
           // whose output columns j fall there (wn = 2h, 2h+1: one warp per SM sub-partition)
           // add C[i][j] * X[j][i]; X[j][i] sits in box i/8 = 4wm + mi, row j - 32h, 16-byte
           // slot (i%8) ^ (j%8) = g ^ (2t+e) — conflict-free across each quarter warp
-          const int f = p >> 1, h = p & 1;
+          const int f = p / PSTAGES, h = PHALF >= 2 ? (wn >> 1) : p & 1;
           if ((wn >> 1) == h) {
-            const uint8_t* sP = smem + st * STAGE;
+            const uint8_t* sP = smem + st * STAGE + (PHALF >= 2 ? h * TSTAGE : 0);
             double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
 #pragma unroll
             for (int i = 0; i < C::MI; ++i)
