@@ -472,7 +472,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
       d.tmap = int32_t(tmaps.size() / 256);
       tmaps.resize(tmaps.size() + 256);
       const bool ok = n.op == CC_BB3 ? df_encode_bb3_maps(tmaps.data() + size_t(d.tmap) * 256, a, b, Lt, N, g.S)
-                                     : df_encode_trace_maps(tmaps.data() + size_t(d.tmap) * 256, a, b, Lt, N);
+                                     : df_encode_trace_maps(tmaps.data() + size_t(d.tmap) * 256, a, b, Lt, N, &d.tr_cw);
       if (!ok) throw Error(CC_E_CUDA, "TMA descriptor encoding failed");
       g_items += d.n_items;
       df_index[size_t(i)] = int32_t(gops.size());

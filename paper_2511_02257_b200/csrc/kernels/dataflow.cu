@@ -111,6 +111,7 @@ struct ItemInfo {
                                             // partner maps ptmap0.., tile index within its slice
   int32_t t, u0, nb, piece;                 // TRACE
   int32_t gj, gs;                           // TRACE: BB3 j extent and spin count (gj = 0: TR_MM)
+  int32_t cw;                               // TRACE: chunk-wide maps (one box per operand block)
   unsigned long long t_disp, t_ready;       // profiling (producer)
   unsigned long long t_first, t_comp;       // profiling (consumers)
 };
@@ -153,6 +154,7 @@ __device__ __forceinline__ void decode_item(const DfQueue& q, int64_t item, Item
     inf.nb = op.nb;
     inf.gj = op.tr_Gj;
     inf.gs = op.tr_S;
+    inf.cw = op.tr_cw;
     inf.u0 = int((int64_t(p) * U) / op.P);
     inf.npos = int((int64_t(p + 1) * U) / op.P) - inf.u0;
   }
@@ -179,6 +181,9 @@ __device__ __forceinline__ bool deps_ready(const DfArgs& a, const DfOp& op, int 
   return true;
 }
 
+#ifndef DF_TR_CW
+#define DF_TR_CW 1        // TR_MM stages as one chunk-wide box per operand block (N % 8 == 0)
+#endif
 // Stage descriptor (producer -> consumers, one per ring stage)
 constexpr uint32_t SK_STOP = 2;   // 0: data stage
 constexpr uint32_t SD_FIRST = 1u << 5, SD_LAST = 1u << 6;
@@ -219,7 +224,12 @@ __device__ __forceinline__ void trace_stage_loads(const ItemInfo& inf, int k, ui
   const int nb2 = inf.nb * inf.nb;
   const int g = u / nb2, rem = u - g * nb2;
   const int I = rem / inf.nb, J = rem - I * inf.nb;
-  if (inf.gj == 0) {
+  if (inf.gj == 0 && inf.cw) {
+    // one box per operand block: (16 doubles, 32 rows, 4 column chunks) lands as the same
+    // [chunk][row][128 B] swizzled layout as four 32-row boxes
+    tma_load_4d_g(sA, inf.tA, bar, 0, I * TB, J * (TB / 8), inf.t);
+    tma_load_4d_g(sB, inf.tB, bar, 0, J * TB, I * (TB / 8), inf.t);
+  } else if (inf.gj == 0) {
 #pragma unroll
     for (int ch = 0; ch < TB / 8; ++ch) {  // A[t, I*32 + r, J*32 + 8ch + s] and B[t, J*32 + r, I*32 + 8ch + s]
       tma_load_4d_g(sA + ch * TB * 128, inf.tA, bar, 2 * (J * TB + 8 * ch), I * TB, 0, inf.t);
@@ -857,7 +867,20 @@ bool df_encode_bb3_maps(void* dst, const void* A, const void* B, int64_t Lt, int
   return encode_map_4d(dst, A, dims, strides, box) && encode_map_4d(static_cast<uint8_t*>(dst) + 128, B, dims, strides, box);
 }
 
-bool df_encode_trace_maps(void* dst, const void* A, const void* B, int64_t Lt, int64_t N) {
+bool df_encode_trace_maps(void* dst, const void* A, const void* B, int64_t Lt, int64_t N, int32_t* chunk_wide) {
+#if DF_TR_CW
+  if (N % 8 == 0) {
+    // A, B as 4-d views (16 doubles of a 128-byte column chunk, row, chunk, t): a box of
+    // 16 x 32 x 4 is one 32 x 32 complex block, written to shared memory chunk-major (the
+    // chunk stride, 128 B, is below the row stride: the view only reorders the box walk)
+    const uint64_t dims[4] = {16, uint64_t(N), uint64_t(N / 8), uint64_t(Lt)};
+    const uint64_t strides[3] = {uint64_t(N) * 16, 128, uint64_t(N * N) * 16};
+    const uint32_t box[4] = {16, uint32_t(TB), uint32_t(TB / 8), 1};
+    *chunk_wide = 1;
+    return encode_map_4d(dst, A, dims, strides, box) && encode_map_4d(static_cast<uint8_t*>(dst) + 128, B, dims, strides, box);
+  }
+#endif
+  *chunk_wide = 0;
   // A, B as [Lt][N rows][N complex]: boxes of 32 rows x 8 complex (128-byte swizzle)
   ZgemmProblem p{};
   p.A = A;

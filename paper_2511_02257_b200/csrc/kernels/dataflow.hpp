@@ -44,7 +44,9 @@ struct DfOp {
   int64_t N, Lt;
   int32_t nb, P;          // 32x32 blocks per row; items (pieces) per time slice
   int32_t tr_G, tr_Gj;    // sub-matrices per slice; BB3: j extent (0 for TR_MM: 3-dim maps)
-  int32_t tr_S, pad_;     // BB3: spin components (time-spin index of the maps: t S + s)
+  int32_t tr_S;           // BB3: spin components (time-spin index of the maps: t S + s)
+  int32_t tr_cw;          // TR_MM: chunk-wide maps (N % 8 == 0): one TMA box per 32x32 block
+                          // (16 doubles x 32 rows x 4 column chunks) instead of four
   void* tr_part;          // [Lt][P] complex partials
   int* tr_cnt;            // [Lt] tickets (reset by the finisher)
   // GEMM with fused traces: after its k-tiles every output tile also computes, for each
@@ -99,8 +101,9 @@ bool df_supports_fusion();
 // Encode the TMA maps of one GEMM problem into dst[0] (A) and dst[1] (B).
 bool df_encode_maps(void* dst, const void* A, const void* B, int64_t M, int64_t Nn, int64_t Kin, int64_t Ko,
                     int64_t batch, int64_t lda, int64_t sAo, int64_t sAb, int64_t ldb, int64_t sBo, int64_t sBb);
-// TMA maps of a TR_MM op's operands ([Lt][N][N] complex, 32-row boxes).
-bool df_encode_trace_maps(void* dst, const void* A, const void* B, int64_t Lt, int64_t N);
+// TMA maps of a TR_MM op's operands ([Lt][N][N] complex, 32-row boxes); *chunk_wide is set
+// when the maps cover a whole 32x32 block per box (N % 8 == 0).
+bool df_encode_trace_maps(void* dst, const void* A, const void* B, int64_t Lt, int64_t N, int32_t* chunk_wide);
 // TMA maps of a BB3 op's operands (baryons [Lt][S][N][N][N] as 4-d tensors (k, j, i, t S + s):
 // boxes of 8 complex x 1 x 32 rows, so a stage holds the same 32x32 sub-matrix block pair).
 bool df_encode_bb3_maps(void* dst, const void* A, const void* B, int64_t Lt, int64_t N, int64_t S);
