@@ -17,7 +17,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 w = bench.workload(cfg)
 dev = torch.device("cuda:0")
 streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
-arena = torch.empty(6 << 30, dtype=torch.uint8, device=dev)
+arena = torch.empty(int(float(os.environ.get("PROF_ARENA_GB", "6")) * (1 << 30)), dtype=torch.uint8, device=dev)
 ctx = cc.Context(0, arena, streams=streams)
 ctx.load_workload(w)
 ctx.schedule(cc.CC_TREE)
