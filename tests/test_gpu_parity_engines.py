@@ -216,3 +216,21 @@ def test_c3_full_size_sampled_slices(flags):
     for t in (0, 31):
         r = _oracle_trees(w, dag, [0], host, t_range=(t, t + 1))
         assert_roots_close({0: got[t:t + 1]}, r)
+
+
+@pytest.mark.parametrize("N", [36, 56, 136])
+def test_trace_stage_box_paths(N):
+    """The worker's TR_MM stages load each 32x32 operand block as one chunk-wide TMA box when
+    N % 8 == 0 (56: ragged blocks with zero-filled chunks and rows; 136: past one 128-row
+    block) and as four 32-row boxes otherwise (36); random-phase leaves against R_abs."""
+    w = dags.config_c2(N=N, Lt=2, n_loop4=24, n_loop2=4, n_corr=3, coefs="complex")
+    w.leaf_mode = srng.MODE_RANDOM_PHASE
+    dag = Dag(w)
+    ops = {u: n.op for u, n in dag.nodes.items()}
+    leaf = lambda u: values.synthetic_leaf(w, u, ops[u])   # noqa: E731
+    r_or = values.evaluate(dag, leaf)
+    c_or = values.correlators(dag, r_or)
+    r_abs = _abs_roots(dag, leaf)
+    for flags in (0, 1):
+        _, roots, corr, st, ex = run_gpu(w, flags=flags, arena_mb=512)
+        _check_scaled(roots, corr, dag, r_or, c_or, r_abs)
