@@ -307,13 +307,17 @@ cc_status cc_execute_async(cc_ctx* ctx, int32_t flags);
  *   leaf_slots        unbounded plans: place every host leaf in a fixed slot of the pool so no
  *                     leaf copy waits for freed memory (falls back when the pool cannot hold the
  *                     leaves next to the plan's intermediates) [1]
+ *   trace_groups      dataflow: traces adjacent in the queue (no other work between them) are
+ *                     clustered by shared operand, and (op-major queues) run in chunks time
+ *                     slice by time slice, so a shared operand's slices are read from L2 after
+ *                     the first [1]
  * Errors: CC_E_INVAL for out-of-range values. */
 typedef struct {
   int32_t trace_fusion, copy_reorder, early_copies, precopy, ozaki_leaf_cache, ozaki_slices;
   int64_t h2d_chunk_bytes;
   double tr_ratio;
   int32_t debug, slice_major;
-  int32_t leaf_slots, pad_;
+  int32_t leaf_slots, trace_groups;
 } cc_options;
 cc_status cc_get_options(cc_ctx* ctx, cc_options* out);
 cc_status cc_set_options(cc_ctx* ctx, const cc_options* opt);

@@ -80,7 +80,7 @@ class cc_options(ctypes.Structure):
     _fields_ = [(n, c_i32) for n in ("trace_fusion", "copy_reorder", "early_copies", "precopy", "ozaki_leaf_cache",
                                      "ozaki_slices")] + \
                [("h2d_chunk_bytes", c_i64), ("tr_ratio", c_dbl), ("debug", c_i32), ("slice_major", c_i32),
-                ("leaf_slots", c_i32), ("pad_", c_i32)]
+                ("leaf_slots", c_i32), ("trace_groups", c_i32)]
 
 
 class cc_part_stats(ctypes.Structure):

@@ -613,10 +613,9 @@ cc_status cc_set_options(cc_ctx* ctx, const cc_options* opt) {
   if (!bit(o.trace_fusion) || !bit(o.copy_reorder) || !bit(o.early_copies) || !bit(o.precopy) ||
       !bit(o.ozaki_leaf_cache) || o.ozaki_slices < 4 || o.ozaki_slices > 7 || o.h2d_chunk_bytes < 0 ||
       !(o.tr_ratio >= 0.0 && o.tr_ratio <= 64.0) || o.debug < 0 || o.debug > 3 || !bit(o.slice_major) ||
-      !bit(o.leaf_slots))
+      !bit(o.leaf_slots) || !bit(o.trace_groups))
     throw Error(CC_E_INVAL, "option out of range");
   ctx->opt = o;
-  ctx->opt.pad_ = 0;
   if (!ctx->host_only) ctx->release_phys();   // scratch sizes, graphs and dataflow metadata depend on them
   ctx->phys_valid = false;
   API_END

@@ -542,6 +542,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     }
   tmr.lap("items+tmaps");
   std::vector<int64_t> qpos(size_t(n_ops), INT64_MAX);   // merged queue position of compute ops
+  std::vector<int32_t> tr_run(size_t(n_ops), -1);         // trace run of each TR op (3a', 3b)
   std::vector<int64_t> avail(size_t(n_ops), 0);
   // 3. queue order: a topological order of the plan's ops (compute and copy; consecutive
   // copies on one stream are chained, since a copy stream runs in plan order) that delays each
@@ -596,6 +597,51 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     size_t n_fused_ops = 0;
     for (int32_t i = 0; i < n_ops; ++i) n_fused_ops += fuse_host[size_t(i)] >= 0;
     if (order.size() != gops.size() + n_fused_ops) throw Error(CC_E_STATE, "dataflow: dependency cycle");
+    // 3a'. trace runs (option trace_groups): TR ops that are consecutive in the merged order
+    // (no GEMM or copy between them) are mutually independent with the same predecessors and
+    // successors, so any permutation of a run keeps the order topological.  Each run is
+    // clustered by shared operand (greedy: the operand most traces of the run read first), so
+    // traces reading the same tensor are adjacent in the TR queue and — interleaved slice by
+    // slice below — read its time slices from L2 after the first.
+    if (ctx->opt.trace_groups) {
+      auto is_tr = [&](int32_t i) { return df_index[size_t(i)] >= 0 && gops[size_t(df_index[size_t(i)])].kind == 1; };
+      int32_t runs = 0;
+      for (size_t k = 0; k < order.size();) {
+        if (!is_tr(order[k])) {
+          ++k;
+          continue;
+        }
+        size_t e = k;
+        while (e < order.size() && is_tr(order[e])) ++e;
+        if (e - k > 1) {
+          std::vector<int32_t> rest(order.begin() + int64_t(k), order.begin() + int64_t(e)), out;
+          auto opnd = [&](int32_t i, int w) {
+            const DfOp& d = gops[size_t(df_index[size_t(i)])];
+            return w ? d.B : d.A;
+          };
+          while (!rest.empty()) {
+            std::map<const void*, int32_t> cnt;
+            const void* best = nullptr;
+            int32_t bc = 0;
+            for (int32_t i : rest)
+              for (int w = 0; w < 2; ++w) {
+                const int32_t c = ++cnt[opnd(i, w)];
+                if (c > bc) {   // first operand to reach the highest count (deterministic)
+                  bc = c;
+                  best = opnd(i, w);
+                }
+              }
+            std::vector<int32_t> keep;
+            for (int32_t i : rest) (opnd(i, 0) == best || opnd(i, 1) == best ? out : keep).push_back(i);
+            rest.swap(keep);
+          }
+          std::copy(out.begin(), out.end(), order.begin() + int64_t(k));
+        }
+        for (size_t x = k; x < e; ++x) tr_run[size_t(order[x])] = runs;
+        ++runs;
+        k = e;
+      }
+    }
     std::vector<DfOp> nops, tops_v;
     std::vector<int32_t> nplan, tplan_v;
     int64_t first = 0, tfirst = 0;
@@ -675,7 +721,21 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
         size_t k1 = k0 + 1;
         if (sm)
           while (k1 < v.size() && avail[size_t(plan[k1])] == avail[size_t(plan[k0])]) ++k1;
-        if (!sm) {
+        const bool trq = !v.empty() && v[0].kind == 1;
+        if (!sm && trq && tr_run[size_t(plan[k0])] >= 0) {
+          // a trace run in op-major mode: chunks of consecutive TR ops that never share a
+          // partial-ring slot (< DF_TRACE_RING ops) go time slice by time slice, so the
+          // clustered traces read a shared operand's slice from L2 after the first
+          k1 = k0 + 1;
+          while (k1 < v.size() && k1 - k0 < size_t(DF_TRACE_RING) && tr_run[size_t(plan[k1])] == tr_run[size_t(plan[k0])])
+            ++k1;
+          for (int64_t t = 0; t < Lt; ++t)
+            for (size_t k = k0; k < k1; ++k)
+              for (int64_t x = t * v[k].P; x < (t + 1) * v[k].P; ++x) {
+                iop.push_back(int32_t(k));
+                iloc.push_back(int32_t(x));
+              }
+        } else if (!sm) {
           for (int32_t x = 0; x < v[k0].n_items; ++x) {
             iop.push_back(int32_t(k0));
             iloc.push_back(x);

@@ -86,7 +86,7 @@ using namespace ccx;
 
 struct cc_ctx {
   int device = -1;
-  cc_options opt{0, 1, 1, 1, 1, 5, 0, 0.0, 0, 1, 1, 0};   // cc_set_options (cc.h)
+  cc_options opt{0, 1, 1, 1, 1, 5, 0, 0.0, 0, 1, 1, 1};   // cc_set_options (cc.h)
   bool mm1_ozaki = false;     // execute flags bit 6: MM1/BM1/BB2 on the tcgen05 Ozaki engine (op-by-op)
   int pre_n = 0;              // the plan's first pre_n leaf copies were started before the physical plan
   cudaEvent_t ev_precopy = nullptr;

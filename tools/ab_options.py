@@ -20,12 +20,13 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--flags", type=int, default=1)
+    ap.add_argument("--arena-gb", type=float, default=6)
     ap.add_argument("variants", nargs="+")
     a = ap.parse_args()
     w = bench.workload(a.config)
     dev = torch.device("cuda:0")
     streams = [torch.cuda.Stream(device=dev) for _ in range(3)]
-    arena = torch.empty(6 << 30, dtype=torch.uint8, device=dev)
+    arena = torch.empty(int(a.arena_gb * (1 << 30)), dtype=torch.uint8, device=dev)
     ctx = cc.Context(0, arena, streams=streams)
     ctx.load_workload(w)
     ctx.schedule(cc.CC_TREE)
