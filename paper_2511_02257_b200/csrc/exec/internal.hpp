@@ -80,7 +80,7 @@ struct KindTimes {
   int64_t count[CC_N_OPS] = {0};
 };
 constexpr int64_t DF_CHUNK_RING = 4;   // GEMM ops split in k that may be in flight at once
-constexpr int64_t DF_TRACE_RING = 16;  // TR ops that may be in flight at once
+constexpr int64_t DF_TRACE_RING = 64;  // TR ops that may be in flight at once
 }  // namespace ccx
 using namespace ccx;
 

@@ -9,9 +9,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2511_02257_b200 import cc  # noqa: E402
 from synth import dags, rng as srng  # noqa: E402
 
-w = dags.config_c2() if len(sys.argv) < 2 else getattr(dags, "config_" + sys.argv[1])()
+import bench  # noqa: E402
+w = bench.workload(sys.argv[1] if len(sys.argv) > 1 else "c2")
 dev = torch.device("cuda:0")
-ctx = cc.Context(0, torch.empty(6 << 30, dtype=torch.uint8, device=dev))
+ctx = cc.Context(0, torch.empty(int(float(os.environ.get("PROF_ARENA_GB", "6")) * (1 << 30)), dtype=torch.uint8, device=dev))
 ctx.load_workload(w)
 ctx.schedule(cc.CC_TREE)
 keep = []
@@ -82,14 +83,15 @@ print("consumers: stage loops %.1f%%, between loops %.1f%% of summed per-SM time
       % (100 * loop_sum / (loop_sum + gap_sum), 100 * gap_sum / (loop_sum + gap_sum)))
 # time bins: items running and mean duration per 0.5 ms
 span_ns = t1 - t0
-nb = int(span_ns // 500000) + 1
+binw = max(500000, int(span_ns // 40))   # at most ~40 bins
+nb = int(span_ns // binw) + 1
 print("bin(ms)  gemm_items  gemm_us  trace_items  trace_us  trace_SMs")
 for k in range(nb):
-    lo, hi = t0 + k * 500000, t0 + (k + 1) * 500000
+    lo, hi = t0 + k * binw, t0 + (k + 1) * binw
     row = []
     for a in (g, t):
         m = (a[:, 1] >= lo) & (a[:, 1] < hi)
         d = (a[m, 2].astype(np.float64) - a[m, 1]) / 1e3
         row.append((int(m.sum()), d.mean() if m.any() else 0.0, len(np.unique(a[m, 3]))))
-    print("%5.1f  %8d  %7.1f  %8d  %7.1f  %4d" % (k * 0.5, row[0][0], row[0][1], row[1][0], row[1][1], row[1][2]))
+    print("%5.1f  %8d  %7.1f  %8d  %7.1f  %4d" % (k * binw / 1e6, row[0][0], row[0][1], row[1][0], row[1][1], row[1][2]))
 os._exit(0)
