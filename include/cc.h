@@ -275,7 +275,7 @@ cc_status cc_ipc_close(void* dev);
  * (cc_dataflow_profile); bit 6 runs every MM1 / BM1 / BB2 on the tcgen05 INT8 Ozaki engine
  * (cc_gemm_ozaki, 5 slices; leaves split once per execute; implies op-by-op launches); bit 7
  * (CC_EXEC_AUTO) chooses bit 6 or the dataflow worker by the measured rule of DESIGN §7 (the
- * Ozaki engine for GEMMs with N >= 256, or baryon GEMMs with N >= 128). */
+ * Ozaki engine for GEMMs with N >= 512, or baryon GEMMs with N >= 128). */
 #define CC_EXEC_OZAKI 64
 #define CC_EXEC_AUTO 128
 cc_status cc_execute(cc_ctx* ctx, int32_t flags, cc_exec_stats* stats);

@@ -74,14 +74,16 @@ void execute(cc_ctx* ctx, int32_t flags, bool blocking, cc_exec_stats* stats) {
   }
   if (flags & 128) {
     // CC_EXEC_AUTO: the Ozaki engine (bit 6) where it measured faster than the dataflow worker
-    // (DESIGN §7): GEMMs with N >= 256, or baryon GEMMs with N >= 128
+    // (profiles/r02_configs_final.txt): GEMMs with N >= 512 (c5 N = 512 part 0.74 vs
+    // 0.91 s, N = 1024 part 1.84 vs 3.35 s; at N = 256 the worker wins, 1.21 vs 1.41 s), or
+    // baryon GEMMs with N >= 128 (c4 1.41 vs 1.57 s)
     const Dag& gd = *ctx->dag;
     bool gemm = false, baryon = false;
     for (const auto& n : gd.nodes) {
       gemm |= is_gemm_kind(n.op);
       baryon |= is_gemm_kind(n.op) && n.op != CC_MM1;
     }
-    if (gemm && (gd.N >= 256 || (baryon && gd.N >= 128))) flags |= 64;
+    if (gemm && (gd.N >= 512 || (baryon && gd.N >= 128))) flags |= 64;
     flags &= ~128;
   }
   ctx->mm1_ozaki = (flags & 64) != 0;

@@ -236,8 +236,8 @@ def test_executor_ozaki_baryon_dags():
 
 def test_executor_auto_flag():
     """CC_EXEC_AUTO (flags bit 7): a c2-shaped DAG at N=72 stays on the dataflow worker (one
-    persistent launch + correlator), a c5-shaped one at N=256 goes to the Ozaki engine; both
-    match the oracle."""
+    persistent launch + correlator), a c5-shaped one at N=512 goes to the Ozaki engine (N = 256
+    stays on the worker since the round-2 measurements); all match the oracle."""
     from synth import dags
     from oracle.dag import Dag
     from paper_2511_02257_b200 import cc
@@ -248,6 +248,10 @@ def test_executor_auto_flag():
     assert_roots_close(roots, values.run_workload(w, Dag(w))[0])
     w = dags.config_c5(N=256, Lt=2, n_pairs=12, n_trees=30, n_corr=3)
     _, roots, _, _, ex = run_gpu(w, flags=cc.EXEC_AUTO, arena_mb=2048)
+    assert ex["n_kernels"] <= 3
+    assert_roots_close(roots, values.run_workload(w, Dag(w))[0])
+    w = dags.config_c5(N=512, Lt=2, n_pairs=12, n_trees=30, n_corr=3)
+    _, roots, _, _, ex = run_gpu(w, flags=cc.EXEC_AUTO, arena_mb=3072)
     assert ex["n_kernels"] > 10
     assert_roots_close(roots, values.run_workload(w, Dag(w))[0])
 
