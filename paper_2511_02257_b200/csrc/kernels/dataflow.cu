@@ -515,6 +515,9 @@ __global__ void __launch_bounds__(NT, 1) df_worker(DfArgs a) {
     uint32_t rt = 0;
     bool t_stop = false;
     long long n_tst = 0;
+    // profile (trace warp 0, lane 0): cycles from the end of one stage until the next stage's
+    // data is there (waiting for the issuer / TMA), and cycles computing stages
+    long long tw_wait = 0, tw_work = 0, tw_mark = PROF ? clock64() : 0;
     // one trace stage if it is there; false when nothing was done
     auto trace_step = [&]() -> bool {
       if (t_stop) return false;
@@ -524,6 +527,11 @@ __global__ void __launch_bounds__(NT, 1) df_worker(DfArgs a) {
       if ((d & 3u) == SK_STOP) {
         t_stop = true;
         return false;
+      }
+      long long tw0 = 0;
+      if (PROF && lane == 0) {
+        tw0 = clock64();
+        tw_wait += tw0 - tw_mark;
       }
       if (d & SD_FIRST) {
 #pragma unroll
@@ -550,6 +558,10 @@ __global__ void __launch_bounds__(NT, 1) df_worker(DfArgs a) {
       if (lane == 0) mbar_arrive(&empty_t[st]);
       ++rt;
       if (PROF) ++n_tst;
+      if (PROF && lane == 0) {
+        tw_mark = clock64();
+        tw_work += tw_mark - tw0;
+      }
       if (d & SD_LAST) {
         const int slot = int((d >> 2) & 7u);
         if (ax == 0 && lane == 0 && PROF) s_info[1][slot].t_comp = gtimer();
@@ -577,7 +589,13 @@ __global__ void __launch_bounds__(NT, 1) df_worker(DfArgs a) {
         __nanosleep(20);
       }
     }
-    if (PROF && lane == 0 && a.prof_sm) a.prof_sm[16 * blockIdx.x + 8 + ax] = n_tst;
+    if (PROF && lane == 0 && a.prof_sm) {
+      a.prof_sm[16 * blockIdx.x + 8 + ax] = n_tst;
+      if (ax == 0) {
+        a.prof_sm[16 * blockIdx.x + 12] = tw_wait;
+        a.prof_sm[16 * blockIdx.x + 13] = tw_work;
+      }
+    }
     return;
   }
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_MMA));

@@ -39,6 +39,10 @@ print("consumer warps (thread 0, clock64): stage wait %.1f%%, stage math %.1f%%;
       % (100 * psm[:, 0].sum() / tot.sum(), 100 * psm[:, 2].sum() / tot.sum(), psm[:, 4].sum(),
          psm[:, 0].sum() / max(psm[:, 4].sum(), 1), psm[:, 2].sum() / max(psm[:, 4].sum(), 1),
          psm[:, 8:12].sum(axis=0).tolist()))
+if psm.shape[1] > 13 and psm[:, 13].sum() > 0:
+    ntr = psm[:, 8].sum()
+    print("trace warp 0 (clock64): waiting for stage data %.0f cycles per stage, computing %.0f cycles per stage "
+          "(%d stages)" % (psm[:, 12].sum() / max(ntr, 1), psm[:, 13].sum() / max(ntr, 1), ntr))
 g0 = np.vstack([gp, tp])
 g, t = g0[g0[:, 6] == 0], g0[g0[:, 6] == 1]
 t0 = min(g[:, 0].min() if len(g) else 2**63, t[:, 0].min() if len(t) else 2**63)
