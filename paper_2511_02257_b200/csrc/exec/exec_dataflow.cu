@@ -588,9 +588,16 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     for (int32_t i = 0; i < n_ops; ++i)
       if (slot[size_t(i)] >= 0 && indeg[size_t(i)] == 0) ready.push({key(i), i});
     std::vector<int32_t> order;
+    // pop segment of each op: it changes at every op that is not a trace (GEMMs AND copies), so
+    // traces with equal segments were popped back to back (3a')
+    std::vector<int32_t> pop_seg(size_t(n_ops), -1);
+    int32_t seg = 0;
     while (!ready.empty()) {
       const int32_t i = ready.top().second;
       ready.pop();
+      const bool trace = ops[size_t(i)].kind == OP_CONTRACT && is_root_kind(g.nodes[size_t(ops[size_t(i)].node)].op);
+      if (!trace) ++seg;
+      pop_seg[size_t(i)] = seg;
       if (ops[size_t(i)].kind == OP_CONTRACT) {
         qpos[size_t(i)] = int64_t(order.size());
         order.push_back(i);
@@ -601,9 +608,10 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
     size_t n_fused_ops = 0;
     for (int32_t i = 0; i < n_ops; ++i) n_fused_ops += fuse_host[size_t(i)] >= 0;
     if (order.size() != gops.size() + n_fused_ops) throw Error(CC_E_STATE, "dataflow: dependency cycle");
-    // 3a'. trace runs (option trace_groups): TR ops that are consecutive in the merged order
-    // (no GEMM or copy between them) are mutually independent with the same predecessors and
-    // successors, so any permutation of a run keeps the order topological.  Each run is
+    // 3a'. trace runs (option trace_groups): TR ops popped back to back by the topological sort
+    // (no GEMM and no copy between them: equal pop segment) are mutually independent with the
+    // same predecessors and successors, so any permutation of a run keeps the merged order —
+    // copies included, the deadlock-freedom witness (dataflow.hpp) — topological.  Each run is
     // clustered by shared operand (greedy: the operand most traces of the run read first), so
     // traces reading the same tensor are adjacent in the TR queue and — interleaved slice by
     // slice below — read its time slices from L2 after the first.
@@ -616,7 +624,7 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
           continue;
         }
         size_t e = k;
-        while (e < order.size() && is_tr(order[e])) ++e;
+        while (e < order.size() && is_tr(order[e]) && pop_seg[size_t(order[e])] == pop_seg[size_t(order[k])]) ++e;
         if (e - k > 1) {
           std::vector<int32_t> rest(order.begin() + int64_t(k), order.begin() + int64_t(e)), out;
           auto opnd = [&](int32_t i, int w) {

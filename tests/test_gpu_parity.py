@@ -508,3 +508,22 @@ def test_compaction_on_a_fragmented_pool(flags):
     # compacting plan runs op by op and copies them again (counted: they crossed PCIe)
     assert ex["d2h_bytes"] == st2["d2h_bytes"]
     assert st2["h2d_bytes"] <= ex["h2d_bytes"] <= st2["h2d_bytes"] + (4 * 16 * 4 * 8 ** 3 if flags == 0 else 0)
+
+
+def test_trace_runs_with_refetched_leaves_under_cap():
+    """Leaf-reading traces under a cap that evicts and re-fetches leaves: H2D copies sit between
+    traces in the dataflow order (a copy waits for the traces reading the memory it overwrites,
+    the next traces wait for the copy), so trace runs must break at copies (3a').  Values vs the
+    oracle on the dataflow worker, trace runs on and off, stream and graph."""
+    w = dags.config_c2(N=16, Lt=2, n_loop4=10, n_loop2=60, n_corr=3)
+    dag = Dag(w)
+    cap = 6 * 2 * 16 * 16 * 16
+    p = lru.plan(dag, tree.schedule(dag), cap)
+    assert p["evictions"] > 0 and p["h2d_count"] > 32
+    r_or, c_or = values.run_workload(w, dag)
+    for tg in (1, 0):
+        for flags in (0, 1):
+            _, roots, corr, st, ex = run_gpu(w, cap=cap, flags=flags, options={"trace_groups": tg})
+            assert st["evictions"] == p["evictions"] and ex["h2d_bytes"] == p["h2d_bytes"]
+            assert_roots_close(roots, r_or)
+            assert_corr_close(dag, r_or, corr, c_or)
