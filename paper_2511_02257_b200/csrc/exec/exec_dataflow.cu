@@ -2,10 +2,6 @@
 // (kernels/dataflow.hpp), copies on the copy streams, synchronised through integer slots.
 #include "internal.hpp"
 
-#include <array>
-#include <set>
-#include <unordered_map>
-
 namespace ccx {
 namespace {
 
@@ -631,45 +627,8 @@ void prepare_dataflow(cc_ctx* ctx, bool early) {
             const DfOp& d = gops[size_t(df_index[size_t(i)])];
             return w ? d.B : d.A;
           };
-          // greedy in O(n log n): operands keyed by (count desc, first appearance); taking the
-          // best operand's remaining traces lowers their other operands' counts
-          const size_t n = rest.size();
-          std::unordered_map<const void*, int32_t> id;
-          std::vector<int32_t> cnt, first_at;
-          std::vector<std::vector<int32_t>> users;
-          std::vector<std::array<int32_t, 2>> ids(n);
-          for (size_t x = 0; x < n; ++x)
-            for (int w = 0; w < 2; ++w) {
-              auto ins = id.emplace(opnd(rest[x], w), int32_t(cnt.size()));
-              if (ins.second) {
-                cnt.push_back(0);
-                first_at.push_back(int32_t(x));
-                users.emplace_back();
-              }
-              const int32_t o = ins.first->second;
-              ids[x][size_t(w)] = o;
-              if (w == 0 || ids[x][0] != o) {
-                ++cnt[size_t(o)];
-                users[size_t(o)].push_back(int32_t(x));
-              }
-            }
-          std::set<std::array<int32_t, 3>> q;   // (-count, first appearance, operand)
-          for (size_t o = 0; o < cnt.size(); ++o) q.insert({-cnt[o], first_at[o], int32_t(o)});
-          std::vector<uint8_t> taken(n, 0);
-          while (!q.empty()) {
-            const int32_t best = (*q.begin())[2];
-            q.erase(q.begin());
-            for (int32_t x : users[size_t(best)]) {
-              if (taken[size_t(x)]) continue;
-              taken[size_t(x)] = 1;
-              out.push_back(rest[size_t(x)]);
-              const int32_t other = ids[size_t(x)][0] == best ? ids[size_t(x)][1] : ids[size_t(x)][0];
-              if (other == best) continue;
-              q.erase({-cnt[size_t(other)], first_at[size_t(other)], other});
-              if (--cnt[size_t(other)] > 0) q.insert({-cnt[size_t(other)], first_at[size_t(other)], other});
-            }
-            cnt[size_t(best)] = 0;
-          }
+          for (int32_t x : cluster_by_operand(rest.size(), [&](size_t x, int w) { return opnd(rest[x], w); }))
+            out.push_back(rest[size_t(x)]);
           std::copy(out.begin(), out.end(), order.begin() + int64_t(k));
         }
         for (size_t x = k; x < e; ++x) tr_run[size_t(order[x])] = runs;

@@ -23,6 +23,8 @@
 #include <fstream>
 #include <map>
 #include <queue>
+#include <set>
+#include <unordered_map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -70,6 +72,51 @@ inline int oz_kind(int op) {
 constexpr int GEMM_OPS[5] = {CC_MM1, CC_BM1, CC_BB2, CC_BB1, CC_BT2};
 constexpr int TRACE_OPS[2] = {CC_TR_MM, CC_BB3};
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Traces clustered by shared operand: a permutation of 0..n-1 that puts the traces reading the
+// operand most of them read first (adjacent, in their original order), then the next such
+// operand among the rest, ...; greedy in O(n log n) (ordered set keyed by remaining count and
+// first appearance).  opnd(x, w) is operand w (0, 1) of trace x.
+template <class F>
+std::vector<int32_t> cluster_by_operand(size_t n, F&& opnd) {
+  std::unordered_map<const void*, int32_t> id;
+  std::vector<int32_t> cnt, first_at, out;
+  std::vector<std::vector<int32_t>> users;
+  std::vector<std::array<int32_t, 2>> ids(n);
+  for (size_t x = 0; x < n; ++x)
+    for (int w = 0; w < 2; ++w) {
+      auto ins = id.emplace(opnd(x, w), int32_t(cnt.size()));
+      if (ins.second) {
+        cnt.push_back(0);
+        first_at.push_back(int32_t(x));
+        users.emplace_back();
+      }
+      const int32_t o = ins.first->second;
+      ids[x][size_t(w)] = o;
+      if (w == 0 || ids[x][0] != o) {
+        ++cnt[size_t(o)];
+        users[size_t(o)].push_back(int32_t(x));
+      }
+    }
+  std::set<std::array<int32_t, 3>> q;   // (-count, first appearance, operand)
+  for (size_t o = 0; o < cnt.size(); ++o) q.insert({-cnt[o], first_at[o], int32_t(o)});
+  std::vector<uint8_t> taken(n, 0);
+  while (!q.empty()) {
+    const int32_t best = (*q.begin())[2];
+    q.erase(q.begin());
+    for (int32_t x : users[size_t(best)]) {
+      if (taken[size_t(x)]) continue;
+      taken[size_t(x)] = 1;
+      out.push_back(x);
+      const int32_t other = ids[size_t(x)][0] == best ? ids[size_t(x)][1] : ids[size_t(x)][0];
+      if (other == best) continue;
+      q.erase({-cnt[size_t(other)], first_at[size_t(other)], other});
+      if (--cnt[size_t(other)] > 0) q.insert({-cnt[size_t(other)], first_at[size_t(other)], other});
+    }
+    cnt[size_t(best)] = 0;
+  }
+  return out;
+}
 
 inline void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw Error(CC_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
