@@ -36,6 +36,8 @@ def workload(name):
         return dags.config_c1()
     if name == "c3":
         return dags.config_c3()
+    if name == "c4":   # diagnostic (the bench's c4 record builds its own): the two-baryon DAG
+        return dags.config_c4()
     if name.startswith("c5:"):   # diagnostic: c5 at a given N, e.g. c5:N=256 (not a bench line)
         return dags.config_c5(**{k: int(v) for k, v in (x.split("=") for x in name[3:].split(","))})
     if name.startswith("c2:"):   # diagnostic variants of c2, e.g. c2:n_loop4=192 (not bench lines)
