@@ -527,3 +527,20 @@ def test_trace_runs_with_refetched_leaves_under_cap():
             assert st["evictions"] == p["evictions"] and ex["h2d_bytes"] == p["h2d_bytes"]
             assert_roots_close(roots, r_or)
             assert_corr_close(dag, r_or, corr, c_or)
+
+
+def test_trace_runs_bit_identical():
+    """Trace runs (option trace_groups) only reorder work items: roots are bit-identical with the
+    option off, on a slice-major plan (c2-shaped) and on an op-major plan with split traces
+    (c5-shaped at N = 256: 4 pieces per slice through the partial ring, memory reuse)."""
+    for w, arena in ((dags.config_c2(N=40, Lt=4, n_loop4=60, n_loop2=6, n_corr=3), 256),
+                     (dags.config_c5(N=256, Lt=3, n_mes=8, n_pairs=20, n_trees=120, n_corr=3), 1024)):
+        dag = Dag(w)
+        r_or, _ = values.run_workload(w, dag)
+        got = []
+        for tg in (0, 1):
+            _, roots, corr, st, ex = run_gpu(w, flags=0, arena_mb=arena, options={"trace_groups": tg})
+            assert_roots_close(roots, r_or)
+            got.append(roots)
+        for t in r_or:
+            assert np.array_equal(got[0][t], got[1][t]), t
