@@ -544,3 +544,25 @@ def test_trace_runs_bit_identical():
             got.append(roots)
         for t in r_or:
             assert np.array_equal(got[0][t], got[1][t]), t
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13, 14])
+def test_dataflow_random_dags_under_caps(seed):
+    """Randomised c2-shaped DAGs (ragged N, few slices) through the dataflow worker, unbounded and
+    under a cap that evicts and re-fetches leaves: trace runs, copy order and slice-major items
+    must keep the queues topological (no hang) and the values exact (oracle)."""
+    r = np.random.default_rng(seed)
+    N = int(r.choice([24, 40, 56]))
+    Lt = int(r.integers(2, 4))
+    w = dags.config_c2(N=N, Lt=Lt, n_loop4=int(r.integers(20, 60)), n_loop2=int(r.integers(4, 30)), n_corr=3,
+                       seed=seed)
+    dag = Dag(w)
+    r_or, c_or = values.run_workload(w, dag)
+    leaf = Lt * N * N * 16
+    for cap in (0, 8 * leaf):
+        p = lru.plan(dag, tree.schedule(dag), cap) if cap else None
+        _, roots, corr, st, ex = run_gpu(w, cap=cap, flags=0)
+        if p is not None:
+            assert st["evictions"] == p["evictions"] and ex["h2d_bytes"] == p["h2d_bytes"]
+        assert_roots_close(roots, r_or)
+        assert_corr_close(dag, r_or, corr, c_or)
